@@ -1,0 +1,322 @@
+#!/usr/bin/env python3
+"""Env-step throughput on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+Workload (BASELINE.json configs[1], bench_sim protocol proj/src/bench.cpp:97-135):
+PSM TargetReaching, 16384 envs per GPU, actions U[-1,1) drawn from
+make_stream(seed, 0xac7104) in the reference's row-major order (bench.cpp:31-35),
+every step writes the full StepResult (observations, rewards, flags,
+task_error, terminal observations on ended rows) and auto-resets ended envs.
+
+  value  = env-steps/s with state resident in HBM: sg_env_bench_step launches
+           of F fused steps (actions generated in-kernel), CUDA-event timed per
+           launch on the env stream, L2 flushed (256 MiB write) between launches.
+  e2e    = the same metric through the host C-ABI call sg_env_step_host:
+           per step H2D of the actions from pinned memory and D2H of the full
+           StepResult, one launch per step.
+  --impl reference: the reference's CPU path (oracle port, all host cores).
+
+Multi-GPU (torchrun): rank r owns global envs [r*N, (r+1)*N) with per-env
+streams seeded by global id (weak scaling, no collective in the timed loop);
+timing = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/sec at 1/2/4/8 B200 (PSM reach, 16K envs/GPU); % of HBM roofline"
+CONFIGS = {
+    "psm": dict(robot="psm", task="target_reaching", n_envs=16384, goal_sigma=0.05,
+                workload="dVRK PSM reach, 16384 envs/GPU, random actions (BASELINE configs[1])"),
+    "ecm": dict(robot="ecm", task="target_reaching", n_envs=65536, goal_sigma=0.05,
+                workload="dVRK ECM camera reach, 65536 envs/GPU, random actions (BASELINE configs[2])"),
+    "star": dict(robot="star", task="path_following", n_envs=16384, goal_sigma=0.15,
+                 workload="STAR path following, 16384 envs/GPU, random actions (BASELINE configs[3])"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def step_bytes(A: int, O: int, fused: int, reset_frac: float) -> dict:
+    """Algorithmic HBM bytes of one fused launch per env.
+    Per launch: joint state q/qdot/q_target read+write (3*A*4*2), goal read+write
+    and tip write (3*4*3), step/hold counters r+w (16), bench stream state r+w (16).
+    Per step: generated actions written (A*4), observation row (O*4), reward,
+    task_error (4+4), terminated+timed_out (2).
+    Per reset (amortised by reset_frac): terminal observation row (O*4), RNG
+    state r+w (16), episode counter r+w (16), reset state write + reload
+    (3*A*4*2 + 24)."""
+    per_launch = 3 * A * 4 * 2 + 3 * 4 * 3 + 16 + 16
+    per_step = A * 4 + O * 4 + 8 + 2
+    per_reset = O * 4 + 16 + 16 + 3 * A * 4 * 2 + 24
+    total = per_launch + fused * (per_step + reset_frac * per_reset)
+    return dict(per_launch=per_launch, per_step=per_step, per_reset=per_reset,
+                per_env_launch=total, per_env_step=total / fused)
+
+
+class Clocks:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = f"/tmp/sg_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines() if l.strip()]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
+                          and "Not" not in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_reference(cfg: dict, steps: int, budget_s: float, threads: int = 0):
+    """The reference's CPU path (oracle port of bench_sim) on the host cores.
+    Returns (env-steps/s, lanes, sample description)."""
+    from oracle import oracle as O
+    O.build()
+    m = O.resolve_robot(cfg["robot"])
+    task = O.PATH_FOLLOWING if cfg["task"] == "path_following" else O.TARGET_REACHING
+    ocfg = O.env_config(n_envs=cfg["n_envs"], seed=0, task=task, goal_sigma=cfg["goal_sigma"])
+    lanes = threads or os.cpu_count() or 1
+    # calibrate, then size the sample to the time budget
+    secs, st = O.bench_sim(ocfg, m, cfg["n_envs"] * 3, 1, lanes)
+    rate = st[0] / secs[0]
+    n_steps = max(3, min(steps, int(budget_s * rate / cfg["n_envs"])))
+    secs, st = O.bench_sim(ocfg, m, cfg["n_envs"] * n_steps, 1, lanes)
+    sample = (f"{cfg['n_envs']} envs x {int(st[0] // cfg['n_envs'])} steps after reset + 1 warm-up step "
+              f"(bench_sim protocol, serial action fill and serial resets as in the reference), fp64, "
+              f"{lanes} pool lanes")
+    return float(st[0] / secs[0]), lanes, sample
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=6400)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="psm", choices=sorted(CONFIGS))
+    ap.add_argument("--fuse", type=int, default=64, help="steps per fused launch")
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        total = max(args.steps, 3)
+        rate, lanes, sample = cpu_reference(cfg, total, budget_s=120.0)
+        line = dict(metric=METRIC, value=rate, unit="env-steps/s", n_gpus=args.gpus, steps=args.steps,
+                    warmup=args.warmup, ms_per_step=1e3 * cfg["n_envs"] / rate, higher_is_better=True,
+                    scaling="weak", vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
+                    config=dict(workload=cfg["workload"], n_envs=cfg["n_envs"]),
+                    cpu_baseline=dict(value=rate, unit="env-steps/s", cores=lanes, kind="port", sample=sample),
+                    e2e=dict(value=rate, unit="env-steps/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+        print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+    from paper_2310_04676_b200 import sg
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    n = cfg["n_envs"]
+    env = sg.VecTaskEnv(robots=(cfg["robot"],), device=local, n_envs=n, seed=0, task=cfg["task"],
+                        goal_sigma=cfg["goal_sigma"], row_offset=rank * n)
+    A, O = env.action_dim, env.obs_dim
+    env.reset()
+    env.bench_begin(0, first_step=0, global_n_envs=world * n)
+    F = max(1, min(args.fuse, args.steps))
+    # warm-up: W untimed steps (first is the bench_sim warm-up step), plus one
+    # untimed fused launch so the timed launches see a warm instruction cache
+    for _ in range(max(args.warmup, 1)):
+        env.bench_step(1)
+    env.bench_step(F)
+    steps_done = max(args.warmup, 1) + F
+    torch.cuda.synchronize()
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
+    launches = []
+    k = args.steps
+    while k > 0:
+        launches.append(min(F, k))
+        k -= launches[-1]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for (e0, e1), kf in zip(ev, launches):
+            flush.zero_()
+            e0.record()
+            env.bench_step(kf)
+            e1.record()
+        torch.cuda.synchronize()
+    env.synchronize()
+    steps_done += args.steps
+    launch_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    t_ms = sum(launch_ms)
+    if dist:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        dist.barrier()
+    value = world * n * args.steps / (t_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (env_step_kernel, fused bench variant)
+    resets = (steps_done // 300) - ((steps_done - args.steps) // 300)
+    b = step_bytes(A, O, F, resets / max(args.steps, 1))
+    full = [ms for ms, kf in zip(launch_ms, launches) if kf == F]
+    avg_launch_s = (sum(full) / len(full)) * 1e-3 if full else t_ms * 1e-3 / len(launches)
+    peak, peak_kind = peaks()
+    achieved = n * b["per_env_launch"] / avg_launch_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the host C-ABI call (pinned host buffers) --------------
+    e2e = None
+    if args.e2e_steps > 0:
+        E = args.e2e_steps
+        h_act = torch.empty((E, n, A), dtype=torch.float32).pin_memory()
+        for s in range(E):  # pre-generate the bench stream (device generator), outside timing
+            env.bench_step(1)
+            h_act[s].copy_(env.bench_actions())
+        outs = {k2: torch.empty(shape, dtype=dt).pin_memory() for k2, shape, dt in (
+            ("observations", (n, O), torch.float32), ("terminal_observations", (n, O), torch.float32),
+            ("rewards", (n,), torch.float32), ("task_error", (n,), torch.float32),
+            ("terminated", (n,), torch.uint8), ("timed_out", (n,), torch.uint8))}
+        hr = sg.HostResult()
+        for k2, t in outs.items():
+            setattr(hr, k2, t.data_ptr())
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(E):
+            env.step_host_ptr(h_act[s].data_ptr(), hr)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        d2h = sum(t.numel() * t.element_size() for t in outs.values()) + 8
+        e2e = dict(value=world * n * E / (e2e_ms * 1e-3), unit="env-steps/s", h2d_bytes_per_step=n * A * 4,
+                   d2h_bytes_per_step=d2h, steps=E, path="sg_env_step_host (C-ABI), 1 launch/step")
+
+    # ---- per-step API in a CUDA graph (1 launch per step, no fusion) --------
+    single = None
+    try:
+        G = 64
+        g = torch.cuda.CUDAGraph()
+        s_ = torch.cuda.Stream()
+        env.set_stream(s_)
+        with torch.cuda.graph(g, stream=s_):
+            for _ in range(G):
+                env.bench_step(1)
+        env.set_stream(None)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        reps = 10
+        tot = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        single = dict(value=n * G * reps / (tot * 1e-3), unit="env-steps/s",
+                      how=f"CUDA graph of {G} single-step launches, L2 flushed between replays")
+    except Exception as ex:  # informational only
+        single = dict(error=str(ex)[:200])
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, lanes, sample = cpu_reference(cfg, 10_000, budget_s=args.cpu_budget)
+        cpu = dict(value=rate, unit="env-steps/s", cores=lanes, kind="port", sample=sample)
+
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit="env-steps/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+            ms_per_step=t_ms / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+            dtype="fp32", data="synthetic",
+            config=dict(workload=cfg["workload"], n_envs_per_gpu=n, global_envs=world * n,
+                        fused_steps_per_launch=F, parallelism=f"env-shard x{world}",
+                        l2="256 MiB flush between timed launches; per-launch state read cold from HBM"),
+            roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+                          traffic=traffic, peak_kind=peak_kind, kernel="env_step_kernel<8,true>",
+                          bytes_per_env_step=b["per_env_step"], bytes_per_launch=n * b["per_env_launch"],
+                          avg_launch_us=avg_launch_s * 1e6),
+            cpu_baseline=cpu, e2e=e2e, single_step_launches=single,
+            gpu_launches=len(launches), clocks=clk.summary(),
+        )
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

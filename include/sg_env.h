@@ -1,0 +1,227 @@
+/*
+ * sg_env.h — C-ABI drop-in boundary for the batched environment step
+ * (B200-native replacement of the reference "scalpel" VecTaskEnv hot path).
+ *
+ * Plain pointers and sizes only: no torch, no Eigen, no C++ types. Device
+ * buffers are owned by the env handle; views returned by reset/step stay
+ * valid until the next call on the same handle (ownership rule of the
+ * reference: `reset()`/`step()` return const refs to member buffers,
+ * proj/include/scalpel/envs.hpp:113-114,177).
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *   sg_env_create            VecTaskEnv::VecTaskEnv        src/envs.cpp:118-223
+ *                            + make_env / resolve_robot      src/config.cpp:366-370,
+ *                                                             src/robot_model.cpp:337-349
+ *   sg_env_destroy           ~VecTaskEnv
+ *   sg_env_dims              BatchedEnv::n_envs/obs_dim/action_dim  include/scalpel/envs.hpp:110-112
+ *   sg_env_layout_*          VecTaskEnv::layout()          include/scalpel/envs.hpp:137, src/envs.cpp:166-192
+ *   sg_env_reset             BatchedEnv::reset()           src/envs.cpp:425-435
+ *   sg_env_step              BatchedEnv::step(actions)     src/envs.cpp:437-617
+ *   sg_env_step_host         BatchedEnv::step on host buffers (same call a host-side
+ *                            caller such as Trainer::iterate, src/ppo.cpp:279, makes)
+ *   sg_env_task_error        BatchedEnv::task_error()      include/scalpel/envs.hpp:117
+ *   sg_env_bench_*           bench_sim's action stream + step loop  src/bench.cpp:31-35,97-135
+ *   sg_robot_*               parse_robot / forward_kinematics_batch  src/robot_model.cpp:191-283,404-443
+ *   sg_last_error            exception message (what()) of the reference's
+ *                            ConfigError / ParseError / SimError  include/scalpel/errors.hpp:23-48
+ *
+ * Error convention (tools/main.cpp:246-255 exit codes): every int-returning
+ * entry point returns SG_OK (0), SG_ERR_SIM (1: SimError — shape mismatch,
+ * non-finite action or reward, out-of-limit FK input) or SG_ERR_CONFIG
+ * (2: ConfigError/ParseError — bad config or descriptor, goal sampling
+ * exhaustion). The message is thread-local, read with sg_last_error().
+ * Device-detected errors (non-finite action/reward, goal-sampling exhaustion)
+ * are latched in a device error word and reported by the next synchronising
+ * call (sg_env_step_host, sg_env_synchronize, sg_env_read_*).
+ */
+#ifndef SG_ENV_H
+#define SG_ENV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_OK 0
+#define SG_ERR_SIM 1
+#define SG_ERR_CONFIG 2
+
+/* Task enum, same order as scalpel::Task (include/scalpel/envs.hpp:31-37). */
+enum {
+  SG_TASK_TARGET_REACHING = 0,
+  SG_TASK_ACTIVE_TRACKING = 1,
+  SG_TASK_IMAGE_MATCHING = 2,
+  SG_TASK_PATH_FOLLOWING = 3,
+  SG_TASK_MULTI_TOOL_REACHING = 4
+};
+
+/* scalpel::ControlMode (include/scalpel/dynamics.hpp:27). */
+enum { SG_CONTROL_POSITION = 0, SG_CONTROL_VELOCITY = 1, SG_CONTROL_TORQUE = 2 };
+
+/* scalpel::EnvConfig (include/scalpel/envs.hpp:42-63); defaults from
+ * sg_env_config_init. row_offset = global index of this handle's row 0, so
+ * per-env RNG streams are seeded by GLOBAL env id (multi-GPU sharding: rank r
+ * of an N-per-rank job passes row_offset = r*N and is bit-identical to the
+ * same rows of a single-device run). */
+typedef struct sg_env_config {
+  int32_t task;
+  int32_t episode_len;
+  int64_t n_envs;
+  double goal_sigma;
+  double goal_offset_clip;
+  double reward_scale;
+  double path_penalty;
+  double success_radius;
+  int32_t success_hold;
+  int32_t reserved0;
+  double workspace_radius;
+  double waypoint_spacing;
+  double tracking_vel_noise_std;
+  double tracking_vel_clamp;
+  double collision_threshold;
+  double collision_penalty;
+  double view_penalty;
+  uint64_t seed;
+  int64_t row_offset;
+} sg_env_config;
+
+/* scalpel::DynamicsConfig (include/scalpel/dynamics.hpp:34-44). Gain arrays
+ * follow VecTaskEnv's resolution rule (src/envs.cpp:145-153): length 0 ->
+ * per-robot defaults, 1 -> broadcast, dof -> per-DoF. */
+typedef struct sg_dynamics_config {
+  double control_dt;
+  int32_t substeps;
+  int32_t control_mode;
+  const double* kp;
+  int32_t n_kp;
+  int32_t n_kd;
+  const double* kd;
+  const double* inertia;
+  int32_t n_inertia;
+  int32_t n_damping;
+  const double* damping;
+} sg_dynamics_config;
+
+/* Device views of one StepResult (include/scalpel/envs.hpp:82-89), fp32 /
+ * u8, row-major n_envs x obs_dim like the reference's MatrixXdR. Rows of ended
+ * envs in `observations` are already post-reset; `terminal_observations` is
+ * valid on ended rows only. `action_saturations_total` is a device u64 that
+ * accumulates StepDiagnostics::saturated_actions over the handle's lifetime
+ * (per-step value = difference of consecutive reads). */
+typedef struct sg_step_views {
+  float* observations;
+  float* terminal_observations;
+  float* rewards;
+  float* task_error;
+  uint8_t* terminated;
+  uint8_t* timed_out;
+  unsigned long long* action_saturations_total;
+  int64_t n_envs;
+  int32_t obs_dim;
+  int32_t action_dim;
+} sg_step_views;
+
+/* Host copy of one StepResult (sg_env_step_host). Any pointer may be NULL
+ * to skip that field's device->host copy. */
+typedef struct sg_host_result {
+  float* observations;
+  float* terminal_observations;
+  float* rewards;
+  float* task_error;
+  uint8_t* terminated;
+  uint8_t* timed_out;
+  int64_t action_saturations; /* this step */
+} sg_host_result;
+
+/* Device state views (SimBatch + TaskState, include/scalpel/sim_batch.hpp:28-41,
+ * envs.hpp:66-80) for parity tests and integration. Joint arrays are DoF-major
+ * structure-of-arrays: element (row, dof) lives at [dof * n_envs + row].
+ * goals/tips: [k * n_envs + row], k = 0..2. Waypoint table: row-major
+ * [row][waypoint_cap][3]. */
+typedef struct sg_state_views {
+  float* q;
+  float* qdot;
+  float* q_target;
+  float* goals;
+  float* tips;
+  int32_t* step_count;
+  int32_t* hold_count;
+  int64_t* episode_count;
+  int32_t* waypoint_idx;
+  int32_t* waypoint_len;
+  float* waypoints;
+  uint64_t* rng_state;
+  uint64_t* rng_inc;
+  int32_t waypoint_cap;
+  int32_t dof;
+  int64_t n_envs;
+} sg_state_views;
+
+typedef struct sg_env sg_env;
+
+void sg_env_config_init(sg_env_config* cfg);
+void sg_dynamics_config_init(sg_dynamics_config* dyn);
+
+/* robots[i] is a builtin name ("psm", "ecm", "star") or a path to a .robot
+ * descriptor (resolve_robot semantics). device: CUDA ordinal. */
+int sg_env_create(const sg_env_config* cfg, const sg_dynamics_config* dyn,
+                  const char* const* robots, int32_t n_robots, int32_t device, sg_env** out);
+/* Same, from descriptor texts; origins[i] names the text in ParseError messages. */
+int sg_env_create_from_text(const sg_env_config* cfg, const sg_dynamics_config* dyn,
+                            const char* const* texts, const char* const* origins,
+                            int32_t n_robots, int32_t device, sg_env** out);
+void sg_env_destroy(sg_env* env);
+
+/* cudaStream_t as void*; NULL = the legacy default stream. */
+int sg_env_set_stream(sg_env* env, void* stream);
+int sg_env_dims(const sg_env* env, int64_t* n_envs, int32_t* obs_dim, int32_t* action_dim);
+int32_t sg_env_layout_count(const sg_env* env);
+int sg_env_layout_field(const sg_env* env, int32_t index, const char** name, int32_t* offset,
+                        int32_t* length);
+int sg_env_workspace(const sg_env* env, double* center3, double* radius);
+
+int sg_env_reset(sg_env* env, sg_step_views* out);
+/* d_actions: device, row-major n_envs x action_dim fp32 (stride = action_dim). */
+int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out);
+/* Host actions (pinned or pageable): H2D copy, step, D2H copy of the fields
+ * requested in `out`, synchronise, report errors. */
+int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out);
+int sg_env_task_error(const sg_env* env, float** d_task_error);
+int sg_env_state(const sg_env* env, sg_state_views* out);
+/* Waits for the env stream and converts the device error word. */
+int sg_env_synchronize(sg_env* env);
+
+/* Bench workload of bench_sim (src/bench.cpp:31-35,97-135): actions are draw
+ * #(s*G*A + g*A + d) of make_stream(seed, 0xac7104) for step s, GLOBAL env g,
+ * DoF d — the reference's serial row-major fill, reproduced bit-for-bit on the
+ * device by PCG32 jump-ahead. global_n_envs/row_offset describe the sharding
+ * (single device: n_envs / 0). first_step: index of the next step (0 = the
+ * untimed warm-up step of bench_sim). */
+int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t global_n_envs);
+/* k_steps fused steps in ONE launch: per step, generate the actions (also
+ * written to the env's action buffer), step, write the full StepResult and
+ * auto-reset. Equivalent to k_steps calls of sg_env_step with those actions. */
+int sg_env_bench_step(sg_env* env, int32_t k_steps);
+/* Device buffer the bench generator writes (n_envs x action_dim fp32). */
+int sg_env_bench_actions(const sg_env* env, float** d_actions);
+
+/* Robot-model utilities. */
+typedef struct sg_robot sg_robot;
+int sg_robot_parse(const char* text, const char* origin, sg_robot** out);
+int sg_robot_resolve(const char* name_or_path, sg_robot** out);
+void sg_robot_destroy(sg_robot* robot);
+int sg_robot_dof(const sg_robot* robot, int32_t* dof, int32_t* jaw_dof);
+/* Batched FK on the device: d_q row-major n x dof fp32 -> d_pos n x 3 fp32.
+ * Out-of-limit rows (check_q, src/robot_model.cpp:353-367) raise SG_ERR_SIM. */
+int sg_robot_fk(const sg_robot* robot, const float* d_q, int64_t n, float* d_pos, void* stream);
+
+const char* sg_last_error(void);
+const char* sg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SG_ENV_H */

@@ -1,0 +1,776 @@
+// Host side of the drop-in boundary: env object, device allocation, kernel
+// launch, and the extern "C" entry points declared in include/sg_env.h.
+//
+// Mirrors VecTaskEnv construction (proj/src/envs.cpp:118-223): config
+// validation (:65-81), gain resolution (:142-158, default_dynamics_config
+// dynamics.cpp:69-86, DynamicsConfig::validate :44-67), SimBatch seeding
+// (dynamics.cpp:225-241), workspace centre = FK(mid) (:161-162), observation
+// layout (:166-192). The step itself is one fused kernel (kernels.cuh).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <array>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "robot.hpp"
+#include "sg_env.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw sg::SimError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+// ---- host PCG32 (rng.hpp:25-83) for stream seeding and jump tables --------
+struct HostPcg {
+  uint64_t state = 0, inc = 0;
+  uint32_t next() {
+    const uint64_t old = state;
+    state = old * sg::kPcgMult + inc;
+    const uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+    const uint32_t rot = static_cast<uint32_t>(old >> 59u);
+    return (xs >> rot) | (xs << ((32u - rot) & 31u));
+  }
+  void seed(uint64_t initstate, uint64_t initseq) {
+    state = 0;
+    inc = (initseq << 1u) | 1u;
+    next();
+    state += initstate;
+    next();
+  }
+};
+
+uint64_t splitmix64(uint64_t& x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+HostPcg make_stream(uint64_t seed, uint64_t id) {
+  uint64_t x = seed ^ (0x2545f4914f6cdd1dULL * (id + 1));
+  const uint64_t a = splitmix64(x);
+  const uint64_t b = splitmix64(x);
+  HostPcg r;
+  r.seed(a, b);
+  return r;
+}
+
+// Affine map s -> mult * s + add equal to k PCG32 advances with increment inc.
+void pcg_jump(uint64_t k, uint64_t inc, uint64_t& mult, uint64_t& add) {
+  uint64_t acc_m = 1, acc_a = 0, cur_m = sg::kPcgMult, cur_a = inc;
+  while (k) {
+    if (k & 1) {
+      acc_m *= cur_m;
+      acc_a = acc_a * cur_m + cur_a;
+    }
+    cur_a = (cur_m + 1) * cur_a;
+    cur_m *= cur_m;
+    k >>= 1;
+  }
+  mult = acc_m;
+  add = acc_a;
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  CK(cudaMemset(p, 0, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+using Mat3 = std::array<double, 9>;
+
+Mat3 quat_to_mat(const sg::Quat& q) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  return {1 - 2 * (y * y + z * z), 2 * (x * y - w * z),     2 * (x * z + w * y),
+          2 * (x * y + w * z),     1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+          2 * (x * z - w * y),     2 * (y * z + w * x),     1 - 2 * (x * x + y * y)};
+}
+
+Mat3 mat_mul(const Mat3& a, const Mat3& b) {
+  Mat3 o{};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) o[r * 3 + c] = a[r * 3] * b[c] + a[r * 3 + 1] * b[3 + c] + a[r * 3 + 2] * b[6 + c];
+  return o;
+}
+
+sg::Vec3 mat_vec(const Mat3& a, const sg::Vec3& v) {
+  return {a[0] * v[0] + a[1] * v[1] + a[2] * v[2], a[3] * v[0] + a[4] * v[1] + a[5] * v[2],
+          a[6] * v[0] + a[7] * v[1] + a[8] * v[2]};
+}
+
+bool is_identity(const Mat3& m) {
+  const Mat3 I{1, 0, 0, 0, 1, 0, 0, 0, 1};
+  return m == I;
+}
+
+// Packs the chain per actuated joint. A pending rigid transform (p, R)
+// accumulates fixed joints (fk_walk: p += R*o; R = R*R_o) and is folded into
+// the next actuated joint's origin, or into the tool tip at the end.
+sg::RobotTable build_table(const sg::RobotModel& m, double dt_sub, const std::vector<double>& kp,
+                           const std::vector<double>& kd, const std::vector<double>& inertia,
+                           const std::vector<double>& damping) {
+  if (m.dof_count > sg::kMaxDof)
+    throw sg::ConfigError("robot '" + m.name + "' has more than " + std::to_string(sg::kMaxDof) + " DoF");
+  sg::RobotTable t;
+  std::memset(&t, 0, sizeof(t));
+  t.dof = m.dof_count;
+  t.jaw = m.jaw_dof();
+  sg::Vec3 pend_p{0, 0, 0};
+  Mat3 pend_R{1, 0, 0, 0, 1, 0, 0, 0, 1};
+  int d = 0;
+  for (const auto& j : m.joints) {
+    const Mat3 Rj = quat_to_mat(j.origin_rotation);
+    const sg::Vec3 o = mat_vec(pend_R, j.origin_translation);
+    const sg::Vec3 p{pend_p[0] + o[0], pend_p[1] + o[1], pend_p[2] + o[2]};
+    // exact identity when the quaternion is (1,0,0,0) (every builtin origin)
+    const bool ident_j = j.origin_rotation == sg::Quat{1, 0, 0, 0};
+    const Mat3 Rc = ident_j ? pend_R : mat_mul(pend_R, Rj);
+    if (j.kind == sg::JointKind::Fixed) {
+      pend_p = p;
+      pend_R = Rc;
+      continue;
+    }
+    auto& e = t.j[d++];
+    e.kind = static_cast<int32_t>(j.kind);
+    e.axis_code = 6;
+    for (int k = 0; k < 3; ++k) {
+      const int o1 = (k + 1) % 3, o2 = (k + 2) % 3;
+      if (j.axis[o1] == 0.0 && j.axis[o2] == 0.0) {
+        if (j.axis[k] == 1.0) e.axis_code = k;
+        if (j.axis[k] == -1.0) e.axis_code = k + 3;
+      }
+    }
+    for (int k = 0; k < 3; ++k) {
+      e.axis[k] = static_cast<float>(j.axis[k]);
+      e.o[k] = static_cast<float>(p[k]);
+      if (p[k] != 0.0) e.flags |= 1 << k;
+    }
+    if (!is_identity(Rc)) {
+      e.flags |= 8;
+      for (int k = 0; k < 9; ++k) e.R[k] = static_cast<float>(Rc[k]);
+    }
+    pend_p = {0, 0, 0};
+    pend_R = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  }
+  // tip = pending o (p + R * tip_xyz); the tip orientation does not move the point
+  const sg::Vec3 tt = mat_vec(pend_R, m.tip_position);
+  for (int k = 0; k < 3; ++k) {
+    const double v = pend_p[k] + tt[k];
+    t.tip[k] = static_cast<float>(v);
+    if (v != 0.0) t.tip_flags |= 1 << k;
+  }
+  for (int dd = 0; dd < m.dof_count; ++dd) {
+    const auto& j = m.dof_joint(dd);
+    t.lo[dd] = static_cast<float>(j.limit_lo);
+    t.hi[dd] = static_cast<float>(j.limit_hi);
+    t.vel[dd] = static_cast<float>(j.velocity_limit);
+    t.eff[dd] = static_cast<float>(j.effort_limit);
+    t.lo_d[dd] = j.limit_lo;
+    t.hi_d[dd] = j.limit_hi;
+    t.kp[dd] = static_cast<float>(kp[dd]);
+    t.kd[dd] = static_cast<float>(kd[dd]);
+    t.damping[dd] = static_cast<float>(damping[dd]);
+    t.dt_over_inertia[dd] = static_cast<float>(dt_sub / inertia[dd]);
+  }
+  return t;
+}
+
+int block_size() {
+  static int b = [] {
+    const char* s = std::getenv("SG_BLOCK");
+    int v = s ? std::atoi(s) : 64;
+    if (v < 32 || v > 128 || (v & 31)) v = 64;
+    return v;
+  }();
+  return b;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return SG_OK;
+  } catch (const sg::SimError& e) {
+    g_last_error = e.what();
+    return SG_ERR_SIM;
+  } catch (const sg::ConfigError& e) {
+    g_last_error = e.what();
+    return SG_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SG_ERR_SIM;
+  }
+}
+
+}  // namespace
+
+struct sg_robot {
+  sg::RobotModel model;
+  sg::RobotTable table;
+};
+
+struct sg_env {
+  sg::RobotModel model;
+  sg_env_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  sg::StepParams P{};
+  int A = 0, O = 0;
+  int64_t n = 0;
+  double center[3]{};
+  double radius = 0;
+  std::vector<std::pair<std::string, std::pair<int, int>>> layout;
+  float* d_actions_in = nullptr;  // staging for sg_env_step_host
+  unsigned long long last_sat = 0;
+  bool bench_ready = false;
+
+  ~sg_env() {
+    cudaSetDevice(device);
+    cudaStreamSynchronize(stream);
+    const auto& p = P.p;
+    void* bufs[] = {p.q,   p.qd,       p.qt,         p.goals,      p.tips,     p.step_count, p.hold_count,
+                    p.episode_count, p.wp_idx,     p.wp_len,     p.wps,      p.rng_state,  p.rng_inc,
+                    p.obs, p.tobs,     p.rewards,    p.task_error, p.terminated, p.timed_out, p.sat_total,
+                    p.err, p.act_state, p.act_buf, d_actions_in};
+    for (void* b : bufs)
+      if (b) cudaFree(b);
+  }
+
+  int dmax() const { return A <= 8 ? 8 : 16; }
+
+  size_t smem_bytes() const { return static_cast<size_t>(block_size()) * (O + A) * sizeof(float); }
+
+  void launch_step(int k_steps, bool gen) {
+    const int b = block_size();
+    const unsigned grid = static_cast<unsigned>((n + b - 1) / b);
+    const size_t sm = smem_bytes();
+    if (dmax() == 8) {
+      if (gen) sg::env_step_kernel<8, true><<<grid, b, sm, stream>>>(P, k_steps);
+      else sg::env_step_kernel<8, false><<<grid, b, sm, stream>>>(P, k_steps);
+    } else {
+      if (gen) sg::env_step_kernel<16, true><<<grid, b, sm, stream>>>(P, k_steps);
+      else sg::env_step_kernel<16, false><<<grid, b, sm, stream>>>(P, k_steps);
+    }
+    CK(cudaGetLastError());
+  }
+
+  void launch_reset() {
+    const int b = block_size();
+    const unsigned grid = static_cast<unsigned>((n + b - 1) / b);
+    const size_t sm = static_cast<size_t>(b) * O * sizeof(float);
+    if (dmax() == 8) sg::env_reset_kernel<8><<<grid, b, sm, stream>>>(P);
+    else sg::env_reset_kernel<16><<<grid, b, sm, stream>>>(P);
+    CK(cudaGetLastError());
+  }
+
+  void views(sg_step_views* out) const {
+    if (!out) return;
+    out->observations = P.p.obs;
+    out->terminal_observations = P.p.tobs;
+    out->rewards = P.p.rewards;
+    out->task_error = P.p.task_error;
+    out->terminated = P.p.terminated;
+    out->timed_out = P.p.timed_out;
+    out->action_saturations_total = P.p.sat_total;
+    out->n_envs = n;
+    out->obs_dim = O;
+    out->action_dim = A;
+  }
+
+  // Synchronise and convert the device error word (errors.hpp semantics).
+  void check() {
+    CK(cudaStreamSynchronize(stream));
+    int32_t err = 0;
+    CK(cudaMemcpy(&err, P.p.err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (!err) return;
+    CK(cudaMemset(P.p.err, 0, sizeof(int32_t)));
+    if (err & sg::kErrNonFiniteAction) throw sg::SimError("dynamics.step: non-finite action entry");
+    if (err & sg::kErrNonFiniteReward) throw sg::SimError("env.step: non-finite reward");
+    if (err & sg::kErrGoalSampling)
+      throw sg::ConfigError("goal sampling rejected 1000 candidates; workspace_radius is misconfigured for goal_sigma");
+    if (err & sg::kErrWaypointCap) throw sg::SimError("env: waypoint table capacity exceeded");
+    throw sg::SimError("env: device error " + std::to_string(err));
+  }
+};
+
+namespace {
+
+void validate_env_config(const sg_env_config& c) {  // envs.cpp:65-81
+  if (c.n_envs < 1) throw sg::ConfigError("env.n_envs must be >= 1");
+  if (c.episode_len < 1) throw sg::ConfigError("env.episode_len must be >= 1");
+  if (!(c.goal_sigma > 0.0)) throw sg::ConfigError("env.goal_sigma must be > 0");
+  if (!(c.success_radius > 0.0)) throw sg::ConfigError("env.success_radius must be > 0");
+  if (!(c.reward_scale < 0.0)) throw sg::ConfigError("env.reward_scale (rho) must be < 0");
+  if (!(c.path_penalty > 0.0)) throw sg::ConfigError("env.path_penalty (alpha) must be > 0");
+  if (c.success_hold < 1) throw sg::ConfigError("env.success_hold must be >= 1");
+  if (!(c.goal_offset_clip > 0.0)) throw sg::ConfigError("env.goal_offset_clip must be > 0");
+  if (!(c.waypoint_spacing > 0.0)) throw sg::ConfigError("env.waypoint_spacing must be > 0");
+  if (c.workspace_radius < 0.0) throw sg::ConfigError("env.workspace_radius must be >= 0");
+  if (c.tracking_vel_noise_std < 0.0) throw sg::ConfigError("env.tracking_vel_noise_std must be >= 0");
+  if (!(c.tracking_vel_clamp > 0.0)) throw sg::ConfigError("env.tracking_vel_clamp must be > 0");
+  if (c.collision_threshold < 0.0) throw sg::ConfigError("env.collision_threshold must be >= 0");
+  if (c.collision_penalty < 0.0) throw sg::ConfigError("env.collision_penalty must be >= 0");
+  if (c.view_penalty < 0.0) throw sg::ConfigError("env.view_penalty must be >= 0");
+}
+
+const char* task_name(int t) {
+  switch (t) {
+    case SG_TASK_TARGET_REACHING: return "target_reaching";
+    case SG_TASK_ACTIVE_TRACKING: return "active_tracking";
+    case SG_TASK_IMAGE_MATCHING: return "image_matching";
+    case SG_TASK_PATH_FOLLOWING: return "path_following";
+    case SG_TASK_MULTI_TOOL_REACHING: return "multi_tool_reaching";
+  }
+  return "?";
+}
+
+std::vector<double> resolve_gain(const double* v, int32_t count, const std::vector<double>& fallback, int dof,
+                                 const char* name) {
+  if (count < 0) throw sg::ConfigError(std::string("dynamics.") + name + ": negative length");
+  if (count == 0) return fallback;
+  if (count == 1) return std::vector<double>(dof, v[0]);
+  return std::vector<double>(v, v + count);
+}
+
+std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_config* dyn,
+                                 std::vector<sg::RobotModel> models, int device) {
+  validate_env_config(cfg);
+  if (models.empty()) throw sg::ConfigError("env: at least one robot is required");
+  if (cfg.task == SG_TASK_MULTI_TOOL_REACHING) {
+    if (models.size() < 2) throw sg::ConfigError("multi_tool_reaching requires >= 2 robots");
+  } else if (models.size() != 1) {
+    throw sg::ConfigError(std::string(task_name(cfg.task)) + " requires exactly 1 robot");
+  }
+  if (cfg.task != SG_TASK_TARGET_REACHING && cfg.task != SG_TASK_PATH_FOLLOWING)
+    throw sg::ConfigError(std::string("task '") + task_name(cfg.task) +
+                          "' is not on the sg_env device path (target_reaching, path_following)");
+
+  auto env = std::make_unique<sg_env>();
+  env->model = std::move(models[0]);
+  const sg::RobotModel& m = env->model;
+  env->cfg = cfg;
+  env->device = device;
+  CK(cudaSetDevice(device));
+  env->n = cfg.n_envs;
+  env->A = m.dof_count;
+  env->O = 3 * m.dof_count + 6;
+
+  // ---- dynamics (dynamics.cpp:44-86, envs.cpp:142-158) ---------------------
+  sg_dynamics_config dc;
+  sg_dynamics_config_init(&dc);
+  if (dyn) dc = *dyn;
+  const int dof = m.dof_count;
+  std::vector<double> dkp(dof), dkd(dof), dinert(dof), ddamp(dof);
+  for (int d = 0; d < dof; ++d) {
+    const double mass = m.dof_joint(d).kind == sg::JointKind::Prismatic ? 0.5 : 0.05;
+    dinert[d] = mass;
+    dkp[d] = 380.0 * mass;
+    dkd[d] = 2.0 * std::sqrt(dkp[d] * mass);
+    ddamp[d] = 0.1 * dkd[d];
+  }
+  auto kp = resolve_gain(dc.kp, dc.n_kp, dkp, dof, "kp");
+  auto kd = resolve_gain(dc.kd, dc.n_kd, dkd, dof, "kd");
+  auto inertia = resolve_gain(dc.inertia, dc.n_inertia, dinert, dof, "inertia");
+  auto damping = resolve_gain(dc.damping, dc.n_damping, ddamp, dof, "damping");
+  if (!(dc.control_dt > 0.0)) throw sg::ConfigError("dynamics.control_dt must be > 0");
+  if (dc.substeps < 1) throw sg::ConfigError("dynamics.substeps must be >= 1");
+  if (dc.control_mode < 0 || dc.control_mode > 2) throw sg::ConfigError("unknown control mode");
+  auto check_vec = [&](const std::vector<double>& v, const char* name, bool positive) {
+    if (static_cast<int>(v.size()) != dof)
+      throw sg::ConfigError(std::string("dynamics.") + name + " must have one entry per DoF (" +
+                            std::to_string(dof) + "), got " + std::to_string(v.size()));
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (positive && !(v[i] > 0.0))
+        throw sg::ConfigError(std::string("dynamics.") + name + "[" + std::to_string(i) + "] must be > 0");
+      if (!positive && v[i] < 0.0)
+        throw sg::ConfigError(std::string("dynamics.") + name + "[" + std::to_string(i) + "] must be >= 0");
+    }
+  };
+  check_vec(kp, "kp", true);
+  check_vec(kd, "kd", true);
+  check_vec(inertia, "inertia", true);
+  check_vec(damping, "damping", false);
+  const double dt_sub = dc.control_dt / dc.substeps;
+
+  auto& P = env->P;
+  P.robot = build_table(m, dt_sub, kp, kd, inertia, damping);
+
+  // ---- task params ------------------------------------------------------------
+  env->radius = cfg.workspace_radius > 0.0 ? cfg.workspace_radius : 3.0 * cfg.goal_sigma;  // envs.cpp:134
+  const sg::Vec3 c = sg::forward_kinematics_position(m, m.mid_configuration());           // envs.cpp:161-162
+  for (int k = 0; k < 3; ++k) env->center[k] = c[k];
+  auto& T = P.task;
+  T.task = cfg.task;
+  T.episode_len = cfg.episode_len;
+  T.success_hold = cfg.success_hold;
+  T.substeps = dc.substeps;
+  T.control_mode = dc.control_mode;
+  T.n = env->n;
+  T.rho = static_cast<float>(cfg.reward_scale);
+  T.neg_alpha = static_cast<float>(-cfg.path_penalty);
+  T.success_radius = static_cast<float>(cfg.success_radius);
+  T.dt_sub = static_cast<float>(dt_sub);
+  T.goal_sigma = cfg.goal_sigma;
+  T.radius = env->radius;
+  for (int k = 0; k < 3; ++k) T.center[k] = env->center[k];
+  T.spacing = cfg.waypoint_spacing;
+  // Path length bound: |S'(u)| <= 3|a|u^2 + 2|b|u + |c| integrates to
+  // |a| + |b| + |c| <= (0.5 + 0.5 + 0.3) * sqrt(3) (coefficient ranges of
+  // sample_path, envs.cpp:244-246); shrinking only shortens the path.
+  T.wp_cap = cfg.task == SG_TASK_PATH_FOLLOWING
+                 ? static_cast<int32_t>(std::floor(1.3 * std::sqrt(3.0) / cfg.waypoint_spacing)) + 4
+                 : 0;
+
+  // ---- layout (envs.cpp:166-192) ---------------------------------------------
+  int off = 0;
+  auto add = [&](const char* name, int len) {
+    env->layout.push_back({name, {off, len}});
+    off += len;
+  };
+  add("dof_pos", dof);
+  add("dof_vel", dof);
+  add("tip_pos", 3);
+  add("dof_target", dof);
+  add(cfg.task == SG_TASK_PATH_FOLLOWING ? "waypoint" : "goal", 3);
+
+  // ---- device state (SoA) -------------------------------------------------------
+  const int64_t n = env->n;
+  auto& p = P.p;
+  p.q = dalloc<float>(n * dof);
+  p.qd = dalloc<float>(n * dof);
+  p.qt = dalloc<float>(n * dof);
+  p.goals = dalloc<float>(n * 3);
+  p.tips = dalloc<float>(n * 3);
+  p.step_count = dalloc<int32_t>(n);
+  p.hold_count = dalloc<int32_t>(n);
+  p.episode_count = dalloc<int64_t>(n);
+  p.wp_idx = dalloc<int32_t>(n);
+  p.wp_len = dalloc<int32_t>(n);
+  p.wps = T.wp_cap ? dalloc<float>(static_cast<size_t>(n) * T.wp_cap * 3) : nullptr;
+  p.rng_state = dalloc<uint64_t>(n);
+  p.rng_inc = dalloc<uint64_t>(n);
+  p.obs = dalloc<float>(n * env->O);
+  p.tobs = dalloc<float>(n * env->O);
+  p.rewards = dalloc<float>(n);
+  p.task_error = dalloc<float>(n);
+  p.terminated = dalloc<uint8_t>(n);
+  p.timed_out = dalloc<uint8_t>(n);
+  p.sat_total = dalloc<unsigned long long>(1);
+  p.err = dalloc<int32_t>(1);
+  p.act_state = nullptr;
+  p.act_buf = nullptr;
+  // SimBatch::create (dynamics.cpp:225-241): mid configuration at rest, stream
+  // id = salt * 2^32 + global row (single tool: salt 0).
+  {
+    const auto mid = m.mid_configuration();
+    std::vector<float> qh(static_cast<size_t>(n) * dof);
+    for (int d = 0; d < dof; ++d)
+      for (int64_t i = 0; i < n; ++i) qh[d * n + i] = static_cast<float>(mid[d]);
+    CK(cudaMemcpy(p.q, qh.data(), qh.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p.qt, qh.data(), qh.size() * sizeof(float), cudaMemcpyHostToDevice));
+    std::vector<uint64_t> st(n), inc(n);
+    for (int64_t i = 0; i < n; ++i) {
+      HostPcg r = make_stream(cfg.seed, static_cast<uint64_t>(cfg.row_offset + i));
+      st[i] = r.state;
+      inc[i] = r.inc;
+    }
+    CK(cudaMemcpy(p.rng_state, st.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p.rng_inc, inc.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
+  env->d_actions_in = dalloc<float>(n * dof);
+  // opt in to > 48 KB dynamic shared memory if a large robot needs it
+  const size_t sm = env->smem_bytes();
+  if (sm > 48 * 1024) {
+    CK(cudaFuncSetAttribute(sg::env_step_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(sg::env_step_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(sg::env_reset_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  }
+  CK(cudaDeviceSynchronize());
+  return env;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sg_last_error(void) { return g_last_error.c_str(); }
+const char* sg_version(void) { return "sg_env 0.1 (sm_100a)"; }
+
+void sg_env_config_init(sg_env_config* c) {  // envs.hpp:42-63
+  std::memset(c, 0, sizeof(*c));
+  c->task = SG_TASK_TARGET_REACHING;
+  c->n_envs = 1024;
+  c->episode_len = 300;
+  c->goal_sigma = 0.05;
+  c->goal_offset_clip = 0.2;
+  c->reward_scale = -1.0;
+  c->path_penalty = 1.0;
+  c->success_radius = 0.005;
+  c->success_hold = 10;
+  c->workspace_radius = 0.0;
+  c->waypoint_spacing = 0.02;
+  c->tracking_vel_noise_std = 0.01;
+  c->tracking_vel_clamp = 0.01;
+  c->collision_threshold = 0.01;
+  c->collision_penalty = 1.0;
+  c->view_penalty = 0.1;
+  c->seed = 0;
+  c->row_offset = 0;
+}
+
+void sg_dynamics_config_init(sg_dynamics_config* d) {  // dynamics.hpp:34-44
+  std::memset(d, 0, sizeof(*d));
+  d->control_dt = 0.01;
+  d->substeps = 4;
+  d->control_mode = SG_CONTROL_POSITION;
+}
+
+int sg_env_create(const sg_env_config* cfg, const sg_dynamics_config* dyn, const char* const* robots,
+                  int32_t n_robots, int32_t device, sg_env** out) {
+  return guard([&] {
+    if (!cfg || !out) throw sg::ConfigError("sg_env_create: null argument");
+    std::vector<sg::RobotModel> models;
+    for (int i = 0; i < n_robots; ++i) models.push_back(sg::resolve_robot(robots[i]));
+    *out = make_env(*cfg, dyn, std::move(models), device).release();
+  });
+}
+
+int sg_env_create_from_text(const sg_env_config* cfg, const sg_dynamics_config* dyn, const char* const* texts,
+                            const char* const* origins, int32_t n_robots, int32_t device, sg_env** out) {
+  return guard([&] {
+    if (!cfg || !out) throw sg::ConfigError("sg_env_create_from_text: null argument");
+    std::vector<sg::RobotModel> models;
+    for (int i = 0; i < n_robots; ++i)
+      models.push_back(sg::parse_robot(texts[i], origins && origins[i] ? origins[i] : "inline"));
+    *out = make_env(*cfg, dyn, std::move(models), device).release();
+  });
+}
+
+void sg_env_destroy(sg_env* env) { delete env; }
+
+int sg_env_set_stream(sg_env* env, void* stream) {
+  return guard([&] { env->stream = static_cast<cudaStream_t>(stream); });
+}
+
+int sg_env_dims(const sg_env* env, int64_t* n, int32_t* obs_dim, int32_t* action_dim) {
+  return guard([&] {
+    if (n) *n = env->n;
+    if (obs_dim) *obs_dim = env->O;
+    if (action_dim) *action_dim = env->A;
+  });
+}
+
+int32_t sg_env_layout_count(const sg_env* env) { return static_cast<int32_t>(env->layout.size()); }
+
+int sg_env_layout_field(const sg_env* env, int32_t index, const char** name, int32_t* offset, int32_t* length) {
+  return guard([&] {
+    if (index < 0 || index >= static_cast<int32_t>(env->layout.size()))
+      throw sg::ConfigError("layout field index out of range");
+    const auto& f = env->layout[index];
+    if (name) *name = f.first.c_str();
+    if (offset) *offset = f.second.first;
+    if (length) *length = f.second.second;
+  });
+}
+
+int sg_env_workspace(const sg_env* env, double* center3, double* radius) {
+  return guard([&] {
+    for (int k = 0; k < 3; ++k) center3[k] = env->center[k];
+    *radius = env->radius;
+  });
+}
+
+int sg_env_reset(sg_env* env, sg_step_views* out) {
+  return guard([&] {
+    CK(cudaSetDevice(env->device));
+    env->launch_reset();
+    env->views(out);
+  });
+}
+
+int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
+  return guard([&] {
+    if (!d_actions) throw sg::SimError("env.step: action shape mismatch");
+    CK(cudaSetDevice(env->device));
+    env->P.actions = d_actions;
+    env->P.actions_aligned = (reinterpret_cast<uintptr_t>(d_actions) & 15u) == 0;
+    env->launch_step(1, false);
+    env->views(out);
+  });
+}
+
+int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
+  return guard([&] {
+    if (!h_actions) throw sg::SimError("env.step: action shape mismatch");
+    CK(cudaSetDevice(env->device));
+    const int64_t n = env->n;
+    const int O = env->O;
+    auto& s = env->stream;
+    CK(cudaMemcpyAsync(env->d_actions_in, h_actions, n * env->A * sizeof(float), cudaMemcpyHostToDevice, s));
+    env->P.actions = env->d_actions_in;
+    env->P.actions_aligned = 1;
+    env->launch_step(1, false);
+    unsigned long long sat = 0;
+    if (out) {
+      const auto& p = env->P.p;
+      if (out->observations)
+        CK(cudaMemcpyAsync(out->observations, p.obs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
+      if (out->terminal_observations)
+        CK(cudaMemcpyAsync(out->terminal_observations, p.tobs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
+      if (out->rewards) CK(cudaMemcpyAsync(out->rewards, p.rewards, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+      if (out->task_error)
+        CK(cudaMemcpyAsync(out->task_error, p.task_error, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+      if (out->terminated) CK(cudaMemcpyAsync(out->terminated, p.terminated, n, cudaMemcpyDeviceToHost, s));
+      if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, p.timed_out, n, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&sat, p.sat_total, sizeof(sat), cudaMemcpyDeviceToHost, s));
+    }
+    env->check();
+    if (out) {
+      out->action_saturations = static_cast<int64_t>(sat - env->last_sat);
+      env->last_sat = sat;
+    }
+  });
+}
+
+int sg_env_task_error(const sg_env* env, float** d) {
+  return guard([&] { *d = env->P.p.task_error; });
+}
+
+int sg_env_state(const sg_env* env, sg_state_views* o) {
+  return guard([&] {
+    const auto& p = env->P.p;
+    o->q = p.q;
+    o->qdot = p.qd;
+    o->q_target = p.qt;
+    o->goals = p.goals;
+    o->tips = p.tips;
+    o->step_count = p.step_count;
+    o->hold_count = p.hold_count;
+    o->episode_count = p.episode_count;
+    o->waypoint_idx = p.wp_idx;
+    o->waypoint_len = p.wp_len;
+    o->waypoints = p.wps;
+    o->rng_state = p.rng_state;
+    o->rng_inc = p.rng_inc;
+    o->waypoint_cap = env->P.task.wp_cap;
+    o->dof = env->A;
+    o->n_envs = env->n;
+  });
+}
+
+int sg_env_synchronize(sg_env* env) {
+  return guard([&] {
+    CK(cudaSetDevice(env->device));
+    env->check();
+  });
+}
+
+int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t global_n) {
+  return guard([&] {
+    CK(cudaSetDevice(env->device));
+    if (global_n < env->n + env->cfg.row_offset) throw sg::ConfigError("bench: global_n_envs smaller than this shard");
+    auto& p = env->P.p;
+    if (!p.act_state) {
+      p.act_state = dalloc<uint64_t>(env->n);
+      p.act_buf = dalloc<float>(env->n * env->A);
+    }
+    const HostPcg r = make_stream(seed, 0xac7104);  // bench.cpp:115
+    sg::JumpTable J;
+    for (int b = 0; b < 64; ++b) pcg_jump(1ULL << b, r.inc, J.mult[b], J.add[b]);
+    const uint64_t A = static_cast<uint64_t>(env->A);
+    const uint64_t first_draw = static_cast<uint64_t>(first_step) * static_cast<uint64_t>(global_n) * A;
+    const int b = 128;
+    const unsigned grid = static_cast<unsigned>((env->n + b - 1) / b);
+    sg::bench_seed_kernel<<<grid, b, 0, env->stream>>>(p.act_state, env->n, r.state, first_draw,
+                                                       env->cfg.row_offset, env->A, J);
+    CK(cudaGetLastError());
+    env->P.bench.inc = r.inc;
+    pcg_jump(static_cast<uint64_t>(global_n - 1) * A, r.inc, env->P.bench.jump_mult, env->P.bench.jump_add);
+    env->bench_ready = true;
+  });
+}
+
+int sg_env_bench_step(sg_env* env, int32_t k_steps) {
+  return guard([&] {
+    if (!env->bench_ready) throw sg::ConfigError("sg_env_bench_step before sg_env_bench_begin");
+    if (k_steps < 1) throw sg::ConfigError("bench: k_steps must be >= 1");
+    CK(cudaSetDevice(env->device));
+    env->launch_step(k_steps, true);
+  });
+}
+
+int sg_env_bench_actions(const sg_env* env, float** d_actions) {
+  return guard([&] {
+    if (!env->P.p.act_buf) throw sg::ConfigError("sg_env_bench_actions before sg_env_bench_begin");
+    *d_actions = env->P.p.act_buf;
+  });
+}
+
+// ---- robot utilities ----------------------------------------------------------
+int sg_robot_parse(const char* text, const char* origin, sg_robot** out) {
+  return guard([&] {
+    auto r = std::make_unique<sg_robot>();
+    r->model = sg::parse_robot(text, origin ? origin : "inline");
+    std::vector<double> ones(r->model.dof_count, 1.0);
+    r->table = build_table(r->model, 0.0025, ones, ones, ones, ones);
+    *out = r.release();
+  });
+}
+
+int sg_robot_resolve(const char* name_or_path, sg_robot** out) {
+  return guard([&] {
+    auto r = std::make_unique<sg_robot>();
+    r->model = sg::resolve_robot(name_or_path);
+    std::vector<double> ones(r->model.dof_count, 1.0);
+    r->table = build_table(r->model, 0.0025, ones, ones, ones, ones);
+    *out = r.release();
+  });
+}
+
+void sg_robot_destroy(sg_robot* r) { delete r; }
+
+int sg_robot_dof(const sg_robot* r, int32_t* dof, int32_t* jaw) {
+  return guard([&] {
+    if (dof) *dof = r->model.dof_count;
+    if (jaw) *jaw = r->model.jaw_dof();
+  });
+}
+
+int sg_robot_fk(const sg_robot* r, const float* d_q, int64_t n, float* d_pos, void* stream) {
+  return guard([&] {
+    if (n <= 0) return;
+    int32_t* d_err = nullptr;
+    CK(cudaMalloc(&d_err, sizeof(int32_t)));
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
+    const int b = 128;
+    const unsigned grid = static_cast<unsigned>((n + b - 1) / b);
+    if (r->model.dof_count <= 8)
+      sg::fk_batch_kernel<8><<<grid, b, 0, static_cast<cudaStream_t>(stream)>>>(r->table, d_q, n, d_pos, d_err);
+    else
+      sg::fk_batch_kernel<16><<<grid, b, 0, static_cast<cudaStream_t>(stream)>>>(r->table, d_q, n, d_pos, d_err);
+    cudaError_t le = cudaGetLastError();
+    int32_t err = 0;
+    cudaError_t ce = cudaMemcpyAsync(&err, d_err, sizeof(err), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    cudaFree(d_err);
+    CK(le);
+    CK(ce);
+    if (err) throw sg::SimError("forward_kinematics: joint value outside limits");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,389 @@
+"""Python plumbing over the C-ABI of include/sg_env.h (ctypes).
+
+The product is the CUDA library ``lib/libsg_env.so`` (host C++ + sm_100a
+kernels). This module only binds it for tests, the smoke check and bench.py:
+device buffers owned by an env handle are exposed as zero-copy torch views via
+``__cuda_array_interface__``. There is no fallback: if the library is missing
+the import of :func:`lib` raises.
+
+Names follow the reference's BatchedEnv / VecTaskEnv surface
+(proj/include/scalpel/envs.hpp:107-179): ``n_envs``, ``obs_dim``,
+``action_dim``, ``reset()``, ``step(actions)``, ``task_error()``, ``layout()``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _build
+
+SG_OK, SG_ERR_SIM, SG_ERR_CONFIG = 0, 1, 2
+TASKS = {"target_reaching": 0, "active_tracking": 1, "image_matching": 2, "path_following": 3,
+         "multi_tool_reaching": 4}
+CONTROL_MODES = {"position": 0, "velocity": 1, "torque": 2}
+
+
+class ConfigError(RuntimeError):
+    """scalpel::ConfigError / ParseError (exit code 2)."""
+
+
+class SimError(RuntimeError):
+    """scalpel::SimError (exit code 1)."""
+
+
+class EnvConfig(C.Structure):  # sg_env_config
+    _fields_ = [
+        ("task", C.c_int32), ("episode_len", C.c_int32), ("n_envs", C.c_int64),
+        ("goal_sigma", C.c_double), ("goal_offset_clip", C.c_double), ("reward_scale", C.c_double),
+        ("path_penalty", C.c_double), ("success_radius", C.c_double), ("success_hold", C.c_int32),
+        ("reserved0", C.c_int32), ("workspace_radius", C.c_double), ("waypoint_spacing", C.c_double),
+        ("tracking_vel_noise_std", C.c_double), ("tracking_vel_clamp", C.c_double),
+        ("collision_threshold", C.c_double), ("collision_penalty", C.c_double),
+        ("view_penalty", C.c_double), ("seed", C.c_uint64), ("row_offset", C.c_int64),
+    ]
+
+
+class DynConfig(C.Structure):  # sg_dynamics_config
+    _fields_ = [
+        ("control_dt", C.c_double), ("substeps", C.c_int32), ("control_mode", C.c_int32),
+        ("kp", C.POINTER(C.c_double)), ("n_kp", C.c_int32), ("n_kd", C.c_int32),
+        ("kd", C.POINTER(C.c_double)), ("inertia", C.POINTER(C.c_double)), ("n_inertia", C.c_int32),
+        ("n_damping", C.c_int32), ("damping", C.POINTER(C.c_double)),
+    ]
+
+
+class StepViews(C.Structure):  # sg_step_views
+    _fields_ = [
+        ("observations", C.c_void_p), ("terminal_observations", C.c_void_p), ("rewards", C.c_void_p),
+        ("task_error", C.c_void_p), ("terminated", C.c_void_p), ("timed_out", C.c_void_p),
+        ("action_saturations_total", C.c_void_p), ("n_envs", C.c_int64), ("obs_dim", C.c_int32),
+        ("action_dim", C.c_int32),
+    ]
+
+
+class HostResult(C.Structure):  # sg_host_result
+    _fields_ = [
+        ("observations", C.c_void_p), ("terminal_observations", C.c_void_p), ("rewards", C.c_void_p),
+        ("task_error", C.c_void_p), ("terminated", C.c_void_p), ("timed_out", C.c_void_p),
+        ("action_saturations", C.c_int64),
+    ]
+
+
+class StateViews(C.Structure):  # sg_state_views
+    _fields_ = [
+        ("q", C.c_void_p), ("qdot", C.c_void_p), ("q_target", C.c_void_p), ("goals", C.c_void_p),
+        ("tips", C.c_void_p), ("step_count", C.c_void_p), ("hold_count", C.c_void_p),
+        ("episode_count", C.c_void_p), ("waypoint_idx", C.c_void_p), ("waypoint_len", C.c_void_p),
+        ("waypoints", C.c_void_p), ("rng_state", C.c_void_p), ("rng_inc", C.c_void_p),
+        ("waypoint_cap", C.c_int32), ("dof", C.c_int32), ("n_envs", C.c_int64),
+    ]
+
+
+_P = C.POINTER
+_SIGS = {
+    "sg_last_error": (C.c_char_p, []),
+    "sg_version": (C.c_char_p, []),
+    "sg_env_config_init": (None, [_P(EnvConfig)]),
+    "sg_dynamics_config_init": (None, [_P(DynConfig)]),
+    "sg_env_create": (C.c_int, [_P(EnvConfig), _P(DynConfig), _P(C.c_char_p), C.c_int32, C.c_int32,
+                                _P(C.c_void_p)]),
+    "sg_env_create_from_text": (C.c_int, [_P(EnvConfig), _P(DynConfig), _P(C.c_char_p), _P(C.c_char_p),
+                                          C.c_int32, C.c_int32, _P(C.c_void_p)]),
+    "sg_env_destroy": (None, [C.c_void_p]),
+    "sg_env_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sg_env_dims": (C.c_int, [C.c_void_p, _P(C.c_int64), _P(C.c_int32), _P(C.c_int32)]),
+    "sg_env_layout_count": (C.c_int32, [C.c_void_p]),
+    "sg_env_layout_field": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_char_p), _P(C.c_int32), _P(C.c_int32)]),
+    "sg_env_workspace": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double)]),
+    "sg_env_reset": (C.c_int, [C.c_void_p, _P(StepViews)]),
+    "sg_env_step": (C.c_int, [C.c_void_p, C.c_void_p, _P(StepViews)]),
+    "sg_env_step_host": (C.c_int, [C.c_void_p, C.c_void_p, _P(HostResult)]),
+    "sg_env_task_error": (C.c_int, [C.c_void_p, _P(C.c_void_p)]),
+    "sg_env_state": (C.c_int, [C.c_void_p, _P(StateViews)]),
+    "sg_env_synchronize": (C.c_int, [C.c_void_p]),
+    "sg_env_bench_begin": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64]),
+    "sg_env_bench_step": (C.c_int, [C.c_void_p, C.c_int32]),
+    "sg_env_bench_actions": (C.c_int, [C.c_void_p, _P(C.c_void_p)]),
+    "sg_robot_parse": (C.c_int, [C.c_char_p, C.c_char_p, _P(C.c_void_p)]),
+    "sg_robot_resolve": (C.c_int, [C.c_char_p, _P(C.c_void_p)]),
+    "sg_robot_destroy": (None, [C.c_void_p]),
+    "sg_robot_dof": (C.c_int, [C.c_void_p, _P(C.c_int32), _P(C.c_int32)]),
+    "sg_robot_fk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+}
+
+_LIB: C.CDLL | None = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib() -> C.CDLL:
+    """Load libsg_env.so (building it first when the sources are newer).
+    Raises if it cannot be built or loaded — there is no fallback path."""
+    global _LIB
+    if _LIB is None:
+        path = _build.LIB
+        if not os.path.exists(path) or os.environ.get("SG_REBUILD"):
+            _build.build()
+        L = C.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def header_symbols() -> list[str]:
+    """Every function declared in include/sg_env.h."""
+    with open(os.path.join(_build.INCLUDE, "sg_env.h")) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sg_[a-z0-9_]+)\s*\(", text)))
+
+
+def _check(rc: int) -> None:
+    if rc == SG_OK:
+        return
+    msg = lib().sg_last_error().decode()
+    if rc == SG_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise SimError(msg)
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ carrier for a raw device pointer."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, shape: tuple, dtype: str, device: int = 0):
+    """Zero-copy torch view of env-owned device memory (valid while the env lives)."""
+    import torch
+    typestr = {"f32": "<f4", "u8": "|u1", "i32": "<i4", "i64": "<i8", "u64": "<u8"}[dtype]
+    if ptr is None or ptr == 0:
+        return None
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=f"cuda:{device}")
+
+
+# ----------------------------------------------------------------------------- robot
+
+class Robot:
+    """Parsed descriptor (parse_robot / resolve_robot, robot_model.cpp:191-349)."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+        dof, jaw = C.c_int32(), C.c_int32()
+        _check(lib().sg_robot_dof(self._h, C.byref(dof), C.byref(jaw)))
+        self.dof, self.jaw_dof = dof.value, jaw.value
+
+    @classmethod
+    def parse(cls, text: str, origin: str = "inline") -> "Robot":
+        h = C.c_void_p()
+        _check(lib().sg_robot_parse(text.encode(), origin.encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def resolve(cls, name_or_path: str) -> "Robot":
+        h = C.c_void_p()
+        _check(lib().sg_robot_resolve(name_or_path.encode(), C.byref(h)))
+        return cls(h.value)
+
+    def fk(self, q):
+        """Batched device FK: q (n x dof, cuda fp32) -> tip positions (n x 3)."""
+        import torch
+        q = q.contiguous().to(torch.float32)
+        out = torch.empty((q.shape[0], 3), device=q.device, dtype=torch.float32)
+        stream = torch.cuda.current_stream(q.device).cuda_stream
+        _check(lib().sg_robot_fk(self._h, q.data_ptr(), q.shape[0], out.data_ptr(), stream))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.sg_robot_destroy(self._h)
+            self._h = None
+
+
+# ----------------------------------------------------------------------------- env
+
+@dataclass
+class StepResult:
+    """scalpel::StepResult (envs.hpp:82-89) as device views."""
+    observations: object
+    rewards: object
+    terminated: object
+    timed_out: object
+    terminal_observations: object
+    task_error: object
+    saturations_total: object
+
+
+def env_config(**kw) -> EnvConfig:
+    c = EnvConfig()
+    lib().sg_env_config_init(C.byref(c))
+    for k, v in kw.items():
+        if k == "task" and isinstance(v, str):
+            v = TASKS[v]
+        setattr(c, k, v)
+    return c
+
+
+def dyn_config(control_dt=0.01, substeps=4, control_mode="position", kp=(), kd=(), inertia=(),
+               damping=()) -> tuple[DynConfig, list]:
+    d = DynConfig()
+    lib().sg_dynamics_config_init(C.byref(d))
+    d.control_dt, d.substeps = control_dt, substeps
+    d.control_mode = CONTROL_MODES[control_mode] if isinstance(control_mode, str) else control_mode
+    keep = []
+    for name in ("kp", "kd", "inertia", "damping"):
+        vals = list(locals()[name])
+        arr = (C.c_double * max(len(vals), 1))(*vals)
+        keep.append(arr)
+        setattr(d, name, C.cast(arr, C.POINTER(C.c_double)))
+        setattr(d, "n_" + name, len(vals))
+    return d, keep
+
+
+class VecTaskEnv:
+    """Device-resident VecTaskEnv behind the C-ABI (envs.hpp:123-179)."""
+
+    def __init__(self, robots=("psm",), device: int = 0, dynamics: dict | None = None,
+                 robot_texts: list[str] | None = None, **cfg):
+        self.device = device
+        self.cfg = env_config(**cfg)
+        dyn, self._keep = dyn_config(**(dynamics or {}))
+        h = C.c_void_p()
+        if robot_texts is not None:
+            arr = (C.c_char_p * len(robot_texts))(*[t.encode() for t in robot_texts])
+            org = (C.c_char_p * len(robot_texts))(*[f"inline{i}".encode() for i in range(len(robot_texts))])
+            _check(lib().sg_env_create_from_text(C.byref(self.cfg), C.byref(dyn), arr, org, len(robot_texts),
+                                                 device, C.byref(h)))
+        else:
+            arr = (C.c_char_p * len(robots))(*[r.encode() for r in robots])
+            _check(lib().sg_env_create(C.byref(self.cfg), C.byref(dyn), arr, len(robots), device, C.byref(h)))
+        self._h = h.value
+        n, o, a = C.c_int64(), C.c_int32(), C.c_int32()
+        _check(lib().sg_env_dims(self._h, C.byref(n), C.byref(o), C.byref(a)))
+        self.n_envs, self.obs_dim, self.action_dim = n.value, o.value, a.value
+        self._views = StepViews()
+        self._stream = None
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.sg_env_destroy(self._h)
+            self._h = None
+
+    # -- plumbing ------------------------------------------------------------
+    def set_stream(self, stream) -> None:
+        """Bind a torch.cuda.Stream (or None for the legacy default stream)."""
+        self._stream = stream
+        _check(lib().sg_env_set_stream(self._h, None if stream is None else stream.cuda_stream))
+
+    def layout(self) -> list[tuple[str, int, int]]:
+        out = []
+        for i in range(lib().sg_env_layout_count(self._h)):
+            name, off, ln = C.c_char_p(), C.c_int32(), C.c_int32()
+            _check(lib().sg_env_layout_field(self._h, i, C.byref(name), C.byref(off), C.byref(ln)))
+            out.append((name.value.decode(), off.value, ln.value))
+        return out
+
+    def workspace(self):
+        c = (C.c_double * 3)()
+        r = C.c_double()
+        _check(lib().sg_env_workspace(self._h, c, C.byref(r)))
+        return np.array(list(c)), r.value
+
+    def _result(self) -> StepResult:
+        v, n, o, d = self._views, self.n_envs, self.obs_dim, self.device
+        return StepResult(
+            observations=device_view(v.observations, (n, o), "f32", d),
+            rewards=device_view(v.rewards, (n,), "f32", d),
+            terminated=device_view(v.terminated, (n,), "u8", d),
+            timed_out=device_view(v.timed_out, (n,), "u8", d),
+            terminal_observations=device_view(v.terminal_observations, (n, o), "f32", d),
+            task_error=device_view(v.task_error, (n,), "f32", d),
+            saturations_total=device_view(v.action_saturations_total, (1,), "u64", d),
+        )
+
+    # -- BatchedEnv surface -----------------------------------------------------
+    def reset(self):
+        _check(lib().sg_env_reset(self._h, C.byref(self._views)))
+        return self._result().observations
+
+    def step(self, actions) -> StepResult:
+        """actions: cuda fp32 tensor (n_envs x action_dim), row-major."""
+        if tuple(actions.shape) != (self.n_envs, self.action_dim):
+            raise SimError("env.step: action shape mismatch")
+        if not actions.is_contiguous() or str(actions.dtype) != "torch.float32":
+            raise SimError("env.step: actions must be contiguous float32")
+        _check(lib().sg_env_step(self._h, actions.data_ptr(), C.byref(self._views)))
+        return self._result()
+
+    def step_host(self, actions: np.ndarray, out: dict | None = None) -> dict:
+        """Host actions in, host StepResult out (synchronous; e2e path)."""
+        a = np.ascontiguousarray(actions, dtype=np.float32)
+        if a.shape != (self.n_envs, self.action_dim):
+            raise SimError("env.step: action shape mismatch")
+        n, o = self.n_envs, self.obs_dim
+        if out is None:
+            out = dict(observations=np.empty((n, o), np.float32),
+                       terminal_observations=np.empty((n, o), np.float32),
+                       rewards=np.empty(n, np.float32), task_error=np.empty(n, np.float32),
+                       terminated=np.empty(n, np.uint8), timed_out=np.empty(n, np.uint8))
+        hr = HostResult()
+        for k in ("observations", "terminal_observations", "rewards", "task_error", "terminated", "timed_out"):
+            arr = out.get(k)
+            setattr(hr, k, None if arr is None else arr.ctypes.data)
+        _check(lib().sg_env_step_host(self._h, a.ctypes.data, C.byref(hr)))
+        out["action_saturations"] = hr.action_saturations
+        return out
+
+    def step_host_ptr(self, actions_ptr: int, hr: HostResult) -> None:
+        """Raw-pointer variant (pinned buffers) used by bench.py's e2e leg."""
+        _check(lib().sg_env_step_host(self._h, actions_ptr, C.byref(hr)))
+
+    def task_error(self):
+        p = C.c_void_p()
+        _check(lib().sg_env_task_error(self._h, C.byref(p)))
+        return device_view(p.value, (self.n_envs,), "f32", self.device)
+
+    def synchronize(self) -> None:
+        _check(lib().sg_env_synchronize(self._h))
+
+    def state(self) -> dict:
+        s = StateViews()
+        _check(lib().sg_env_state(self._h, C.byref(s)))
+        n, A, d = self.n_envs, self.action_dim, self.device
+        cap = s.waypoint_cap
+        return dict(
+            q=device_view(s.q, (A, n), "f32", d), qdot=device_view(s.qdot, (A, n), "f32", d),
+            q_target=device_view(s.q_target, (A, n), "f32", d), goals=device_view(s.goals, (3, n), "f32", d),
+            tips=device_view(s.tips, (3, n), "f32", d), step_count=device_view(s.step_count, (n,), "i32", d),
+            hold_count=device_view(s.hold_count, (n,), "i32", d),
+            episode_count=device_view(s.episode_count, (n,), "i64", d),
+            waypoint_idx=device_view(s.waypoint_idx, (n,), "i32", d),
+            waypoint_len=device_view(s.waypoint_len, (n,), "i32", d),
+            waypoints=device_view(s.waypoints, (n, cap, 3), "f32", d) if cap else None,
+            rng_state=device_view(s.rng_state, (n,), "u64", d), rng_inc=device_view(s.rng_inc, (n,), "u64", d),
+            waypoint_cap=cap,
+        )
+
+    # -- bench workload (bench.cpp:31-35,97-135) --------------------------------
+    def bench_begin(self, seed: int, first_step: int = 0, global_n_envs: int | None = None) -> None:
+        g = self.n_envs + self.cfg.row_offset if global_n_envs is None else global_n_envs
+        _check(lib().sg_env_bench_begin(self._h, seed, first_step, g))
+
+    def bench_step(self, k_steps: int = 1) -> None:
+        _check(lib().sg_env_bench_step(self._h, k_steps))
+
+    def bench_actions(self):
+        p = C.c_void_p()
+        _check(lib().sg_env_bench_actions(self._h, C.byref(p)))
+        return device_view(p.value, (self.n_envs, self.action_dim), "f32", self.device)

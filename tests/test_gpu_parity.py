@@ -1,0 +1,364 @@
+"""GPU parity: the sm_100a step behind the C-ABI vs the fp64 CPU oracle.
+
+Contract (north_star): reset masks, termination/timeout
+flags, step/hold/episode counters, waypoint indices and per-env RNG states are
+BIT-EXACT; joint state, tips, observations and rewards agree within the fp32
+tolerances below on every step of a fixed horizon. The tolerances are set from
+the intrinsic fp32-vs-fp64 drift the oracle measures on the same inputs
+(tests/test_oracle_env.py::test_fp32_drift_bounds).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL = dict(q=1e-5, qdot=1e-4, q_target=1e-5, tips=2e-5, goals=1e-6, obs_pos=2e-5, reward=2e-5)
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+
+
+def _soa(t):  # device SoA (dof x n) -> host (n x dof)
+    return t.detach().cpu().numpy().T.astype(np.float64)
+
+
+def _run_pair(sg, oracle, robot, task, n, steps, seed=0, sigma=0.05, check_every=1, actions_fn=None):
+    """Step the device env and the fp64 oracle with the same actions; compare."""
+    _cuda()
+    m = oracle.resolve_robot(robot)
+    ocfg = oracle.env_config(n_envs=n, seed=seed, task=task, goal_sigma=sigma)
+    ref = oracle.Env(ocfg, m)
+    ref.reset()
+    env = sg.VecTaskEnv(robots=(robot,), n_envs=n, seed=seed, task=task, goal_sigma=sigma)
+    obs = env.reset()
+    torch.cuda.synchronize()
+    A, O = env.action_dim, env.obs_dim
+    o_ref = ref.obs()[0]
+    _compare_obs(obs.cpu().numpy(), o_ref, A)
+    ar = oracle.make_stream(seed, 0xAC7104)
+    worst = {}
+    for s in range(steps):
+        a = actions_fn(s) if actions_fn else oracle.fill_uniform_actions(ar, n, A)
+        a32 = a.astype(np.float32)
+        res = env.step(torch.from_numpy(a32).cuda())
+        ref.step(a32.astype(np.float64))
+        if s % check_every and s != steps - 1:
+            continue
+        torch.cuda.synchronize()
+        r = ref.result()
+        # ---- bit-exact --------------------------------------------------------
+        np.testing.assert_array_equal(res.terminated.cpu().numpy(), r["terminated"], err_msg=f"terminated @{s}")
+        np.testing.assert_array_equal(res.timed_out.cpu().numpy(), r["timed_out"], err_msg=f"timed_out @{s}")
+        st = env.state()
+        c = ref.counters()
+        np.testing.assert_array_equal(st["step_count"].cpu().numpy(), c["step_count"], err_msg=f"step_count @{s}")
+        np.testing.assert_array_equal(st["hold_count"].cpu().numpy(), c["hold_count"], err_msg=f"hold @{s}")
+        np.testing.assert_array_equal(st["episode_count"].cpu().numpy(), c["episode_count"], err_msg=f"episodes @{s}")
+        if task == oracle.PATH_FOLLOWING:
+            np.testing.assert_array_equal(st["waypoint_idx"].cpu().numpy(), c["waypoint_idx"], err_msg=f"wp idx @{s}")
+            np.testing.assert_array_equal(st["waypoint_len"].cpu().numpy(), c["waypoint_len"], err_msg=f"wp len @{s}")
+        rs, ri = ref.rng()
+        np.testing.assert_array_equal(st["rng_state"].cpu().numpy(), rs, err_msg=f"rng @{s}")
+        np.testing.assert_array_equal(st["rng_inc"].cpu().numpy(), ri)
+        # ---- tolerance ---------------------------------------------------------
+        sr = ref.state()
+        for k in ("q", "qdot", "q_target"):
+            err = np.abs(_soa(st[k]) - sr[k]).max()
+            worst[k] = max(worst.get(k, 0.0), err)
+            assert err <= TOL[k], f"{robot} {k} err {err:.3e} @ step {s}"
+        for k in ("tips", "goals"):
+            err = np.abs(_soa(st[k]) - sr[k]).max()
+            worst[k] = max(worst.get(k, 0.0), err)
+            assert err <= TOL[k], f"{robot} {k} err {err:.3e} @ step {s}"
+        err = np.abs(res.rewards.cpu().numpy() - r["rewards"]).max()
+        worst["reward"] = max(worst.get("reward", 0.0), err)
+        assert err <= TOL["reward"]
+        err = np.abs(res.task_error.cpu().numpy() - r["task_error"]).max()
+        assert err <= TOL["reward"]
+        o_dev = res.observations.cpu().numpy()
+        o_ref, t_ref = ref.obs()
+        _compare_obs(o_dev, o_ref, A)
+        ended = (r["terminated"] | r["timed_out"]).astype(bool)
+        if ended.any():
+            _compare_obs(res.terminal_observations.cpu().numpy()[ended], t_ref[ended], A)
+    return env, ref, worst
+
+
+def _compare_obs(o_dev, o_ref, A):
+    # layout [q | qdot | tip | q_target | goal] (envs.cpp:166-192)
+    tol = np.concatenate([np.full(A, TOL["q"]), np.full(A, TOL["qdot"]), np.full(3, TOL["obs_pos"]),
+                          np.full(A, TOL["q_target"]), np.full(3, TOL["obs_pos"])])
+    err = np.abs(o_dev.astype(np.float64) - o_ref)
+    bad = err > tol
+    assert not bad.any(), f"obs mismatch at {np.argwhere(bad)[:5]} max err {err.max():.3e}"
+
+
+def test_config1_psm_reach_1000_steps(sg, oracle):
+    """BASELINE config 1: PSM reach, 64 envs, 1000 steps (+ warm-up), seed 0,
+    random actions from make_stream(0, 0xac7104) — three synchronized reset
+    bursts at steps 300/600/900."""
+    env, ref, worst = _run_pair(sg, oracle, "psm", oracle.TARGET_REACHING, 64, 1001)
+    c = ref.counters()
+    assert (c["episode_count"] == 3).all()
+    assert ref.goal_draws() == 264  # 256 resets + 8 rejections (survey probe, Appendix E)
+
+
+def test_ecm_reach(sg, oracle):
+    _run_pair(sg, oracle, "ecm", oracle.TARGET_REACHING, 96, 650, seed=3)
+
+
+def test_star_path_following(sg, oracle):
+    env, ref, worst = _run_pair(sg, oracle, "star", oracle.PATH_FOLLOWING, 48, 620, seed=1, sigma=0.15)
+    # waypoint tables: fp64 arithmetic on both sides, rounded to fp32 on the device
+    st = env.state()
+    wl = st["waypoint_len"].cpu().numpy()
+    wps = st["waypoints"].cpu().numpy()
+    for row in range(env.n_envs):
+        ref_w = ref.waypoints(row)
+        assert len(ref_w) == wl[row]
+        np.testing.assert_array_equal(wps[row, : wl[row]], ref_w.astype(np.float32))
+
+
+def test_path_following_waypoint_advance(sg, oracle):
+    """Drive the tip onto its path with a large success radius so waypoint
+    indices advance and episodes terminate by goal; indices stay bit-exact."""
+    _cuda()
+    m = oracle.resolve_robot("star")
+    n = 32
+    kw = dict(n_envs=n, seed=5, task=oracle.PATH_FOLLOWING, goal_sigma=0.15, success_radius=0.25)
+    ref = oracle.Env(oracle.env_config(**kw), m)
+    ref.reset()
+    env = sg.VecTaskEnv(robots=("star",), **kw)
+    env.reset()
+    ar = oracle.make_stream(5, 0xAC7104)
+    advanced = 0
+    for s in range(400):
+        a = (0.05 * oracle.fill_uniform_actions(ar, n, m.dof)).astype(np.float32)
+        res = env.step(torch.from_numpy(a).cuda())
+        ref.step(a.astype(np.float64))
+        c = ref.counters()
+        st = env.state()
+        np.testing.assert_array_equal(st["waypoint_idx"].cpu().numpy(), c["waypoint_idx"], err_msg=f"@{s}")
+        np.testing.assert_array_equal(res.terminated.cpu().numpy(), ref.result()["terminated"], err_msg=f"@{s}")
+        advanced += int((c["waypoint_idx"] > 0).sum())
+    assert advanced > 0
+
+
+def test_target_reaching_terminations(sg, oracle):
+    """Large success radius: hold counters run up to success_hold and episodes
+    terminate by goal; terminated flags, holds and resets stay bit-exact."""
+    _cuda()
+    m = oracle.resolve_robot("psm")
+    n = 64
+    kw = dict(n_envs=n, seed=9, success_radius=0.06, success_hold=3)
+    ref = oracle.Env(oracle.env_config(**kw), m)
+    ref.reset()
+    env = sg.VecTaskEnv(robots=("psm",), **kw)
+    env.reset()
+    zeros = np.zeros((n, m.dof), np.float32)
+    terms = 0
+    for s in range(200):
+        res = env.step(torch.from_numpy(zeros).cuda())
+        ref.step(zeros.astype(np.float64))
+        r = ref.result()
+        np.testing.assert_array_equal(res.terminated.cpu().numpy(), r["terminated"], err_msg=f"@{s}")
+        np.testing.assert_array_equal(env.state()["hold_count"].cpu().numpy(), ref.counters()["hold_count"])
+        np.testing.assert_array_equal(env.state()["rng_state"].cpu().numpy(), ref.rng()[0])
+        terms += int(r["terminated"].sum())
+    assert terms > 0
+
+
+def test_bench_action_stream_bit_exact(sg, oracle):
+    """Device jump-ahead generator == the reference's serial fill
+    (bench.cpp:31-35) rounded to fp32, across steps and with sharding."""
+    _cuda()
+    n, A = 300, 7
+    ar = oracle.make_stream(11, 0xAC7104)
+    expected = [oracle.fill_uniform_actions(ar, n, A).astype(np.float32) for _ in range(4)]
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=11)
+    env.reset()
+    env.bench_begin(11, first_step=0)
+    for s in range(4):
+        env.bench_step(1)
+        np.testing.assert_array_equal(env.bench_actions().cpu().numpy(), expected[s])
+    # shard: rows [100, 300) of the same global stream, starting at step 2
+    shard = sg.VecTaskEnv(robots=("psm",), n_envs=200, seed=11, row_offset=100)
+    shard.reset()
+    shard.bench_begin(11, first_step=2, global_n_envs=n)
+    shard.bench_step(1)
+    np.testing.assert_array_equal(shard.bench_actions().cpu().numpy(), expected[2][100:])
+
+
+def test_fused_k_steps_equal_single_steps(sg, oracle):
+    _cuda()
+    n = 1000
+    a = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=2, episode_len=7)
+    b = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=2, episode_len=7)
+    a.reset(); b.reset()
+    a.bench_begin(2); b.bench_begin(2)
+    for _ in range(20):
+        a.bench_step(1)
+    b.bench_step(20)
+    torch.cuda.synchronize()
+    sa, sb = a.state(), b.state()
+    for k in ("q", "qdot", "q_target", "goals", "tips", "step_count", "episode_count", "rng_state"):
+        assert torch.equal(sa[k], sb[k]), k
+    ra, rb = a._result(), b._result()
+    assert torch.equal(ra.observations, rb.observations)
+    assert torch.equal(ra.terminal_observations, rb.terminal_observations)
+
+
+def test_sharded_rows_match_single_device(sg, oracle):
+    """Rank r of a sharded job (row_offset) is bit-identical to rows of one env."""
+    _cuda()
+    full = sg.VecTaskEnv(robots=("psm",), n_envs=256, seed=4)
+    part = sg.VecTaskEnv(robots=("psm",), n_envs=128, seed=4, row_offset=128)
+    full.reset(); part.reset()
+    full.bench_begin(4); part.bench_begin(4, global_n_envs=256)
+    full.bench_step(350); part.bench_step(350)
+    torch.cuda.synchronize()
+    assert torch.equal(full._result().observations[128:], part._result().observations)
+    assert torch.equal(full.state()["rng_state"][128:], part.state()["rng_state"])
+
+
+def test_host_step_matches_device_step(sg, oracle):
+    _cuda()
+    n = 200
+    a = sg.VecTaskEnv(robots=("ecm",), n_envs=n, seed=8)
+    b = sg.VecTaskEnv(robots=("ecm",), n_envs=n, seed=8)
+    a.reset(); b.reset()
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        act = rng.uniform(-1.5, 1.5, size=(n, 6)).astype(np.float32)
+        hr = a.step_host(act)
+        dr = b.step(torch.from_numpy(act).cuda())
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(hr["observations"], dr.observations.cpu().numpy())
+        np.testing.assert_array_equal(hr["rewards"], dr.rewards.cpu().numpy())
+        assert hr["action_saturations"] == int(((act < -1) | (act > 1)).sum())
+
+
+def test_nonfinite_action_is_sim_error(sg, oracle):
+    _cuda()
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=8)
+    env.reset()
+    act = np.zeros((8, 7), np.float32)
+    act[3, 2] = np.nan
+    with pytest.raises(sg.SimError, match="non-finite action"):
+        env.step_host(act)
+    with pytest.raises(sg.SimError, match="shape"):
+        env.step_host(np.zeros((8, 6), np.float32))
+
+
+@pytest.mark.parametrize("mode", ["position", "velocity", "torque"])
+def test_control_modes_limits_and_parity(sg, oracle, mode):
+    """Adversarial actions in [-2, 2] (test_dynamics.cpp:134-163): limits and
+    velocity bounds hold; state matches the oracle in every control mode."""
+    _cuda()
+    m = oracle.resolve_robot("psm")
+    n = 64
+    dyn = oracle.default_dynamics(m)
+    dyn.control_mode = {"position": 0, "velocity": 1, "torque": 2}[mode]
+    ref = oracle.Env(oracle.env_config(n_envs=n, seed=99), m, dyn)
+    ref.reset()
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=99, dynamics=dict(control_mode=mode))
+    env.reset()
+    rng = oracle.make_stream(42, 0)
+    lo = np.array([m.dof_joint(d).limit_lo for d in range(m.dof)])
+    hi = np.array([m.dof_joint(d).limit_hi for d in range(m.dof)])
+    vl = np.array([m.dof_joint(d).velocity_limit for d in range(m.dof)])
+    sat_total = 0
+    for s in range(250):
+        a = (2.0 * oracle.fill_uniform_actions(rng, n, m.dof)).astype(np.float32)
+        hr = env.step_host(a)
+        ref.step(a.astype(np.float64))
+        sat_total += hr["action_saturations"]
+        assert hr["action_saturations"] == ref.result()["saturations"]
+        st = env.state()
+        q, qd = _soa(st["q"]), _soa(st["qdot"])
+        assert (q >= lo).all() and (q <= hi).all()
+        assert (np.abs(qd) <= vl).all()
+        sr = ref.state()
+        assert np.abs(q - sr["q"]).max() <= TOL["q"] * 10
+    assert sat_total > 0
+
+
+def test_fk_batch_matches_matrix_oracle(sg, oracle):
+    """FK vs the 4x4 homogeneous-matrix oracle (test_robot_model.cpp:139-151):
+    1000 random in-limit q per robot; fp32 device vs fp64 oracle."""
+    _cuda()
+    rng = oracle.make_stream(2024, 11)
+    for name in ("psm", "ecm", "star"):
+        m = oracle.resolve_robot(name)
+        qs = np.array([[oracle.uniform(rng, m.dof_joint(d).limit_lo, m.dof_joint(d).limit_hi)
+                        for d in range(m.dof)] for _ in range(1000)])
+        ref = np.array([oracle.fk_matrix(m, q)[:3, 3] for q in qs])
+        rob = sg.Robot.resolve(name)
+        pos = rob.fk(torch.from_numpy(qs.astype(np.float32)).cuda()).cpu().numpy()
+        assert np.abs(pos - ref).max() < 2e-6, name
+    with pytest.raises(sg.SimError, match="outside"):
+        bad = np.zeros((1, 7), np.float32)
+        bad[0, 0] = 5.0
+        sg.Robot.resolve("psm").fk(torch.from_numpy(bad).cuda())
+
+
+def test_custom_descriptor_generic_axes_and_fixed_joints(sg, oracle):
+    """Generic (non axis-aligned) joint axes, rotated origins and fixed joints
+    take the generic FK path; parity vs the oracle FK."""
+    _cuda()
+    s3 = 1 / np.sqrt(3.0)
+    text = f"""[robot]
+name = weird
+[joint]
+name = a
+kind = revolute
+axis = {s3!r} {s3!r} {s3!r}
+origin_xyz = 0.1 0 0.2
+origin_rpy = 0.3 -0.2 0.5
+limits = -2 2
+velocity_limit = 3
+effort_limit = 10
+[joint]
+name = f
+kind = fixed
+origin_xyz = 0 0.05 0
+origin_rpy = 0.1 0.2 0.3
+[joint]
+name = b
+kind = prismatic
+axis = 0 0.6 0.8
+origin_xyz = 0 0 0.1
+origin_rpy = 0 0 0
+limits = -0.1 0.3
+velocity_limit = 1
+effort_limit = 10
+[joint]
+name = c
+kind = revolute
+axis = 0 -1 0
+origin_xyz = 0.02 0 0
+origin_rpy = 0 0 0
+limits = -1 1
+velocity_limit = 3
+effort_limit = 10
+[joint]
+name = g
+kind = fixed
+origin_xyz = 0 0 0.07
+origin_rpy = 0 0.4 0
+[tool_tip]
+xyz = 0.01 0.02 0.03
+rpy = 0 0 0
+"""
+    m = oracle.parse_robot(text)
+    rng = oracle.make_stream(3, 3)
+    qs = np.array([[oracle.uniform(rng, m.dof_joint(d).limit_lo, m.dof_joint(d).limit_hi)
+                    for d in range(m.dof)] for _ in range(500)])
+    ref = np.array([oracle.fk_matrix(m, q)[:3, 3] for q in qs])
+    rob = sg.Robot.parse(text)
+    pos = rob.fk(torch.from_numpy(qs.astype(np.float32)).cuda()).cpu().numpy()
+    assert np.abs(pos - ref).max() < 2e-6
