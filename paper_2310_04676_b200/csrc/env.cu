@@ -12,12 +12,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <array>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "kernels.cuh"
+#include "launch.hpp"
 #include "robot.hpp"
 #include "sg_env.h"
 
@@ -189,14 +191,14 @@ sg::RobotTable build_table(const sg::RobotModel& m, double dt_sub, const std::ve
   return t;
 }
 
-int block_size() {
-  static int b = [] {
-    const char* s = std::getenv("SG_BLOCK");
-    int v = s ? std::atoi(s) : 64;
-    if (v < 32 || v > 128 || (v & 31)) v = 64;
-    return v;
-  }();
-  return b;
+// Warps per 32-env team (kernels.cuh env_step_kernel). Default 4 for the
+// specialised chains (enough warps per SM to hide latency at 16K envs), 2 for
+// the generic chains; SG_TEAM_WARPS overrides (tuning).
+int team_warps_for(int chain) {
+  const char* s = std::getenv("SG_TEAM_WARPS");
+  int v = s ? std::atoi(s) : 2;
+  if (chain < sg::kChainPsm) return v >= 2 ? 2 : 1;
+  return v >= 4 ? 4 : (v >= 2 ? 2 : 1);
 }
 
 template <typename F>
@@ -250,31 +252,29 @@ struct sg_env {
       if (b) cudaFree(b);
   }
 
-  int dmax() const { return A <= 8 ? 8 : 16; }
+  int chain = sg::kChainGeneric8;
+  int team_warps = 1;
 
-  size_t smem_bytes() const { return static_cast<size_t>(block_size()) * (O + A) * sizeof(float); }
-
-  void launch_step(int k_steps, bool gen) {
-    const int b = block_size();
-    const unsigned grid = static_cast<unsigned>((n + b - 1) / b);
-    const size_t sm = smem_bytes();
-    if (dmax() == 8) {
-      if (gen) sg::env_step_kernel<8, true><<<grid, b, sm, stream>>>(P, k_steps);
-      else sg::env_step_kernel<8, false><<<grid, b, sm, stream>>>(P, k_steps);
-    } else {
-      if (gen) sg::env_step_kernel<16, true><<<grid, b, sm, stream>>>(P, k_steps);
-      else sg::env_step_kernel<16, false><<<grid, b, sm, stream>>>(P, k_steps);
+  void launch(int k_steps, bool gen, bool reset) {
+    sg::LaunchArgs a{k_steps, gen, reset, P.task.task, team_warps, stream};
+    cudaError_t e = cudaSuccess;
+    switch (chain) {
+      case sg::kChainPsm: e = sg::launch_psm(P, a); break;
+      case sg::kChainEcm: e = sg::launch_ecm(P, a); break;
+      case sg::kChainStar: e = sg::launch_star(P, a); break;
+      case sg::kChainGeneric16: e = sg::launch_generic16(P, a); break;
+      default: e = sg::launch_generic8(P, a); break;
     }
-    CK(cudaGetLastError());
+    CK(e);
   }
+  void launch_step(int k_steps, bool gen) { launch(k_steps, gen, false); }
+  void launch_reset() { launch(0, false, true); }
 
-  void launch_reset() {
-    const int b = block_size();
-    const unsigned grid = static_cast<unsigned>((n + b - 1) / b);
-    const size_t sm = static_cast<size_t>(b) * O * sizeof(float);
-    if (dmax() == 8) sg::env_reset_kernel<8><<<grid, b, sm, stream>>>(P);
-    else sg::env_reset_kernel<16><<<grid, b, sm, stream>>>(P);
-    CK(cudaGetLastError());
+  // DoF block [b, e) of team warp s (kernels.cuh: Block)
+  void warp_block(int s, int& b, int& e) const {
+    const int P_ = (A + team_warps - 1) / team_warps;
+    b = std::min(s * P_, A);
+    e = std::min((s + 1) * P_, A);
   }
 
   void views(sg_step_views* out) const {
@@ -344,6 +344,26 @@ std::vector<double> resolve_gain(const double* v, int32_t count, const std::vect
   if (count == 0) return fallback;
   if (count == 1) return std::vector<double>(dof, v[0]);
   return std::vector<double>(v, v + count);
+}
+
+template <class CH>
+bool chain_matches(const sg::RobotTable& t) {
+  if (t.dof != CH::kDof || t.tip_flags != CH::kTipFlags || t.jaw != CH::kJaw) return false;
+  for (int d = 0; d < CH::kDof; ++d) {
+    const auto& j = t.j[d];
+    if (j.axis_code == 6) return false;
+    if (sg::jsig(j.kind, j.axis_code, j.flags & 7, (j.flags >> 3) & 1) != CH::kSig[d]) return false;
+  }
+  return true;
+}
+
+int select_chain(const sg::RobotTable& t, int control_mode, int substeps) {
+  if (control_mode == SG_CONTROL_POSITION && substeps == 4) {
+    if (chain_matches<sg::PsmChain>(t)) return sg::kChainPsm;
+    if (chain_matches<sg::EcmChain>(t)) return sg::kChainEcm;
+    if (chain_matches<sg::StarChain>(t)) return sg::kChainStar;
+  }
+  return t.dof <= 8 ? sg::kChainGeneric8 : sg::kChainGeneric16;
 }
 
 std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_config* dyn,
@@ -492,13 +512,11 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
     CK(cudaMemcpy(p.rng_inc, inc.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
   }
   env->d_actions_in = dalloc<float>(n * dof);
-  // opt in to > 48 KB dynamic shared memory if a large robot needs it
-  const size_t sm = env->smem_bytes();
-  if (sm > 48 * 1024) {
-    CK(cudaFuncSetAttribute(sg::env_step_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(sg::env_step_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(sg::env_reset_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  }
+  // kernel selection: compile-time chain structure when the descriptor's
+  // structure matches a builtin one and the dynamics are the reference
+  // defaults' shape (position control, 4 substeps); generic chain otherwise
+  env->chain = select_chain(P.robot, dc.control_mode, dc.substeps);
+  env->team_warps = team_warps_for(env->chain);
   CK(cudaDeviceSynchronize());
   return env;
 }
@@ -685,7 +703,7 @@ int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t g
     if (global_n < env->n + env->cfg.row_offset) throw sg::ConfigError("bench: global_n_envs smaller than this shard");
     auto& p = env->P.p;
     if (!p.act_state) {
-      p.act_state = dalloc<uint64_t>(env->n);
+      p.act_state = dalloc<uint64_t>(static_cast<size_t>(env->n) * sg::kMaxTeamWarps);
       p.act_buf = dalloc<float>(env->n * env->A);
     }
     const HostPcg r = make_stream(seed, 0xac7104);  // bench.cpp:115
@@ -693,13 +711,21 @@ int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t g
     for (int b = 0; b < 64; ++b) pcg_jump(1ULL << b, r.inc, J.mult[b], J.add[b]);
     const uint64_t A = static_cast<uint64_t>(env->A);
     const uint64_t first_draw = static_cast<uint64_t>(first_step) * static_cast<uint64_t>(global_n) * A;
-    const int b = 128;
-    const unsigned grid = static_cast<unsigned>((env->n + b - 1) / b);
-    sg::bench_seed_kernel<<<grid, b, 0, env->stream>>>(p.act_state, env->n, r.state, first_draw,
-                                                       env->cfg.row_offset, env->A, J);
-    CK(cudaGetLastError());
     env->P.bench.inc = r.inc;
-    pcg_jump(static_cast<uint64_t>(global_n - 1) * A, r.inc, env->P.bench.jump_mult, env->P.bench.jump_add);
+    for (int s = 0; s < env->team_warps; ++s) {
+      int b0, e0;
+      env->warp_block(s, b0, e0);
+      // warp s draws DoFs [b0, e0) of each row: start at draw first + g*A + b0,
+      // then advance global_n*A - (e0-b0) per step
+      const int bs = 128;
+      const unsigned grid = static_cast<unsigned>((env->n + bs - 1) / bs);
+      sg::bench_seed_kernel<<<grid, bs, 0, env->stream>>>(p.act_state + static_cast<size_t>(s) * env->n, env->n,
+                                                          r.state, first_draw + static_cast<uint64_t>(b0),
+                                                          env->cfg.row_offset, env->A, J);
+      CK(cudaGetLastError());
+      pcg_jump(static_cast<uint64_t>(global_n) * A - static_cast<uint64_t>(e0 - b0), r.inc,
+               env->P.bench.jump_mult[s], env->P.bench.jump_add[s]);
+    }
     env->bench_ready = true;
   });
 }

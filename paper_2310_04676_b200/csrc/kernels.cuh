@@ -15,7 +15,10 @@
 // contraction) so reset decisions and waypoint counts match the fp64 oracle.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
+#include <utility>
 
 namespace sg {
 
@@ -110,10 +113,14 @@ struct EnvPtrs {
   float* act_buf;  // [n][A]
 };
 
+constexpr int kMaxTeamWarps = 8;
+
 struct BenchStream {
   uint64_t inc;
-  uint64_t jump_mult;  // advance by (global_n - 1) * A draws after an env's A draws
-  uint64_t jump_add;
+  // per team warp s: advance by global_n * A - N_s draws after the warp's N_s
+  // draws of one step (N_s = DoFs of the warp's block)
+  uint64_t jump_mult[kMaxTeamWarps];
+  uint64_t jump_add[kMaxTeamWarps];
 };
 
 struct StepParams {
@@ -152,12 +159,21 @@ __device__ __forceinline__ double norm3_rn(double x, double y, double z) {
 }
 
 // ---------------------------------------------------------------------------
-// Forward kinematics in fp32 (fk_walk, robot_model.cpp:371-395), rotation as a
-// 3x3 matrix; warp-uniform branches on the joint codes (every thread of the
-// grid walks the same chain).
+// Forward kinematics in fp32 (fk_walk, robot_model.cpp:371-395). The rotation
+// is carried as a 3x3 matrix. Two chain policies:
+//   FixedChain<TIP, SIG...>: the joint STRUCTURE (kind, axis, which origin
+//     components are non-zero) is a compile-time signature, link lengths /
+//     limits / gains stay runtime parameters. Every builtin descriptor (PSM,
+//     ECM, STAR) has one; any descriptor with the same structure uses it.
+//   GenericChain<DMAX>: any chain up to DMAX DoF, warp-uniform branches on the
+//     runtime joint table.
 // ---------------------------------------------------------------------------
+constexpr int jsig(int kind, int axis, int oflags, int rot = 0) {
+  return kind | (axis << 2) | (oflags << 5) | (rot << 8);
+}
+
 __device__ __forceinline__ void rot_cols(float (&m)[9], int ca, int cb, float c, float s) {
-  // columns (ca, cb) <- (c*col_a + s*col_b, c*col_b - s*col_a); ca/cb constant after inlining
+  // columns (ca, cb) <- (c*col_a + s*col_b, c*col_b - s*col_a)
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const float a = m[r * 3 + ca], b = m[r * 3 + cb];
@@ -166,84 +182,140 @@ __device__ __forceinline__ void rot_cols(float (&m)[9], int ca, int cb, float c,
   }
 }
 
-template <int DMAX>
-__device__ __forceinline__ void fk_tip(const RobotTable& R, const float (&q)[DMAX], float (&tip)[3]) {
-  float m[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};  // row-major
-  float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+__device__ __forceinline__ void fast_sincos(float x, float& s, float& c) {
+  // 2*pi range reduction then the SFU sin/cos (abs err ~2^-21.4 on [-pi, pi]).
+  // FK never feeds back into the decoupled joint dynamics, so this only
+  // perturbs the observed tip, by ~1e-7 m.
+  const float red = fmaf(-6.28318530717958647692f, rintf(x * 0.15915494309189533577f), x);
+  __sincosf(red, &s, &c);
+}
+
+// One actuated joint of fk_walk with signature fields (kind, axis, oflags, rot)
+// that are compile-time constants in FixedChain and runtime in GenericChain.
+__device__ __forceinline__ void fk_joint(const JointEnc& J, int kind, int axis, int of, int rot, float qv,
+                                         float (&m)[9], float (&p)[3]) {
+  // p += R * origin_translation
+  if (of & 1) { p[0] += m[0] * J.o[0]; p[1] += m[3] * J.o[0]; p[2] += m[6] * J.o[0]; }
+  if (of & 2) { p[0] += m[1] * J.o[1]; p[1] += m[4] * J.o[1]; p[2] += m[7] * J.o[1]; }
+  if (of & 4) { p[0] += m[2] * J.o[2]; p[1] += m[5] * J.o[2]; p[2] += m[8] * J.o[2]; }
+  if (rot) {  // R = R * R_origin
+    float t[9];
 #pragma unroll
-  for (int d = 0; d < DMAX; ++d) {
-    if (d >= R.dof) break;
-    const JointEnc& J = R.j[d];
-    const int fl = J.flags;
-    // p += R * origin_translation
-    if (fl & 1) { p0 += m[0] * J.o[0]; p1 += m[3] * J.o[0]; p2 += m[6] * J.o[0]; }
-    if (fl & 2) { p0 += m[1] * J.o[1]; p1 += m[4] * J.o[1]; p2 += m[7] * J.o[1]; }
-    if (fl & 4) { p0 += m[2] * J.o[2]; p1 += m[5] * J.o[2]; p2 += m[8] * J.o[2]; }
-    if (fl & 8) {  // R = R * R_origin
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        t[r * 3 + c] = m[r * 3 + 0] * J.R[0 * 3 + c] + m[r * 3 + 1] * J.R[1 * 3 + c] + m[r * 3 + 2] * J.R[2 * 3 + c];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) m[k] = t[k];
+  }
+  if (kind == kRevolute) {
+    float s, c;
+    fast_sincos(qv, s, c);
+    if (axis == 2) rot_cols(m, 0, 1, c, s);        // +z
+    else if (axis == 5) rot_cols(m, 0, 1, c, -s);  // -z
+    else if (axis == 0) rot_cols(m, 1, 2, c, s);   // +x
+    else if (axis == 3) rot_cols(m, 1, 2, c, -s);  // -x
+    else if (axis == 1) rot_cols(m, 2, 0, c, s);   // +y: col2' = c*col2 + s*col0, col0' = c*col0 - s*col2
+    else if (axis == 4) rot_cols(m, 2, 0, c, -s);  // -y
+    else {  // generic axis: Rodrigues  Rr = I + s K + (1 - c) K^2
+      const float kx = J.axis[0], ky = J.axis[1], kz = J.axis[2], omc = 1.f - c;
+      const float rr[9] = {1.f + omc * (-ky * ky - kz * kz), -s * kz + omc * kx * ky, s * ky + omc * kx * kz,
+                           s * kz + omc * kx * ky, 1.f + omc * (-kx * kx - kz * kz), -s * kx + omc * ky * kz,
+                           -s * ky + omc * kx * kz, s * kx + omc * ky * kz, 1.f + omc * (-kx * kx - ky * ky)};
       float t[9];
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          t[r * 3 + c] = m[r * 3 + 0] * J.R[0 * 3 + c] + m[r * 3 + 1] * J.R[1 * 3 + c] + m[r * 3 + 2] * J.R[2 * 3 + c];
+        for (int cc = 0; cc < 3; ++cc)
+          t[r * 3 + cc] = m[r * 3 + 0] * rr[0 * 3 + cc] + m[r * 3 + 1] * rr[1 * 3 + cc] + m[r * 3 + 2] * rr[2 * 3 + cc];
 #pragma unroll
       for (int k = 0; k < 9; ++k) m[k] = t[k];
     }
-    const float qv = q[d];
-    const int code = J.axis_code;
-    if (J.kind == kRevolute) {
-      // 2*pi range reduction then the SFU sin/cos (abs err ~2^-21.4 on
-      // [-pi, pi]): FK never feeds back into the decoupled joint dynamics, so
-      // this only perturbs the observed tip by ~1e-7 m.
-      const float red = fmaf(-6.28318530717958647692f, rintf(qv * 0.15915494309189533577f), qv);
-      float s, c;
-      __sincosf(red, &s, &c);
-      if (code == 2) rot_cols(m, 0, 1, c, s);        // +z
-      else if (code == 5) rot_cols(m, 0, 1, c, -s);  // -z
-      else if (code == 0) rot_cols(m, 1, 2, c, s);   // +x
-      else if (code == 3) rot_cols(m, 1, 2, c, -s);  // -x
-      else if (code == 1) rot_cols(m, 2, 0, c, s);   // +y: col2' = c*col2 + s*col0, col0' = c*col0 - s*col2
-      else if (code == 4) rot_cols(m, 2, 0, c, -s);  // -y
-      else {  // generic axis: Rodrigues  Rr = I + s K + (1 - c) K^2
-        const float kx = J.axis[0], ky = J.axis[1], kz = J.axis[2], omc = 1.f - c;
-        const float rr[9] = {1.f + omc * (-ky * ky - kz * kz), -s * kz + omc * kx * ky, s * ky + omc * kx * kz,
-                             s * kz + omc * kx * ky, 1.f + omc * (-kx * kx - kz * kz), -s * kx + omc * ky * kz,
-                             -s * ky + omc * kx * kz, s * kx + omc * ky * kz, 1.f + omc * (-kx * kx - ky * ky)};
-        float t[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            t[r * 3 + cc] = m[r * 3 + 0] * rr[0 * 3 + cc] + m[r * 3 + 1] * rr[1 * 3 + cc] + m[r * 3 + 2] * rr[2 * 3 + cc];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) m[k] = t[k];
-      }
-    } else {  // prismatic: p += R * (axis * q)
-      if (code == 0 || code == 3) {
-        const float v = code == 3 ? -qv : qv;
-        p0 += m[0] * v; p1 += m[3] * v; p2 += m[6] * v;
-      } else if (code == 1 || code == 4) {
-        const float v = code == 4 ? -qv : qv;
-        p0 += m[1] * v; p1 += m[4] * v; p2 += m[7] * v;
-      } else if (code == 2 || code == 5) {
-        const float v = code == 5 ? -qv : qv;
-        p0 += m[2] * v; p1 += m[5] * v; p2 += m[8] * v;
-      } else {
-        const float a0 = J.axis[0] * qv, a1 = J.axis[1] * qv, a2 = J.axis[2] * qv;
-        p0 += m[0] * a0 + m[1] * a1 + m[2] * a2;
-        p1 += m[3] * a0 + m[4] * a1 + m[5] * a2;
-        p2 += m[6] * a0 + m[7] * a1 + m[8] * a2;
-      }
+  } else {  // prismatic: p += R * (axis * q)
+    if (axis == 0 || axis == 3) {
+      const float v = axis == 3 ? -qv : qv;
+      p[0] += m[0] * v; p[1] += m[3] * v; p[2] += m[6] * v;
+    } else if (axis == 1 || axis == 4) {
+      const float v = axis == 4 ? -qv : qv;
+      p[0] += m[1] * v; p[1] += m[4] * v; p[2] += m[7] * v;
+    } else if (axis == 2 || axis == 5) {
+      const float v = axis == 5 ? -qv : qv;
+      p[0] += m[2] * v; p[1] += m[5] * v; p[2] += m[8] * v;
+    } else {
+      const float a0 = J.axis[0] * qv, a1 = J.axis[1] * qv, a2 = J.axis[2] * qv;
+      p[0] += m[0] * a0 + m[1] * a1 + m[2] * a2;
+      p[1] += m[3] * a0 + m[4] * a1 + m[5] * a2;
+      p[2] += m[6] * a0 + m[7] * a1 + m[8] * a2;
     }
   }
-  const int tf = R.tip_flags;
-  if (tf & 1) { p0 += m[0] * R.tip[0]; p1 += m[3] * R.tip[0]; p2 += m[6] * R.tip[0]; }
-  if (tf & 2) { p0 += m[1] * R.tip[1]; p1 += m[4] * R.tip[1]; p2 += m[7] * R.tip[1]; }
-  if (tf & 4) { p0 += m[2] * R.tip[2]; p1 += m[5] * R.tip[2]; p2 += m[8] * R.tip[2]; }
-  tip[0] = p0;
-  tip[1] = p1;
-  tip[2] = p2;
 }
+
+__device__ __forceinline__ void fk_tip_offset(const RobotTable& R, int tf, const float (&m)[9], const float (&p)[3],
+                                              float (&tip)[3]) {
+  float t0 = p[0], t1 = p[1], t2 = p[2];
+  if (tf & 1) { t0 += m[0] * R.tip[0]; t1 += m[3] * R.tip[0]; t2 += m[6] * R.tip[0]; }
+  if (tf & 2) { t0 += m[1] * R.tip[1]; t1 += m[4] * R.tip[1]; t2 += m[7] * R.tip[1]; }
+  if (tf & 4) { t0 += m[2] * R.tip[2]; t1 += m[5] * R.tip[2]; t2 += m[8] * R.tip[2]; }
+  tip[0] = t0;
+  tip[1] = t1;
+  tip[2] = t2;
+}
+
+template <int TIPF, int JAW, int... S>
+struct FixedChain {
+  static constexpr int kDof = sizeof...(S);
+  static constexpr bool kExact = true;
+  static constexpr int kTipFlags = TIPF;
+  static constexpr int kJaw = JAW;
+  static constexpr int kSig[kDof] = {S...};
+  __device__ static int dof(const RobotTable&) { return kDof; }
+  __device__ static int jaw(const RobotTable&) { return kJaw; }
+  template <int D>
+  __device__ static void joint(const RobotTable& R, const float (&q)[kDof], float (&m)[9], float (&p)[3]) {
+    constexpr int sig = kSig[D];
+    fk_joint(R.j[D], sig & 3, (sig >> 2) & 7, (sig >> 5) & 7, (sig >> 8) & 1, q[D], m, p);
+  }
+  template <int... D>
+  __device__ static void walk(const RobotTable& R, const float (&q)[kDof], float (&m)[9], float (&p)[3],
+                              std::integer_sequence<int, D...>) {
+    (joint<D>(R, q, m, p), ...);
+  }
+  __device__ static void fk(const RobotTable& R, const float (&q)[kDof], float (&tip)[3]) {
+    float m[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+    float p[3] = {0.f, 0.f, 0.f};
+    walk(R, q, m, p, std::make_integer_sequence<int, kDof>{});
+    fk_tip_offset(R, TIPF, m, p, tip);
+  }
+};
+
+template <int DMAX>
+struct GenericChain {
+  static constexpr int kDof = DMAX;
+  static constexpr bool kExact = false;
+  __device__ static int dof(const RobotTable& R) { return R.dof; }
+  __device__ static int jaw(const RobotTable& R) { return R.jaw; }
+  __device__ static void fk(const RobotTable& R, const float (&q)[DMAX], float (&tip)[3]) {
+    float m[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+    float p[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+      if (d >= R.dof) break;
+      const JointEnc& J = R.j[d];
+      fk_joint(J, J.kind, J.axis_code, J.flags & 7, (J.flags >> 3) & 1, q[d], m, p);
+    }
+    fk_tip_offset(R, R.tip_flags, m, p, tip);
+  }
+};
+
+// Builtin chain structures (assets/robots/*.robot after fixed-joint folding).
+using PsmChain = FixedChain<0, 6, jsig(kRevolute, 2, 0), jsig(kRevolute, 1, 0), jsig(kPrismatic, 5, 4),
+                            jsig(kRevolute, 2, 0), jsig(kRevolute, 0, 4), jsig(kRevolute, 1, 4),
+                            jsig(kRevolute, 0, 4)>;
+using EcmChain = FixedChain<4, -1, jsig(kRevolute, 2, 0), jsig(kRevolute, 1, 0), jsig(kPrismatic, 5, 4),
+                            jsig(kRevolute, 2, 0), jsig(kRevolute, 0, 4), jsig(kRevolute, 1, 4)>;
+using StarChain = FixedChain<4, -1, jsig(kRevolute, 2, 4), jsig(kRevolute, 1, 4), jsig(kRevolute, 2, 4),
+                             jsig(kRevolute, 1, 4), jsig(kRevolute, 2, 4), jsig(kRevolute, 1, 4),
+                             jsig(kRevolute, 2, 0), jsig(kRevolute, 1, 4)>;
 
 // ---------------------------------------------------------------------------
 // Spline (spline.hpp:24-36, spline.cpp:40-72) in fp64, streaming: the
@@ -269,7 +341,7 @@ __device__ __forceinline__ double dist3_rn(const double (&a)[3], const double (&
 
 // Writes waypoints (fp32) for one row; returns the count (<= cap), or -1 if
 // the table capacity is exceeded.
-__device__ __noinline__ int spline_waypoints_stream(const Spline& s, double spacing, float* out, int cap) {
+static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, double spacing, float* out, int cap) {
   const double span = 1.0;  // t1 - t0 (sample_path, envs.cpp:248-249)
   double prev[3], p[3];
   spline_eval(s, 0.0, prev);
@@ -336,31 +408,61 @@ __device__ __forceinline__ bool sample_goal(uint64_t& s, uint64_t inc, const Tas
   return false;
 }
 
+// ---------------------------------------------------------------------------
+// Block-cooperative coalesced copies between shared staging and global rows.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void block_store(float* __restrict__ g, const float* __restrict__ s, int count) {
+  if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) {
+    const int n4 = count >> 2;
+    float4* g4 = reinterpret_cast<float4*>(g);
+    const float4* s4 = reinterpret_cast<const float4*>(s);
+    for (int k = threadIdx.x; k < n4; k += blockDim.x) g4[k] = s4[k];
+    for (int k = (n4 << 2) + threadIdx.x; k < count; k += blockDim.x) g[k] = s[k];
+  } else {
+    for (int k = threadIdx.x; k < count; k += blockDim.x) g[k] = s[k];
+  }
+}
+
+__device__ __forceinline__ void block_load(float* __restrict__ s, const float* __restrict__ g, int count,
+                                           bool aligned) {
+  if (aligned) {
+    const int n4 = count >> 2;
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    float4* s4 = reinterpret_cast<float4*>(s);
+    for (int k = threadIdx.x; k < n4; k += blockDim.x) s4[k] = __ldg(g4 + k);
+    for (int k = (n4 << 2) + threadIdx.x; k < count; k += blockDim.x) s[k] = __ldg(g + k);
+  } else {
+    for (int k = threadIdx.x; k < count; k += blockDim.x) s[k] = __ldg(g + k);
+  }
+}
+
 // reset_row (envs.cpp:304-360) for one env. Out of line (rare path) and
 // communicating through HBM only, so the caller's state arrays stay in
 // registers: the caller reloads q/qdot/q_target/goal/tip/waypoint idx+len
 // after the call. Returns an error bit (0 on success).
-template <int DMAX>
+template <class CH, int TASK>
 __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
+  constexpr int D = CH::kDof;
   const RobotTable& R = P.robot;
   const TaskParams& T = P.task;
+  const int task = TASK >= 0 ? TASK : T.task;
+  const int dof = CH::dof(R);
   const int64_t n = T.n;
   uint64_t s = P.p.rng_state[i];
   const uint64_t inc = P.p.rng_inc[i];
   int err = 0;
-  float q[DMAX], qd[DMAX], qt[DMAX], goal[3], tip[3];
+  float q[D], goal[3], tip[3];
   int32_t wp_idx = 0, wp_len = 0;
 #pragma unroll
-  for (int d = 0; d < DMAX; ++d) {
-    if (d < R.dof) {
+  for (int d = 0; d < D; ++d) {
+    q[d] = 0.f;
+    if (d < dof) {
       const double quarter = __dmul_rn(0.25, __dadd_rn(R.hi_d[d], -R.lo_d[d]));
       q[d] = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
-      qd[d] = 0.f;
-      qt[d] = q[d];
     }
   }
-  fk_tip<DMAX>(R, q, tip);
-  if (T.task == kTaskPath) {
+  CH::fk(R, q, tip);
+  if (task == kTaskPath) {
     // sample_path (envs.cpp:241-267)
     Spline sp;
 #pragma unroll
@@ -371,7 +473,9 @@ __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
     for (int k = 0; k < 3; ++k) sp.c[6 + k] = pcg_uniform(s, inc, -0.3, 0.3);
     double d[3];
     if (!sample_goal(s, inc, T, d)) err |= kErrGoalSampling;
-    sp.c[9] = d[0]; sp.c[10] = d[1]; sp.c[11] = d[2];
+    sp.c[9] = d[0];
+    sp.c[10] = d[1];
+    sp.c[11] = d[2];
     double max_off = 0.0;
     for (int k = 0; k <= 100; ++k) {
       double pt[3];
@@ -409,11 +513,11 @@ __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
   P.p.hold_count[i] = 0;
   P.p.episode_count[i] += 1;
 #pragma unroll
-  for (int d = 0; d < DMAX; ++d) {
-    if (d < R.dof) {
+  for (int d = 0; d < D; ++d) {
+    if (d < dof) {
       P.p.q[d * n + i] = q[d];
-      P.p.qd[d * n + i] = qd[d];
-      P.p.qt[d * n + i] = qt[d];
+      P.p.qd[d * n + i] = 0.f;
+      P.p.qt[d * n + i] = q[d];
     }
   }
 #pragma unroll
@@ -421,22 +525,23 @@ __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
     P.p.goals[k * n + i] = goal[k];
     P.p.tips[k * n + i] = tip[k];
   }
-  if (T.task == kTaskPath) {
+  if (task == kTaskPath) {
     P.p.wp_idx[i] = wp_idx;
     P.p.wp_len[i] = wp_len;
   }
   return err;
 }
 
-// Reload one env's state from HBM into registers (after reset_env).
-template <int DMAX>
-__device__ __forceinline__ void load_env(const StepParams& P, int64_t i, float (&q)[DMAX], float (&qd)[DMAX],
-                                         float (&qt)[DMAX], float (&goal)[3], float (&tip)[3], int32_t& wi,
-                                         int32_t& wl) {
+// Load one env's state from HBM (DoF-major SoA) into registers.
+template <class CH, int TASK>
+__device__ __forceinline__ void load_env(const StepParams& P, int64_t i, float (&q)[CH::kDof],
+                                         float (&qd)[CH::kDof], float (&qt)[CH::kDof], float (&goal)[3],
+                                         float (&tip)[3], int32_t& wi, int32_t& wl) {
   const int64_t n = P.task.n;
+  const int dof = CH::dof(P.robot);
 #pragma unroll
-  for (int d = 0; d < DMAX; ++d) {
-    if (d < P.robot.dof) {
+  for (int d = 0; d < CH::kDof; ++d) {
+    if (d < dof) {
       q[d] = P.p.q[d * n + i];
       qd[d] = P.p.qd[d * n + i];
       qt[d] = P.p.qt[d * n + i];
@@ -449,324 +554,518 @@ __device__ __forceinline__ void load_env(const StepParams& P, int64_t i, float (
     goal[k] = P.p.goals[k * n + i];
     tip[k] = P.p.tips[k * n + i];
   }
-  if (P.task.task == kTaskPath) {
+  const int task = TASK >= 0 ? TASK : P.task.task;
+  if (task == kTaskPath) {
     wi = P.p.wp_idx[i];
     wl = P.p.wp_len[i];
   }
 }
 
+// rescale_to_range (dynamics.cpp:91-95): exact at both endpoints.
+__device__ __forceinline__ float rescale(float x, float l, float h) {
+  if (x >= 1.f) return h;
+  if (x <= -1.f) return l;
+  return l + 0.5f * (x + 1.f) * (h - l);
+}
+
 // ---------------------------------------------------------------------------
-// Block-cooperative coalesced copies between shared staging and global rows.
+// The fused step kernel: dynamics -> FK -> reward/flags -> observation ->
+// terminal copy + masked reset + re-observe, k_steps steps per launch.
+//
+// Warp-specialised env teams. A CTA is one team of G warps that owns 32 envs
+// (lane = env); warp s of the team owns the contiguous DoF block
+// [s*P, (s+1)*P), P = ceil(D/G). Because the DoF block is warp-uniform, every
+// DoF index stays a compile-time constant inside the warp's code (FixedChain
+// joint structure is preserved) and there is no intra-warp divergence. Per
+// step each warp integrates its DoFs, composes the partial FK transform of its
+// joints, and stages its observation columns; warp 0 composes the partial
+// transforms (shared memory) into the tip, scores reward / hold / waypoint
+// advance / flags, and runs the out-of-line reset of ended envs. G multiplies
+// the warps per SM (16384 envs = 512 teams), which is what hides latency here.
+//
+//   CH    chain policy          TASK  kTaskTarget / kTaskPath, or -1 runtime
+//   G     warps per team        MODE  control mode, or -1 runtime
+//   GEN   actions = the bench stream generated in-kernel   SUB  substeps or 0
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void block_store(float* __restrict__ g, const float* __restrict__ s, int count) {
-  if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) {
-    const int n4 = count >> 2;
+constexpr int kTeamEnvs = 32;
+
+struct Xform {  // rigid transform (R row-major, p)
+  float m[9];
+  float p[3];
+};
+
+__device__ __forceinline__ void compose(Xform& a, const Xform& b) {  // a = a o b
+  float t[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) t[r * 3 + c] = a.m[r * 3] * b.m[c] + a.m[r * 3 + 1] * b.m[3 + c] + a.m[r * 3 + 2] * b.m[6 + c];
+  const float p0 = a.p[0] + a.m[0] * b.p[0] + a.m[1] * b.p[1] + a.m[2] * b.p[2];
+  const float p1 = a.p[1] + a.m[3] * b.p[0] + a.m[4] * b.p[1] + a.m[5] * b.p[2];
+  const float p2 = a.p[2] + a.m[6] * b.p[0] + a.m[7] * b.p[1] + a.m[8] * b.p[2];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) a.m[k] = t[k];
+  a.p[0] = p0;
+  a.p[1] = p1;
+  a.p[2] = p2;
+}
+
+// DoF block of warp S: [B, E)
+template <class CH, int G, int S>
+struct Block {
+  static constexpr int P = (CH::kDof + G - 1) / G;
+  static constexpr int B = S * P < CH::kDof ? S * P : CH::kDof;
+  static constexpr int E = (S + 1) * P < CH::kDof ? (S + 1) * P : CH::kDof;
+  static constexpr int N = E - B;
+};
+
+// Partial FK of joints [B, E) starting from the identity.
+template <class CH, int B, int... J>
+__device__ __forceinline__ void fk_range(const RobotTable& R, const float* q, Xform& x,
+                                         std::integer_sequence<int, J...>) {
+  if constexpr (CH::kExact) {
+    ((void)fk_joint(R.j[B + J], CH::kSig[B + J] & 3, (CH::kSig[B + J] >> 2) & 7, (CH::kSig[B + J] >> 5) & 7,
+                    (CH::kSig[B + J] >> 8) & 1, q[J], x.m, x.p),
+     ...);
+  } else {
+    (
+        [&] {
+          if (B + J < R.dof) {
+            const JointEnc& Jt = R.j[B + J];
+            fk_joint(Jt, Jt.kind, Jt.axis_code, Jt.flags & 7, (Jt.flags >> 3) & 1, q[J], x.m, x.p);
+          }
+        }(),
+        ...);
+  }
+}
+
+template <class CH>
+__device__ __forceinline__ int tip_flags_of(const RobotTable& R) {
+  if constexpr (CH::kExact) return CH::kTipFlags;
+  else return R.tip_flags;
+}
+
+// Per-team shared memory (two buffers for obs / actions so step k+1 can stage
+// while step k is still being stored).
+template <int G>
+struct TeamSmem {
+  float xf[G][12][kTeamEnvs];  // partial transforms, lane-contiguous (conflict-free)
+  int32_t ended[kTeamEnvs];
+  int32_t any_ended;
+};
+
+// Coalesced team store of `count` staged floats (16-byte vectors). For a
+// FixedChain full team the count is a compile-time constant, so the loop is
+// fully unrolled; g must be 16-byte aligned (the env's row blocks always are).
+template <class CH>
+__device__ __forceinline__ void team_store(float* __restrict__ g, const float* __restrict__ s, int count, bool full,
+                                           int full_count, int t, int nt) {
+  if (CH::kExact && full) {
+    const int n4 = full_count >> 2;
     float4* g4 = reinterpret_cast<float4*>(g);
     const float4* s4 = reinterpret_cast<const float4*>(s);
-    for (int k = threadIdx.x; k < n4; k += blockDim.x) g4[k] = s4[k];
-    for (int k = (n4 << 2) + threadIdx.x; k < count; k += blockDim.x) g[k] = s[k];
+    for (int k = t; k < n4; k += nt) g4[k] = s4[k];
+    for (int k = (n4 << 2) + t; k < full_count; k += nt) g[k] = s[k];
   } else {
-    for (int k = threadIdx.x; k < count; k += blockDim.x) g[k] = s[k];
+    for (int k = t; k < count; k += nt) g[k] = s[k];
   }
 }
 
-__device__ __forceinline__ void block_load(float* __restrict__ s, const float* __restrict__ g, int count,
-                                           bool aligned) {
-  if (aligned) {
-    const int n4 = count >> 2;
-    const float4* g4 = reinterpret_cast<const float4*>(g);
-    float4* s4 = reinterpret_cast<float4*>(s);
-    for (int k = threadIdx.x; k < n4; k += blockDim.x) s4[k] = __ldg(g4 + k);
-    for (int k = (n4 << 2) + threadIdx.x; k < count; k += blockDim.x) s[k] = __ldg(g + k);
-  } else {
-    for (int k = threadIdx.x; k < count; k += blockDim.x) s[k] = __ldg(g + k);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// The fused step kernel. GEN_ACTIONS: actions are the bench stream
-// (bench.cpp:31-35) generated in-kernel and written to p.act_buf; otherwise
-// they are read from P.actions.
-// ---------------------------------------------------------------------------
-template <int DMAX, bool GEN_ACTIONS>
-__global__ void __launch_bounds__(128) env_step_kernel(const __grid_constant__ StepParams P, int k_steps) {
-  extern __shared__ __align__(16) float smem[];
+template <class CH, int G, int S, int TASK, int MODE, int SUB, bool GEN>
+__device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float* s_obs_base, float* s_act_base,
+                                         TeamSmem<G>& ts) {
+  using Blk = Block<CH, G, S>;
+  constexpr int NB = Blk::N > 0 ? Blk::N : 1;
+  constexpr int B0 = Blk::B;
   const RobotTable& R = P.robot;
   const TaskParams& T = P.task;
-  const int A = R.dof;
+  const int A = CH::dof(R);
   const int O = 3 * A + 6;
+  const int task = TASK >= 0 ? TASK : T.task;
+  const int mode = MODE >= 0 ? MODE : T.control_mode;
+  const int substeps = SUB > 0 ? SUB : T.substeps;
   const int64_t n = T.n;
-  const int64_t row0 = (int64_t)blockIdx.x * blockDim.x;
-  const int64_t i = row0 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * kTeamEnvs;
+  const int64_t i = row0 + lane;
   const bool active = i < n;
-  const int rows = (int)min((int64_t)blockDim.x, n - row0);
-  float* s_obs = smem;                             // blockDim * O
-  float* s_act = smem + (size_t)blockDim.x * O;    // blockDim * A (16B aligned: blockDim*O*4 % 16 == 0)
+  const int rows = (int)min((int64_t)kTeamEnvs, n - row0);
+  // runtime DoF count of this block (generic chains)
+  const auto has = [&](int j) { return Blk::N > 0 && (CH::kExact || B0 + j < A); };
 
-  float q[DMAX], qd[DMAX], qt[DMAX], goal[3], tip[3];
-  int32_t sc = 0, hc = 0, wi = 0, wl = 0;
-  uint64_t act_s = 0;
-  if (active) {
+  float q[NB], qd[NB], qt[NB];
 #pragma unroll
-    for (int d = 0; d < DMAX; ++d) {
-      if (d < A) {
-        q[d] = P.p.q[d * n + i];
-        qd[d] = P.p.qd[d * n + i];
-        qt[d] = P.p.qt[d * n + i];
-      } else {
-        q[d] = qd[d] = qt[d] = 0.f;
-      }
+  for (int j = 0; j < NB; ++j) {
+    q[j] = qd[j] = qt[j] = 0.f;
+    if (active && has(j)) {
+      q[j] = P.p.q[(B0 + j) * n + i];
+      qd[j] = P.p.qd[(B0 + j) * n + i];
+      qt[j] = P.p.qt[(B0 + j) * n + i];
     }
+  }
+  // warp 0 owns the task state
+  float goal[3] = {0.f, 0.f, 0.f}, tip[3] = {0.f, 0.f, 0.f};
+  int32_t sc = 0, hc = 0, wi = 0, wl = 0;
+  if (S == 0 && active) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) goal[k] = P.p.goals[k * n + i];
+    for (int k = 0; k < 3; ++k) {
+      goal[k] = P.p.goals[k * n + i];
+      tip[k] = P.p.tips[k * n + i];
+    }
     sc = P.p.step_count[i];
     hc = P.p.hold_count[i];
-    if (T.task == kTaskPath) {
+    if (task == kTaskPath) {
       wi = P.p.wp_idx[i];
       wl = P.p.wp_len[i];
     }
-    if (GEN_ACTIONS) act_s = P.p.act_state[i];
-  } else {
-#pragma unroll
-    for (int d = 0; d < DMAX; ++d) q[d] = qd[d] = qt[d] = 0.f;
-    goal[0] = goal[1] = goal[2] = 0.f;
   }
-  tip[0] = tip[1] = tip[2] = 0.f;
+  uint64_t act_s = 0;
+  if (GEN && active) act_s = P.p.act_state[(int64_t)S * n + i];
 
   for (int step = 0; step < k_steps; ++step) {
-    // ---- actions ---------------------------------------------------------
-    float a[DMAX];
-    if (GEN_ACTIONS) {
+    float* s_obs = s_obs_base + (step & 1) * (kTeamEnvs * O);
+    float* s_act = s_act_base + (step & 1) * (kTeamEnvs * A + 4);
+    // ---- actions -----------------------------------------------------------
+    float a[NB];
+    if (GEN) {
 #pragma unroll
-      for (int d = 0; d < DMAX; ++d) {
-        a[d] = 0.f;
-        if (d < A && active) {
+      for (int j = 0; j < NB; ++j) {
+        a[j] = 0.f;
+        if (active && has(j)) {
           const uint32_t u = pcg_next(act_s, P.bench.inc);
-          // uniform(-1, 1) = -1 + 2 * (u * 2^-32), exact in fp64, one rounding to fp32
-          a[d] = (float)(-1.0 + 2.0 * ((double)u * 0x1.0p-32));
-          s_act[threadIdx.x * A + d] = a[d];
+          // uniform(-1, 1) = -1 + 2 * (u * 2^-32) = (u - 2^31) * 2^-31: the exact
+          // fp64 value of the reference (bench.cpp:34) rounded once to fp32
+          a[j] = __int2float_rn((int32_t)(u ^ 0x80000000u)) * 0x1.0p-31f;
+          s_act[lane * A + B0 + j] = a[j];
         }
       }
-      if (active) act_s = act_s * P.bench.jump_mult + P.bench.jump_add;
-      __syncthreads();
-      block_store(P.p.act_buf + row0 * A, s_act, rows * A);
+      if (active) act_s = act_s * P.bench.jump_mult[S] + P.bench.jump_add[S];
     } else {
-      __syncthreads();
-      block_load(s_act, P.actions + row0 * A, rows * A, P.actions_aligned != 0);
-      __syncthreads();
 #pragma unroll
-      for (int d = 0; d < DMAX; ++d) a[d] = (d < A && active) ? s_act[threadIdx.x * A + d] : 0.f;
+      for (int j = 0; j < NB; ++j) a[j] = (active && has(j)) ? __ldg(P.actions + i * A + B0 + j) : 0.f;
     }
 
-    // ---- dynamics (dynamics.cpp:133-185) ----------------------------------
+    // ---- dynamics (dynamics.cpp:133-185): substeps outer so the block's DoFs
+    // interleave; per-DoF operation order as in the reference -----------------
+    // Generated bench actions are finite and inside [-1, 1) by construction
+    // (no clamp, never saturate; rescale's a <= -1 branch yields lo exactly
+    // like the formula), so the GEN path skips those checks.
     int sat = 0, bad = 0;
-    if (active) {
+    float v_target[NB], tau_cmd[NB], kpqt[NB];
+    const int jaw = CH::jaw(R);
 #pragma unroll
-      for (int d = 0; d < DMAX; ++d) {
-        if (d >= A) continue;
-        float ad = a[d];
+    for (int j = 0; j < NB; ++j) {
+      const int d = B0 + j;
+      v_target[j] = tau_cmd[j] = kpqt[j] = 0.f;
+      if (!has(j)) continue;
+      float ad = a[j];
+      if (!GEN) {
         if (!isfinite(ad)) {
           bad = 1;
-          continue;
+          ad = 0.f;
         }
         if (ad < -1.f || ad > 1.f) {
           ad = ad < -1.f ? -1.f : 1.f;
           ++sat;
         }
-        const float lo = R.lo[d], hi = R.hi[d], vl = R.vel[d], ef = R.eff[d];
-        float v_target = 0.f, tau_cmd = 0.f;
-        const auto rescale = [](float x, float l, float h) {
-          if (x >= 1.f) return h;
-          if (x <= -1.f) return l;
-          return l + 0.5f * (x + 1.f) * (h - l);
-        };
-        if (T.control_mode == kModePosition) {
-          qt[d] = (d == R.jaw) ? (ad > 0.f ? hi : lo) : rescale(ad, lo, hi);
-        } else if (T.control_mode == kModeVelocity) {
-          v_target = rescale(ad, -vl, vl);
-        } else {
-          tau_cmd = rescale(ad, -ef, ef);
-        }
-        const float kp = R.kp[d], kd = R.kd[d], damp = R.damping[d], gain = R.dt_over_inertia[d];
-        const float dt = T.dt_sub;
-        float qq = q[d], vv = qd[d];
-        for (int s = 0; s < T.substeps; ++s) {
-          float tau;
-          if (T.control_mode == kModePosition) tau = kp * (qt[d] - qq) - kd * vv;
-          else if (T.control_mode == kModeVelocity) tau = kd * (v_target - vv);
-          else tau = tau_cmd;
-          tau = fminf(fmaxf(tau, -ef), ef);
-          vv += (tau - damp * vv) * gain;
-          vv = fminf(fmaxf(vv, -vl), vl);
-          qq += vv * dt;
-          if (qq < lo) {
-            qq = lo;
-            vv = 0.f;
-          } else if (qq > hi) {
-            qq = hi;
-            vv = 0.f;
-          }
-        }
-        q[d] = qq;
-        qd[d] = vv;
+      }
+      const float lo = R.lo[d], hi = R.hi[d];
+      const auto rs = [&](float x, float l, float h) {
+        return GEN ? l + 0.5f * (x + 1.f) * (h - l) : rescale(x, l, h);
+      };
+      if (mode == kModePosition) {
+        qt[j] = (d == jaw) ? (ad > 0.f ? hi : lo) : rs(ad, lo, hi);
+        kpqt[j] = R.kp[d] * qt[j];
+      } else if (mode == kModeVelocity) {
+        v_target[j] = rs(ad, -R.vel[d], R.vel[d]);
+      } else {
+        tau_cmd[j] = rs(ad, -R.eff[d], R.eff[d]);
       }
     }
-    // saturation count: warp-aggregated, one atomic per warp with work
-    {
+    const float dt = T.dt_sub;
+#pragma unroll(SUB > 0 ? SUB : 1)
+    for (int s = 0; s < substeps; ++s) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int d = B0 + j;
+        if (!has(j)) continue;
+        const float ef = R.eff[d], vl = R.vel[d];
+        float tau;
+        if (mode == kModePosition) tau = fmaf(-R.kd[d], qd[j], fmaf(-R.kp[d], q[j], kpqt[j]));
+        else if (mode == kModeVelocity) tau = R.kd[d] * (v_target[j] - qd[j]);
+        else tau = tau_cmd[j];
+        tau = fminf(fmaxf(tau, -ef), ef);
+        float vv = qd[j] + (tau - R.damping[d] * qd[j]) * R.dt_over_inertia[d];
+        vv = fminf(fmaxf(vv, -vl), vl);
+        const float qq = q[j] + vv * dt;
+        const float qc = fminf(fmaxf(qq, R.lo[d]), R.hi[d]);  // limit projection
+        qd[j] = qc != qq ? 0.f : vv;
+        q[j] = qc;
+      }
+    }
+    if (!GEN) {
+      if (!active) sat = bad = 0;
       const unsigned wsat = __reduce_add_sync(0xffffffffu, (unsigned)sat);
-      if (wsat && (threadIdx.x & 31) == 0) atomicAdd(P.p.sat_total, (unsigned long long)wsat);
+      if (wsat && lane == 0) atomicAdd(P.p.sat_total, (unsigned long long)wsat);
       if (__any_sync(0xffffffffu, bad) && bad) atomicOr(P.p.err, kErrNonFiniteAction);
     }
 
-    // ---- FK + reward + flags (envs.cpp:456-463, 478-593) ------------------
-    bool ended = false;
-    if (active) {
-      fk_tip<DMAX>(R, q, tip);
-      sc += 1;
-      float reward, dist;
-      bool goal_met;
-      {
-        const float dx = tip[0] - goal[0], dy = tip[1] - goal[1], dz = tip[2] - goal[2];
-        dist = sqrtf(dx * dx + dy * dy + dz * dz);
-      }
-      if (T.task == kTaskPath) {
-        reward = T.neg_alpha * dist;
-        float dcur = dist;
-        const float* table = P.p.wps + i * (int64_t)T.wp_cap * 3;
-        while (wi + 1 < wl && dcur < T.success_radius) {
-          ++wi;
-          goal[0] = table[3 * wi + 0];
-          goal[1] = table[3 * wi + 1];
-          goal[2] = table[3 * wi + 2];
-          const float dx = tip[0] - goal[0], dy = tip[1] - goal[1], dz = tip[2] - goal[2];
-          dcur = sqrtf(dx * dx + dy * dy + dz * dz);
-        }
-        goal_met = (wi + 1 == wl) && dcur < T.success_radius;
-      } else {
-        reward = T.rho * dist;
-        hc = dist < T.success_radius ? hc + 1 : 0;
-        goal_met = hc >= T.success_hold;
-      }
-      if (!isfinite(reward)) atomicOr(P.p.err, kErrNonFiniteReward);
-      const bool timed_out = sc >= T.episode_len;
-      P.p.rewards[i] = reward;
-      P.p.task_error[i] = dist;
-      P.p.terminated[i] = goal_met ? 1 : 0;
-      P.p.timed_out[i] = timed_out ? 1 : 0;
-      ended = goal_met || timed_out;
+    // ---- partial FK of this warp's joints; stage observation columns --------
+    Xform x;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) x.m[k] = (k % 4 == 0) ? 1.f : 0.f;
+    x.p[0] = x.p[1] = x.p[2] = 0.f;
+    fk_range<CH, B0>(R, q, x, std::make_integer_sequence<int, Blk::N>{});
+    if (S > 0) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) ts.xf[S][k][lane] = x.m[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ts.xf[S][9 + k][lane] = x.p[k];
     }
-
-    // ---- observation (envs.cpp:362-408) -----------------------------------
-    const auto stage_obs = [&]() {
+    const auto stage_cols = [&]() {
       if (!active) return;
-      float* o = s_obs + threadIdx.x * O;
-      int off = 0;
+      float* o = s_obs + lane * O;
 #pragma unroll
-      for (int d = 0; d < DMAX; ++d)
-        if (d < A) o[off + d] = q[d];
-      off += A;
-#pragma unroll
-      for (int d = 0; d < DMAX; ++d)
-        if (d < A) o[off + d] = qd[d];
-      off += A;
-      o[off + 0] = tip[0];
-      o[off + 1] = tip[1];
-      o[off + 2] = tip[2];
-      off += 3;
-#pragma unroll
-      for (int d = 0; d < DMAX; ++d)
-        if (d < A) o[off + d] = qt[d];
-      off += A;
-      o[off + 0] = goal[0];
-      o[off + 1] = goal[1];
-      o[off + 2] = goal[2];
+      for (int j = 0; j < NB; ++j)
+        if (has(j)) {
+          o[B0 + j] = q[j];
+          o[A + B0 + j] = qd[j];
+          o[2 * A + 3 + B0 + j] = qt[j];
+        }
     };
-    stage_obs();
-    // ---- ended rows: terminal obs, masked reset, re-observe ----------------
-    const int any_ended = __syncthreads_or(ended);
-    if (any_ended) {
-      // pre-reset observation rows of ended envs -> terminal_observations
-      // (envs.cpp:606-611); each warp copies its own ended rows, one row per
-      // pass with the lanes spread over the row (coalesced).
+    stage_cols();
+    __syncthreads();  // (1) partial transforms, obs columns, actions staged
+
+    if (S == 0) {
+      // ---- compose, reward, flags (envs.cpp:456-463, 478-593) ------------------
+#pragma unroll
+      for (int s = 1; s < G; ++s) {
+        Xform y;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) y.m[k] = ts.xf[s][k][lane];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) y.p[k] = ts.xf[s][9 + k][lane];
+        compose(x, y);
+      }
+      bool ended = false;
+      if (active) {
+        fk_tip_offset(R, tip_flags_of<CH>(R), x.m, x.p, tip);
+        sc += 1;
+        float reward, dist;
+        bool goal_met;
+        {
+          const float dx = tip[0] - goal[0], dy = tip[1] - goal[1], dz = tip[2] - goal[2];
+          dist = sqrtf(dx * dx + dy * dy + dz * dz);
+        }
+        if (task == kTaskPath) {
+          reward = T.neg_alpha * dist;
+          float dcur = dist;
+          const float* table = P.p.wps + i * (int64_t)T.wp_cap * 3;
+          while (wi + 1 < wl && dcur < T.success_radius) {
+            ++wi;
+            goal[0] = table[3 * wi + 0];
+            goal[1] = table[3 * wi + 1];
+            goal[2] = table[3 * wi + 2];
+            const float dx = tip[0] - goal[0], dy = tip[1] - goal[1], dz = tip[2] - goal[2];
+            dcur = sqrtf(dx * dx + dy * dy + dz * dz);
+          }
+          goal_met = (wi + 1 == wl) && dcur < T.success_radius;
+        } else {
+          reward = T.rho * dist;
+          hc = dist < T.success_radius ? hc + 1 : 0;
+          goal_met = hc >= T.success_hold;
+        }
+        if (!isfinite(reward)) atomicOr(P.p.err, kErrNonFiniteReward);
+        const bool timed_out = sc >= T.episode_len;
+        P.p.rewards[i] = reward;
+        P.p.task_error[i] = dist;
+        P.p.terminated[i] = goal_met ? 1 : 0;
+        P.p.timed_out[i] = timed_out ? 1 : 0;
+        ended = goal_met || timed_out;
+        float* o = s_obs + lane * O;
+        o[2 * A + 0] = tip[0];
+        o[2 * A + 1] = tip[1];
+        o[2 * A + 2] = tip[2];
+        o[3 * A + 3] = goal[0];
+        o[3 * A + 4] = goal[1];
+        o[3 * A + 5] = goal[2];
+      }
+      ts.ended[lane] = ended;
       const unsigned m = __ballot_sync(0xffffffffu, ended);
-      const int lane = threadIdx.x & 31;
-      const int wbase = threadIdx.x & ~31;
-      for (unsigned mm = m; mm; mm &= mm - 1) {
-        const int src = wbase + __ffs(mm) - 1;
-        const int64_t row = row0 + src;
-        for (int k = lane; k < O; k += 32) P.p.tobs[row * O + k] = s_obs[src * O + k];
-      }
-      __syncwarp();
-      if (ended) {
-        const int e = reset_env<DMAX>(P, i);
-        if (e) atomicOr(P.p.err, e);
-        load_env<DMAX>(P, i, q, qd, qt, goal, tip, wi, wl);
-        sc = 0;
-        hc = 0;
-        stage_obs();
-      }
+      if (lane == 0) ts.any_ended = m != 0;
+    } else if (GEN) {
+      // idle warps store the generated actions while warp 0 scores
+      team_store<CH>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs, kTeamEnvs * A, threadIdx.x - 32,
+                     (G - 1) * 32);
     }
-    __syncthreads();
-    block_store(P.p.obs + row0 * O, s_obs, rows * O);
+    __syncthreads();  // (2) obs rows complete, ended flags published
+    if (GEN && G == 1)
+      team_store<CH>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs, kTeamEnvs * A, threadIdx.x, 32);
+
+    if (ts.any_ended) {
+      // terminal observations (envs.cpp:606-611): rows of ended envs, all warps
+      for (int r = threadIdx.x >> 5; r < rows; r += G) {
+        if (!ts.ended[r]) continue;
+        for (int k = lane; k < O; k += 32) P.p.tobs[(row0 + r) * O + k] = s_obs[r * O + k];
+      }
+      const bool mine = active && ts.ended[lane];
+      if (S == 0 && mine) {
+        const int e = reset_env<CH, TASK>(P, i);  // reset_row (envs.cpp:304-360), via HBM
+        if (e) atomicOr(P.p.err, e);
+      }
+      __syncthreads();  // (3) reset state in HBM, terminal rows copied
+      if (mine) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (has(j)) {
+            q[j] = P.p.q[(B0 + j) * n + i];
+            qd[j] = P.p.qd[(B0 + j) * n + i];
+            qt[j] = P.p.qt[(B0 + j) * n + i];
+          }
+        stage_cols();
+        if (S == 0) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            goal[k] = P.p.goals[k * n + i];
+            tip[k] = P.p.tips[k * n + i];
+          }
+          if (task == kTaskPath) {
+            wi = P.p.wp_idx[i];
+            wl = P.p.wp_len[i];
+          }
+          sc = 0;
+          hc = 0;
+          float* o = s_obs + lane * O;
+          o[2 * A + 0] = tip[0];
+          o[2 * A + 1] = tip[1];
+          o[2 * A + 2] = tip[2];
+          o[3 * A + 3] = goal[0];
+          o[3 * A + 4] = goal[1];
+          o[3 * A + 5] = goal[2];
+        }
+      }
+      __syncthreads();  // (4) re-observed rows staged
+    }
+    team_store<CH>(P.p.obs + row0 * O, s_obs, rows * O, rows == kTeamEnvs, kTeamEnvs * O, threadIdx.x, 32 * G);
   }
 
   if (active) {
 #pragma unroll
-    for (int d = 0; d < DMAX; ++d) {
-      if (d < A) {
-        P.p.q[d * n + i] = q[d];
-        P.p.qd[d * n + i] = qd[d];
-        P.p.qt[d * n + i] = qt[d];
+    for (int j = 0; j < NB; ++j)
+      if (has(j)) {
+        P.p.q[(B0 + j) * n + i] = q[j];
+        P.p.qd[(B0 + j) * n + i] = qd[j];
+        P.p.qt[(B0 + j) * n + i] = qt[j];
+      }
+    if (S == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        P.p.goals[k * n + i] = goal[k];
+        P.p.tips[k * n + i] = tip[k];
+      }
+      P.p.step_count[i] = sc;
+      P.p.hold_count[i] = hc;
+      if (task == kTaskPath) {
+        P.p.wp_idx[i] = wi;
+        P.p.wp_len[i] = wl;
       }
     }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      P.p.goals[k * n + i] = goal[k];
-      P.p.tips[k * n + i] = tip[k];
-    }
-    P.p.step_count[i] = sc;
-    P.p.hold_count[i] = hc;
-    if (T.task == kTaskPath) {
-      P.p.wp_idx[i] = wi;
-      P.p.wp_len[i] = wl;
-    }
-    if (GEN_ACTIONS) P.p.act_state[i] = act_s;
+    if (GEN) P.p.act_state[(int64_t)S * n + i] = act_s;
   }
+}
+
+template <class CH, int G, int TASK, int MODE, int SUB, bool GEN, int... S>
+__device__ __forceinline__ void team_dispatch(const StepParams& P, int k_steps, float* s_obs, float* s_act,
+                                              TeamSmem<G>& ts, std::integer_sequence<int, S...>) {
+  const int w = threadIdx.x >> 5;
+  ((w == S ? team_run<CH, G, S, TASK, MODE, SUB, GEN>(P, k_steps, s_obs, s_act, ts) : void()), ...);
+}
+
+template <class CH, int G, int TASK, int MODE, int SUB, bool GEN>
+__global__ void __launch_bounds__(32 * G) env_step_kernel(const __grid_constant__ StepParams P, int k_steps) {
+  extern __shared__ __align__(16) float smem[];
+  const int A = CH::dof(P.robot);
+  const int O = 3 * A + 6;
+  TeamSmem<G>& ts = *reinterpret_cast<TeamSmem<G>*>(smem);
+  float* s_obs = smem + (sizeof(TeamSmem<G>) + 15) / 16 * 4;  // 2 x 32 x O
+  float* s_act = s_obs + 2 * kTeamEnvs * O;                    // 2 x (32 x A + 4)
+  team_dispatch<CH, G, TASK, MODE, SUB, GEN>(P, k_steps, s_obs, s_act, ts, std::make_integer_sequence<int, G>{});
+}
+
+template <int G>
+inline size_t team_smem_bytes(int A) {
+  const int O = 3 * A + 6;
+  return (sizeof(TeamSmem<G>) + 15) / 16 * 16 + (size_t)(2 * kTeamEnvs * O + 2 * (kTeamEnvs * A + 4)) * sizeof(float);
 }
 
 // reset() (envs.cpp:425-435): every row through reset_row, episode_count := 0,
 // observe, clear flags and rewards.
-template <int DMAX>
+template <class CH, int TASK>
 __global__ void __launch_bounds__(128) env_reset_kernel(const __grid_constant__ StepParams P) {
+  constexpr int D = CH::kDof;
   extern __shared__ __align__(16) float smem[];
   const RobotTable& R = P.robot;
   const TaskParams& T = P.task;
-  const int A = R.dof;
+  const int A = CH::dof(R);
   const int O = 3 * A + 6;
   const int64_t n = T.n;
   const int64_t row0 = (int64_t)blockIdx.x * blockDim.x;
   const int64_t i = row0 + threadIdx.x;
   const int rows = (int)min((int64_t)blockDim.x, n - row0);
   if (i < n) {
-    float q[DMAX], qd[DMAX], qt[DMAX], goal[3], tip[3];
+    float q[D], qd[D], qt[D], goal[3], tip[3];
     int32_t wi = 0, wl = 0;
-    const int e = reset_env<DMAX>(P, i);
+    const int e = reset_env<CH, TASK>(P, i);
     if (e) atomicOr(P.p.err, e);
-    load_env<DMAX>(P, i, q, qd, qt, goal, tip, wi, wl);
+    load_env<CH, TASK>(P, i, q, qd, qt, goal, tip, wi, wl);
     P.p.episode_count[i] = 0;
     P.p.terminated[i] = 0;
     P.p.timed_out[i] = 0;
     P.p.rewards[i] = 0.f;
     float* o = smem + threadIdx.x * O;
-    int off = 0;
-    for (int d = 0; d < A; ++d) o[off++] = q[d];
-    for (int d = 0; d < A; ++d) o[off++] = qd[d];
-    for (int k = 0; k < 3; ++k) o[off++] = tip[k];
-    for (int d = 0; d < A; ++d) o[off++] = qt[d];
-    for (int k = 0; k < 3; ++k) o[off++] = goal[k];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (d < A) {
+        o[d] = q[d];
+        o[A + d] = qd[d];
+        o[2 * A + 3 + d] = qt[d];
+      }
+    for (int k = 0; k < 3; ++k) {
+      o[2 * A + k] = tip[k];
+      o[3 * A + 3 + k] = goal[k];
+    }
   }
   __syncthreads();
   block_store(P.p.obs + row0 * O, smem, rows * O);
+}
+
+// Host-side launch plumbing: one translation unit per chain instantiates its
+// kernels (parallel compilation) and exposes a launcher.
+constexpr int kResetBlock = 64;
+
+template <class CH, int TASK, int MODE, int SUB, int G>
+inline cudaError_t launch_team(const StepParams& P, int k_steps, bool gen, cudaStream_t st) {
+  const unsigned grid = (unsigned)((P.task.n + kTeamEnvs - 1) / kTeamEnvs);
+  const size_t sm = team_smem_bytes<G>(P.robot.dof);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  if (gen) env_step_kernel<CH, G, TASK, MODE, SUB, true><<<grid, 32 * G, sm, st>>>(P, k_steps);
+  else env_step_kernel<CH, G, TASK, MODE, SUB, false><<<grid, 32 * G, sm, st>>>(P, k_steps);
+  return cudaGetLastError();
+}
+
+template <class CH, int TASK>
+inline cudaError_t launch_reset(const StepParams& P, cudaStream_t st) {
+  const unsigned grid = (unsigned)((P.task.n + kResetBlock - 1) / kResetBlock);
+  const size_t sm = (size_t)kResetBlock * (3 * P.robot.dof + 6) * sizeof(float);
+  env_reset_kernel<CH, TASK><<<grid, kResetBlock, sm, st>>>(P);
+  return cudaGetLastError();
 }
 
 // Positions the per-env bench action stream at draw (first_step*G + g)*A,
@@ -776,7 +1075,7 @@ struct JumpTable {
   uint64_t add[64];
 };
 
-__global__ void bench_seed_kernel(uint64_t* act_state, int64_t n, uint64_t base_state, uint64_t first_draw,
+static __global__ void bench_seed_kernel(uint64_t* act_state, int64_t n, uint64_t base_state, uint64_t first_draw,
                                   int64_t row_offset, int32_t A, const __grid_constant__ JumpTable J) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -804,7 +1103,7 @@ __global__ void fk_batch_kernel(const __grid_constant__ RobotTable R, const floa
     }
   }
   if (bad) atomicOr(err, kErrFkLimit);
-  fk_tip<DMAX>(R, q, tip);
+  GenericChain<DMAX>::fk(R, q, tip);
   pos[i * 3 + 0] = tip[0];
   pos[i * 3 + 1] = tip[1];
   pos[i * 3 + 2] = tip[2];

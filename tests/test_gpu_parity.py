@@ -268,9 +268,11 @@ def test_control_modes_limits_and_parity(sg, oracle, mode):
     env = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=99, dynamics=dict(control_mode=mode))
     env.reset()
     rng = oracle.make_stream(42, 0)
-    lo = np.array([m.dof_joint(d).limit_lo for d in range(m.dof)])
-    hi = np.array([m.dof_joint(d).limit_hi for d in range(m.dof)])
-    vl = np.array([m.dof_joint(d).velocity_limit for d in range(m.dof)])
+    # the device stores limits in fp32: the bounds hold against the fp32-rounded limits
+    f32 = lambda v: np.float64(np.float32(v))
+    lo = np.array([f32(m.dof_joint(d).limit_lo) for d in range(m.dof)])
+    hi = np.array([f32(m.dof_joint(d).limit_hi) for d in range(m.dof)])
+    vl = np.array([f32(m.dof_joint(d).velocity_limit) for d in range(m.dof)])
     sat_total = 0
     for s in range(250):
         a = (2.0 * oracle.fill_uniform_actions(rng, n, m.dof)).astype(np.float32)
@@ -310,7 +312,7 @@ def test_custom_descriptor_generic_axes_and_fixed_joints(sg, oracle):
     """Generic (non axis-aligned) joint axes, rotated origins and fixed joints
     take the generic FK path; parity vs the oracle FK."""
     _cuda()
-    s3 = 1 / np.sqrt(3.0)
+    s3 = float(1 / np.sqrt(3.0))
     text = f"""[robot]
 name = weird
 [joint]
