@@ -68,6 +68,24 @@ def step_bytes(A: int, O: int, fused: int, reset_frac: float) -> dict:
                 per_env_launch=total, per_env_step=total / fused)
 
 
+def shard_plan(rank: int, world: int, n_per_gpu: int) -> dict:
+    """Env sharding across ranks (weak scaling): rank r owns global envs
+    [r*N, (r+1)*N); per-env RNG streams and the bench action stream are
+    indexed by global env id, so the union of the shards is bit-identical to
+    one device stepping world*N envs. No collective touches the step."""
+    return dict(row_offset=rank * n_per_gpu, n_envs=n_per_gpu, global_n_envs=world * n_per_gpu)
+
+
+def max_over_ranks(value: float, dist, device) -> float:
+    """Timing reduction: the job is as slow as its slowest rank."""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 class Clocks:
     """SM clock and throttle-reason sampling (NVML, the source nvidia-smi reads)
     on a background thread every 5 ms while the timed region runs."""
@@ -185,11 +203,12 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 
     n = cfg["n_envs"]
+    plan = shard_plan(rank, world, n)
     env = sg.VecTaskEnv(robots=(cfg["robot"],), device=local, n_envs=n, seed=0, task=cfg["task"],
-                        goal_sigma=cfg["goal_sigma"], row_offset=rank * n)
+                        goal_sigma=cfg["goal_sigma"], row_offset=plan["row_offset"])
     A, O = env.action_dim, env.obs_dim
     env.reset()
-    env.bench_begin(0, first_step=0, global_n_envs=world * n)
+    env.bench_begin(0, first_step=0, global_n_envs=plan["global_n_envs"])
     F = max(1, min(args.fuse, args.steps))
     # warm-up: W untimed steps (first is the bench_sim warm-up step), plus one
     # untimed fused launch so the timed launches see a warm instruction cache
@@ -220,10 +239,8 @@ def main():
     steps_done += args.steps
     launch_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     t_ms = sum(launch_ms)
+    t_ms = max_over_ranks(t_ms, dist, f"cuda:{local}")
     if dist:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
         dist.barrier()
     value = world * n * args.steps / (t_ms * 1e-3)
 
@@ -267,10 +284,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
-        if dist:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(e2e_ms, dist, f"cuda:{local}")
         d2h = sum(t.numel() * t.element_size() for t in outs.values()) + 8
         e2e = dict(value=world * n * E / (e2e_ms * 1e-3), unit="env-steps/s", h2d_bytes_per_step=n * A * 4,
                    d2h_bytes_per_step=d2h, steps=E, path="sg_env_step_host (C-ABI), 1 launch/step")

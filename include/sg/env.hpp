@@ -1,0 +1,140 @@
+// C++ drop-in over the C-ABI (include/sg_env.h): the method set of the
+// reference's BatchedEnv / VecTaskEnv (proj/include/scalpel/envs.hpp:107-179),
+// namespace scalpel_b200 in place of scalpel. Header-only; link libsg_env.so.
+//
+// Differences a caller sees: buffers are fp32 device
+// memory (row-major n_envs x dim, the reference's MatrixXdR layout) owned by
+// the env; step() takes device actions (or host actions via step_host());
+// device-detected errors surface at the next synchronising call.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../sg_env.h"
+
+namespace scalpel_b200 {
+
+class ConfigError : public std::runtime_error {  // errors.hpp:23-26 (exit code 2)
+ public:
+  explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+class SimError : public std::runtime_error {  // errors.hpp:44-47 (exit code 1)
+ public:
+  explicit SimError(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void check(int rc) {
+  if (rc == SG_OK) return;
+  if (rc == SG_ERR_CONFIG) throw ConfigError(sg_last_error());
+  throw SimError(sg_last_error());
+}
+
+struct EnvConfig : sg_env_config {  // envs.hpp:42-63 defaults
+  EnvConfig() { sg_env_config_init(this); }
+};
+struct DynamicsConfig : sg_dynamics_config {  // dynamics.hpp:34-44 defaults
+  DynamicsConfig() { sg_dynamics_config_init(this); }
+};
+
+// StepResult (envs.hpp:82-89) as device views.
+struct StepResult {
+  const float* observations = nullptr;
+  const float* rewards = nullptr;
+  const uint8_t* terminated = nullptr;
+  const uint8_t* timed_out = nullptr;
+  const float* terminal_observations = nullptr;
+};
+
+struct ObservationField {
+  std::string name;
+  int offset = 0;
+  int length = 0;
+};
+
+class BatchedEnv {  // envs.hpp:107-118
+ public:
+  virtual ~BatchedEnv() = default;
+  virtual int64_t n_envs() const = 0;
+  virtual int obs_dim() const = 0;
+  virtual int action_dim() const = 0;
+  virtual const float* reset() = 0;
+  virtual const StepResult& step(const float* d_actions) = 0;
+  virtual const float* task_error() const = 0;
+};
+
+class VecTaskEnv : public BatchedEnv {
+ public:
+  // robots: builtin names ("psm", "ecm", "star") or .robot paths.
+  VecTaskEnv(const EnvConfig& cfg, const std::vector<std::string>& robots,
+             const DynamicsConfig& dyn = DynamicsConfig(), int device = 0) {
+    std::vector<const char*> names;
+    for (const auto& r : robots) names.push_back(r.c_str());
+    check(sg_env_create(&cfg, &dyn, names.data(), static_cast<int32_t>(names.size()), device, &env_));
+    int32_t o = 0, a = 0;
+    check(sg_env_dims(env_, &n_, &o, &a));
+    obs_dim_ = o;
+    action_dim_ = a;
+  }
+  ~VecTaskEnv() override { sg_env_destroy(env_); }
+  VecTaskEnv(const VecTaskEnv&) = delete;
+  VecTaskEnv& operator=(const VecTaskEnv&) = delete;
+
+  int64_t n_envs() const override { return n_; }
+  int obs_dim() const override { return obs_dim_; }
+  int action_dim() const override { return action_dim_; }
+
+  void set_stream(void* cuda_stream) { check(sg_env_set_stream(env_, cuda_stream)); }
+
+  const float* reset() override {
+    check(sg_env_reset(env_, &views_));
+    fill();
+    return views_.observations;
+  }
+  const StepResult& step(const float* d_actions) override {
+    check(sg_env_step(env_, d_actions, &views_));
+    fill();
+    return result_;
+  }
+  // Host actions -> host StepResult (synchronous; reports device errors).
+  int64_t step_host(const float* h_actions, sg_host_result* out) {
+    check(sg_env_step_host(env_, h_actions, out));
+    return out ? out->action_saturations : 0;
+  }
+  const float* task_error() const override {
+    float* p = nullptr;
+    check(sg_env_task_error(env_, &p));
+    return p;
+  }
+  void synchronize() { check(sg_env_synchronize(env_)); }
+
+  std::vector<ObservationField> layout() const {  // envs.cpp:166-192
+    std::vector<ObservationField> out;
+    for (int32_t i = 0; i < sg_env_layout_count(env_); ++i) {
+      const char* name = nullptr;
+      int32_t off = 0, len = 0;
+      check(sg_env_layout_field(env_, i, &name, &off, &len));
+      out.push_back({name, off, len});
+    }
+    return out;
+  }
+  sg_env* handle() { return env_; }
+
+ private:
+  void fill() {
+    result_.observations = views_.observations;
+    result_.rewards = views_.rewards;
+    result_.terminated = views_.terminated;
+    result_.timed_out = views_.timed_out;
+    result_.terminal_observations = views_.terminal_observations;
+  }
+  sg_env* env_ = nullptr;
+  int64_t n_ = 0;
+  int obs_dim_ = 0, action_dim_ = 0;
+  sg_step_views views_{};
+  StepResult result_{};
+};
+
+}  // namespace scalpel_b200

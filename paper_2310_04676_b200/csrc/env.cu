@@ -271,10 +271,13 @@ struct sg_env {
   void launch_reset() { launch(0, false, true); }
 
   // DoF block [b, e) of team warp s (kernels.cuh: Block)
+  // (blocks are cut from the chain's compile-time DoF count: A for the fixed
+  // chains, 8/16 for the generic ones, whose warps skip DoFs >= A)
   void warp_block(int s, int& b, int& e) const {
-    const int P_ = (A + team_warps - 1) / team_warps;
-    b = std::min(s * P_, A);
-    e = std::min((s + 1) * P_, A);
+    const int D = chain == sg::kChainGeneric8 ? 8 : (chain == sg::kChainGeneric16 ? 16 : A);
+    const int b0 = sg::dof_block_begin(D, team_warps, s);
+    b = std::min(b0, A);
+    e = std::min(b0 + sg::dof_block_size(D, team_warps, s), A);
   }
 
   void views(sg_step_views* out) const {

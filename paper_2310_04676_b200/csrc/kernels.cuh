@@ -610,13 +610,21 @@ __device__ __forceinline__ void compose(Xform& a, const Xform& b) {  // a = a o 
   a.p[2] = p2;
 }
 
-// DoF block of warp S: [B, E)
+// DoF block of team warp S: [B, B + N). Blocks are contiguous; the remainder
+// DoFs go to the LAST warps so warp 0 (which also composes the transform and
+// scores the step) carries the fewest DoFs. Shared by host and device.
+__host__ __device__ constexpr int dof_block_begin(int D, int G, int S) {
+  return S * (D / G) + ((S - (G - D % G)) > 0 ? (S - (G - D % G)) : 0);
+}
+__host__ __device__ constexpr int dof_block_size(int D, int G, int S) {
+  return D / G + (S >= G - D % G ? 1 : 0);
+}
+
 template <class CH, int G, int S>
 struct Block {
-  static constexpr int P = (CH::kDof + G - 1) / G;
-  static constexpr int B = S * P < CH::kDof ? S * P : CH::kDof;
-  static constexpr int E = (S + 1) * P < CH::kDof ? (S + 1) * P : CH::kDof;
-  static constexpr int N = E - B;
+  static constexpr int B = dof_block_begin(CH::kDof, G, S);
+  static constexpr int N = dof_block_size(CH::kDof, G, S);
+  static constexpr int E = B + N;
 };
 
 // Partial FK of joints [B, E) starting from the identity.
@@ -654,20 +662,29 @@ struct TeamSmem {
   int32_t any_ended;
 };
 
-// Coalesced team store of `count` staged floats (16-byte vectors). For a
-// FixedChain full team the count is a compile-time constant, so the loop is
-// fully unrolled; g must be 16-byte aligned (the env's row blocks always are).
-template <class CH>
+// Coalesced team store of `count` staged floats with 16-byte vectors. For a
+// FixedChain full team the count and thread count are compile-time constants:
+// all shared loads of the thread are issued before its global stores. g must
+// be 16-byte aligned (an env's row block always is).
+template <class CH, int FULL, int NT>
 __device__ __forceinline__ void team_store(float* __restrict__ g, const float* __restrict__ s, int count, bool full,
-                                           int full_count, int t, int nt) {
+                                           int t) {
   if (CH::kExact && full) {
-    const int n4 = full_count >> 2;
+    constexpr int n4 = FULL / 4;
+    constexpr int iters = (n4 + NT - 1) / NT;
     float4* g4 = reinterpret_cast<float4*>(g);
     const float4* s4 = reinterpret_cast<const float4*>(s);
-    for (int k = t; k < n4; k += nt) g4[k] = s4[k];
-    for (int k = (n4 << 2) + t; k < full_count; k += nt) g[k] = s[k];
+    float4 v[iters];
+#pragma unroll
+    for (int it = 0; it < iters; ++it)
+      if (t + it * NT < n4) v[it] = s4[t + it * NT];
+#pragma unroll
+    for (int it = 0; it < iters; ++it)
+      if (t + it * NT < n4) g4[t + it * NT] = v[it];
+    if constexpr (FULL % 4 != 0)
+      for (int k = n4 * 4 + t; k < FULL; k += NT) g[k] = s[k];
   } else {
-    for (int k = t; k < count; k += nt) g[k] = s[k];
+    for (int k = t; k < count; k += NT) g[k] = s[k];
   }
 }
 
@@ -895,12 +912,13 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       if (lane == 0) ts.any_ended = m != 0;
     } else if (GEN) {
       // idle warps store the generated actions while warp 0 scores
-      team_store<CH>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs, kTeamEnvs * A, threadIdx.x - 32,
-                     (G - 1) * 32);
+      team_store<CH, kTeamEnvs * CH::kDof, (G > 1 ? G - 1 : 1) * 32>(P.p.act_buf + row0 * A, s_act, rows * A,
+                                                                    rows == kTeamEnvs, threadIdx.x - 32);
     }
     __syncthreads();  // (2) obs rows complete, ended flags published
     if (GEN && G == 1)
-      team_store<CH>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs, kTeamEnvs * A, threadIdx.x, 32);
+      team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs,
+                                               threadIdx.x);
 
     if (ts.any_ended) {
       // terminal observations (envs.cpp:606-611): rows of ended envs, all warps
@@ -946,7 +964,8 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       }
       __syncthreads();  // (4) re-observed rows staged
     }
-    team_store<CH>(P.p.obs + row0 * O, s_obs, rows * O, rows == kTeamEnvs, kTeamEnvs * O, threadIdx.x, 32 * G);
+    team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32 * G>(P.p.obs + row0 * O, s_obs, rows * O, rows == kTeamEnvs,
+                                                          threadIdx.x);
   }
 
   if (active) {
