@@ -23,6 +23,7 @@
  *   sg_env_task_error        BatchedEnv::task_error()      include/scalpel/envs.hpp:117
  *   sg_env_bench_*           bench_sim's action stream + step loop  src/bench.cpp:31-35,97-135
  *   sg_robot_*               parse_robot / forward_kinematics_batch  src/robot_model.cpp:191-283,404-443
+ *   sg_policy_*              Policy ctor / forward (tensor cores)   src/policy.cpp:42-161
  *   sg_last_error            exception message (what()) of the reference's
  *                            ConfigError / ParseError / SimError  include/scalpel/errors.hpp:23-48
  *
@@ -217,6 +218,25 @@ int sg_robot_dof(const sg_robot* robot, int32_t* dof, int32_t* jaw_dof);
 /* Batched FK on the device: d_q row-major n x dof fp32 -> d_pos n x 3 fp32.
  * Out-of-limit rows (check_q, src/robot_model.cpp:353-367) raise SG_ERR_SIM. */
 int sg_robot_fk(const sg_robot* robot, const float* d_q, int64_t n, float* d_pos, void* stream);
+
+/* Policy MLP forward on the tensor cores (tcgen05, BF16 in / FP32 accumulate):
+ * Policy::forward (src/policy.cpp:110-161) for the reference's default
+ * 256/128/64 ELU actor and critic trunks. d_flat is the reference's flat
+ * parameter vector (policy.cpp:42-63) in fp32 on the device; load_params
+ * packs it into bf16 UMMA images (call after every parameter update). */
+typedef struct sg_policy sg_policy;
+int sg_policy_create(int32_t obs_dim, int32_t action_dim, const int32_t* hidden, int32_t n_hidden,
+                     int32_t device, sg_policy** out);
+void sg_policy_destroy(sg_policy* policy);
+int sg_policy_param_count(const sg_policy* policy, int64_t* count, int64_t* log_std_offset);
+int sg_policy_load_params(sg_policy* policy, const float* d_flat, void* stream);
+/* Policy::init_params (policy.cpp:87-102) on the host into h_flat (param_count fp32). */
+int sg_policy_init_params(const sg_policy* policy, uint64_t seed, double init_log_std, float* h_flat);
+/* d_obs: n x obs_stride fp32 (e.g. the env's observation view) -> d_mean
+ * (n x action_dim), d_value (n). */
+int sg_policy_forward(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
+                      float* d_mean, float* d_value, void* stream);
+const char* sg_policy_last_error(void);
 
 const char* sg_last_error(void);
 const char* sg_version(void);

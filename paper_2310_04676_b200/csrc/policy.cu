@@ -1,0 +1,585 @@
+// Policy MLP forward on the 5th-generation tensor cores (tcgen05 / TMEM).
+//
+// Reference: Policy::forward / trunk_forward (proj/src/policy.cpp:110-161):
+// actor  obs -> 256 -> 128 -> 64 -> A  (ELU on hidden layers, policy.cpp:33)
+// critic obs -> 256 -> 128 -> 64 -> 1
+// flat fp64 parameter vector laid out actor (W_l [out x in] row-major, b_l)
+// for l = 0..3, then critic, then log_std (policy.cpp:42-63).
+//
+// Device design (one CTA = one 128-row tile, 4 warps, 1 CTA per SM):
+//  * weights are packed once per parameter update into bf16 images in the
+//    UMMA K-major no-swizzle canonical layout and streamed into shared memory
+//    with 1-D bulk copies (cp.async.bulk -> UBLKCP, mbarrier complete_tx);
+//  * every layer is tcgen05.mma.cta_group::1.kind::f16 (BF16 x BF16 -> FP32)
+//    issued by one thread, M = 128, accumulators in TMEM (512 columns);
+//  * the epilogue warps read their TMEM lane quarter (tcgen05.ld 32x32b),
+//    add bias, apply ELU, round to bf16 and write the next layer's A operand
+//    straight into shared memory; the last layer writes fp32 mean / value.
+//  * L1 of actor and critic is ONE N=512 product (shared input); the critic's
+//    hidden layer waits in TMEM columns 256..511 while the actor finishes.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sg_env.h"
+
+namespace sgp {
+
+constexpr int kRows = 128;  // UMMA M
+constexpr int kK0 = 32;     // padded obs width
+constexpr int kH1 = 256, kH2 = 128, kH3 = 64, kNOut = 16;  // kNOut: padded output width
+
+// Shared-memory plan (bytes). R0 holds the obs tile + W1 during layer 1 and
+// W3/W4 afterwards; R1 = A2 (h1), R2 = W2 (actor, then critic), R3 = A3,
+// R4 = A4.
+constexpr uint32_t kX0 = 0;                                // 128 x 32 bf16
+constexpr uint32_t kW1 = 8192;                             // 512 x 32 bf16
+constexpr uint32_t kW3a = 0, kW3c = 16384;                 // 64 x 128 bf16 each
+constexpr uint32_t kW4a = 32768, kW4c = 34816;             // 16 x 64 bf16 each
+constexpr uint32_t kA2 = 40960;                            // 128 x 256 bf16
+constexpr uint32_t kW2 = kA2 + 65536;                      // 128 x 256 bf16
+constexpr uint32_t kA3 = kW2 + 65536;                      // 128 x 128 bf16
+constexpr uint32_t kA4 = kA3 + 32768;                      // 128 x 64 bf16
+constexpr uint32_t kBar = kA4 + 16384;                     // mbarriers
+constexpr uint32_t kSmem = kBar + 128;
+
+// Packed parameter image (global): same byte layout as the smem regions.
+struct PolicyImage {
+  const uint8_t* w1;    // 32768 B
+  const uint8_t* w2a;   // 65536 B
+  const uint8_t* w2c;
+  const uint8_t* w34;   // W3a | W3c | W4a | W4c, 36864 B
+  const float* b1;      // 512 (actor | critic)
+  const float* b2a;     // 128
+  const float* b2c;
+  const float* b3a;     // 64
+  const float* b3c;
+  const float* b4a;     // 16 (padded)
+  const float* b4c;     // 16 (padded)
+};
+
+// Byte offset of element (r, k) in a K-major, no-swizzle UMMA tile with R
+// rows: 8x(16 B) core matrices, 8-row groups contiguous (SBO = 128 B), K
+// chunks of 8 elements R*16 B apart (LBO).
+__host__ __device__ constexpr uint32_t kmajor_off(uint32_t r, uint32_t k, uint32_t R) {
+  return (k >> 3) * (R * 16u) + (r >> 3) * 128u + (r & 7u) * 16u + (k & 7u) * 2u;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major.
+__host__ __device__ constexpr uint32_t make_idesc(uint32_t M, uint32_t N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void async_proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 16 consecutive fp32 accumulator columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+__device__ __forceinline__ float elu(float x) { return x > 0.f ? x : __expf(x) - 1.f; }  // policy.cpp:33
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Epilogue for a hidden layer: TMEM columns [c0, c0+N) of this thread's row
+// -> +bias -> ELU -> bf16 -> K-major A tile (128 rows) at a_base.
+template <int N>
+__device__ __forceinline__ void epi_hidden(uint32_t tmem_row, uint32_t c0, const float* __restrict__ bias,
+                                           uint8_t* a_base, int row) {
+#pragma unroll 1
+  for (int c = 0; c < N; c += 16) {
+    float v[16];
+    tmem_ld16(tmem_row + c0 + c, v);
+    uint32_t p[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      p[k] = pack_bf16(elu(v[2 * k] + __ldg(bias + c + 2 * k)), elu(v[2 * k + 1] + __ldg(bias + c + 2 * k + 1)));
+    uint4* d0 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c, kRows));
+    uint4* d1 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c + 8, kRows));
+    *d0 = make_uint4(p[0], p[1], p[2], p[3]);
+    *d1 = make_uint4(p[4], p[5], p[6], p[7]);
+  }
+}
+
+// Issue one layer: D[128 x N] (+)= A[128 x K] * B[N x K]^T, K in steps of 16.
+__device__ __forceinline__ void issue_layer(uint32_t d_tmem, uint32_t a_addr, uint32_t a_rows, uint32_t b_addr,
+                                            uint32_t b_rows, int K, int N) {
+  const uint32_t idesc = make_idesc(kRows, N);
+  const uint32_t lbo_a = a_rows * 16u, lbo_b = b_rows * 16u;
+  for (int s = 0; s < K / 16; ++s) {
+    const uint64_t a = make_desc(a_addr + 2u * s * lbo_a, lbo_a, 128u);
+    const uint64_t b = make_desc(b_addr + 2u * s * lbo_b, lbo_b, 128u);
+    mma_bf16(d_tmem, a, b, idesc, s > 0 ? 1u : 0u);
+  }
+}
+
+struct FwdArgs {
+  const float* obs;  // n x obs_stride fp32 (first obs_dim columns used)
+  int64_t n;
+  int32_t obs_dim;
+  int32_t obs_stride;
+  int32_t act_dim;
+  float* mean;   // n x act_dim
+  float* value;  // n
+};
+
+__global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constant__ PolicyImage W,
+                                                            const __grid_constant__ FwdArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * kRows;
+  const int row = tid;  // TMEM lane == tile row
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBar + 64);
+  const uint32_t bar_w1 = smem_u32(&bars[0]), bar_w2 = smem_u32(&bars[1]), bar_w34 = smem_u32(&bars[2]);
+  const uint32_t bar_mma = smem_u32(&bars[3]);
+  const uint32_t sbase = smem_u32(smem);
+
+  if (tid == 0) {
+    for (int b = 0; b < 4; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: all 512 columns (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  if (tid == 0) {  // stream the first weights while the obs tile is converted
+    bulk_load(sbase + kW1, W.w1, 32768, bar_w1);
+    bulk_load(sbase + kW2, W.w2a, 65536, bar_w2);
+  }
+  // obs tile -> bf16 K-major [128 x 32] (zero padded rows / columns)
+  {
+    float x[kK0];
+#pragma unroll
+    for (int k = 0; k < kK0; ++k) x[k] = 0.f;
+    if (row0 + row < args.n) {
+      const float* src = args.obs + (row0 + row) * args.obs_stride;
+#pragma unroll
+      for (int k = 0; k < kK0; ++k)
+        if (k < args.obs_dim) x[k] = __ldg(src + k);
+    }
+#pragma unroll
+    for (int c = 0; c < kK0; c += 8) {
+      uint4* d = reinterpret_cast<uint4*>(smem + kX0 + kmajor_off(row, c, kRows));
+      *d = make_uint4(pack_bf16(x[c], x[c + 1]), pack_bf16(x[c + 2], x[c + 3]), pack_bf16(x[c + 4], x[c + 5]),
+                      pack_bf16(x[c + 6], x[c + 7]));
+    }
+  }
+  async_proxy_fence();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_row = tmem + ((uint32_t)(warp * 32) << 16);
+  uint32_t mma_phase = 0;
+
+  // ---- layer 1: [128 x 32] x [512 x 32]^T -> TMEM cols 0..511 (actor | critic)
+  if (tid == 0) {
+    mbar_wait(bar_w1, 0);
+    tc_fence_after();
+    issue_layer(tmem + 0, sbase + kX0, kRows, sbase + kW1, 512, kK0, 256);
+    issue_layer(tmem + 256, sbase + kX0, kRows, sbase + kW1 + kmajor_off(256, 0, 512), 512, kK0, 256);
+    mma_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, mma_phase);
+  mma_phase ^= 1;
+  tc_fence_after();
+  // R0 is free: stream W3/W4 (both trunks) while the actor's h1 is processed
+  if (tid == 0) bulk_load(sbase + kW3a, W.w34, 36864, bar_w34);
+  epi_hidden<kH1>(tmem_row, 0, W.b1, smem + kA2, row);
+
+  // ---- actor: layer 2 (A2 x W2a -> cols 0..127), 3 (-> 128..191), 4 (-> 192..207)
+  async_proxy_fence();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    mbar_wait(bar_w2, 0);
+    issue_layer(tmem + 0, sbase + kA2, kRows, sbase + kW2, kH2, kH1, kH2);
+    mma_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, mma_phase);
+  mma_phase ^= 1;
+  tc_fence_after();
+  if (tid == 0) bulk_load(sbase + kW2, W.w2c, 65536, bar_w2);  // W2a consumed: stream W2c
+  epi_hidden<kH2>(tmem_row, 0, W.b2a, smem + kA3, row);
+  async_proxy_fence();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    mbar_wait(bar_w34, 0);
+    issue_layer(tmem + 128, sbase + kA3, kRows, sbase + kW3a, kH3, kH2, kH3);
+    mma_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, mma_phase);
+  mma_phase ^= 1;
+  tc_fence_after();
+  epi_hidden<kH3>(tmem_row, 128, W.b3a, smem + kA4, row);
+  async_proxy_fence();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    issue_layer(tmem + 192, sbase + kA4, kRows, sbase + kW4a, kNOut, kH3, kNOut);
+    mma_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, mma_phase);
+  mma_phase ^= 1;
+  tc_fence_after();
+  {
+    float v[16];
+    tmem_ld16(tmem_row + 192, v);
+    if (row0 + row < args.n) {
+      float* dst = args.mean + (row0 + row) * args.act_dim;
+      for (int k = 0; k < args.act_dim; ++k) dst[k] = v[k] + __ldg(W.b4a + k);
+    }
+  }
+  // ---- critic: h1 waits in cols 256..511
+  epi_hidden<kH1>(tmem_row, 256, W.b1 + 256, smem + kA2, row);
+  async_proxy_fence();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    mbar_wait(bar_w2, 1);
+    issue_layer(tmem + 0, sbase + kA2, kRows, sbase + kW2, kH2, kH1, kH2);
+    mma_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, mma_phase);
+  mma_phase ^= 1;
+  tc_fence_after();
+  epi_hidden<kH2>(tmem_row, 0, W.b2c, smem + kA3, row);
+  async_proxy_fence();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    issue_layer(tmem + 128, sbase + kA3, kRows, sbase + kW3c, kH3, kH2, kH3);
+    mma_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, mma_phase);
+  mma_phase ^= 1;
+  tc_fence_after();
+  epi_hidden<kH3>(tmem_row, 128, W.b3c, smem + kA4, row);
+  async_proxy_fence();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    issue_layer(tmem + 192, sbase + kA4, kRows, sbase + kW4c, kNOut, kH3, kNOut);
+    mma_commit(bar_mma);
+  }
+  mbar_wait(bar_mma, mma_phase);
+  mma_phase ^= 1;
+  tc_fence_after();
+  {
+    float v[16];
+    tmem_ld16(tmem_row + 192, v);
+    if (row0 + row < args.n) args.value[row0 + row] = v[0] + __ldg(W.b4c);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---- packing: flat fp32 params (reference layout) -> bf16 UMMA images -----
+struct PackTable {
+  int64_t w_off[2][4];  // flat offsets of W_l [out x in] per trunk
+  int64_t b_off[2][4];
+  int32_t in_dim[4];
+  int32_t out_dim[2][4];
+};
+
+__global__ void policy_pack_kernel(const float* __restrict__ flat, const __grid_constant__ PackTable t, uint8_t* w1,
+                                   uint8_t* w2a, uint8_t* w2c, uint8_t* w34, float* bias) {
+  // one thread per destination bf16 element of every image, then biases
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // image element counts: W1 512x32, W2 128x256 (x2), W3 64x128 (x2), W4 16x64 (x2)
+  const int64_t n1 = 512 * 32, n2 = 128 * 256, n3 = 64 * 128, n4 = 16 * 64;
+  int64_t k = i;
+  auto emit = [&](uint8_t* base, int trunk, int layer, int R, int K, int64_t e) {
+    const int r = (int)(e / K), c = (int)(e % K);
+    float v = 0.f;
+    if (r < t.out_dim[trunk][layer] && c < t.in_dim[layer])
+      v = flat[t.w_off[trunk][layer] + (int64_t)r * t.in_dim[layer] + c];
+    *reinterpret_cast<__nv_bfloat16*>(base + kmajor_off(r, c, R)) = __float2bfloat16_rn(v);
+  };
+  if (k < n1) {  // W1: actor rows 0..255, critic rows 256..511
+    const int r = (int)(k / 32), c = (int)(k % 32), trunk = r >= 256;
+    const int rr = r - 256 * trunk;
+    float v = 0.f;
+    if (c < t.in_dim[0]) v = flat[t.w_off[trunk][0] + (int64_t)rr * t.in_dim[0] + c];
+    *reinterpret_cast<__nv_bfloat16*>(w1 + kmajor_off(r, c, 512)) = __float2bfloat16_rn(v);
+    return;
+  }
+  k -= n1;
+  if (k < n2) return emit(w2a, 0, 1, 128, 256, k);
+  k -= n2;
+  if (k < n2) return emit(w2c, 1, 1, 128, 256, k);
+  k -= n2;
+  if (k < n3) return emit(w34 + 0, 0, 2, 64, 128, k);
+  k -= n3;
+  if (k < n3) return emit(w34 + 16384, 1, 2, 64, 128, k);
+  k -= n3;
+  if (k < n4) return emit(w34 + 32768, 0, 3, 16, 64, k);
+  k -= n4;
+  if (k < n4) return emit(w34 + 34816, 1, 3, 16, 64, k);
+  k -= n4;
+  // biases: b1 (512) | b2a b2c (128+128) | b3a b3c (64+64) | b4a b4c (16+16)
+  if (k < 512) {
+    const int trunk = k >= 256, r = (int)k - 256 * trunk;
+    bias[k] = flat[t.b_off[trunk][0] + r];
+    return;
+  }
+  k -= 512;
+  if (k < 256) {
+    const int trunk = k >= 128, r = (int)k - 128 * trunk;
+    bias[512 + k] = flat[t.b_off[trunk][1] + r];
+    return;
+  }
+  k -= 256;
+  if (k < 128) {
+    const int trunk = k >= 64, r = (int)k - 64 * trunk;
+    bias[768 + k] = flat[t.b_off[trunk][2] + r];
+    return;
+  }
+  k -= 128;
+  if (k < 32) {
+    const int trunk = k >= 16, r = (int)k - 16 * trunk;
+    bias[896 + k] = r < t.out_dim[trunk][3] ? flat[t.b_off[trunk][3] + r] : 0.f;
+  }
+}
+
+}  // namespace sgp
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+struct sg_policy {
+  int obs_dim = 0, act_dim = 0, device = 0;
+  int64_t param_count = 0, log_std_offset = 0;
+  uint8_t* img = nullptr;  // w1 | w2a | w2c | w34
+  float* bias = nullptr;   // 928
+  sgp::PackTable table{};
+  std::string err;
+};
+
+namespace {
+thread_local std::string g_policy_err;
+
+int fail(int code, const std::string& m) {
+  g_policy_err = m;
+  return code;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sg_policy_last_error(void) { return g_policy_err.c_str(); }
+
+int sg_policy_create(int32_t obs_dim, int32_t action_dim, const int32_t* hidden, int32_t n_hidden, int32_t device,
+                     sg_policy** out) {
+  // Policy::Policy (policy.cpp:42-63); the tensor-core kernel is built for the
+  // reference's default trunk 256/128/64 and obs_dim <= 32, action_dim <= 16.
+  if (obs_dim < 1 || action_dim < 1) return fail(SG_ERR_CONFIG, "policy: bad dimensions");
+  if (n_hidden != 3 || hidden[0] != 256 || hidden[1] != 128 || hidden[2] != 64)
+    return fail(SG_ERR_CONFIG, "policy: the sm_100a kernel implements hidden = {256, 128, 64}");
+  if (obs_dim > sgp::kK0 || action_dim > sgp::kNOut)
+    return fail(SG_ERR_CONFIG, "policy: obs_dim <= 32 and action_dim <= 16 required");
+  if (cudaSetDevice(device) != cudaSuccess) return fail(SG_ERR_SIM, "policy: cudaSetDevice failed");
+  auto* p = new sg_policy;
+  p->obs_dim = obs_dim;
+  p->act_dim = action_dim;
+  p->device = device;
+  int64_t off = 0;
+  const int dims[5] = {obs_dim, 256, 128, 64, 0};
+  for (int trunk = 0; trunk < 2; ++trunk) {
+    const int out_last = trunk == 0 ? action_dim : 1;
+    for (int l = 0; l < 4; ++l) {
+      const int in = dims[l], o = l < 3 ? dims[l + 1] : out_last;
+      p->table.w_off[trunk][l] = off;
+      off += (int64_t)o * in;
+      p->table.b_off[trunk][l] = off;
+      off += o;
+      p->table.in_dim[l] = in;
+      p->table.out_dim[trunk][l] = o;
+    }
+  }
+  p->log_std_offset = off;
+  p->param_count = off + action_dim;
+  if (cudaMalloc(&p->img, 32768 + 65536 * 2 + 36864) != cudaSuccess ||
+      cudaMalloc(&p->bias, 928 * sizeof(float)) != cudaSuccess) {
+    delete p;
+    return fail(SG_ERR_SIM, "policy: cudaMalloc failed");
+  }
+  cudaMemset(p->img, 0, 32768 + 65536 * 2 + 36864);
+  cudaMemset(p->bias, 0, 928 * sizeof(float));
+  if (cudaFuncSetAttribute(sgp::policy_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sgp::kSmem) !=
+      cudaSuccess) {
+    delete p;
+    return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+  }
+  *out = p;
+  return SG_OK;
+}
+
+void sg_policy_destroy(sg_policy* p) {
+  if (!p) return;
+  cudaFree(p->img);
+  cudaFree(p->bias);
+  delete p;
+}
+
+int sg_policy_param_count(const sg_policy* p, int64_t* count, int64_t* log_std_offset) {
+  *count = p->param_count;
+  *log_std_offset = p->log_std_offset;
+  return SG_OK;
+}
+
+// Policy::init_params (policy.cpp:87-102): weights N(0, 2/fan_in) from
+// make_stream(seed, 0x9019) in (trunk, layer, row, col) order, last layer
+// scaled by 0.01, biases 0, log-std = init_log_std. Host fp64, then fp32.
+int sg_policy_init_params(const sg_policy* p, uint64_t seed, double init_log_std, float* h_flat) {
+  uint64_t x = seed ^ (0x2545f4914f6cdd1dULL * (0x9019ULL + 1));
+  auto splitmix = [&]() {
+    x += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  };
+  const uint64_t initstate = splitmix(), initseq = splitmix();
+  uint64_t st = 0, inc = (initseq << 1u) | 1u;
+  auto next = [&]() {
+    const uint64_t old = st;
+    st = old * 6364136223846793005ULL + inc;
+    const uint32_t xs = (uint32_t)(((old >> 18u) ^ old) >> 27u), rot = (uint32_t)(old >> 59u);
+    return (xs >> rot) | (xs << ((32u - rot) & 31u));
+  };
+  next();
+  st += initstate;
+  next();
+  auto normal = [&]() {
+    const double u1 = (next() + 0.5) * 0x1.0p-32;
+    const double u2 = next() * 0x1.0p-32;
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586477 * u2);
+  };
+  for (int64_t k = 0; k < p->param_count; ++k) h_flat[k] = 0.f;
+  for (int trunk = 0; trunk < 2; ++trunk)
+    for (int l = 0; l < 4; ++l) {
+      const int rows = p->table.out_dim[trunk][l], cols = p->table.in_dim[l];
+      const double scale = std::sqrt(2.0 / cols);
+      for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+          double w = scale * normal();
+          if (l == 3) w *= 0.01;
+          h_flat[p->table.w_off[trunk][l] + (int64_t)r * cols + c] = (float)w;
+        }
+    }
+  for (int a = 0; a < p->act_dim; ++a) h_flat[p->log_std_offset + a] = (float)init_log_std;
+  return SG_OK;
+}
+
+int sg_policy_load_params(sg_policy* p, const float* d_flat, void* stream) {
+  const int64_t total = 512 * 32 + 2 * 128 * 256 + 2 * 64 * 128 + 2 * 16 * 64 + 928;
+  const int b = 256;
+  sgp::policy_pack_kernel<<<(unsigned)((total + b - 1) / b), b, 0, (cudaStream_t)stream>>>(
+      d_flat, p->table, p->img, p->img + 32768, p->img + 32768 + 65536, p->img + 32768 + 131072, p->bias);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, float* d_mean,
+                      float* d_value, void* stream) {
+  if (n <= 0) return SG_OK;
+  sgp::PolicyImage W;
+  W.w1 = p->img;
+  W.w2a = p->img + 32768;
+  W.w2c = p->img + 32768 + 65536;
+  W.w34 = p->img + 32768 + 131072;
+  W.b1 = p->bias;
+  W.b2a = p->bias + 512;
+  W.b2c = p->bias + 640;
+  W.b3a = p->bias + 768;
+  W.b3c = p->bias + 832;
+  W.b4a = p->bias + 896;
+  W.b4c = p->bias + 912;
+  sgp::FwdArgs a{d_obs, n, p->obs_dim, obs_stride > 0 ? obs_stride : p->obs_dim, p->act_dim, d_mean, d_value};
+  const unsigned grid = (unsigned)((n + sgp::kRows - 1) / sgp::kRows);
+  sgp::policy_fwd_kernel<<<grid, 128, sgp::kSmem, (cudaStream_t)stream>>>(W, a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+}  // extern "C"

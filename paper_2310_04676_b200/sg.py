@@ -113,6 +113,14 @@ _SIGS = {
     "sg_robot_destroy": (None, [C.c_void_p]),
     "sg_robot_dof": (C.c_int, [C.c_void_p, _P(C.c_int32), _P(C.c_int32)]),
     "sg_robot_fk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "sg_policy_create": (C.c_int, [C.c_int32, C.c_int32, _P(C.c_int32), C.c_int32, C.c_int32, _P(C.c_void_p)]),
+    "sg_policy_destroy": (None, [C.c_void_p]),
+    "sg_policy_param_count": (C.c_int, [C.c_void_p, _P(C.c_int64), _P(C.c_int64)]),
+    "sg_policy_load_params": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_init_params": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, C.c_void_p]),
+    "sg_policy_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]),
+    "sg_policy_last_error": (C.c_char_p, []),
 }
 
 _LIB: C.CDLL | None = None
@@ -387,3 +395,56 @@ class VecTaskEnv:
         p = C.c_void_p()
         _check(lib().sg_env_bench_actions(self._h, C.byref(p)))
         return device_view(p.value, (self.n_envs, self.action_dim), "f32", self.device)
+
+
+# ----------------------------------------------------------------------------- policy
+
+def _pcheck(rc: int) -> None:
+    if rc == SG_OK:
+        return
+    msg = lib().sg_policy_last_error().decode()
+    raise (ConfigError if rc == SG_ERR_CONFIG else SimError)(msg)
+
+
+class Policy:
+    """Actor-critic MLP (policy.hpp:63-72) with the tcgen05 forward kernel.
+    Parameters live in one flat fp32 vector in the reference's layout."""
+
+    def __init__(self, obs_dim: int, action_dim: int, hidden=(256, 128, 64), device: int = 0):
+        self.obs_dim, self.action_dim, self.device = obs_dim, action_dim, device
+        hid = (C.c_int32 * len(hidden))(*hidden)
+        h = C.c_void_p()
+        _pcheck(lib().sg_policy_create(obs_dim, action_dim, hid, len(hidden), device, C.byref(h)))
+        self._h = h.value
+        cnt, ls = C.c_int64(), C.c_int64()
+        _pcheck(lib().sg_policy_param_count(self._h, C.byref(cnt), C.byref(ls)))
+        self.param_count, self.log_std_offset = cnt.value, ls.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.sg_policy_destroy(self._h)
+            self._h = None
+
+    def init_params(self, seed: int, init_log_std: float = -1.0) -> np.ndarray:
+        out = np.zeros(self.param_count, np.float32)
+        _pcheck(lib().sg_policy_init_params(self._h, seed, init_log_std, out.ctypes.data))
+        return out
+
+    def load_params(self, flat) -> None:
+        """flat: cuda fp32 tensor (param_count) in the reference layout."""
+        import torch
+        assert flat.is_cuda and flat.dtype == torch.float32 and flat.numel() == self.param_count
+        stream = torch.cuda.current_stream(flat.device).cuda_stream
+        _pcheck(lib().sg_policy_load_params(self._h, flat.contiguous().data_ptr(), stream))
+
+    def forward(self, obs, mean=None, value=None):
+        import torch
+        n = obs.shape[0]
+        if mean is None:
+            mean = torch.empty((n, self.action_dim), device=obs.device, dtype=torch.float32)
+        if value is None:
+            value = torch.empty((n,), device=obs.device, dtype=torch.float32)
+        stream = torch.cuda.current_stream(obs.device).cuda_stream
+        _pcheck(lib().sg_policy_forward(self._h, obs.data_ptr(), n, obs.stride(0), mean.data_ptr(),
+                                        value.data_ptr(), stream))
+        return mean, value
