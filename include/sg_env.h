@@ -236,6 +236,25 @@ int sg_policy_init_params(const sg_policy* policy, uint64_t seed, double init_lo
  * (n x action_dim), d_value (n). */
 int sg_policy_forward(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
                       float* d_mean, float* d_value, void* stream);
+/* Bootstrap values (ppo.cpp:304-313): V(terminal obs) for rows with
+ * timed_out && !terminated, 0 elsewhere; tiles without such rows skip all
+ * tensor-core work. */
+int sg_policy_bootstrap(const sg_policy* policy, const float* d_terminal_obs, int64_t n, int32_t obs_stride,
+                        const uint8_t* d_timed_out, const uint8_t* d_terminated, float* d_value, void* stream);
+/* Rollout sampling (ppo.cpp:262-277): actions = mean + exp(clamp(log_std)) * z,
+ * logp = sum(-z^2/2 - log_std - log(2 pi)/2), z drawn from the trainer stream
+ * (stream_state/inc = make_stream(seed, 0x7261696e)) at u32 draw
+ * *d_draw_pos + step_offset + 2*(e*A + i), i.e. the reference's serial order. */
+int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const float* d_log_std_raw,
+                     uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos,
+                     uint64_t step_offset, float* d_actions, float* d_logp, void* stream);
+/* compute_gae (rollout.cpp:42-66, time-major [n_steps][n_envs]) without the
+ * normalisation, plus episode statistics (ppo.cpp:286-303) accumulated into
+ * d_stats4 = {reward_sum, episode_reward_sum, final_error_sum, episodes}. */
+int sg_compute_gae(const float* d_rewards, const float* d_values, const uint8_t* d_terminated,
+                   const uint8_t* d_timed_out, const float* d_bootstrap, const float* d_last_values,
+                   const float* d_task_error, int32_t n_steps, int64_t n_envs, double gamma, double lambda,
+                   float* d_advantages, float* d_returns, float* d_ep_acc, double* d_stats4, void* stream);
 const char* sg_policy_last_error(void);
 
 const char* sg_last_error(void);

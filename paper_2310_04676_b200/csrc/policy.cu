@@ -185,8 +185,13 @@ struct FwdArgs {
   int32_t obs_dim;
   int32_t obs_stride;
   int32_t act_dim;
-  float* mean;   // n x act_dim
+  float* mean;   // n x act_dim (may be null: value only)
   float* value;  // n
+  // bootstrap mode (ppo.cpp:304-313): when set, only rows with
+  // timed_out && !terminated get V(terminal obs); other rows get 0 and tiles
+  // without such rows exit before any tensor-core work.
+  const uint8_t* timed_out;
+  const uint8_t* terminated;
 };
 
 __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constant__ PolicyImage W,
@@ -195,6 +200,15 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t row0 = (int64_t)blockIdx.x * kRows;
   const int row = tid;  // TMEM lane == tile row
+  bool boot_row = true;
+  if (args.timed_out) {
+    const int64_t r = row0 + row;
+    boot_row = r < args.n && args.timed_out[r] && !args.terminated[r];
+    if (!__syncthreads_or(boot_row)) {
+      if (r < args.n) args.value[r] = 0.f;
+      return;
+    }
+  }
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBar + 64);
   const uint32_t bar_w1 = smem_u32(&bars[0]), bar_w2 = smem_u32(&bars[1]), bar_w34 = smem_u32(&bars[2]);
@@ -297,7 +311,7 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   {
     float v[16];
     tmem_ld16(tmem_row + 192, v);
-    if (row0 + row < args.n) {
+    if (row0 + row < args.n && args.mean) {
       float* dst = args.mean + (row0 + row) * args.act_dim;
       for (int k = 0; k < args.act_dim; ++k) dst[k] = v[k] + __ldg(W.b4a + k);
     }
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   {
     float v[16];
     tmem_ld16(tmem_row + 192, v);
-    if (row0 + row < args.n) args.value[row0 + row] = v[0] + __ldg(W.b4c);
+    if (row0 + row < args.n) args.value[row0 + row] = boot_row ? v[0] + __ldg(W.b4c) : 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -418,6 +432,106 @@ __global__ void policy_pack_kernel(const float* __restrict__ flat, const __grid_
   if (k < 32) {
     const int trunk = k >= 16, r = (int)k - 16 * trunk;
     bias[896 + k] = r < t.out_dim[trunk][3] ? flat[t.b_off[trunk][3] + r] : 0.f;
+  }
+}
+
+// ---- rollout sampling (ppo.cpp:262-277) ------------------------------------
+// The reference draws z for (env e, dim i) from ONE trainer stream
+// make_stream(seed, 0x7261696e) in row-major order, 2 u32 per Box-Muller
+// normal. Each thread jumps its copy of that stream to draw
+// pos + step_off + 2*(e*A + i) (O(log k) PCG32 jump table) so the device
+// consumes exactly the reference's u32 sequence.
+struct Jump64 {
+  uint64_t mult[64];
+  uint64_t add[64];
+};
+
+__device__ __forceinline__ uint32_t pcg32_next(uint64_t& s, uint64_t inc) {
+  const uint64_t old = s;
+  s = old * 6364136223846793005ULL + inc;
+  const uint32_t xs = (uint32_t)(((old >> 18u) ^ old) >> 27u), rot = (uint32_t)(old >> 59u);
+  return (xs >> rot) | (xs << ((32u - rot) & 31u));
+}
+
+__global__ void policy_sample_kernel(const float* __restrict__ mean, int64_t n, int A,
+                                     const float* __restrict__ log_std_raw, uint64_t s0, uint64_t inc,
+                                     const uint64_t* __restrict__ pos, uint64_t step_off,
+                                     const __grid_constant__ Jump64 J, float* __restrict__ actions,
+                                     float* __restrict__ logp) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  uint64_t k = *pos + step_off + 2ull * (uint64_t)e * (uint64_t)A;
+  uint64_t s = s0;
+  for (int b = 0; k; ++b, k >>= 1)
+    if (k & 1) s = s * J.mult[b] + J.add[b];
+  double lp = 0.0;
+  for (int i = 0; i < A; ++i) {
+    double ls = (double)log_std_raw[i];
+    ls = ls < -5.0 ? -5.0 : (ls > 2.0 ? 2.0 : ls);  // Policy::log_std clamp (policy.hpp:28-29)
+    const double sigma = exp(ls);
+    const double u1 = __dmul_rn(__dadd_rn((double)pcg32_next(s, inc), 0.5), 0x1.0p-32);
+    const double u2 = (double)pcg32_next(s, inc) * 0x1.0p-32;
+    const double z = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586477, u2)));
+    actions[e * A + i] = (float)__dadd_rn((double)mean[e * A + i], __dmul_rn(sigma, z));
+    lp = __dadd_rn(lp, __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(-0.5, z), z), -ls), -0.9189385332046727));
+  }
+  logp[e] = (float)lp;
+}
+
+// ---- GAE (rollout.cpp:42-66) + episode statistics (ppo.cpp:286-303) --------
+// Time-major buffers [T][n]. One thread per env: backward GAE recursion with
+// terminated masking and timeout bootstrap, then a forward pass accumulating
+// per-env episode returns (carried across iterations in ep_acc).
+__global__ void gae_kernel(const float* __restrict__ rewards, const float* __restrict__ values,
+                           const uint8_t* __restrict__ term, const uint8_t* __restrict__ tout,
+                           const float* __restrict__ boot, const float* __restrict__ last_values,
+                           const float* __restrict__ task_error, int T, int64_t n, float gamma, float lam,
+                           float* __restrict__ adv, float* __restrict__ ret, float* __restrict__ ep_acc,
+                           double* __restrict__ stats) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double reward_sum = 0.0, ep_reward = 0.0, ep_err = 0.0, episodes = 0.0;
+  if (e < n) {
+    float running = 0.f;
+    for (int t = T - 1; t >= 0; --t) {
+      const int64_t k = (int64_t)t * n + e;
+      const bool te = term[k] != 0, to = tout[k] != 0;
+      float delta;
+      if (te) delta = rewards[k] - values[k];
+      else if (to) delta = rewards[k] + gamma * boot[k] - values[k];
+      else {
+        const float v_next = t == T - 1 ? last_values[e] : values[k + n];
+        delta = rewards[k] + gamma * v_next - values[k];
+      }
+      running = (te || to) ? delta : delta + gamma * lam * running;
+      adv[k] = running;
+      ret[k] = running + values[k];
+    }
+    float acc = ep_acc[e];
+    for (int t = 0; t < T; ++t) {
+      const int64_t k = (int64_t)t * n + e;
+      reward_sum += rewards[k];
+      acc += rewards[k];
+      if (term[k] || tout[k]) {
+        ep_reward += acc;
+        ep_err += task_error[k];
+        episodes += 1.0;
+        acc = 0.f;
+      }
+    }
+    ep_acc[e] = acc;
+  }
+  // warp reduce, one atomic per warp
+  for (int o = 16; o; o >>= 1) {
+    reward_sum += __shfl_down_sync(0xffffffffu, reward_sum, o);
+    ep_reward += __shfl_down_sync(0xffffffffu, ep_reward, o);
+    ep_err += __shfl_down_sync(0xffffffffu, ep_err, o);
+    episodes += __shfl_down_sync(0xffffffffu, episodes, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(stats + 0, reward_sum);
+    atomicAdd(stats + 1, ep_reward);
+    atomicAdd(stats + 2, ep_err);
+    atomicAdd(stats + 3, episodes);
   }
 }
 
@@ -560,8 +674,8 @@ int sg_policy_load_params(sg_policy* p, const float* d_flat, void* stream) {
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
 
-int sg_policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, float* d_mean,
-                      float* d_value, void* stream) {
+static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, float* d_mean,
+                          float* d_value, const uint8_t* d_timed_out, const uint8_t* d_terminated, void* stream) {
   if (n <= 0) return SG_OK;
   sgp::PolicyImage W;
   W.w1 = p->img;
@@ -575,9 +689,51 @@ int sg_policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t
   W.b3c = p->bias + 832;
   W.b4a = p->bias + 896;
   W.b4c = p->bias + 912;
-  sgp::FwdArgs a{d_obs, n, p->obs_dim, obs_stride > 0 ? obs_stride : p->obs_dim, p->act_dim, d_mean, d_value};
+  sgp::FwdArgs a{d_obs, n, p->obs_dim, obs_stride > 0 ? obs_stride : p->obs_dim, p->act_dim, d_mean, d_value,
+                 d_timed_out, d_terminated};
   const unsigned grid = (unsigned)((n + sgp::kRows - 1) / sgp::kRows);
   sgp::policy_fwd_kernel<<<grid, 128, sgp::kSmem, (cudaStream_t)stream>>>(W, a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, float* d_mean,
+                      float* d_value, void* stream) {
+  return policy_forward(p, d_obs, n, obs_stride, d_mean, d_value, nullptr, nullptr, stream);
+}
+
+int sg_policy_bootstrap(const sg_policy* p, const float* d_terminal_obs, int64_t n, int32_t obs_stride,
+                        const uint8_t* d_timed_out, const uint8_t* d_terminated, float* d_value, void* stream) {
+  return policy_forward(p, d_terminal_obs, n, obs_stride, nullptr, d_value, d_timed_out, d_terminated, stream);
+}
+
+int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const float* d_log_std_raw,
+                     uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos, uint64_t step_offset,
+                     float* d_actions, float* d_logp, void* stream) {
+  if (n <= 0) return SG_OK;
+  sgp::Jump64 J;
+  uint64_t cm = 6364136223846793005ULL, ca = stream_inc;
+  for (int b = 0; b < 64; ++b) {  // J[b] = 2^b advances
+    J.mult[b] = cm;
+    J.add[b] = ca;
+    ca = (cm + 1) * ca;
+    cm *= cm;
+  }
+  const int b = 128;
+  sgp::policy_sample_kernel<<<(unsigned)((n + b - 1) / b), b, 0, (cudaStream_t)stream>>>(
+      d_mean, n, action_dim, d_log_std_raw, stream_state, stream_inc, d_draw_pos, step_offset, J, d_actions, d_logp);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_compute_gae(const float* d_rewards, const float* d_values, const uint8_t* d_terminated,
+                   const uint8_t* d_timed_out, const float* d_bootstrap, const float* d_last_values,
+                   const float* d_task_error, int32_t n_steps, int64_t n_envs, double gamma, double lambda,
+                   float* d_advantages, float* d_returns, float* d_ep_acc, double* d_stats4, void* stream) {
+  const int b = 128;
+  sgp::gae_kernel<<<(unsigned)((n_envs + b - 1) / b), b, 0, (cudaStream_t)stream>>>(
+      d_rewards, d_values, d_terminated, d_timed_out, d_bootstrap, d_last_values, d_task_error, n_steps, n_envs,
+      (float)gamma, (float)lambda, d_advantages, d_returns, d_ep_acc, d_stats4);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }

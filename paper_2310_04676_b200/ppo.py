@@ -1,0 +1,293 @@
+"""On-device PPO trainer closing the rollout loop (BASELINE config 5).
+
+Reference: Trainer::iterate / ppo_update / ppo_loss_and_grad / Adam
+(proj/src/ppo.cpp:56-341), compute_gae (proj/src/rollout.cpp:42-77),
+RolloutBuffer (proj/include/scalpel/rollout.hpp:28-48).
+
+Device mapping (everything stays in HBM; the host only sequences launches):
+  rollout step t   sg_policy_forward (tcgen05 BF16 MLP) -> sg_policy_sample
+                   (reference trainer stream, bit-exact u32 draws) -> env step
+                   (fused sm_100a kernel) -> sg_policy_bootstrap (only tiles
+                   with timed-out rows do work) -> D2D copies into the
+                   time-major rollout buffer.
+  after rollout    sg_policy_forward(last obs) -> sg_compute_gae (+ episode
+                   statistics) -> advantage normalisation (global over ranks).
+  update           epochs x minibatches of the clipped-surrogate loss on the
+                   same MLP in PyTorch (library GEMMs, autograd), gradient
+                   all-reduce over ranks (NCCL), global-norm clip, Adam with
+                   the reference's bias correction, log-std clamp, then
+                   sg_policy_load_params repacks the bf16 tensor-core images.
+
+Documented deviations: the minibatch permutation is a
+device permutation (torch.randperm) instead of the reference's Fisher-Yates
+over the shared stream; the trainer stream position is still advanced by the
+Fisher-Yates draw count so every rollout's z draws match the reference's
+stream. With world_size > 1 each rank shuffles its own shard and gradients
+are averaged (PPO is not bit-identical across world sizes).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from . import sg
+
+HALF_LOG_2PI = 0.9189385332046727  # ppo.cpp:28
+LOG_STD_MIN, LOG_STD_MAX = -5.0, 2.0  # policy.hpp:28-29
+TRAIN_STREAM = 0x7261696E  # ppo.cpp:233
+
+M64 = (1 << 64) - 1
+
+
+def make_stream(seed: int, stream_id: int) -> tuple[int, int]:
+    """rng.hpp:69-83 (host side; returns PCG32 (state, inc))."""
+    x = (seed ^ ((0x2545F4914F6CDD1D * (stream_id + 1)) & M64)) & M64
+
+    def splitmix(x):
+        x = (x + 0x9E3779B97F4A7C15) & M64
+        z = x
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+        return x, z ^ (z >> 31)
+
+    x, a = splitmix(x)
+    x, b = splitmix(x)
+    inc = ((b << 1) | 1) & M64
+    s = inc  # 0 * mult + inc
+    s = (s + a) & M64
+    s = (s * 6364136223846793005 + inc) & M64
+    return s, inc
+
+
+@dataclass
+class TrainConfig:  # ppo.hpp:25-45
+    gamma: float = 0.99
+    lam: float = 0.95
+    clip_eps: float = 0.2
+    learning_rate: float = 3e-4
+    epochs: int = 5
+    minibatch_count: int = 4
+    value_coef: float = 1.0
+    entropy_coef: float = 0.0
+    max_grad_norm: float = 1.0
+    n_steps: int = 32
+    init_log_std: float = -1.0
+    timeout_bootstrap: bool = True
+    seed: int = 0
+    update_precision: str = "tf32"  # fp32 | tf32 | bf16 (autocast) for the update GEMMs
+
+    def validate(self):  # ppo.cpp:31-48 (subset relevant on device)
+        if not 0.0 <= self.gamma <= 1.0:
+            raise sg.ConfigError("train.gamma must be in [0, 1]")
+        if not 0.0 <= self.lam <= 1.0:
+            raise sg.ConfigError("train.lambda must be in [0, 1]")
+        if not self.clip_eps > 0.0:
+            raise sg.ConfigError("train.clip_eps must be > 0")
+        if not self.learning_rate > 0.0:
+            raise sg.ConfigError("train.learning_rate must be > 0")
+        if self.epochs < 1 or self.minibatch_count < 1:
+            raise sg.ConfigError("train.epochs and minibatch_count must be >= 1")
+        if self.n_steps < 25:
+            raise sg.ConfigError("train.n_steps must be >= 25 (GAE horizon floor)")
+
+
+def mlp_forward(params: torch.Tensor, obs: torch.Tensor, obs_dim: int, act_dim: int):
+    """Policy::forward (policy.cpp:110-161) on a flat parameter view."""
+    dims = [obs_dim, 256, 128, 64]
+    off = 0
+    outs = []
+    for trunk in (0, 1):
+        h = obs
+        o_last = act_dim if trunk == 0 else 1
+        for l in range(4):
+            i, o = dims[l], (dims[l + 1] if l < 3 else o_last)
+            W = params[off: off + o * i].view(o, i)
+            off += o * i
+            b = params[off: off + o]
+            off += o
+            h = F.linear(h, W, b)
+            if l < 3:
+                h = F.elu(h)
+        outs.append(h)
+    return outs[0], outs[1][:, 0], off
+
+
+def loss_head(mean, value, log_std_raw, actions, old_logp, adv, ret, cfg: TrainConfig):
+    """The data part of ppo_loss_and_grad (ppo.cpp:90-154) on (mean, value,
+    raw log-std); autograd reproduces the reference's analytic gradients."""
+    log_std = log_std_raw.clamp(LOG_STD_MIN, LOG_STD_MAX)  # projection: no gradient outside the box
+    inv_std = torch.exp(-log_std)
+    diff = actions - mean
+    logp = (-0.5 * (diff * inv_std) ** 2 - log_std - HALF_LOG_2PI).sum(1)
+    ratio = torch.exp(logp - old_logp)
+    unclipped = ratio * adv
+    clipped = ratio.clamp(1.0 - cfg.clip_eps, 1.0 + cfg.clip_eps) * adv
+    # d(-surr)/dlogp follows the unclipped branch when it is the min (ties included)
+    surr = torch.where(unclipped <= clipped, unclipped, clipped.detach())
+    policy_loss = -surr.mean()
+    value_loss = 0.5 * ((value - ret) ** 2).mean()
+    entropy = (log_std + 0.5 + HALF_LOG_2PI).sum()
+    loss = policy_loss + cfg.value_coef * value_loss - cfg.entropy_coef * entropy
+    with torch.no_grad():
+        metrics = torch.stack([policy_loss.detach(), value_loss.detach(), entropy.detach(),
+                               (old_logp - logp).mean().detach(),
+                               ((ratio - 1.0).abs() > cfg.clip_eps).float().mean()])
+    return loss, metrics
+
+
+def ppo_loss(params, obs, actions, old_logp, adv, ret, cfg: TrainConfig, obs_dim, act_dim):
+    """ppo_loss_and_grad (ppo.cpp:76-155): MLP forward + loss head."""
+    mean, value, ls_off = mlp_forward(params, obs, obs_dim, act_dim)
+    return loss_head(mean.float(), value.float(), params[ls_off: ls_off + act_dim], actions, old_logp, adv, ret,
+                     cfg)
+
+
+def allreduce_mean_(t: torch.Tensor, dist) -> torch.Tensor:
+    """Gradient all-reduce (sum, then / world) before clipping (ppo.cpp:201)."""
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t)
+        t /= dist.get_world_size()
+    return t
+
+
+def global_adv_stats(adv: torch.Tensor, dist) -> tuple[torch.Tensor, torch.Tensor]:
+    """rollout.cpp:70-76 normalisation statistics over every rank's buffer."""
+    s = torch.stack([adv.sum(), (adv * adv).sum(), torch.tensor(float(adv.numel()), device=adv.device)]).double()
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(s)
+    mean = s[0] / s[2]
+    var = (s[1] / s[2] - mean * mean).clamp_min(0.0)
+    return mean.float(), var.sqrt().float()
+
+
+class Trainer:
+    def __init__(self, env: "sg.VecTaskEnv", policy: "sg.Policy", cfg: TrainConfig, dist=None):
+        cfg.validate()
+        self.env, self.policy, self.cfg, self.dist = env, policy, cfg, dist
+        dev = torch.device(f"cuda:{env.device}")
+        self.dev = dev
+        N, A, O, T = env.n_envs, env.action_dim, env.obs_dim, cfg.n_steps
+        self.N, self.A, self.O, self.T = N, A, O, T
+        self.params = torch.from_numpy(policy.init_params(cfg.seed, cfg.init_log_std)).to(dev).requires_grad_(True)
+        self.ls_off = policy.log_std_offset
+        self.opt = torch.optim.Adam([self.params], lr=cfg.learning_rate, betas=(0.9, 0.999), eps=1e-8)
+        policy.load_params(self.params.detach())
+        z = lambda *s, dt=torch.float32: torch.zeros(*s, device=dev, dtype=dt)
+        self.buf = dict(obs=z(T, N, O), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
+                        terminated=z(T, N, dt=torch.uint8), timed_out=z(T, N, dt=torch.uint8), boot=z(T, N),
+                        task_error=z(T, N), adv=z(T, N), ret=z(T, N), last_values=z(N))
+        self.mean = z(N, A)
+        self.ep_acc = z(N)
+        self.stats = z(4, dt=torch.float64)
+        self.stream_state, self.stream_inc = make_stream(cfg.seed, TRAIN_STREAM)
+        self.draw_pos = 0  # u32 draws consumed from the trainer stream
+        self.d_pos = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.obs = None
+        self.env_steps = 0
+        self.iteration = 0
+        self.gen = torch.Generator(device=dev)
+        self.gen.manual_seed(cfg.seed * 1000003 + (dist.get_rank() if dist is not None and dist.is_initialized() else 0))
+
+    # -- rollout -----------------------------------------------------------
+    def _stream(self):
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def rollout(self):
+        env, pol, b = self.env, self.policy, self.buf
+        N, A, T = self.N, self.A, self.T
+        if self.obs is None:
+            self.obs = env.reset()
+        L = sg.lib()
+        st = self._stream()
+        self.d_pos.fill_(self.draw_pos)
+        log_std = self.params.detach()[self.ls_off: self.ls_off + A].contiguous()
+        for t in range(T):
+            obs = self.obs
+            pol.forward(obs, self.mean, b["values"][t])
+            sg._pcheck(L.sg_policy_sample(self.mean.data_ptr(), N, A, log_std.data_ptr(), self.stream_state,
+                                          self.stream_inc, self.d_pos.data_ptr(), 2 * t * N * A,
+                                          b["actions"][t].data_ptr(), b["logp"][t].data_ptr(), st))
+            b["obs"][t].copy_(obs)
+            res = env.step(b["actions"][t])
+            b["rewards"][t].copy_(res.rewards)
+            b["terminated"][t].copy_(res.terminated)
+            b["timed_out"][t].copy_(res.timed_out)
+            b["task_error"][t].copy_(res.task_error)
+            if self.cfg.timeout_bootstrap:
+                sg._pcheck(L.sg_policy_bootstrap(pol._h, res.terminal_observations.data_ptr(), N, self.O,
+                                                 res.timed_out.data_ptr(), res.terminated.data_ptr(),
+                                                 b["boot"][t].data_ptr(), st))
+            else:
+                b["boot"][t].zero_()
+            self.obs = res.observations
+        self.draw_pos += 2 * T * N * A
+        pol.forward(self.obs, self.mean, b["last_values"])
+        self.env_steps += N * T
+
+    def gae(self):
+        b = self.buf
+        self.stats.zero_()
+        sg._pcheck(sg.lib().sg_compute_gae(
+            b["rewards"].data_ptr(), b["values"].data_ptr(), b["terminated"].data_ptr(), b["timed_out"].data_ptr(),
+            b["boot"].data_ptr(), b["last_values"].data_ptr(), b["task_error"].data_ptr(), self.T, self.N,
+            self.cfg.gamma, self.cfg.lam, b["adv"].data_ptr(), b["ret"].data_ptr(), self.ep_acc.data_ptr(),
+            self.stats.data_ptr(), self._stream()))
+        mean, std = global_adv_stats(b["adv"], self.dist)
+        b["adv"].sub_(mean).div_(std + 1e-8)
+
+    # -- update ------------------------------------------------------------
+    def update(self):
+        cfg, b = self.cfg, self.buf
+        cap = self.T * self.N
+        mb = (cap + cfg.minibatch_count - 1) // cfg.minibatch_count
+        obs = b["obs"].view(cap, self.O)
+        act = b["actions"].view(cap, self.A)
+        logp, adv, ret = b["logp"].view(cap), b["adv"].view(cap), b["ret"].view(cap)
+        prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = cfg.update_precision == "tf32"
+        metrics = torch.zeros(5, device=self.dev)
+        updates = 0
+        try:
+            for _ in range(cfg.epochs):
+                perm = torch.randperm(cap, device=self.dev, generator=self.gen)
+                for start in range(0, cap, mb):
+                    idx = perm[start: start + mb]
+                    self.opt.zero_grad(set_to_none=False)
+                    with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
+                        loss, m = ppo_loss(self.params, obs[idx], act[idx], logp[idx], adv[idx], ret[idx], cfg,
+                                           self.O, self.A)
+                    loss.backward()
+                    g = self.params.grad
+                    allreduce_mean_(g, self.dist)
+                    if cfg.max_grad_norm > 0:
+                        norm = g.norm()
+                        g.mul_(torch.clamp(cfg.max_grad_norm / (norm + 0.0), max=1.0))
+                    self.opt.step()
+                    with torch.no_grad():
+                        self.params[self.ls_off: self.ls_off + self.A].clamp_(LOG_STD_MIN, LOG_STD_MAX)
+                    metrics += m
+                    updates += 1
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+        # the reference's Fisher-Yates consumed cap-1 draws per epoch from the stream
+        self.draw_pos += cfg.epochs * (cap - 1)
+        self.policy.load_params(self.params.detach())
+        return metrics / max(updates, 1)
+
+    def iterate(self) -> dict:
+        self.rollout()
+        self.gae()
+        m = self.update()
+        self.iteration += 1
+        s = self.stats.tolist()
+        pm = m.tolist()
+        return dict(iteration=self.iteration, env_steps=self.env_steps, episodes_completed=int(s[3]),
+                    mean_episode_reward=s[1] / s[3] if s[3] else float("nan"),
+                    mean_final_error=s[2] / s[3] if s[3] else float("nan"),
+                    mean_step_reward=s[0] / (self.N * self.T), policy_loss=pm[0], value_loss=pm[1],
+                    entropy=pm[2], kl=pm[3], clip_fraction=pm[4],
+                    log_std_mean=float(self.params.detach()[self.ls_off: self.ls_off + self.A]
+                                       .clamp(LOG_STD_MIN, LOG_STD_MAX).mean()))

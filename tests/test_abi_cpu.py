@@ -115,3 +115,10 @@ def test_cpp_dropin_compiles_and_links(sg, tmp_path):
     if not torch.cuda.is_available():  # no device: the binary must fail loudly, not fall back
         run = subprocess.run([exe, "64", "2"], capture_output=True, text=True)
         assert run.returncode == 1 and "CUDA" in run.stderr
+
+
+def test_every_header_symbol_has_a_ctypes_signature(sg):
+    """Guards against calling an entry point with ctypes' default int
+    conversion (pointer truncation)."""
+    missing = [s for s in sg.header_symbols() if s not in sg._SIGS]
+    assert not missing, missing

@@ -1,0 +1,84 @@
+"""GPU: rollout sampling on the reference trainer stream, the GAE kernel, and
+a short on-device PPO run (config 5 path: tcgen05 policy -> env step ->
+GAE -> update)."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from tests.test_ppo_cpu import _gae_reference  # noqa: E402
+
+
+def test_sample_kernel_uses_reference_stream(sg, oracle):
+    from paper_2310_04676_b200 import ppo
+    n, A, seed = 300, 7, 4
+    L = sg.lib()
+    s0, inc = ppo.make_stream(seed, ppo.TRAIN_STREAM)
+    mean = torch.zeros(n, A, device="cuda")
+    log_std = torch.tensor([0.0, 0.0, 0.0, 0.0, -7.0, 3.0, -1.0], device="cuda")  # two clamped
+    act = torch.empty(n, A, device="cuda")
+    logp = torch.empty(n, device="cuda")
+    skip = 2 * n * A * 3 + 999  # three earlier rollout steps + an update's draws
+    pos = torch.tensor([skip], dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    sg._pcheck(L.sg_policy_sample(mean.data_ptr(), n, A, log_std.data_ptr(), s0, inc, pos.data_ptr(), 2 * n * A,
+                                  act.data_ptr(), logp.data_ptr(), st))
+    torch.cuda.synchronize()
+    r = oracle.make_stream(seed, ppo.TRAIN_STREAM)
+    for _ in range(skip + 2 * n * A):
+        oracle.next_u32(r)
+    ls = np.clip(log_std.cpu().numpy().astype(np.float64), -5, 2)
+    ref_a = np.zeros((n, A)); ref_lp = np.zeros(n)
+    for e in range(n):
+        for i in range(A):
+            z = oracle.normal(r)
+            ref_a[e, i] = np.exp(ls[i]) * z
+            ref_lp[e] += -0.5 * z * z - ls[i] - 0.9189385332046727
+    np.testing.assert_allclose(act.cpu().numpy(), ref_a, rtol=2e-7, atol=1e-30)
+    np.testing.assert_allclose(logp.cpu().numpy(), ref_lp, rtol=1e-6)
+
+
+def test_gae_kernel_matches_reference(sg):
+    rng = np.random.default_rng(7)
+    T, n = 32, 2000
+    rew = rng.normal(size=(T, n)).astype(np.float32)
+    val = rng.normal(size=(T, n)).astype(np.float32)
+    term = (rng.random((T, n)) < 0.02).astype(np.uint8)
+    tout = ((rng.random((T, n)) < 0.03) & (term == 0)).astype(np.uint8)
+    boot = (rng.normal(size=(T, n)) * tout).astype(np.float32)
+    last = rng.normal(size=n).astype(np.float32)
+    terr = rng.random((T, n)).astype(np.float32)
+    d = lambda x: torch.from_numpy(x).cuda()
+    adv = torch.empty(T, n, device="cuda"); ret = torch.empty(T, n, device="cuda")
+    ep_acc = torch.zeros(n, device="cuda"); stats = torch.zeros(4, dtype=torch.float64, device="cuda")
+    args = [d(rew), d(val), d(term), d(tout), d(boot), d(last), d(terr)]
+    sg._pcheck(sg.lib().sg_compute_gae(*[a.data_ptr() for a in args], T, n, 0.99, 0.95, adv.data_ptr(),
+                                       ret.data_ptr(), ep_acc.data_ptr(), stats.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    ra, rr = _gae_reference(rew.astype(np.float64), val.astype(np.float64), term, tout, boot.astype(np.float64),
+                            last.astype(np.float64), 0.99, 0.95)
+    np.testing.assert_allclose(adv.cpu().numpy(), ra, rtol=1e-4, atol=1e-4)
+    np.testing.assert_allclose(ret.cpu().numpy(), rr, rtol=1e-4, atol=1e-4)
+    ends = (term | tout).astype(bool)
+    assert stats[3].item() == ends.sum()
+    assert abs(stats[0].item() - rew.astype(np.float64).sum()) < 1e-2
+
+
+def test_ppo_trainer_runs_and_learns_signal(sg):
+    from paper_2310_04676_b200 import ppo
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=4096, seed=0, episode_len=60)
+    pol = sg.Policy(env.obs_dim, env.action_dim)
+    tr = ppo.Trainer(env, pol, ppo.TrainConfig(seed=0, n_steps=32))
+    hist = [tr.iterate() for _ in range(4)]
+    for h in hist:
+        for k in ("policy_loss", "value_loss", "kl", "mean_step_reward"):
+            assert math.isfinite(h[k]), (k, h)
+    assert hist[-1]["env_steps"] == 4 * 32 * 4096
+    assert hist[-1]["episodes_completed"] > 0  # episode_len 60 -> timeouts inside the run
+    assert -5.0 <= hist[-1]["log_std_mean"] <= 2.0
+    # the critic fits returns: value loss falls from the first to the last iteration
+    assert hist[-1]["value_loss"] < hist[0]["value_loss"]
