@@ -39,7 +39,13 @@ CONFIGS = {
                 workload="dVRK ECM camera reach, 65536 envs/GPU, random actions (BASELINE configs[2])"),
     "star": dict(robot="star", task="path_following", n_envs=16384, goal_sigma=0.15,
                  workload="STAR path following, 16384 envs/GPU, random actions (BASELINE configs[3])"),
+    "ppo": dict(robot="psm", task="target_reaching", n_envs=16384, goal_sigma=0.05,
+                workload="full PPO rollout+update on PSM reach, 16384 envs/GPU, n_steps 32, 5 epochs x 4 "
+                         "minibatches, 256/128/64 ELU MLP (BASELINE configs[4])"),
 }
+
+# Policy::forward FLOPs per env (PSM): 2 * MACs of actor + critic trunks
+POLICY_FLOPS_PER_ENV = 2 * 2 * (27 * 256 + 256 * 128 + 128 * 64) + 2 * (64 * 7 + 64 * 1)
 
 
 def peaks():
@@ -160,10 +166,89 @@ def cpu_reference(cfg: dict, steps: int, budget_s: float, threads: int = 0):
     return float(st[0] / secs[0]), lanes, sample
 
 
+def bench_ppo(args, cfg, rank, world, local, dist):
+    """Config 5: env-steps/s with learning (bench_learning, bench.cpp:137-174):
+    whole trainer iterations (rollout of n_steps x N env steps with the tcgen05
+    policy in the loop, GAE, 5 x 4 PPO minibatch updates, NCCL gradient
+    all-reduce when world > 1) timed with CUDA events, max over ranks."""
+    import torch
+    from paper_2310_04676_b200 import ppo, sg
+    n = cfg["n_envs"]
+    plan = shard_plan(rank, world, n)
+    env = sg.VecTaskEnv(robots=(cfg["robot"],), device=local, n_envs=n, seed=0, task=cfg["task"],
+                        goal_sigma=cfg["goal_sigma"], row_offset=plan["row_offset"])
+    pol = sg.Policy(env.obs_dim, env.action_dim, device=local)
+    tcfg = ppo.TrainConfig(seed=0, update_precision=args.update_precision)
+    tr = ppo.Trainer(env, pol, tcfg, dist=dist)
+    iters = max(1, -(-args.steps // tcfg.n_steps)) if args.steps else 4
+    for _ in range(max(1, args.warmup // tcfg.n_steps + 1)):
+        tr.iterate()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(iters)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stats = None
+    with Clocks(local) as clk:
+        for e in ev:
+            e[0].record()
+            tr.rollout()
+            e[1].record()
+            tr.gae()
+            e[2].record()
+            tr.update()
+            e[3].record()
+        torch.cuda.synchronize()
+    t_ms = sum(e[0].elapsed_time(e[3]) for e in ev)
+    roll_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / iters
+    upd_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / iters
+    t_ms = max_over_ranks(t_ms, dist, f"cuda:{local}")
+    steps = iters * tcfg.n_steps
+    value = world * n * steps / (t_ms * 1e-3)
+    # dominant tensor-core kernel: policy forward on the env's observation rows
+    obs = env._result().observations
+    mean = torch.empty(n, env.action_dim, device=f"cuda:{local}")
+    val = torch.empty(n, device=f"cuda:{local}")
+    for _ in range(5):
+        pol.forward(obs, mean, val)
+    reps = 200
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        pol.forward(obs, mean, val)
+    e1.record()
+    torch.cuda.synchronize()
+    fwd_s = e0.elapsed_time(e1) * 1e-3 / reps
+    peak = None
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        pk = "measured burst"
+    except Exception:
+        peak, pk = 1590.0, "fallback"
+    achieved = n * POLICY_FLOPS_PER_ENV / fwd_s / 1e12
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit="env-steps/s (with learning)", n_gpus=world, steps=steps,
+            warmup=args.warmup, ms_per_step=t_ms / steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+            dtype="bf16 policy fwd / fp32 env / " + args.update_precision + " update", data="synthetic",
+            config=dict(workload=cfg["workload"], n_envs_per_gpu=n, global_envs=world * n, iterations=iters,
+                        parallelism=f"env-shard x{world} + NCCL grad all-reduce" if world > 1 else "1 GPU",
+                        rollout_ms_per_iter=roll_ms, update_ms_per_iter=upd_ms,
+                        l2="not flushed: the rollout buffer (80 MB) and weights are reused across steps by design"),
+            roofline=dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak,
+                          traffic=None, peak_kind=pk, kernel="policy_fwd_kernel (tcgen05)",
+                          flops_per_env=POLICY_FLOPS_PER_ENV, avg_launch_us=fwd_s * 1e6),
+            cpu_baseline=None, e2e=None, gpu_launches=iters * (tcfg.n_steps * 3 + 2),
+            clocks=clk.summary(),
+        )
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64000)
+    ap.add_argument("--steps", type=int, default=None, help="timed env steps (default 64000; ppo: 320)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="psm", choices=sorted(CONFIGS))
@@ -171,8 +256,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--update-precision", default="tf32", choices=["fp32", "tf32", "bf16"])
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = 320 if args.config == "ppo" else 64000
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -201,6 +289,11 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if args.config == "ppo":
+        bench_ppo(args, cfg, rank, world, local, dist)
+        if dist:
+            dist.destroy_process_group()
+        return
 
     n = cfg["n_envs"]
     plan = shard_plan(rank, world, n)
