@@ -339,54 +339,59 @@ __device__ __forceinline__ double dist3_rn(const double (&a)[3], const double (&
   return norm3_rn(__dadd_rn(a[0], -b[0]), __dadd_rn(a[1], -b[1]), __dadd_rn(a[2], -b[2]));
 }
 
-// Writes waypoints (fp32) for one row; returns the count (<= cap), or -1 if
-// the table capacity is exceeded.
+// sample_spline_waypoints (spline.cpp:40-72) in ONE pass over the 1001-point
+// chord table, without storing it: the cumulative sums are formed in the
+// reference's order, and the waypoint loop
+//   for (s = spacing; s < total - 1e-12; s += spacing) {
+//     while (seg + 1 < 1000 && cum[seg + 1] < s) ++seg; emit(seg, s) }
+// is advanced as soon as cum[seg + 1] is known: a target s is emitted at the
+// first k with cum[k] >= s (seg = k - 1), exactly where the reference's while
+// loop stops. total is known only at the end, so emissions with
+// s >= total - 1e-12 (at most one, since spacing >> 1e-12) are truncated.
+// Same operations, same rounding; half the fp64 work of a two-pass walk.
+// Writes fp32 waypoints; returns the count, or -1 past the table capacity.
 static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, double spacing, float* out, int cap) {
   const double span = 1.0;  // t1 - t0 (sample_path, envs.cpp:248-249)
-  double prev[3], p[3];
-  spline_eval(s, 0.0, prev);
-  double total = 0.0;
+  double p_prev[3], p[3];
+  spline_eval(s, 0.0, p_prev);
+  out[0] = (float)p_prev[0];
+  out[1] = (float)p_prev[1];
+  out[2] = (float)p_prev[2];
+  int count = 1, tentative = 1;
+  double cum_prev = 0.0, sv = spacing;
+  double s_emit[2] = {0.0, 0.0};  // targets of the last two tentative emissions
   for (int k = 1; k <= kSplineSubdiv; ++k) {
     spline_eval(s, __dmul_rn(span, (double)k) / (double)kSplineSubdiv, p);
-    total = __dadd_rn(total, dist3_rn(p, prev));
-    prev[0] = p[0]; prev[1] = p[1]; prev[2] = p[2];
-  }
-  int count = 0;
-  double p0[3];
-  spline_eval(s, 0.0, p0);
-  out[0] = (float)p0[0]; out[1] = (float)p0[1]; out[2] = (float)p0[2];
-  count = 1;
-  if (total <= 1e-12) return count;
-  int seg = 0;
-  double cum_seg = 0.0, p_seg[3] = {p0[0], p0[1], p0[2]}, p_next[3];
-  spline_eval(s, __dmul_rn(span, 1.0) / (double)kSplineSubdiv, p_next);
-  double cum_next = __dadd_rn(cum_seg, dist3_rn(p_next, p_seg));
-  const double limit = __dadd_rn(total, -1e-12);
-  for (double sv = spacing; sv < limit; sv = __dadd_rn(sv, spacing)) {
-    while (seg + 1 < kSplineSubdiv && cum_next < sv) {
-      ++seg;
-      cum_seg = cum_next;
-      p_seg[0] = p_next[0]; p_seg[1] = p_next[1]; p_seg[2] = p_next[2];
-      spline_eval(s, __dmul_rn(span, (double)(seg + 1)) / (double)kSplineSubdiv, p_next);
-      cum_next = __dadd_rn(cum_seg, dist3_rn(p_next, p_seg));
+    const double cum_k = __dadd_rn(cum_prev, dist3_rn(p, p_prev));
+    while (cum_k >= sv) {  // the reference's while loop stops at seg = k - 1 for this s
+      const double seg_len = __dadd_rn(cum_k, -cum_prev);
+      const double frac = seg_len > 0.0 ? __dadd_rn(sv, -cum_prev) / seg_len : 0.0;
+      const double t = __dmul_rn(span, __dadd_rn((double)(k - 1), frac)) / (double)kSplineSubdiv;
+      double w[3];
+      spline_eval(s, t, w);
+      if (tentative < cap) {
+        out[3 * tentative + 0] = (float)w[0];
+        out[3 * tentative + 1] = (float)w[1];
+        out[3 * tentative + 2] = (float)w[2];
+      }
+      s_emit[tentative & 1] = sv;
+      ++tentative;
+      sv = __dadd_rn(sv, spacing);
     }
-    const double seg_len = __dadd_rn(cum_next, -cum_seg);
-    const double frac = seg_len > 0.0 ? __dadd_rn(sv, -cum_seg) / seg_len : 0.0;
-    const double t = __dmul_rn(span, __dadd_rn((double)seg, frac)) / (double)kSplineSubdiv;
-    double w[3];
-    spline_eval(s, t, w);
-    if (count >= cap) return -1;
-    out[3 * count + 0] = (float)w[0];
-    out[3 * count + 1] = (float)w[1];
-    out[3 * count + 2] = (float)w[2];
-    ++count;
+    cum_prev = cum_k;
+    p_prev[0] = p[0];
+    p_prev[1] = p[1];
+    p_prev[2] = p[2];
   }
-  double pe[3];
-  spline_eval(s, __dmul_rn(span, (double)kSplineSubdiv) / (double)kSplineSubdiv, pe);
+  const double total = cum_prev;
+  if (total <= 1e-12) return count;
+  const double limit = __dadd_rn(total, -1e-12);
+  count = tentative;
+  while (count > 1 && !(s_emit[(count - 1) & 1] < limit)) --count;  // drop s >= total - 1e-12
   if (count >= cap) return -1;
-  out[3 * count + 0] = (float)pe[0];
-  out[3 * count + 1] = (float)pe[1];
-  out[3 * count + 2] = (float)pe[2];
+  out[3 * count + 0] = (float)p_prev[0];  // pts[1000] == eval(span * 1000 / 1000)
+  out[3 * count + 1] = (float)p_prev[1];
+  out[3 * count + 2] = (float)p_prev[2];
   return count + 1;
 }
 
@@ -927,8 +932,10 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         for (int k = lane; k < O; k += 32) P.p.tobs[(row0 + r) * O + k] = s_obs[r * O + k];
       }
       const bool mine = active && ts.ended[lane];
-      if (S == 0 && mine) {
-        const int e = reset_env<CH, TASK>(P, i);  // reset_row (envs.cpp:304-360), via HBM
+      // reset_row (envs.cpp:304-360) through HBM, so any team warp can run it:
+      // lane l's reset goes to warp l % G (more independent fp64 streams)
+      if (mine && (lane % G) == S) {
+        const int e = reset_env<CH, TASK>(P, i);
         if (e) atomicOr(P.p.err, e);
       }
       __syncthreads();  // (3) reset state in HBM, terminal rows copied
