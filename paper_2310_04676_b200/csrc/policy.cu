@@ -45,8 +45,11 @@ constexpr uint32_t kA2 = 40960;                            // 128 x 256 bf16
 constexpr uint32_t kW2 = kA2 + 65536;                      // 128 x 256 bf16
 constexpr uint32_t kA3 = kW2 + 65536;                      // 128 x 128 bf16
 constexpr uint32_t kA4 = kA3 + 32768;                      // 128 x 64 bf16
-constexpr uint32_t kBar = kA4 + 16384;                     // mbarriers
-constexpr uint32_t kSmem = kBar + 128;
+constexpr uint32_t kBar = kA4 + 16384;                     // mbarriers + TMEM slot
+constexpr uint32_t kBias = kBar + 128;                     // 928 fp32 biases
+constexpr uint32_t kSmem = kBias + 928 * 4;
+constexpr int kThreads = 512;  // 16 warps: 4 TMEM lane quarters x 4 column groups
+constexpr int kGroups = kThreads / kRows;
 
 // Packed parameter image (global): same byte layout as the smem regions.
 struct PolicyImage {
@@ -147,19 +150,21 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// Epilogue for a hidden layer: TMEM columns [c0, c0+N) of this thread's row
-// -> +bias -> ELU -> bf16 -> K-major A tile (128 rows) at a_base.
+// Epilogue for a hidden layer: this warp's column group of TMEM columns
+// [c0, c0+N) for its row -> +bias -> ELU -> bf16 -> K-major A tile (128 rows).
+// Warp w reads TMEM lane quarter w%4 (hardware rule) and column group w/4.
 template <int N>
 __device__ __forceinline__ void epi_hidden(uint32_t tmem_row, uint32_t c0, const float* __restrict__ bias,
-                                           uint8_t* a_base, int row) {
-#pragma unroll 1
-  for (int c = 0; c < N; c += 16) {
+                                           uint8_t* a_base, int row, int group) {
+  constexpr int kPer = N / kGroups;
+#pragma unroll
+  for (int cc = 0; cc < kPer; cc += 16) {
+    const int c = group * kPer + cc;
     float v[16];
     tmem_ld16(tmem_row + c0 + c, v);
     uint32_t p[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      p[k] = pack_bf16(elu(v[2 * k] + __ldg(bias + c + 2 * k)), elu(v[2 * k + 1] + __ldg(bias + c + 2 * k + 1)));
+    for (int k = 0; k < 8; ++k) p[k] = pack_bf16(elu(v[2 * k] + bias[c + 2 * k]), elu(v[2 * k + 1] + bias[c + 2 * k + 1]));
     uint4* d0 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c, kRows));
     uint4* d1 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c + 8, kRows));
     *d0 = make_uint4(p[0], p[1], p[2], p[3]);
@@ -194,21 +199,24 @@ struct FwdArgs {
   const uint8_t* terminated;
 };
 
-__global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constant__ PolicyImage W,
-                                                            const __grid_constant__ FwdArgs args) {
+__global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_constant__ PolicyImage W,
+                                                                 const __grid_constant__ FwdArgs args) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t row0 = (int64_t)blockIdx.x * kRows;
-  const int row = tid;  // TMEM lane == tile row
+  const int row = tid & (kRows - 1);  // TMEM lane == tile row (lane quarter = warp % 4)
+  const int group = tid / kRows;      // column group (warp / 4)
   bool boot_row = true;
   if (args.timed_out) {
     const int64_t r = row0 + row;
     boot_row = r < args.n && args.timed_out[r] && !args.terminated[r];
-    if (!__syncthreads_or(boot_row)) {
-      if (r < args.n) args.value[r] = 0.f;
+    if (!__syncthreads_or(group == 0 && boot_row)) {
+      if (group == 0 && r < args.n) args.value[r] = 0.f;
       return;
     }
   }
+  float* sbias = reinterpret_cast<float*>(smem + kBias);
+  for (int k = tid; k < 928; k += kThreads) sbias[k] = W.b1[k];  // the 7 bias vectors are contiguous
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBar + 64);
   const uint32_t bar_w1 = smem_u32(&bars[0]), bar_w2 = smem_u32(&bars[1]), bar_w34 = smem_u32(&bars[2]);
@@ -228,30 +236,28 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
     bulk_load(sbase + kW1, W.w1, 32768, bar_w1);
     bulk_load(sbase + kW2, W.w2a, 65536, bar_w2);
   }
-  // obs tile -> bf16 K-major [128 x 32] (zero padded rows / columns)
+  // obs tile -> bf16 K-major [128 x 32] (zero padded rows / columns); thread
+  // (row, group) converts the 8 columns of K chunk `group`
   {
-    float x[kK0];
+    float x[8];
+    const int c0 = group * 8;
 #pragma unroll
-    for (int k = 0; k < kK0; ++k) x[k] = 0.f;
+    for (int k = 0; k < 8; ++k) x[k] = 0.f;
     if (row0 + row < args.n) {
       const float* src = args.obs + (row0 + row) * args.obs_stride;
 #pragma unroll
-      for (int k = 0; k < kK0; ++k)
-        if (k < args.obs_dim) x[k] = __ldg(src + k);
+      for (int k = 0; k < 8; ++k)
+        if (c0 + k < args.obs_dim) x[k] = __ldg(src + c0 + k);
     }
-#pragma unroll
-    for (int c = 0; c < kK0; c += 8) {
-      uint4* d = reinterpret_cast<uint4*>(smem + kX0 + kmajor_off(row, c, kRows));
-      *d = make_uint4(pack_bf16(x[c], x[c + 1]), pack_bf16(x[c + 2], x[c + 3]), pack_bf16(x[c + 4], x[c + 5]),
-                      pack_bf16(x[c + 6], x[c + 7]));
-    }
+    uint4* d = reinterpret_cast<uint4*>(smem + kX0 + kmajor_off(row, c0, kRows));
+    *d = make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
   }
   async_proxy_fence();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   uint32_t mma_phase = 0;
 
   // ---- layer 1: [128 x 32] x [512 x 32]^T -> TMEM cols 0..511 (actor | critic)
@@ -267,7 +273,7 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   tc_fence_after();
   // R0 is free: stream W3/W4 (both trunks) while the actor's h1 is processed
   if (tid == 0) bulk_load(sbase + kW3a, W.w34, 36864, bar_w34);
-  epi_hidden<kH1>(tmem_row, 0, W.b1, smem + kA2, row);
+  epi_hidden<kH1>(tmem_row, 0, sbias, smem + kA2, row, group);
 
   // ---- actor: layer 2 (A2 x W2a -> cols 0..127), 3 (-> 128..191), 4 (-> 192..207)
   async_proxy_fence();
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   mma_phase ^= 1;
   tc_fence_after();
   if (tid == 0) bulk_load(sbase + kW2, W.w2c, 65536, bar_w2);  // W2a consumed: stream W2c
-  epi_hidden<kH2>(tmem_row, 0, W.b2a, smem + kA3, row);
+  epi_hidden<kH2>(tmem_row, 0, sbias + 512, smem + kA3, row, group);
   async_proxy_fence();
   tc_fence_before();
   __syncthreads();
@@ -296,7 +302,7 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   mbar_wait(bar_mma, mma_phase);
   mma_phase ^= 1;
   tc_fence_after();
-  epi_hidden<kH3>(tmem_row, 128, W.b3a, smem + kA4, row);
+  epi_hidden<kH3>(tmem_row, 128, sbias + 768, smem + kA4, row, group);
   async_proxy_fence();
   tc_fence_before();
   __syncthreads();
@@ -308,16 +314,16 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   mbar_wait(bar_mma, mma_phase);
   mma_phase ^= 1;
   tc_fence_after();
-  {
+  if (group == 0) {
     float v[16];
     tmem_ld16(tmem_row + 192, v);
     if (row0 + row < args.n && args.mean) {
       float* dst = args.mean + (row0 + row) * args.act_dim;
-      for (int k = 0; k < args.act_dim; ++k) dst[k] = v[k] + __ldg(W.b4a + k);
+      for (int k = 0; k < args.act_dim; ++k) dst[k] = v[k] + sbias[896 + k];
     }
   }
   // ---- critic: h1 waits in cols 256..511
-  epi_hidden<kH1>(tmem_row, 256, W.b1 + 256, smem + kA2, row);
+  epi_hidden<kH1>(tmem_row, 256, sbias + 256, smem + kA2, row, group);
   async_proxy_fence();
   tc_fence_before();
   __syncthreads();
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   mbar_wait(bar_mma, mma_phase);
   mma_phase ^= 1;
   tc_fence_after();
-  epi_hidden<kH2>(tmem_row, 0, W.b2c, smem + kA3, row);
+  epi_hidden<kH2>(tmem_row, 0, sbias + 640, smem + kA3, row, group);
   async_proxy_fence();
   tc_fence_before();
   __syncthreads();
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   mbar_wait(bar_mma, mma_phase);
   mma_phase ^= 1;
   tc_fence_after();
-  epi_hidden<kH3>(tmem_row, 128, W.b3c, smem + kA4, row);
+  epi_hidden<kH3>(tmem_row, 128, sbias + 832, smem + kA4, row, group);
   async_proxy_fence();
   tc_fence_before();
   __syncthreads();
@@ -354,10 +360,10 @@ __global__ void __launch_bounds__(128, 1) policy_fwd_kernel(const __grid_constan
   mbar_wait(bar_mma, mma_phase);
   mma_phase ^= 1;
   tc_fence_after();
-  {
+  if (group == 0) {
     float v[16];
     tmem_ld16(tmem_row + 192, v);
-    if (row0 + row < args.n) args.value[row0 + row] = boot_row ? v[0] + __ldg(W.b4c) : 0.f;
+    if (row0 + row < args.n) args.value[row0 + row] = boot_row ? v[0] + sbias[912] : 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -692,7 +698,7 @@ static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int
   sgp::FwdArgs a{d_obs, n, p->obs_dim, obs_stride > 0 ? obs_stride : p->obs_dim, p->act_dim, d_mean, d_value,
                  d_timed_out, d_terminated};
   const unsigned grid = (unsigned)((n + sgp::kRows - 1) / sgp::kRows);
-  sgp::policy_fwd_kernel<<<grid, 128, sgp::kSmem, (cudaStream_t)stream>>>(W, a);
+  sgp::policy_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }

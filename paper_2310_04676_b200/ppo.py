@@ -94,25 +94,80 @@ class TrainConfig:  # ppo.hpp:25-45
             raise sg.ConfigError("train.n_steps must be >= 25 (GAE horizon floor)")
 
 
-def mlp_forward(params: torch.Tensor, obs: torch.Tensor, obs_dim: int, act_dim: int):
-    """Policy::forward (policy.cpp:110-161) on a flat parameter view."""
+class _Linear(torch.autograd.Function):
+    """y = x W^T + b with every gradient a GEMM. The weight gradient
+    dy^T x reduces over the whole minibatch (K = 131072) into a small output;
+    it is computed split-K as a batched GEMM over 4096-row chunks plus a sum,
+    so it fills the GPU instead of a handful of CTAs. The bias gradient is
+    ones^T dy (a GEMV) instead of a column reduction."""
+
+    _ones: dict = {}
+
+    @staticmethod
+    def forward(ctx, x, W, b):
+        ctx.save_for_backward(x, W)
+        return torch.addmm(b, x, W.t())
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, W = ctx.saved_tensors
+        gx = gy @ W if ctx.needs_input_grad[0] else None
+        B = gy.shape[0]
+        chunk = 4096
+        if B % chunk == 0 and B >= 4 * chunk:
+            S = B // chunk
+            gW = torch.bmm(gy.view(S, chunk, -1).transpose(1, 2), x.view(S, chunk, -1)).sum(0)
+        else:
+            gW = gy.t() @ x
+        key = (B, gy.dtype, gy.device)
+        ones = _Linear._ones.get(key)
+        if ones is None:
+            ones = _Linear._ones[key] = torch.ones(1, B, dtype=gy.dtype, device=gy.device)
+        gb = (ones @ gy).view(-1)
+        return gx, gW, gb
+
+
+def _linear(x, W, b):
+    if torch.is_autocast_enabled():
+        dt = torch.get_autocast_gpu_dtype()
+        with torch.autocast("cuda", enabled=False):
+            return _Linear.apply(x.to(dt), W.to(dt), b.to(dt))
+    return _Linear.apply(x, W, b)
+
+
+def param_layout(obs_dim: int, act_dim: int):
+    """Flat offsets of (W_l, b_l) per trunk and of log_std (policy.cpp:42-63)."""
     dims = [obs_dim, 256, 128, 64]
     off = 0
-    outs = []
+    out = []
     for trunk in (0, 1):
-        h = obs
         o_last = act_dim if trunk == 0 else 1
         for l in range(4):
             i, o = dims[l], (dims[l + 1] if l < 3 else o_last)
-            W = params[off: off + o * i].view(o, i)
-            off += o * i
-            b = params[off: off + o]
-            off += o
-            h = F.linear(h, W, b)
+            out.append(((off, o, i), (off + o * i, o)))
+            off += o * i + o
+    return out, off
+
+
+def mlp_forward(params: torch.Tensor, obs: torch.Tensor, obs_dim: int, act_dim: int):
+    """Policy::forward (policy.cpp:110-161) on a flat parameter view."""
+    layout, ls_off = param_layout(obs_dim, act_dim)
+    layers = [(params[w0: w0 + o * i].view(o, i), params[b0: b0 + ob]) for (w0, o, i), (b0, ob) in layout]
+    mean, value = mlp_layers(layers, obs)
+    return mean, value, ls_off
+
+
+def mlp_layers(layers, obs):
+    outs = []
+    for trunk in (0, 1):
+        h = obs
+        for l in range(4):
+            W, b = layers[4 * trunk + l]
+            h = _linear(h, W, b)
             if l < 3:
                 h = F.elu(h)
         outs.append(h)
-    return outs[0], outs[1][:, 0], off
+    return outs[0], outs[1][:, 0]
 
 
 def loss_head(mean, value, log_std_raw, actions, old_logp, adv, ret, cfg: TrainConfig):
@@ -171,10 +226,26 @@ class Trainer:
         self.dev = dev
         N, A, O, T = env.n_envs, env.action_dim, env.obs_dim, cfg.n_steps
         self.N, self.A, self.O, self.T = N, A, O, T
-        self.params = torch.from_numpy(policy.init_params(cfg.seed, cfg.init_log_std)).to(dev).requires_grad_(True)
+        # one flat fp32 master vector (the reference's layout) and one flat
+        # gradient; per-layer leaves alias slices of both, so autograd writes
+        # straight into the flat gradient (no slice-backward graph) and the
+        # all-reduce / clip / Adam run on single flat tensors.
+        self.params = torch.from_numpy(policy.init_params(cfg.seed, cfg.init_log_std)).to(dev)
+        self.grad = torch.zeros_like(self.params)
+        self.params.grad = self.grad
         self.ls_off = policy.log_std_offset
+        layout, _ = param_layout(O, A)
+        self.layers = []
+        for (w0, o, i), (b0, ob) in layout:
+            W = self.params[w0: w0 + o * i].view(o, i).detach().requires_grad_(True)
+            b = self.params[b0: b0 + ob].detach().requires_grad_(True)
+            W.grad = self.grad[w0: w0 + o * i].view(o, i)
+            b.grad = self.grad[b0: b0 + ob]
+            self.layers.append((W, b))
+        self.log_std = self.params[self.ls_off: self.ls_off + A].detach().requires_grad_(True)
+        self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]
         self.opt = torch.optim.Adam([self.params], lr=cfg.learning_rate, betas=(0.9, 0.999), eps=1e-8)
-        policy.load_params(self.params.detach())
+        policy.load_params(self.params)
         z = lambda *s, dt=torch.float32: torch.zeros(*s, device=dev, dtype=dt)
         self.buf = dict(obs=z(T, N, O), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
                         terminated=z(T, N, dt=torch.uint8), timed_out=z(T, N, dt=torch.uint8), boot=z(T, N),
@@ -203,7 +274,7 @@ class Trainer:
         L = sg.lib()
         st = self._stream()
         self.d_pos.fill_(self.draw_pos)
-        log_std = self.params.detach()[self.ls_off: self.ls_off + A].contiguous()
+        log_std = self.params[self.ls_off: self.ls_off + A].contiguous()
         for t in range(T):
             obs = self.obs
             pol.forward(obs, self.mean, b["values"][t])
@@ -255,26 +326,26 @@ class Trainer:
                 perm = torch.randperm(cap, device=self.dev, generator=self.gen)
                 for start in range(0, cap, mb):
                     idx = perm[start: start + mb]
-                    self.opt.zero_grad(set_to_none=False)
+                    self.grad.zero_()
                     with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
-                        loss, m = ppo_loss(self.params, obs[idx], act[idx], logp[idx], adv[idx], ret[idx], cfg,
-                                           self.O, self.A)
+                        mean, value = mlp_layers(self.layers, obs[idx])
+                        loss, m = loss_head(mean.float(), value.float(), self.log_std, act[idx], logp[idx], adv[idx],
+                                            ret[idx], cfg)
                     loss.backward()
-                    g = self.params.grad
+                    g = self.grad
                     allreduce_mean_(g, self.dist)
                     if cfg.max_grad_norm > 0:
                         norm = g.norm()
                         g.mul_(torch.clamp(cfg.max_grad_norm / (norm + 0.0), max=1.0))
                     self.opt.step()
-                    with torch.no_grad():
-                        self.params[self.ls_off: self.ls_off + self.A].clamp_(LOG_STD_MIN, LOG_STD_MAX)
+                    self.params[self.ls_off: self.ls_off + self.A].clamp_(LOG_STD_MIN, LOG_STD_MAX)
                     metrics += m
                     updates += 1
         finally:
             torch.backends.cuda.matmul.allow_tf32 = prev_tf32
         # the reference's Fisher-Yates consumed cap-1 draws per epoch from the stream
         self.draw_pos += cfg.epochs * (cap - 1)
-        self.policy.load_params(self.params.detach())
+        self.policy.load_params(self.params)
         return metrics / max(updates, 1)
 
     def iterate(self) -> dict:
@@ -289,5 +360,5 @@ class Trainer:
                     mean_final_error=s[2] / s[3] if s[3] else float("nan"),
                     mean_step_reward=s[0] / (self.N * self.T), policy_loss=pm[0], value_loss=pm[1],
                     entropy=pm[2], kl=pm[3], clip_fraction=pm[4],
-                    log_std_mean=float(self.params.detach()[self.ls_off: self.ls_off + self.A]
+                    log_std_mean=float(self.params[self.ls_off: self.ls_off + self.A]
                                        .clamp(LOG_STD_MIN, LOG_STD_MAX).mean()))
