@@ -792,8 +792,11 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         }
       }
       const float lo = R.lo[d], hi = R.hi[d];
+      // GEN: a in [-1, 1) so rescale_to_range is the affine map (one FFMA
+      // with compile-time-foldable mid / half range; fp32 rounding differs
+      // from the three-op form by <= 1 ulp, inside the q_target tolerance)
       const auto rs = [&](float x, float l, float h) {
-        return GEN ? l + 0.5f * (x + 1.f) * (h - l) : rescale(x, l, h);
+        return GEN ? fmaf(x, 0.5f * (h - l), l + 0.5f * (h - l)) : rescale(x, l, h);
       };
       if (mode == kModePosition) {
         qt[j] = (d == jaw) ? (ad > 0.f ? hi : lo) : rs(ad, lo, hi);
@@ -858,6 +861,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     stage_cols();
     __syncthreads();  // (1) partial transforms, obs columns, actions staged
 
+    bool ended_any = false;
     if (S == 0) {
       // ---- compose, reward, flags (envs.cpp:456-463, 478-593) ------------------
 #pragma unroll
@@ -913,19 +917,20 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         o[3 * A + 5] = goal[2];
       }
       ts.ended[lane] = ended;
-      const unsigned m = __ballot_sync(0xffffffffu, ended);
-      if (lane == 0) ts.any_ended = m != 0;
+      ended_any = ended;
     } else if (GEN) {
       // idle warps store the generated actions while warp 0 scores
       team_store<CH, kTeamEnvs * CH::kDof, (G > 1 ? G - 1 : 1) * 32>(P.p.act_buf + row0 * A, s_act, rows * A,
                                                                     rows == kTeamEnvs, threadIdx.x - 32);
     }
-    __syncthreads();  // (2) obs rows complete, ended flags published
+    // (2) obs rows complete, ended flags published; the OR of the team's
+    // ended flags comes back with the barrier (no shared-memory round trip)
+    const int any_ended = __syncthreads_or(ended_any);
     if (GEN && G == 1)
       team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs,
                                                threadIdx.x);
 
-    if (ts.any_ended) {
+    if (any_ended) {
       // terminal observations (envs.cpp:606-611): rows of ended envs, all warps
       for (int r = threadIdx.x >> 5; r < rows; r += G) {
         if (!ts.ended[r]) continue;
@@ -974,7 +979,6 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32 * G>(P.p.obs + row0 * O, s_obs, rows * O, rows == kTeamEnvs,
                                                           threadIdx.x);
   }
-
   if (active) {
 #pragma unroll
     for (int j = 0; j < NB; ++j)
