@@ -253,7 +253,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="psm", choices=sorted(CONFIGS))
     ap.add_argument("--fuse", type=int, default=250, help="steps per fused launch")
-    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=400)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--update-precision", default="tf32", choices=["fp32", "tf32", "bf16"])
@@ -371,16 +371,26 @@ def main():
         if dist:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        # the timed region spans a synchronized reset burst (every 300 steps),
+        # so the conditional terminal-observation copy is exercised
         for s in range(E):
             env.step_host_ptr(h_act[s].data_ptr(), hr)
+            if s == 0:
+                ended0 = env.host_counters()[0]
+                e0.record()
         e1.record()
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
+        E -= 1
+        burst_steps = -(-(env.host_counters()[0] - ended0) // n)
         e2e_ms = max_over_ranks(e2e_ms, dist, f"cuda:{local}")
-        d2h = sum(t.numel() * t.element_size() for t in outs.values()) + 8
+        tobs_b = outs["terminal_observations"].numel() * 4
+        d2h = sum(t.numel() * t.element_size() for k2, t in outs.items() if k2 != "terminal_observations") + 16
+        d2h += tobs_b * burst_steps / max(E, 1)
         e2e = dict(value=world * n * E / (e2e_ms * 1e-3), unit="env-steps/s", h2d_bytes_per_step=n * A * 4,
-                   d2h_bytes_per_step=d2h, steps=E, path="sg_env_step_host (C-ABI), 1 launch/step")
+                   d2h_bytes_per_step=d2h, steps=E, reset_burst_steps=burst_steps,
+                   path="sg_env_step_host (C-ABI), 1 launch/step; terminal observations copied on steps "
+                        "where rows ended")
 
     # ---- per-step API in a CUDA graph (1 launch per step, no fusion) --------
     single = None

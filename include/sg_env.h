@@ -188,9 +188,14 @@ int sg_env_reset(sg_env* env, sg_step_views* out);
 /* d_actions: device, row-major n_envs x action_dim fp32 (stride = action_dim). */
 int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out);
 /* Host actions (pinned or pageable): H2D copy, step, D2H copy of the fields
- * requested in `out`, synchronise, report errors. */
+ * requested in `out`, synchronise, report errors. terminal_observations is
+ * copied only on steps where at least one row ended (it is defined on ended
+ * rows only); otherwise the host buffer is left untouched. */
 int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out);
 int sg_env_task_error(const sg_env* env, float** d_task_error);
+/* Running totals observed by the last sg_env_step_host (host side, no sync):
+ * rows that ended (terminated or timed out) and saturated action entries. */
+int sg_env_host_counters(const sg_env* env, uint64_t* ended_rows_total, uint64_t* saturations_total);
 int sg_env_state(const sg_env* env, sg_state_views* out);
 /* Waits for the env stream and converts the device error word. */
 int sg_env_synchronize(sg_env* env);

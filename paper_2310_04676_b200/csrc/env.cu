@@ -238,15 +238,18 @@ struct sg_env {
   std::vector<std::pair<std::string, std::pair<int, int>>> layout;
   float* d_actions_in = nullptr;  // staging for sg_env_step_host
   unsigned long long last_sat = 0;
+  unsigned long long last_ended = 0;
+  unsigned long long* h_counters = nullptr;  // pinned {sat_total, ended_total}
   bool bench_ready = false;
 
   ~sg_env() {
     cudaSetDevice(device);
     cudaStreamSynchronize(stream);
+    if (h_counters) cudaFreeHost(h_counters);
     const auto& p = P.p;
     void* bufs[] = {p.q,   p.qd,       p.qt,         p.goals,      p.tips,     p.step_count, p.hold_count,
                     p.episode_count, p.wp_idx,     p.wp_len,     p.wps,      p.rng_state,  p.rng_inc,
-                    p.obs, p.tobs,     p.rewards,    p.task_error, p.terminated, p.timed_out, p.sat_total,
+                    p.obs, p.tobs,     p.rewards,    p.task_error, p.terminated, p.timed_out, p.sat_total, p.ended_total,
                     p.err, p.act_state, p.act_buf, d_actions_in};
     for (void* b : bufs)
       if (b) cudaFree(b);
@@ -493,6 +496,7 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   p.terminated = dalloc<uint8_t>(n);
   p.timed_out = dalloc<uint8_t>(n);
   p.sat_total = dalloc<unsigned long long>(1);
+  p.ended_total = dalloc<unsigned long long>(1);
   p.err = dalloc<int32_t>(1);
   p.act_state = nullptr;
   p.act_buf = nullptr;
@@ -641,29 +645,43 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
     const int64_t n = env->n;
     const int O = env->O;
     auto& s = env->stream;
+    if (!env->h_counters) CK(cudaMallocHost(&env->h_counters, 2 * sizeof(unsigned long long)));
     CK(cudaMemcpyAsync(env->d_actions_in, h_actions, n * env->A * sizeof(float), cudaMemcpyHostToDevice, s));
     env->P.actions = env->d_actions_in;
     env->P.actions_aligned = 1;
+    const auto& p = env->P.p;
+    CK(cudaMemsetAsync(p.ended_total, 0, sizeof(unsigned long long), s));  // rows ended in THIS step
     env->launch_step(1, false);
-    unsigned long long sat = 0;
     if (out) {
-      const auto& p = env->P.p;
       if (out->observations)
         CK(cudaMemcpyAsync(out->observations, p.obs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
-      if (out->terminal_observations)
-        CK(cudaMemcpyAsync(out->terminal_observations, p.tobs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
       if (out->rewards) CK(cudaMemcpyAsync(out->rewards, p.rewards, n * sizeof(float), cudaMemcpyDeviceToHost, s));
       if (out->task_error)
         CK(cudaMemcpyAsync(out->task_error, p.task_error, n * sizeof(float), cudaMemcpyDeviceToHost, s));
       if (out->terminated) CK(cudaMemcpyAsync(out->terminated, p.terminated, n, cudaMemcpyDeviceToHost, s));
       if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, p.timed_out, n, cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(&sat, p.sat_total, sizeof(sat), cudaMemcpyDeviceToHost, s));
     }
+    CK(cudaMemcpyAsync(&env->h_counters[0], p.sat_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&env->h_counters[1], p.ended_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     env->check();
+    const unsigned long long sat = env->h_counters[0], ended = env->h_counters[1];
+    // terminal_observations are only meaningful on ended rows (envs.hpp:87):
+    // copied only on steps where some row ended (1 step in 300 under random
+    // actions), which removes the largest D2H transfer from the other steps
+    if (out && out->terminal_observations && ended != 0)
+      CK(cudaMemcpy(out->terminal_observations, p.tobs, n * O * sizeof(float), cudaMemcpyDeviceToHost));
+    env->last_ended += ended;
     if (out) {
       out->action_saturations = static_cast<int64_t>(sat - env->last_sat);
       env->last_sat = sat;
     }
+  });
+}
+
+int sg_env_host_counters(const sg_env* env, uint64_t* ended_rows_total, uint64_t* saturations_total) {
+  return guard([&] {
+    if (ended_rows_total) *ended_rows_total = env->last_ended;
+    if (saturations_total) *saturations_total = env->last_sat;
   });
 }
 

@@ -107,6 +107,7 @@ struct EnvPtrs {
   uint8_t* terminated;
   uint8_t* timed_out;
   unsigned long long* sat_total;
+  unsigned long long* ended_total;  // running count of ended rows (host polls it)
   int32_t* err;
   // bench action stream (per-env PCG state positioned at the env's next draw)
   uint64_t* act_state;
@@ -931,6 +932,10 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
                                                threadIdx.x);
 
     if (any_ended) {
+      if (S == 0) {
+        const unsigned m = __ballot_sync(0xffffffffu, active && ts.ended[lane]);
+        if (lane == 0) atomicAdd(P.p.ended_total, (unsigned long long)__popc(m));
+      }
       // terminal observations (envs.cpp:606-611): rows of ended envs, all warps
       for (int r = threadIdx.x >> 5; r < rows; r += G) {
         if (!ts.ended[r]) continue;

@@ -103,6 +103,7 @@ _SIGS = {
     "sg_env_step": (C.c_int, [C.c_void_p, C.c_void_p, _P(StepViews)]),
     "sg_env_step_host": (C.c_int, [C.c_void_p, C.c_void_p, _P(HostResult)]),
     "sg_env_task_error": (C.c_int, [C.c_void_p, _P(C.c_void_p)]),
+    "sg_env_host_counters": (C.c_int, [C.c_void_p, _P(C.c_uint64), _P(C.c_uint64)]),
     "sg_env_state": (C.c_int, [C.c_void_p, _P(StateViews)]),
     "sg_env_synchronize": (C.c_int, [C.c_void_p]),
     "sg_env_bench_begin": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64]),
@@ -363,6 +364,12 @@ class VecTaskEnv:
     def step_host_ptr(self, actions_ptr: int, hr: HostResult) -> None:
         """Raw-pointer variant (pinned buffers) used by bench.py's e2e leg."""
         _check(lib().sg_env_step_host(self._h, actions_ptr, C.byref(hr)))
+
+    def host_counters(self) -> tuple[int, int]:
+        """(ended rows, saturated entries) seen by step_host so far."""
+        e, s_ = C.c_uint64(), C.c_uint64()
+        _check(lib().sg_env_host_counters(self._h, C.byref(e), C.byref(s_)))
+        return e.value, s_.value
 
     def task_error(self):
         p = C.c_void_p()

@@ -226,20 +226,30 @@ def test_sharded_rows_match_single_device(sg, oracle):
 
 
 def test_host_step_matches_device_step(sg, oracle):
+    """sg_env_step_host == sg_env_step; terminal observations reach the host on
+    every step where rows ended (episode_len 3 -> ends every third step)."""
     _cuda()
     n = 200
-    a = sg.VecTaskEnv(robots=("ecm",), n_envs=n, seed=8)
-    b = sg.VecTaskEnv(robots=("ecm",), n_envs=n, seed=8)
+    a = sg.VecTaskEnv(robots=("ecm",), n_envs=n, seed=8, episode_len=3)
+    b = sg.VecTaskEnv(robots=("ecm",), n_envs=n, seed=8, episode_len=3)
     a.reset(); b.reset()
     rng = np.random.default_rng(0)
-    for _ in range(5):
+    ends = 0
+    for _ in range(7):
         act = rng.uniform(-1.5, 1.5, size=(n, 6)).astype(np.float32)
         hr = a.step_host(act)
         dr = b.step(torch.from_numpy(act).cuda())
         torch.cuda.synchronize()
         np.testing.assert_array_equal(hr["observations"], dr.observations.cpu().numpy())
         np.testing.assert_array_equal(hr["rewards"], dr.rewards.cpu().numpy())
+        ended = (hr["terminated"] | hr["timed_out"]).astype(bool)
+        np.testing.assert_array_equal(ended, (dr.terminated | dr.timed_out).cpu().numpy().astype(bool))
+        if ended.any():
+            ends += 1
+            np.testing.assert_array_equal(hr["terminal_observations"][ended],
+                                          dr.terminal_observations.cpu().numpy()[ended])
         assert hr["action_saturations"] == int(((act < -1) | (act > 1)).sum())
+    assert ends == 2 and a.host_counters()[0] == 2 * n
 
 
 def test_nonfinite_action_is_sim_error(sg, oracle):
