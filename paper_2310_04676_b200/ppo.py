@@ -78,6 +78,7 @@ class TrainConfig:  # ppo.hpp:25-45
     timeout_bootstrap: bool = True
     seed: int = 0
     update_precision: str = "tf32"  # fp32 | tf32 | bf16 (autocast) for the update GEMMs
+    cuda_graph: bool = True  # capture the update in a CUDA graph (single rank)
 
     def validate(self):  # ppo.cpp:31-48 (subset relevant on device)
         if not 0.0 <= self.gamma <= 1.0:
@@ -244,8 +245,14 @@ class Trainer:
             self.layers.append((W, b))
         self.log_std = self.params[self.ls_off: self.ls_off + A].detach().requires_grad_(True)
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]
-        self.opt = torch.optim.Adam([self.params], lr=cfg.learning_rate, betas=(0.9, 0.999), eps=1e-8)
+        single = dist is None or not dist.is_initialized() or dist.get_world_size() == 1
+        self.use_graph = cfg.cuda_graph and single
+        self.opt = torch.optim.Adam([self.params], lr=cfg.learning_rate, betas=(0.9, 0.999), eps=1e-8,
+                                    capturable=self.use_graph)
         policy.load_params(self.params)
+        self.perms = torch.empty(cfg.epochs, T * N, dtype=torch.int64, device=dev)
+        self.g_metrics = torch.zeros(5, device=dev)
+        self.graph = None
         z = lambda *s, dt=torch.float32: torch.zeros(*s, device=dev, dtype=dt)
         self.buf = dict(obs=z(T, N, O), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
                         terminated=z(T, N, dt=torch.uint8), timed_out=z(T, N, dt=torch.uint8), boot=z(T, N),
@@ -310,43 +317,90 @@ class Trainer:
         b["adv"].sub_(mean).div_(std + 1e-8)
 
     # -- update ------------------------------------------------------------
-    def update(self):
+    def _update_body(self, perms: torch.Tensor, metrics: torch.Tensor):
+        """epochs x minibatches of ppo_update (ppo.cpp:157-224) on device
+        tensors only (no host synchronisation, so it can be graph-captured)."""
         cfg, b = self.cfg, self.buf
         cap = self.T * self.N
         mb = (cap + cfg.minibatch_count - 1) // cfg.minibatch_count
         obs = b["obs"].view(cap, self.O)
         act = b["actions"].view(cap, self.A)
         logp, adv, ret = b["logp"].view(cap), b["adv"].view(cap), b["ret"].view(cap)
+        for e in range(cfg.epochs):
+            for start in range(0, cap, mb):
+                idx = perms[e, start: start + mb]
+                self.grad.zero_()
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
+                    mean, value = mlp_layers(self.layers, obs.index_select(0, idx))
+                    loss, m = loss_head(mean.float(), value.float(), self.log_std, act.index_select(0, idx),
+                                        logp.index_select(0, idx), adv.index_select(0, idx),
+                                        ret.index_select(0, idx), cfg)
+                loss.backward()
+                g = self.grad
+                allreduce_mean_(g, self.dist)
+                if cfg.max_grad_norm > 0:  # global-norm clip without a host read
+                    g.mul_(torch.clamp(cfg.max_grad_norm / g.norm(), max=1.0))
+                self.opt.step()
+                self.params[self.ls_off: self.ls_off + self.A].clamp_(LOG_STD_MIN, LOG_STD_MAX)
+                metrics += m
+
+    def _new_perms(self) -> None:
+        cap = self.T * self.N
+        for e in range(self.cfg.epochs):
+            self.perms[e].copy_(torch.randperm(cap, device=self.dev, generator=self.gen))
+
+    def _capture_update(self) -> None:
+        """Capture the whole update (5 epochs x 4 minibatches: gathers, forward,
+        backward, clip, Adam, log-std clamp) in one CUDA graph so the host no
+        longer paces ~2000 small launches. Warm-up runs on saved copies of the
+        parameters / optimizer state, which are restored before training."""
+        saved_p = self.params.clone()
+        self.opt.step()  # materialise optimizer state (grad is zero here)
+        saved_state = {k: (v.clone() if torch.is_tensor(v) else v)
+                       for k, v in self.opt.state[self.params].items()}
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self._new_perms()
+            for _ in range(2):
+                self._update_body(self.perms, self.g_metrics)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._update_body(self.perms, self.g_metrics)
+        with torch.no_grad():
+            self.params.copy_(saved_p)
+            for k, v in saved_state.items():
+                if torch.is_tensor(v):
+                    self.opt.state[self.params][k].copy_(v)
+            # the materialising step above was the optimizer's first: the real
+            # first update must see t = 1 (Adam::step, ppo.cpp:56-64)
+            self.opt.state[self.params]["step"].zero_()
+        self.grad.zero_()
+
+    def update(self):
+        cfg = self.cfg
+        cap = self.T * self.N
         prev_tf32 = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = cfg.update_precision == "tf32"
-        metrics = torch.zeros(5, device=self.dev)
-        updates = 0
         try:
-            for _ in range(cfg.epochs):
-                perm = torch.randperm(cap, device=self.dev, generator=self.gen)
-                for start in range(0, cap, mb):
-                    idx = perm[start: start + mb]
-                    self.grad.zero_()
-                    with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
-                        mean, value = mlp_layers(self.layers, obs[idx])
-                        loss, m = loss_head(mean.float(), value.float(), self.log_std, act[idx], logp[idx], adv[idx],
-                                            ret[idx], cfg)
-                    loss.backward()
-                    g = self.grad
-                    allreduce_mean_(g, self.dist)
-                    if cfg.max_grad_norm > 0:
-                        norm = g.norm()
-                        g.mul_(torch.clamp(cfg.max_grad_norm / (norm + 0.0), max=1.0))
-                    self.opt.step()
-                    self.params[self.ls_off: self.ls_off + self.A].clamp_(LOG_STD_MIN, LOG_STD_MAX)
-                    metrics += m
-                    updates += 1
+            if self.use_graph:
+                if self.graph is None:
+                    self._capture_update()
+                self._new_perms()
+                self.g_metrics.zero_()
+                self.graph.replay()
+                metrics = self.g_metrics.clone()
+            else:
+                metrics = torch.zeros(5, device=self.dev)
+                self._new_perms()
+                self._update_body(self.perms, metrics)
         finally:
             torch.backends.cuda.matmul.allow_tf32 = prev_tf32
         # the reference's Fisher-Yates consumed cap-1 draws per epoch from the stream
         self.draw_pos += cfg.epochs * (cap - 1)
         self.policy.load_params(self.params)
-        return metrics / max(updates, 1)
+        return metrics / (cfg.epochs * cfg.minibatch_count)
 
     def iterate(self) -> dict:
         self.rollout()
