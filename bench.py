@@ -256,7 +256,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=400)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--update-precision", default="tf32", choices=["fp32", "tf32", "bf16"])
+    ap.add_argument("--update-precision", default="bf16", choices=["fp32", "tf32", "bf16"])
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:

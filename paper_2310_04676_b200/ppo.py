@@ -150,6 +150,40 @@ def param_layout(obs_dim: int, act_dim: int):
     return out, off
 
 
+def _up8(x: int) -> int:
+    return (x + 7) // 8 * 8
+
+
+def padded_layout(obs_dim: int, act_dim: int):
+    """Training copy of the parameters with GEMM-friendly shapes: the obs
+    width and the output widths padded to multiples of 8 (odd leading
+    dimensions such as 27 and 7 push cuBLAS onto 4-8x slower kernels; see
+    tools/gemm_probe.py). Padded weights / biases start at zero and receive
+    zero gradients (padded inputs are zero, padded outputs are unused), so
+    Adam keeps them at zero. Returns (layout, log_std offset, total size,
+    reference index -> padded index map)."""
+    import numpy as np
+    ref_layout, ls_ref = param_layout(obs_dim, act_dim)
+    dims_p = [_up8(obs_dim), 256, 128, 64]
+    layout = []
+    ref_to_pad = np.zeros(ls_ref + act_dim, dtype=np.int64)
+    off = 0
+    for k, ((w0, o, i), (b0, ob)) in enumerate(ref_layout):
+        l = k % 4
+        ip = dims_p[l]
+        op = _up8(o) if l == 3 else o
+        rows = np.arange(o)[:, None]
+        cols = np.arange(i)[None, :]
+        ref_to_pad[w0: w0 + o * i] = (off + rows * ip + cols).reshape(-1)
+        bo = off + op * ip
+        ref_to_pad[b0: b0 + ob] = bo + np.arange(ob)
+        layout.append(((off, op, ip), (bo, op)))
+        off = bo + op
+    ls_pad = off
+    ref_to_pad[ls_ref: ls_ref + act_dim] = ls_pad + np.arange(act_dim)
+    return layout, ls_pad, ls_pad + _up8(act_dim), ref_to_pad
+
+
 def mlp_forward(params: torch.Tensor, obs: torch.Tensor, obs_dim: int, act_dim: int):
     """Policy::forward (policy.cpp:110-161) on a flat parameter view."""
     layout, ls_off = param_layout(obs_dim, act_dim)
@@ -227,15 +261,20 @@ class Trainer:
         self.dev = dev
         N, A, O, T = env.n_envs, env.action_dim, env.obs_dim, cfg.n_steps
         self.N, self.A, self.O, self.T = N, A, O, T
-        # one flat fp32 master vector (the reference's layout) and one flat
-        # gradient; per-layer leaves alias slices of both, so autograd writes
-        # straight into the flat gradient (no slice-backward graph) and the
-        # all-reduce / clip / Adam run on single flat tensors.
-        self.params = torch.from_numpy(policy.init_params(cfg.seed, cfg.init_log_std)).to(dev)
+        # fp32 master parameters in the padded training layout (padded_layout)
+        # plus one flat gradient; per-layer leaves alias slices of both, so
+        # autograd writes straight into the flat gradient (no slice-backward
+        # graph) and the all-reduce / clip / Adam run on single flat tensors.
+        # The reference-layout vector the tensor-core kernel packs from is a
+        # gather of the master (self.ref_params).
+        layout, ls_pad, total, ref_to_pad = padded_layout(O, A)
+        self.ref_to_pad = torch.from_numpy(ref_to_pad).to(dev)
+        self.params = torch.zeros(total, device=dev)
+        self.params[self.ref_to_pad] = torch.from_numpy(policy.init_params(cfg.seed, cfg.init_log_std)).to(dev)
         self.grad = torch.zeros_like(self.params)
         self.params.grad = self.grad
-        self.ls_off = policy.log_std_offset
-        layout, _ = param_layout(O, A)
+        self.ls_off = ls_pad
+        self.O_pad = _up8(O)
         self.layers = []
         for (w0, o, i), (b0, ob) in layout:
             W = self.params[w0: w0 + o * i].view(o, i).detach().requires_grad_(True)
@@ -249,12 +288,12 @@ class Trainer:
         self.use_graph = cfg.cuda_graph and single
         self.opt = torch.optim.Adam([self.params], lr=cfg.learning_rate, betas=(0.9, 0.999), eps=1e-8,
                                     capturable=self.use_graph)
-        policy.load_params(self.params)
+        policy.load_params(self.ref_params())
         self.perms = torch.empty(cfg.epochs, T * N, dtype=torch.int64, device=dev)
         self.g_metrics = torch.zeros(5, device=dev)
         self.graph = None
         z = lambda *s, dt=torch.float32: torch.zeros(*s, device=dev, dtype=dt)
-        self.buf = dict(obs=z(T, N, O), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
+        self.buf = dict(obs=z(T, N, _up8(O)), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
                         terminated=z(T, N, dt=torch.uint8), timed_out=z(T, N, dt=torch.uint8), boot=z(T, N),
                         task_error=z(T, N), adv=z(T, N), ret=z(T, N), last_values=z(N))
         self.mean = z(N, A)
@@ -288,7 +327,7 @@ class Trainer:
             sg._pcheck(L.sg_policy_sample(self.mean.data_ptr(), N, A, log_std.data_ptr(), self.stream_state,
                                           self.stream_inc, self.d_pos.data_ptr(), 2 * t * N * A,
                                           b["actions"][t].data_ptr(), b["logp"][t].data_ptr(), st))
-            b["obs"][t].copy_(obs)
+            b["obs"][t][:, :self.O].copy_(obs)
             res = env.step(b["actions"][t])
             b["rewards"][t].copy_(res.rewards)
             b["terminated"][t].copy_(res.terminated)
@@ -317,13 +356,17 @@ class Trainer:
         b["adv"].sub_(mean).div_(std + 1e-8)
 
     # -- update ------------------------------------------------------------
+    def ref_params(self) -> torch.Tensor:
+        """The reference's flat parameter layout (policy.cpp:42-63), fp32."""
+        return self.params[self.ref_to_pad]
+
     def _update_body(self, perms: torch.Tensor, metrics: torch.Tensor):
         """epochs x minibatches of ppo_update (ppo.cpp:157-224) on device
         tensors only (no host synchronisation, so it can be graph-captured)."""
         cfg, b = self.cfg, self.buf
         cap = self.T * self.N
         mb = (cap + cfg.minibatch_count - 1) // cfg.minibatch_count
-        obs = b["obs"].view(cap, self.O)
+        obs = b["obs"].view(cap, self.O_pad)
         act = b["actions"].view(cap, self.A)
         logp, adv, ret = b["logp"].view(cap), b["adv"].view(cap), b["ret"].view(cap)
         for e in range(cfg.epochs):
@@ -332,7 +375,8 @@ class Trainer:
                 self.grad.zero_()
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
                     mean, value = mlp_layers(self.layers, obs.index_select(0, idx))
-                    loss, m = loss_head(mean.float(), value.float(), self.log_std, act.index_select(0, idx),
+                    loss, m = loss_head(mean[:, :self.A].float(), value.float(), self.log_std,
+                                        act.index_select(0, idx),
                                         logp.index_select(0, idx), adv.index_select(0, idx),
                                         ret.index_select(0, idx), cfg)
                 loss.backward()
@@ -399,7 +443,7 @@ class Trainer:
             torch.backends.cuda.matmul.allow_tf32 = prev_tf32
         # the reference's Fisher-Yates consumed cap-1 draws per epoch from the stream
         self.draw_pos += cfg.epochs * (cap - 1)
-        self.policy.load_params(self.params)
+        self.policy.load_params(self.ref_params())
         return metrics / (cfg.epochs * cfg.minibatch_count)
 
     def iterate(self) -> dict:

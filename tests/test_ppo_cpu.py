@@ -119,3 +119,30 @@ def test_gradient_and_advantage_reductions_two_ranks():
     assert g == [1.5] * 5
     allv = np.concatenate([np.arange(4), np.arange(4) + 10]).astype(np.float64)
     assert abs(mean - allv.mean()) < 1e-6 and abs(std - allv.std()) < 1e-5
+
+
+def test_padded_training_layout_is_equivalent():
+    """The padded training copy (odd widths rounded up to 8 for the GEMMs)
+    computes the same MLP as the reference layout, and padded entries get
+    zero gradient."""
+    torch.manual_seed(0)
+    O, A = 27, 7
+    _, ls_ref = ppo.param_layout(O, A)
+    flat = torch.randn(ls_ref + A, dtype=torch.float64)
+    layout, ls_pad, total, r2p = ppo.padded_layout(O, A)
+    r2p = torch.from_numpy(r2p)
+    assert len(set(r2p.tolist())) == r2p.numel()
+    pad = torch.zeros(total, dtype=torch.float64)
+    pad[r2p] = flat
+    obs = torch.randn(64, O, dtype=torch.float64)
+    m_ref, v_ref, _ = ppo.mlp_forward(flat, obs, O, A)
+    pad = pad.requires_grad_(True)
+    layers = [(pad[w0: w0 + o * i].view(o, i), pad[b0: b0 + ob]) for (w0, o, i), (b0, ob) in layout]
+    obs_p = torch.zeros(64, 32, dtype=torch.float64)
+    obs_p[:, :O] = obs
+    m_pad, v_pad = ppo.mlp_layers(layers, obs_p)
+    assert torch.allclose(m_pad[:, :A], m_ref, atol=1e-12) and torch.allclose(v_pad, v_ref, atol=1e-12)
+    (m_pad[:, :A].sum() + v_pad.sum()).backward()
+    mask = torch.ones(total, dtype=torch.bool)
+    mask[r2p] = False
+    assert pad.grad[mask].abs().max().item() == 0.0
