@@ -198,7 +198,7 @@ int team_warps_for(int chain) {
   const char* s = std::getenv("SG_TEAM_WARPS");
   int v = s ? std::atoi(s) : 2;
   if (chain < sg::kChainPsm) return v >= 2 ? 2 : 1;
-  return v >= 4 ? 4 : (v >= 2 ? 2 : 1);
+  return v >= 4 ? 4 : (v < 1 ? 1 : v);
 }
 
 template <typename F>

@@ -619,12 +619,21 @@ __device__ __forceinline__ void compose(Xform& a, const Xform& b) {  // a = a o 
 // DoF block of team warp S: [B, B + N). Blocks are contiguous; the remainder
 // DoFs go to the LAST warps so warp 0 (which also composes the transform and
 // scores the step) carries the fewest DoFs. Shared by host and device.
+#ifndef SG_REMAINDER_FIRST
 __host__ __device__ constexpr int dof_block_begin(int D, int G, int S) {
   return S * (D / G) + ((S - (G - D % G)) > 0 ? (S - (G - D % G)) : 0);
 }
 __host__ __device__ constexpr int dof_block_size(int D, int G, int S) {
   return D / G + (S >= G - D % G ? 1 : 0);
 }
+#else
+__host__ __device__ constexpr int dof_block_begin(int D, int G, int S) {
+  return S * (D / G) + (S < D % G ? S : D % G);
+}
+__host__ __device__ constexpr int dof_block_size(int D, int G, int S) {
+  return D / G + (S < D % G ? 1 : 0);
+}
+#endif
 
 template <class CH, int G, int S>
 struct Block {

@@ -34,6 +34,7 @@ inline cudaError_t launch_fixed(const StepParams& P, const LaunchArgs& a) {
   switch (a.team_warps) {
     case 1: return launch_team<CH, TASK, MODE, SUB, 1>(P, a.k_steps, a.gen, a.stream);
     case 2: return launch_team<CH, TASK, MODE, SUB, 2>(P, a.k_steps, a.gen, a.stream);
+    case 3: return launch_team<CH, TASK, MODE, SUB, 3>(P, a.k_steps, a.gen, a.stream);
     default: return launch_team<CH, TASK, MODE, SUB, 4>(P, a.k_steps, a.gen, a.stream);
   }
 }

@@ -143,8 +143,8 @@ def lib() -> C.CDLL:
     Raises if it cannot be built or loaded — there is no fallback path."""
     global _LIB
     if _LIB is None:
-        path = _build.LIB
-        if not os.path.exists(path) or os.environ.get("SG_REBUILD"):
+        path = os.environ.get("SG_LIB_PATH") or _build.LIB  # override: A/B experiments only
+        if path == _build.LIB and (not os.path.exists(path) or os.environ.get("SG_REBUILD")):
             _build.build()
         L = C.CDLL(path)
         for name, (res, args) in _SIGS.items():
