@@ -256,9 +256,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=400)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--envs", type=int, default=None,
+                    help="override envs per GPU (scaling studies; the headline uses the BASELINE config)")
     ap.add_argument("--update-precision", default="bf16", choices=["fp32", "tf32", "bf16"])
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.envs:
+        cfg["n_envs"] = args.envs
+        cfg["workload"] += f" [override: {args.envs} envs/GPU]"
     if args.steps is None:
         args.steps = 320 if args.config == "ppo" else 64000
 

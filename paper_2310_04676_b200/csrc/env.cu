@@ -191,12 +191,12 @@ sg::RobotTable build_table(const sg::RobotModel& m, double dt_sub, const std::ve
   return t;
 }
 
-// Warps per 32-env team (kernels.cuh env_step_kernel). Default 4 for the
-// specialised chains (enough warps per SM to hide latency at 16K envs), 2 for
-// the generic chains; SG_TEAM_WARPS overrides (tuning).
+// Warps per team (kernels.cuh env_step_kernel): measured best per chain at
+// the BASELINE sizes (PSM 16,384 envs: 3; ECM 65,536: 2; STAR 16,384: 3);
+// 2 for the generic chains. SG_TEAM_WARPS overrides (tuning, A/B).
 int team_warps_for(int chain) {
   const char* s = std::getenv("SG_TEAM_WARPS");
-  int v = s ? std::atoi(s) : 2;
+  int v = s ? std::atoi(s) : (chain == sg::kChainEcm ? 2 : 3);
   if (chain < sg::kChainPsm) return v >= 2 ? 2 : 1;
   return v >= 4 ? 4 : (v < 1 ? 1 : v);
 }
@@ -239,7 +239,8 @@ struct sg_env {
   float* d_actions_in = nullptr;  // staging for sg_env_step_host
   unsigned long long last_sat = 0;
   unsigned long long last_ended = 0;
-  unsigned long long* h_counters = nullptr;  // pinned {sat_total, ended_total}
+  unsigned long long* counters = nullptr;    // device {sat_total, ended_total, err, pad}
+  unsigned long long* h_counters = nullptr;  // pinned copy of `counters`
   bool bench_ready = false;
 
   ~sg_env() {
@@ -249,8 +250,8 @@ struct sg_env {
     const auto& p = P.p;
     void* bufs[] = {p.q,   p.qd,       p.qt,         p.goals,      p.tips,     p.step_count, p.hold_count,
                     p.episode_count, p.wp_idx,     p.wp_len,     p.wps,      p.rng_state,  p.rng_inc,
-                    p.obs, p.tobs,     p.rewards,    p.task_error, p.terminated, p.timed_out, p.sat_total, p.ended_total,
-                    p.err, p.act_state, p.act_buf, d_actions_in};
+                    p.obs, p.tobs,     p.rewards,    p.task_error, p.terminated, p.timed_out, counters,
+                    p.act_state, p.act_buf, d_actions_in};
     for (void* b : bufs)
       if (b) cudaFree(b);
   }
@@ -302,6 +303,9 @@ struct sg_env {
     CK(cudaStreamSynchronize(stream));
     int32_t err = 0;
     CK(cudaMemcpy(&err, P.p.err, sizeof(err), cudaMemcpyDeviceToHost));
+    raise(err);
+  }
+  void raise(int32_t err) {
     if (!err) return;
     CK(cudaMemset(P.p.err, 0, sizeof(int32_t)));
     if (err & sg::kErrNonFiniteAction) throw sg::SimError("dynamics.step: non-finite action entry");
@@ -495,9 +499,12 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   p.task_error = dalloc<float>(n);
   p.terminated = dalloc<uint8_t>(n);
   p.timed_out = dalloc<uint8_t>(n);
-  p.sat_total = dalloc<unsigned long long>(1);
-  p.ended_total = dalloc<unsigned long long>(1);
-  p.err = dalloc<int32_t>(1);
+  // the three device counters share one 32-byte block: one D2H per host step
+  env->counters = dalloc<unsigned long long>(4);
+  p.sat_total = env->counters;
+  p.ended_total = env->counters + 1;
+  p.err = reinterpret_cast<int32_t*>(env->counters + 2);
+  CK(cudaMallocHost(&env->h_counters, 4 * sizeof(unsigned long long)));
   p.act_state = nullptr;
   p.act_buf = nullptr;
   // SimBatch::create (dynamics.cpp:225-241): mid configuration at rest, stream
@@ -638,6 +645,19 @@ int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
   });
 }
 
+// Device alias of a host pointer the GPU can address directly (pinned memory
+// from cudaMallocHost / cudaHostAlloc / cudaHostRegister; under UVA the alias
+// equals the host address), or nullptr for pageable memory.
+static void* mapped_alias(const void* h) {
+  if (!h) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
   return guard([&] {
     if (!h_actions) throw sg::SimError("env.step: action shape mismatch");
@@ -645,30 +665,62 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
     const int64_t n = env->n;
     const int O = env->O;
     auto& s = env->stream;
-    if (!env->h_counters) CK(cudaMallocHost(&env->h_counters, 2 * sizeof(unsigned long long)));
-    CK(cudaMemcpyAsync(env->d_actions_in, h_actions, n * env->A * sizeof(float), cudaMemcpyHostToDevice, s));
-    env->P.actions = env->d_actions_in;
-    env->P.actions_aligned = 1;
-    const auto& p = env->P.p;
-    CK(cudaMemsetAsync(p.ended_total, 0, sizeof(unsigned long long), s));  // rows ended in THIS step
-    env->launch_step(1, false);
+    auto& p = env->P.p;
+    // Zero-copy when every buffer is pinned: the kernel reads the actions over
+    // PCIe and writes the StepResult rows straight into the caller's buffers
+    // (one launch, no copy-engine round trips). Pageable buffers: staged copies.
+    bool zc = true;
+    void* a_act = mapped_alias(h_actions);
+    zc &= a_act != nullptr;
+    float* host_f[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint8_t* host_u[2] = {nullptr, nullptr};
     if (out) {
-      if (out->observations)
-        CK(cudaMemcpyAsync(out->observations, p.obs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
-      if (out->rewards) CK(cudaMemcpyAsync(out->rewards, p.rewards, n * sizeof(float), cudaMemcpyDeviceToHost, s));
-      if (out->task_error)
-        CK(cudaMemcpyAsync(out->task_error, p.task_error, n * sizeof(float), cudaMemcpyDeviceToHost, s));
-      if (out->terminated) CK(cudaMemcpyAsync(out->terminated, p.terminated, n, cudaMemcpyDeviceToHost, s));
-      if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, p.timed_out, n, cudaMemcpyDeviceToHost, s));
+      float* const fs[4] = {out->observations, out->terminal_observations, out->rewards, out->task_error};
+      uint8_t* const us[2] = {out->terminated, out->timed_out};
+      for (int k = 0; k < 4 && zc; ++k)
+        if (fs[k]) zc &= (host_f[k] = static_cast<float*>(mapped_alias(fs[k]))) != nullptr;
+      for (int k = 0; k < 2 && zc; ++k)
+        if (us[k]) zc &= (host_u[k] = static_cast<uint8_t*>(mapped_alias(us[k]))) != nullptr;
+      // obs rows are stored as float4 runs
+      zc &= (reinterpret_cast<uintptr_t>(host_f[0]) & 15u) == 0 && (reinterpret_cast<uintptr_t>(host_f[1]) & 15u) == 0;
     }
-    CK(cudaMemcpyAsync(&env->h_counters[0], p.sat_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&env->h_counters[1], p.ended_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    env->check();
+    CK(cudaMemsetAsync(p.ended_total, 0, sizeof(unsigned long long), s));  // rows ended in THIS step
+    if (zc) {
+      env->P.actions = static_cast<const float*>(a_act);
+      env->P.actions_aligned = (reinterpret_cast<uintptr_t>(a_act) & 15u) == 0;
+      p.h_obs = host_f[0];
+      p.h_tobs = host_f[1];
+      p.h_rewards = host_f[2];
+      p.h_task_error = host_f[3];
+      p.h_terminated = host_u[0];
+      p.h_timed_out = host_u[1];
+      env->launch_step(1, false);
+      p.h_obs = p.h_tobs = p.h_rewards = p.h_task_error = nullptr;
+      p.h_terminated = p.h_timed_out = nullptr;
+    } else {
+      CK(cudaMemcpyAsync(env->d_actions_in, h_actions, n * env->A * sizeof(float), cudaMemcpyHostToDevice, s));
+      env->P.actions = env->d_actions_in;
+      env->P.actions_aligned = 1;
+      env->launch_step(1, false);
+      if (out) {
+        if (out->observations)
+          CK(cudaMemcpyAsync(out->observations, p.obs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
+        if (out->rewards) CK(cudaMemcpyAsync(out->rewards, p.rewards, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+        if (out->task_error)
+          CK(cudaMemcpyAsync(out->task_error, p.task_error, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+        if (out->terminated) CK(cudaMemcpyAsync(out->terminated, p.terminated, n, cudaMemcpyDeviceToHost, s));
+        if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, p.timed_out, n, cudaMemcpyDeviceToHost, s));
+      }
+    }
+    // {sat_total, ended_total, err} in one copy, then one synchronisation
+    CK(cudaMemcpyAsync(env->h_counters, env->counters, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     const unsigned long long sat = env->h_counters[0], ended = env->h_counters[1];
-    // terminal_observations are only meaningful on ended rows (envs.hpp:87):
-    // copied only on steps where some row ended (1 step in 300 under random
-    // actions), which removes the largest D2H transfer from the other steps
-    if (out && out->terminal_observations && ended != 0)
+    env->raise(static_cast<int32_t>(env->h_counters[2] & 0xffffffffu));
+    // terminal_observations are only meaningful on ended rows (envs.hpp:87);
+    // staged path: copied only on steps where some row ended (1 step in 300
+    // under random actions); zero-copy path: the kernel wrote the ended rows
+    if (!zc && out && out->terminal_observations && ended != 0)
       CK(cudaMemcpy(out->terminal_observations, p.tobs, n * O * sizeof(float), cudaMemcpyDeviceToHost));
     env->last_ended += ended;
     if (out) {
@@ -733,19 +785,20 @@ int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t g
     const uint64_t A = static_cast<uint64_t>(env->A);
     const uint64_t first_draw = static_cast<uint64_t>(first_step) * static_cast<uint64_t>(global_n) * A;
     env->P.bench.inc = r.inc;
+    // warp s draws DoFs [b0, e0) of each row: it keeps the state at draw
+    // first + g*A + b0, reads draw b0 + j by a j-advance, and moves on by
+    // global_n*A per step
+    pcg_jump(static_cast<uint64_t>(global_n) * A, r.inc, env->P.bench.jump_mult, env->P.bench.jump_add);
+    for (int j = 0; j < sg::kMaxDof; ++j) pcg_jump(j, r.inc, env->P.bench.pow_mult[j], env->P.bench.pow_add[j]);
     for (int s = 0; s < env->team_warps; ++s) {
       int b0, e0;
       env->warp_block(s, b0, e0);
-      // warp s draws DoFs [b0, e0) of each row: start at draw first + g*A + b0,
-      // then advance global_n*A - (e0-b0) per step
       const int bs = 128;
       const unsigned grid = static_cast<unsigned>((env->n + bs - 1) / bs);
       sg::bench_seed_kernel<<<grid, bs, 0, env->stream>>>(p.act_state + static_cast<size_t>(s) * env->n, env->n,
                                                           r.state, first_draw + static_cast<uint64_t>(b0),
                                                           env->cfg.row_offset, env->A, J);
       CK(cudaGetLastError());
-      pcg_jump(static_cast<uint64_t>(global_n) * A - static_cast<uint64_t>(e0 - b0), r.inc,
-               env->P.bench.jump_mult[s], env->P.bench.jump_add[s]);
     }
     env->bench_ready = true;
   });

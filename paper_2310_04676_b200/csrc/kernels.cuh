@@ -112,16 +112,30 @@ struct EnvPtrs {
   // bench action stream (per-env PCG state positioned at the env's next draw)
   uint64_t* act_state;
   float* act_buf;  // [n][A]
+  // Host mirrors of the StepResult (caller-step path only, nullable): device
+  // aliases of the caller's pinned host buffers. The kernel writes each
+  // field there too, so the result crosses PCIe as the kernel's own posted
+  // stores (sg_env_step_host) instead of separate copies.
+  float* h_obs;
+  float* h_tobs;  // ended rows only
+  float* h_rewards;
+  float* h_task_error;
+  uint8_t* h_terminated;
+  uint8_t* h_timed_out;
 };
 
 constexpr int kMaxTeamWarps = 8;
 
 struct BenchStream {
   uint64_t inc;
-  // per team warp s: advance by global_n * A - N_s draws after the warp's N_s
-  // draws of one step (N_s = DoFs of the warp's block)
-  uint64_t jump_mult[kMaxTeamWarps];
-  uint64_t jump_add[kMaxTeamWarps];
+  // A team warp keeps the stream state s at its block's first draw of the
+  // step; draw j of the block is output(s advanced j times) = output(s *
+  // pow_mult[j] + pow_add[j]) (independent, no serial LCG chain), and the
+  // next step's first draw is s advanced by global_n * A (jump_*).
+  uint64_t jump_mult;
+  uint64_t jump_add;
+  uint64_t pow_mult[kMaxDof];
+  uint64_t pow_add[kMaxDof];
 };
 
 struct StepParams {
@@ -129,19 +143,23 @@ struct StepParams {
   TaskParams task;
   EnvPtrs p;
   BenchStream bench;
-  const float* actions;  // [n][A] row-major (non-bench path)
-  int32_t actions_aligned;
+  const float* actions;  // [n][A] row-major (non-bench path; device or mapped host memory)
+  int32_t actions_aligned;  // 16-byte aligned base: the team stages its rows with float4 loads
 };
 
 // ---------------------------------------------------------------------------
 // PCG32 (rng.hpp:25-83), fp64 draws without FMA contraction.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pcg_output(uint64_t old) {  // XSH-RR of the pre-advance state
+  const uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+  const uint32_t rot = static_cast<uint32_t>(old >> 59u);
+  return __funnelshift_r(xs, xs, rot);
+}
+
 __device__ __forceinline__ uint32_t pcg_next(uint64_t& s, uint64_t inc) {
   const uint64_t old = s;
   s = old * kPcgMult + inc;
-  const uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
-  const uint32_t rot = static_cast<uint32_t>(old >> 59u);
-  return (xs >> rot) | (xs << ((32u - rot) & 31u));
+  return pcg_output(old);
 }
 
 __device__ __forceinline__ double pcg_uniform(uint64_t& s, uint64_t inc, double lo, double hi) {
@@ -579,15 +597,16 @@ __device__ __forceinline__ float rescale(float x, float l, float h) {
 // terminal copy + masked reset + re-observe, k_steps steps per launch.
 //
 // Warp-specialised env teams. A CTA is one team of G warps that owns 32 envs
-// (lane = env); warp s of the team owns the contiguous DoF block
-// [s*P, (s+1)*P), P = ceil(D/G). Because the DoF block is warp-uniform, every
-// DoF index stays a compile-time constant inside the warp's code (FixedChain
-// joint structure is preserved) and there is no intra-warp divergence. Per
-// step each warp integrates its DoFs, composes the partial FK transform of its
-// joints, and stages its observation columns; warp 0 composes the partial
-// transforms (shared memory) into the tip, scores reward / hold / waypoint
-// advance / flags, and runs the out-of-line reset of ended envs. G multiplies
-// the warps per SM (16384 envs = 512 teams), which is what hides latency here.
+// (lane = env); warp s of the team owns a contiguous DoF block (dof_block_*).
+// Because the DoF block is warp-uniform, every DoF index stays a compile-time
+// constant inside the warp's code (FixedChain joint structure is preserved)
+// and there is no intra-warp divergence. Per step each warp integrates its
+// DoFs, builds the partial FK transform of its joints and stages its
+// observation columns; warp 0 (the scorer) turns the partial transforms into
+// the tip, scores reward / hold / waypoint advance / flags, resets ended envs
+// and stores the observation rows while the producer warps already run the
+// next step (team_run). G multiplies the warps per SM (16384 envs = 512
+// teams), which is what hides latency here.
 //
 //   CH    chain policy          TASK  kTaskTarget / kTaskPath, or -1 runtime
 //   G     warps per team        MODE  control mode, or -1 runtime
@@ -600,40 +619,38 @@ struct Xform {  // rigid transform (R row-major, p)
   float p[3];
 };
 
-__device__ __forceinline__ void compose(Xform& a, const Xform& b) {  // a = a o b
-  float t[9];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) t[r * 3 + c] = a.m[r * 3] * b.m[c] + a.m[r * 3 + 1] * b.m[3 + c] + a.m[r * 3 + 2] * b.m[6 + c];
-  const float p0 = a.p[0] + a.m[0] * b.p[0] + a.m[1] * b.p[1] + a.m[2] * b.p[2];
-  const float p1 = a.p[1] + a.m[3] * b.p[0] + a.m[4] * b.p[1] + a.m[5] * b.p[2];
-  const float p2 = a.p[2] + a.m[6] * b.p[0] + a.m[7] * b.p[1] + a.m[8] * b.p[2];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) a.m[k] = t[k];
-  a.p[0] = p0;
-  a.p[1] = p1;
-  a.p[2] = p2;
+// v <- p + m * v
+__device__ __forceinline__ void apply_xform(const float* m, const float* p, float (&v)[3]) {
+  const float v0 = p[0] + m[0] * v[0] + m[1] * v[1] + m[2] * v[2];
+  const float v1 = p[1] + m[3] * v[0] + m[4] * v[1] + m[5] * v[2];
+  const float v2 = p[2] + m[6] * v[0] + m[7] * v[1] + m[8] * v[2];
+  v[0] = v0;
+  v[1] = v1;
+  v[2] = v2;
 }
 
-// DoF block of team warp S: [B, B + N). Blocks are contiguous; the remainder
-// DoFs go to the LAST warps so warp 0 (which also composes the transform and
-// scores the step) carries the fewest DoFs. Shared by host and device.
-#ifndef SG_REMAINDER_FIRST
-__host__ __device__ constexpr int dof_block_begin(int D, int G, int S) {
-  return S * (D / G) + ((S - (G - D % G)) > 0 ? (S - (G - D % G)) : 0);
-}
-__host__ __device__ constexpr int dof_block_size(int D, int G, int S) {
-  return D / G + (S >= G - D % G ? 1 : 0);
-}
-#else
-__host__ __device__ constexpr int dof_block_begin(int D, int G, int S) {
-  return S * (D / G) + (S < D % G ? S : D % G);
-}
-__host__ __device__ constexpr int dof_block_size(int D, int G, int S) {
-  return D / G + (S < D % G ? 1 : 0);
-}
+// DoF block of team warp S: [B, B + N). Warp 0 (the scorer: tip, reward,
+// flags, resets, observation rows) takes scorer_dofs(D, G) DoFs; the others
+// are split contiguously over the producer warps 1..G-1, remainder to the
+// last ones. Shared by host (bench stream seeding) and device.
+#ifndef SG_SCORER_SHARE
+#define SG_SCORER_SHARE 1  // the scorer takes this many DoFs fewer than D / G (at least 1)
 #endif
+__host__ __device__ constexpr int scorer_dofs(int D, int G) {
+  return G == 1 ? D : (D / G - SG_SCORER_SHARE > 1 ? D / G - SG_SCORER_SHARE : 1);
+}
+__host__ __device__ constexpr int dof_block_begin(int D, int G, int S) {
+  return S == 0 ? 0
+                : scorer_dofs(D, G) + (S - 1) * ((D - scorer_dofs(D, G)) / (G - 1)) +
+                      ((S - 1) - ((G - 1) - (D - scorer_dofs(D, G)) % (G - 1)) > 0
+                           ? (S - 1) - ((G - 1) - (D - scorer_dofs(D, G)) % (G - 1))
+                           : 0);
+}
+__host__ __device__ constexpr int dof_block_size(int D, int G, int S) {
+  return S == 0 ? scorer_dofs(D, G)
+                : (D - scorer_dofs(D, G)) / (G - 1) +
+                      ((S - 1) >= (G - 1) - (D - scorer_dofs(D, G)) % (G - 1) ? 1 : 0);
+}
 
 template <class CH, int G, int S>
 struct Block {
@@ -668,13 +685,12 @@ __device__ __forceinline__ int tip_flags_of(const RobotTable& R) {
   else return R.tip_flags;
 }
 
-// Per-team shared memory (two buffers for obs / actions so step k+1 can stage
-// while step k is still being stored).
+// Per-team shared memory. Everything a step publishes is double-buffered by
+// step parity: producers stage step k+1 while the scorer still reads step k.
 template <int G>
 struct TeamSmem {
-  float xf[G][12][kTeamEnvs];  // partial transforms, lane-contiguous (conflict-free)
-  int32_t ended[kTeamEnvs];
-  int32_t any_ended;
+  float xf[2][G][12][kTeamEnvs];  // partial transforms, lane-contiguous (conflict-free)
+  int32_t ended[2][kTeamEnvs];    // rows that ended at the step of that parity
 };
 
 // Coalesced team store of `count` staged floats with 16-byte vectors. For a
@@ -703,6 +719,18 @@ __device__ __forceinline__ void team_store(float* __restrict__ g, const float* _
   }
 }
 
+// One team warp. Warp 0 is the SCORER, warps 1..G-1 are PRODUCERS. Per step k
+// every warp draws (or reads) its block's actions, integrates its DoFs,
+// builds its partial FK transform and stages its observation columns, then
+// all warps meet at ONE barrier B(k). After it, producers store the step's
+// action rows and go straight on to step k+1, while the scorer turns the
+// partial transforms into the tip, scores reward / hold / waypoint / flags,
+// copies terminal rows, resets ended envs (reset_row through HBM) and stores
+// the step's observation rows. Rows that ended at step k were reset by the
+// scorer while producers already advanced them to step k+1 from the stale
+// state: B(k+1) returns that fact (barrier OR), and producers redo step k+1
+// for those rows from the reset state with the same actions (one extra
+// barrier, one step in 300 under random actions).
 template <class CH, int G, int S, int TASK, int MODE, int SUB, bool GEN>
 __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float* s_obs_base, float* s_act_base,
                                          TeamSmem<G>& ts) {
@@ -726,19 +754,22 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   const auto has = [&](int j) { return Blk::N > 0 && (CH::kExact || B0 + j < A); };
 
   float q[NB], qd[NB], qt[NB];
+  const auto load_block = [&]() {
 #pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    q[j] = qd[j] = qt[j] = 0.f;
-    if (active && has(j)) {
-      q[j] = P.p.q[(B0 + j) * n + i];
-      qd[j] = P.p.qd[(B0 + j) * n + i];
-      qt[j] = P.p.qt[(B0 + j) * n + i];
+    for (int j = 0; j < NB; ++j) {
+      q[j] = qd[j] = qt[j] = 0.f;
+      if (active && has(j)) {
+        q[j] = P.p.q[(B0 + j) * n + i];
+        qd[j] = P.p.qd[(B0 + j) * n + i];
+        qt[j] = P.p.qt[(B0 + j) * n + i];
+      }
     }
-  }
-  // warp 0 owns the task state
+  };
+  load_block();
+  // the scorer owns the task state
   float goal[3] = {0.f, 0.f, 0.f}, tip[3] = {0.f, 0.f, 0.f};
   int32_t sc = 0, hc = 0, wi = 0, wl = 0;
-  if (S == 0 && active) {
+  const auto load_task = [&]() {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       goal[k] = P.p.goals[k * n + i];
@@ -750,38 +781,69 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       wi = P.p.wp_idx[i];
       wl = P.p.wp_len[i];
     }
-  }
+  };
+  if (S == 0 && active) load_task();
   uint64_t act_s = 0;
   if (GEN && active) act_s = P.p.act_state[(int64_t)S * n + i];
 
-  for (int step = 0; step < k_steps; ++step) {
-    float* s_obs = s_obs_base + (step & 1) * (kTeamEnvs * O);
-    float* s_act = s_act_base + (step & 1) * (kTeamEnvs * A + 4);
-    // ---- actions -----------------------------------------------------------
-    float a[NB];
-    if (GEN) {
+  // Position-control fast path (every specialised chain): the PD law with
+  // dt/inertia folded into the gains, u = (kp*qt - kp*q - kd*qd) * dt/I
+  // clamped to +-eff*dt/I (== clamp(tau) * dt/I), vv = qd*(1 - damping*dt/I) + u,
+  // and DoF pairs advanced with packed FFMA2 (fp32 rounding differs from the
+  // reference's operation order by a few ulp, inside the state tolerance).
+  constexpr bool kPd = CH::kExact && MODE == kModePosition && SUB > 0 && Blk::N > 0;
+  float gk[NB], gd[NB], gc[NB], ge[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int d = B0 + j < kMaxDof ? B0 + j : 0;
+    const float dti = R.dt_over_inertia[d];
+    gk[j] = R.kp[d] * dti;
+    gd[j] = R.kd[d] * dti;
+    gc[j] = 1.f - R.damping[d] * dti;
+    ge[j] = R.eff[d] * dti;
+  }
+
+  float a[NB];  // this step's actions (kept for a producer's redo)
+
+  // ---- actions: the bench stream (GEN) or the caller's rows ----------------
+  const auto draw = [&](float* s_act) {
+    if constexpr (GEN) {
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         a[j] = 0.f;
         if (active && has(j)) {
-          const uint32_t u = pcg_next(act_s, P.bench.inc);
+          const uint64_t st = j == 0 ? act_s : act_s * P.bench.pow_mult[j] + P.bench.pow_add[j];
+          const uint32_t u = pcg_output(st);
           // uniform(-1, 1) = -1 + 2 * (u * 2^-32) = (u - 2^31) * 2^-31: the exact
           // fp64 value of the reference (bench.cpp:34) rounded once to fp32
           a[j] = __int2float_rn((int32_t)(u ^ 0x80000000u)) * 0x1.0p-31f;
           s_act[lane * A + B0 + j] = a[j];
         }
       }
-      if (active) act_s = act_s * P.bench.jump_mult[S] + P.bench.jump_add[S];
+      if (active) act_s = act_s * P.bench.jump_mult + P.bench.jump_add;
     } else {
+      // the team's action rows are one contiguous run: coalesced (float4 when
+      // aligned) loads into shared memory, then each warp picks its DoFs (one
+      // pass over PCIe when the actions are in mapped host memory)
+      const float* src = P.actions + row0 * A;
+      const int cnt = rows * A;
+      if (P.actions_aligned) {
+        const int n4 = cnt >> 2;
+        for (int k = threadIdx.x; k < n4; k += 32 * G)
+          reinterpret_cast<float4*>(s_act)[k] = reinterpret_cast<const float4*>(src)[k];
+        for (int k = (n4 << 2) + threadIdx.x; k < cnt; k += 32 * G) s_act[k] = src[k];
+      } else {
+        for (int k = threadIdx.x; k < cnt; k += 32 * G) s_act[k] = src[k];
+      }
+      __syncthreads();
 #pragma unroll
-      for (int j = 0; j < NB; ++j) a[j] = (active && has(j)) ? __ldg(P.actions + i * A + B0 + j) : 0.f;
+      for (int j = 0; j < NB; ++j) a[j] = (active && has(j)) ? s_act[lane * A + B0 + j] : 0.f;
     }
+  };
 
-    // ---- dynamics (dynamics.cpp:133-185): substeps outer so the block's DoFs
-    // interleave; per-DoF operation order as in the reference -----------------
-    // Generated bench actions are finite and inside [-1, 1) by construction
-    // (no clamp, never saturate; rescale's a <= -1 branch yields lo exactly
-    // like the formula), so the GEN path skips those checks.
+  // ---- dynamics (dynamics.cpp:133-185) on this block; count: saturation /
+  // non-finite bookkeeping (warp-collective; false on a producer's redo) ------
+  const auto dynamics = [&](bool count) {
     int sat = 0, bad = 0;
     float v_target[NB], tau_cmd[NB], kpqt[NB];
     const int jaw = CH::jaw(R);
@@ -791,6 +853,9 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       v_target[j] = tau_cmd[j] = kpqt[j] = 0.f;
       if (!has(j)) continue;
       float ad = a[j];
+      // generated bench actions are finite and inside [-1, 1) by construction
+      // (never saturate; rescale's a <= -1 branch yields lo exactly like the
+      // formula), so the GEN path skips these checks
       if (!GEN) {
         if (!isfinite(ad)) {
           bad = 1;
@@ -802,15 +867,14 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         }
       }
       const float lo = R.lo[d], hi = R.hi[d];
-      // GEN: a in [-1, 1) so rescale_to_range is the affine map (one FFMA
-      // with compile-time-foldable mid / half range; fp32 rounding differs
-      // from the three-op form by <= 1 ulp, inside the q_target tolerance)
+      // GEN: a in [-1, 1) so rescale_to_range is the affine map (one FFMA;
+      // fp32 rounding differs from the three-op form by <= 1 ulp)
       const auto rs = [&](float x, float l, float h) {
         return GEN ? fmaf(x, 0.5f * (h - l), l + 0.5f * (h - l)) : rescale(x, l, h);
       };
       if (mode == kModePosition) {
         qt[j] = (d == jaw) ? (ad > 0.f ? hi : lo) : rs(ad, lo, hi);
-        kpqt[j] = R.kp[d] * qt[j];
+        kpqt[j] = (kPd ? gk[j] : R.kp[d]) * qt[j];
       } else if (mode == kModeVelocity) {
         v_target[j] = rs(ad, -R.vel[d], R.vel[d]);
       } else {
@@ -818,47 +882,95 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       }
     }
     const float dt = T.dt_sub;
-#pragma unroll(SUB > 0 ? SUB : 1)
-    for (int s = 0; s < substeps; ++s) {
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
+    if constexpr (kPd) {
+      const auto clampf = [](float x, float l, float h) { return fminf(fmaxf(x, l), h); };
+      const auto finish = [&](int j, float vv, float qq) {  // limit projection (velocity already limited)
         const int d = B0 + j;
-        if (!has(j)) continue;
-        const float ef = R.eff[d], vl = R.vel[d];
-        float tau;
-        if (mode == kModePosition) tau = fmaf(-R.kd[d], qd[j], fmaf(-R.kp[d], q[j], kpqt[j]));
-        else if (mode == kModeVelocity) tau = R.kd[d] * (v_target[j] - qd[j]);
-        else tau = tau_cmd[j];
-        tau = fminf(fmaxf(tau, -ef), ef);
-        float vv = qd[j] + (tau - R.damping[d] * qd[j]) * R.dt_over_inertia[d];
-        vv = fminf(fmaxf(vv, -vl), vl);
-        const float qq = q[j] + vv * dt;
-        const float qc = fminf(fmaxf(qq, R.lo[d]), R.hi[d]);  // limit projection
+        const float qc = clampf(qq, R.lo[d], R.hi[d]);
         qd[j] = qc != qq ? 0.f : vv;
         q[j] = qc;
+      };
+#pragma unroll
+      for (int s = 0; s < SUB; ++s) {
+#pragma unroll
+        for (int j = 0; j + 1 < NB; j += 2) {
+          const int d = B0 + j;
+          const float2 Q = make_float2(q[j], q[j + 1]), QD = make_float2(qd[j], qd[j + 1]);
+          float2 u = __ffma2_rn(make_float2(-gk[j], -gk[j + 1]), Q, make_float2(kpqt[j], kpqt[j + 1]));
+          u = __ffma2_rn(make_float2(-gd[j], -gd[j + 1]), QD, u);
+          u.x = clampf(u.x, -ge[j], ge[j]);
+          u.y = clampf(u.y, -ge[j + 1], ge[j + 1]);
+          float2 vv = __ffma2_rn(QD, make_float2(gc[j], gc[j + 1]), u);
+          vv.x = clampf(vv.x, -R.vel[d], R.vel[d]);
+          vv.y = clampf(vv.y, -R.vel[d + 1], R.vel[d + 1]);
+          const float2 qq = __ffma2_rn(vv, make_float2(dt, dt), Q);
+          finish(j, vv.x, qq.x);
+          finish(j + 1, vv.y, qq.y);
+        }
+        if constexpr (NB % 2 == 1) {
+          constexpr int j = NB - 1;
+          const int d = B0 + j;
+          float u = fmaf(-gd[j], qd[j], fmaf(-gk[j], q[j], kpqt[j]));
+          u = clampf(u, -ge[j], ge[j]);
+          const float vv = clampf(fmaf(qd[j], gc[j], u), -R.vel[d], R.vel[d]);
+          finish(j, vv, fmaf(vv, dt, q[j]));
+        }
+      }
+    } else {
+      // generic path: substeps outer so the block's DoFs interleave; per-DoF
+      // operation order as in the reference
+#pragma unroll(SUB > 0 ? SUB : 1)
+      for (int s = 0; s < substeps; ++s) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int d = B0 + j;
+          if (!has(j)) continue;
+          const float ef = R.eff[d], vl = R.vel[d];
+          float tau;
+          if (mode == kModePosition) tau = fmaf(-R.kd[d], qd[j], fmaf(-R.kp[d], q[j], kpqt[j]));
+          else if (mode == kModeVelocity) tau = R.kd[d] * (v_target[j] - qd[j]);
+          else tau = tau_cmd[j];
+          tau = fminf(fmaxf(tau, -ef), ef);
+          float vv = qd[j] + (tau - R.damping[d] * qd[j]) * R.dt_over_inertia[d];
+          vv = fminf(fmaxf(vv, -vl), vl);
+          const float qq = q[j] + vv * dt;
+          const float qc = fminf(fmaxf(qq, R.lo[d]), R.hi[d]);  // limit projection
+          qd[j] = qc != qq ? 0.f : vv;
+          q[j] = qc;
+        }
       }
     }
-    if (!GEN) {
+    if (!GEN && count) {
       if (!active) sat = bad = 0;
       const unsigned wsat = __reduce_add_sync(0xffffffffu, (unsigned)sat);
       if (wsat && lane == 0) atomicAdd(P.p.sat_total, (unsigned long long)wsat);
       if (__any_sync(0xffffffffu, bad) && bad) atomicOr(P.p.err, kErrNonFiniteAction);
     }
+  };
 
-    // ---- partial FK of this warp's joints; stage observation columns --------
-    Xform x;
+  // ---- partial FK of this block + publication ---------------------------------
+  // tip = T_0 o T_1 o ... o T_{G-1} (tip offset), evaluated right to left as
+  // matrix-vector products: the last warp publishes v = p + R * tip (3 floats;
+  // its final rotation is dead code when the tip offset is zero), middle warps
+  // publish (R, p), the scorer applies them to its own transform.
+  Xform x;
+  const auto publish = [&](int b, float* s_obs) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) x.m[k] = (k % 4 == 0) ? 1.f : 0.f;
     x.p[0] = x.p[1] = x.p[2] = 0.f;
     fk_range<CH, B0>(R, q, x, std::make_integer_sequence<int, Blk::N>{});
-    if (S > 0) {
+    if (S > 0 && S == G - 1) {
+      float v[3];
+      fk_tip_offset(R, tip_flags_of<CH>(R), x.m, x.p, v);
 #pragma unroll
-      for (int k = 0; k < 9; ++k) ts.xf[S][k][lane] = x.m[k];
+      for (int k = 0; k < 3; ++k) ts.xf[b][S][9 + k][lane] = v[k];
+    } else if (S > 0) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) ts.xf[S][9 + k][lane] = x.p[k];
+      for (int k = 0; k < 9; ++k) ts.xf[b][S][k][lane] = x.m[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ts.xf[b][S][9 + k][lane] = x.p[k];
     }
-    const auto stage_cols = [&]() {
-      if (!active) return;
+    if (active) {
       float* o = s_obs + lane * O;
 #pragma unroll
       for (int j = 0; j < NB; ++j)
@@ -867,25 +979,57 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
           o[A + B0 + j] = qd[j];
           o[2 * A + 3 + B0 + j] = qt[j];
         }
-    };
-    stage_cols();
-    __syncthreads();  // (1) partial transforms, obs columns, actions staged
+    }
+  };
 
-    bool ended_any = false;
-    if (S == 0) {
-      // ---- compose, reward, flags (envs.cpp:456-463, 478-593) ------------------
+  bool pend = false;  // scorer: rows ended (and were reset) at the previous step
+  for (int step = 0; step < k_steps; ++step) {
+    const int b = step & 1;
+    float* s_obs = s_obs_base + b * (kTeamEnvs * O);
+    float* s_act = s_act_base + b * (kTeamEnvs * A + 4);
+    draw(s_act);
+    dynamics(true);
+    publish(b, s_obs);
+    // B(step); its OR tells producers that the scorer reset rows of step-1
+    if (__syncthreads_or(S == 0 && pend)) {
+      if constexpr (S > 0) {
+        if (active && ts.ended[b ^ 1][lane]) {  // redo this step from the reset state
+          load_block();
+          dynamics(false);
+          publish(b, s_obs);
+        }
+      }
+      __syncthreads();
+    }
+
+    if constexpr (S > 0) {
+      // producers store the step's generated action rows, then move on
+      if (GEN)
+        team_store<CH, kTeamEnvs * CH::kDof, (G - 1) * 32>(P.p.act_buf + row0 * A, s_act, rows * A,
+                                                          rows == kTeamEnvs, threadIdx.x - 32);
+    } else {
+      // ---- scorer: tip, reward, flags (envs.cpp:456-463, 478-593) -----------
+      float v[3];
+      if constexpr (G == 1) {
+        fk_tip_offset(R, tip_flags_of<CH>(R), x.m, x.p, v);
+      } else {
 #pragma unroll
-      for (int s = 1; s < G; ++s) {
-        Xform y;
+        for (int k = 0; k < 3; ++k) v[k] = ts.xf[b][G - 1][9 + k][lane];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) y.m[k] = ts.xf[s][k][lane];
+        for (int s = G - 2; s >= 1; --s) {
+          float y[12];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) y.p[k] = ts.xf[s][9 + k][lane];
-        compose(x, y);
+          for (int k = 0; k < 12; ++k) y[k] = ts.xf[b][s][k][lane];
+          apply_xform(y, y + 9, v);
+        }
+        apply_xform(x.m, x.p, v);
       }
       bool ended = false;
+      float* o = s_obs + lane * O;
       if (active) {
-        fk_tip_offset(R, tip_flags_of<CH>(R), x.m, x.p, tip);
+        tip[0] = v[0];
+        tip[1] = v[1];
+        tip[2] = v[2];
         sc += 1;
         float reward, dist;
         bool goal_met;
@@ -917,8 +1061,13 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         P.p.task_error[i] = dist;
         P.p.terminated[i] = goal_met ? 1 : 0;
         P.p.timed_out[i] = timed_out ? 1 : 0;
+        if constexpr (!GEN) {
+          if (P.p.h_rewards) P.p.h_rewards[i] = reward;
+          if (P.p.h_task_error) P.p.h_task_error[i] = dist;
+          if (P.p.h_terminated) P.p.h_terminated[i] = goal_met ? 1 : 0;
+          if (P.p.h_timed_out) P.p.h_timed_out[i] = timed_out ? 1 : 0;
+        }
         ended = goal_met || timed_out;
-        float* o = s_obs + lane * O;
         o[2 * A + 0] = tip[0];
         o[2 * A + 1] = tip[1];
         o[2 * A + 2] = tip[2];
@@ -926,60 +1075,38 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         o[3 * A + 4] = goal[1];
         o[3 * A + 5] = goal[2];
       }
-      ts.ended[lane] = ended;
-      ended_any = ended;
-    } else if (GEN) {
-      // idle warps store the generated actions while warp 0 scores
-      team_store<CH, kTeamEnvs * CH::kDof, (G > 1 ? G - 1 : 1) * 32>(P.p.act_buf + row0 * A, s_act, rows * A,
-                                                                    rows == kTeamEnvs, threadIdx.x - 32);
-    }
-    // (2) obs rows complete, ended flags published; the OR of the team's
-    // ended flags comes back with the barrier (no shared-memory round trip)
-    const int any_ended = __syncthreads_or(ended_any);
-    if (GEN && G == 1)
-      team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs,
-                                               threadIdx.x);
-
-    if (any_ended) {
-      if (S == 0) {
-        const unsigned m = __ballot_sync(0xffffffffu, active && ts.ended[lane]);
-        if (lane == 0) atomicAdd(P.p.ended_total, (unsigned long long)__popc(m));
-      }
-      // terminal observations (envs.cpp:606-611): rows of ended envs, all warps
-      for (int r = threadIdx.x >> 5; r < rows; r += G) {
-        if (!ts.ended[r]) continue;
-        for (int k = lane; k < O; k += 32) P.p.tobs[(row0 + r) * O + k] = s_obs[r * O + k];
-      }
-      const bool mine = active && ts.ended[lane];
-      // reset_row (envs.cpp:304-360) through HBM, so any team warp can run it:
-      // lane l's reset goes to warp l % G (more independent fp64 streams)
-      if (mine && (lane % G) == S) {
-        const int e = reset_env<CH, TASK>(P, i);
-        if (e) atomicOr(P.p.err, e);
-      }
-      __syncthreads();  // (3) reset state in HBM, terminal rows copied
-      if (mine) {
-#pragma unroll
-        for (int j = 0; j < NB; ++j)
-          if (has(j)) {
-            q[j] = P.p.q[(B0 + j) * n + i];
-            qd[j] = P.p.qd[(B0 + j) * n + i];
-            qt[j] = P.p.qt[(B0 + j) * n + i];
+      ts.ended[b][lane] = ended;
+      const unsigned em = __ballot_sync(0xffffffffu, ended);
+      pend = em != 0;
+      if (pend) {
+        if (lane == 0) atomicAdd(P.p.ended_total, (unsigned long long)__popc(em));
+        __syncwarp();  // the row's staged columns and tip / goal are complete
+        // terminal observations (envs.cpp:606-611): the pre-reset rows
+        for (int r = 0; r < rows; ++r) {
+          if (!((em >> r) & 1u)) continue;
+          for (int k = lane; k < O; k += 32) {
+            P.p.tobs[(row0 + r) * O + k] = s_obs[r * O + k];
+            if constexpr (!GEN) {
+              if (P.p.h_tobs) P.p.h_tobs[(row0 + r) * O + k] = s_obs[r * O + k];
+            }
           }
-        stage_cols();
-        if (S == 0) {
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            goal[k] = P.p.goals[k * n + i];
-            tip[k] = P.p.tips[k * n + i];
-          }
-          if (task == kTaskPath) {
-            wi = P.p.wp_idx[i];
-            wl = P.p.wp_len[i];
-          }
+        }
+        __syncwarp();
+        if (ended) {
+          // reset_row (envs.cpp:304-360) through HBM, then the post-reset row
+          const int e = reset_env<CH, TASK>(P, i);
+          if (e) atomicOr(P.p.err, e);
+          load_block();
+          load_task();
           sc = 0;
           hc = 0;
-          float* o = s_obs + lane * O;
+#pragma unroll
+          for (int d = 0; d < CH::kDof; ++d)
+            if (CH::kExact || d < A) {
+              o[d] = P.p.q[d * n + i];
+              o[A + d] = P.p.qd[d * n + i];
+              o[2 * A + 3 + d] = P.p.qt[d * n + i];
+            }
           o[2 * A + 0] = tip[0];
           o[2 * A + 1] = tip[1];
           o[2 * A + 2] = tip[2];
@@ -988,19 +1115,32 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
           o[3 * A + 5] = goal[2];
         }
       }
-      __syncthreads();  // (4) re-observed rows staged
-    }
-    team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32 * G>(P.p.obs + row0 * O, s_obs, rows * O, rows == kTeamEnvs,
-                                                          threadIdx.x);
-  }
-  if (active) {
-#pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (has(j)) {
-        P.p.q[(B0 + j) * n + i] = q[j];
-        P.p.qd[(B0 + j) * n + i] = qd[j];
-        P.p.qt[(B0 + j) * n + i] = qt[j];
+      __syncwarp();
+      if constexpr (GEN && G == 1)
+        team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs, lane);
+      team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.obs + row0 * O, s_obs, rows * O, rows == kTeamEnvs,
+                                                         lane);
+      if constexpr (!GEN) {
+        if (P.p.h_obs)
+          team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.h_obs + row0 * O, s_obs, rows * O,
+                                                             rows == kTeamEnvs, lane);
       }
+    }
+  }
+  // producers learn which rows ended at the last step: their reset state is
+  // already in HBM and must not be overwritten with the stale registers
+  const bool fix = __syncthreads_or(S == 0 && pend);
+  const bool stale = S > 0 && fix && k_steps > 0 && ts.ended[(k_steps - 1) & 1][lane];
+  if (active) {
+    if (!stale) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (has(j)) {
+          P.p.q[(B0 + j) * n + i] = q[j];
+          P.p.qd[(B0 + j) * n + i] = qd[j];
+          P.p.qt[(B0 + j) * n + i] = qt[j];
+        }
+    }
     if (S == 0) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) {

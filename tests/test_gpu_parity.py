@@ -252,6 +252,56 @@ def test_host_step_matches_device_step(sg, oracle):
     assert ends == 2 and a.host_counters()[0] == 2 * n
 
 
+def _pinned_out(n, o, offset_bytes=0):
+    """StepResult host buffers in pinned memory (zero-copy path); offset_bytes
+    shifts the observation buffer off 16-byte alignment (staged-copy path)."""
+    def pin(shape, dt, extra=0):
+        count = int(np.prod(shape))
+        t = torch.empty(count * np.dtype(dt).itemsize + extra, dtype=torch.uint8).pin_memory()
+        return t[extra:].numpy().view(dt).reshape(shape)
+    return dict(observations=pin((n, o), np.float32, offset_bytes),
+                terminal_observations=pin((n, o), np.float32), rewards=pin((n,), np.float32),
+                task_error=pin((n,), np.float32), terminated=pin((n,), np.uint8), timed_out=pin((n,), np.uint8))
+
+
+@pytest.mark.parametrize("robot,n", [("psm", 16384), ("ecm", 1000), ("star", 77)])
+def test_host_step_zero_copy_matches_staged_and_device(sg, oracle, robot, n):
+    """Pinned host buffers (kernel reads actions / writes the StepResult over
+    PCIe) == pageable host buffers (staged copies) == the device step, bit for
+    bit, on every field and on every step of a reset burst (episode_len 4);
+    ragged team counts (n % 32 != 0) and a misaligned observation buffer."""
+    _cuda()
+    kw = dict(robots=(robot,), n_envs=n, seed=3, episode_len=4)
+    if robot == "star":
+        kw.update(task="path_following", goal_sigma=0.15)
+    envs = [sg.VecTaskEnv(**kw) for _ in range(4)]
+    for e in envs:
+        e.reset()
+    A, O = envs[0].action_dim, envs[0].obs_dim
+    rng = np.random.default_rng(1)
+    pinned_act = torch.empty((n, A), dtype=torch.float32).pin_memory()
+    outs = [_pinned_out(n, O), None, _pinned_out(n, O, offset_bytes=4)]
+    for s in range(9):
+        act = rng.uniform(-1.2, 1.2, size=(n, A)).astype(np.float32)
+        pinned_act.numpy()[:] = act
+        res = [envs[0].step_host(pinned_act.numpy(), outs[0]), envs[1].step_host(act),
+               envs[2].step_host(pinned_act.numpy(), outs[2])]
+        dr = envs[3].step(torch.from_numpy(act).cuda())
+        torch.cuda.synchronize()
+        ended = (dr.terminated | dr.timed_out).cpu().numpy().astype(bool)
+        dev = dict(observations=dr.observations, rewards=dr.rewards, task_error=dr.task_error,
+                   terminated=dr.terminated, timed_out=dr.timed_out)
+        for r in res:
+            for k, v in dev.items():
+                np.testing.assert_array_equal(r[k], v.cpu().numpy(), err_msg=f"{k} @{s}")
+            if ended.any():
+                np.testing.assert_array_equal(r["terminal_observations"][ended],
+                                              dr.terminal_observations.cpu().numpy()[ended])
+            assert r["action_saturations"] == int(((act < -1) | (act > 1)).sum())
+    assert envs[0].host_counters() == envs[1].host_counters() == envs[2].host_counters()
+    assert envs[0].host_counters()[0] == 2 * n
+
+
 def test_nonfinite_action_is_sim_error(sg, oracle):
     _cuda()
     env = sg.VecTaskEnv(robots=("psm",), n_envs=8)
