@@ -191,12 +191,12 @@ sg::RobotTable build_table(const sg::RobotModel& m, double dt_sub, const std::ve
   return t;
 }
 
-// Warps per team (kernels.cuh env_step_kernel): measured best per chain at
-// the BASELINE sizes (PSM 16,384 envs: 3; ECM 65,536: 2; STAR 16,384: 3);
-// 2 for the generic chains. SG_TEAM_WARPS overrides (tuning, A/B).
+// Warps per team (kernels.cuh env_step_kernel): 2 measured best for PSM
+// (16,384 envs), ECM (65,536) and STAR (16,384) alike (tools/ab.sh); the
+// generic chains use 2 as well. SG_TEAM_WARPS overrides (tuning, A/B).
 int team_warps_for(int chain) {
   const char* s = std::getenv("SG_TEAM_WARPS");
-  int v = s ? std::atoi(s) : (chain == sg::kChainEcm ? 2 : 3);
+  int v = s ? std::atoi(s) : 2;
   if (chain < sg::kChainPsm) return v >= 2 ? 2 : 1;
   return v >= 4 ? 4 : (v < 1 ? 1 : v);
 }

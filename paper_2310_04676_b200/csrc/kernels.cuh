@@ -358,6 +358,18 @@ __device__ __forceinline__ double dist3_rn(const double (&a)[3], const double (&
   return norm3_rn(__dadd_rn(a[0], -b[0]), __dadd_rn(a[1], -b[1]), __dadd_rn(a[2], -b[2]));
 }
 
+// Knot parameters t_k = k / 1000 of the chord table, correctly rounded at
+// compile time: a constant-cache broadcast instead of an fp64 division per point.
+struct SplineTTable {
+  double t[kSplineSubdiv + 1];
+};
+constexpr SplineTTable make_spline_t() {
+  SplineTTable r{};
+  for (int k = 0; k <= kSplineSubdiv; ++k) r.t[k] = static_cast<double>(k) / static_cast<double>(kSplineSubdiv);
+  return r;
+}
+static __constant__ SplineTTable kSplineT = make_spline_t();
+
 // sample_spline_waypoints (spline.cpp:40-72) in ONE pass over the 1001-point
 // chord table, without storing it: the cumulative sums are formed in the
 // reference's order, and the waypoint loop
@@ -380,7 +392,7 @@ static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, doub
   double cum_prev = 0.0, sv = spacing;
   double s_emit[2] = {0.0, 0.0};  // targets of the last two tentative emissions
   for (int k = 1; k <= kSplineSubdiv; ++k) {
-    spline_eval(s, __dmul_rn(span, (double)k) / (double)kSplineSubdiv, p);
+    spline_eval(s, kSplineT.t[k], p);  // == span * k / 1000 (span = 1), correctly rounded
     const double cum_k = __dadd_rn(cum_prev, dist3_rn(p, p_prev));
     while (cum_k >= sv) {  // the reference's while loop stops at seg = k - 1 for this s
       const double seg_len = __dadd_rn(cum_k, -cum_prev);
@@ -792,7 +804,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   // and DoF pairs advanced with packed FFMA2 (fp32 rounding differs from the
   // reference's operation order by a few ulp, inside the state tolerance).
   constexpr bool kPd = CH::kExact && MODE == kModePosition && SUB > 0 && Blk::N > 0;
-  float gk[NB], gd[NB], gc[NB], ge[NB];
+  float gk[NB], gd[NB], gc[NB], ge[NB], glo[NB], ghi[NB], gvl[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     const int d = B0 + j < kMaxDof ? B0 + j : 0;
@@ -801,6 +813,9 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     gd[j] = R.kd[d] * dti;
     gc[j] = 1.f - R.damping[d] * dti;
     ge[j] = R.eff[d] * dti;
+    glo[j] = R.lo[d];
+    ghi[j] = R.hi[d];
+    gvl[j] = R.vel[d];
   }
 
   float a[NB];  // this step's actions (kept for a producer's redo)
@@ -811,7 +826,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         a[j] = 0.f;
-        if (active && has(j)) {
+        if (has(j)) {  // inactive lanes (ragged last team) draw too: no divergence, never stored
           const uint64_t st = j == 0 ? act_s : act_s * P.bench.pow_mult[j] + P.bench.pow_add[j];
           const uint32_t u = pcg_output(st);
           // uniform(-1, 1) = -1 + 2 * (u * 2^-32) = (u - 2^31) * 2^-31: the exact
@@ -820,26 +835,30 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
           s_act[lane * A + B0 + j] = a[j];
         }
       }
-      if (active) act_s = act_s * P.bench.jump_mult + P.bench.jump_add;
+      act_s = act_s * P.bench.jump_mult + P.bench.jump_add;
     } else {
-      // the team's action rows are one contiguous run: coalesced (float4 when
-      // aligned) loads into shared memory, then each warp picks its DoFs (one
-      // pass over PCIe when the actions are in mapped host memory)
-      const float* src = P.actions + row0 * A;
-      const int cnt = rows * A;
-      if (P.actions_aligned) {
-        const int n4 = cnt >> 2;
-        for (int k = threadIdx.x; k < n4; k += 32 * G)
-          reinterpret_cast<float4*>(s_act)[k] = reinterpret_cast<const float4*>(src)[k];
-        for (int k = (n4 << 2) + threadIdx.x; k < cnt; k += 32 * G) s_act[k] = src[k];
-      } else {
-        for (int k = threadIdx.x; k < cnt; k += 32 * G) s_act[k] = src[k];
-      }
-      __syncthreads();
+      // the caller's rows, staged once per launch (below)
 #pragma unroll
-      for (int j = 0; j < NB; ++j) a[j] = (active && has(j)) ? s_act[lane * A + B0 + j] : 0.f;
+      for (int j = 0; j < NB; ++j) a[j] = (active && has(j)) ? s_act_base[lane * A + B0 + j] : 0.f;
     }
   };
+  if constexpr (!GEN) {
+    // The team's action rows are one contiguous run: coalesced (float4 when
+    // aligned) loads into shared memory, then each warp picks its DoFs (one
+    // pass over PCIe when the actions are in mapped host memory). A launch
+    // with caller actions applies the same rows at every step.
+    const float* src = P.actions + row0 * A;
+    const int cnt = rows * A;
+    if (P.actions_aligned) {
+      const int n4 = cnt >> 2;
+      for (int k = threadIdx.x; k < n4; k += 32 * G)
+        reinterpret_cast<float4*>(s_act_base)[k] = reinterpret_cast<const float4*>(src)[k];
+      for (int k = (n4 << 2) + threadIdx.x; k < cnt; k += 32 * G) s_act_base[k] = src[k];
+    } else {
+      for (int k = threadIdx.x; k < cnt; k += 32 * G) s_act_base[k] = src[k];
+    }
+    __syncthreads();
+  }
 
   // ---- dynamics (dynamics.cpp:133-185) on this block; count: saturation /
   // non-finite bookkeeping (warp-collective; false on a producer's redo) ------
@@ -885,8 +904,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     if constexpr (kPd) {
       const auto clampf = [](float x, float l, float h) { return fminf(fmaxf(x, l), h); };
       const auto finish = [&](int j, float vv, float qq) {  // limit projection (velocity already limited)
-        const int d = B0 + j;
-        const float qc = clampf(qq, R.lo[d], R.hi[d]);
+        const float qc = clampf(qq, glo[j], ghi[j]);
         qd[j] = qc != qq ? 0.f : vv;
         q[j] = qc;
       };
@@ -901,8 +919,8 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
           u.x = clampf(u.x, -ge[j], ge[j]);
           u.y = clampf(u.y, -ge[j + 1], ge[j + 1]);
           float2 vv = __ffma2_rn(QD, make_float2(gc[j], gc[j + 1]), u);
-          vv.x = clampf(vv.x, -R.vel[d], R.vel[d]);
-          vv.y = clampf(vv.y, -R.vel[d + 1], R.vel[d + 1]);
+          vv.x = clampf(vv.x, -gvl[j], gvl[j]);
+          vv.y = clampf(vv.y, -gvl[j + 1], gvl[j + 1]);
           const float2 qq = __ffma2_rn(vv, make_float2(dt, dt), Q);
           finish(j, vv.x, qq.x);
           finish(j + 1, vv.y, qq.y);
@@ -912,7 +930,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
           const int d = B0 + j;
           float u = fmaf(-gd[j], qd[j], fmaf(-gk[j], q[j], kpqt[j]));
           u = clampf(u, -ge[j], ge[j]);
-          const float vv = clampf(fmaf(qd[j], gc[j], u), -R.vel[d], R.vel[d]);
+          const float vv = clampf(fmaf(qd[j], gc[j], u), -gvl[j], gvl[j]);
           finish(j, vv, fmaf(vv, dt, q[j]));
         }
       }
@@ -970,7 +988,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
 #pragma unroll
       for (int k = 0; k < 3; ++k) ts.xf[b][S][9 + k][lane] = x.p[k];
     }
-    if (active) {
+    {  // (inactive lanes stage rows past `rows`, never stored)
       float* o = s_obs + lane * O;
 #pragma unroll
       for (int j = 0; j < NB; ++j)
@@ -982,17 +1000,74 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     }
   };
 
-  bool pend = false;  // scorer: rows ended (and were reset) at the previous step
+  // scorer: store step rows of parity pb (generated actions when G == 1,
+  // observation rows, host mirror)
+  const auto store_rows = [&](int pb) {
+    const float* so = s_obs_base + pb * (kTeamEnvs * O);
+    if constexpr (GEN && G == 1)
+      team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act_base + pb * (kTeamEnvs * A + 4),
+                                               rows * A, rows == kTeamEnvs, lane);
+    team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.obs + row0 * O, so, rows * O, rows == kTeamEnvs, lane);
+    if constexpr (!GEN) {
+      if (P.p.h_obs)
+        team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.h_obs + row0 * O, so, rows * O, rows == kTeamEnvs,
+                                                           lane);
+    }
+  };
+
+  // Rows that ended at step k (pb = parity of k) are reset by the WHOLE team
+  // (env lane l by warp l % G: reset_row is fp64-heavy, PathFollowing most of
+  // all), after which the scorer re-observes them and stores step k's rows.
+  const auto reset_phase = [&](int pb) {
+    if (active && ts.ended[pb][lane] && (lane % G) == S) {
+      const int e = reset_env<CH, TASK>(P, i);  // reset_row (envs.cpp:304-360) through HBM
+      if (e) atomicOr(P.p.err, e);
+    }
+    __syncthreads();
+    if constexpr (S == 0) {
+      float* so = s_obs_base + pb * (kTeamEnvs * O);
+      if (active && ts.ended[pb][lane]) {  // the post-reset observation row
+        load_block();
+        load_task();
+        float* o = so + lane * O;
+#pragma unroll
+        for (int d = 0; d < CH::kDof; ++d)
+          if (CH::kExact || d < A) {
+            o[d] = P.p.q[d * n + i];
+            o[A + d] = P.p.qd[d * n + i];
+            o[2 * A + 3 + d] = P.p.qt[d * n + i];
+          }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          o[2 * A + k] = tip[k];
+          o[3 * A + 3 + k] = goal[k];
+        }
+      }
+      __syncwarp();
+      store_rows(pb);
+    }
+  };
+
+  bool pend = false;  // scorer: rows ended at the previous step (reset pending)
   for (int step = 0; step < k_steps; ++step) {
     const int b = step & 1;
     float* s_obs = s_obs_base + b * (kTeamEnvs * O);
     float* s_act = s_act_base + b * (kTeamEnvs * A + 4);
-    draw(s_act);
-    dynamics(true);
-    publish(b, s_obs);
-    // B(step); its OR tells producers that the scorer reset rows of step-1
+    if (!(S == 0 && pend)) {  // a scorer with pending resets produces after them
+      draw(s_act);
+      dynamics(true);
+      publish(b, s_obs);
+    }
+    // B(step); its OR says rows of step-1 ended: reset them as a team, then the
+    // scorer produces this step and producers redo it for the reset rows
     if (__syncthreads_or(S == 0 && pend)) {
-      if constexpr (S > 0) {
+      reset_phase(b ^ 1);
+      if constexpr (S == 0) {
+        draw(s_act);
+        dynamics(true);
+        publish(b, s_obs);
+        pend = false;
+      } else {
         if (active && ts.ended[b ^ 1][lane]) {  // redo this step from the reset state
           load_block();
           dynamics(false);
@@ -1026,7 +1101,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       }
       bool ended = false;
       float* o = s_obs + lane * O;
-      if (active) {
+      {  // computed on every lane (no divergence); global side effects on active lanes only
         tip[0] = v[0];
         tip[1] = v[1];
         tip[2] = v[2];
@@ -1055,19 +1130,21 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
           hc = dist < T.success_radius ? hc + 1 : 0;
           goal_met = hc >= T.success_hold;
         }
-        if (!isfinite(reward)) atomicOr(P.p.err, kErrNonFiniteReward);
         const bool timed_out = sc >= T.episode_len;
-        P.p.rewards[i] = reward;
-        P.p.task_error[i] = dist;
-        P.p.terminated[i] = goal_met ? 1 : 0;
-        P.p.timed_out[i] = timed_out ? 1 : 0;
-        if constexpr (!GEN) {
-          if (P.p.h_rewards) P.p.h_rewards[i] = reward;
-          if (P.p.h_task_error) P.p.h_task_error[i] = dist;
-          if (P.p.h_terminated) P.p.h_terminated[i] = goal_met ? 1 : 0;
-          if (P.p.h_timed_out) P.p.h_timed_out[i] = timed_out ? 1 : 0;
+        if (active) {
+          if (!isfinite(reward)) atomicOr(P.p.err, kErrNonFiniteReward);
+          P.p.rewards[i] = reward;
+          P.p.task_error[i] = dist;
+          P.p.terminated[i] = goal_met ? 1 : 0;
+          P.p.timed_out[i] = timed_out ? 1 : 0;
+          if constexpr (!GEN) {
+            if (P.p.h_rewards) P.p.h_rewards[i] = reward;
+            if (P.p.h_task_error) P.p.h_task_error[i] = dist;
+            if (P.p.h_terminated) P.p.h_terminated[i] = goal_met ? 1 : 0;
+            if (P.p.h_timed_out) P.p.h_timed_out[i] = timed_out ? 1 : 0;
+          }
         }
-        ended = goal_met || timed_out;
+        ended = active && (goal_met || timed_out);
         o[2 * A + 0] = tip[0];
         o[2 * A + 1] = tip[1];
         o[2 * A + 2] = tip[2];
@@ -1078,10 +1155,11 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       ts.ended[b][lane] = ended;
       const unsigned em = __ballot_sync(0xffffffffu, ended);
       pend = em != 0;
+      __syncwarp();  // staged columns, tip / goal and ended flags are complete
       if (pend) {
         if (lane == 0) atomicAdd(P.p.ended_total, (unsigned long long)__popc(em));
-        __syncwarp();  // the row's staged columns and tip / goal are complete
-        // terminal observations (envs.cpp:606-611): the pre-reset rows
+        // terminal observations (envs.cpp:606-611): the pre-reset rows; the
+        // step's observation rows are stored after the team reset phase
         for (int r = 0; r < rows; ++r) {
           if (!((em >> r) & 1u)) continue;
           for (int k = lane; k < O; k += 32) {
@@ -1091,46 +1169,17 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
             }
           }
         }
-        __syncwarp();
-        if (ended) {
-          // reset_row (envs.cpp:304-360) through HBM, then the post-reset row
-          const int e = reset_env<CH, TASK>(P, i);
-          if (e) atomicOr(P.p.err, e);
-          load_block();
-          load_task();
-          sc = 0;
-          hc = 0;
-#pragma unroll
-          for (int d = 0; d < CH::kDof; ++d)
-            if (CH::kExact || d < A) {
-              o[d] = P.p.q[d * n + i];
-              o[A + d] = P.p.qd[d * n + i];
-              o[2 * A + 3 + d] = P.p.qt[d * n + i];
-            }
-          o[2 * A + 0] = tip[0];
-          o[2 * A + 1] = tip[1];
-          o[2 * A + 2] = tip[2];
-          o[3 * A + 3] = goal[0];
-          o[3 * A + 4] = goal[1];
-          o[3 * A + 5] = goal[2];
-        }
-      }
-      __syncwarp();
-      if constexpr (GEN && G == 1)
-        team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act, rows * A, rows == kTeamEnvs, lane);
-      team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.obs + row0 * O, s_obs, rows * O, rows == kTeamEnvs,
-                                                         lane);
-      if constexpr (!GEN) {
-        if (P.p.h_obs)
-          team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.h_obs + row0 * O, s_obs, rows * O,
-                                                             rows == kTeamEnvs, lane);
+      } else {
+        store_rows(b);
       }
     }
   }
-  // producers learn which rows ended at the last step: their reset state is
-  // already in HBM and must not be overwritten with the stale registers
+  // rows that ended at the last step: team reset, then the scorer stores the
+  // rows; the producers' registers of those rows are stale (the reset state
+  // is already in HBM)
   const bool fix = __syncthreads_or(S == 0 && pend);
-  const bool stale = S > 0 && fix && k_steps > 0 && ts.ended[(k_steps - 1) & 1][lane];
+  if (fix) reset_phase((k_steps - 1) & 1);
+  const bool stale = S > 0 && fix && ts.ended[(k_steps - 1) & 1][lane];
   if (active) {
     if (!stale) {
 #pragma unroll
