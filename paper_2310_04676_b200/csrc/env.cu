@@ -362,6 +362,8 @@ bool chain_matches(const sg::RobotTable& t) {
   for (int d = 0; d < CH::kDof; ++d) {
     const auto& j = t.j[d];
     if (j.axis_code == 6) return false;
+    // the specialised kernels evaluate sin/cos without range reduction
+    if (j.kind == sg::kRevolute && (t.lo_d[d] < -M_PI || t.hi_d[d] > M_PI)) return false;
     if (sg::jsig(j.kind, j.axis_code, j.flags & 7, (j.flags >> 3) & 1) != CH::kSig[d]) return false;
   }
   return true;

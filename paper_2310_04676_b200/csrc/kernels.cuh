@@ -211,8 +211,11 @@ __device__ __forceinline__ void fast_sincos(float x, float& s, float& c) {
 
 // One actuated joint of fk_walk with signature fields (kind, axis, oflags, rot)
 // that are compile-time constants in FixedChain and runtime in GenericChain.
+// reduce: 2*pi range reduction before the SFU sin/cos. The specialised
+// chains skip it: the host selects them only when every revolute limit lies
+// in [-pi, pi] (select_chain), where __sincosf is accurate as is.
 __device__ __forceinline__ void fk_joint(const JointEnc& J, int kind, int axis, int of, int rot, float qv,
-                                         float (&m)[9], float (&p)[3]) {
+                                         float (&m)[9], float (&p)[3], bool reduce = true) {
   // p += R * origin_translation
   if (of & 1) { p[0] += m[0] * J.o[0]; p[1] += m[3] * J.o[0]; p[2] += m[6] * J.o[0]; }
   if (of & 2) { p[0] += m[1] * J.o[1]; p[1] += m[4] * J.o[1]; p[2] += m[7] * J.o[1]; }
@@ -229,7 +232,8 @@ __device__ __forceinline__ void fk_joint(const JointEnc& J, int kind, int axis, 
   }
   if (kind == kRevolute) {
     float s, c;
-    fast_sincos(qv, s, c);
+    if (reduce) fast_sincos(qv, s, c);
+    else __sincosf(qv, &s, &c);
     if (axis == 2) rot_cols(m, 0, 1, c, s);        // +z
     else if (axis == 5) rot_cols(m, 0, 1, c, -s);  // -z
     else if (axis == 0) rot_cols(m, 1, 2, c, s);   // +x
@@ -292,7 +296,7 @@ struct FixedChain {
   template <int D>
   __device__ static void joint(const RobotTable& R, const float (&q)[kDof], float (&m)[9], float (&p)[3]) {
     constexpr int sig = kSig[D];
-    fk_joint(R.j[D], sig & 3, (sig >> 2) & 7, (sig >> 5) & 7, (sig >> 8) & 1, q[D], m, p);
+    fk_joint(R.j[D], sig & 3, (sig >> 2) & 7, (sig >> 5) & 7, (sig >> 8) & 1, q[D], m, p, false);
   }
   template <int... D>
   __device__ static void walk(const RobotTable& R, const float (&q)[kDof], float (&m)[9], float (&p)[3],
@@ -383,7 +387,7 @@ static __constant__ SplineTTable kSplineT = make_spline_t();
 // Writes fp32 waypoints; returns the count, or -1 past the table capacity.
 static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, double spacing, float* out, int cap) {
   const double span = 1.0;  // t1 - t0 (sample_path, envs.cpp:248-249)
-  double p_prev[3], p[3];
+  double p_prev[3];
   spline_eval(s, 0.0, p_prev);
   out[0] = (float)p_prev[0];
   out[1] = (float)p_prev[1];
@@ -391,9 +395,26 @@ static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, doub
   int count = 1, tentative = 1;
   double cum_prev = 0.0, sv = spacing;
   double s_emit[2] = {0.0, 0.0};  // targets of the last two tentative emissions
-  for (int k = 1; k <= kSplineSubdiv; ++k) {
-    spline_eval(s, kSplineT.t[k], p);  // == span * k / 1000 (span = 1), correctly rounded
-    const double cum_k = __dadd_rn(cum_prev, dist3_rn(p, p_prev));
+  // Points in batches of U: the U evaluations and chord lengths are
+  // independent (instruction-level parallelism for the fp64 latency chains);
+  // only the cumulative sum and the emission loop run point by point, in the
+  // reference's order, so every value is unchanged.
+#ifndef SG_SPLINE_BATCH
+#define SG_SPLINE_BATCH 4
+#endif
+  constexpr int U = SG_SPLINE_BATCH;
+  static_assert(kSplineSubdiv % U == 0, "batch must divide the subdivision count");
+  for (int kb = 1; kb <= kSplineSubdiv; kb += U) {
+    double px[U][3], dk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) spline_eval(s, kSplineT.t[kb + u], px[u]);  // t_k == span * k / 1000
+    dk[0] = dist3_rn(px[0], p_prev);
+#pragma unroll
+    for (int u = 1; u < U; ++u) dk[u] = dist3_rn(px[u], px[u - 1]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const int k = kb + u;
+    const double cum_k = __dadd_rn(cum_prev, dk[u]);
     while (cum_k >= sv) {  // the reference's while loop stops at seg = k - 1 for this s
       const double seg_len = __dadd_rn(cum_k, -cum_prev);
       const double frac = seg_len > 0.0 ? __dadd_rn(sv, -cum_prev) / seg_len : 0.0;
@@ -410,9 +431,10 @@ static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, doub
       sv = __dadd_rn(sv, spacing);
     }
     cum_prev = cum_k;
-    p_prev[0] = p[0];
-    p_prev[1] = p[1];
-    p_prev[2] = p[2];
+    }
+    p_prev[0] = px[U - 1][0];
+    p_prev[1] = px[U - 1][1];
+    p_prev[2] = px[U - 1][2];
   }
   const double total = cum_prev;
   if (total <= 1e-12) return count;
@@ -513,7 +535,8 @@ __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
     sp.c[10] = d[1];
     sp.c[11] = d[2];
     double max_off = 0.0;
-    for (int k = 0; k <= 100; ++k) {
+#pragma unroll 4
+    for (int k = 0; k <= 100; ++k) {  // independent samples: unrolled for ILP, max in order
       double pt[3];
       spline_eval(sp, __dmul_rn(0.01, (double)k), pt);
       const double off = dist3_rn(pt, d);
@@ -677,7 +700,7 @@ __device__ __forceinline__ void fk_range(const RobotTable& R, const float* q, Xf
                                          std::integer_sequence<int, J...>) {
   if constexpr (CH::kExact) {
     ((void)fk_joint(R.j[B + J], CH::kSig[B + J] & 3, (CH::kSig[B + J] >> 2) & 7, (CH::kSig[B + J] >> 5) & 7,
-                    (CH::kSig[B + J] >> 8) & 1, q[J], x.m, x.p),
+                    (CH::kSig[B + J] >> 8) & 1, q[J], x.m, x.p, false),
      ...);
   } else {
     (
@@ -804,7 +827,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   // and DoF pairs advanced with packed FFMA2 (fp32 rounding differs from the
   // reference's operation order by a few ulp, inside the state tolerance).
   constexpr bool kPd = CH::kExact && MODE == kModePosition && SUB > 0 && Blk::N > 0;
-  float gk[NB], gd[NB], gc[NB], ge[NB], glo[NB], ghi[NB], gvl[NB];
+  float gk[NB], gd[NB], gc[NB], ge[NB], glo[NB], ghi[NB], gvl[NB], ghalf[NB], gmid[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     const int d = B0 + j < kMaxDof ? B0 + j : 0;
@@ -816,26 +839,43 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     glo[j] = R.lo[d];
     ghi[j] = R.hi[d];
     gvl[j] = R.vel[d];
+    ghalf[j] = 0.5f * (R.hi[d] - R.lo[d]);  // rescale_to_range as one FFMA (GEN)
+    gmid[j] = R.lo[d] + ghalf[j];
   }
 
   float a[NB];  // this step's actions (kept for a producer's redo)
 
   // ---- actions: the bench stream (GEN) or the caller's rows ----------------
-  const auto draw = [&](float* s_act) {
+  // GEN: the next step's draws are made one step ahead (an[], from state
+  // act_pf) so the 64-bit LCG / XSH-RR chains overlap the current step's FK
+  // instead of heading the next step's critical path.
+  float an[NB];
+  uint64_t act_pf = act_s;
+  const auto prefetch = [&]() {
     if constexpr (GEN) {
+      act_pf = act_s;
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        a[j] = 0.f;
+        an[j] = 0.f;
         if (has(j)) {  // inactive lanes (ragged last team) draw too: no divergence, never stored
           const uint64_t st = j == 0 ? act_s : act_s * P.bench.pow_mult[j] + P.bench.pow_add[j];
           const uint32_t u = pcg_output(st);
           // uniform(-1, 1) = -1 + 2 * (u * 2^-32) = (u - 2^31) * 2^-31: the exact
           // fp64 value of the reference (bench.cpp:34) rounded once to fp32
-          a[j] = __int2float_rn((int32_t)(u ^ 0x80000000u)) * 0x1.0p-31f;
-          s_act[lane * A + B0 + j] = a[j];
+          an[j] = __int2float_rn((int32_t)(u ^ 0x80000000u)) * 0x1.0p-31f;
         }
       }
       act_s = act_s * P.bench.jump_mult + P.bench.jump_add;
+    }
+  };
+  prefetch();
+  const auto draw = [&](float* s_act) {
+    if constexpr (GEN) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        a[j] = an[j];
+        if (has(j)) s_act[lane * A + B0 + j] = a[j];
+      }
     } else {
       // the caller's rows, staged once per launch (below)
 #pragma unroll
@@ -892,7 +932,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         return GEN ? fmaf(x, 0.5f * (h - l), l + 0.5f * (h - l)) : rescale(x, l, h);
       };
       if (mode == kModePosition) {
-        qt[j] = (d == jaw) ? (ad > 0.f ? hi : lo) : rs(ad, lo, hi);
+        qt[j] = (d == jaw) ? (ad > 0.f ? hi : lo) : (GEN ? fmaf(ad, ghalf[j], gmid[j]) : rs(ad, lo, hi));
         kpqt[j] = (kPd ? gk[j] : R.kp[d]) * qt[j];
       } else if (mode == kModeVelocity) {
         v_target[j] = rs(ad, -R.vel[d], R.vel[d]);
@@ -1019,7 +1059,11 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   // (env lane l by warp l % G: reset_row is fp64-heavy, PathFollowing most of
   // all), after which the scorer re-observes them and stores step k's rows.
   const auto reset_phase = [&](int pb) {
+#ifdef SG_RESET_FULLWARP
+    if (active && ts.ended[pb][lane] && (int)(blockIdx.x % G) == S) {
+#else
     if (active && ts.ended[pb][lane] && (lane % G) == S) {
+#endif
       const int e = reset_env<CH, TASK>(P, i);  // reset_row (envs.cpp:304-360) through HBM
       if (e) atomicOr(P.p.err, e);
     }
@@ -1056,6 +1100,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     if (!(S == 0 && pend)) {  // a scorer with pending resets produces after them
       draw(s_act);
       dynamics(true);
+      prefetch();
       publish(b, s_obs);
     }
     // B(step); its OR says rows of step-1 ended: reset them as a team, then the
@@ -1065,6 +1110,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       if constexpr (S == 0) {
         draw(s_act);
         dynamics(true);
+        prefetch();
         publish(b, s_obs);
         pend = false;
       } else {
@@ -1203,7 +1249,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         P.p.wp_len[i] = wl;
       }
     }
-    if (GEN) P.p.act_state[(int64_t)S * n + i] = act_s;
+    if (GEN) P.p.act_state[(int64_t)S * n + i] = act_pf;  // the drawn-ahead step was not consumed
   }
 }
 
