@@ -239,8 +239,11 @@ struct sg_env {
   float* d_actions_in = nullptr;  // staging for sg_env_step_host
   unsigned long long last_sat = 0;
   unsigned long long last_ended = 0;
-  unsigned long long* counters = nullptr;    // device {sat_total, ended_total, err, pad}
-  unsigned long long* h_counters = nullptr;  // pinned copy of `counters`
+  // device {sat_total, ended slot A, err, ended slot B, ticket, pad...}
+  unsigned long long* counters = nullptr;
+  unsigned long long* h_counters = nullptr;  // pinned, mapped: {sat_total, ended, err} of the last host step
+  unsigned long long* d_status = nullptr;    // device alias of h_counters
+  int host_slot = 0;                          // ended slot of the next host step
   bool bench_ready = false;
 
   ~sg_env() {
@@ -501,12 +504,14 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   p.task_error = dalloc<float>(n);
   p.terminated = dalloc<uint8_t>(n);
   p.timed_out = dalloc<uint8_t>(n);
-  // the three device counters share one 32-byte block: one D2H per host step
-  env->counters = dalloc<unsigned long long>(4);
+  // device counters in one 64-byte block; the host step reads them through
+  // a mapped pinned status the kernel's last CTA fills (no copy, no memset)
+  env->counters = dalloc<unsigned long long>(8);
   p.sat_total = env->counters;
   p.ended_total = env->counters + 1;
   p.err = reinterpret_cast<int32_t*>(env->counters + 2);
-  CK(cudaMallocHost(&env->h_counters, 4 * sizeof(unsigned long long)));
+  CK(cudaHostAlloc(&env->h_counters, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&env->d_status), env->h_counters, 0));
   p.act_state = nullptr;
   p.act_buf = nullptr;
   // SimBatch::create (dynamics.cpp:225-241): mid configuration at rest, stream
@@ -686,7 +691,14 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
       // obs rows are stored as float4 runs
       zc &= (reinterpret_cast<uintptr_t>(host_f[0]) & 15u) == 0 && (reinterpret_cast<uintptr_t>(host_f[1]) & 15u) == 0;
     }
-    CK(cudaMemsetAsync(p.ended_total, 0, sizeof(unsigned long long), s));  // rows ended in THIS step
+    // rows ended in THIS step: alternate between two counter slots; the
+    // launch zeroes the other one for the next host step
+    const int slot = env->host_slot;
+    env->host_slot ^= 1;
+    p.ended_total = env->counters + (slot ? 3 : 1);
+    p.ended_clear = env->counters + (slot ? 1 : 3);
+    p.ticket = reinterpret_cast<unsigned int*>(env->counters + 4);
+    p.h_status = env->d_status;
     if (zc) {
       env->P.actions = static_cast<const float*>(a_act);
       env->P.actions_aligned = (reinterpret_cast<uintptr_t>(a_act) & 15u) == 0;
@@ -714,8 +726,8 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
         if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, p.timed_out, n, cudaMemcpyDeviceToHost, s));
       }
     }
-    // {sat_total, ended_total, err} in one copy, then one synchronisation
-    CK(cudaMemcpyAsync(env->h_counters, env->counters, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    p.h_status = nullptr;
+    p.ended_clear = nullptr;
     CK(cudaStreamSynchronize(s));
     const unsigned long long sat = env->h_counters[0], ended = env->h_counters[1];
     env->raise(static_cast<int32_t>(env->h_counters[2] & 0xffffffffu));

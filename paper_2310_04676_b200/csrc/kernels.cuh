@@ -118,6 +118,12 @@ struct EnvPtrs {
   // stores (sg_env_step_host) instead of separate copies.
   float* h_obs;
   float* h_tobs;  // ended rows only
+  // Host-step status (nullable): the launch's last CTA copies {sat_total,
+  // ended rows of this step, error word} into mapped pinned memory, so the
+  // host reads them after its one synchronisation without a copy.
+  unsigned long long* h_status;
+  unsigned long long* ended_clear;  // zeroed at launch start: the next host step's ended slot
+  unsigned int* ticket;             // CTA completion counter (last CTA publishes, then re-arms it)
   float* h_rewards;
   float* h_task_error;
   uint8_t* h_terminated;
@@ -1268,7 +1274,21 @@ __global__ void __launch_bounds__(32 * G) env_step_kernel(const __grid_constant_
   TeamSmem<G>& ts = *reinterpret_cast<TeamSmem<G>*>(smem);
   float* s_obs = smem + (sizeof(TeamSmem<G>) + 15) / 16 * 4;  // 2 x 32 x O
   float* s_act = s_obs + 2 * kTeamEnvs * O;                    // 2 x (32 x A + 4)
+  if (P.p.ended_clear && blockIdx.x == 0 && threadIdx.x == 0) *P.p.ended_clear = 0;
   team_dispatch<CH, G, TASK, MODE, SUB, GEN>(P, k_steps, s_obs, s_act, ts, std::make_integer_sequence<int, G>{});
+  if (P.p.h_status) {  // host step: the last CTA to finish publishes the counters
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(P.p.ticket, 1u) == gridDim.x - 1) {
+        __threadfence();
+        P.p.h_status[0] = *reinterpret_cast<volatile unsigned long long*>(P.p.sat_total);
+        P.p.h_status[1] = *reinterpret_cast<volatile unsigned long long*>(P.p.ended_total);
+        P.p.h_status[2] = static_cast<unsigned long long>(static_cast<uint32_t>(*reinterpret_cast<volatile int32_t*>(P.p.err)));
+        *P.p.ticket = 0;
+      }
+    }
+  }
 }
 
 template <int G>

@@ -96,7 +96,28 @@ int main() {
       cudaStreamSynchronize(s0);
     }
     double ts = (now_us() - t) / 1000;
-    printf("host per call: memcpyAsync %.2f us, launch %.2f us, launch+sync round trip %.2f us\n", tm, tl, ts);
+    cudaPointerAttributes pa;
+    t = now_us();
+    for (int r = 0; r < 1000; ++r) cudaPointerGetAttributes(&pa, hi + (r & 63) * 64);
+    double tp = (now_us() - t) / 1000;
+    cudaDeviceSynchronize();
+    t = now_us();
+    for (int r = 0; r < 1000; ++r) {
+      cudaMemsetAsync(di, 0, 8, s0);
+      noop<<<1, 32, 0, s0>>>();
+      cudaMemcpyAsync(ho, di, 24, cudaMemcpyDeviceToHost, s0);
+      cudaStreamSynchronize(s0);
+    }
+    double tc = (now_us() - t) / 1000;
+    t = now_us();
+    for (int r = 0; r < 1000; ++r) {
+      noop<<<1, 32, 0, s0>>>();
+      cudaStreamSynchronize(s0);
+    }
+    double tk = (now_us() - t) / 1000;
+    printf("host per call: memcpyAsync %.2f us, launch %.2f us, launch+sync round trip %.2f us, "
+           "cudaPointerGetAttributes %.2f us, memset+launch+memcpy+sync %.2f us, launch+sync %.2f us\n",
+           tm, tl, ts, tp, tc, tk);
   }
   // step mimic: H2D actions, kernel, D2H results, sync — per step wall time
   {
