@@ -440,7 +440,7 @@ def main():
                         fused_steps_per_launch=F, parallelism=f"env-shard x{world}",
                         l2="256 MiB flush between timed launches; per-launch state read cold from HBM"),
             roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                          traffic=traffic, peak_kind=peak_kind, kernel="env_step_kernel<8,true>",
+                          traffic=traffic, peak_kind=peak_kind, kernel=f"env_step_kernel<{cfg['robot'].upper()} chain, 2 team warps, GEN> ({F} fused steps/launch)",
                           bytes_per_env_step=b["per_env_step"], bytes_per_launch=n * b["per_env_launch"],
                           avg_launch_us=avg_launch_s * 1e6),
             cpu_baseline=cpu, e2e=e2e, single_step_launches=single,
