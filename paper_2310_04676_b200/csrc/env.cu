@@ -254,7 +254,8 @@ struct sg_env {
     void* bufs[] = {p.q,   p.qd,       p.qt,         p.goals,      p.tips,     p.step_count, p.hold_count,
                     p.episode_count, p.wp_idx,     p.wp_len,     p.wps,      p.rng_state,  p.rng_inc,
                     p.obs, p.tobs,     p.rewards,    p.task_error, p.terminated, p.timed_out, counters,
-                    p.act_state, p.act_buf, d_actions_in};
+                    p.act_state, p.act_buf, d_actions_in, p.rec_valid, p.rec_q, p.rec_len, p.rec_err, p.rec_rng,
+                    p.rec_wps};
     for (void* b : bufs)
       if (b) cudaFree(b);
   }
@@ -274,7 +275,17 @@ struct sg_env {
     }
     CK(e);
   }
-  void launch_step(int k_steps, bool gen) { launch(k_steps, gen, false); }
+  // Fused multi-step launches of a PathFollowing env first bring the reset
+  // records up to date (path_record_kernel, kernels.cuh): the launch's reset
+  // bursts then install precomputed resets. Single steps reset inline.
+  void launch_step(int k_steps, bool gen) {
+    if (k_steps > 1 && P.p.rec_valid) {
+      const unsigned grid = static_cast<unsigned>((n + sg::kRecThreads - 1) / sg::kRecThreads);
+      sg::path_record_kernel<<<grid, sg::kRecThreads, 0, stream>>>(P);
+      CK(cudaGetLastError());
+    }
+    launch(k_steps, gen, false);
+  }
   void launch_reset() { launch(0, false, true); }
 
   // DoF block [b, e) of team warp s (kernels.cuh: Block)
@@ -496,6 +507,14 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   p.wp_idx = dalloc<int32_t>(n);
   p.wp_len = dalloc<int32_t>(n);
   p.wps = T.wp_cap ? dalloc<float>(static_cast<size_t>(n) * T.wp_cap * 3) : nullptr;
+  if (T.wp_cap) {  // PathFollowing reset records (kernels.cuh path_record_kernel)
+    p.rec_valid = dalloc<uint8_t>(n);
+    p.rec_q = dalloc<float>(n * dof);
+    p.rec_len = dalloc<int32_t>(n);
+    p.rec_err = dalloc<int32_t>(n);
+    p.rec_rng = dalloc<uint64_t>(n);
+    p.rec_wps = dalloc<float>(static_cast<size_t>(n) * T.wp_cap * 3);
+  }
   p.rng_state = dalloc<uint64_t>(n);
   p.rng_inc = dalloc<uint64_t>(n);
   p.obs = dalloc<float>(n * env->O);

@@ -97,6 +97,17 @@ struct EnvPtrs {
   int32_t* wp_idx;
   int32_t* wp_len;
   float* wps;     // [n][wp_cap][3]
+  // PathFollowing reset records (nullable): the NEXT reset_row of env i is a
+  // function of its PCG32 state only, which changes only at resets, so it is
+  // computed ahead by path_record_kernel (full warps, many warps per SM) and
+  // a reset just installs it. rec_valid[i] == 1 when the record matches the
+  // current state.
+  uint8_t* rec_valid;
+  float* rec_q;      // [dof][n]
+  int32_t* rec_len;  // waypoint count
+  int32_t* rec_err;  // error bits of the sampling
+  uint64_t* rec_rng; // PCG32 state after the reset's draws
+  float* rec_wps;    // [n][wp_cap][3]
   uint64_t* rng_state;
   uint64_t* rng_inc;
   // StepResult
@@ -391,6 +402,7 @@ static __constant__ SplineTTable kSplineT = make_spline_t();
 // s >= total - 1e-12 (at most one, since spacing >> 1e-12) are truncated.
 // Same operations, same rounding; half the fp64 work of a two-pass walk.
 // Writes fp32 waypoints; returns the count, or -1 past the table capacity.
+template <int U>
 static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, double spacing, float* out, int cap) {
   const double span = 1.0;  // t1 - t0 (sample_path, envs.cpp:248-249)
   double p_prev[3];
@@ -405,10 +417,6 @@ static __device__ __noinline__ int spline_waypoints_stream(const Spline& s, doub
   // independent (instruction-level parallelism for the fp64 latency chains);
   // only the cumulative sum and the emission loop run point by point, in the
   // reference's order, so every value is unchanged.
-#ifndef SG_SPLINE_BATCH
-#define SG_SPLINE_BATCH 4
-#endif
-  constexpr int U = SG_SPLINE_BATCH;
   static_assert(kSplineSubdiv % U == 0, "batch must divide the subdivision count");
   for (int kb = 1; kb <= kSplineSubdiv; kb += U) {
     double px[U][3], dk[U];
@@ -500,6 +508,83 @@ __device__ __forceinline__ void block_load(float* __restrict__ s, const float* _
   }
 }
 
+// sample_path (envs.cpp:241-267) + sample_spline_waypoints: draws the cubic
+// from the env stream, shrinks it into the workspace ball and writes the
+// waypoint table (fp32 copies of the fp64 waypoints). cnt = waypoint count.
+// Returns error bits.
+__device__ __forceinline__ int sample_path_spline(const TaskParams& T, uint64_t& s, uint64_t inc, Spline& sp) {
+  int err = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sp.c[k] = pcg_uniform(s, inc, -0.5, 0.5);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sp.c[3 + k] = pcg_uniform(s, inc, -0.5, 0.5);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sp.c[6 + k] = pcg_uniform(s, inc, -0.3, 0.3);
+  double d[3];
+  if (!sample_goal(s, inc, T, d)) err |= kErrGoalSampling;
+  sp.c[9] = d[0];
+  sp.c[10] = d[1];
+  sp.c[11] = d[2];
+  double max_off = 0.0;
+#pragma unroll 4
+  for (int k = 0; k <= 100; ++k) {  // independent samples: unrolled for ILP, max in order
+    double pt[3];
+    spline_eval(sp, __dmul_rn(0.01, (double)k), pt);
+    const double off = dist3_rn(pt, d);
+    max_off = max_off > off ? max_off : off;
+  }
+  const double ctr[3] = {T.center[0], T.center[1], T.center[2]};
+  const double allowed = __dadd_rn(T.radius, -dist3_rn(d, ctr));
+  if (max_off > 0.0 && max_off > allowed) {
+    const double scale = __dmul_rn(0.95, allowed > 0.0 ? allowed : 0.0) / max_off;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sp.c[k] = __dmul_rn(sp.c[k], scale);
+  }
+  return err;
+}
+
+// U: knots per batch (independent fp64 chains)
+template <int U>
+__device__ __forceinline__ int sample_path_waypoints(const TaskParams& T, uint64_t& s, uint64_t inc, float* table,
+                                                     int& cnt) {
+  Spline sp;
+  int err = sample_path_spline(T, s, inc, sp);
+  cnt = spline_waypoints_stream<U>(sp, T.spacing, table, T.wp_cap);
+  if (cnt < 0) {
+    err |= kErrWaypointCap;
+    cnt = T.wp_cap;
+  }
+  return err;
+}
+
+// Computes the next reset_row of every PathFollowing env whose record is
+// stale (after its last reset consumed it): q draws (middle half of each
+// range, rounded once) then sample_path, from the env's current stream
+// state, into the record buffers. One env per thread (the fp64 knot walk is
+// latency bound: measured 207 us per 16,384-env burst with batches of 4
+// knots, 232 us with 20, 350 us with a point-parallel warp-cooperative
+// variant; a reset burst inside the step kernel costs about the same).
+constexpr int kRecThreads = 128;
+static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const __grid_constant__ StepParams P) {
+  const RobotTable& R = P.robot;
+  const TaskParams& T = P.task;
+  const int64_t n = T.n;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || P.p.rec_valid[i]) return;
+  uint64_t s = P.p.rng_state[i];
+  const uint64_t inc = P.p.rng_inc[i];
+  for (int d = 0; d < R.dof; ++d) {
+    const double quarter = __dmul_rn(0.25, __dadd_rn(R.hi_d[d], -R.lo_d[d]));
+    P.p.rec_q[d * n + i] = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
+  }
+  int cnt = 0;
+  const int err = sample_path_waypoints<4>(T, s, inc, P.p.rec_wps + i * (int64_t)T.wp_cap * 3, cnt);
+  P.p.rec_len[i] = cnt;
+  P.p.rec_err[i] = err;
+  P.p.rec_rng[i] = s;
+  P.p.rec_valid[i] = 1;
+}
+
 // reset_row (envs.cpp:304-360) for one env. Out of line (rare path) and
 // communicating through HBM only, so the caller's state arrays stay in
 // registers: the caller reloads q/qdot/q_target/goal/tip/waypoint idx+len
@@ -517,49 +602,32 @@ __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
   int err = 0;
   float q[D], goal[3], tip[3];
   int32_t wp_idx = 0, wp_len = 0;
+  const bool rec = task == kTaskPath && P.p.rec_valid && P.p.rec_valid[i];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     q[d] = 0.f;
     if (d < dof) {
-      const double quarter = __dmul_rn(0.25, __dadd_rn(R.hi_d[d], -R.lo_d[d]));
-      q[d] = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
+      if (rec) {
+        q[d] = P.p.rec_q[d * n + i];
+      } else {
+        const double quarter = __dmul_rn(0.25, __dadd_rn(R.hi_d[d], -R.lo_d[d]));
+        q[d] = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
+      }
     }
   }
   CH::fk(R, q, tip);
   if (task == kTaskPath) {
-    // sample_path (envs.cpp:241-267)
-    Spline sp;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) sp.c[k] = pcg_uniform(s, inc, -0.5, 0.5);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) sp.c[3 + k] = pcg_uniform(s, inc, -0.5, 0.5);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) sp.c[6 + k] = pcg_uniform(s, inc, -0.3, 0.3);
-    double d[3];
-    if (!sample_goal(s, inc, T, d)) err |= kErrGoalSampling;
-    sp.c[9] = d[0];
-    sp.c[10] = d[1];
-    sp.c[11] = d[2];
-    double max_off = 0.0;
-#pragma unroll 4
-    for (int k = 0; k <= 100; ++k) {  // independent samples: unrolled for ILP, max in order
-      double pt[3];
-      spline_eval(sp, __dmul_rn(0.01, (double)k), pt);
-      const double off = dist3_rn(pt, d);
-      max_off = max_off > off ? max_off : off;
-    }
-    const double ctr[3] = {T.center[0], T.center[1], T.center[2]};
-    const double allowed = __dadd_rn(T.radius, -dist3_rn(d, ctr));
-    if (max_off > 0.0 && max_off > allowed) {
-      const double scale = __dmul_rn(0.95, allowed > 0.0 ? allowed : 0.0) / max_off;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) sp.c[k] = __dmul_rn(sp.c[k], scale);
-    }
     float* table = P.p.wps + i * (int64_t)T.wp_cap * 3;
-    int cnt = spline_waypoints_stream(sp, T.spacing, table, T.wp_cap);
-    if (cnt < 0) {
-      err |= kErrWaypointCap;
-      cnt = T.wp_cap;
+    int cnt;
+    if (rec) {  // install the precomputed reset (same draws, same arithmetic)
+      cnt = P.p.rec_len[i];
+      err |= P.p.rec_err[i];
+      s = P.p.rec_rng[i];
+      const float* src = P.p.rec_wps + i * (int64_t)T.wp_cap * 3;
+      for (int k = 0; k < 3 * cnt; ++k) table[k] = src[k];
+      P.p.rec_valid[i] = 0;
+    } else {
+      err |= sample_path_waypoints<4>(T, s, inc, table, cnt);
     }
     wp_len = cnt;
     wp_idx = 0;

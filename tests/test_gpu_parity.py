@@ -193,23 +193,39 @@ def test_bench_action_stream_bit_exact(sg, oracle):
     np.testing.assert_array_equal(shard.bench_actions().cpu().numpy(), expected[2][100:])
 
 
-def test_fused_k_steps_equal_single_steps(sg, oracle):
+@pytest.mark.parametrize("robot,task", [("psm", "target_reaching"), ("star", "path_following")])
+def test_fused_k_steps_equal_single_steps(sg, oracle, robot, task):
+    """K fused steps == K single-step launches, bit for bit. For PathFollowing
+    the fused launches install precomputed reset records (path_record_kernel)
+    while single steps reset inline: both must give identical state,
+    waypoint tables and RNG streams (episode_len 7 -> resets inside and
+    across launches, ragged team count)."""
     _cuda()
     n = 1000
-    a = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=2, episode_len=7)
-    b = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=2, episode_len=7)
+    kw = dict(robots=(robot,), n_envs=n, seed=2, episode_len=7, task=task,
+              goal_sigma=0.15 if robot == "star" else 0.05)
+    a, b = sg.VecTaskEnv(**kw), sg.VecTaskEnv(**kw)
     a.reset(); b.reset()
     a.bench_begin(2); b.bench_begin(2)
-    for _ in range(20):
-        a.bench_step(1)
-    b.bench_step(20)
-    torch.cuda.synchronize()
-    sa, sb = a.state(), b.state()
-    for k in ("q", "qdot", "q_target", "goals", "tips", "step_count", "episode_count", "rng_state"):
-        assert torch.equal(sa[k], sb[k]), k
-    ra, rb = a._result(), b._result()
-    assert torch.equal(ra.observations, rb.observations)
-    assert torch.equal(ra.terminal_observations, rb.terminal_observations)
+    for launch in (20, 3, 11):
+        for _ in range(launch):
+            a.bench_step(1)
+        b.bench_step(launch)
+        torch.cuda.synchronize()
+        sa, sb = a.state(), b.state()
+        keys = ["q", "qdot", "q_target", "goals", "tips", "step_count", "episode_count", "rng_state"]
+        if task == "path_following":
+            keys += ["waypoint_idx", "waypoint_len"]
+            wl = sa["waypoint_len"].cpu().numpy()
+            wa, wb = sa["waypoints"].cpu().numpy(), sb["waypoints"].cpu().numpy()
+            for row in range(n):
+                np.testing.assert_array_equal(wa[row, : wl[row]], wb[row, : wl[row]])
+        for k in keys:
+            assert torch.equal(sa[k], sb[k]), k
+        ra, rb = a._result(), b._result()
+        assert torch.equal(ra.observations, rb.observations)
+        ended = (ra.terminated | ra.timed_out).bool()
+        assert torch.equal(ra.terminal_observations[ended], rb.terminal_observations[ended])
 
 
 def test_sharded_rows_match_single_device(sg, oracle):
