@@ -512,6 +512,10 @@ __device__ __forceinline__ void block_load(float* __restrict__ s, const float* _
 // from the env stream, shrinks it into the workspace ball and writes the
 // waypoint table (fp32 copies of the fp64 waypoints). cnt = waypoint count.
 // Returns error bits.
+// QUAD > 1: the QUAD lanes of a group (same stream state) split the 101-point
+// offset scan and combine the maximum by shuffle (max is exact, so the
+// result is unchanged).
+template <int QUAD = 1>
 __device__ __forceinline__ int sample_path_spline(const TaskParams& T, uint64_t& s, uint64_t inc, Spline& sp) {
   int err = 0;
 #pragma unroll
@@ -526,12 +530,20 @@ __device__ __forceinline__ int sample_path_spline(const TaskParams& T, uint64_t&
   sp.c[10] = d[1];
   sp.c[11] = d[2];
   double max_off = 0.0;
+  const int r = QUAD > 1 ? (threadIdx.x & (QUAD - 1)) : 0;
 #pragma unroll 4
-  for (int k = 0; k <= 100; ++k) {  // independent samples: unrolled for ILP, max in order
+  for (int k = r; k <= 100; k += QUAD) {  // independent samples: unrolled for ILP
     double pt[3];
     spline_eval(sp, __dmul_rn(0.01, (double)k), pt);
     const double off = dist3_rn(pt, d);
     max_off = max_off > off ? max_off : off;
+  }
+  if constexpr (QUAD > 1) {
+#pragma unroll
+    for (int o = 1; o < QUAD; o <<= 1) {
+      const double other = __shfl_xor_sync(0xffffffffu, max_off, o);
+      max_off = max_off > other ? max_off : other;
+    }
   }
   const double ctr[3] = {T.center[0], T.center[1], T.center[2]};
   const double allowed = __dadd_rn(T.radius, -dist3_rn(d, ctr));
@@ -560,26 +572,127 @@ __device__ __forceinline__ int sample_path_waypoints(const TaskParams& T, uint64
 // Computes the next reset_row of every PathFollowing env whose record is
 // stale (after its last reset consumed it): q draws (middle half of each
 // range, rounded once) then sample_path, from the env's current stream
-// state, into the record buffers. One env per thread (the fp64 knot walk is
-// latency bound: measured 207 us per 16,384-env burst with batches of 4
-// knots, 232 us with 20, 350 us with a point-parallel warp-cooperative
-// variant; a reset burst inside the step kernel costs about the same).
+// state, into the record buffers.
+//
+// Four lanes per env (a quad; 8 envs per warp, 4x the warps of one lane per
+// env): every lane of the quad draws the same spline; per round of 20 knots
+// lane r evaluates knots r*5+1..r*5+5 and their chord lengths (5 independent
+// fp64 chains), the quad exchanges the 20 chords by shuffle, and all four
+// lanes walk them in order (cumulative sum + waypoint emission exactly as
+// sample_spline_waypoints; lane 0 writes). Same operations and summation
+// order as spline_waypoints_stream, so the tables are bit-identical.
 constexpr int kRecThreads = 128;
 static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const __grid_constant__ StepParams P) {
+  constexpr int kQ = 4, kU = 5, kRound = kQ * kU;  // lanes per env, knots per lane per round
+  static_assert(kSplineSubdiv % kRound == 0, "rounds must tile the knots");
   const RobotTable& R = P.robot;
   const TaskParams& T = P.task;
   const int64_t n = T.n;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || P.p.rec_valid[i]) return;
-  uint64_t s = P.p.rng_state[i];
-  const uint64_t inc = P.p.rng_inc[i];
-  for (int d = 0; d < R.dof; ++d) {
+  const int lane = threadIdx.x & 31, r = lane & (kQ - 1), base = lane & ~(kQ - 1);
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kQ;
+  const bool need = i < n && !P.p.rec_valid[i];
+  if (!__any_sync(0xffffffffu, need)) return;
+  uint64_t s = need ? P.p.rng_state[i] : 0;
+  const uint64_t inc = need ? P.p.rng_inc[i] : 1;
+  int err = 0;
+  Spline sp;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) sp.c[k] = 0.0;
+  for (int d = 0; d < R.dof; ++d) {  // (lanes without work draw from a dummy stream)
     const double quarter = __dmul_rn(0.25, __dadd_rn(R.hi_d[d], -R.lo_d[d]));
-    P.p.rec_q[d * n + i] = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
+    const float qv = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
+    if (need && r == 0) P.p.rec_q[d * n + i] = qv;
   }
-  int cnt = 0;
-  const int err = sample_path_waypoints<4>(T, s, inc, P.p.rec_wps + i * (int64_t)T.wp_cap * 3, cnt);
-  P.p.rec_len[i] = cnt;
+  err = sample_path_spline<kQ>(T, s, inc, sp);
+  if (!need) err = 0;
+  const bool writer = need && r == 0;
+  float* out = P.p.rec_wps + (need ? i : 0) * (int64_t)T.wp_cap * 3;
+  const int cap = T.wp_cap;
+  const double spacing = T.spacing;
+  double p_end[3];  // last knot of the previous round (lane r = 0 needs it)
+  spline_eval(sp, 0.0, p_end);
+  if (writer) {
+    out[0] = (float)p_end[0];
+    out[1] = (float)p_end[1];
+    out[2] = (float)p_end[2];
+  }
+  int tentative = 1;
+  double cum_prev = 0.0, sv = spacing;
+  double s_emit[2] = {0.0, 0.0};  // targets of the last two tentative emissions
+  for (int kb = 1; kb <= kSplineSubdiv; kb += kRound) {
+    const int k0 = kb + r * kU;  // this lane's first knot
+    double px[kU][3], dk[kU], pp[3];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) spline_eval(sp, kSplineT.t[k0 + u], px[u]);
+    // knot k0 - 1: the previous lane's last knot, or the previous round's end
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double up = __shfl_sync(0xffffffffu, px[kU - 1][k], (lane + 31) & 31);  // lane - 1
+      pp[k] = r == 0 ? p_end[k] : up;
+    }
+    dk[0] = dist3_rn(px[0], pp);
+#pragma unroll
+    for (int u = 1; u < kU; ++u) dk[u] = dist3_rn(px[u], px[u - 1]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p_end[k] = __shfl_sync(0xffffffffu, px[kU - 1][k], base + kQ - 1);
+    // every lane of the quad walks the round's chords in knot order; cum is
+    // non-decreasing, so a round whose last cumulative length is below the
+    // next target emits nothing and needs only its sums
+    double dr[kRound];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+#pragma unroll
+      for (int u = 0; u < kU; ++u) dr[q * kU + u] = __shfl_sync(0xffffffffu, dk[u], base + q);
+    double cum_end = cum_prev;
+#pragma unroll
+    for (int j = 0; j < kRound; ++j) cum_end = __dadd_rn(cum_end, dr[j]);
+    if (!(cum_end >= sv)) {
+      cum_prev = cum_end;
+      continue;
+    }
+#pragma unroll 1
+    for (int j = 0; j < kRound; ++j) {
+      {
+        const double d = dr[j];
+        const int k = kb + j;
+        const double cum_k = __dadd_rn(cum_prev, d);
+        while (cum_k >= sv) {  // the reference's while loop stops at seg = k - 1 for this s
+          const double seg_len = __dadd_rn(cum_k, -cum_prev);
+          const double frac = seg_len > 0.0 ? __dadd_rn(sv, -cum_prev) / seg_len : 0.0;
+          const double tw = __dmul_rn(1.0, __dadd_rn((double)(k - 1), frac)) / (double)kSplineSubdiv;
+          double wv[3];
+          spline_eval(sp, tw, wv);
+          if (writer && tentative < cap) {
+            out[3 * tentative + 0] = (float)wv[0];
+            out[3 * tentative + 1] = (float)wv[1];
+            out[3 * tentative + 2] = (float)wv[2];
+          }
+          s_emit[tentative & 1] = sv;
+          ++tentative;
+          sv = __dadd_rn(sv, spacing);
+        }
+        cum_prev = cum_k;
+      }
+    }
+  }
+  if (!writer) return;
+  const double total = cum_prev;
+  int count = 1;
+  if (total > 1e-12) {
+    const double limit = __dadd_rn(total, -1e-12);
+    count = tentative;
+    while (count > 1 && !(s_emit[(count - 1) & 1] < limit)) --count;  // drop s >= total - 1e-12
+    if (count >= cap) {
+      err |= kErrWaypointCap;
+      count = cap;
+    } else {
+      out[3 * count + 0] = (float)p_end[0];  // pts[1000]
+      out[3 * count + 1] = (float)p_end[1];
+      out[3 * count + 2] = (float)p_end[2];
+      count += 1;
+    }
+  }
+  P.p.rec_len[i] = count;
   P.p.rec_err[i] = err;
   P.p.rec_rng[i] = s;
   P.p.rec_valid[i] = 1;
