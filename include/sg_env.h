@@ -260,6 +260,17 @@ int sg_compute_gae(const float* d_rewards, const float* d_values, const uint8_t*
                    const uint8_t* d_timed_out, const float* d_bootstrap, const float* d_last_values,
                    const float* d_task_error, int32_t n_steps, int64_t n_envs, double gamma, double lambda,
                    float* d_advantages, float* d_returns, float* d_ep_acc, double* d_stats4, void* stream);
+/* ppo_update's optimizer step (ppo.cpp:199-207) on a flat fp32 parameter
+ * vector: global-norm clip of d_grad to max_grad_norm (when larger), Adam with
+ * the reference's bias correction (Adam::step, ppo.cpp:56-64; m, v state,
+ * step counter *d_step incremented on device), box projection of the log-std
+ * segment [log_std_offset, +log_std_n) to [log_std_min, log_std_max], d_grad
+ * zeroed, and (if non-NULL) a bf16 copy of the new parameters written to
+ * d_bf16_mirror. d_grad_sq: one float of scratch. Graph-capturable. */
+int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d_bf16_mirror, int64_t n,
+                 float* d_grad_sq, int32_t* d_step, double lr, double beta1, double beta2, double eps,
+                 double max_grad_norm, int64_t log_std_offset, int32_t log_std_n, double log_std_min,
+                 double log_std_max, void* stream);
 const char* sg_policy_last_error(void);
 
 const char* sg_last_error(void);

@@ -564,7 +564,79 @@ int fail(int code, const std::string& m) {
 }
 }  // namespace
 
+namespace sgp {
+
+// ---- ppo_update's optimizer step (ppo.cpp:199-207, Adam::step :56-64) -------
+// grad_sq: global sum of squared gradients; the Adam kernel applies the clip
+// scale max_norm / norm (when norm > max_norm), the reference's Adam with
+// bias correction, the log-std box projection, and refreshes the bf16 mirror
+// of the parameters the next minibatch's GEMMs read.
+__global__ void grad_sq_kernel(const float* __restrict__ g, int64_t n, float* __restrict__ out, int32_t* step) {
+  float acc = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc = fmaf(g[i], g[i], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ float part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) atomicAdd(out, acc);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(step, 1);  // Adam::step ++t_
+}
+
+struct AdamArgs {
+  float lr, beta1, beta2, eps, max_norm;
+  int64_t ls_off;
+  int32_t ls_n;
+  float ls_min, ls_max;
+};
+
+__global__ void adam_kernel(float* __restrict__ p, float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
+                            __nv_bfloat16* __restrict__ mirror, int64_t n, const float* __restrict__ grad_sq,
+                            const int32_t* __restrict__ step, const __grid_constant__ AdamArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float norm = sqrtf(*grad_sq);
+  const float scale = (a.max_norm > 0.f && norm > a.max_norm) ? a.max_norm / norm : 1.f;
+  const int t = *step;
+  const float bc1 = 1.f - powf(a.beta1, (float)t), bc2 = 1.f - powf(a.beta2, (float)t);
+  const float gi = g[i] * scale;
+  const float mi = fmaf(a.beta1, m[i], (1.f - a.beta1) * gi);
+  const float vi = fmaf(a.beta2, v[i], (1.f - a.beta2) * gi * gi);
+  m[i] = mi;
+  v[i] = vi;
+  float pi = p[i] - a.lr * (mi / bc1) / (sqrtf(vi / bc2) + a.eps);
+  if (i >= a.ls_off && i < a.ls_off + a.ls_n) pi = fminf(fmaxf(pi, a.ls_min), a.ls_max);
+  p[i] = pi;
+  g[i] = 0.f;  // ready for the next minibatch's accumulation
+  if (mirror) mirror[i] = __float2bfloat16_rn(pi);
+}
+
+}  // namespace sgp
+
 extern "C" {
+
+int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d_bf16_mirror, int64_t n,
+                 float* d_grad_sq, int32_t* d_step, double lr, double beta1, double beta2, double eps,
+                 double max_grad_norm, int64_t log_std_offset, int32_t log_std_n, double log_std_min,
+                 double log_std_max, void* stream) {
+  const cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(d_grad_sq, 0, sizeof(float), st);
+  sgp::grad_sq_kernel<<<148, 512, 0, st>>>(d_grad, n, d_grad_sq, d_step);
+  const sgp::AdamArgs a{(float)lr, (float)beta1, (float)beta2, (float)eps, (float)max_grad_norm, log_std_offset,
+                        log_std_n, (float)log_std_min, (float)log_std_max};
+  const int b = 256;
+  sgp::adam_kernel<<<(unsigned)((n + b - 1) / b), b, 0, st>>>(d_params, d_grad, d_m, d_v,
+                                                               (__nv_bfloat16*)d_bf16_mirror, n, d_grad_sq, d_step, a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
 
 const char* sg_policy_last_error(void) { return g_policy_err.c_str(); }
 

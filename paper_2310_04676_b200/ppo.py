@@ -105,9 +105,14 @@ class _Linear(torch.autograd.Function):
     _ones: dict = {}
 
     @staticmethod
-    def forward(ctx, x, W, b):
-        ctx.save_for_backward(x, W)
-        return torch.addmm(b, x, W.t())
+    def forward(ctx, x, W, b, Wc=None, bc=None):
+        # Wc / bc: compute copies (the bf16 mirror the fused Adam step keeps
+        # current); gradients still flow to the fp32 leaves W / b
+        Wc = W if Wc is None else Wc
+        bc = b if bc is None else bc
+        ctx.w_dtype = W.dtype
+        ctx.save_for_backward(x, Wc)
+        return torch.addmm(bc, x, Wc.t())
 
     @staticmethod
     def backward(ctx, gy):
@@ -125,13 +130,15 @@ class _Linear(torch.autograd.Function):
         if ones is None:
             ones = _Linear._ones[key] = torch.ones(1, B, dtype=gy.dtype, device=gy.device)
         gb = (ones @ gy).view(-1)
-        return gx, gW, gb
+        return gx, gW.to(ctx.w_dtype), gb.to(ctx.w_dtype), None, None
 
 
-def _linear(x, W, b):
+def _linear(x, W, b, Wm=None, bm=None):
     if torch.is_autocast_enabled():
-        dt = torch.get_autocast_gpu_dtype()
+        dt = torch.get_autocast_dtype("cuda")
         with torch.autocast("cuda", enabled=False):
+            if Wm is not None and Wm.dtype == dt:
+                return _Linear.apply(x.to(dt), W, b, Wm, bm)
             return _Linear.apply(x.to(dt), W.to(dt), b.to(dt))
     return _Linear.apply(x, W, b)
 
@@ -193,12 +200,12 @@ def mlp_forward(params: torch.Tensor, obs: torch.Tensor, obs_dim: int, act_dim: 
 
 
 def mlp_layers(layers, obs):
+    """layers[k] = (W, b) or (W, b, W_bf16_mirror, b_bf16_mirror)."""
     outs = []
     for trunk in (0, 1):
         h = obs
         for l in range(4):
-            W, b = layers[4 * trunk + l]
-            h = _linear(h, W, b)
+            h = _linear(h, *layers[4 * trunk + l])
             if l < 3:
                 h = F.elu(h)
         outs.append(h)
@@ -276,18 +283,30 @@ class Trainer:
         self.ls_off = ls_pad
         self.O_pad = _up8(O)
         self.layers = []
+        # bf16 update: the fused Adam step (sg_adam_step) keeps a bf16 mirror
+        # of the master parameters for the GEMMs (no per-call weight casts)
+        self.mirror = (torch.zeros(total, device=dev, dtype=torch.bfloat16)
+                       if cfg.update_precision == "bf16" else None)
         for (w0, o, i), (b0, ob) in layout:
             W = self.params[w0: w0 + o * i].view(o, i).detach().requires_grad_(True)
             b = self.params[b0: b0 + ob].detach().requires_grad_(True)
             W.grad = self.grad[w0: w0 + o * i].view(o, i)
             b.grad = self.grad[b0: b0 + ob]
-            self.layers.append((W, b))
+            if self.mirror is not None:
+                self.layers.append((W, b, self.mirror[w0: w0 + o * i].view(o, i), self.mirror[b0: b0 + ob]))
+            else:
+                self.layers.append((W, b))
         self.log_std = self.params[self.ls_off: self.ls_off + A].detach().requires_grad_(True)
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]
         single = dist is None or not dist.is_initialized() or dist.get_world_size() == 1
         self.use_graph = cfg.cuda_graph and single
-        self.opt = torch.optim.Adam([self.params], lr=cfg.learning_rate, betas=(0.9, 0.999), eps=1e-8,
-                                    capturable=self.use_graph)
+        # Adam state (ppo.cpp:50-64) for the fused optimizer step
+        self.adam_m = torch.zeros_like(self.params)
+        self.adam_v = torch.zeros_like(self.params)
+        self.adam_t = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.grad_sq = torch.zeros(1, device=dev)
+        if self.mirror is not None:
+            self.mirror.copy_(self.params)
         policy.load_params(self.ref_params())
         self.perms = torch.empty(cfg.epochs, T * N, dtype=torch.int64, device=dev)
         self.g_metrics = torch.zeros(5, device=dev)
@@ -372,7 +391,7 @@ class Trainer:
         for e in range(cfg.epochs):
             for start in range(0, cap, mb):
                 idx = perms[e, start: start + mb]
-                self.grad.zero_()
+                # (self.grad is zero here: initially, and after every fused Adam step)
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
                     mean, value = mlp_layers(self.layers, obs.index_select(0, idx))
                     loss, m = loss_head(mean[:, :self.A].float(), value.float(), self.log_std,
@@ -380,13 +399,20 @@ class Trainer:
                                         logp.index_select(0, idx), adv.index_select(0, idx),
                                         ret.index_select(0, idx), cfg)
                 loss.backward()
-                g = self.grad
-                allreduce_mean_(g, self.dist)
-                if cfg.max_grad_norm > 0:  # global-norm clip without a host read
-                    g.mul_(torch.clamp(cfg.max_grad_norm / g.norm(), max=1.0))
-                self.opt.step()
-                self.params[self.ls_off: self.ls_off + self.A].clamp_(LOG_STD_MIN, LOG_STD_MAX)
+                allreduce_mean_(self.grad, self.dist)
+                self._adam_step()
                 metrics += m
+
+    def _adam_step(self) -> None:
+        """Global-norm clip (ppo.cpp:201-204), Adam::step (ppo.cpp:56-64),
+        log-std box projection (:206-207), gradient reset and bf16 mirror
+        refresh in two kernels (sg_adam_step), no host synchronisation."""
+        cfg = self.cfg
+        sg._pcheck(sg.lib().sg_adam_step(
+            self.params.data_ptr(), self.grad.data_ptr(), self.adam_m.data_ptr(), self.adam_v.data_ptr(),
+            self.mirror.data_ptr() if self.mirror is not None else None, self.params.numel(),
+            self.grad_sq.data_ptr(), self.adam_t.data_ptr(), cfg.learning_rate, 0.9, 0.999, 1e-8,
+            cfg.max_grad_norm, self.ls_off, self.A, LOG_STD_MIN, LOG_STD_MAX, self._stream()))
 
     def _new_perms(self) -> None:
         cap = self.T * self.N
@@ -398,10 +424,7 @@ class Trainer:
         backward, clip, Adam, log-std clamp) in one CUDA graph so the host no
         longer paces ~2000 small launches. Warm-up runs on saved copies of the
         parameters / optimizer state, which are restored before training."""
-        saved_p = self.params.clone()
-        self.opt.step()  # materialise optimizer state (grad is zero here)
-        saved_state = {k: (v.clone() if torch.is_tensor(v) else v)
-                       for k, v in self.opt.state[self.params].items()}
+        saved = [t.clone() for t in (self.params, self.adam_m, self.adam_v, self.adam_t)]
         side = torch.cuda.Stream(self.dev)
         side.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(side):
@@ -413,13 +436,10 @@ class Trainer:
         with torch.cuda.graph(self.graph):
             self._update_body(self.perms, self.g_metrics)
         with torch.no_grad():
-            self.params.copy_(saved_p)
-            for k, v in saved_state.items():
-                if torch.is_tensor(v):
-                    self.opt.state[self.params][k].copy_(v)
-            # the materialising step above was the optimizer's first: the real
-            # first update must see t = 1 (Adam::step, ppo.cpp:56-64)
-            self.opt.state[self.params]["step"].zero_()
+            for t, v in zip((self.params, self.adam_m, self.adam_v, self.adam_t), saved):
+                t.copy_(v)
+            if self.mirror is not None:
+                self.mirror.copy_(self.params)
         self.grad.zero_()
 
     def update(self):

@@ -126,6 +126,9 @@ _SIGS = {
                                       C.c_void_p, C.c_void_p]),
     "sg_policy_sample": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_uint64, C.c_uint64,
                                    C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                               C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
+                               C.c_int32, C.c_double, C.c_double, C.c_void_p]),
     "sg_compute_gae": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

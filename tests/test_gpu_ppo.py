@@ -82,3 +82,59 @@ def test_ppo_trainer_runs_and_learns_signal(sg):
     assert -5.0 <= hist[-1]["log_std_mean"] <= 2.0
     # the critic fits returns: value loss falls from the first to the last iteration
     assert hist[-1]["value_loss"] < hist[0]["value_loss"]
+
+
+def test_fused_adam_step_matches_reference_formulas(sg):
+    """sg_adam_step == ppo.cpp:199-207 (clip to max_grad_norm when the norm
+    exceeds it) + Adam::step (ppo.cpp:56-64) + log-std projection, restated in
+    fp64 numpy, over steps with gradients above and below the clip norm;
+    the gradient is zeroed and the bf16 mirror refreshed."""
+    rng = np.random.default_rng(3)
+    n, ls_off, ls_n = 5000, 4990, 7
+    p = rng.normal(size=n)
+    p[ls_off: ls_off + ls_n] = [-4.9, 1.95, 0.0, -1.0, 1.99, -4.99, 0.5]
+    m = np.zeros(n); v = np.zeros(n)
+    P = torch.tensor(p, dtype=torch.float32, device="cuda")
+    G = torch.zeros(n, device="cuda")
+    M, V = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    mirror = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
+    t = torch.zeros(1, dtype=torch.int32, device="cuda")
+    gsq = torch.zeros(1, device="cuda")
+    lr, b1, b2, eps, max_norm = 1e-2, 0.9, 0.999, 1e-8, 1.0
+    for step, gscale in enumerate((0.001, 1.0, 0.003, 5.0), start=1):
+        g = rng.normal(size=n) * gscale
+        G.copy_(torch.tensor(g, dtype=torch.float32))
+        sg._pcheck(sg.lib().sg_adam_step(P.data_ptr(), G.data_ptr(), M.data_ptr(), V.data_ptr(), mirror.data_ptr(),
+                                         n, gsq.data_ptr(), t.data_ptr(), lr, b1, b2, eps, max_norm, ls_off, ls_n,
+                                         -5.0, 2.0, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        g = g.astype(np.float32).astype(np.float64)
+        norm = np.linalg.norm(g)
+        if norm > max_norm:
+            g *= max_norm / norm
+        m = b1 * m + (1 - b1) * g
+        v = b2 * v + (1 - b2) * g * g
+        p = p - lr * (m / (1 - b1 ** step)) / (np.sqrt(v / (1 - b2 ** step)) + eps)
+        p[ls_off: ls_off + ls_n] = np.clip(p[ls_off: ls_off + ls_n], -5.0, 2.0)
+        assert t.item() == step
+        np.testing.assert_allclose(P.cpu().numpy(), p, rtol=2e-5, atol=2e-6)
+        assert not G.any()
+        assert torch.equal(mirror, P.to(torch.bfloat16))
+        p = P.cpu().numpy().astype(np.float64)  # continue from the device's fp32 state
+        m = M.cpu().numpy().astype(np.float64)
+        v = V.cpu().numpy().astype(np.float64)
+
+
+def test_ppo_trainer_bf16_update_runs(sg):
+    """The bench's update precision: bf16 GEMMs on the fused-Adam bf16 mirror,
+    captured in a CUDA graph."""
+    from paper_2310_04676_b200 import ppo
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=4096, seed=0, episode_len=60)
+    pol = sg.Policy(env.obs_dim, env.action_dim)
+    tr = ppo.Trainer(env, pol, ppo.TrainConfig(seed=0, n_steps=32, update_precision="bf16"))
+    hist = [tr.iterate() for _ in range(4)]
+    for h in hist:
+        for k in ("policy_loss", "value_loss", "kl", "mean_step_reward"):
+            assert math.isfinite(h[k]), (k, h)
+    assert torch.equal(tr.mirror, tr.params.to(torch.bfloat16))
+    assert hist[-1]["value_loss"] < hist[0]["value_loss"]
