@@ -271,6 +271,20 @@ int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d
                  float* d_grad_sq, int32_t* d_step, double lr, double beta1, double beta2, double eps,
                  double max_grad_norm, int64_t log_std_offset, int32_t log_std_n, double log_std_min,
                  double log_std_max, void* stream);
+/* Policy checkpoints in the reference's versioned binary format
+ * (save_checkpoint / load_checkpoint, src/policy.cpp:220-295): "SCLPCKP1",
+ * u32 version 1, obs_dim, action_dim, n_hidden, hidden[], length-prefixed
+ * robot and task names, u64 param count, the flat parameter vector as
+ * little-endian fp64 (reference layout, policy.cpp:42-63). load: any pointer
+ * may be NULL (header-only read); hidden must hold 64 entries; the reference's
+ * ConfigError messages (not a checkpoint, version, corrupt, truncated, count
+ * mismatch) come back as SG_ERR_CONFIG. */
+int sg_checkpoint_save(const char* path, int32_t obs_dim, int32_t action_dim, const int32_t* hidden,
+                       int32_t n_hidden, const char* robot, const char* task, const double* h_params,
+                       int64_t param_count);
+int sg_checkpoint_load(const char* path, int32_t* obs_dim, int32_t* action_dim, int32_t* hidden, int32_t* n_hidden,
+                       char* robot, int32_t robot_cap, char* task, int32_t task_cap, double* h_params,
+                       int64_t params_cap, int64_t* param_count);
 const char* sg_policy_last_error(void);
 
 const char* sg_last_error(void);

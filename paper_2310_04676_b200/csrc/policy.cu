@@ -22,6 +22,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -802,6 +803,118 @@ int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const f
       d_mean, n, action_dim, d_log_std_raw, stream_state, stream_inc, d_draw_pos, step_offset, J, d_actions, d_logp);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+// ---- checkpoints (save_checkpoint / load_checkpoint, policy.cpp:220-295) ---
+// Byte layout of the reference: "SCLPCKP1", u32 version 1, u32 obs_dim,
+// u32 action_dim, u32 n_hidden, n_hidden x u32, u32-length-prefixed robot and
+// task strings, u64 param count, param_count little-endian fp64.
+namespace {
+constexpr char kCkptMagic[8] = {'S', 'C', 'L', 'P', 'C', 'K', 'P', '1'};
+constexpr uint32_t kCkptVersion = 1;
+
+int64_t trunk_param_count(int obs_dim, int act_dim, const int32_t* hidden, int n_hidden) {
+  int64_t total = 0;
+  for (int trunk = 0; trunk < 2; ++trunk) {  // Policy::Policy (policy.cpp:42-63)
+    int in = obs_dim;
+    for (int l = 0; l <= n_hidden; ++l) {
+      const int out = l < n_hidden ? hidden[l] : (trunk == 0 ? act_dim : 1);
+      total += (int64_t)out * in + out;
+      in = out;
+    }
+  }
+  return total + act_dim;  // log_std
+}
+}  // namespace
+
+int sg_checkpoint_save(const char* path, int32_t obs_dim, int32_t action_dim, const int32_t* hidden,
+                       int32_t n_hidden, const char* robot, const char* task, const double* h_params,
+                       int64_t param_count) {
+  if (param_count != trunk_param_count(obs_dim, action_dim, hidden, n_hidden))
+    return fail(SG_ERR_CONFIG, "checkpoint: parameter count does not match the shape");
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(SG_ERR_SIM, std::string("cannot write checkpoint '") + path + "'");
+  bool ok = std::fwrite(kCkptMagic, 1, 8, f) == 8;
+  const auto u32 = [&](uint32_t v) { ok = ok && std::fwrite(&v, 4, 1, f) == 1; };
+  const auto str = [&](const char* c) {
+    const std::string v = c ? c : "";
+    u32(static_cast<uint32_t>(v.size()));
+    ok = ok && std::fwrite(v.data(), 1, v.size(), f) == v.size();
+  };
+  u32(kCkptVersion);
+  u32(static_cast<uint32_t>(obs_dim));
+  u32(static_cast<uint32_t>(action_dim));
+  u32(static_cast<uint32_t>(n_hidden));
+  for (int i = 0; i < n_hidden; ++i) u32(static_cast<uint32_t>(hidden[i]));
+  str(robot);
+  str(task);
+  const uint64_t cnt = static_cast<uint64_t>(param_count);
+  ok = ok && std::fwrite(&cnt, 8, 1, f) == 1;
+  ok = ok && std::fwrite(h_params, sizeof(double), param_count, f) == static_cast<size_t>(param_count);
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) return fail(SG_ERR_SIM, std::string("short write on checkpoint '") + path + "'");
+  return SG_OK;
+}
+
+int sg_checkpoint_load(const char* path, int32_t* obs_dim, int32_t* action_dim, int32_t* hidden, int32_t* n_hidden,
+                       char* robot, int32_t robot_cap, char* task, int32_t task_cap, double* h_params,
+                       int64_t params_cap, int64_t* param_count) {
+  FILE* f = std::fopen(path, "rb");
+  const std::string p = path;
+  if (!f) return fail(SG_ERR_CONFIG, "cannot open checkpoint '" + p + "'");
+  struct Closer {
+    FILE* f;
+    ~Closer() { std::fclose(f); }
+  } closer{f};
+  bool ok = true;
+  const auto u32 = [&]() {
+    uint32_t v = 0;
+    ok = ok && std::fread(&v, 4, 1, f) == 1;
+    return v;
+  };
+  char magic[8];
+  if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kCkptMagic, 8) != 0)
+    return fail(SG_ERR_CONFIG, "'" + p + "' is not a scalpel checkpoint");
+  const uint32_t version = u32();
+  if (version != kCkptVersion)
+    return fail(SG_ERR_CONFIG, "checkpoint '" + p + "' has unsupported version " + std::to_string(version));
+  const int od = static_cast<int>(u32()), ad = static_cast<int>(u32());
+  const uint32_t nh = u32();
+  if (!ok || nh > 64) return fail(SG_ERR_CONFIG, "corrupt checkpoint '" + p + "'");
+  std::vector<int32_t> hid(nh);
+  for (auto& h : hid) h = static_cast<int32_t>(u32());
+  std::string strs[2];
+  for (auto& s : strs) {
+    const uint32_t len = u32();
+    if (!ok || len > (1u << 20)) return fail(SG_ERR_CONFIG, "corrupt checkpoint '" + p + "'");
+    s.resize(len);
+    ok = ok && std::fread(s.data(), 1, len, f) == len;
+  }
+  uint64_t cnt = 0;
+  ok = ok && std::fread(&cnt, 8, 1, f) == 1;
+  if (!ok) return fail(SG_ERR_CONFIG, "checkpoint '" + p + "' is truncated");
+  if (static_cast<int64_t>(cnt) != trunk_param_count(od, ad, hid.data(), static_cast<int>(nh)))
+    return fail(SG_ERR_CONFIG, "checkpoint '" + p + "' parameter count does not match its shape header");
+  if (obs_dim) *obs_dim = od;
+  if (action_dim) *action_dim = ad;
+  if (n_hidden) *n_hidden = static_cast<int32_t>(nh);
+  if (hidden)
+    for (uint32_t i = 0; i < nh && i < 64; ++i) hidden[i] = hid[i];
+  const auto put = [](char* dst, int32_t cap, const std::string& v) {
+    if (!dst || cap <= 0) return;
+    const size_t k = std::min(v.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(dst, v.data(), k);
+    dst[k] = '\0';
+  };
+  put(robot, robot_cap, strs[0]);
+  put(task, task_cap, strs[1]);
+  if (param_count) *param_count = static_cast<int64_t>(cnt);
+  if (h_params) {
+    if (params_cap < static_cast<int64_t>(cnt)) return fail(SG_ERR_CONFIG, "checkpoint: parameter buffer too small");
+    if (std::fread(h_params, sizeof(double), cnt, f) != cnt)
+      return fail(SG_ERR_CONFIG, "checkpoint '" + p + "' is truncated");
+  }
+  return SG_OK;
 }
 
 int sg_compute_gae(const float* d_rewards, const float* d_values, const uint8_t* d_terminated,

@@ -466,6 +466,27 @@ class Trainer:
         self.policy.load_params(self.ref_params())
         return metrics / (cfg.epochs * cfg.minibatch_count)
 
+    def save_checkpoint(self, path: str, robot: str, task: str = "target_reaching") -> None:
+        """The current policy as a reference checkpoint (policy.cpp:220-242),
+        readable by the reference's load_checkpoint / evaluate_policy."""
+        sg.save_checkpoint(path, self.ref_params().double().cpu().numpy(), self.O, self.A, robot, task)
+
+    def load_checkpoint(self, path: str) -> dict:
+        """Initialise the policy from a reference checkpoint (load_checkpoint,
+        policy.cpp:244-295); Adam state restarts (the reference does not store it)."""
+        meta, p = sg.load_checkpoint(path)
+        if (meta["obs_dim"], meta["action_dim"], meta["hidden"]) != (self.O, self.A, (256, 128, 64)):
+            raise sg.ConfigError(f"checkpoint '{path}' shape {meta} does not match this trainer")
+        with torch.no_grad():
+            self.params[self.ref_to_pad] = torch.from_numpy(p).float().to(self.dev)
+            self.adam_m.zero_()
+            self.adam_v.zero_()
+            self.adam_t.zero_()
+            if self.mirror is not None:
+                self.mirror.copy_(self.params)
+        self.policy.load_params(self.ref_params())
+        return meta
+
     def iterate(self) -> dict:
         self.rollout()
         self.gae()

@@ -129,6 +129,10 @@ _SIGS = {
     "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p]),
+    "sg_checkpoint_save": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_char_p,
+                                     C.c_char_p, C.c_void_p, C.c_int64]),
+    "sg_checkpoint_load": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p,
+                                     C.c_int32, C.c_char_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
     "sg_compute_gae": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -465,3 +469,30 @@ class Policy:
         _pcheck(lib().sg_policy_forward(self._h, obs.data_ptr(), n, obs.stride(0), mean.data_ptr(),
                                         value.data_ptr(), stream))
         return mean, value
+
+
+# -- checkpoints (save_checkpoint / load_checkpoint, policy.cpp:220-295) -------
+def save_checkpoint(path: str, params, obs_dim: int, action_dim: int, robot: str, task: str,
+                    hidden=(256, 128, 64)) -> None:
+    """Write the reference's SCLPCKP1 checkpoint from a flat parameter vector
+    in the reference layout (any array-like; stored as fp64)."""
+    p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(-1))
+    hid = (C.c_int32 * len(hidden))(*hidden)
+    _pcheck(lib().sg_checkpoint_save(path.encode(), obs_dim, action_dim, hid, len(hidden), robot.encode(),
+                                     task.encode(), p.ctypes.data, p.size))
+
+
+def load_checkpoint(path: str) -> tuple[dict, np.ndarray]:
+    """Read a SCLPCKP1 checkpoint: (meta {obs_dim, action_dim, hidden, robot,
+    task}, fp64 flat parameters in the reference layout)."""
+    od, ad, nh, cnt = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+    hid = (C.c_int32 * 64)()
+    robot, task = C.create_string_buffer(1 << 12), C.create_string_buffer(1 << 12)
+    _pcheck(lib().sg_checkpoint_load(path.encode(), C.byref(od), C.byref(ad), hid, C.byref(nh), robot, 1 << 12,
+                                     task, 1 << 12, None, 0, C.byref(cnt)))
+    params = np.empty(cnt.value, np.float64)
+    _pcheck(lib().sg_checkpoint_load(path.encode(), None, None, None, None, None, 0, None, 0, params.ctypes.data,
+                                     params.size, None))
+    meta = dict(obs_dim=od.value, action_dim=ad.value, hidden=tuple(hid[: nh.value]), robot=robot.value.decode(),
+                task=task.value.decode())
+    return meta, params

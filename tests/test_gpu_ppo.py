@@ -138,3 +138,27 @@ def test_ppo_trainer_bf16_update_runs(sg):
             assert math.isfinite(h[k]), (k, h)
     assert torch.equal(tr.mirror, tr.params.to(torch.bfloat16))
     assert hist[-1]["value_loss"] < hist[0]["value_loss"]
+
+
+def test_trainer_checkpoint_round_trip(sg, tmp_path):
+    """Trainer.save_checkpoint writes the reference format; a second trainer
+    loading it has the same reference-layout parameters and policy outputs."""
+    from paper_2310_04676_b200 import ppo
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=1024, seed=1)
+    a = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim), ppo.TrainConfig(seed=3))
+    a.iterate()
+    path = str(tmp_path / "psm.ckpt")
+    a.save_checkpoint(path, "psm")
+    env2 = sg.VecTaskEnv(robots=("psm",), n_envs=1024, seed=1)
+    pol2 = sg.Policy(env2.obs_dim, env2.action_dim)
+    b = ppo.Trainer(env2, pol2, ppo.TrainConfig(seed=9))
+    meta = b.load_checkpoint(path)
+    assert meta["robot"] == "psm" and meta["hidden"] == (256, 128, 64)
+    assert torch.equal(a.ref_params(), b.ref_params())
+    obs = env.reset()
+    m1, v1 = torch.empty(1024, 7, device="cuda"), torch.empty(1024, device="cuda")
+    m2, v2 = torch.empty_like(m1), torch.empty_like(v1)
+    a.policy.forward(obs, m1, v1)
+    pol2.forward(obs, m2, v2)
+    torch.cuda.synchronize()
+    assert torch.equal(m1, m2) and torch.equal(v1, v2)
