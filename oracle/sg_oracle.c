@@ -897,6 +897,7 @@ struct sgo_env {
   sgo_pcg32* rng;
   /* TaskState */
   real* goals;
+  real *goal_spawn, *goal_vel; /* ActiveTracking (envs.cpp:199-201) */
   int32_t *step_count, *hold_count, *wp_idx, *wp_len;
   int64_t* episode_count;
   real* wps; /* n x WP_CAP x 3 */
@@ -976,10 +977,16 @@ static int reset_row(sgo_env* e, int64_t row) { /* envs.cpp:304-360 */
     e->qt[row * A + d] = e->q[row * A + d];
   }
   refresh_tip(e, row);
-  if (e->cfg.task == SGO_TARGET_REACHING) {
+  if (e->cfg.task == SGO_TARGET_REACHING || e->cfg.task == SGO_ACTIVE_TRACKING) {
     double g[3];
     if (sample_goal(e, r, g)) return 2;
     for (int k = 0; k < 3; ++k) e->goals[row * 3 + k] = (real)g[k];
+    if (e->cfg.task == SGO_ACTIVE_TRACKING) { /* envs.cpp:322-327 */
+      for (int k = 0; k < 3; ++k) {
+        e->goal_spawn[row * 3 + k] = (real)g[k];
+        e->goal_vel[row * 3 + k] = 0;
+      }
+    }
   } else { /* PathFollowing */
     int rc = sample_path(e, row);
     if (rc) return rc;
@@ -999,7 +1006,7 @@ static void observe_row(sgo_env* e, int64_t row, real* dst) { /* envs.cpp:362-40
   for (int d = 0; d < A; ++d) out[off++] = e->qd[row * A + d];
   for (int k = 0; k < 3; ++k) out[off++] = e->tips[row * 3 + k];
   for (int d = 0; d < A; ++d) out[off++] = e->qt[row * A + d];
-  if (e->cfg.task == SGO_TARGET_REACHING) {
+  if (e->cfg.task == SGO_TARGET_REACHING || e->cfg.task == SGO_ACTIVE_TRACKING) {
     for (int k = 0; k < 3; ++k) out[off++] = e->goals[row * 3 + k];
   } else {
     const real* wp = e->wps + (row * WP_CAP + e->wp_idx[row]) * 3;
@@ -1047,6 +1054,23 @@ static void phase_reward(void* ctx, int64_t b, int64_t end) { /* envs.cpp:478-59
       e->task_error[i] = dist;
       e->hold_count[i] = dist < sr ? e->hold_count[i] + 1 : 0;
       goal_met = e->hold_count[i] >= e->cfg.success_hold;
+    } else if (e->cfg.task == SGO_ACTIVE_TRACKING) { /* envs.cpp:493-512 */
+      real* g = e->goals + i * 3;
+      const real dist = dist3(tip, g);
+      reward = rho * dist;
+      e->task_error[i] = dist;
+      /* the goal drifts after the reward is scored */
+      sgo_pcg32* r = &e->rng[i];
+      real* vel = e->goal_vel + i * 3;
+      const real* spawn = e->goal_spawn + i * 3;
+      const real clip = (real)e->cfg.goal_offset_clip, vc = (real)e->cfg.tracking_vel_clamp;
+      for (int k = 0; k < 3; ++k) g[k] += vel[k];
+      for (int k = 0; k < 3; ++k) {
+        const real lo = spawn[k] - clip, hi = spawn[k] + clip;
+        g[k] = g[k] < lo ? lo : (hi < g[k] ? hi : g[k]); /* std::clamp */
+        vel[k] += (real)(0.0 + e->cfg.tracking_vel_noise_std * sgo_pcg32_normal(r)); /* normal(0, std) */
+        vel[k] = vel[k] < -vc ? -vc : (vc < vel[k] ? vc : vel[k]);
+      }
     } else { /* PathFollowing, envs.cpp:524-539 */
       const real* wps = e->wps + i * WP_CAP * 3;
       int32_t idx = e->wp_idx[i];
@@ -1089,7 +1113,9 @@ sgo_env* sgo_env_create(const sgo_env_cfg* c, const sgo_robot* m, const sgo_dyn*
   if (c->success_hold < 1) { seterr(err, errlen, "env.success_hold must be >= 1"); return NULL; }
   if (!(c->waypoint_spacing > 0.0)) { seterr(err, errlen, "env.waypoint_spacing must be > 0"); return NULL; }
   if (c->workspace_radius < 0.0) { seterr(err, errlen, "env.workspace_radius must be >= 0"); return NULL; }
-  if (c->task != SGO_TARGET_REACHING && c->task != SGO_PATH_FOLLOWING) {
+  if (c->tracking_vel_noise_std < 0.0) { seterr(err, errlen, "env.tracking_vel_noise_std must be >= 0"); return NULL; }
+  if (!(c->tracking_vel_clamp > 0.0)) { seterr(err, errlen, "env.tracking_vel_clamp must be > 0"); return NULL; }
+  if (c->task != SGO_TARGET_REACHING && c->task != SGO_PATH_FOLLOWING && c->task != SGO_ACTIVE_TRACKING) {
     seterr(err, errlen, "oracle: task %d not restated", c->task);
     return NULL;
   }
@@ -1123,6 +1149,10 @@ sgo_env* sgo_env_create(const sgo_env_cfg* c, const sgo_robot* m, const sgo_dyn*
   e->wp_len = (int32_t*)calloc((size_t)n, sizeof(int32_t));
   e->episode_count = (int64_t*)calloc((size_t)n, sizeof(int64_t));
   if (c->task == SGO_PATH_FOLLOWING) e->wps = (real*)calloc((size_t)(n * WP_CAP * 3), sizeof(real));
+  if (c->task == SGO_ACTIVE_TRACKING) {
+    e->goal_spawn = (real*)calloc((size_t)(n * 3), sizeof(real));
+    e->goal_vel = (real*)calloc((size_t)(n * 3), sizeof(real));
+  }
   e->tips = (real*)calloc((size_t)(n * 3), sizeof(real));
   e->obs = (real*)calloc((size_t)(n * O), sizeof(real));
   e->tobs = (real*)calloc((size_t)(n * O), sizeof(real));
@@ -1141,6 +1171,7 @@ void sgo_env_destroy(sgo_env* e) {
   if (!e) return;
   if (e->pool) pool_destroy(e->pool);
   free(e->q); free(e->qd); free(e->qt); free(e->rng); free(e->goals);
+  free(e->goal_spawn); free(e->goal_vel);
   free(e->step_count); free(e->hold_count); free(e->wp_idx); free(e->wp_len);
   free(e->episode_count); free(e->wps); free(e->tips); free(e->obs); free(e->tobs);
   free(e->rewards); free(e->task_error); free(e->terminated); free(e->timed_out);

@@ -255,7 +255,7 @@ struct sg_env {
                     p.episode_count, p.wp_idx,     p.wp_len,     p.wps,      p.rng_state,  p.rng_inc,
                     p.obs, p.tobs,     p.rewards,    p.task_error, p.terminated, p.timed_out, counters,
                     p.act_state, p.act_buf, d_actions_in, p.rec_valid, p.rec_q, p.rec_len, p.rec_err, p.rec_rng,
-                    p.rec_wps};
+                    p.rec_wps, p.goal_spawn, p.goal_vel};
     for (void* b : bufs)
       if (b) cudaFree(b);
   }
@@ -401,9 +401,11 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   } else if (models.size() != 1) {
     throw sg::ConfigError(std::string(task_name(cfg.task)) + " requires exactly 1 robot");
   }
-  if (cfg.task != SG_TASK_TARGET_REACHING && cfg.task != SG_TASK_PATH_FOLLOWING)
+  if (cfg.task != SG_TASK_TARGET_REACHING && cfg.task != SG_TASK_PATH_FOLLOWING &&
+      cfg.task != SG_TASK_ACTIVE_TRACKING)
     throw sg::ConfigError(std::string("task '") + task_name(cfg.task) +
-                          "' is not on the sg_env device path (target_reaching, path_following)");
+                          "' is not on the sg_env device path (target_reaching, active_tracking, "
+                          "path_following)");
 
   auto env = std::make_unique<sg_env>();
   env->model = std::move(models[0]);
@@ -474,6 +476,9 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   T.radius = env->radius;
   for (int k = 0; k < 3; ++k) T.center[k] = env->center[k];
   T.spacing = cfg.waypoint_spacing;
+  T.goal_offset_clip = static_cast<float>(cfg.goal_offset_clip);
+  T.track_noise_std = static_cast<float>(cfg.tracking_vel_noise_std);
+  T.track_vel_clamp = static_cast<float>(cfg.tracking_vel_clamp);
   // Path length bound: |S'(u)| <= 3|a|u^2 + 2|b|u + |c| integrates to
   // |a| + |b| + |c| <= (0.5 + 0.5 + 0.3) * sqrt(3) (coefficient ranges of
   // sample_path, envs.cpp:244-246); shrinking only shortens the path.
@@ -507,6 +512,10 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   p.wp_idx = dalloc<int32_t>(n);
   p.wp_len = dalloc<int32_t>(n);
   p.wps = T.wp_cap ? dalloc<float>(static_cast<size_t>(n) * T.wp_cap * 3) : nullptr;
+  if (cfg.task == SG_TASK_ACTIVE_TRACKING) {
+    p.goal_spawn = dalloc<float>(n * 3);
+    p.goal_vel = dalloc<float>(n * 3);
+  }
   if (T.wp_cap) {  // PathFollowing reset records (kernels.cuh path_record_kernel)
     p.rec_valid = dalloc<uint8_t>(n);
     p.rec_q = dalloc<float>(n * dof);
@@ -555,7 +564,9 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   // kernel selection: compile-time chain structure when the descriptor's
   // structure matches a builtin one and the dynamics are the reference
   // defaults' shape (position control, 4 substeps); generic chain otherwise
-  env->chain = select_chain(P.robot, dc.control_mode, dc.substeps);
+  // ActiveTracking runs on the generic chains (runtime task; no specialised instantiation)
+  env->chain = cfg.task == SG_TASK_ACTIVE_TRACKING ? (P.robot.dof <= 8 ? sg::kChainGeneric8 : sg::kChainGeneric16)
+                                                    : select_chain(P.robot, dc.control_mode, dc.substeps);
   env->team_warps = team_warps_for(env->chain);
   CK(cudaDeviceSynchronize());
   return env;

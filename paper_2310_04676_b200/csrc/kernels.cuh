@@ -28,7 +28,7 @@ constexpr int kSplineSubdiv = 1000;        // spline.cpp:24
 constexpr uint64_t kPcgMult = 6364136223846793005ULL;
 
 enum : int32_t { kRevolute = 0, kPrismatic = 1, kFixed = 2 };
-enum : int32_t { kTaskTarget = 0, kTaskPath = 3 };
+enum : int32_t { kTaskTarget = 0, kTaskTrack = 1, kTaskPath = 3 };
 enum : int32_t { kModePosition = 0, kModeVelocity = 1, kModeTorque = 2 };
 enum : int32_t {
   kErrNonFiniteAction = 1,
@@ -83,6 +83,10 @@ struct TaskParams {
   double radius;        // workspace radius
   double center[3];
   double spacing;
+  // ActiveTracking (envs.cpp:493-512)
+  float goal_offset_clip;
+  float track_noise_std;
+  float track_vel_clamp;
 };
 
 struct EnvPtrs {
@@ -97,6 +101,8 @@ struct EnvPtrs {
   int32_t* wp_idx;
   int32_t* wp_len;
   float* wps;     // [n][wp_cap][3]
+  float* goal_spawn;  // [3][n] ActiveTracking: goal at reset
+  float* goal_vel;    // [3][n] ActiveTracking: goal velocity
   // PathFollowing reset records (nullable): the NEXT reset_row of env i is a
   // function of its PCG32 state only, which changes only at resets, so it is
   // computed ahead by path_record_kernel (full warps, many warps per SM) and
@@ -753,6 +759,13 @@ __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
     goal[0] = (float)g[0];
     goal[1] = (float)g[1];
     goal[2] = (float)g[2];
+    if (task == kTaskTrack) {  // envs.cpp:322-327
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        P.p.goal_spawn[k * n + i] = goal[k];
+        P.p.goal_vel[k * n + i] = 0.f;
+      }
+    }
   }
   P.p.rng_state[i] = s;
   P.p.step_count[i] = 0;
@@ -776,6 +789,41 @@ __device__ __noinline__ int reset_env(const StepParams& P, int64_t i) {
     P.p.wp_len[i] = wp_len;
   }
   return err;
+}
+
+// rng.normal() (rng.hpp:53-57) with the uniforms formed exactly in fp64 and
+// the transform in fp32 (the stream consumption, 2 u32, is exact).
+__device__ __forceinline__ float pcg_normal_f32(uint64_t& s, uint64_t inc) {
+  const uint32_t a = pcg_next(s, inc), b = pcg_next(s, inc);
+  const float u1 = (float)__dmul_rn(__dadd_rn((double)a, 0.5), 0x1.0p-32);  // (0, 1)
+  const float u2 = (float)((double)b * 0x1.0p-32);
+  return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+}
+
+// ActiveTracking goal drift after scoring (envs.cpp:497-510): g += vel; per
+// axis clamp g to spawn +- goal_offset_clip, vel += N(0, noise_std) from the
+// env's stream, clamp vel to +- vel_clamp. Spawn / velocity / stream state
+// live in HBM (the generic-chain kernel runs this task).
+static __device__ __noinline__ void track_drift(const StepParams& P, int64_t i, float* goal) {
+  const TaskParams& T = P.task;
+  const int64_t n = T.n;
+  uint64_t s = P.p.rng_state[i];
+  const uint64_t inc = P.p.rng_inc[i];
+  float vel[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    vel[k] = P.p.goal_vel[k * n + i];
+    goal[k] += vel[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float sp = P.p.goal_spawn[k * n + i];
+    goal[k] = fminf(fmaxf(goal[k], sp - T.goal_offset_clip), sp + T.goal_offset_clip);
+    vel[k] += T.track_noise_std * pcg_normal_f32(s, inc);
+    vel[k] = fminf(fmaxf(vel[k], -T.track_vel_clamp), T.track_vel_clamp);
+    P.p.goal_vel[k * n + i] = vel[k];
+  }
+  P.p.rng_state[i] = s;
 }
 
 // Load one env's state from HBM (DoF-major SoA) into registers.
@@ -1358,6 +1406,12 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
             dcur = sqrtf(dx * dx + dy * dy + dz * dz);
           }
           goal_met = (wi + 1 == wl) && dcur < T.success_radius;
+        } else if (task == kTaskTrack) {
+          // ActiveTracking (envs.cpp:493-512): scored against the current
+          // goal, which then drifts (env stream, 2 u32 per normal)
+          reward = T.rho * dist;
+          goal_met = false;
+          if (active) track_drift(P, i, goal);
         } else {
           reward = T.rho * dist;
           hc = dist < T.success_radius ? hc + 1 : 0;

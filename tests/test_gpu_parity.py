@@ -26,9 +26,10 @@ def _soa(t):  # device SoA (dof x n) -> host (n x dof)
     return t.detach().cpu().numpy().T.astype(np.float64)
 
 
-def _run_pair(sg, oracle, robot, task, n, steps, seed=0, sigma=0.05, check_every=1, actions_fn=None):
+def _run_pair(sg, oracle, robot, task, n, steps, seed=0, sigma=0.05, check_every=1, actions_fn=None, tol=None):
     """Step the device env and the fp64 oracle with the same actions; compare."""
     _cuda()
+    TOL = dict(globals()["TOL"], **(tol or {}))
     m = oracle.resolve_robot(robot)
     ocfg = oracle.env_config(n_envs=n, seed=seed, task=task, goal_sigma=sigma)
     ref = oracle.Env(ocfg, m)
@@ -81,14 +82,14 @@ def _run_pair(sg, oracle, robot, task, n, steps, seed=0, sigma=0.05, check_every
         assert err <= TOL["reward"]
         o_dev = res.observations.cpu().numpy()
         o_ref, t_ref = ref.obs()
-        _compare_obs(o_dev, o_ref, A)
+        _compare_obs(o_dev, o_ref, A, TOL)
         ended = (r["terminated"] | r["timed_out"]).astype(bool)
         if ended.any():
-            _compare_obs(res.terminal_observations.cpu().numpy()[ended], t_ref[ended], A)
+            _compare_obs(res.terminal_observations.cpu().numpy()[ended], t_ref[ended], A, TOL)
     return env, ref, worst
 
 
-def _compare_obs(o_dev, o_ref, A):
+def _compare_obs(o_dev, o_ref, A, TOL=TOL):
     # layout [q | qdot | tip | q_target | goal] (envs.cpp:166-192)
     tol = np.concatenate([np.full(A, TOL["q"]), np.full(A, TOL["qdot"]), np.full(3, TOL["obs_pos"]),
                           np.full(A, TOL["q_target"]), np.full(3, TOL["obs_pos"])])
@@ -105,6 +106,18 @@ def test_config1_psm_reach_1000_steps(sg, oracle):
     c = ref.counters()
     assert (c["episode_count"] == 3).all()
     assert ref.goal_draws() == 264  # 256 resets + 8 rejections (survey probe, Appendix E)
+
+
+def test_active_tracking_drifting_goals(sg, oracle):
+    """ActiveTracking (envs.cpp:493-512): the goal drifts after
+    scoring with velocity noise from the env stream (6 u32 per env-step) and
+    both clamps active; streams, flags and counters bit-exact, goals within
+    2e-5 m (fp32 random walk vs the oracle's fp64) over two reset bursts."""
+    env, ref, worst = _run_pair(sg, oracle, "psm", oracle.ACTIVE_TRACKING, 64, 650, seed=5,
+                                tol=dict(goals=2e-5))
+    c = ref.counters()
+    assert (c["episode_count"] == 2).all() and (c["hold_count"] == 0).all()  # bursts at 300, 600
+    assert worst["goals"] > 0.0
 
 
 def test_ecm_reach(sg, oracle):

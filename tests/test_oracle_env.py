@@ -117,3 +117,27 @@ def test_golden_digests(oracle):
     for case in golden["cases"]:
         got = _digest(oracle, case["robot"], case["task"], case["sigma"], case["n"], case["steps"], case["seed"])
         assert got == case["rows"], case["name"]
+
+
+def test_active_tracking_stream_consumption(oracle):
+    """ActiveTracking (envs.cpp:493-512): after the reset draws, every step
+    takes exactly 3 normals (6 u32) from each env's stream for the goal
+    velocity noise, and goals stay inside spawn +- goal_offset_clip."""
+    m = oracle.resolve_robot("psm")
+    n = 8
+    env = oracle.Env(oracle.env_config(n_envs=n, seed=11, task=oracle.ACTIVE_TRACKING), m)
+    env.reset()
+    s0, inc = env.rng()
+    spawn = env.state()["goals"].copy()
+    rng = oracle.make_stream(0, 0xAC7104)
+    for _ in range(20):
+        env.step(oracle.fill_uniform_actions(rng, n, m.dof))
+    s1, _ = env.rng()
+    for i in range(n):
+        r = oracle.Pcg32(int(s0[i]), int(inc[i]))
+        for _ in range(6 * 20):
+            oracle.next_u32(r)
+        assert r.state == s1[i]
+    g = env.state()["goals"]
+    assert (np.abs(g - spawn) <= 0.2 + 1e-12).all()
+    assert np.abs(g - spawn).max() > 0.0
