@@ -16,6 +16,8 @@
  *   sg_env_destroy           ~VecTaskEnv
  *   sg_env_dims              BatchedEnv::n_envs/obs_dim/action_dim  include/scalpel/envs.hpp:110-112
  *   sg_env_layout_*          VecTaskEnv::layout()          include/scalpel/envs.hpp:137, src/envs.cpp:166-192
+ *   sg_env_tools             VecTaskEnv::tool_base / workspace centres  include/scalpel/envs.hpp:144,
+ *                                                             src/envs.cpp:101-116,136-161
  *   sg_env_reset             BatchedEnv::reset()           src/envs.cpp:425-435
  *   sg_env_step              BatchedEnv::step(actions)     src/envs.cpp:437-617
  *   sg_env_step_host         BatchedEnv::step on host buffers (same call a host-side
@@ -87,6 +89,13 @@ typedef struct sg_env_config {
   double view_penalty;
   uint64_t seed;
   int64_t row_offset;
+  /* MultiToolReaching tool base poses (EnvConfig::tool_bases, envs.hpp:59):
+   * n_tool_bases x 7 doubles (x, y, z, qw, qx, qy, qz); 0 -> the reference's
+   * default_tool_bases (envs.cpp:101-116), otherwise one per robot
+   * ("env.tool_bases must have one entry per robot", envs.cpp:137-139). */
+  const double* tool_bases;
+  int32_t n_tool_bases;
+  int32_t reserved1;
 } sg_env_config;
 
 /* scalpel::DynamicsConfig (include/scalpel/dynamics.hpp:34-44). Gain arrays
@@ -159,6 +168,8 @@ typedef struct sg_state_views {
   int32_t waypoint_cap;
   int32_t dof;
   int64_t n_envs;
+  int32_t n_tools; /* MultiToolReaching: goals/tips are [3*n_tools][n], rng [n_tools][n] */
+  int32_t reserved;
 } sg_state_views;
 
 typedef struct sg_env sg_env;
@@ -183,6 +194,11 @@ int32_t sg_env_layout_count(const sg_env* env);
 int sg_env_layout_field(const sg_env* env, int32_t index, const char** name, int32_t* offset,
                         int32_t* length);
 int sg_env_workspace(const sg_env* env, double* center3, double* radius);
+/* Per-tool geometry (VecTaskEnv::tool_base / workspace centres, envs.hpp:144,
+ * envs.cpp:159-161): n_tools, and when non-NULL centers (3 per tool), bases
+ * (7 per tool: xyz, quaternion wxyz), dofs (1 per tool). Single-robot tasks
+ * report one tool with the identity base. */
+int sg_env_tools(const sg_env* env, int32_t* n_tools, double* centers, double* bases, int32_t* dofs);
 
 int sg_env_reset(sg_env* env, sg_step_views* out);
 /* d_actions: device, row-major n_envs x action_dim fp32 (stride = action_dim). */

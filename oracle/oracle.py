@@ -86,7 +86,14 @@ class EnvCfg(C.Structure):
         ("tracking_vel_clamp", C.c_double),
         ("seed", C.c_uint64),
         ("row_offset", C.c_int64),
+        ("collision_threshold", C.c_double),
+        ("collision_penalty", C.c_double),
+        ("view_penalty", C.c_double),
     ]
+
+
+class Pose(C.Structure):
+    _fields_ = [("xyz", C.c_double * 3), ("quat", C.c_double * 4)]
 
 
 class OracleError(RuntimeError):
@@ -152,6 +159,21 @@ def _load(precision: str) -> C.CDLL:
         "sgo_env_workspace": (None, [C.c_void_p, _d, _d]),
         "sgo_env_goal_draws": (C.c_int64, [C.c_void_p]),
         "sgo_env_set_state": (None, [C.c_void_p, _d, _d, _d]),
+        "sgo_default_tool_bases": (None, [C.c_int, C.c_double, _P(Pose)]),
+        "sgo_multi_tool_min_separation": (C.c_double, [_d, C.c_int]),
+        "sgo_mt_env_create": (C.c_void_p, [_P(EnvCfg), _P(Robot), C.c_int, _P(Pose), _P(Dyn), C.c_int,
+                                           C.c_char_p, C.c_int]),
+        "sgo_mt_env_destroy": (None, [C.c_void_p]),
+        "sgo_mt_env_dims": (None, [C.c_void_p, _P(C.c_int), _P(C.c_int), _P(C.c_int)]),
+        "sgo_mt_env_reset": (C.c_int, [C.c_void_p]),
+        "sgo_mt_env_step": (C.c_int, [C.c_void_p, _d]),
+        "sgo_mt_env_error": (C.c_char_p, [C.c_void_p]),
+        "sgo_mt_env_get_obs": (None, [C.c_void_p, _d, _d]),
+        "sgo_mt_env_get_result": (None, [C.c_void_p, _d, _P(C.c_uint8), _P(C.c_uint8), _d, _P(C.c_int64)]),
+        "sgo_mt_env_get_state": (None, [C.c_void_p, _d, _d, _d, _d, _d, _d]),
+        "sgo_mt_env_get_counters": (None, [C.c_void_p, _P(C.c_int32), _P(C.c_int32), _P(C.c_int64)]),
+        "sgo_mt_env_get_rng": (None, [C.c_void_p, _P(C.c_uint64), _P(C.c_uint64)]),
+        "sgo_mt_env_workspace": (None, [C.c_void_p, _d, _d, _d]),
         "sgo_bench_sim": (C.c_int, [_P(EnvCfg), _P(Robot), C.c_int64, C.c_int, C.c_int, _d,
                                     _P(C.c_int64)]),
     }
@@ -398,6 +420,103 @@ class Env:
         self._lib.sgo_env_set_state(self._h, _ptr(q) if q is not None else None,
                                     _ptr(qdot) if qdot is not None else None,
                                     _ptr(q_target) if q_target is not None else None)
+
+
+def default_tool_bases(n_tools: int, workspace_radius: float) -> np.ndarray:
+    """default_tool_bases (envs.cpp:101-116) as an (n_tools, 7) array: xyz, quat (w, x, y, z)."""
+    arr = (Pose * n_tools)()
+    lib().sgo_default_tool_bases(n_tools, workspace_radius, arr)
+    return np.array([list(p.xyz) + list(p.quat) for p in arr])
+
+
+def multi_tool_min_separation(tips) -> float:
+    t = np.ascontiguousarray(tips, dtype=np.float64).reshape(-1, 3)
+    return lib().sgo_multi_tool_min_separation(_ptr(t), len(t))
+
+
+class MultiToolEnv:
+    """Oracle VecTaskEnv for MultiToolReaching (envs.cpp:101-116, 304-360, 540-593):
+    one SimBatch per tool (stream id = tool * 2^32 + global row), tool-major
+    action / observation columns, base poses applied to every tip."""
+
+    def __init__(self, cfg: EnvCfg, robots, bases=None, dyns=None, threads: int = 1,
+                 precision: str = "f64"):
+        self._lib = lib(precision)
+        T = len(robots)
+        arr = (Robot * T)(*robots)
+        pb = None
+        if bases is not None:
+            b = np.asarray(bases, dtype=np.float64).reshape(T, 7)
+            pb = (Pose * T)()
+            for t in range(T):
+                pb[t].xyz[:] = list(b[t, :3])
+                pb[t].quat[:] = list(b[t, 3:])
+        pd = (Dyn * T)(*dyns) if dyns is not None else None
+        err = C.create_string_buffer(512)
+        self._h = self._lib.sgo_mt_env_create(C.byref(cfg), arr, T, pb, pd, threads, err, 512)
+        if not self._h:
+            raise OracleError(2, err.value.decode())
+        a, o, dofs = C.c_int(0), C.c_int(0), (C.c_int * T)()
+        self._lib.sgo_mt_env_dims(self._h, C.byref(a), C.byref(o), dofs)
+        self.n, self.n_tools = cfg.n_envs, T
+        self.action_dim, self.obs_dim, self.dofs = a.value, o.value, list(dofs)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.sgo_mt_env_destroy(self._h)
+            self._h = None
+
+    def _check(self, rc: int):
+        if rc:
+            raise OracleError(rc, self._lib.sgo_mt_env_error(self._h).decode())
+
+    def reset(self) -> np.ndarray:
+        self._check(self._lib.sgo_mt_env_reset(self._h))
+        return self.obs()[0]
+
+    def step(self, actions: np.ndarray) -> None:
+        a = np.ascontiguousarray(actions, dtype=np.float64)
+        assert a.shape == (self.n, self.action_dim)
+        self._check(self._lib.sgo_mt_env_step(self._h, _ptr(a)))
+
+    def obs(self):
+        o = np.zeros((self.n, self.obs_dim)); t = np.zeros_like(o)
+        self._lib.sgo_mt_env_get_obs(self._h, _ptr(o), _ptr(t))
+        return o, t
+
+    def result(self):
+        r = np.zeros(self.n); te = np.zeros(self.n)
+        term = np.zeros(self.n, np.uint8); tout = np.zeros(self.n, np.uint8)
+        sat = C.c_int64(0)
+        self._lib.sgo_mt_env_get_result(self._h, _ptr(r), _ptr(term, C.c_uint8), _ptr(tout, C.c_uint8),
+                                        _ptr(te), C.byref(sat))
+        return dict(rewards=r, terminated=term, timed_out=tout, task_error=te, saturations=sat.value)
+
+    def state(self):
+        A, T = self.action_dim, self.n_tools
+        q = np.zeros((self.n, A)); qd = np.zeros_like(q); qt = np.zeros_like(q)
+        tips = np.zeros((self.n, 3 * T)); goals = np.zeros_like(tips); axes = np.zeros_like(tips)
+        self._lib.sgo_mt_env_get_state(self._h, _ptr(q), _ptr(qd), _ptr(qt), _ptr(tips), _ptr(goals),
+                                       _ptr(axes))
+        return dict(q=q, qdot=qd, q_target=qt, tips=tips, goals=goals, axes=axes)
+
+    def counters(self):
+        sc = np.zeros(self.n, np.int32); hc = np.zeros(self.n, np.int32)
+        ec = np.zeros(self.n, np.int64)
+        self._lib.sgo_mt_env_get_counters(self._h, _ptr(sc, C.c_int32), _ptr(hc, C.c_int32),
+                                          _ptr(ec, C.c_int64))
+        return dict(step_count=sc, hold_count=hc, episode_count=ec)
+
+    def rng(self):
+        s = np.zeros((self.n_tools, self.n), np.uint64); i = np.zeros_like(s)
+        self._lib.sgo_mt_env_get_rng(self._h, _ptr(s, C.c_uint64), _ptr(i, C.c_uint64))
+        return s, i
+
+    def workspace(self):
+        T = self.n_tools
+        c = np.zeros((T, 3)); b = np.zeros((T, 7)); r = C.c_double(0)
+        self._lib.sgo_mt_env_workspace(self._h, _ptr(c), C.byref(r), _ptr(b))
+        return c, r.value, b
 
 
 def bench_sim(cfg: EnvCfg, robot: Robot, total_steps: int, runs: int, threads: int,

@@ -39,6 +39,7 @@ typedef SGO_REAL real;
 #define SGO_SIN(x) (sizeof(real) == sizeof(float) ? (real)sinf((float)(x)) : (real)sin((double)(x)))
 #define SGO_COS(x) (sizeof(real) == sizeof(float) ? (real)cosf((float)(x)) : (real)cos((double)(x)))
 #define SGO_SQRT(x) (sizeof(real) == sizeof(float) ? (real)sqrtf((float)(x)) : (real)sqrt((double)(x)))
+#define SGO_ACOS(x) (sizeof(real) == sizeof(float) ? (real)acosf((float)(x)) : (real)acos((double)(x)))
 
 /* ======================================================================
  * PCG32 — rng.hpp:25-83
@@ -882,6 +883,9 @@ void sgo_env_cfg_default(sgo_env_cfg* c) { /* envs.hpp:42-63 */
   c->tracking_vel_clamp = 0.01;
   c->seed = 0;
   c->row_offset = 0;
+  c->collision_threshold = 0.01;
+  c->collision_penalty = 1.0;
+  c->view_penalty = 0.1;
 }
 
 struct sgo_env {
@@ -1307,6 +1311,439 @@ void sgo_env_set_state(sgo_env* e, const double* q, const double* qd, const doub
     if (qd) e->qd[k] = (real)qd[k];
     if (qt) e->qt[k] = (real)qt[k];
   }
+}
+
+/* ======================================================================
+ * MultiToolReaching — envs.cpp:90-116, 118-223, 304-360, 362-408, 437-617
+ * (one SimBatch per tool; tool-major action / observation columns)
+ * ====================================================================== */
+double sgo_multi_tool_min_separation(const double* tips, int n) { /* envs.cpp:90-99 */
+  double best = INFINITY;
+  if (n < 2) return best;
+  for (int i = 0; i + 1 < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      const double d = norm3d(tips + 3 * i, tips + 3 * j);
+      best = d < best ? d : best; /* std::min(best, d) */
+    }
+  return best;
+}
+
+void sgo_default_tool_bases(int n_tools, double r, sgo_pose* b) { /* envs.cpp:101-116 */
+  for (int t = 0; t < n_tools; ++t) {
+    memset(&b[t], 0, sizeof(b[t]));
+    b[t].quat[0] = 1.0;
+  }
+  if (n_tools == 1) return;
+  const double dx = 0.7 * r;
+  b[0].xyz[0] = -dx;
+  b[1].xyz[0] = dx;
+  if (n_tools >= 3) { /* camera arm behind the scene, pitched toward it */
+    b[2].xyz[1] = -2.0 * r;
+    b[2].xyz[2] = 0.5 * r;
+    quat_from_rpy(0.9, 0.0, 0.0, b[2].quat);
+  }
+  for (int t = 3; t < n_tools; ++t) b[t].xyz[1] = ((double)t - 1.0) * 2.0 * dx;
+}
+
+struct sgo_mt_env {
+  sgo_env_cfg cfg;
+  int T, A, O;
+  int64_t n;
+  sgo_robot m[SGO_MAX_TOOLS];
+  sgo_dyn dyn[SGO_MAX_TOOLS];
+  int dof[SGO_MAX_TOOLS], off[SGO_MAX_TOOLS], jaw[SGO_MAX_TOOLS], ecm[SGO_MAX_TOOLS];
+  sgo_pose base[SGO_MAX_TOOLS];
+  double center[SGO_MAX_TOOLS][3], radius;
+  pool_t* pool;
+  real *q[SGO_MAX_TOOLS], *qd[SGO_MAX_TOOLS], *qt[SGO_MAX_TOOLS]; /* n x dof_t */
+  sgo_pcg32* rng[SGO_MAX_TOOLS];
+  real *tips, *tquat; /* n x T x 3, n x T x 4 (world frame) */
+  real* goals;        /* n x 3T */
+  int32_t *step_count, *hold_count;
+  int64_t* episode_count;
+  real *obs, *tobs, *rewards, *task_error;
+  uint8_t *terminated, *timed_out;
+  int64_t saturations;
+  int64_t* chunk_sat;
+  uint8_t *chunk_bad, *chunk_bad_reward;
+  const double* cur_actions;
+  char err[512];
+};
+
+/* tip_pose / refresh_tips (envs.cpp:225-228, 297-302): base ∘ FK */
+static void mt_refresh_tips(struct sgo_mt_env* e, int64_t row) {
+  for (int t = 0; t < e->T; ++t) {
+    real p[3], qq[4], bp[3], bq[4], v[3];
+    fk_r(&e->m[t], e->q[t] + row * e->dof[t], p, qq);
+    for (int k = 0; k < 3; ++k) bp[k] = (real)e->base[t].xyz[k];
+    for (int k = 0; k < 4; ++k) bq[k] = (real)e->base[t].quat[k];
+    qrot_r(bq, p, v); /* Pose::compose: position + orientation * other.position */
+    real* tp = e->tips + (row * e->T + t) * 3;
+    for (int k = 0; k < 3; ++k) tp[k] = bp[k] + v[k];
+    qmul_r(bq, qq, e->tquat + (row * e->T + t) * 4);
+  }
+}
+
+/* Camera arm goal: midpoint of the other tools' tips (envs.cpp:339-348, 547-555). */
+static void mt_camera_mid(const struct sgo_mt_env* e, int64_t row, int t, real* mid) {
+  mid[0] = mid[1] = mid[2] = 0;
+  int count = 0;
+  for (int u = 0; u < e->T; ++u) {
+    if (u == t) continue;
+    const real* tp = e->tips + (row * e->T + u) * 3;
+    for (int k = 0; k < 3; ++k) mid[k] += tp[k];
+    ++count;
+  }
+  for (int k = 0; k < 3; ++k) mid[k] /= (real)count;
+}
+
+static int mt_sample_goal(const struct sgo_mt_env* e, sgo_pcg32* r, const double* c, double* g) {
+  const double s = e->cfg.goal_sigma; /* envs.cpp:230-239, z drawn first (g++) */
+  for (int attempt = 0; attempt < GOAL_REJECTION_LIMIT; ++attempt) {
+    double nz = 0.0 + s * sgo_pcg32_normal(r);
+    double ny = 0.0 + s * sgo_pcg32_normal(r);
+    double nx = 0.0 + s * sgo_pcg32_normal(r);
+    g[0] = c[0] + nx;
+    g[1] = c[1] + ny;
+    g[2] = c[2] + nz;
+    if (norm3d(g, c) <= e->radius) return 0;
+  }
+  return 2;
+}
+
+static int mt_reset_row(struct sgo_mt_env* e, int64_t row) { /* envs.cpp:304-360 */
+  for (int t = 0; t < e->T; ++t) {
+    const int A = e->dof[t];
+    sgo_pcg32* r = &e->rng[t][row];
+    for (int d = 0; d < A; ++d) {
+      const sgo_joint* j = &e->m[t].joints[e->m[t].dof_to_joint[d]];
+      const double quarter = 0.25 * (j->limit_hi - j->limit_lo);
+      e->q[t][row * A + d] = (real)sgo_pcg32_uniform(r, j->limit_lo + quarter, j->limit_hi - quarter);
+      e->qd[t][row * A + d] = 0;
+      e->qt[t][row * A + d] = e->q[t][row * A + d];
+    }
+  }
+  mt_refresh_tips(e, row);
+  for (int t = 0; t < e->T; ++t) { /* envs.cpp:336-354 */
+    real* g = e->goals + row * 3 * e->T + 3 * t;
+    if (e->ecm[t]) {
+      mt_camera_mid(e, row, t, g);
+    } else {
+      double gd[3];
+      if (mt_sample_goal(e, &e->rng[t][row], e->center[t], gd)) return 2;
+      for (int k = 0; k < 3; ++k) g[k] = (real)gd[k];
+    }
+  }
+  e->step_count[row] = 0;
+  e->hold_count[row] = 0;
+  e->episode_count[row] += 1;
+  return 0;
+}
+
+static void mt_observe_row(struct sgo_mt_env* e, int64_t row, real* dst) { /* envs.cpp:362-408 */
+  real* out = dst + row * e->O;
+  int off = 0;
+  for (int t = 0; t < e->T; ++t)
+    for (int d = 0; d < e->dof[t]; ++d) out[off++] = e->q[t][row * e->dof[t] + d];
+  for (int t = 0; t < e->T; ++t)
+    for (int d = 0; d < e->dof[t]; ++d) out[off++] = e->qd[t][row * e->dof[t] + d];
+  for (int t = 0; t < e->T; ++t)
+    for (int k = 0; k < 3; ++k) out[off++] = e->tips[(row * e->T + t) * 3 + k];
+  for (int t = 0; t < e->T; ++t)
+    for (int d = 0; d < e->dof[t]; ++d) out[off++] = e->qt[t][row * e->dof[t] + d];
+  for (int k = 0; k < 3 * e->T; ++k) out[off++] = e->goals[row * 3 * e->T + k];
+}
+
+static void mt_phase_dynamics(void* ctx, int64_t b, int64_t end) { /* dynamics.cpp:124-188 per tool */
+  struct sgo_mt_env* e = (struct sgo_mt_env*)ctx;
+  int64_t sat = 0;
+  for (int64_t i = b; i < end; ++i) {
+    for (int t = 0; t < e->T; ++t) {
+      const int A = e->dof[t];
+      int r = dyn_row(&e->m[t], &e->dyn[t], e->jaw[t], e->q[t] + i * A, e->qd[t] + i * A,
+                      e->qt[t] + i * A, e->cur_actions + i * e->A + e->off[t]);
+      if (r < 0) {
+        e->chunk_bad[b / ROW_GRAIN] = 1;
+        return;
+      }
+      sat += r;
+    }
+  }
+  e->chunk_sat[b / ROW_GRAIN] += sat;
+}
+
+static void mt_phase_fk(void* ctx, int64_t b, int64_t end) { /* envs.cpp:456-463 */
+  struct sgo_mt_env* e = (struct sgo_mt_env*)ctx;
+  for (int64_t i = b; i < end; ++i) mt_refresh_tips(e, i);
+}
+
+static void mt_phase_reward(void* ctx, int64_t b, int64_t end) { /* envs.cpp:540-593 */
+  struct sgo_mt_env* e = (struct sgo_mt_env*)ctx;
+  const int T = e->T;
+  const real rho = (real)e->cfg.reward_scale, sr = (real)e->cfg.success_radius;
+  for (int64_t i = b; i < end; ++i) {
+    e->step_count[i] += 1;
+    real reward = 0, err_sum = 0;
+    int err_count = 0, all_in = 1;
+    const real* tips = e->tips + i * T * 3;
+    real* goals = e->goals + i * 3 * T;
+    for (int t = 0; t < T; ++t) {
+      const real* tp = tips + 3 * t;
+      if (e->ecm[t]) {
+        real mid[3];
+        mt_camera_mid(e, i, t, mid);
+        for (int k = 0; k < 3; ++k) goals[3 * t + k] = mid[k];
+        const real down[3] = {0, 0, -1};
+        real axis[3];
+        qrot_r(e->tquat + (i * T + t) * 4, down, axis);
+        const real to_mid[3] = {mid[0] - tp[0], mid[1] - tp[1], mid[2] - tp[2]};
+        const real nrm = SGO_SQRT(to_mid[0] * to_mid[0] + to_mid[1] * to_mid[1] + to_mid[2] * to_mid[2]);
+        if (nrm > (real)1e-12) {
+          /* Eigen normalized(): v / norm */
+          real c = axis[0] * (to_mid[0] / nrm) + axis[1] * (to_mid[1] / nrm) + axis[2] * (to_mid[2] / nrm);
+          c = c < (real)-1 ? (real)-1 : ((real)1 < c ? (real)1 : c); /* std::clamp */
+          reward += -(real)e->cfg.view_penalty * SGO_ACOS(c);
+        }
+      } else {
+        const real dist = dist3(tp, goals + 3 * t);
+        reward += rho * dist;
+        err_sum += dist;
+        ++err_count;
+        if (dist >= sr) all_in = 0;
+      }
+    }
+    real min_sep = (real)INFINITY;
+    for (int t = 0; t + 1 < T; ++t)
+      for (int u = t + 1; u < T; ++u) {
+        const real d = dist3(tips + 3 * t, tips + 3 * u);
+        min_sep = d < min_sep ? d : min_sep;
+      }
+    if (min_sep < (real)e->cfg.collision_threshold) reward += -(real)e->cfg.collision_penalty;
+    e->task_error[i] = err_count > 0 ? err_sum / (real)err_count : 0;
+    e->hold_count[i] = all_in ? e->hold_count[i] + 1 : 0;
+    const int goal_met = e->hold_count[i] >= e->cfg.success_hold;
+    if (!isfinite((double)reward)) e->chunk_bad_reward[b / ROW_GRAIN] = 1;
+    e->rewards[i] = reward;
+    e->terminated[i] = goal_met ? 1 : 0;
+    e->timed_out[i] = e->step_count[i] >= e->cfg.episode_len ? 1 : 0;
+  }
+}
+
+static void mt_phase_observe(void* ctx, int64_t b, int64_t end) {
+  struct sgo_mt_env* e = (struct sgo_mt_env*)ctx;
+  for (int64_t i = b; i < end; ++i) mt_observe_row(e, i, e->obs);
+}
+
+sgo_mt_env* sgo_mt_env_create(const sgo_env_cfg* c, const sgo_robot* models, int n_tools,
+                              const sgo_pose* bases, const sgo_dyn* dyn, int threads, char* err,
+                              int errlen) {
+  if (c->n_envs < 1) { seterr(err, errlen, "env.n_envs must be >= 1"); return NULL; }
+  if (c->episode_len < 1) { seterr(err, errlen, "env.episode_len must be >= 1"); return NULL; }
+  if (!(c->goal_sigma > 0.0)) { seterr(err, errlen, "env.goal_sigma must be > 0"); return NULL; }
+  if (!(c->success_radius > 0.0)) { seterr(err, errlen, "env.success_radius must be > 0"); return NULL; }
+  if (!(c->reward_scale < 0.0)) { seterr(err, errlen, "env.reward_scale (rho) must be < 0"); return NULL; }
+  if (c->success_hold < 1) { seterr(err, errlen, "env.success_hold must be >= 1"); return NULL; }
+  if (c->workspace_radius < 0.0) { seterr(err, errlen, "env.workspace_radius must be >= 0"); return NULL; }
+  if (c->collision_threshold < 0.0) { seterr(err, errlen, "env.collision_threshold must be >= 0"); return NULL; }
+  if (c->collision_penalty < 0.0) { seterr(err, errlen, "env.collision_penalty must be >= 0"); return NULL; }
+  if (c->view_penalty < 0.0) { seterr(err, errlen, "env.view_penalty must be >= 0"); return NULL; }
+  if (n_tools < 2) { seterr(err, errlen, "multi_tool_reaching requires >= 2 robots"); return NULL; }
+  if (n_tools > SGO_MAX_TOOLS) { seterr(err, errlen, "oracle: at most %d tools", SGO_MAX_TOOLS); return NULL; }
+  struct sgo_mt_env* e = (struct sgo_mt_env*)calloc(1, sizeof(*e));
+  e->cfg = *c;
+  e->T = n_tools;
+  e->n = c->n_envs;
+  e->radius = c->workspace_radius > 0.0 ? c->workspace_radius : 3.0 * c->goal_sigma; /* :134 */
+  if (bases) memcpy(e->base, bases, sizeof(sgo_pose) * (size_t)n_tools);
+  else sgo_default_tool_bases(n_tools, e->radius, e->base);
+  const int64_t n = e->n;
+  for (int t = 0; t < n_tools; ++t) {
+    e->m[t] = models[t];
+    if (dyn) e->dyn[t] = dyn[t];
+    else sgo_default_dynamics(&models[t], &e->dyn[t]);
+    e->dof[t] = models[t].dof;
+    e->off[t] = e->A;
+    e->jaw[t] = sgo_jaw_dof(&models[t]);
+    e->ecm[t] = strcmp(models[t].name, "ecm") == 0; /* models_[t].name == "ecm" */
+    e->A += models[t].dof;
+    /* workspace centre: base.transform_point(FK(mid).position) (envs.cpp:159-161) */
+    double mid[SGO_MAX_JOINTS], p[3], tq[4], v[3];
+    mid_configuration(&models[t], mid);
+    fk_d(&models[t], mid, p, tq);
+    qrot_d(e->base[t].quat, p, v);
+    for (int k = 0; k < 3; ++k) e->center[t][k] = e->base[t].xyz[k] + v[k];
+    const int A = e->dof[t];
+    e->q[t] = (real*)calloc((size_t)(n * A), sizeof(real));
+    e->qd[t] = (real*)calloc((size_t)(n * A), sizeof(real));
+    e->qt[t] = (real*)calloc((size_t)(n * A), sizeof(real));
+    e->rng[t] = (sgo_pcg32*)calloc((size_t)n, sizeof(sgo_pcg32));
+    for (int64_t i = 0; i < n; ++i) { /* SimBatch::create, salt = tool (dynamics.cpp:225-241) */
+      for (int d = 0; d < A; ++d) e->q[t][i * A + d] = e->qt[t][i * A + d] = (real)mid[d];
+      sgo_make_stream(c->seed, ((uint64_t)t << 32) + (uint64_t)(c->row_offset + i), &e->rng[t][i]);
+    }
+  }
+  e->O = 3 * e->A + 6 * n_tools; /* envs.cpp:166-192 */
+  e->pool = threads == 1 ? NULL : pool_create(threads);
+  e->tips = (real*)calloc((size_t)(n * n_tools * 3), sizeof(real));
+  e->tquat = (real*)calloc((size_t)(n * n_tools * 4), sizeof(real));
+  e->goals = (real*)calloc((size_t)(n * n_tools * 3), sizeof(real));
+  e->step_count = (int32_t*)calloc((size_t)n, sizeof(int32_t));
+  e->hold_count = (int32_t*)calloc((size_t)n, sizeof(int32_t));
+  e->episode_count = (int64_t*)calloc((size_t)n, sizeof(int64_t));
+  e->obs = (real*)calloc((size_t)(n * e->O), sizeof(real));
+  e->tobs = (real*)calloc((size_t)(n * e->O), sizeof(real));
+  e->rewards = (real*)calloc((size_t)n, sizeof(real));
+  e->task_error = (real*)calloc((size_t)n, sizeof(real));
+  e->terminated = (uint8_t*)calloc((size_t)n, 1);
+  e->timed_out = (uint8_t*)calloc((size_t)n, 1);
+  const int64_t chunks = (n + ROW_GRAIN - 1) / ROW_GRAIN;
+  e->chunk_sat = (int64_t*)calloc((size_t)chunks, sizeof(int64_t));
+  e->chunk_bad = (uint8_t*)calloc((size_t)chunks, 1);
+  e->chunk_bad_reward = (uint8_t*)calloc((size_t)chunks, 1);
+  return e;
+}
+
+void sgo_mt_env_destroy(sgo_mt_env* e) {
+  if (!e) return;
+  if (e->pool) pool_destroy(e->pool);
+  for (int t = 0; t < e->T; ++t) {
+    free(e->q[t]); free(e->qd[t]); free(e->qt[t]); free(e->rng[t]);
+  }
+  free(e->tips); free(e->tquat); free(e->goals); free(e->step_count); free(e->hold_count);
+  free(e->episode_count); free(e->obs); free(e->tobs); free(e->rewards); free(e->task_error);
+  free(e->terminated); free(e->timed_out); free(e->chunk_sat); free(e->chunk_bad);
+  free(e->chunk_bad_reward);
+  free(e);
+}
+
+void sgo_mt_env_dims(const sgo_mt_env* e, int* action_dim, int* obs_dim, int* dofs) {
+  if (action_dim) *action_dim = e->A;
+  if (obs_dim) *obs_dim = e->O;
+  if (dofs)
+    for (int t = 0; t < e->T; ++t) dofs[t] = e->dof[t];
+}
+
+const char* sgo_mt_env_error(const sgo_mt_env* e) { return e->err; }
+
+static int mt_fail(sgo_mt_env* e, int code, const char* msg) {
+  snprintf(e->err, sizeof(e->err), "%s", msg);
+  return code;
+}
+
+int sgo_mt_env_reset(sgo_mt_env* e) { /* envs.cpp:425-435 */
+  for (int64_t i = 0; i < e->n; ++i) {
+    if (mt_reset_row(e, i))
+      return mt_fail(e, 2, "goal sampling rejected 1000 candidates; workspace_radius is misconfigured for goal_sigma");
+    e->episode_count[i] = 0;
+  }
+  parallel_for(e->pool, e->n, ROW_GRAIN, mt_phase_observe, e);
+  memset(e->terminated, 0, (size_t)e->n);
+  memset(e->timed_out, 0, (size_t)e->n);
+  for (int64_t i = 0; i < e->n; ++i) e->rewards[i] = 0;
+  return 0;
+}
+
+int sgo_mt_env_step(sgo_mt_env* e, const double* actions) { /* envs.cpp:437-617 */
+  const int64_t n = e->n, chunks = (n + ROW_GRAIN - 1) / ROW_GRAIN;
+  memset(e->chunk_sat, 0, (size_t)chunks * sizeof(int64_t));
+  memset(e->chunk_bad, 0, (size_t)chunks);
+  memset(e->chunk_bad_reward, 0, (size_t)chunks);
+  e->cur_actions = actions;
+  parallel_for(e->pool, n, ROW_GRAIN, mt_phase_dynamics, e);
+  e->saturations = 0;
+  for (int64_t c = 0; c < chunks; ++c)
+    if (e->chunk_bad[c]) return mt_fail(e, 1, "dynamics.step: non-finite action entry");
+  for (int64_t c = 0; c < chunks; ++c) e->saturations += e->chunk_sat[c];
+  parallel_for(e->pool, n, ROW_GRAIN, mt_phase_fk, e);
+  parallel_for(e->pool, n, ROW_GRAIN, mt_phase_reward, e);
+  for (int64_t c = 0; c < chunks; ++c)
+    if (e->chunk_bad_reward[c]) return mt_fail(e, 1, "env.step: non-finite reward");
+  parallel_for(e->pool, n, ROW_GRAIN, mt_phase_observe, e);
+  const int O = e->O;
+  int any = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (e->terminated[i] || e->timed_out[i]) {
+      memcpy(e->tobs + i * O, e->obs + i * O, (size_t)O * sizeof(real));
+      any = 1;
+    }
+  if (any) {
+    for (int64_t i = 0; i < n; ++i)
+      if ((e->terminated[i] || e->timed_out[i]) && mt_reset_row(e, i))
+        return mt_fail(e, 2, "goal sampling rejected 1000 candidates; workspace_radius is misconfigured for goal_sigma");
+    for (int64_t i = 0; i < n; ++i)
+      if (e->terminated[i] || e->timed_out[i]) mt_observe_row(e, i, e->obs);
+  }
+  return 0;
+}
+
+void sgo_mt_env_get_obs(const sgo_mt_env* e, double* obs, double* tobs) {
+  for (int64_t k = 0; k < e->n * e->O; ++k) {
+    if (obs) obs[k] = e->obs[k];
+    if (tobs) tobs[k] = e->tobs[k];
+  }
+}
+
+void sgo_mt_env_get_result(const sgo_mt_env* e, double* rewards, uint8_t* term, uint8_t* tout,
+                           double* task_error, int64_t* sat) {
+  for (int64_t i = 0; i < e->n; ++i) {
+    if (rewards) rewards[i] = e->rewards[i];
+    if (term) term[i] = e->terminated[i];
+    if (tout) tout[i] = e->timed_out[i];
+    if (task_error) task_error[i] = e->task_error[i];
+  }
+  if (sat) *sat = e->saturations;
+}
+
+void sgo_mt_env_get_state(const sgo_mt_env* e, double* q, double* qd, double* qt, double* tips,
+                          double* goals, double* axes) {
+  const int T = e->T;
+  for (int64_t i = 0; i < e->n; ++i) {
+    for (int t = 0; t < T; ++t) {
+      const int A = e->dof[t];
+      for (int d = 0; d < A; ++d) {
+        const int64_t k = i * e->A + e->off[t] + d;
+        if (q) q[k] = e->q[t][i * A + d];
+        if (qd) qd[k] = e->qd[t][i * A + d];
+        if (qt) qt[k] = e->qt[t][i * A + d];
+      }
+      const real down[3] = {0, 0, -1};
+      real ax[3];
+      qrot_r(e->tquat + (i * T + t) * 4, down, ax);
+      for (int k = 0; k < 3; ++k) {
+        if (tips) tips[(i * T + t) * 3 + k] = e->tips[(i * T + t) * 3 + k];
+        if (goals) goals[(i * T + t) * 3 + k] = e->goals[(i * T + t) * 3 + k];
+        if (axes) axes[(i * T + t) * 3 + k] = ax[k];
+      }
+    }
+  }
+}
+
+void sgo_mt_env_get_counters(const sgo_mt_env* e, int32_t* sc, int32_t* hc, int64_t* ec) {
+  for (int64_t i = 0; i < e->n; ++i) {
+    if (sc) sc[i] = e->step_count[i];
+    if (hc) hc[i] = e->hold_count[i];
+    if (ec) ec[i] = e->episode_count[i];
+  }
+}
+
+void sgo_mt_env_get_rng(const sgo_mt_env* e, uint64_t* state, uint64_t* inc) {
+  for (int t = 0; t < e->T; ++t)
+    for (int64_t i = 0; i < e->n; ++i) {
+      if (state) state[t * e->n + i] = e->rng[t][i].state;
+      if (inc) inc[t * e->n + i] = e->rng[t][i].inc;
+    }
+}
+
+void sgo_mt_env_workspace(const sgo_mt_env* e, double* centers, double* radius, double* bases) {
+  for (int t = 0; t < e->T; ++t) {
+    for (int k = 0; k < 3; ++k) {
+      if (centers) centers[3 * t + k] = e->center[t][k];
+      if (bases) bases[7 * t + k] = e->base[t].xyz[k];
+    }
+    if (bases)
+      for (int k = 0; k < 4; ++k) bases[7 * t + 3 + k] = e->base[t].quat[k];
+  }
+  if (radius) *radius = e->radius;
 }
 
 /* ======================================================================

@@ -110,6 +110,8 @@ typedef struct {
   double tracking_vel_noise_std, tracking_vel_clamp;
   uint64_t seed;
   int64_t row_offset; /* global id of row 0: stream id = row_offset + row */
+  /* MultiToolReaching (envs.hpp:56-58) */
+  double collision_threshold, collision_penalty, view_penalty;
 } sgo_env_cfg;
 void sgo_env_cfg_default(sgo_env_cfg* c);
 
@@ -141,6 +143,40 @@ void sgo_env_workspace(const sgo_env* e, double* center3, double* radius);
 int64_t sgo_env_goal_draws(const sgo_env* e); /* total sample_goal attempts so far */
 /* overwrite state (for adversarial tests) */
 void sgo_env_set_state(sgo_env* e, const double* q, const double* qdot, const double* q_target);
+
+/* ---- MultiToolReaching: envs.cpp:101-116 (bases, min separation), 118-223
+ * (ctor), 304-360 (reset_row), 362-408 (observe), 437-617 (step), 540-587
+ * (reward). One SimBatch per tool, stream id = tool * 2^32 + global row. */
+#define SGO_MAX_TOOLS 8
+typedef struct { double xyz[3]; double quat[4]; /* w x y z */ } sgo_pose;
+/* default_tool_bases (envs.cpp:101-116) */
+void sgo_default_tool_bases(int n_tools, double workspace_radius, sgo_pose* out);
+/* multi_tool_min_separation (envs.cpp:90-99) over tips[n][3]; +inf below 2 */
+double sgo_multi_tool_min_separation(const double* tips, int n);
+typedef struct sgo_mt_env sgo_mt_env;
+/* models: n_tools contiguous robots; bases: NULL -> defaults; dyn: NULL ->
+ * per-robot defaults, else n_tools entries. */
+sgo_mt_env* sgo_mt_env_create(const sgo_env_cfg* c, const sgo_robot* models, int n_tools,
+                              const sgo_pose* bases, const sgo_dyn* dyn, int threads, char* err,
+                              int errlen);
+void sgo_mt_env_destroy(sgo_mt_env* e);
+/* total action / observation dims; dofs[t] = DoF of tool t (n_tools entries) */
+void sgo_mt_env_dims(const sgo_mt_env* e, int* action_dim, int* obs_dim, int* dofs);
+int sgo_mt_env_reset(sgo_mt_env* e);
+int sgo_mt_env_step(sgo_mt_env* e, const double* actions);
+const char* sgo_mt_env_error(const sgo_mt_env* e);
+void sgo_mt_env_get_obs(const sgo_mt_env* e, double* obs, double* terminal_obs);
+void sgo_mt_env_get_result(const sgo_mt_env* e, double* rewards, uint8_t* terminated,
+                           uint8_t* timed_out, double* task_error, int64_t* saturations);
+/* q/qdot/q_target: n x action_dim (tool-major columns); tips/goals: n x 3T;
+ * axes: n x 3T camera view axes (orientation * (0,0,-1)) */
+void sgo_mt_env_get_state(const sgo_mt_env* e, double* q, double* qdot, double* q_target,
+                          double* tips, double* goals, double* axes);
+void sgo_mt_env_get_counters(const sgo_mt_env* e, int32_t* step_count, int32_t* hold_count,
+                             int64_t* episode_count);
+/* rng: n_tools x n */
+void sgo_mt_env_get_rng(const sgo_mt_env* e, uint64_t* state, uint64_t* inc);
+void sgo_mt_env_workspace(const sgo_mt_env* e, double* centers3t, double* radius, double* bases7t);
 
 /* ---- bench.cpp:97-135 ------------------------------------------------- */
 /* Runs the reference protocol: fresh env per run (seed+run), reset, warm-up

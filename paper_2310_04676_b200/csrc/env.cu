@@ -20,6 +20,7 @@
 
 #include "kernels.cuh"
 #include "launch.hpp"
+#include "multi.cuh"
 #include "robot.hpp"
 #include "sg_env.h"
 
@@ -245,6 +246,13 @@ struct sg_env {
   unsigned long long* d_status = nullptr;    // device alias of h_counters
   int host_slot = 0;                          // ended slot of the next host step
   bool bench_ready = false;
+  // MultiToolReaching (multi.cuh): its own parameter block and buffers
+  bool multi = false;
+  sg::MtParams M{};
+  std::vector<sg::RobotModel> tools;
+  std::vector<std::array<double, 7>> bases;    // per tool: xyz, quaternion wxyz
+  std::vector<std::array<double, 3>> centers;  // per tool workspace centre
+  unsigned long long mt_ended_seen = 0;        // device ended-row total at the last host step
 
   ~sg_env() {
     cudaSetDevice(device);
@@ -258,7 +266,16 @@ struct sg_env {
                     p.rec_wps, p.goal_spawn, p.goal_vel};
     for (void* b : bufs)
       if (b) cudaFree(b);
+    if (multi) {
+      void* mb[] = {M.q, M.qd, M.qt, M.goals, M.tips, M.step_count, M.hold_count, M.episode_count, M.rng_state,
+                    M.rng_inc, M.obs, M.tobs, M.rewards, M.task_error, M.terminated, M.timed_out, M.act_state,
+                    M.act_buf};
+      for (void* b : mb)
+        if (b) cudaFree(b);
+    }
   }
+  int32_t* err_word() const { return multi ? M.err : P.p.err; }
+  void launch_mt(int k_steps, bool gen, bool reset) { CK(sg::launch_multi(M, k_steps, gen, reset, stream)); }
 
   int chain = sg::kChainGeneric8;
   int team_warps = 1;
@@ -300,6 +317,19 @@ struct sg_env {
 
   void views(sg_step_views* out) const {
     if (!out) return;
+    if (multi) {
+      out->observations = M.obs;
+      out->terminal_observations = M.tobs;
+      out->rewards = M.rewards;
+      out->task_error = M.task_error;
+      out->terminated = M.terminated;
+      out->timed_out = M.timed_out;
+      out->action_saturations_total = M.sat_total;
+      out->n_envs = n;
+      out->obs_dim = O;
+      out->action_dim = A;
+      return;
+    }
     out->observations = P.p.obs;
     out->terminal_observations = P.p.tobs;
     out->rewards = P.p.rewards;
@@ -316,12 +346,12 @@ struct sg_env {
   void check() {
     CK(cudaStreamSynchronize(stream));
     int32_t err = 0;
-    CK(cudaMemcpy(&err, P.p.err, sizeof(err), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&err, err_word(), sizeof(err), cudaMemcpyDeviceToHost));
     raise(err);
   }
   void raise(int32_t err) {
     if (!err) return;
-    CK(cudaMemset(P.p.err, 0, sizeof(int32_t)));
+    CK(cudaMemset(err_word(), 0, sizeof(int32_t)));
     if (err & sg::kErrNonFiniteAction) throw sg::SimError("dynamics.step: non-finite action entry");
     if (err & sg::kErrNonFiniteReward) throw sg::SimError("env.step: non-finite reward");
     if (err & sg::kErrGoalSampling)
@@ -392,32 +422,16 @@ int select_chain(const sg::RobotTable& t, int control_mode, int substeps) {
   return t.dof <= 8 ? sg::kChainGeneric8 : sg::kChainGeneric16;
 }
 
-std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_config* dyn,
-                                 std::vector<sg::RobotModel> models, int device) {
-  validate_env_config(cfg);
-  if (models.empty()) throw sg::ConfigError("env: at least one robot is required");
-  if (cfg.task == SG_TASK_MULTI_TOOL_REACHING) {
-    if (models.size() < 2) throw sg::ConfigError("multi_tool_reaching requires >= 2 robots");
-  } else if (models.size() != 1) {
-    throw sg::ConfigError(std::string(task_name(cfg.task)) + " requires exactly 1 robot");
-  }
-  if (cfg.task != SG_TASK_TARGET_REACHING && cfg.task != SG_TASK_PATH_FOLLOWING &&
-      cfg.task != SG_TASK_ACTIVE_TRACKING)
-    throw sg::ConfigError(std::string("task '") + task_name(cfg.task) +
-                          "' is not on the sg_env device path (target_reaching, active_tracking, "
-                          "path_following)");
+// DynamicsConfig resolution for one robot (envs.cpp:142-158: empty gain
+// vectors -> default_dynamics_config, dynamics.cpp:69-86; one value ->
+// broadcast) and DynamicsConfig::validate (dynamics.cpp:44-67).
+struct ResolvedDyn {
+  sg_dynamics_config dc;
+  std::vector<double> kp, kd, inertia, damping;
+  double dt_sub;
+};
 
-  auto env = std::make_unique<sg_env>();
-  env->model = std::move(models[0]);
-  const sg::RobotModel& m = env->model;
-  env->cfg = cfg;
-  env->device = device;
-  CK(cudaSetDevice(device));
-  env->n = cfg.n_envs;
-  env->A = m.dof_count;
-  env->O = 3 * m.dof_count + 6;
-
-  // ---- dynamics (dynamics.cpp:44-86, envs.cpp:142-158) ---------------------
+ResolvedDyn resolve_dynamics(const sg_dynamics_config* dyn, const sg::RobotModel& m) {
   sg_dynamics_config dc;
   sg_dynamics_config_init(&dc);
   if (dyn) dc = *dyn;
@@ -452,10 +466,227 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   check_vec(kd, "kd", true);
   check_vec(inertia, "inertia", true);
   check_vec(damping, "damping", false);
-  const double dt_sub = dc.control_dt / dc.substeps;
+  return ResolvedDyn{dc, kp, kd, inertia, damping, dc.control_dt / dc.substeps};
+}
+
+// Eigen's quaternion * vector (_transformVector): uv = 2 (u x v); v + w uv + u x uv.
+sg::Vec3 quat_rotate(const double* q, const sg::Vec3& v) {
+  const double u[3] = {q[1], q[2], q[3]};
+  double uv[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+  for (double& x : uv) x += x;
+  const double c[3] = {u[1] * uv[2] - u[2] * uv[1], u[2] * uv[0] - u[0] * uv[2], u[0] * uv[1] - u[1] * uv[0]};
+  return {v[0] + q[0] * uv[0] + c[0], v[1] + q[0] * uv[1] + c[1], v[2] + q[0] * uv[2] + c[2]};
+}
+
+// default_tool_bases (envs.cpp:101-116): xyz + quaternion (w, x, y, z).
+std::vector<std::array<double, 7>> default_tool_bases(size_t n_tools, double r) {
+  std::vector<std::array<double, 7>> b(n_tools, std::array<double, 7>{0, 0, 0, 1, 0, 0, 0});
+  if (n_tools == 1) return b;
+  const double dx = 0.7 * r;
+  b[0][0] = -dx;
+  b[1][0] = dx;
+  if (n_tools >= 3) {  // camera arm behind the scene, pitched toward it
+    b[2][1] = -2.0 * r;
+    b[2][2] = 0.5 * r;
+    const sg::Quat q = sg::quat_from_rpy(0.9, 0.0, 0.0);
+    for (int k = 0; k < 4; ++k) b[2][3 + k] = q[k];
+  }
+  for (size_t t = 3; t < n_tools; ++t) b[t][1] = (static_cast<double>(t) - 1.0) * 2.0 * dx;
+  return b;
+}
+
+// Rotation between the last actuated joint's frame and the tool-tip frame:
+// the trailing fixed joints' origin rotations times the tip orientation
+// (fk_walk, robot_model.cpp:371-395). build_table folds the trailing
+// translations into the tip offset; the camera axis needs the rotation too.
+Mat3 trailing_tip_rotation(const sg::RobotModel& m) {
+  Mat3 R{1, 0, 0, 0, 1, 0, 0, 0, 1};
+  for (const auto& j : m.joints) {
+    if (j.kind != sg::JointKind::Fixed) {
+      R = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+      continue;
+    }
+    if (!(j.origin_rotation == sg::Quat{1, 0, 0, 0})) R = mat_mul(R, quat_to_mat(j.origin_rotation));
+  }
+  if (!(m.tip_orientation == sg::Quat{1, 0, 0, 0})) R = mat_mul(R, quat_to_mat(m.tip_orientation));
+  return R;
+}
+
+// VecTaskEnv construction for MultiToolReaching (envs.cpp:118-223): per-tool
+// gain resolution and SimBatch (stream salt = tool), tool bases, workspace
+// centres through the bases, tool-major observation layout.
+std::unique_ptr<sg_env> make_multi_env(const sg_env_config& cfg, const sg_dynamics_config* dyn,
+                                       std::vector<sg::RobotModel> models, int device) {
+  const int T = static_cast<int>(models.size());
+  if (T > sg::kMaxTools)
+    throw sg::ConfigError("multi_tool_reaching: the device path supports at most " + std::to_string(sg::kMaxTools) +
+                          " robots");
+  auto env = std::make_unique<sg_env>();
+  env->multi = true;
+  env->cfg = cfg;
+  env->device = device;
+  CK(cudaSetDevice(device));
+  env->n = cfg.n_envs;
+  env->radius = cfg.workspace_radius > 0.0 ? cfg.workspace_radius : 3.0 * cfg.goal_sigma;  // envs.cpp:134
+  if (cfg.n_tool_bases == 0) {
+    env->bases = default_tool_bases(T, env->radius);
+  } else {
+    if (cfg.n_tool_bases != T || !cfg.tool_bases)
+      throw sg::ConfigError("env.tool_bases must have one entry per robot");
+    for (int t = 0; t < T; ++t) {
+      std::array<double, 7> b;
+      for (int k = 0; k < 7; ++k) b[k] = cfg.tool_bases[7 * t + k];
+      env->bases.push_back(b);
+    }
+  }
+  auto& M = env->M;
+  M.T = T;
+  int A = 0;
+  ResolvedDyn rd0{};
+  for (int t = 0; t < T; ++t) {
+    const sg::RobotModel& m = models[t];
+    if (m.dof_count > sg::kMaxToolDof)
+      throw sg::ConfigError("multi_tool_reaching: robot '" + m.name + "' has more than " +
+                            std::to_string(sg::kMaxToolDof) + " DoF (device path limit)");
+    const ResolvedDyn rd = resolve_dynamics(dyn, m);
+    if (t == 0) rd0 = rd;
+    sg::ToolEnc& E = M.tool[t];
+    E.robot = build_table(m, rd.dt_sub, rd.kp, rd.kd, rd.inertia, rd.damping);
+    const auto& b = env->bases[t];
+    const Mat3 bR = quat_to_mat(sg::Quat{b[3], b[4], b[5], b[6]});
+    for (int k = 0; k < 9; ++k) E.base_R[k] = static_cast<float>(bR[k]);
+    for (int k = 0; k < 3; ++k) E.base_p[k] = static_cast<float>(b[k]);
+    const sg::Vec3 view = mat_vec(trailing_tip_rotation(m), sg::Vec3{0.0, 0.0, -1.0});
+    for (int k = 0; k < 3; ++k) E.view[k] = static_cast<float>(view[k]);
+    E.camera = m.name == "ecm" ? 1 : 0;  // envs.cpp:339, 545
+    E.off = A;
+    A += m.dof_count;
+    // workspace centre: tool_bases_[t].transform_point(FK(mid).position) (envs.cpp:159-161)
+    const sg::Vec3 tip = sg::forward_kinematics_position(m, m.mid_configuration());
+    const sg::Vec3 rt = quat_rotate(b.data() + 3, tip);
+    const std::array<double, 3> c{b[0] + rt[0], b[1] + rt[1], b[2] + rt[2]};
+    env->centers.push_back(c);
+    for (int k = 0; k < 3; ++k) E.center[k] = c[k];
+  }
+  for (int k = 0; k < 3; ++k) env->center[k] = env->centers[0][k];
+  M.A = A;
+  M.O = 3 * A + 6 * T;  // envs.cpp:166-192
+  M.Os = M.O | 1;
+  M.episode_len = cfg.episode_len;
+  M.success_hold = cfg.success_hold;
+  M.substeps = rd0.dc.substeps;
+  M.control_mode = rd0.dc.control_mode;
+  M.n = env->n;
+  M.rho = static_cast<float>(cfg.reward_scale);
+  M.success_radius = static_cast<float>(cfg.success_radius);
+  M.dt_sub = static_cast<float>(rd0.dt_sub);
+  M.collision_threshold = static_cast<float>(cfg.collision_threshold);
+  M.collision_penalty = static_cast<float>(cfg.collision_penalty);
+  M.view_penalty = static_cast<float>(cfg.view_penalty);
+  M.goal_sigma = cfg.goal_sigma;
+  M.radius = env->radius;
+  env->A = A;
+  env->O = M.O;
+
+  int off = 0;
+  auto add = [&](const char* name, int len) {
+    env->layout.push_back({name, {off, len}});
+    off += len;
+  };
+  add("dof_pos", A);
+  add("dof_vel", A);
+  add("tip_pos", 3 * T);
+  add("dof_target", A);
+  add("goal", 3 * T);
+
+  const int64_t n = env->n;
+  M.q = dalloc<float>(n * A);
+  M.qd = dalloc<float>(n * A);
+  M.qt = dalloc<float>(n * A);
+  M.goals = dalloc<float>(n * 3 * T);
+  M.tips = dalloc<float>(n * 3 * T);
+  M.step_count = dalloc<int32_t>(n);
+  M.hold_count = dalloc<int32_t>(n);
+  M.episode_count = dalloc<int64_t>(n);
+  M.rng_state = dalloc<uint64_t>(n * T);
+  M.rng_inc = dalloc<uint64_t>(n * T);
+  M.obs = dalloc<float>(n * M.O);
+  M.tobs = dalloc<float>(n * M.O);
+  M.rewards = dalloc<float>(n);
+  M.task_error = dalloc<float>(n);
+  M.terminated = dalloc<uint8_t>(n);
+  M.timed_out = dalloc<uint8_t>(n);
+  env->counters = dalloc<unsigned long long>(8);
+  M.sat_total = env->counters;
+  M.ended_total = env->counters + 1;
+  M.err = reinterpret_cast<int32_t*>(env->counters + 2);
+  CK(cudaHostAlloc(&env->h_counters, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
+  // SimBatch::create per tool (dynamics.cpp:225-241): mid configuration at
+  // rest, stream id = tool * 2^32 + global row
+  std::vector<float> qh(static_cast<size_t>(n) * A);
+  std::vector<uint64_t> st(static_cast<size_t>(n) * T), inc(static_cast<size_t>(n) * T);
+  for (int t = 0; t < T; ++t) {
+    const auto mid = models[t].mid_configuration();
+    for (int d = 0; d < models[t].dof_count; ++d)
+      for (int64_t i = 0; i < n; ++i) qh[(M.tool[t].off + d) * n + i] = static_cast<float>(mid[d]);
+    for (int64_t i = 0; i < n; ++i) {
+      const HostPcg r =
+          make_stream(cfg.seed, (static_cast<uint64_t>(t) << 32) + static_cast<uint64_t>(cfg.row_offset + i));
+      st[t * n + i] = r.state;
+      inc[t * n + i] = r.inc;
+    }
+  }
+  CK(cudaMemcpy(M.q, qh.data(), qh.size() * sizeof(float), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(M.qt, qh.data(), qh.size() * sizeof(float), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(M.rng_state, st.data(), st.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(M.rng_inc, inc.data(), inc.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  env->d_actions_in = dalloc<float>(n * A);
+  env->tools = std::move(models);
+  env->model = env->tools[0];
+  CK(cudaDeviceSynchronize());
+  return env;
+}
+
+std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_config* dyn,
+                                 std::vector<sg::RobotModel> models, int device) {
+  validate_env_config(cfg);
+  if (models.empty()) throw sg::ConfigError("env: at least one robot is required");
+  if (cfg.task == SG_TASK_MULTI_TOOL_REACHING) {
+    if (models.size() < 2) throw sg::ConfigError("multi_tool_reaching requires >= 2 robots");
+  } else if (models.size() != 1) {
+    throw sg::ConfigError(std::string(task_name(cfg.task)) + " requires exactly 1 robot");
+  }
+  if (cfg.task == SG_TASK_MULTI_TOOL_REACHING) return make_multi_env(cfg, dyn, std::move(models), device);
+  if (cfg.n_tool_bases != 0 && cfg.n_tool_bases != 1)
+    throw sg::ConfigError("env.tool_bases must have one entry per robot");
+  if (cfg.n_tool_bases == 1) {  // the single-tool kernels work in the robot base frame
+    const double ident[7] = {0, 0, 0, 1, 0, 0, 0};
+    if (!cfg.tool_bases || !std::equal(ident, ident + 7, cfg.tool_bases))
+      throw sg::ConfigError("env.tool_bases: a non-identity base is only supported for multi_tool_reaching");
+  }
+  if (cfg.task != SG_TASK_TARGET_REACHING && cfg.task != SG_TASK_PATH_FOLLOWING &&
+      cfg.task != SG_TASK_ACTIVE_TRACKING)
+    throw sg::ConfigError(std::string("task '") + task_name(cfg.task) +
+                          "' is not on the sg_env device path (target_reaching, active_tracking, "
+                          "path_following, multi_tool_reaching)");
+
+  auto env = std::make_unique<sg_env>();
+  env->model = std::move(models[0]);
+  const sg::RobotModel& m = env->model;
+  env->cfg = cfg;
+  env->device = device;
+  CK(cudaSetDevice(device));
+  env->n = cfg.n_envs;
+  env->A = m.dof_count;
+  env->O = 3 * m.dof_count + 6;
+
+  const ResolvedDyn rd = resolve_dynamics(dyn, m);
+  const int dof = m.dof_count;
+  const double dt_sub = rd.dt_sub;
+  const sg_dynamics_config& dc = rd.dc;
 
   auto& P = env->P;
-  P.robot = build_table(m, dt_sub, kp, kd, inertia, damping);
+  P.robot = build_table(m, dt_sub, rd.kp, rd.kd, rd.inertia, rd.damping);
 
   // ---- task params ------------------------------------------------------------
   env->radius = cfg.workspace_radius > 0.0 ? cfg.workspace_radius : 3.0 * cfg.goal_sigma;  // envs.cpp:134
@@ -663,10 +894,25 @@ int sg_env_workspace(const sg_env* env, double* center3, double* radius) {
   });
 }
 
+int sg_env_tools(const sg_env* env, int32_t* n_tools, double* centers, double* bases, int32_t* dofs) {
+  return guard([&] {
+    const int T = env->multi ? env->M.T : 1;
+    if (n_tools) *n_tools = T;
+    for (int t = 0; t < T; ++t) {
+      for (int k = 0; k < 3; ++k)
+        if (centers) centers[3 * t + k] = env->multi ? env->centers[t][k] : env->center[k];
+      for (int k = 0; k < 7; ++k)
+        if (bases) bases[7 * t + k] = env->multi ? env->bases[t][k] : (k == 3 ? 1.0 : 0.0);
+      if (dofs) dofs[t] = env->multi ? env->tools[t].dof_count : env->A;
+    }
+  });
+}
+
 int sg_env_reset(sg_env* env, sg_step_views* out) {
   return guard([&] {
     CK(cudaSetDevice(env->device));
-    env->launch_reset();
+    if (env->multi) env->launch_mt(0, false, true);
+    else env->launch_reset();
     env->views(out);
   });
 }
@@ -675,6 +921,12 @@ int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
   return guard([&] {
     if (!d_actions) throw sg::SimError("env.step: action shape mismatch");
     CK(cudaSetDevice(env->device));
+    if (env->multi) {
+      env->M.actions = d_actions;
+      env->launch_mt(1, false, false);
+      env->views(out);
+      return;
+    }
     env->P.actions = d_actions;
     env->P.actions_aligned = (reinterpret_cast<uintptr_t>(d_actions) & 15u) == 0;
     env->launch_step(1, false);
@@ -695,10 +947,43 @@ static void* mapped_alias(const void* h) {
   return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 
+// MultiToolReaching host step: staged copies around one launch, counters read
+// back with the result (the zero-copy publication path is single-tool only).
+static void multi_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
+  const int64_t n = env->n;
+  const int O = env->O;
+  auto& s = env->stream;
+  auto& M = env->M;
+  CK(cudaMemcpyAsync(env->d_actions_in, h_actions, n * env->A * sizeof(float), cudaMemcpyHostToDevice, s));
+  M.actions = env->d_actions_in;
+  env->launch_mt(1, false, false);
+  if (out) {
+    if (out->observations)
+      CK(cudaMemcpyAsync(out->observations, M.obs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (out->rewards) CK(cudaMemcpyAsync(out->rewards, M.rewards, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (out->task_error)
+      CK(cudaMemcpyAsync(out->task_error, M.task_error, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (out->terminated) CK(cudaMemcpyAsync(out->terminated, M.terminated, n, cudaMemcpyDeviceToHost, s));
+    if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, M.timed_out, n, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaMemcpyAsync(env->h_counters, env->counters, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const unsigned long long sat = env->h_counters[0], ended_total = env->h_counters[1];
+  env->raise(static_cast<int32_t>(env->h_counters[2] & 0xffffffffu));
+  const unsigned long long ended = ended_total - env->mt_ended_seen;
+  env->mt_ended_seen = ended_total;
+  if (out && out->terminal_observations && ended != 0)
+    CK(cudaMemcpy(out->terminal_observations, M.tobs, n * O * sizeof(float), cudaMemcpyDeviceToHost));
+  env->last_ended += ended;
+  if (out) out->action_saturations = static_cast<int64_t>(sat - env->last_sat);
+  env->last_sat = sat;
+}
+
 int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
   return guard([&] {
     if (!h_actions) throw sg::SimError("env.step: action shape mismatch");
     CK(cudaSetDevice(env->device));
+    if (env->multi) return multi_step_host(env, h_actions, out);
     const int64_t n = env->n;
     const int O = env->O;
     auto& s = env->stream;
@@ -782,11 +1067,30 @@ int sg_env_host_counters(const sg_env* env, uint64_t* ended_rows_total, uint64_t
 }
 
 int sg_env_task_error(const sg_env* env, float** d) {
-  return guard([&] { *d = env->P.p.task_error; });
+  return guard([&] { *d = env->multi ? env->M.task_error : env->P.p.task_error; });
 }
 
 int sg_env_state(const sg_env* env, sg_state_views* o) {
   return guard([&] {
+    std::memset(o, 0, sizeof(*o));
+    if (env->multi) {
+      const auto& M = env->M;
+      o->q = M.q;
+      o->qdot = M.qd;
+      o->q_target = M.qt;
+      o->goals = M.goals;
+      o->tips = M.tips;
+      o->step_count = M.step_count;
+      o->hold_count = M.hold_count;
+      o->episode_count = M.episode_count;
+      o->rng_state = M.rng_state;
+      o->rng_inc = M.rng_inc;
+      o->dof = env->A;
+      o->n_envs = env->n;
+      o->n_tools = M.T;
+      return;
+    }
+    o->n_tools = 1;
     const auto& p = env->P.p;
     o->q = p.q;
     o->qdot = p.qd;
@@ -818,6 +1122,26 @@ int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t g
   return guard([&] {
     CK(cudaSetDevice(env->device));
     if (global_n < env->n + env->cfg.row_offset) throw sg::ConfigError("bench: global_n_envs smaller than this shard");
+    if (env->multi) {  // one stream state per env at its row start; A consecutive draws per row
+      auto& M = env->M;
+      if (!M.act_state) {
+        M.act_state = dalloc<uint64_t>(env->n);
+        M.act_buf = dalloc<float>(env->n * env->A);
+      }
+      const HostPcg r = make_stream(seed, 0xac7104);  // bench.cpp:115
+      sg::JumpTable J;
+      for (int b = 0; b < 64; ++b) pcg_jump(1ULL << b, r.inc, J.mult[b], J.add[b]);
+      const uint64_t A = static_cast<uint64_t>(env->A);
+      M.act_inc = r.inc;
+      pcg_jump(static_cast<uint64_t>(global_n) * A, r.inc, M.jump_mult, M.jump_add);
+      const unsigned grid = static_cast<unsigned>((env->n + 127) / 128);
+      sg::bench_seed_kernel<<<grid, 128, 0, env->stream>>>(M.act_state, env->n, r.state,
+                                                           static_cast<uint64_t>(first_step) * global_n * A,
+                                                           env->cfg.row_offset, env->A, J);
+      CK(cudaGetLastError());
+      env->bench_ready = true;
+      return;
+    }
     auto& p = env->P.p;
     if (!p.act_state) {
       p.act_state = dalloc<uint64_t>(static_cast<size_t>(env->n) * sg::kMaxTeamWarps);
@@ -853,14 +1177,16 @@ int sg_env_bench_step(sg_env* env, int32_t k_steps) {
     if (!env->bench_ready) throw sg::ConfigError("sg_env_bench_step before sg_env_bench_begin");
     if (k_steps < 1) throw sg::ConfigError("bench: k_steps must be >= 1");
     CK(cudaSetDevice(env->device));
-    env->launch_step(k_steps, true);
+    if (env->multi) env->launch_mt(k_steps, true, false);
+    else env->launch_step(k_steps, true);
   });
 }
 
 int sg_env_bench_actions(const sg_env* env, float** d_actions) {
   return guard([&] {
-    if (!env->P.p.act_buf) throw sg::ConfigError("sg_env_bench_actions before sg_env_bench_begin");
-    *d_actions = env->P.p.act_buf;
+    float* buf = env->multi ? env->M.act_buf : env->P.p.act_buf;
+    if (!buf) throw sg::ConfigError("sg_env_bench_actions before sg_env_bench_begin");
+    *d_actions = buf;
   });
 }
 

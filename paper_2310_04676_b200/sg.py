@@ -44,6 +44,7 @@ class EnvConfig(C.Structure):  # sg_env_config
         ("tracking_vel_noise_std", C.c_double), ("tracking_vel_clamp", C.c_double),
         ("collision_threshold", C.c_double), ("collision_penalty", C.c_double),
         ("view_penalty", C.c_double), ("seed", C.c_uint64), ("row_offset", C.c_int64),
+        ("tool_bases", C.POINTER(C.c_double)), ("n_tool_bases", C.c_int32), ("reserved1", C.c_int32),
     ]
 
 
@@ -80,6 +81,7 @@ class StateViews(C.Structure):  # sg_state_views
         ("episode_count", C.c_void_p), ("waypoint_idx", C.c_void_p), ("waypoint_len", C.c_void_p),
         ("waypoints", C.c_void_p), ("rng_state", C.c_void_p), ("rng_inc", C.c_void_p),
         ("waypoint_cap", C.c_int32), ("dof", C.c_int32), ("n_envs", C.c_int64),
+        ("n_tools", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
@@ -99,6 +101,7 @@ _SIGS = {
     "sg_env_layout_count": (C.c_int32, [C.c_void_p]),
     "sg_env_layout_field": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_char_p), _P(C.c_int32), _P(C.c_int32)]),
     "sg_env_workspace": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double)]),
+    "sg_env_tools": (C.c_int, [C.c_void_p, _P(C.c_int32), _P(C.c_double), _P(C.c_double), _P(C.c_int32)]),
     "sg_env_reset": (C.c_int, [C.c_void_p, _P(StepViews)]),
     "sg_env_step": (C.c_int, [C.c_void_p, C.c_void_p, _P(StepViews)]),
     "sg_env_step_host": (C.c_int, [C.c_void_p, C.c_void_p, _P(HostResult)]),
@@ -249,11 +252,19 @@ class StepResult:
 
 
 def env_config(**kw) -> EnvConfig:
+    """sg_env_config with the reference defaults; tool_bases: (T, 7) array-like
+    of xyz + quaternion (w, x, y, z) per robot (kept alive on the struct)."""
     c = EnvConfig()
     lib().sg_env_config_init(C.byref(c))
     for k, v in kw.items():
         if k == "task" and isinstance(v, str):
             v = TASKS[v]
+        if k == "tool_bases":
+            b = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1, 7))
+            c._tool_bases = b
+            c.tool_bases = b.ctypes.data_as(C.POINTER(C.c_double))
+            c.n_tool_bases = b.shape[0]
+            continue
         setattr(c, k, v)
     return c
 
@@ -323,6 +334,14 @@ class VecTaskEnv:
         _check(lib().sg_env_workspace(self._h, c, C.byref(r)))
         return np.array(list(c)), r.value
 
+    def tools(self):
+        """(centers (T, 3), bases (T, 7) xyz + wxyz, dofs) per tool (envs.hpp:144)."""
+        T = C.c_int32()
+        _check(lib().sg_env_tools(self._h, C.byref(T), None, None, None))
+        c, b, d = (C.c_double * (3 * T.value))(), (C.c_double * (7 * T.value))(), (C.c_int32 * T.value)()
+        _check(lib().sg_env_tools(self._h, C.byref(T), c, b, d))
+        return np.array(list(c)).reshape(-1, 3), np.array(list(b)).reshape(-1, 7), list(d)
+
     def _result(self) -> StepResult:
         v, n, o, d = self._views, self.n_envs, self.obs_dim, self.device
         return StepResult(
@@ -390,18 +409,20 @@ class VecTaskEnv:
         s = StateViews()
         _check(lib().sg_env_state(self._h, C.byref(s)))
         n, A, d = self.n_envs, self.action_dim, self.device
-        cap = s.waypoint_cap
+        cap, T = s.waypoint_cap, s.n_tools
+        rng_shape = (n,) if T == 1 else (T, n)
         return dict(
             q=device_view(s.q, (A, n), "f32", d), qdot=device_view(s.qdot, (A, n), "f32", d),
-            q_target=device_view(s.q_target, (A, n), "f32", d), goals=device_view(s.goals, (3, n), "f32", d),
-            tips=device_view(s.tips, (3, n), "f32", d), step_count=device_view(s.step_count, (n,), "i32", d),
+            q_target=device_view(s.q_target, (A, n), "f32", d), goals=device_view(s.goals, (3 * T, n), "f32", d),
+            tips=device_view(s.tips, (3 * T, n), "f32", d), step_count=device_view(s.step_count, (n,), "i32", d),
             hold_count=device_view(s.hold_count, (n,), "i32", d),
             episode_count=device_view(s.episode_count, (n,), "i64", d),
             waypoint_idx=device_view(s.waypoint_idx, (n,), "i32", d),
             waypoint_len=device_view(s.waypoint_len, (n,), "i32", d),
             waypoints=device_view(s.waypoints, (n, cap, 3), "f32", d) if cap else None,
-            rng_state=device_view(s.rng_state, (n,), "u64", d), rng_inc=device_view(s.rng_inc, (n,), "u64", d),
-            waypoint_cap=cap,
+            rng_state=device_view(s.rng_state, rng_shape, "u64", d),
+            rng_inc=device_view(s.rng_inc, rng_shape, "u64", d),
+            waypoint_cap=cap, n_tools=T,
         )
 
     # -- bench workload (bench.cpp:31-35,97-135) --------------------------------
