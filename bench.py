@@ -39,6 +39,9 @@ CONFIGS = {
                 workload="dVRK ECM camera reach, 65536 envs/GPU, random actions (BASELINE configs[2])"),
     "star": dict(robot="star", task="path_following", n_envs=16384, goal_sigma=0.15,
                  workload="STAR path following, 16384 envs/GPU, random actions (BASELINE configs[3])"),
+    "multitool": dict(robots=("psm", "psm", "ecm"), task="multi_tool_reaching", n_envs=16384, goal_sigma=0.05,
+                      workload="trimanual MultiToolReaching (PSM + PSM + ECM camera), 16384 envs/GPU, random "
+                               "actions (SURVEY 8f rank 3; not a BASELINE config)"),
     "ppo": dict(robot="psm", task="target_reaching", n_envs=16384, goal_sigma=0.05,
                 workload="full PPO rollout+update on PSM reach, 16384 envs/GPU, n_steps 32, 5 epochs x 4 "
                          "minibatches, 256/128/64 ELU MLP (BASELINE configs[4])"),
@@ -57,7 +60,7 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def step_bytes(A: int, O: int, fused: int, reset_frac: float) -> dict:
+def step_bytes(A: int, O: int, fused: int, reset_frac: float, tools: int = 1) -> dict:
     """Algorithmic HBM bytes of one fused launch per env.
     Per launch: joint state q/qdot/q_target read+write (3*A*4*2), goal read+write
     and tip write (3*4*3), step/hold counters r+w (16), bench stream state r+w (16).
@@ -66,9 +69,9 @@ def step_bytes(A: int, O: int, fused: int, reset_frac: float) -> dict:
     Per reset (amortised by reset_frac): terminal observation row (O*4), RNG
     state r+w (16), episode counter r+w (16), reset state write + reload
     (3*A*4*2 + 24)."""
-    per_launch = 3 * A * 4 * 2 + 3 * 4 * 3 + 16 + 16
+    per_launch = 3 * A * 4 * 2 + 3 * tools * 4 * 3 + 16 + 16
     per_step = A * 4 + O * 4 + 8 + 2
-    per_reset = O * 4 + 16 + 16 + 3 * A * 4 * 2 + 24
+    per_reset = O * 4 + 16 * tools + 16 + 3 * A * 4 * 2 + 24 * tools
     total = per_launch + fused * (per_step + reset_frac * per_reset)
     return dict(per_launch=per_launch, per_step=per_step, per_reset=per_reset,
                 per_env_launch=total, per_env_step=total / fused)
@@ -151,6 +154,8 @@ def cpu_reference(cfg: dict, steps: int, budget_s: float, threads: int = 0):
     Returns (env-steps/s, lanes, sample description)."""
     from oracle import oracle as O
     O.build()
+    if "robots" in cfg:
+        return cpu_reference_multi(O, cfg, steps, budget_s, threads)
     m = O.resolve_robot(cfg["robot"])
     task = O.PATH_FOLLOWING if cfg["task"] == "path_following" else O.TARGET_REACHING
     ocfg = O.env_config(n_envs=cfg["n_envs"], seed=0, task=task, goal_sigma=cfg["goal_sigma"])
@@ -166,6 +171,28 @@ def cpu_reference(cfg: dict, steps: int, budget_s: float, threads: int = 0):
     return float(st[0] / secs[0]), lanes, sample
 
 
+def cpu_reference_multi(O, cfg: dict, steps: int, budget_s: float, threads: int = 0):
+    """MultiToolReaching on the oracle (bench_sim protocol: serial action fill
+    from make_stream(seed, 0xac7104), reset, warm-up step, timed steps)."""
+    import time
+    ms = [O.resolve_robot(r) for r in cfg["robots"]]
+    n = cfg["n_envs"]
+    lanes = threads or os.cpu_count() or 1
+    e = O.MultiToolEnv(O.env_config(n_envs=n, seed=0, task=O.MULTI_TOOL, goal_sigma=cfg["goal_sigma"]), ms,
+                       threads=lanes)
+    ar = O.make_stream(0, 0xAC7104)
+    e.reset()
+    e.step(O.fill_uniform_actions(ar, n, e.action_dim))
+    done, t0 = 0, time.perf_counter()
+    while done < steps and time.perf_counter() - t0 < budget_s:
+        e.step(O.fill_uniform_actions(ar, n, e.action_dim))
+        done += 1
+    dt = time.perf_counter() - t0
+    sample = (f"{n} envs x {done} steps after reset + 1 warm-up step (bench_sim protocol, serial action fill "
+              f"and serial resets), fp64, {lanes} pool lanes")
+    return n * done / dt, lanes, sample
+
+
 def bench_ppo(args, cfg, rank, world, local, dist):
     """Config 5: env-steps/s with learning (bench_learning, bench.cpp:137-174):
     whole trainer iterations (rollout of n_steps x N env steps with the tcgen05
@@ -175,7 +202,8 @@ def bench_ppo(args, cfg, rank, world, local, dist):
     from paper_2310_04676_b200 import ppo, sg
     n = cfg["n_envs"]
     plan = shard_plan(rank, world, n)
-    env = sg.VecTaskEnv(robots=(cfg["robot"],), device=local, n_envs=n, seed=0, task=cfg["task"],
+    robots = cfg.get("robots", (cfg.get("robot"),))
+    env = sg.VecTaskEnv(robots=robots, device=local, n_envs=n, seed=0, task=cfg["task"],
                         goal_sigma=cfg["goal_sigma"], row_offset=plan["row_offset"])
     pol = sg.Policy(env.obs_dim, env.action_dim, device=local)
     tcfg = ppo.TrainConfig(seed=0, update_precision=args.update_precision)
@@ -302,7 +330,8 @@ def main():
 
     n = cfg["n_envs"]
     plan = shard_plan(rank, world, n)
-    env = sg.VecTaskEnv(robots=(cfg["robot"],), device=local, n_envs=n, seed=0, task=cfg["task"],
+    robots = cfg.get("robots", (cfg.get("robot"),))
+    env = sg.VecTaskEnv(robots=robots, device=local, n_envs=n, seed=0, task=cfg["task"],
                         goal_sigma=cfg["goal_sigma"], row_offset=plan["row_offset"])
     A, O = env.action_dim, env.obs_dim
     env.reset()
@@ -344,7 +373,7 @@ def main():
 
     # ---- roofline of the dominant kernel (env_step_kernel, fused bench variant)
     resets = (steps_done // 300) - ((steps_done - args.steps) // 300)
-    b = step_bytes(A, O, F, resets / max(args.steps, 1))
+    b = step_bytes(A, O, F, resets / max(args.steps, 1), tools=len(robots))
     full = [ms for ms, kf in zip(launch_ms, launches) if kf == F]
     avg_launch_s = (sum(full) / len(full)) * 1e-3 if full else t_ms * 1e-3 / len(launches)
     peak, peak_kind = peaks()
@@ -440,7 +469,8 @@ def main():
                         fused_steps_per_launch=F, parallelism=f"env-shard x{world}",
                         l2="256 MiB flush between timed launches; per-launch state read cold from HBM"),
             roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                          traffic=traffic, peak_kind=peak_kind, kernel=f"env_step_kernel<{cfg['robot'].upper()} chain, 2 team warps, GEN> ({F} fused steps/launch)",
+                          traffic=traffic, peak_kind=peak_kind, kernel=(f"mt_step_kernel<T={len(robots)}, GEN> ({F} fused steps/launch)" if len(robots) > 1 else
+                                  f"env_step_kernel<{cfg['robot'].upper()} chain, 2 team warps, GEN> ({F} fused steps/launch)"),
                           bytes_per_env_step=b["per_env_step"], bytes_per_launch=n * b["per_env_launch"],
                           avg_launch_us=avg_launch_s * 1e6),
             cpu_baseline=cpu, e2e=e2e, single_step_launches=single,

@@ -89,6 +89,11 @@ class EnvCfg(C.Structure):
         ("collision_threshold", C.c_double),
         ("collision_penalty", C.c_double),
         ("view_penalty", C.c_double),
+        ("render_w", C.c_int32),
+        ("render_h", C.c_int32),
+        ("render_fov", C.c_double),
+        ("render_near", C.c_double),
+        ("render_far", C.c_double),
     ]
 
 
@@ -159,6 +164,8 @@ def _load(precision: str) -> C.CDLL:
         "sgo_env_workspace": (None, [C.c_void_p, _d, _d]),
         "sgo_env_goal_draws": (C.c_int64, [C.c_void_p]),
         "sgo_env_set_state": (None, [C.c_void_p, _d, _d, _d]),
+        "sgo_render": (None, [_d, _d, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _d, C.c_int, _d]),
+        "sgo_env_get_images": (None, [C.c_void_p, _d, _d, _d, _d]),
         "sgo_default_tool_bases": (None, [C.c_int, C.c_double, _P(Pose)]),
         "sgo_multi_tool_min_separation": (C.c_double, [_d, C.c_int]),
         "sgo_mt_env_create": (C.c_void_p, [_P(EnvCfg), _P(Robot), C.c_int, _P(Pose), _P(Dyn), C.c_int,
@@ -411,6 +418,15 @@ class Env:
         self._lib.sgo_env_workspace(self._h, _ptr(c), C.byref(r))
         return c, r.value
 
+    def images(self):
+        """ImageMatching state: target / current images (n, w*h), scenes (n, 3, 5)
+        {cx, cy, cz, radius, albedo}, target cameras (n, 7) xyz + wxyz."""
+        wh = (self.obs_dim - 3 * self.action_dim - 3) // 2
+        t = np.zeros((self.n, wh)); c = np.zeros_like(t)
+        sc = np.zeros((self.n, 3, 5)); cam = np.zeros((self.n, 7))
+        self._lib.sgo_env_get_images(self._h, _ptr(t), _ptr(c), _ptr(sc), _ptr(cam))
+        return dict(target=t, current=c, scenes=sc, target_cameras=cam)
+
     def goal_draws(self) -> int:
         return self._lib.sgo_env_goal_draws(self._h)
 
@@ -420,6 +436,17 @@ class Env:
         self._lib.sgo_env_set_state(self._h, _ptr(q) if q is not None else None,
                                     _ptr(qdot) if qdot is not None else None,
                                     _ptr(q_target) if q_target is not None else None)
+
+
+def render(cam_pos, cam_quat, spheres, width=32, height=32, fov=1.0471975511965976, near=0.005, far=2.0,
+           precision: str = "f64") -> np.ndarray:
+    """render.cpp:34-67: spheres (k, 5) {cx, cy, cz, radius, albedo} -> (h, w) image."""
+    sp = np.ascontiguousarray(np.asarray(spheres, dtype=np.float64).reshape(-1, 5))
+    p = np.ascontiguousarray(cam_pos, dtype=np.float64)
+    q = np.ascontiguousarray(cam_quat, dtype=np.float64)
+    out = np.zeros(width * height)
+    lib(precision).sgo_render(_ptr(p), _ptr(q), width, height, fov, near, far, _ptr(sp), len(sp), _ptr(out))
+    return out.reshape(height, width)
 
 
 def default_tool_bases(n_tools: int, workspace_radius: float) -> np.ndarray:

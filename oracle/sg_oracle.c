@@ -886,6 +886,71 @@ void sgo_env_cfg_default(sgo_env_cfg* c) { /* envs.hpp:42-63 */
   c->collision_threshold = 0.01;
   c->collision_penalty = 1.0;
   c->view_penalty = 0.1;
+  c->render_w = 32; /* render.hpp:31-36 */
+  c->render_h = 32;
+  c->render_fov = 1.0471975511965976;
+  c->render_near = 0.005;
+  c->render_far = 2.0;
+}
+
+/* ======================================================================
+ * Renderer — render.cpp:34-67 (Eigen formulas: toRotationMatrix, normalized()
+ * = v / sqrt(squaredNorm), dot = (a0 b0 + a1 b1) + a2 b2)
+ * ====================================================================== */
+static void quat_to_rot_r(const real* q, real* R) { /* Quaternion::toRotationMatrix */
+  const real tx = 2 * q[1], ty = 2 * q[2], tz = 2 * q[3];
+  const real twx = tx * q[0], twy = ty * q[0], twz = tz * q[0];
+  const real txx = tx * q[1], txy = ty * q[1], txz = tz * q[1];
+  const real tyy = ty * q[2], tyz = tz * q[2], tzz = tz * q[3];
+  R[0] = 1 - (tyy + tzz); R[1] = txy - twz; R[2] = txz + twy;
+  R[3] = txy + twz; R[4] = 1 - (txx + tzz); R[5] = tyz - twx;
+  R[6] = txz - twy; R[7] = tyz + twx; R[8] = 1 - (txx + tyy);
+}
+
+static void render_real(const real* pos, const real* quat, int w, int h, double fov, double near_,
+                        double far_, const double* sph, int ns, real* out) {
+  const real f = (real)(0.5 * w / tan(0.5 * fov)); /* focal length in pixels */
+  real R[9];
+  quat_to_rot_r(quat, R);
+  for (int py = 0; py < h; ++py) {
+    for (int px = 0; px < w; ++px) {
+      const real u = (real)(px + 0.5 - 0.5 * w) / f;
+      const real v = (real)(py + 0.5 - 0.5 * h) / f;
+      const real dc[3] = {u, -v, -1}; /* top row looks up */
+      real d[3];
+      for (int r = 0; r < 3; ++r) d[r] = R[r * 3] * dc[0] + R[r * 3 + 1] * dc[1] + R[r * 3 + 2] * dc[2];
+      const real nn = SGO_SQRT(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+      for (int r = 0; r < 3; ++r) d[r] = d[r] / nn;
+      real best_t = (real)far_, value = 0;
+      for (int s = 0; s < ns; ++s) {
+        const double* S = sph + 5 * s;
+        const real oc[3] = {pos[0] - (real)S[0], pos[1] - (real)S[1], pos[2] - (real)S[2]};
+        const real rad = (real)S[3];
+        const real b = oc[0] * d[0] + oc[1] * d[1] + oc[2] * d[2];
+        const real disc = b * b - ((oc[0] * oc[0] + oc[1] * oc[1] + oc[2] * oc[2]) - rad * rad);
+        if (disc < 0) continue;
+        const real t = -b - SGO_SQRT(disc);
+        if (t < (real)near_ || t >= best_t) continue;
+        best_t = t;
+        real nrm[3];
+        for (int k = 0; k < 3; ++k) nrm[k] = ((pos[k] + t * d[k]) - (real)S[k]) / rad;
+        const real lambert = nrm[0] * -d[0] + nrm[1] * -d[1] + nrm[2] * -d[2];
+        value = lambert > 0 ? (real)S[4] * lambert : 0;
+      }
+      out[py * w + px] = value;
+    }
+  }
+}
+
+void sgo_render(const double* cam_pos, const double* cam_quat, int w, int h, double fov, double near_,
+                double far_, const double* spheres, int n_spheres, double* out) {
+  real p[3], q[4];
+  for (int k = 0; k < 3; ++k) p[k] = (real)cam_pos[k];
+  for (int k = 0; k < 4; ++k) q[k] = (real)cam_quat[k];
+  real* o = (real*)malloc(sizeof(real) * (size_t)(w * h));
+  render_real(p, q, w, h, fov, near_, far_, spheres, n_spheres, o);
+  for (int k = 0; k < w * h; ++k) out[k] = o[k];
+  free(o);
 }
 
 struct sgo_env {
@@ -902,6 +967,11 @@ struct sgo_env {
   /* TaskState */
   real* goals;
   real *goal_spawn, *goal_vel; /* ActiveTracking (envs.cpp:199-201) */
+  /* ImageMatching (envs.cpp:203-209): images n x wh, scenes n x 15, cameras n x 7 */
+  int W, H, wh;
+  real *timg, *cimg;
+  double* scenes;
+  real* tcam;
   int32_t *step_count, *hold_count, *wp_idx, *wp_len;
   int64_t* episode_count;
   real* wps; /* n x WP_CAP x 3 */
@@ -970,6 +1040,42 @@ static void refresh_tip(sgo_env* e, int64_t row) { /* envs.cpp:297-302 */
   fk_r(&e->m, e->q + row * e->A, e->tips + row * 3, NULL);
 }
 
+/* envs.cpp:269-286: three spheres below the workspace, then a target view
+ * from a mildly tilted configuration (sample_q_fraction 0.25, envs.cpp:31-39).
+ * Eigen::Vector3d(x, y, z) arguments are drawn right to left (g++): z, y, x. */
+static void sample_scene(sgo_env* e, int64_t row) {
+  sgo_pcg32* r = &e->rng[row];
+  const double s2 = 2.0 * e->cfg.goal_sigma;
+  double* sc = e->scenes + row * 15;
+  for (int k = 0; k < 3; ++k) {
+    const double z = -(e->radius + sgo_pcg32_uniform(r, 0.1, 0.25));
+    const double y = sgo_pcg32_uniform(r, -s2, s2);
+    const double x = sgo_pcg32_uniform(r, -s2, s2);
+    sc[5 * k + 0] = e->center[0] + x;
+    sc[5 * k + 1] = e->center[1] + y;
+    sc[5 * k + 2] = e->center[2] + z;
+    sc[5 * k + 3] = sgo_pcg32_uniform(r, 0.02, 0.05);
+    sc[5 * k + 4] = sgo_pcg32_uniform(r, 0.5, 1.0);
+  }
+  real q[SGO_MAX_JOINTS];
+  for (int d = 0; d < e->A; ++d) {
+    const sgo_joint* j = &e->m.joints[e->m.dof_to_joint[d]];
+    const double margin = 0.5 * (1.0 - 0.25) * (j->limit_hi - j->limit_lo);
+    q[d] = (real)sgo_pcg32_uniform(r, j->limit_lo + margin, j->limit_hi - margin);
+  }
+  real* cam = e->tcam + row * 7; /* identity tool base: compose is exact */
+  fk_r(&e->m, q, cam, cam + 3);
+  render_real(cam, cam + 3, e->W, e->H, e->cfg.render_fov, e->cfg.render_near, e->cfg.render_far, sc, 3,
+              e->timg + row * e->wh);
+}
+
+static void render_row(sgo_env* e, int64_t row) { /* envs.cpp:288-295 */
+  real cam[7];
+  fk_r(&e->m, e->q + row * e->A, cam, cam + 3);
+  render_real(cam, cam + 3, e->W, e->H, e->cfg.render_fov, e->cfg.render_near, e->cfg.render_far,
+              e->scenes + row * 15, 3, e->cimg + row * e->wh);
+}
+
 static int reset_row(sgo_env* e, int64_t row) { /* envs.cpp:304-360 */
   const int A = e->A;
   sgo_pcg32* r = &e->rng[row];
@@ -991,6 +1097,9 @@ static int reset_row(sgo_env* e, int64_t row) { /* envs.cpp:304-360 */
         e->goal_vel[row * 3 + k] = 0;
       }
     }
+  } else if (e->cfg.task == SGO_IMAGE_MATCHING) { /* envs.cpp:333-335 */
+    sample_scene(e, row);
+    render_row(e, row);
   } else { /* PathFollowing */
     int rc = sample_path(e, row);
     if (rc) return rc;
@@ -1012,6 +1121,9 @@ static void observe_row(sgo_env* e, int64_t row, real* dst) { /* envs.cpp:362-40
   for (int d = 0; d < A; ++d) out[off++] = e->qt[row * A + d];
   if (e->cfg.task == SGO_TARGET_REACHING || e->cfg.task == SGO_ACTIVE_TRACKING) {
     for (int k = 0; k < 3; ++k) out[off++] = e->goals[row * 3 + k];
+  } else if (e->cfg.task == SGO_IMAGE_MATCHING) { /* envs.cpp:400-406 */
+    for (int k = 0; k < e->wh; ++k) out[off++] = e->timg[row * e->wh + k];
+    for (int k = 0; k < e->wh; ++k) out[off++] = e->cimg[row * e->wh + k];
   } else {
     const real* wp = e->wps + (row * WP_CAP + e->wp_idx[row]) * 3;
     for (int k = 0; k < 3; ++k) out[off++] = wp[k];
@@ -1042,6 +1154,11 @@ static void phase_dynamics(void* ctx, int64_t b, int64_t end) { /* dynamics.cpp:
 static void phase_fk(void* ctx, int64_t b, int64_t end) { /* envs.cpp:456-463 */
   sgo_env* e = (sgo_env*)ctx;
   for (int64_t i = b; i < end; ++i) refresh_tip(e, i);
+}
+
+static void phase_render(void* ctx, int64_t b, int64_t end) { /* envs.cpp:464-473 */
+  sgo_env* e = (sgo_env*)ctx;
+  for (int64_t i = b; i < end; ++i) render_row(e, i);
 }
 
 static void phase_reward(void* ctx, int64_t b, int64_t end) { /* envs.cpp:478-594 */
@@ -1075,6 +1192,14 @@ static void phase_reward(void* ctx, int64_t b, int64_t end) { /* envs.cpp:478-59
         vel[k] += (real)(0.0 + e->cfg.tracking_vel_noise_std * sgo_pcg32_normal(r)); /* normal(0, std) */
         vel[k] = vel[k] < -vc ? -vc : (vc < vel[k] ? vc : vel[k]);
       }
+    } else if (e->cfg.task == SGO_IMAGE_MATCHING) { /* envs.cpp:513-523 */
+      const real* cur = e->cimg + i * e->wh;
+      const real* tgt = e->timg + i * e->wh;
+      real sum = 0;
+      for (int k = 0; k < e->wh; ++k) sum += (real)fabs((double)(cur[k] - tgt[k]));
+      const real err = sum / (real)e->wh;
+      reward = -err;
+      e->task_error[i] = err;
     } else { /* PathFollowing, envs.cpp:524-539 */
       const real* wps = e->wps + i * WP_CAP * 3;
       int32_t idx = e->wp_idx[i];
@@ -1119,7 +1244,13 @@ sgo_env* sgo_env_create(const sgo_env_cfg* c, const sgo_robot* m, const sgo_dyn*
   if (c->workspace_radius < 0.0) { seterr(err, errlen, "env.workspace_radius must be >= 0"); return NULL; }
   if (c->tracking_vel_noise_std < 0.0) { seterr(err, errlen, "env.tracking_vel_noise_std must be >= 0"); return NULL; }
   if (!(c->tracking_vel_clamp > 0.0)) { seterr(err, errlen, "env.tracking_vel_clamp must be > 0"); return NULL; }
-  if (c->task != SGO_TARGET_REACHING && c->task != SGO_PATH_FOLLOWING && c->task != SGO_ACTIVE_TRACKING) {
+  if (c->task == SGO_IMAGE_MATCHING) { /* RenderConfig::validate (render.cpp:24-32) */
+    if (c->render_w < 8 || c->render_h < 8) { seterr(err, errlen, "render: width and height must be >= 8"); return NULL; }
+    if (!(c->render_near > 0.0) || !(c->render_near < c->render_far)) { seterr(err, errlen, "render: require 0 < near < far"); return NULL; }
+    if (!(c->render_fov > 0.0) || !(c->render_fov < 3.1)) { seterr(err, errlen, "render: fov must be in (0, pi)"); return NULL; }
+  }
+  if (c->task != SGO_TARGET_REACHING && c->task != SGO_PATH_FOLLOWING && c->task != SGO_ACTIVE_TRACKING &&
+      c->task != SGO_IMAGE_MATCHING) {
     seterr(err, errlen, "oracle: task %d not restated", c->task);
     return NULL;
   }
@@ -1130,6 +1261,12 @@ sgo_env* sgo_env_create(const sgo_env_cfg* c, const sgo_robot* m, const sgo_dyn*
   else sgo_default_dynamics(m, &e->dyn);
   e->A = m->dof;
   e->O = 3 * m->dof + 6;
+  if (c->task == SGO_IMAGE_MATCHING) { /* envs.cpp:185-188 */
+    e->W = c->render_w;
+    e->H = c->render_h;
+    e->wh = e->W * e->H;
+    e->O = 3 * m->dof + 3 + 2 * e->wh;
+  }
   e->jaw = sgo_jaw_dof(m);
   e->n = c->n_envs;
   e->radius = c->workspace_radius > 0.0 ? c->workspace_radius : 3.0 * c->goal_sigma; /* :134 */
@@ -1153,6 +1290,12 @@ sgo_env* sgo_env_create(const sgo_env_cfg* c, const sgo_robot* m, const sgo_dyn*
   e->wp_len = (int32_t*)calloc((size_t)n, sizeof(int32_t));
   e->episode_count = (int64_t*)calloc((size_t)n, sizeof(int64_t));
   if (c->task == SGO_PATH_FOLLOWING) e->wps = (real*)calloc((size_t)(n * WP_CAP * 3), sizeof(real));
+  if (c->task == SGO_IMAGE_MATCHING) {
+    e->timg = (real*)calloc((size_t)(n * e->wh), sizeof(real));
+    e->cimg = (real*)calloc((size_t)(n * e->wh), sizeof(real));
+    e->scenes = (double*)calloc((size_t)(n * 15), sizeof(double));
+    e->tcam = (real*)calloc((size_t)(n * 7), sizeof(real));
+  }
   if (c->task == SGO_ACTIVE_TRACKING) {
     e->goal_spawn = (real*)calloc((size_t)(n * 3), sizeof(real));
     e->goal_vel = (real*)calloc((size_t)(n * 3), sizeof(real));
@@ -1176,6 +1319,7 @@ void sgo_env_destroy(sgo_env* e) {
   if (e->pool) pool_destroy(e->pool);
   free(e->q); free(e->qd); free(e->qt); free(e->rng); free(e->goals);
   free(e->goal_spawn); free(e->goal_vel);
+  free(e->timg); free(e->cimg); free(e->scenes); free(e->tcam);
   free(e->step_count); free(e->hold_count); free(e->wp_idx); free(e->wp_len);
   free(e->episode_count); free(e->wps); free(e->tips); free(e->obs); free(e->tobs);
   free(e->rewards); free(e->task_error); free(e->terminated); free(e->timed_out);
@@ -1215,6 +1359,7 @@ int sgo_env_step(sgo_env* e, const double* actions) { /* envs.cpp:437-617 */
   }
   for (int64_t c = 0; c < chunks; ++c) e->saturations += e->chunk_sat[c];
   parallel_for(e->pool, n, ROW_GRAIN, phase_fk, e);
+  if (e->cfg.task == SGO_IMAGE_MATCHING) parallel_for(e->pool, n, ROW_GRAIN, phase_render, e);
   parallel_for(e->pool, n, ROW_GRAIN, phase_reward, e);
   for (int64_t c = 0; c < chunks; ++c)
     if (e->chunk_bad_reward[c]) return env_fail(e, 1, "env.step: non-finite reward");
@@ -1296,6 +1441,19 @@ int sgo_env_get_waypoints(const sgo_env* e, int64_t row, double* out, int cap) {
   for (int k = 0; k < cnt && k < cap; ++k)
     for (int c = 0; c < 3; ++c) out[k * 3 + c] = e->wps[(row * WP_CAP + k) * 3 + c];
   return cnt;
+}
+
+void sgo_env_get_images(const sgo_env* e, double* target, double* current, double* scenes,
+                        double* tcams) {
+  if (!e->timg) return;
+  for (int64_t k = 0; k < e->n * e->wh; ++k) {
+    if (target) target[k] = e->timg[k];
+    if (current) current[k] = e->cimg[k];
+  }
+  for (int64_t k = 0; k < e->n * 15; ++k)
+    if (scenes) scenes[k] = e->scenes[k];
+  for (int64_t k = 0; k < e->n * 7; ++k)
+    if (tcams) tcams[k] = e->tcam[k];
 }
 
 void sgo_env_workspace(const sgo_env* e, double* center, double* radius) {

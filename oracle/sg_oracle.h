@@ -112,6 +112,9 @@ typedef struct {
   int64_t row_offset; /* global id of row 0: stream id = row_offset + row */
   /* MultiToolReaching (envs.hpp:56-58) */
   double collision_threshold, collision_penalty, view_penalty;
+  /* ImageMatching: RenderConfig (render.hpp:31-38) */
+  int32_t render_w, render_h;
+  double render_fov, render_near, render_far;
 } sgo_env_cfg;
 void sgo_env_cfg_default(sgo_env_cfg* c);
 
@@ -143,6 +146,16 @@ void sgo_env_workspace(const sgo_env* e, double* center3, double* radius);
 int64_t sgo_env_goal_draws(const sgo_env* e); /* total sample_goal attempts so far */
 /* overwrite state (for adversarial tests) */
 void sgo_env_set_state(sgo_env* e, const double* q, const double* qdot, const double* q_target);
+
+/* ---- render.cpp:34-67 ------------------------------------------------- */
+/* Pinhole render of spheres (n x {cx, cy, cz, radius, albedo}) from the camera
+ * pose (pos[3], quat wxyz); out: w*h row-major, top row first. */
+void sgo_render(const double* cam_pos, const double* cam_quat, int w, int h, double fov, double near_,
+                double far_, const double* spheres, int n_spheres, double* out);
+/* ImageMatching views: target / current images n x w*h, scenes n x 15,
+ * target cameras n x 7 (xyz, wxyz). */
+void sgo_env_get_images(const sgo_env* e, double* target, double* current, double* scenes,
+                        double* target_cameras);
 
 /* ---- MultiToolReaching: envs.cpp:101-116 (bases, min separation), 118-223
  * (ctor), 304-360 (reset_row), 362-408 (observe), 437-617 (step), 540-587

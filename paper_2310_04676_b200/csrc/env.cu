@@ -1134,6 +1134,8 @@ int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t g
       const uint64_t A = static_cast<uint64_t>(env->A);
       M.act_inc = r.inc;
       pcg_jump(static_cast<uint64_t>(global_n) * A, r.inc, M.jump_mult, M.jump_add);
+      for (int t = 0; t < M.T; ++t)  // a tool warp's first draw of the row: `off` draws after the row start
+        pcg_jump(static_cast<uint64_t>(M.tool[t].off), r.inc, M.tool[t].col_mult, M.tool[t].col_add);
       const unsigned grid = static_cast<unsigned>((env->n + 127) / 128);
       sg::bench_seed_kernel<<<grid, 128, 0, env->stream>>>(M.act_state, env->n, r.state,
                                                            static_cast<uint64_t>(first_step) * global_n * A,

@@ -1,14 +1,13 @@
-// MultiToolReaching step / reset kernels (multi.cuh). One thread owns one env
-// and walks its T tools in order with the tool index a compile-time constant
-// (T is a template parameter, so every ToolEnc field is a constant-bank load
-// at a fixed offset). Per tool the joint state comes from the DoF-major SoA
-// arrays (a warp's 32 envs read one 128-byte line per DoF), is integrated
-// with the reference's per-DoF PD law (dynamics.cpp:127-185, the same fp32
-// operation order as the single-tool generic kernel), written back, and the
-// tool FK (robot_model.cpp:371-395) is mapped through the tool's base pose.
-// Observation rows are staged per warp in shared memory (odd row stride: no
-// bank conflicts) and stored row by row with coalesced warp stores.
+// MultiToolReaching step / reset kernels (multi.cuh). The step kernel is a
+// team of T warps per 32 envs, warp t = tool t (lane = env): the tool's joint
+// state (DoF-major SoA in HBM, one 128-byte line per DoF per warp) stays in
+// registers for the whole fused launch, is integrated with the reference's
+// per-DoF PD law (dynamics.cpp:127-185, the same fp32 operation order as the
+// single-tool generic kernel), and the tool FK (robot_model.cpp:371-395) is
+// mapped through the tool's base pose. Warp 0 scores; observation rows are
+// staged in shared memory and stored as one contiguous float4 run per team.
 #include "multi.cuh"
+
 
 namespace sg {
 namespace {
@@ -155,118 +154,209 @@ __device__ __forceinline__ void warp_store_rows(float* __restrict__ g, const flo
     for (int c = lane; c < O; c += 32) g[(int64_t)r * O + c] = s[r * Os + c];
 }
 
+// Team shared memory (double-buffered by step parity where a buffer is read
+// after the step's last barrier).
+template <int T>
+struct MtSmem {
+  float tip[2][T][3][32];  // world tips, lane-contiguous
+  float ax[2][T][3][32];   // camera axes
+  uint32_t ended[2];
+};
+
+// One tool's step for the team's 32 envs (warp t = tool t). All tool warps
+// run the SAME code with t a warp-uniform runtime index into the parameter
+// block (per-tool code paths thrash the instruction cache: ncu showed
+// `no_instructions` as the top stall with a compile-time tool index).
+// State lives in registers for the whole launch.
+struct ToolState {
+  float q[kMaxToolDof], qd[kMaxToolDof], qt[kMaxToolDof];
+  uint64_t act_s = 0;  // GEN: stream state at the env's row start
+};
+
 template <int T, bool GEN>
-__global__ void __launch_bounds__(32 * kMtWarps) mt_step_kernel(const __grid_constant__ MtParams P, int k_steps) {
+struct ToolWarp {
+
+  __device__ __forceinline__ static void load(ToolState& S, const MtParams& P, const ToolEnc& E, int64_t i, bool active) {
+    float (&q)[kMaxToolDof] = S.q;
+    float (&qd)[kMaxToolDof] = S.qd;
+    float (&qt)[kMaxToolDof] = S.qt;
+    const int64_t n = P.n;
+#pragma unroll
+    for (int d = 0; d < kMaxToolDof; ++d) {
+      q[d] = qd[d] = qt[d] = 0.f;
+      if (d < E.robot.dof && active) {
+        q[d] = P.q[(E.off + d) * n + i];
+        qd[d] = P.qd[(E.off + d) * n + i];
+        qt[d] = P.qt[(E.off + d) * n + i];
+      }
+    }
+  }
+  __device__ __forceinline__ static void store(const ToolState& S, const MtParams& P, const ToolEnc& E, int64_t i, bool active) {
+    const float (&q)[kMaxToolDof] = S.q;
+    const float (&qd)[kMaxToolDof] = S.qd;
+    const float (&qt)[kMaxToolDof] = S.qt;
+    const int64_t n = P.n;
+    if (!active) return;
+#pragma unroll
+    for (int d = 0; d < kMaxToolDof; ++d) {
+      if (d >= E.robot.dof) continue;
+      P.q[(E.off + d) * n + i] = q[d];
+      P.qd[(E.off + d) * n + i] = qd[d];
+      P.qt[(E.off + d) * n + i] = qt[d];
+    }
+  }
+
+  // dynamics (dynamics.cpp:127-185) + FK + staging of the tool's obs columns
+  __device__ __forceinline__ static void step(ToolState& S, const MtParams& P, const ToolEnc& E, int t, const float* s_act_row,
+                              float* s_act_out, float* o, int& sat, int& bad, float (&tip)[3], float (&axis)[3]) {
+    float (&q)[kMaxToolDof] = S.q;
+    float (&qd)[kMaxToolDof] = S.qd;
+    float (&qt)[kMaxToolDof] = S.qt;
+    uint64_t& act_s = S.act_s;
+    const RobotTable& R = E.robot;
+    const int dof = R.dof, jaw = R.jaw, off = E.off, A = P.A;
+    const int mode = P.control_mode;
+    float kpqt[kMaxToolDof], vt[kMaxToolDof], tc[kMaxToolDof];
+    uint64_t ds = GEN ? act_s * E.col_mult + E.col_add : 0;
+#pragma unroll
+    for (int d = 0; d < kMaxToolDof; ++d) {
+      kpqt[d] = vt[d] = tc[d] = 0.f;
+      if (d >= dof) continue;
+      float ad;
+      if (GEN) {
+        // uniform(-1, 1) of bench.cpp:34 = (u - 2^31) * 2^-31, exact in fp64, rounded once
+        const uint32_t u = pcg_next(ds, P.act_inc);
+        ad = __int2float_rn((int32_t)(u ^ 0x80000000u)) * 0x1.0p-31f;
+        s_act_out[off + d] = ad;
+      } else {
+        ad = s_act_row[off + d];
+        if (!isfinite(ad)) {
+          bad = 1;
+          ad = 0.f;
+        }
+        if (ad < -1.f || ad > 1.f) {
+          ad = ad < -1.f ? -1.f : 1.f;
+          ++sat;
+        }
+      }
+      const float lo = R.lo[d], hi = R.hi[d];
+      if (mode == kModePosition) {
+        qt[d] = (d == jaw) ? (ad > 0.f ? hi : lo) : rescale(ad, lo, hi);
+        kpqt[d] = R.kp[d] * qt[d];
+      } else if (mode == kModeVelocity) {
+        vt[d] = rescale(ad, -R.vel[d], R.vel[d]);
+      } else {
+        tc[d] = rescale(ad, -R.eff[d], R.eff[d]);
+      }
+    }
+    if (GEN) act_s = act_s * P.jump_mult + P.jump_add;
+    const float dt = P.dt_sub;
+    for (int s = 0; s < P.substeps; ++s) {
+#pragma unroll
+      for (int d = 0; d < kMaxToolDof; ++d) {
+        if (d >= dof) continue;
+        const float ef = R.eff[d], vl = R.vel[d];
+        float tau;
+        if (mode == kModePosition) tau = fmaf(-R.kd[d], qd[d], fmaf(-R.kp[d], q[d], kpqt[d]));
+        else if (mode == kModeVelocity) tau = R.kd[d] * (vt[d] - qd[d]);
+        else tau = tc[d];
+        tau = fminf(fmaxf(tau, -ef), ef);
+        float vv = qd[d] + (tau - R.damping[d] * qd[d]) * R.dt_over_inertia[d];
+        vv = fminf(fmaxf(vv, -vl), vl);
+        const float qq = q[d] + vv * dt;
+        const float qc = fminf(fmaxf(qq, R.lo[d]), R.hi[d]);  // limit projection
+        qd[d] = qc != qq ? 0.f : vv;
+        q[d] = qc;
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < kMaxToolDof; ++d) {
+      if (d >= dof) continue;
+      o[off + d] = q[d];
+      o[A + off + d] = qd[d];
+      o[2 * A + 3 * T + off + d] = qt[d];
+    }
+    tool_fk(E, q, tip, axis);  // refresh_tips (envs.cpp:456-463)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o[2 * A + 3 * t + k] = tip[k];
+  }
+};
+
+// Fused multi-tool step: a CTA is a team of T warps for 32 envs; warp t runs
+// tool t (dynamics, FK, its observation columns) with its state in registers
+// for the whole launch, publishes the world tip / camera axis in shared
+// memory, and after one barrier warp 0 scores the 32 envs (camera goals,
+// view / collision penalties, hold, flags); after a second barrier all warps
+// store the team's 32 observation rows (one contiguous run: float4 copy).
+// Rows that ended are copied to terminal_observations, reset by warp 0
+// (reset_row through HBM) and re-observed; the tool warps then reload them.
+template <int T, bool GEN>
+__global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__ MtParams P, int k_steps) {
   extern __shared__ __align__(16) float smem[];
+  __shared__ MtSmem<T> ts;
+  __shared__ __align__(16) ToolEnc s_tool[T];  // per-tool tables, dynamically indexed by warp (LDS, not param LD)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    static_assert(sizeof(ToolEnc) % 16 == 0, "ToolEnc copied as int4");
+    const int4* src = reinterpret_cast<const int4*>(&P.tool[0]);
+    int4* dst = reinterpret_cast<int4*>(s_tool);
+    for (int k = threadIdx.x; k < (int)(T * sizeof(ToolEnc) / 16); k += 32 * T) dst[k] = src[k];
+    __syncthreads();
+  }
+  const ToolEnc& E = s_tool[warp];
   const int64_t n = P.n;
-  const int A = P.A, O = P.O, Os = P.Os;
-  const int64_t row0 = ((int64_t)blockIdx.x * kMtWarps + warp) * 32;
-  if (row0 >= n) return;  // whole warp (no CTA-wide barriers below)
+  const int A = P.A, O = P.O;
+  const int64_t row0 = (int64_t)blockIdx.x * 32;
   const int64_t i = row0 + lane;
   const bool active = i < n;
   const int rows = (int)min((int64_t)32, n - row0);
-  float* s_obs = smem + warp * 32 * (Os + A);
-  float* s_act = s_obs + 32 * Os;
-  float* o = s_obs + lane * Os;
-  const int mode = P.control_mode;
+  float* s_obs = smem;              // [2][32][O]
+  float* s_act = smem + 2 * 32 * O;  // [32][A]
+  const bool full = rows == 32;
 
-  uint64_t act_s = 0;
-  if (GEN) {
-    if (active) act_s = P.act_state[i];
-  } else {
-    // the warp's caller action rows are one contiguous run: coalesced load
+  // one register state per thread; the warp's tool index selects the code
+  // path (ToolWarp<..., t> adds no data, only compile-time offsets)
+  ToolState st;
+  using TW = ToolWarp<T, GEN>;
+  TW::load(st, P, E, i, active);
+  if (GEN && active) st.act_s = P.act_state[i];
+  if (!GEN) {  // the team's caller action rows: one contiguous run
     const float* src = P.actions + row0 * A;
-    for (int k = lane; k < rows * A; k += 32) s_act[k] = src[k];
-    __syncwarp();
+    const int cnt = rows * A;
+    if (full && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+      for (int k = threadIdx.x; k < cnt / 4; k += 32 * T)
+        reinterpret_cast<float4*>(s_act)[k] = reinterpret_cast<const float4*>(src)[k];
+      for (int k = (cnt / 4) * 4 + threadIdx.x; k < cnt; k += 32 * T) s_act[k] = src[k];
+    } else {
+      for (int k = threadIdx.x; k < cnt; k += 32 * T) s_act[k] = src[k];
+    }
+    __syncthreads();
   }
+  // scorer (warp 0) task state
+  int32_t sc = 0, hc = 0;
+  float g[T][3];
+  const auto load_task = [&]() {
+#pragma unroll
+    for (int u = 0; u < T; ++u)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) g[u][k] = active ? P.goals[(3 * u + k) * n + i] : 0.f;
+    sc = active ? P.step_count[i] : 0;
+    hc = active ? P.hold_count[i] : 0;
+  };
+  if (warp == 0) load_task();
 
   for (int step = 0; step < k_steps; ++step) {
+    const int b = step & 1;
+    float* s_rows = s_obs + b * 32 * O;
+    float* o = s_rows + lane * O;
     int sat = 0, bad = 0;
-    float tw[T][3], ax[T][3];
-    uint64_t ds = act_s;  // GEN: the row's draws are consecutive in column order
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const ToolEnc& E = P.tool[t];
-      const RobotTable& R = E.robot;
-      const int dof = R.dof, jaw = R.jaw, off = E.off;
-      float q[kMaxToolDof], qd[kMaxToolDof], qt[kMaxToolDof], kpqt[kMaxToolDof], vt[kMaxToolDof],
-          tc[kMaxToolDof];
-#pragma unroll
-      for (int d = 0; d < kMaxToolDof; ++d) {
-        q[d] = qd[d] = qt[d] = kpqt[d] = vt[d] = tc[d] = 0.f;
-        if (d >= dof) continue;
-        const int64_t c = off + d;
-        if (active) {
-          q[d] = P.q[c * n + i];
-          qd[d] = P.qd[c * n + i];
-          qt[d] = P.qt[c * n + i];
-        }
-        float ad;
-        if (GEN) {
-          // uniform(-1, 1) of bench.cpp:34 = (u - 2^31) * 2^-31, exact in fp64, rounded once
-          const uint32_t u = pcg_next(ds, P.act_inc);
-          ad = __int2float_rn((int32_t)(u ^ 0x80000000u)) * 0x1.0p-31f;
-          s_act[lane * A + c] = ad;
-        } else {
-          ad = s_act[lane * A + c];
-          if (!isfinite(ad)) {
-            bad = 1;
-            ad = 0.f;
-          }
-          if (ad < -1.f || ad > 1.f) {
-            ad = ad < -1.f ? -1.f : 1.f;
-            ++sat;
-          }
-        }
-        const float lo = R.lo[d], hi = R.hi[d];
-        if (mode == kModePosition) {
-          qt[d] = (d == jaw) ? (ad > 0.f ? hi : lo) : rescale(ad, lo, hi);
-          kpqt[d] = R.kp[d] * qt[d];
-        } else if (mode == kModeVelocity) {
-          vt[d] = rescale(ad, -R.vel[d], R.vel[d]);
-        } else {
-          tc[d] = rescale(ad, -R.eff[d], R.eff[d]);
-        }
-      }
-      // dynamics.cpp:133-185, per-DoF operation order of the reference
-      const float dt = P.dt_sub;
-      for (int s = 0; s < P.substeps; ++s) {
-#pragma unroll
-        for (int d = 0; d < kMaxToolDof; ++d) {
-          if (d >= dof) continue;
-          const float ef = R.eff[d], vl = R.vel[d];
-          float tau;
-          if (mode == kModePosition) tau = fmaf(-R.kd[d], qd[d], fmaf(-R.kp[d], q[d], kpqt[d]));
-          else if (mode == kModeVelocity) tau = R.kd[d] * (vt[d] - qd[d]);
-          else tau = tc[d];
-          tau = fminf(fmaxf(tau, -ef), ef);
-          float vv = qd[d] + (tau - R.damping[d] * qd[d]) * R.dt_over_inertia[d];
-          vv = fminf(fmaxf(vv, -vl), vl);
-          const float qq = q[d] + vv * dt;
-          const float qc = fminf(fmaxf(qq, R.lo[d]), R.hi[d]);  // limit projection
-          qd[d] = qc != qq ? 0.f : vv;
-          q[d] = qc;
-        }
-      }
-#pragma unroll
-      for (int d = 0; d < kMaxToolDof; ++d) {
-        if (d >= dof) continue;
-        const int64_t c = off + d;
-        if (active) {
-          P.q[c * n + i] = q[d];
-          P.qd[c * n + i] = qd[d];
-          P.qt[c * n + i] = qt[d];
-        }
-        o[c] = q[d];
-        o[A + c] = qd[d];
-        o[2 * A + 3 * T + c] = qt[d];
-      }
-      tool_fk(E, q, tw[t], ax[t]);  // refresh_tips (envs.cpp:456-463)
+    {
+      float tip[3], axis[3];
+      TW::step(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        o[2 * A + 3 * t + k] = tw[t][k];
-        if (active) P.tips[(3 * t + k) * n + i] = tw[t][k];
+        ts.tip[b][warp][k][lane] = tip[k];
+        ts.ax[b][warp][k][lane] = axis[k];
       }
     }
     if (!GEN) {
@@ -275,113 +365,127 @@ __global__ void __launch_bounds__(32 * kMtWarps) mt_step_kernel(const __grid_con
       if (wsat && lane == 0) atomicAdd(P.sat_total, (unsigned long long)wsat);
       if (__any_sync(0xffffffffu, bad) && bad) atomicOr(P.err, kErrNonFiniteAction);
     }
+    __syncthreads();  // B1: every tool published
 
-    // ---- reward / camera goal / collision / hold / flags (envs.cpp:540-593)
-    int32_t sc = 0, hc = 0;
-    float g[T][3];
-    if (active) {
-      sc = P.step_count[i] + 1;
-      hc = P.hold_count[i];
+    if (warp == 0) {  // ---- scoring (envs.cpp:540-593)
+      float tw[T][3];
 #pragma unroll
-      for (int t = 0; t < T; ++t)
+      for (int u = 0; u < T; ++u)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) g[t][k] = P.goals[(3 * t + k) * n + i];
-    } else {
+        for (int k = 0; k < 3; ++k) tw[u][k] = ts.tip[b][u][k][lane];
+      sc += 1;
+      float reward = 0.f, err_sum = 0.f;
+      int err_count = 0;
+      bool all_in = true;
 #pragma unroll
-      for (int t = 0; t < T; ++t) g[t][0] = g[t][1] = g[t][2] = 0.f;
-    }
-    float reward = 0.f, err_sum = 0.f;
-    int err_count = 0;
-    bool all_in = true;
+      for (int u = 0; u < T; ++u) {
+        if (P.tool[u].camera) {
+          float mid[3];
+          camera_mid<T>(tw, u, mid);
+          const float tm[3] = {mid[0] - tw[u][0], mid[1] - tw[u][1], mid[2] - tw[u][2]};
+          const float nrm = sqrtf(tm[0] * tm[0] + tm[1] * tm[1] + tm[2] * tm[2]);
+          if (nrm > 1e-12f) {
+            // acos(clamp(axis . to_mid/|to_mid|, -1, 1)) evaluated as
+            // atan2(|axis x u|, axis . u): the same angle (|axis| = 1)
+            // without acos's loss of precision near 0 and pi in fp32
+            const float uu[3] = {tm[0] / nrm, tm[1] / nrm, tm[2] / nrm};
+            const float a0 = ts.ax[b][u][0][lane], a1 = ts.ax[b][u][1][lane], a2 = ts.ax[b][u][2][lane];
+            const float cx = a1 * uu[2] - a2 * uu[1], cy = a2 * uu[0] - a0 * uu[2], cz = a0 * uu[1] - a1 * uu[0];
+            reward += -P.view_penalty * atan2f(sqrtf(cx * cx + cy * cy + cz * cz), a0 * uu[0] + a1 * uu[1] + a2 * uu[2]);
+          }
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      if (P.tool[t].camera) {
-        float mid[3];
-        camera_mid<T>(tw, t, mid);
-        const float tm[3] = {mid[0] - tw[t][0], mid[1] - tw[t][1], mid[2] - tw[t][2]};
-        const float nrm = sqrtf(tm[0] * tm[0] + tm[1] * tm[1] + tm[2] * tm[2]);
-        if (nrm > 1e-12f) {
-          // acos(clamp(axis . to_mid/|to_mid|, -1, 1)) evaluated as
-          // atan2(|axis x u|, axis . u): the same angle (|axis| = 1) without
-          // acos's loss of precision near 0 and pi in fp32
-          const float u[3] = {tm[0] / nrm, tm[1] / nrm, tm[2] / nrm};
-          const float* a = ax[t];
-          const float cx = a[1] * u[2] - a[2] * u[1], cy = a[2] * u[0] - a[0] * u[2], cz = a[0] * u[1] - a[1] * u[0];
-          const float ang = atan2f(sqrtf(cx * cx + cy * cy + cz * cz), a[0] * u[0] + a[1] * u[1] + a[2] * u[2]);
-          reward += -P.view_penalty * ang;
+          for (int k = 0; k < 3; ++k) g[u][k] = mid[k];
+        } else {
+          const float dx = tw[u][0] - g[u][0], dy = tw[u][1] - g[u][1], dz = tw[u][2] - g[u][2];
+          const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
+          reward += P.rho * dist;
+          err_sum += dist;
+          ++err_count;
+          if (dist >= P.success_radius) all_in = false;
         }
+      }
+      float min_sep = __int_as_float(0x7f800000);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) g[t][k] = mid[k];
-        if (active)
+      for (int u = 0; u + 1 < T; ++u)
 #pragma unroll
-          for (int k = 0; k < 3; ++k) P.goals[(3 * t + k) * n + i] = mid[k];
-      } else {
-        const float dx = tw[t][0] - g[t][0], dy = tw[t][1] - g[t][1], dz = tw[t][2] - g[t][2];
-        const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
-        reward += P.rho * dist;
-        err_sum += dist;
-        ++err_count;
-        if (dist >= P.success_radius) all_in = false;
+        for (int v = u + 1; v < T; ++v) {
+          const float dx = tw[u][0] - tw[v][0], dy = tw[u][1] - tw[v][1], dz = tw[u][2] - tw[v][2];
+          min_sep = fminf(min_sep, sqrtf(dx * dx + dy * dy + dz * dz));
+        }
+      if (min_sep < P.collision_threshold) reward += -P.collision_penalty;
+      hc = all_in ? hc + 1 : 0;
+      const bool term = hc >= P.success_hold;
+      const bool tout = sc >= P.episode_len;
+      if (active) {
+        if (!isfinite(reward)) atomicOr(P.err, kErrNonFiniteReward);
+        P.rewards[i] = reward;
+        P.task_error[i] = err_count > 0 ? err_sum / (float)err_count : 0.f;
+        P.terminated[i] = term ? 1 : 0;
+        P.timed_out[i] = tout ? 1 : 0;
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            P.tips[(3 * u + k) * n + i] = tw[u][k];
+            if (P.tool[u].camera) P.goals[(3 * u + k) * n + i] = g[u][k];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < T; ++u)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * A + 3 * T + 3 * u + k] = g[u][k];
+      const unsigned ended = __ballot_sync(0xffffffffu, active && (term || tout));
+      if (lane == 0) {
+        ts.ended[b] = ended;
+        if (ended) atomicAdd(P.ended_total, (unsigned long long)__popc(ended));
       }
     }
-    float min_sep = __int_as_float(0x7f800000);
-#pragma unroll
-    for (int t = 0; t + 1 < T; ++t)
-#pragma unroll
-      for (int u = t + 1; u < T; ++u) {
-        const float dx = tw[t][0] - tw[u][0], dy = tw[t][1] - tw[u][1], dz = tw[t][2] - tw[u][2];
-        min_sep = fminf(min_sep, sqrtf(dx * dx + dy * dy + dz * dz));
-      }
-    if (min_sep < P.collision_threshold) reward += -P.collision_penalty;
-    const float terr = err_count > 0 ? err_sum / (float)err_count : 0.f;
-    hc = all_in ? hc + 1 : 0;
-    const bool term = hc >= P.success_hold;
-    const bool tout = sc >= P.episode_len;
-    if (active) {
-      if (!isfinite(reward)) atomicOr(P.err, kErrNonFiniteReward);
-      P.step_count[i] = sc;
-      P.hold_count[i] = hc;
-      P.rewards[i] = reward;
-      P.task_error[i] = terr;
-      P.terminated[i] = term ? 1 : 0;
-      P.timed_out[i] = tout ? 1 : 0;
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) o[3 * A + 3 * T + 3 * t + k] = g[t][k];
-    __syncwarp();
+    __syncthreads();  // B2: rows scored and staged
+
+    // ---- team store of the 32 observation rows (and the generated actions)
     float* g_obs = P.obs + row0 * O;
-    warp_store_rows(g_obs, s_obs, rows, O, Os, lane);
+    const int cnt = rows * O;
+    if (full) {  // 32 * O floats from a 16-byte aligned row block
+      const float4* s4 = reinterpret_cast<const float4*>(s_rows);
+      float4* g4 = reinterpret_cast<float4*>(g_obs);
+      for (int k = threadIdx.x; k < cnt / 4; k += 32 * T) g4[k] = s4[k];
+      for (int k = (cnt / 4) * 4 + threadIdx.x; k < cnt; k += 32 * T) g_obs[k] = s_rows[k];
+    } else {
+      for (int k = threadIdx.x; k < cnt; k += 32 * T) g_obs[k] = s_rows[k];
+    }
     if (GEN) {
       float* g_act = P.act_buf + row0 * A;
-      for (int k = lane; k < rows * A; k += 32) g_act[k] = s_act[k];
-      act_s = act_s * P.jump_mult + P.jump_add;
+      for (int k = threadIdx.x; k < rows * A; k += 32 * T) g_act[k] = s_act[k];
     }
-
-    // ---- ended rows: terminal copy, reset_row, re-observe (envs.cpp:604-615)
-    const unsigned ended = __ballot_sync(0xffffffffu, active && (term || tout));
-    if (ended) {
-      if (lane == 0) atomicAdd(P.ended_total, (unsigned long long)__popc(ended));
+    const unsigned ended = ts.ended[b];
+    if (ended) {  // ---- terminal copy, reset_row, re-observe (envs.cpp:604-615)
       for (unsigned m = ended; m; m &= m - 1) {
         const int r = __ffs(m) - 1;
-        for (int c = lane; c < O; c += 32) P.tobs[(row0 + r) * O + c] = s_obs[r * Os + c];
+        for (int c = threadIdx.x; c < O; c += 32 * T) P.tobs[(row0 + r) * O + c] = s_rows[r * O + c];
       }
-      __syncwarp();
-      if ((ended >> lane) & 1) {
-        const int e = mt_reset_env<T>(P, i);
-        if (e) atomicOr(P.err, e);
-        stage_row_from_state<T>(P, i, o);
+      if (warp == 0) {
+        if ((ended >> lane) & 1) {
+          const int e = mt_reset_env<T>(P, i);
+          if (e) atomicOr(P.err, e);
+          stage_row_from_state<T>(P, i, o);
+        }
+        if ((ended >> lane) & 1) load_task();
       }
-      __syncwarp();
+      __syncthreads();  // reset state in HBM, rows re-staged
       for (unsigned m = ended; m; m &= m - 1) {
         const int r = __ffs(m) - 1;
-        for (int c = lane; c < O; c += 32) g_obs[(int64_t)r * O + c] = s_obs[r * Os + c];
+        for (int c = threadIdx.x; c < O; c += 32 * T) g_obs[(int64_t)r * O + c] = s_rows[r * O + c];
       }
+      if ((ended >> lane) & 1) TW::load(st, P, E, i, active);
     }
-    __syncwarp();
   }
-  if (GEN && active) P.act_state[i] = act_s;
+  if (warp == 0 && active) {
+    P.step_count[i] = sc;
+    P.hold_count[i] = hc;
+  }
+  TW::store(st, P, E, i, active);
+  if (GEN && active && warp == 0) P.act_state[i] = st.act_s;
 }
 
 template <int T>
@@ -420,12 +524,15 @@ cudaError_t launch_t(const MtParams& P, int k_steps, bool gen, bool reset, cudaS
   if (reset) {
     if ((e = prep((const void*)mt_reset_kernel<T>)) != cudaSuccess) return e;
     mt_reset_kernel<T><<<grid, 32 * kMtWarps, sm, st>>>(P);
-  } else if (gen) {
-    if ((e = prep((const void*)mt_step_kernel<T, true>)) != cudaSuccess) return e;
-    mt_step_kernel<T, true><<<grid, 32 * kMtWarps, sm, st>>>(P, k_steps);
   } else {
-    if ((e = prep((const void*)mt_step_kernel<T, false>)) != cudaSuccess) return e;
-    mt_step_kernel<T, false><<<grid, 32 * kMtWarps, sm, st>>>(P, k_steps);
+    const unsigned tgrid = (unsigned)((P.n + 31) / 32);
+    const size_t tsm = (size_t)(2 * 32 * P.O + 32 * P.A) * sizeof(float);
+    const void* fn = gen ? (const void*)mt_step_kernel<T, true> : (const void*)mt_step_kernel<T, false>;
+    if (tsm > 40 * 1024 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm)) !=
+                               cudaSuccess)
+      return e;
+    if (gen) mt_step_kernel<T, true><<<tgrid, 32 * T, tsm, st>>>(P, k_steps);
+    else mt_step_kernel<T, false><<<tgrid, 32 * T, tsm, st>>>(P, k_steps);
   }
   return cudaGetLastError();
 }

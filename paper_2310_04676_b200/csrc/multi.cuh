@@ -15,7 +15,7 @@ namespace sg {
 
 constexpr int kMaxTools = 4;      // device path: up to 4 tools of <= 8 DoF each
 constexpr int kMaxToolDof = 8;
-constexpr int kMtWarps = 4;       // warps per CTA; each warp stages its own 32 rows
+constexpr int kMtWarps = 4;       // reset kernel: warps per CTA, each stages its own 32 rows
 
 struct ToolEnc {
   RobotTable robot;   // build_table: fixed joints folded, tip offset in the last DoF frame
@@ -25,6 +25,7 @@ struct ToolEnc {
   int32_t camera;     // models_[t].name == "ecm" (envs.cpp:339, 545)
   int32_t off;        // first action / DoF column of the tool
   double center[3];   // workspace centre: base.transform_point(FK(mid)) (envs.cpp:159-161)
+  uint64_t col_mult, col_add;  // bench stream: advance by `off` draws (row start -> the tool's first column)
 };
 
 struct MtParams {
