@@ -42,6 +42,9 @@ CONFIGS = {
     "multitool": dict(robots=("psm", "psm", "ecm"), task="multi_tool_reaching", n_envs=16384, goal_sigma=0.05,
                       workload="trimanual MultiToolReaching (PSM + PSM + ECM camera), 16384 envs/GPU, random "
                                "actions (SURVEY 8f rank 3; not a BASELINE config)"),
+    "image": dict(robot="psm", task="image_matching", n_envs=16384, goal_sigma=0.05,
+                  workload="PSM ImageMatching (32x32 camera render per env-step), 16384 envs/GPU, random actions "
+                           "(SURVEY 8f rank 4; not a BASELINE config)"),
     "ppo": dict(robot="psm", task="target_reaching", n_envs=16384, goal_sigma=0.05,
                 workload="full PPO rollout+update on PSM reach, 16384 envs/GPU, n_steps 32, 5 epochs x 4 "
                          "minibatches, 256/128/64 ELU MLP (BASELINE configs[4])"),
@@ -60,7 +63,7 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def step_bytes(A: int, O: int, fused: int, reset_frac: float, tools: int = 1) -> dict:
+def step_bytes(A: int, O: int, fused: int, reset_frac: float, tools: int = 1, step_read: int = 0) -> dict:
     """Algorithmic HBM bytes of one fused launch per env.
     Per launch: joint state q/qdot/q_target read+write (3*A*4*2), goal read+write
     and tip write (3*4*3), step/hold counters r+w (16), bench stream state r+w (16).
@@ -70,7 +73,7 @@ def step_bytes(A: int, O: int, fused: int, reset_frac: float, tools: int = 1) ->
     state r+w (16), episode counter r+w (16), reset state write + reload
     (3*A*4*2 + 24)."""
     per_launch = 3 * A * 4 * 2 + 3 * tools * 4 * 3 + 16 + 16
-    per_step = A * 4 + O * 4 + 8 + 2
+    per_step = A * 4 + O * 4 + 8 + 2 + step_read
     per_reset = O * 4 + 16 * tools + 16 + 3 * A * 4 * 2 + 24 * tools
     total = per_launch + fused * (per_step + reset_frac * per_reset)
     return dict(per_launch=per_launch, per_step=per_step, per_reset=per_reset,
@@ -157,7 +160,7 @@ def cpu_reference(cfg: dict, steps: int, budget_s: float, threads: int = 0):
     if "robots" in cfg:
         return cpu_reference_multi(O, cfg, steps, budget_s, threads)
     m = O.resolve_robot(cfg["robot"])
-    task = O.PATH_FOLLOWING if cfg["task"] == "path_following" else O.TARGET_REACHING
+    task = {"path_following": O.PATH_FOLLOWING, "image_matching": O.IMAGE_MATCHING}.get(cfg["task"], O.TARGET_REACHING)
     ocfg = O.env_config(n_envs=cfg["n_envs"], seed=0, task=task, goal_sigma=cfg["goal_sigma"])
     lanes = threads or os.cpu_count() or 1
     # calibrate, then size the sample to the time budget
@@ -373,7 +376,9 @@ def main():
 
     # ---- roofline of the dominant kernel (env_step_kernel, fused bench variant)
     resets = (steps_done // 300) - ((steps_done - args.steps) // 300)
-    b = step_bytes(A, O, F, resets / max(args.steps, 1), tools=len(robots))
+    # ImageMatching reads the env's target image every step (reward + observation copy)
+    wh = (O - 3 * A - 3) // 2 if cfg["task"] == "image_matching" else 0
+    b = step_bytes(A, O, F, resets / max(args.steps, 1), tools=len(robots), step_read=4 * wh)
     full = [ms for ms, kf in zip(launch_ms, launches) if kf == F]
     avg_launch_s = (sum(full) / len(full)) * 1e-3 if full else t_ms * 1e-3 / len(launches)
     peak, peak_kind = peaks()
@@ -470,6 +475,7 @@ def main():
                         l2="256 MiB flush between timed launches; per-launch state read cold from HBM"),
             roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
                           traffic=traffic, peak_kind=peak_kind, kernel=(f"mt_step_kernel<T={len(robots)}, GEN> ({F} fused steps/launch)" if len(robots) > 1 else
+                                  f"im_step_kernel<8, GEN> ({F} fused steps/launch)" if wh else
                                   f"env_step_kernel<{cfg['robot'].upper()} chain, 2 team warps, GEN> ({F} fused steps/launch)"),
                           bytes_per_env_step=b["per_env_step"], bytes_per_launch=n * b["per_env_launch"],
                           avg_launch_us=avg_launch_s * 1e6),

@@ -18,6 +18,7 @@
  *   sg_env_layout_*          VecTaskEnv::layout()          include/scalpel/envs.hpp:137, src/envs.cpp:166-192
  *   sg_env_tools             VecTaskEnv::tool_base / workspace centres  include/scalpel/envs.hpp:144,
  *                                                             src/envs.cpp:101-116,136-161
+ *   sg_env_images            TaskState image-matching fields         include/scalpel/envs.hpp:73-76
  *   sg_env_reset             BatchedEnv::reset()           src/envs.cpp:425-435
  *   sg_env_step              BatchedEnv::step(actions)     src/envs.cpp:437-617
  *   sg_env_step_host         BatchedEnv::step on host buffers (same call a host-side
@@ -96,6 +97,13 @@ typedef struct sg_env_config {
   const double* tool_bases;
   int32_t n_tool_bases;
   int32_t reserved1;
+  /* ImageMatching camera (RenderConfig, render.hpp:31-38; defaults 32 x 32,
+   * 60 deg horizontal fov, near 0.005, far 2.0). */
+  int32_t render_width;
+  int32_t render_height;
+  double render_fov;
+  double render_near;
+  double render_far;
 } sg_env_config;
 
 /* scalpel::DynamicsConfig (include/scalpel/dynamics.hpp:34-44). Gain arrays
@@ -199,6 +207,13 @@ int sg_env_workspace(const sg_env* env, double* center3, double* radius);
  * (7 per tool: xyz, quaternion wxyz), dofs (1 per tool). Single-robot tasks
  * report one tool with the identity base. */
 int sg_env_tools(const sg_env* env, int32_t* n_tools, double* centers, double* bases, int32_t* dofs);
+/* ImageMatching task state (TaskState::target_images / scenes / target_cameras,
+ * envs.hpp:73-76) as device views: target images n x (w*h) fp32, scenes
+ * n x 16 fp32 (3 spheres x {cx, cy, cz, radius, albedo}, 1 pad), target
+ * cameras n x 12 fp32 (rotation row-major, position). SG_ERR_CONFIG for
+ * other tasks. */
+int sg_env_images(const sg_env* env, float** d_target, float** d_scenes, float** d_target_cameras, int32_t* width,
+                  int32_t* height);
 
 int sg_env_reset(sg_env* env, sg_step_views* out);
 /* d_actions: device, row-major n_envs x action_dim fp32 (stride = action_dim). */

@@ -21,6 +21,7 @@
 #include "kernels.cuh"
 #include "launch.hpp"
 #include "multi.cuh"
+#include "image.cuh"
 #include "robot.hpp"
 #include "sg_env.h"
 
@@ -253,6 +254,10 @@ struct sg_env {
   std::vector<std::array<double, 7>> bases;    // per tool: xyz, quaternion wxyz
   std::vector<std::array<double, 3>> centers;  // per tool workspace centre
   unsigned long long mt_ended_seen = 0;        // device ended-row total at the last host step
+  // ImageMatching (image.cuh)
+  bool image = false;
+  sg::ImParams I{};
+  bool own_kernel() const { return multi || image; }  // task kernels outside the env_step family
 
   ~sg_env() {
     cudaSetDevice(device);
@@ -273,9 +278,19 @@ struct sg_env {
       for (void* b : mb)
         if (b) cudaFree(b);
     }
+    if (image) {
+      void* ib[] = {I.q, I.qd, I.qt, I.tips, I.step_count, I.hold_count, I.episode_count, I.rng_state, I.rng_inc,
+                    I.scenes, I.target, I.tcam, I.obs, I.tobs, I.rewards, I.task_error, I.terminated, I.timed_out,
+                    I.act_state, I.act_buf};
+      for (void* b : ib)
+        if (b) cudaFree(b);
+    }
   }
-  int32_t* err_word() const { return multi ? M.err : P.p.err; }
-  void launch_mt(int k_steps, bool gen, bool reset) { CK(sg::launch_multi(M, k_steps, gen, reset, stream)); }
+  int32_t* err_word() const { return multi ? M.err : (image ? I.err : P.p.err); }
+  void launch_mt(int k_steps, bool gen, bool reset) {
+    if (image) CK(sg::launch_image(I, k_steps, gen, reset, stream));
+    else CK(sg::launch_multi(M, k_steps, gen, reset, stream));
+  }
 
   int chain = sg::kChainGeneric8;
   int team_warps = 1;
@@ -317,6 +332,19 @@ struct sg_env {
 
   void views(sg_step_views* out) const {
     if (!out) return;
+    if (image) {
+      out->observations = I.obs;
+      out->terminal_observations = I.tobs;
+      out->rewards = I.rewards;
+      out->task_error = I.task_error;
+      out->terminated = I.terminated;
+      out->timed_out = I.timed_out;
+      out->action_saturations_total = I.sat_total;
+      out->n_envs = n;
+      out->obs_dim = O;
+      out->action_dim = A;
+      return;
+    }
     if (multi) {
       out->observations = M.obs;
       out->terminal_observations = M.tobs;
@@ -647,6 +675,108 @@ std::unique_ptr<sg_env> make_multi_env(const sg_env_config& cfg, const sg_dynami
   return env;
 }
 
+// VecTaskEnv construction for ImageMatching (envs.cpp:118-223 with
+// RenderConfig::validate, render.cpp:24-32): single robot, identity tool
+// base, per-env scene / target image / target camera, observation
+// [q | qdot | tip | q_target | target image | current image].
+std::unique_ptr<sg_env> make_image_env(const sg_env_config& cfg, const sg_dynamics_config* dyn,
+                                       std::vector<sg::RobotModel> models, int device) {
+  if (cfg.render_width < 8 || cfg.render_height < 8) throw sg::ConfigError("render: width and height must be >= 8");
+  if (!(cfg.render_near > 0.0) || !(cfg.render_near < cfg.render_far))
+    throw sg::ConfigError("render: require 0 < near < far");
+  if (!(cfg.render_fov > 0.0) || !(cfg.render_fov < 3.1)) throw sg::ConfigError("render: fov must be in (0, pi)");
+  auto env = std::make_unique<sg_env>();
+  env->image = true;
+  env->cfg = cfg;
+  env->device = device;
+  CK(cudaSetDevice(device));
+  env->model = std::move(models[0]);
+  const sg::RobotModel& m = env->model;
+  const ResolvedDyn rd = resolve_dynamics(dyn, m);
+  auto& I = env->I;
+  I.robot = build_table(m, rd.dt_sub, rd.kp, rd.kd, rd.inertia, rd.damping);
+  const Mat3 cr = trailing_tip_rotation(m);
+  for (int k = 0; k < 9; ++k) I.cam_R[k] = static_cast<float>(cr[k]);
+  env->n = cfg.n_envs;
+  env->A = m.dof_count;
+  I.A = m.dof_count;
+  I.W = cfg.render_width;
+  I.H = cfg.render_height;
+  I.wh = I.W * I.H;
+  I.O = 3 * I.A + 3 + 2 * I.wh;  // envs.cpp:185-188
+  env->O = I.O;
+  I.episode_len = cfg.episode_len;
+  I.substeps = rd.dc.substeps;
+  I.control_mode = rd.dc.control_mode;
+  I.n = env->n;
+  const double f = 0.5 * cfg.render_width / std::tan(0.5 * cfg.render_fov);  // render.cpp:39
+  I.f = static_cast<float>(f);
+  I.inv_f = static_cast<float>(1.0 / f);
+  I.near_ = static_cast<float>(cfg.render_near);
+  I.far_ = static_cast<float>(cfg.render_far);
+  I.dt_sub = static_cast<float>(rd.dt_sub);
+  I.sigma = cfg.goal_sigma;
+  env->radius = cfg.workspace_radius > 0.0 ? cfg.workspace_radius : 3.0 * cfg.goal_sigma;  // envs.cpp:134
+  I.radius = env->radius;
+  const sg::Vec3 c = sg::forward_kinematics_position(m, m.mid_configuration());  // envs.cpp:159-161
+  for (int k = 0; k < 3; ++k) env->center[k] = I.center[k] = c[k];
+  int off = 0;
+  auto add = [&](const char* name, int len) {
+    env->layout.push_back({name, {off, len}});
+    off += len;
+  };
+  add("dof_pos", I.A);
+  add("dof_vel", I.A);
+  add("tip_pos", 3);
+  add("dof_target", I.A);
+  add("target_image", I.wh);
+  add("current_image", I.wh);
+  const int64_t n = env->n;
+  const int A = I.A;
+  I.q = dalloc<float>(n * A);
+  I.qd = dalloc<float>(n * A);
+  I.qt = dalloc<float>(n * A);
+  I.tips = dalloc<float>(n * 3);
+  I.step_count = dalloc<int32_t>(n);
+  I.hold_count = dalloc<int32_t>(n);
+  I.episode_count = dalloc<int64_t>(n);
+  I.rng_state = dalloc<uint64_t>(n);
+  I.rng_inc = dalloc<uint64_t>(n);
+  I.scenes = dalloc<float>(n * 16);
+  I.target = dalloc<float>(static_cast<size_t>(n) * I.wh);
+  I.tcam = dalloc<float>(n * 12);
+  I.obs = dalloc<float>(static_cast<size_t>(n) * I.O);
+  I.tobs = dalloc<float>(static_cast<size_t>(n) * I.O);
+  I.rewards = dalloc<float>(n);
+  I.task_error = dalloc<float>(n);
+  I.terminated = dalloc<uint8_t>(n);
+  I.timed_out = dalloc<uint8_t>(n);
+  env->counters = dalloc<unsigned long long>(8);
+  I.sat_total = env->counters;
+  I.ended_total = env->counters + 1;
+  I.err = reinterpret_cast<int32_t*>(env->counters + 2);
+  CK(cudaHostAlloc(&env->h_counters, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
+  {  // SimBatch::create (dynamics.cpp:225-241), stream id = global row
+    const auto mid = m.mid_configuration();
+    std::vector<float> qh(static_cast<size_t>(n) * A);
+    for (int d = 0; d < A; ++d)
+      for (int64_t i = 0; i < n; ++i) qh[d * n + i] = static_cast<float>(mid[d]);
+    CK(cudaMemcpy(I.q, qh.data(), qh.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(I.qt, qh.data(), qh.size() * sizeof(float), cudaMemcpyHostToDevice));
+    std::vector<uint64_t> st(n), inc(n);
+    for (int64_t i = 0; i < n; ++i) {
+      const HostPcg r = make_stream(cfg.seed, static_cast<uint64_t>(cfg.row_offset + i));
+      st[i] = r.state;
+      inc[i] = r.inc;
+    }
+    CK(cudaMemcpy(I.rng_state, st.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(I.rng_inc, inc.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
+  env->d_actions_in = dalloc<float>(n * A);
+  CK(cudaDeviceSynchronize());
+  return env;
+}
+
 std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_config* dyn,
                                  std::vector<sg::RobotModel> models, int device) {
   validate_env_config(cfg);
@@ -657,6 +787,10 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
     throw sg::ConfigError(std::string(task_name(cfg.task)) + " requires exactly 1 robot");
   }
   if (cfg.task == SG_TASK_MULTI_TOOL_REACHING) return make_multi_env(cfg, dyn, std::move(models), device);
+  if (cfg.task == SG_TASK_IMAGE_MATCHING) {
+    if (cfg.n_tool_bases != 0) throw sg::ConfigError("env.tool_bases: only supported for multi_tool_reaching");
+    return make_image_env(cfg, dyn, std::move(models), device);
+  }
   if (cfg.n_tool_bases != 0 && cfg.n_tool_bases != 1)
     throw sg::ConfigError("env.tool_bases must have one entry per robot");
   if (cfg.n_tool_bases == 1) {  // the single-tool kernels work in the robot base frame
@@ -666,9 +800,7 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   }
   if (cfg.task != SG_TASK_TARGET_REACHING && cfg.task != SG_TASK_PATH_FOLLOWING &&
       cfg.task != SG_TASK_ACTIVE_TRACKING)
-    throw sg::ConfigError(std::string("task '") + task_name(cfg.task) +
-                          "' is not on the sg_env device path (target_reaching, active_tracking, "
-                          "path_following, multi_tool_reaching)");
+    throw sg::ConfigError(std::string("task '") + task_name(cfg.task) + "' is not on the sg_env device path");
 
   auto env = std::make_unique<sg_env>();
   env->model = std::move(models[0]);
@@ -830,6 +962,11 @@ void sg_env_config_init(sg_env_config* c) {  // envs.hpp:42-63
   c->view_penalty = 0.1;
   c->seed = 0;
   c->row_offset = 0;
+  c->render_width = 32;  // render.hpp:31-36
+  c->render_height = 32;
+  c->render_fov = 1.0471975511965976;
+  c->render_near = 0.005;
+  c->render_far = 2.0;
 }
 
 void sg_dynamics_config_init(sg_dynamics_config* d) {  // dynamics.hpp:34-44
@@ -908,10 +1045,22 @@ int sg_env_tools(const sg_env* env, int32_t* n_tools, double* centers, double* b
   });
 }
 
+int sg_env_images(const sg_env* env, float** d_target, float** d_scenes, float** d_target_cameras, int32_t* width,
+                  int32_t* height) {
+  return guard([&] {
+    if (!env->image) throw sg::ConfigError("sg_env_images: not an image_matching env");
+    if (d_target) *d_target = env->I.target;
+    if (d_scenes) *d_scenes = env->I.scenes;
+    if (d_target_cameras) *d_target_cameras = env->I.tcam;
+    if (width) *width = env->I.W;
+    if (height) *height = env->I.H;
+  });
+}
+
 int sg_env_reset(sg_env* env, sg_step_views* out) {
   return guard([&] {
     CK(cudaSetDevice(env->device));
-    if (env->multi) env->launch_mt(0, false, true);
+    if (env->own_kernel()) env->launch_mt(0, false, true);
     else env->launch_reset();
     env->views(out);
   });
@@ -921,8 +1070,9 @@ int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
   return guard([&] {
     if (!d_actions) throw sg::SimError("env.step: action shape mismatch");
     CK(cudaSetDevice(env->device));
-    if (env->multi) {
+    if (env->own_kernel()) {
       env->M.actions = d_actions;
+      env->I.actions = d_actions;
       env->launch_mt(1, false, false);
       env->views(out);
       return;
@@ -947,24 +1097,27 @@ static void* mapped_alias(const void* h) {
   return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 
-// MultiToolReaching host step: staged copies around one launch, counters read
-// back with the result (the zero-copy publication path is single-tool only).
-static void multi_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
+// Host step of the MultiToolReaching / ImageMatching kernels: staged copies
+// around one launch, counters read back with the result (the zero-copy
+// publication path is the single-tool env_step family's).
+static void task_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
   const int64_t n = env->n;
   const int O = env->O;
   auto& s = env->stream;
-  auto& M = env->M;
   CK(cudaMemcpyAsync(env->d_actions_in, h_actions, n * env->A * sizeof(float), cudaMemcpyHostToDevice, s));
-  M.actions = env->d_actions_in;
+  env->M.actions = env->d_actions_in;
+  env->I.actions = env->d_actions_in;
   env->launch_mt(1, false, false);
+  sg_step_views v;
+  env->views(&v);
   if (out) {
     if (out->observations)
-      CK(cudaMemcpyAsync(out->observations, M.obs, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
-    if (out->rewards) CK(cudaMemcpyAsync(out->rewards, M.rewards, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(out->observations, v.observations, n * O * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (out->rewards) CK(cudaMemcpyAsync(out->rewards, v.rewards, n * sizeof(float), cudaMemcpyDeviceToHost, s));
     if (out->task_error)
-      CK(cudaMemcpyAsync(out->task_error, M.task_error, n * sizeof(float), cudaMemcpyDeviceToHost, s));
-    if (out->terminated) CK(cudaMemcpyAsync(out->terminated, M.terminated, n, cudaMemcpyDeviceToHost, s));
-    if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, M.timed_out, n, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(out->task_error, v.task_error, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (out->terminated) CK(cudaMemcpyAsync(out->terminated, v.terminated, n, cudaMemcpyDeviceToHost, s));
+    if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, v.timed_out, n, cudaMemcpyDeviceToHost, s));
   }
   CK(cudaMemcpyAsync(env->h_counters, env->counters, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -973,7 +1126,8 @@ static void multi_step_host(sg_env* env, const float* h_actions, sg_host_result*
   const unsigned long long ended = ended_total - env->mt_ended_seen;
   env->mt_ended_seen = ended_total;
   if (out && out->terminal_observations && ended != 0)
-    CK(cudaMemcpy(out->terminal_observations, M.tobs, n * O * sizeof(float), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out->terminal_observations, v.terminal_observations, n * O * sizeof(float),
+                  cudaMemcpyDeviceToHost));
   env->last_ended += ended;
   if (out) out->action_saturations = static_cast<int64_t>(sat - env->last_sat);
   env->last_sat = sat;
@@ -983,7 +1137,7 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
   return guard([&] {
     if (!h_actions) throw sg::SimError("env.step: action shape mismatch");
     CK(cudaSetDevice(env->device));
-    if (env->multi) return multi_step_host(env, h_actions, out);
+    if (env->own_kernel()) return task_step_host(env, h_actions, out);
     const int64_t n = env->n;
     const int O = env->O;
     auto& s = env->stream;
@@ -1067,7 +1221,7 @@ int sg_env_host_counters(const sg_env* env, uint64_t* ended_rows_total, uint64_t
 }
 
 int sg_env_task_error(const sg_env* env, float** d) {
-  return guard([&] { *d = env->multi ? env->M.task_error : env->P.p.task_error; });
+  return guard([&] { *d = env->multi ? env->M.task_error : (env->image ? env->I.task_error : env->P.p.task_error); });
 }
 
 int sg_env_state(const sg_env* env, sg_state_views* o) {
@@ -1091,6 +1245,21 @@ int sg_env_state(const sg_env* env, sg_state_views* o) {
       return;
     }
     o->n_tools = 1;
+    if (env->image) {
+      const auto& I = env->I;
+      o->q = I.q;
+      o->qdot = I.qd;
+      o->q_target = I.qt;
+      o->tips = I.tips;
+      o->step_count = I.step_count;
+      o->hold_count = I.hold_count;
+      o->episode_count = I.episode_count;
+      o->rng_state = I.rng_state;
+      o->rng_inc = I.rng_inc;
+      o->dof = env->A;
+      o->n_envs = env->n;
+      return;
+    }
     const auto& p = env->P.p;
     o->q = p.q;
     o->qdot = p.qd;
@@ -1122,6 +1291,27 @@ int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t g
   return guard([&] {
     CK(cudaSetDevice(env->device));
     if (global_n < env->n + env->cfg.row_offset) throw sg::ConfigError("bench: global_n_envs smaller than this shard");
+    if (env->image) {  // one stream state per env at its row start; lane d reads draw d of the row
+      auto& I = env->I;
+      if (!I.act_state) {
+        I.act_state = dalloc<uint64_t>(env->n);
+        I.act_buf = dalloc<float>(env->n * env->A);
+      }
+      const HostPcg r = make_stream(seed, 0xac7104);  // bench.cpp:115
+      sg::JumpTable J;
+      for (int b = 0; b < 64; ++b) pcg_jump(1ULL << b, r.inc, J.mult[b], J.add[b]);
+      const uint64_t A = static_cast<uint64_t>(env->A);
+      I.act_inc = r.inc;
+      pcg_jump(static_cast<uint64_t>(global_n) * A, r.inc, I.jump_mult, I.jump_add);
+      for (int d = 0; d < sg::kMaxDof; ++d) pcg_jump(d, r.inc, I.pow_mult[d], I.pow_add[d]);
+      const unsigned grid = static_cast<unsigned>((env->n + 127) / 128);
+      sg::bench_seed_kernel<<<grid, 128, 0, env->stream>>>(I.act_state, env->n, r.state,
+                                                           static_cast<uint64_t>(first_step) * global_n * A,
+                                                           env->cfg.row_offset, env->A, J);
+      CK(cudaGetLastError());
+      env->bench_ready = true;
+      return;
+    }
     if (env->multi) {  // one stream state per env at its row start; A consecutive draws per row
       auto& M = env->M;
       if (!M.act_state) {
@@ -1179,14 +1369,14 @@ int sg_env_bench_step(sg_env* env, int32_t k_steps) {
     if (!env->bench_ready) throw sg::ConfigError("sg_env_bench_step before sg_env_bench_begin");
     if (k_steps < 1) throw sg::ConfigError("bench: k_steps must be >= 1");
     CK(cudaSetDevice(env->device));
-    if (env->multi) env->launch_mt(k_steps, true, false);
+    if (env->own_kernel()) env->launch_mt(k_steps, true, false);
     else env->launch_step(k_steps, true);
   });
 }
 
 int sg_env_bench_actions(const sg_env* env, float** d_actions) {
   return guard([&] {
-    float* buf = env->multi ? env->M.act_buf : env->P.p.act_buf;
+    float* buf = env->multi ? env->M.act_buf : (env->image ? env->I.act_buf : env->P.p.act_buf);
     if (!buf) throw sg::ConfigError("sg_env_bench_actions before sg_env_bench_begin");
     *d_actions = buf;
   });

@@ -1,0 +1,364 @@
+// ImageMatching step / reset kernels (image.cuh): one warp per env.
+#include "image.cuh"
+
+namespace sg {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// fk_walk (robot_model.cpp:371-395) keeping the rotation: tip position and
+// the camera rotation (last DoF frame x trailing rotation, Pose orientation
+// as a matrix; the tool base of a single-robot env is the identity).
+template <int DMAX>
+__device__ __forceinline__ void camera_pose(const ImParams& P, const float (&q)[DMAX], float (&Rc)[9], float (&pc)[3]) {
+  const RobotTable& R = P.robot;
+  float m[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+  float p[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) {
+    if (d >= R.dof) break;
+    const JointEnc& J = R.j[d];
+    fk_joint(J, J.kind, J.axis_code, J.flags & 7, (J.flags >> 3) & 1, q[d], m, p);
+  }
+  fk_tip_offset(R, R.tip_flags, m, p, pc);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      Rc[r * 3 + c] = m[r * 3 + 0] * P.cam_R[0 * 3 + c] + m[r * 3 + 1] * P.cam_R[1 * 3 + c] +
+                      m[r * 3 + 2] * P.cam_R[2 * 3 + c];
+}
+
+// Per-frame sphere constants: oc = camera - centre, c2 = |oc|^2 - r^2.
+struct Frame {
+  float R[9];
+  float oc[3][3], c2[3], inv_r[3], alb[3];
+};
+
+__device__ __forceinline__ void make_frame(const float (&Rc)[9], const float (&pc)[3], const float (&sc)[15],
+                                           Frame& F) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) F.R[k] = Rc[k];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const float o0 = pc[0] - sc[5 * s + 0], o1 = pc[1] - sc[5 * s + 1], o2 = pc[2] - sc[5 * s + 2];
+    const float r = sc[5 * s + 3];
+    F.oc[s][0] = o0;
+    F.oc[s][1] = o1;
+    F.oc[s][2] = o2;
+    F.c2[s] = (o0 * o0 + o1 * o1 + o2 * o2) - r * r;
+    F.inv_r[s] = 1.f / r;
+    F.alb[s] = sc[5 * s + 4];
+  }
+}
+
+// One pixel of render.cpp:42-64. With the ray direction d normalised, the
+// Lambert term n . (-d) = -(oc . d + t) / r = sqrt(disc) / r (t = -b - sqrt(disc)),
+// so the nearest hit's shade needs no hit-point reconstruction.
+__device__ __forceinline__ float shade(const ImParams& P, const Frame& F, int px, int py) {
+  const float u = ((float)px + 0.5f - 0.5f * (float)P.W) * P.inv_f;
+  const float v = ((float)py + 0.5f - 0.5f * (float)P.H) * P.inv_f;
+  float d0 = fmaf(F.R[0], u, fmaf(-F.R[1], v, -F.R[2]));  // R * (u, -v, -1): top row looks up
+  float d1 = fmaf(F.R[3], u, fmaf(-F.R[4], v, -F.R[5]));
+  float d2 = fmaf(F.R[6], u, fmaf(-F.R[7], v, -F.R[8]));
+  const float inv = rsqrtf(d0 * d0 + d1 * d1 + d2 * d2);
+  d0 *= inv;
+  d1 *= inv;
+  d2 *= inv;
+  float best = P.far_, value = 0.f;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const float b = F.oc[s][0] * d0 + F.oc[s][1] * d1 + F.oc[s][2] * d2;
+    const float disc = b * b - F.c2[s];
+    if (disc < 0.f) continue;
+    const float sq = sqrtf(disc);
+    const float t = -b - sq;
+    if (t < P.near_ || t >= best) continue;
+    best = t;
+    const float lambert = sq * F.inv_r[s];
+    value = lambert > 0.f ? F.alb[s] * lambert : 0.f;
+  }
+  return value;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+template <int DMAX>
+__device__ __forceinline__ void gather_q(float mine, float (&qa)[DMAX]) {
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) qa[d] = __shfl_sync(kFull, mine, d);
+}
+
+// reset_row for ImageMatching (envs.cpp:304-316, 269-295), warp-cooperative:
+// every lane replays the env stream (q in the middle half, three spheres
+// drawn z, y, x, radius, albedo -- g++ argument order --, target q in the
+// middle quarter); the warp writes the new joint state, scene, target view
+// and the post-reset observation row to HBM (the caller reloads its
+// registers from there: no reference arguments, so the hot loop's state
+// never lives on the stack).
+template <int DMAX>
+__device__ __noinline__ void im_reset_env(const ImParams& P, int64_t i, int lane) {
+  float q, sc[15];
+  const RobotTable& R = P.robot;
+  const int64_t n = P.n;
+  const int A = R.dof;
+  uint64_t s = P.rng_state[i];
+  const uint64_t inc = P.rng_inc[i];
+  float q0[DMAX], qT[DMAX];
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) {
+    q0[d] = 0.f;
+    if (d < A) {
+      const double quarter = __dmul_rn(0.25, __dadd_rn(R.hi_d[d], -R.lo_d[d]));
+      q0[d] = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
+    }
+  }
+  const double s2 = __dmul_rn(2.0, P.sigma);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double z = -__dadd_rn(P.radius, pcg_uniform(s, inc, 0.1, 0.25));
+    const double y = pcg_uniform(s, inc, -s2, s2);
+    const double x = pcg_uniform(s, inc, -s2, s2);
+    sc[5 * k + 0] = (float)__dadd_rn(P.center[0], x);
+    sc[5 * k + 1] = (float)__dadd_rn(P.center[1], y);
+    sc[5 * k + 2] = (float)__dadd_rn(P.center[2], z);
+    sc[5 * k + 3] = (float)pcg_uniform(s, inc, 0.02, 0.05);
+    sc[5 * k + 4] = (float)pcg_uniform(s, inc, 0.5, 1.0);
+  }
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) {  // sample_q_fraction(rng, model, 0.25) (envs.cpp:31-39)
+    qT[d] = 0.f;
+    if (d < A) {
+      const double margin = __dmul_rn(__dmul_rn(0.5, 0.75), __dadd_rn(R.hi_d[d], -R.lo_d[d]));
+      qT[d] = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], margin), __dadd_rn(R.hi_d[d], -margin));
+    }
+  }
+  q = 0.f;
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d)
+    if (d == lane) q = q0[d];
+  float RT[9], pT[3], R0[9], p0[3];
+  camera_pose<DMAX>(P, qT, RT, pT);
+  camera_pose<DMAX>(P, q0, R0, p0);
+  if (lane == 0) P.rng_state[i] = s;
+  if (lane < 15) {
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < 15; ++k)
+      if (k == lane) v = sc[k];
+    P.scenes[i * 16 + lane] = v;
+  }
+  if (lane < 12) {
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (k == lane) v = RT[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (k + 9 == lane) v = pT[k];
+    P.tcam[i * 12 + lane] = v;
+  }
+  if (lane < A) {
+    P.q[lane * n + i] = q;
+    P.qd[lane * n + i] = 0.f;
+    P.qt[lane * n + i] = q;
+  }
+  if (lane < 3) P.tips[lane * n + i] = lane == 0 ? p0[0] : (lane == 1 ? p0[1] : p0[2]);
+  if (lane == 0) {
+    P.step_count[i] = 0;
+    P.hold_count[i] = 0;
+    P.episode_count[i] += 1;
+  }
+  // observation row: [q | qdot | tip | q_target | target image | current image]
+  float* row = P.obs + i * P.O;
+  if (lane < A) {
+    row[lane] = q;
+    row[A + lane] = 0.f;
+    row[2 * A + 3 + lane] = q;
+  }
+  if (lane < 3) row[2 * A + lane] = lane == 0 ? p0[0] : (lane == 1 ? p0[1] : p0[2]);
+  Frame FT, F0;
+  make_frame(RT, pT, sc, FT);
+  make_frame(R0, p0, sc, F0);
+  const int head = 3 * A + 3, W = P.W, wh = P.wh;
+  float* tgt = P.target + i * wh;
+  for (int p = lane; p < wh; p += 32) {
+    const int py = p / W, px = p - py * W;
+    const float vt = shade(P, FT, px, py);
+    tgt[p] = vt;
+    row[head + p] = vt;
+    row[head + wh + p] = shade(P, F0, px, py);
+  }
+}
+
+template <int DMAX, bool GEN>
+__global__ void __launch_bounds__(32 * kImWarps) im_step_kernel(const __grid_constant__ ImParams P, int k_steps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kImWarps + (threadIdx.x >> 5);
+  const int64_t n = P.n;
+  if (i >= n) return;  // whole warp
+  const RobotTable& R = P.robot;
+  const int A = R.dof, O = P.O, W = P.W, wh = P.wh;
+  const int head = 3 * A + 3;
+  const bool own = lane < A;
+  const int dl = own ? lane : 0;
+  // lane d's DoF constants in registers (per-lane indices would serialise
+  // the constant cache inside the step loop)
+  const float lo = R.lo[dl], hi = R.hi[dl], vl = R.vel[dl], ef = R.eff[dl], kp = R.kp[dl], kd = R.kd[dl],
+              dmp = R.damping[dl], dti = R.dt_over_inertia[dl];
+  const bool is_jaw = lane == R.jaw;
+  const uint64_t pm = P.pow_mult[dl], pa = P.pow_add[dl];
+  float q = own ? P.q[lane * n + i] : 0.f;
+  float qd = own ? P.qd[lane * n + i] : 0.f;
+  float qt = own ? P.qt[lane * n + i] : 0.f;
+  float sc[15];
+#pragma unroll
+  for (int k = 0; k < 15; ++k) sc[k] = P.scenes[i * 16 + k];
+  uint64_t act_s = GEN ? P.act_state[i] : 0;
+  int32_t step_count = P.step_count[i];
+  const int mode = P.control_mode;
+  const float dt = P.dt_sub;
+
+  for (int step = 0; step < k_steps; ++step) {
+    // ---- dynamics of DoF `lane` (dynamics.cpp:127-185) ----------------------
+    float ad = 0.f;
+    int sat = 0, bad = 0;
+    if (GEN) {
+      const uint32_t u = pcg_output(act_s * pm + pa);
+      ad = __int2float_rn((int32_t)(u ^ 0x80000000u)) * 0x1.0p-31f;
+      if (own) P.act_buf[i * A + lane] = ad;
+      act_s = act_s * P.jump_mult + P.jump_add;
+    } else if (own) {
+      ad = P.actions[i * A + lane];
+      if (!isfinite(ad)) {
+        bad = 1;
+        ad = 0.f;
+      }
+      if (ad < -1.f || ad > 1.f) {
+        ad = ad < -1.f ? -1.f : 1.f;
+        sat = 1;
+      }
+    }
+    float vt = 0.f, tc = 0.f, kpqt = 0.f;
+    if (mode == kModePosition) {
+      qt = is_jaw ? (ad > 0.f ? hi : lo) : rescale(ad, lo, hi);
+      kpqt = kp * qt;
+    } else if (mode == kModeVelocity) {
+      vt = rescale(ad, -vl, vl);
+    } else {
+      tc = rescale(ad, -ef, ef);
+    }
+    for (int s = 0; s < P.substeps; ++s) {
+      float tau;
+      if (mode == kModePosition) tau = fmaf(-kd, qd, fmaf(-kp, q, kpqt));
+      else if (mode == kModeVelocity) tau = kd * (vt - qd);
+      else tau = tc;
+      tau = fminf(fmaxf(tau, -ef), ef);
+      float vv = qd + (tau - dmp * qd) * dti;
+      vv = fminf(fmaxf(vv, -vl), vl);
+      const float qq = q + vv * dt;
+      const float qc = fminf(fmaxf(qq, lo), hi);  // limit projection
+      qd = qc != qq ? 0.f : vv;
+      q = qc;
+    }
+    if (!own) q = qd = qt = 0.f;
+    if (!GEN) {
+      const unsigned ns = __popc(__ballot_sync(kFull, sat));
+      if (ns && lane == 0) atomicAdd(P.sat_total, (unsigned long long)ns);
+      if (__any_sync(kFull, bad) && lane == 0) atomicOr(P.err, kErrNonFiniteAction);
+    }
+    // ---- camera FK (refresh_tips, envs.cpp:456-463) --------------------------
+    float qa[DMAX];
+    gather_q<DMAX>(q, qa);
+    float Rc[9], pc[3];
+    camera_pose<DMAX>(P, qa, Rc, pc);
+    if (lane < 3) P.tips[lane * n + i] = lane == 0 ? pc[0] : (lane == 1 ? pc[1] : pc[2]);
+    step_count += 1;
+    const bool ends = step_count >= P.episode_len;  // goal_met is never set for ImageMatching
+    float* row = (ends ? P.tobs : P.obs) + i * O;
+    if (own) {
+      row[lane] = q;
+      row[A + lane] = qd;
+      row[2 * A + 3 + lane] = qt;
+    }
+    if (lane < 3) row[2 * A + lane] = lane == 0 ? pc[0] : (lane == 1 ? pc[1] : pc[2]);
+    // ---- render (envs.cpp:464-473), L1 image error (envs.cpp:513-523) -------
+    Frame F;
+    make_frame(Rc, pc, sc, F);
+    const float* tgt = P.target + i * wh;
+    float acc = 0.f;
+    for (int p = lane; p < wh; p += 32) {
+      const int py = p / W, px = p - py * W;
+      const float v = shade(P, F, px, py);
+      const float t = tgt[p];
+      acc += fabsf(v - t);
+      row[head + p] = t;
+      row[head + wh + p] = v;
+    }
+    const float err = warp_sum(acc) / (float)wh;
+    if (lane == 0) {
+      const float reward = -err;
+      if (!isfinite(reward)) atomicOr(P.err, kErrNonFiniteReward);
+      P.rewards[i] = reward;
+      P.task_error[i] = err;
+      P.terminated[i] = 0;
+      P.timed_out[i] = ends ? 1 : 0;
+    }
+    if (ends) {  // terminal row written above; reset_row + re-observe
+      if (lane == 0) atomicAdd(P.ended_total, 1ull);
+      __syncwarp();
+      im_reset_env<DMAX>(P, i, lane);
+      __syncwarp();
+      q = own ? P.q[lane * n + i] : 0.f;
+      qd = 0.f;
+      qt = q;
+#pragma unroll
+      for (int k = 0; k < 15; ++k) sc[k] = P.scenes[i * 16 + k];
+      step_count = 0;
+    }
+  }
+  if (own) {
+    P.q[lane * n + i] = q;
+    P.qd[lane * n + i] = qd;
+    P.qt[lane * n + i] = qt;
+  }
+  if (lane == 0) {
+    P.step_count[i] = step_count;
+    if (GEN) P.act_state[i] = act_s;
+  }
+}
+
+template <int DMAX>
+__global__ void __launch_bounds__(32 * kImWarps) im_reset_kernel(const __grid_constant__ ImParams P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kImWarps + (threadIdx.x >> 5);
+  if (i >= P.n) return;
+  im_reset_env<DMAX>(P, i, lane);  // VecTaskEnv::reset (envs.cpp:425-435)
+  if (lane == 0) {
+    P.episode_count[i] = 0;
+    P.terminated[i] = 0;
+    P.timed_out[i] = 0;
+    P.rewards[i] = 0.f;
+  }
+}
+
+template <int DMAX>
+cudaError_t launch_d(const ImParams& P, int k_steps, bool gen, bool reset, cudaStream_t st) {
+  const unsigned grid = (unsigned)((P.n + kImWarps - 1) / kImWarps);
+  if (reset) im_reset_kernel<DMAX><<<grid, 32 * kImWarps, 0, st>>>(P);
+  else if (gen) im_step_kernel<DMAX, true><<<grid, 32 * kImWarps, 0, st>>>(P, k_steps);
+  else im_step_kernel<DMAX, false><<<grid, 32 * kImWarps, 0, st>>>(P, k_steps);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_image(const ImParams& P, int k_steps, bool gen, bool reset, cudaStream_t st) {
+  return P.robot.dof <= 8 ? launch_d<8>(P, k_steps, gen, reset, st) : launch_d<16>(P, k_steps, gen, reset, st);
+}
+
+}  // namespace sg

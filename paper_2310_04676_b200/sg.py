@@ -45,6 +45,8 @@ class EnvConfig(C.Structure):  # sg_env_config
         ("collision_threshold", C.c_double), ("collision_penalty", C.c_double),
         ("view_penalty", C.c_double), ("seed", C.c_uint64), ("row_offset", C.c_int64),
         ("tool_bases", C.POINTER(C.c_double)), ("n_tool_bases", C.c_int32), ("reserved1", C.c_int32),
+        ("render_width", C.c_int32), ("render_height", C.c_int32), ("render_fov", C.c_double),
+        ("render_near", C.c_double), ("render_far", C.c_double),
     ]
 
 
@@ -101,6 +103,8 @@ _SIGS = {
     "sg_env_layout_count": (C.c_int32, [C.c_void_p]),
     "sg_env_layout_field": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_char_p), _P(C.c_int32), _P(C.c_int32)]),
     "sg_env_workspace": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double)]),
+    "sg_env_images": (C.c_int, [C.c_void_p, _P(C.c_void_p), _P(C.c_void_p), _P(C.c_void_p), _P(C.c_int32),
+                                _P(C.c_int32)]),
     "sg_env_tools": (C.c_int, [C.c_void_p, _P(C.c_int32), _P(C.c_double), _P(C.c_double), _P(C.c_int32)]),
     "sg_env_reset": (C.c_int, [C.c_void_p, _P(StepViews)]),
     "sg_env_step": (C.c_int, [C.c_void_p, C.c_void_p, _P(StepViews)]),
@@ -341,6 +345,17 @@ class VecTaskEnv:
         c, b, d = (C.c_double * (3 * T.value))(), (C.c_double * (7 * T.value))(), (C.c_int32 * T.value)()
         _check(lib().sg_env_tools(self._h, C.byref(T), c, b, d))
         return np.array(list(c)).reshape(-1, 3), np.array(list(b)).reshape(-1, 7), list(d)
+
+    def images(self) -> dict:
+        """ImageMatching task state: target images (n, h*w), scenes (n, 16),
+        target cameras (n, 12) as device views."""
+        t, sc, cam = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        w, h = C.c_int32(), C.c_int32()
+        _check(lib().sg_env_images(self._h, C.byref(t), C.byref(sc), C.byref(cam), C.byref(w), C.byref(h)))
+        n, d = self.n_envs, self.device
+        return dict(target=device_view(t.value, (n, w.value * h.value), "f32", d),
+                    scenes=device_view(sc.value, (n, 16), "f32", d),
+                    target_cameras=device_view(cam.value, (n, 12), "f32", d), width=w.value, height=h.value)
 
     def _result(self) -> StepResult:
         v, n, o, d = self._views, self.n_envs, self.obs_dim, self.device
