@@ -6,6 +6,10 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+#ifndef SG_IM_MINB
+#define SG_IM_MINB 2  // CTAs per SM the step kernel is register-budgeted for (A/B: tools/ab.sh)
+#endif
+
 // fk_walk (robot_model.cpp:371-395) keeping the rotation: tip position and
 // the camera rotation (last DoF frame x trailing rotation, Pose orientation
 // as a matrix; the tool base of a single-robot env is the identity).
@@ -52,31 +56,52 @@ __device__ __forceinline__ void make_frame(const float (&Rc)[9], const float (&p
   }
 }
 
-// One pixel of render.cpp:42-64. With the ray direction d normalised, the
-// Lambert term n . (-d) = -(oc . d + t) / r = sqrt(disc) / r (t = -b - sqrt(disc)),
-// so the nearest hit's shade needs no hit-point reconstruction.
-__device__ __forceinline__ float shade(const ImParams& P, const Frame& F, int px, int py) {
-  const float u = ((float)px + 0.5f - 0.5f * (float)P.W) * P.inv_f;
-  const float v = ((float)py + 0.5f - 0.5f * (float)P.H) * P.inv_f;
-  float d0 = fmaf(F.R[0], u, fmaf(-F.R[1], v, -F.R[2]));  // R * (u, -v, -1): top row looks up
-  float d1 = fmaf(F.R[3], u, fmaf(-F.R[4], v, -F.R[5]));
-  float d2 = fmaf(F.R[6], u, fmaf(-F.R[7], v, -F.R[8]));
-  const float inv = rsqrtf(d0 * d0 + d1 * d1 + d2 * d2);
+// MUFU approximations without the IEEE / denormal fix-up sequences rsqrtf and
+// sqrtf expand to (ncu: those fix-ups were 20 % of the kernel's instructions);
+// ~2 ulp, far inside the fp32-vs-fp64 pixel tolerance.
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// One pixel of render.cpp:42-64 for the ray through camera coordinates
+// (u, -v, -1). With the direction d normalised, the Lambert term
+// n . (-d) = -(oc . d + t) / r = sqrt(disc) / r (t = -b - sqrt(disc)), so the
+// nearest hit's shade needs no hit-point reconstruction; the three sphere
+// tests are branch-free (selects) so the warp never diverges per pixel.
+// Column part of the camera ray: a = R * (u, 0, -1).
+struct Column {
+  float a0, a1, a2;
+};
+__device__ __forceinline__ Column column(const Frame& F, float u) {
+  return {fmaf(F.R[0], u, -F.R[2]), fmaf(F.R[3], u, -F.R[5]), fmaf(F.R[6], u, -F.R[8])};
+}
+
+__device__ __forceinline__ float shade(const ImParams& P, const Frame& F, const Column& C, float v) {
+  // R * (u, -v, -1) = a - v * R[:, 1]: top row looks up
+  float d0 = fmaf(-F.R[1], v, C.a0);
+  float d1 = fmaf(-F.R[4], v, C.a1);
+  float d2 = fmaf(-F.R[7], v, C.a2);
+  const float inv = rsqrt_approx(fmaf(d0, d0, fmaf(d1, d1, d2 * d2)));
   d0 *= inv;
   d1 *= inv;
   d2 *= inv;
   float best = P.far_, value = 0.f;
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    const float b = F.oc[s][0] * d0 + F.oc[s][1] * d1 + F.oc[s][2] * d2;
-    const float disc = b * b - F.c2[s];
-    if (disc < 0.f) continue;
-    const float sq = sqrtf(disc);
+    const float b = fmaf(F.oc[s][0], d0, fmaf(F.oc[s][1], d1, F.oc[s][2] * d2));
+    const float disc = fmaf(b, b, -F.c2[s]);
+    const float sq = sqrt_approx(fmaxf(disc, 0.f));
     const float t = -b - sq;
-    if (t < P.near_ || t >= best) continue;
-    best = t;
-    const float lambert = sq * F.inv_r[s];
-    value = lambert > 0.f ? F.alb[s] * lambert : 0.f;
+    const bool hit = disc >= 0.f && t >= P.near_ && t < best;
+    best = hit ? t : best;
+    value = hit ? F.alb[s] * (sq * F.inv_r[s]) : value;
   }
   return value;
 }
@@ -186,17 +211,21 @@ __device__ __noinline__ void im_reset_env(const ImParams& P, int64_t i, int lane
   make_frame(R0, p0, sc, F0);
   const int head = 3 * A + 3, W = P.W, wh = P.wh;
   float* tgt = P.target + i * wh;
-  for (int p = lane; p < wh; p += 32) {
-    const int py = p / W, px = p - py * W;
-    const float vt = shade(P, FT, px, py);
-    tgt[p] = vt;
-    row[head + p] = vt;
-    row[head + wh + p] = shade(P, F0, px, py);
+  for (int py = 0; py < P.H; ++py) {
+    const float v = ((float)py + 0.5f - 0.5f * (float)P.H) * P.inv_f;
+    for (int px = lane; px < W; px += 32) {
+      const float u = ((float)px + 0.5f - 0.5f * (float)W) * P.inv_f;
+      const int p = py * W + px;
+      const float vt = shade(P, FT, column(FT, u), v);
+      tgt[p] = vt;
+      row[head + p] = vt;
+      row[head + wh + p] = shade(P, F0, column(F0, u), v);
+    }
   }
 }
 
 template <int DMAX, bool GEN>
-__global__ void __launch_bounds__(32 * kImWarps) im_step_kernel(const __grid_constant__ ImParams P, int k_steps) {
+__global__ void __launch_bounds__(32 * kImWarps, SG_IM_MINB) im_step_kernel(const __grid_constant__ ImParams P, int k_steps) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kImWarps + (threadIdx.x >> 5);
   const int64_t n = P.n;
@@ -290,14 +319,21 @@ __global__ void __launch_bounds__(32 * kImWarps) im_step_kernel(const __grid_con
     Frame F;
     make_frame(Rc, pc, sc, F);
     const float* tgt = P.target + i * wh;
+    float* o_tgt = row + head;
+    float* o_cur = row + head + wh;
     float acc = 0.f;
-    for (int p = lane; p < wh; p += 32) {
-      const int py = p / W, px = p - py * W;
-      const float v = shade(P, F, px, py);
-      const float t = tgt[p];
-      acc += fabsf(v - t);
-      row[head + p] = t;
-      row[head + wh + p] = v;
+    for (int px = lane; px < W; px += 32) {  // lane-fixed columns, rows in the inner loop
+      const Column C = column(F, ((float)px + 0.5f - 0.5f * (float)W) * P.inv_f);
+#pragma unroll 4
+      for (int py = 0; py < P.H; ++py) {
+        const float v = ((float)py + 0.5f - 0.5f * (float)P.H) * P.inv_f;
+        const int p = py * W + px;
+        const float c = shade(P, F, C, v);
+        const float t = tgt[p];
+        acc += fabsf(c - t);
+        o_tgt[p] = t;
+        o_cur[p] = c;
+      }
     }
     const float err = warp_sum(acc) / (float)wh;
     if (lane == 0) {
