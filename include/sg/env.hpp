@@ -8,6 +8,7 @@
 // device-detected errors surface at the next synchronising call.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -32,8 +33,56 @@ inline void check(int rc) {
   throw SimError(sg_last_error());
 }
 
-struct EnvConfig : sg_env_config {  // envs.hpp:42-63 defaults
+// geometry.hpp Pose: position + unit quaternion (w, x, y, z).
+struct Pose {
+  double position[3] = {0.0, 0.0, 0.0};
+  double orientation[4] = {1.0, 0.0, 0.0, 0.0};
+};
+
+// quat_from_rpy (geometry.hpp:45-49): AngleAxis(yaw, Z) * AngleAxis(pitch, Y) *
+// AngleAxis(roll, X) -- the reference's JSON tool_bases / origin `rpy`.
+inline Pose pose_from_xyz_rpy(double x, double y, double z, double roll, double pitch, double yaw) {
+  const double cr = std::cos(0.5 * roll), sr = std::sin(0.5 * roll), cp = std::cos(0.5 * pitch),
+               sp = std::sin(0.5 * pitch), cy = std::cos(0.5 * yaw), sy = std::sin(0.5 * yaw);
+  // (qz * qy) * qx
+  const double w1 = cy * cp, x1 = -sy * sp, y1 = cy * sp, z1 = sy * cp;
+  Pose p;
+  p.position[0] = x;
+  p.position[1] = y;
+  p.position[2] = z;
+  p.orientation[0] = w1 * cr - x1 * sr;
+  p.orientation[1] = w1 * sr + x1 * cr;
+  p.orientation[2] = y1 * cr + z1 * sr;
+  p.orientation[3] = z1 * cr - y1 * sr;
+  return p;
+}
+
+// envs.hpp:42-63 defaults; tool_bases (envs.hpp:59) kept as Poses and handed
+// to the C-ABI as xyz + wxyz rows.
+struct EnvConfig : sg_env_config {
   EnvConfig() { sg_env_config_init(this); }
+  EnvConfig(const EnvConfig& o) : sg_env_config(o), bases_(o.bases_) { repoint(); }
+  EnvConfig& operator=(const EnvConfig& o) {
+    static_cast<sg_env_config&>(*this) = o;
+    bases_ = o.bases_;
+    repoint();
+    return *this;
+  }
+  void set_tool_bases(const std::vector<Pose>& bases) {
+    bases_.clear();
+    for (const auto& b : bases) {
+      bases_.insert(bases_.end(), b.position, b.position + 3);
+      bases_.insert(bases_.end(), b.orientation, b.orientation + 4);
+    }
+    repoint();
+  }
+
+ private:
+  void repoint() {
+    tool_bases = bases_.empty() ? nullptr : bases_.data();
+    n_tool_bases = static_cast<int32_t>(bases_.size() / 7);
+  }
+  std::vector<double> bases_;
 };
 struct DynamicsConfig : sg_dynamics_config {  // dynamics.hpp:34-44 defaults
   DynamicsConfig() { sg_dynamics_config_init(this); }
@@ -119,6 +168,23 @@ class VecTaskEnv : public BatchedEnv {
       out.push_back({name, off, len});
     }
     return out;
+  }
+  // MultiToolReaching geometry: VecTaskEnv::tool_base (envs.hpp:144) and the
+  // per-tool workspace centres (envs.cpp:159-161).
+  int n_tools() const {
+    int32_t t = 0;
+    check(sg_env_tools(env_, &t, nullptr, nullptr, nullptr));
+    return t;
+  }
+  Pose tool_base(int tool) const {
+    const int t = n_tools();
+    if (tool < 0 || tool >= t) throw ConfigError("tool index out of range");
+    std::vector<double> b(7 * static_cast<size_t>(t));
+    check(sg_env_tools(env_, nullptr, nullptr, b.data(), nullptr));
+    Pose p;
+    for (int k = 0; k < 3; ++k) p.position[k] = b[7 * tool + k];
+    for (int k = 0; k < 4; ++k) p.orientation[k] = b[7 * tool + 3 + k];
+    return p;
   }
   sg_env* handle() { return env_; }
 

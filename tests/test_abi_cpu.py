@@ -122,3 +122,37 @@ def test_every_header_symbol_has_a_ctypes_signature(sg):
     conversion (pointer truncation)."""
     missing = [s for s in sg.header_symbols() if s not in sg._SIGS]
     assert not missing, missing
+
+
+def test_cpp_multitool_example_and_pose_conversion(sg, oracle, tmp_path):
+    """examples/multitool_cpp.cpp (tool bases through scalpel_b200::EnvConfig)
+    compiles and links; pose_from_xyz_rpy reproduces quat_from_rpy
+    (geometry.hpp:45-49) as the oracle's default_tool_bases uses it."""
+    import os
+    import subprocess
+    import numpy as np
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(sg.lib_path())
+    inc = os.path.join(root, "include")
+    exe = str(tmp_path / "multitool_cpp")
+    r = subprocess.run(["g++", "-std=c++17", "-O2", "-I", inc, os.path.join(root, "examples", "multitool_cpp.cpp"),
+                        f"-L{libdir}", "-lsg_env", f"-Wl,-rpath,{libdir}", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    src = tmp_path / "pose.cpp"
+    src.write_text('#include <cstdio>\n#include "sg/env.hpp"\nint main(){ auto p = scalpel_b200::pose_from_xyz_rpy('
+                   '0, -0.3, 0.075, 0.9, 0, 0); auto q = scalpel_b200::pose_from_xyz_rpy(0, 0, 0, 0.1, -0.2, 0.3);\n'
+                   'std::printf("%.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g\\n", p.orientation[0], p.orientation[1],'
+                   ' p.orientation[2], p.orientation[3], q.orientation[0], q.orientation[1], q.orientation[2],'
+                   ' q.orientation[3]); }\n')
+    pe = str(tmp_path / "pose")
+    r = subprocess.run(["g++", "-std=c++17", "-I", inc, str(src), f"-L{libdir}", "-lsg_env", f"-Wl,-rpath,{libdir}",
+                        "-o", pe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    vals = [float(x) for x in subprocess.run([pe], capture_output=True, text=True).stdout.split()]
+    np.testing.assert_allclose(vals[:4], oracle.default_tool_bases(3, 0.15)[2, 3:], atol=1e-16)
+    from tests.test_oracle_image import _quat_rpy
+    np.testing.assert_allclose(vals[4:], _quat_rpy(0.1, -0.2, 0.3), atol=1e-15)
+    import torch
+    if not torch.cuda.is_available():
+        run = subprocess.run([exe], capture_output=True, text=True)
+        assert run.returncode == 1 and "CUDA" in run.stdout

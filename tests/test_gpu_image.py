@@ -150,3 +150,19 @@ def test_image_matching_fused_steps_bench_stream_and_host_step(sg, oracle):
         sg.VecTaskEnv(robots=("psm",), n_envs=4, task="image_matching", render_width=4)
     with pytest.raises(sg.ConfigError, match="exactly 1 robot"):
         sg.VecTaskEnv(robots=("psm", "ecm"), n_envs=4, task="image_matching")
+
+
+def test_image_matching_sharded_rows(sg, oracle):
+    """row_offset shards are bit-identical to the rows of one env (streams by
+    global row, bench stream by global index) across a reset burst."""
+    _cuda()
+    kw = dict(robots=("psm",), seed=3, task="image_matching", episode_len=40)
+    full = sg.VecTaskEnv(n_envs=96, **kw)
+    part = sg.VecTaskEnv(n_envs=40, row_offset=56, **kw)
+    full.reset(); part.reset()
+    full.bench_begin(3); part.bench_begin(3, global_n_envs=96)
+    full.bench_step(45); part.bench_step(45)
+    torch.cuda.synchronize()
+    assert torch.equal(full._result().observations[56:], part._result().observations)
+    assert torch.equal(full.images()["target"][56:], part.images()["target"])
+    assert torch.equal(full.state()["rng_state"][56:], part.state()["rng_state"])

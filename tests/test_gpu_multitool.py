@@ -214,3 +214,30 @@ def test_multitool_host_step_and_errors(sg, oracle):
         sg.VecTaskEnv(robots=("psm", "psm"), n_envs=4, task="multi_tool_reaching", tool_bases=np.zeros((3, 7)))
     with pytest.raises(sg.ConfigError, match="at most 4"):
         sg.VecTaskEnv(robots=("psm",) * 5, n_envs=4, task="multi_tool_reaching")
+
+
+def test_multitool_sharded_rows_and_cpp_example(sg, oracle, tmp_path):
+    """row_offset shards (per-tool streams seeded by global row) are
+    bit-identical to the rows of one env; the C++ drop-in example runs."""
+    _cuda()
+    kw = dict(robots=("psm", "psm", "ecm"), seed=4, task="multi_tool_reaching")
+    full = sg.VecTaskEnv(n_envs=256, **kw)
+    part = sg.VecTaskEnv(n_envs=128, row_offset=128, **kw)
+    full.reset(); part.reset()
+    full.bench_begin(4); part.bench_begin(4, global_n_envs=256)
+    full.bench_step(310); part.bench_step(310)
+    torch.cuda.synchronize()
+    assert torch.equal(full._result().observations[128:], part._result().observations)
+    assert torch.equal(full.state()["rng_state"][:, 128:], part.state()["rng_state"])
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(sg.lib_path())
+    exe = str(tmp_path / "multitool_cpp")
+    r = subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "examples", "multitool_cpp.cpp"), f"-L{libdir}", "-lsg_env",
+                        f"-Wl,-rpath,{libdir}", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stdout + run.stderr
+    assert "tools 3  action_dim 20  obs_dim 78" in run.stdout and run.stdout.count("mean reward") == 10
