@@ -252,3 +252,21 @@ def test_multitool_config_errors(oracle):
         oracle.MultiToolEnv(oracle.env_config(n_envs=2, task=oracle.MULTI_TOOL), [m])
     with pytest.raises(oracle.OracleError, match="collision_threshold"):
         oracle.MultiToolEnv(oracle.env_config(n_envs=2, task=oracle.MULTI_TOOL, collision_threshold=-1.0), [m, m])
+
+
+def test_multitool_row_offset_shards(oracle):
+    """Sharding: tool t of global row g draws from
+    make_stream(seed, t * 2^32 + g), so a shard with row_offset equals the
+    same rows of one env (bench stream indexed by global row)."""
+    ms = [oracle.resolve_robot(r) for r in ("psm", "psm", "ecm")]
+    cfg = dict(seed=9, task=oracle.MULTI_TOOL, episode_len=30)
+    full = oracle.MultiToolEnv(oracle.env_config(n_envs=12, **cfg), ms)
+    part = oracle.MultiToolEnv(oracle.env_config(n_envs=5, row_offset=7, **cfg), ms)
+    full.reset(); part.reset()
+    ar = oracle.make_stream(9, 0xAC7104)
+    for _ in range(40):
+        a = oracle.fill_uniform_actions(ar, 12, 20)
+        full.step(a)
+        part.step(a[7:])
+        np.testing.assert_array_equal(full.obs()[0][7:], part.obs()[0])
+    np.testing.assert_array_equal(full.rng()[0][:, 7:], part.rng()[0])
