@@ -36,7 +36,7 @@ __device__ __forceinline__ void camera_pose(const ImParams& P, const float (&q)[
 // Per-frame sphere constants: oc = camera - centre, c2 = |oc|^2 - r^2.
 struct Frame {
   float R[9];
-  float oc[3][3], c2[3], inv_r[3], alb[3];
+  float oc[3][3], c2[3], ka[3];  // ka = albedo / radius
 };
 
 __device__ __forceinline__ void make_frame(const float (&Rc)[9], const float (&pc)[3], const float (&sc)[15],
@@ -51,8 +51,7 @@ __device__ __forceinline__ void make_frame(const float (&Rc)[9], const float (&p
     F.oc[s][1] = o1;
     F.oc[s][2] = o2;
     F.c2[s] = (o0 * o0 + o1 * o1 + o2 * o2) - r * r;
-    F.inv_r[s] = 1.f / r;
-    F.alb[s] = sc[5 * s + 4];
+    F.ka[s] = sc[5 * s + 4] / r;
   }
 }
 
@@ -75,33 +74,41 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // n . (-d) = -(oc . d + t) / r = sqrt(disc) / r (t = -b - sqrt(disc)), so the
 // nearest hit's shade needs no hit-point reconstruction; the three sphere
 // tests are branch-free (selects) so the warp never diverges per pixel.
-// Column part of the camera ray: a = R * (u, 0, -1).
+// Per-column constants of the camera rays. The unnormalised direction of
+// pixel (u, v) is d = a - v R[:,1] with a = R (u, 0, -1) (top row looks up), so
+// |d|^2 = A0 + v (A1 + v A2) and, per sphere, oc . d = ba + v bb: a pixel needs
+// no direction vector, only these per-lane quadratics / lines in v.
 struct Column {
-  float a0, a1, a2;
+  float A0, A1, A2;
+  float ba[3], bb[3];
 };
 __device__ __forceinline__ Column column(const Frame& F, float u) {
-  return {fmaf(F.R[0], u, -F.R[2]), fmaf(F.R[3], u, -F.R[5]), fmaf(F.R[6], u, -F.R[8])};
+  const float a0 = fmaf(F.R[0], u, -F.R[2]), a1 = fmaf(F.R[3], u, -F.R[5]), a2 = fmaf(F.R[6], u, -F.R[8]);
+  const float r0 = F.R[1], r1 = F.R[4], r2 = F.R[7];
+  Column C;
+  C.A0 = fmaf(a0, a0, fmaf(a1, a1, a2 * a2));
+  C.A1 = -2.f * fmaf(a0, r0, fmaf(a1, r1, a2 * r2));
+  C.A2 = fmaf(r0, r0, fmaf(r1, r1, r2 * r2));
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    C.ba[s] = fmaf(F.oc[s][0], a0, fmaf(F.oc[s][1], a1, F.oc[s][2] * a2));
+    C.bb[s] = -fmaf(F.oc[s][0], r0, fmaf(F.oc[s][1], r1, F.oc[s][2] * r2));
+  }
+  return C;
 }
 
 __device__ __forceinline__ float shade(const ImParams& P, const Frame& F, const Column& C, float v) {
-  // R * (u, -v, -1) = a - v * R[:, 1]: top row looks up
-  float d0 = fmaf(-F.R[1], v, C.a0);
-  float d1 = fmaf(-F.R[4], v, C.a1);
-  float d2 = fmaf(-F.R[7], v, C.a2);
-  const float inv = rsqrt_approx(fmaf(d0, d0, fmaf(d1, d1, d2 * d2)));
-  d0 *= inv;
-  d1 *= inv;
-  d2 *= inv;
+  const float inv = rsqrt_approx(fmaf(v, fmaf(v, C.A2, C.A1), C.A0));  // 1 / |d|
   float best = P.far_, value = 0.f;
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    const float b = fmaf(F.oc[s][0], d0, fmaf(F.oc[s][1], d1, F.oc[s][2] * d2));
+    const float b = fmaf(v, C.bb[s], C.ba[s]) * inv;  // oc . d / |d|
     const float disc = fmaf(b, b, -F.c2[s]);
     const float sq = sqrt_approx(fmaxf(disc, 0.f));
     const float t = -b - sq;
     const bool hit = disc >= 0.f && t >= P.near_ && t < best;
     best = hit ? t : best;
-    value = hit ? F.alb[s] * (sq * F.inv_r[s]) : value;
+    value = hit ? F.ka[s] * sq : value;  // albedo * lambert, lambert = sqrt(disc) / r
   }
   return value;
 }
