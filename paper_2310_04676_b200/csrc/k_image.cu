@@ -329,17 +329,44 @@ __global__ void __launch_bounds__(32 * kImWarps, SG_IM_MINB) im_step_kernel(cons
     float* o_tgt = row + head;
     float* o_cur = row + head + wh;
     float acc = 0.f;
-    for (int px = lane; px < W; px += 32) {  // lane-fixed columns, rows in the inner loop
-      const Column C = column(F, ((float)px + 0.5f - 0.5f * (float)W) * P.inv_f);
+    if (W % 4 == 0 && 128 % W == 0 && wh % 128 == 0) {
+      // 4 consecutive pixels per lane and 128 per warp iteration: the lane's
+      // 4 columns are fixed (128 is a multiple of W), the target read is one
+      // float4, the observation writes are float4 when the row is 16-byte
+      // aligned (3A + 3 and O multiples of 4, e.g. PSM)
+      const int px0 = (4 * lane) % W, prow = (4 * lane) / W, rows_it = 128 / W;
+      Column C[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) C[j] = column(F, ((float)(px0 + j) + 0.5f - 0.5f * (float)W) * P.inv_f);
+      const bool st4 = ((head | O) & 3) == 0;
+      for (int it = 0; it < wh / 128; ++it) {
+        const int p = 128 * it + 4 * lane;
+        const float v = ((float)(it * rows_it + prow) + 0.5f - 0.5f * (float)P.H) * P.inv_f;
+        const float4 t4 = *reinterpret_cast<const float4*>(tgt + p);
+        const float c0 = shade(P, F, C[0], v), c1 = shade(P, F, C[1], v), c2 = shade(P, F, C[2], v),
+                    c3 = shade(P, F, C[3], v);
+        acc += (fabsf(c0 - t4.x) + fabsf(c1 - t4.y)) + (fabsf(c2 - t4.z) + fabsf(c3 - t4.w));
+        if (st4) {
+          *reinterpret_cast<float4*>(o_tgt + p) = t4;
+          *reinterpret_cast<float4*>(o_cur + p) = make_float4(c0, c1, c2, c3);
+        } else {
+          o_tgt[p] = t4.x; o_tgt[p + 1] = t4.y; o_tgt[p + 2] = t4.z; o_tgt[p + 3] = t4.w;
+          o_cur[p] = c0; o_cur[p + 1] = c1; o_cur[p + 2] = c2; o_cur[p + 3] = c3;
+        }
+      }
+    } else {
+      for (int px = lane; px < W; px += 32) {  // lane-fixed columns, rows in the inner loop
+        const Column C = column(F, ((float)px + 0.5f - 0.5f * (float)W) * P.inv_f);
 #pragma unroll 4
-      for (int py = 0; py < P.H; ++py) {
-        const float v = ((float)py + 0.5f - 0.5f * (float)P.H) * P.inv_f;
-        const int p = py * W + px;
-        const float c = shade(P, F, C, v);
-        const float t = tgt[p];
-        acc += fabsf(c - t);
-        o_tgt[p] = t;
-        o_cur[p] = c;
+        for (int py = 0; py < P.H; ++py) {
+          const float v = ((float)py + 0.5f - 0.5f * (float)P.H) * P.inv_f;
+          const int p = py * W + px;
+          const float c = shade(P, F, C, v);
+          const float t = tgt[p];
+          acc += fabsf(c - t);
+          o_tgt[p] = t;
+          o_cur[p] = c;
+        }
       }
     }
     const float err = warp_sum(acc) / (float)wh;
