@@ -475,7 +475,7 @@ def main():
                         l2="256 MiB flush between timed launches; per-launch state read cold from HBM"),
             roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
                           traffic=traffic, peak_kind=peak_kind, kernel=(f"mt_step_kernel<T={len(robots)}, GEN> ({F} fused steps/launch)" if len(robots) > 1 else
-                                  f"im_step_kernel<8, GEN> ({F} fused steps/launch)" if wh else
+                                  f"im_step_kernel<{cfg['robot'].upper()} chain, GEN> ({F} fused steps/launch)" if wh else
                                   f"env_step_kernel<{cfg['robot'].upper()} chain, 2 team warps, GEN> ({F} fused steps/launch)"),
                           bytes_per_env_step=b["per_env_step"], bytes_per_launch=n * b["per_env_launch"],
                           avg_launch_us=avg_launch_s * 1e6),

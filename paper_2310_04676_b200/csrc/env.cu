@@ -697,6 +697,12 @@ std::unique_ptr<sg_env> make_image_env(const sg_env_config& cfg, const sg_dynami
   I.robot = build_table(m, rd.dt_sub, rd.kp, rd.kd, rd.inertia, rd.damping);
   const Mat3 cr = trailing_tip_rotation(m);
   for (int k = 0; k < 9; ++k) I.cam_R[k] = static_cast<float>(cr[k]);
+  // the camera FK only needs the chain structure (any control mode)
+  I.chain = chain_matches<sg::PsmChain>(I.robot)    ? sg::kChainPsm
+            : chain_matches<sg::EcmChain>(I.robot)  ? sg::kChainEcm
+            : chain_matches<sg::StarChain>(I.robot) ? sg::kChainStar
+            : I.robot.dof <= 8                      ? sg::kChainGeneric8
+                                                    : sg::kChainGeneric16;
   env->n = cfg.n_envs;
   env->A = m.dof_count;
   I.A = m.dof_count;

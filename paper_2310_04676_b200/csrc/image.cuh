@@ -21,6 +21,7 @@ struct ImParams {
   RobotTable robot;
   float cam_R[9];  // trailing fixed rotations x tip orientation: camera frame in the last DoF frame
   int32_t A, O, W, H, wh, episode_len, substeps, control_mode;
+  int32_t chain, pad1;  // ChainId of the camera FK (launch.hpp): specialised structure or generic
   int64_t n;
   float f, inv_f, near_, far_, dt_sub, pad0;  // f: focal length in pixels, 0.5 w / tan(fov / 2)
   double sigma, radius, center[3];

@@ -1,5 +1,6 @@
 // ImageMatching step / reset kernels (image.cuh): one warp per env.
 #include "image.cuh"
+#include "launch.hpp"
 
 namespace sg {
 namespace {
@@ -13,18 +14,27 @@ constexpr unsigned kFull = 0xffffffffu;
 // fk_walk (robot_model.cpp:371-395) keeping the rotation: tip position and
 // the camera rotation (last DoF frame x trailing rotation, Pose orientation
 // as a matrix; the tool base of a single-robot env is the identity).
-template <int DMAX>
-__device__ __forceinline__ void camera_pose(const ImParams& P, const float (&q)[DMAX], float (&Rc)[9], float (&pc)[3]) {
+// CH: FixedChain (compile-time joint structure of PSM / ECM / STAR, no sin/cos
+// range reduction: selected only when every revolute limit is within +-pi)
+// or GenericChain<8|16> (runtime joint table).
+template <class CH>
+__device__ __forceinline__ void camera_pose(const ImParams& P, const float (&q)[CH::kDof], float (&Rc)[9],
+                                            float (&pc)[3]) {
   const RobotTable& R = P.robot;
   float m[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
   float p[3] = {0.f, 0.f, 0.f};
+  if constexpr (CH::kExact) {
+    CH::walk(R, q, m, p, std::make_integer_sequence<int, CH::kDof>{});
+    fk_tip_offset(R, CH::kTipFlags, m, p, pc);
+  } else {
 #pragma unroll
-  for (int d = 0; d < DMAX; ++d) {
-    if (d >= R.dof) break;
-    const JointEnc& J = R.j[d];
-    fk_joint(J, J.kind, J.axis_code, J.flags & 7, (J.flags >> 3) & 1, q[d], m, p);
+    for (int d = 0; d < CH::kDof; ++d) {
+      if (d >= R.dof) break;
+      const JointEnc& J = R.j[d];
+      fk_joint(J, J.kind, J.axis_code, J.flags & 7, (J.flags >> 3) & 1, q[d], m, p);
+    }
+    fk_tip_offset(R, R.tip_flags, m, p, pc);
   }
-  fk_tip_offset(R, R.tip_flags, m, p, pc);
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -132,9 +142,10 @@ __device__ __forceinline__ void gather_q(float mine, float (&qa)[DMAX]) {
 // and the post-reset observation row to HBM (the caller reloads its
 // registers from there: no reference arguments, so the hot loop's state
 // never lives on the stack).
-template <int DMAX>
+template <class CH>
 __device__ __noinline__ void im_reset_env(const ImParams& P, int64_t i, int lane) {
   float q, sc[15];
+  constexpr int DMAX = CH::kDof;
   const RobotTable& R = P.robot;
   const int64_t n = P.n;
   const int A = R.dof;
@@ -174,8 +185,8 @@ __device__ __noinline__ void im_reset_env(const ImParams& P, int64_t i, int lane
   for (int d = 0; d < DMAX; ++d)
     if (d == lane) q = q0[d];
   float RT[9], pT[3], R0[9], p0[3];
-  camera_pose<DMAX>(P, qT, RT, pT);
-  camera_pose<DMAX>(P, q0, R0, p0);
+  camera_pose<CH>(P, qT, RT, pT);
+  camera_pose<CH>(P, q0, R0, p0);
   if (lane == 0) P.rng_state[i] = s;
   if (lane < 15) {
     float v = 0.f;
@@ -231,7 +242,7 @@ __device__ __noinline__ void im_reset_env(const ImParams& P, int64_t i, int lane
   }
 }
 
-template <int DMAX, bool GEN>
+template <class CH, bool GEN>
 __global__ void __launch_bounds__(32 * kImWarps, SG_IM_MINB) im_step_kernel(const __grid_constant__ ImParams P, int k_steps) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kImWarps + (threadIdx.x >> 5);
@@ -308,10 +319,11 @@ __global__ void __launch_bounds__(32 * kImWarps, SG_IM_MINB) im_step_kernel(cons
       if (__any_sync(kFull, bad) && lane == 0) atomicOr(P.err, kErrNonFiniteAction);
     }
     // ---- camera FK (refresh_tips, envs.cpp:456-463) --------------------------
+    constexpr int DMAX = CH::kDof;
     float qa[DMAX];
     gather_q<DMAX>(q, qa);
     float Rc[9], pc[3];
-    camera_pose<DMAX>(P, qa, Rc, pc);
+    camera_pose<CH>(P, qa, Rc, pc);
     if (lane < 3) P.tips[lane * n + i] = lane == 0 ? pc[0] : (lane == 1 ? pc[1] : pc[2]);
     step_count += 1;
     const bool ends = step_count >= P.episode_len;  // goal_met is never set for ImageMatching
@@ -381,7 +393,7 @@ __global__ void __launch_bounds__(32 * kImWarps, SG_IM_MINB) im_step_kernel(cons
     if (ends) {  // terminal row written above; reset_row + re-observe
       if (lane == 0) atomicAdd(P.ended_total, 1ull);
       __syncwarp();
-      im_reset_env<DMAX>(P, i, lane);
+      im_reset_env<CH>(P, i, lane);
       __syncwarp();
       q = own ? P.q[lane * n + i] : 0.f;
       qd = 0.f;
@@ -402,12 +414,12 @@ __global__ void __launch_bounds__(32 * kImWarps, SG_IM_MINB) im_step_kernel(cons
   }
 }
 
-template <int DMAX>
+template <class CH>
 __global__ void __launch_bounds__(32 * kImWarps) im_reset_kernel(const __grid_constant__ ImParams P) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kImWarps + (threadIdx.x >> 5);
   if (i >= P.n) return;
-  im_reset_env<DMAX>(P, i, lane);  // VecTaskEnv::reset (envs.cpp:425-435)
+  im_reset_env<CH>(P, i, lane);  // VecTaskEnv::reset (envs.cpp:425-435)
   if (lane == 0) {
     P.episode_count[i] = 0;
     P.terminated[i] = 0;
@@ -416,19 +428,25 @@ __global__ void __launch_bounds__(32 * kImWarps) im_reset_kernel(const __grid_co
   }
 }
 
-template <int DMAX>
+template <class CH>
 cudaError_t launch_d(const ImParams& P, int k_steps, bool gen, bool reset, cudaStream_t st) {
   const unsigned grid = (unsigned)((P.n + kImWarps - 1) / kImWarps);
-  if (reset) im_reset_kernel<DMAX><<<grid, 32 * kImWarps, 0, st>>>(P);
-  else if (gen) im_step_kernel<DMAX, true><<<grid, 32 * kImWarps, 0, st>>>(P, k_steps);
-  else im_step_kernel<DMAX, false><<<grid, 32 * kImWarps, 0, st>>>(P, k_steps);
+  if (reset) im_reset_kernel<CH><<<grid, 32 * kImWarps, 0, st>>>(P);
+  else if (gen) im_step_kernel<CH, true><<<grid, 32 * kImWarps, 0, st>>>(P, k_steps);
+  else im_step_kernel<CH, false><<<grid, 32 * kImWarps, 0, st>>>(P, k_steps);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_image(const ImParams& P, int k_steps, bool gen, bool reset, cudaStream_t st) {
-  return P.robot.dof <= 8 ? launch_d<8>(P, k_steps, gen, reset, st) : launch_d<16>(P, k_steps, gen, reset, st);
+  switch (P.chain) {
+    case kChainPsm: return launch_d<PsmChain>(P, k_steps, gen, reset, st);
+    case kChainEcm: return launch_d<EcmChain>(P, k_steps, gen, reset, st);
+    case kChainStar: return launch_d<StarChain>(P, k_steps, gen, reset, st);
+    case kChainGeneric16: return launch_d<GenericChain<16>>(P, k_steps, gen, reset, st);
+    default: return launch_d<GenericChain<8>>(P, k_steps, gen, reset, st);
+  }
 }
 
 }  // namespace sg
