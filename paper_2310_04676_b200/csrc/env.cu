@@ -587,6 +587,10 @@ std::unique_ptr<sg_env> make_multi_env(const sg_env_config& cfg, const sg_dynami
     const sg::Vec3 view = mat_vec(trailing_tip_rotation(m), sg::Vec3{0.0, 0.0, -1.0});
     for (int k = 0; k < 3; ++k) E.view[k] = static_cast<float>(view[k]);
     E.camera = m.name == "ecm" ? 1 : 0;  // envs.cpp:339, 545
+    E.chain = chain_matches<sg::PsmChain>(E.robot)    ? sg::kChainPsm
+              : chain_matches<sg::EcmChain>(E.robot)  ? sg::kChainEcm
+              : chain_matches<sg::StarChain>(E.robot) ? sg::kChainStar
+                                                      : sg::kChainGeneric8;
     E.off = A;
     A += m.dof_count;
     // workspace centre: tool_bases_[t].transform_point(FK(mid).position) (envs.cpp:159-161)

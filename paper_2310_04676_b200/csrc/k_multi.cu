@@ -7,6 +7,7 @@
 // mapped through the tool's base pose. Warp 0 scores; observation rows are
 // staged in shared memory and stored as one contiguous float4 run per team.
 #include "multi.cuh"
+#include "launch.hpp"
 
 
 namespace sg {
@@ -30,19 +31,27 @@ __device__ __forceinline__ bool mt_sample_goal(uint64_t& s, uint64_t inc, double
 
 // Tool FK: world tip = base_p + base_R * (p + m * tip); the camera axis
 // (tips_[t].orientation * (0, 0, -1), envs.cpp:556-557) = base_R * (m * view).
+// CH: the tool's compile-time chain structure (FixedChain: no runtime joint
+// branches, no sin/cos range reduction) or GenericChain<kMaxToolDof>.
+template <class CH = GenericChain<kMaxToolDof>>
 __device__ __forceinline__ void tool_fk(const ToolEnc& E, const float (&q)[kMaxToolDof], float (&tip)[3],
                                         float (&axis)[3]) {
   const RobotTable& R = E.robot;
   float m[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
   float p[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-  for (int d = 0; d < kMaxToolDof; ++d) {
-    if (d >= R.dof) break;
-    const JointEnc& J = R.j[d];
-    fk_joint(J, J.kind, J.axis_code, J.flags & 7, (J.flags >> 3) & 1, q[d], m, p);
-  }
   float t[3];
-  fk_tip_offset(R, R.tip_flags, m, p, t);
+  if constexpr (CH::kExact) {
+    CH::walk(R, reinterpret_cast<const float(&)[CH::kDof]>(q), m, p, std::make_integer_sequence<int, CH::kDof>{});
+    fk_tip_offset(R, CH::kTipFlags, m, p, t);
+  } else {
+#pragma unroll
+    for (int d = 0; d < kMaxToolDof; ++d) {
+      if (d >= R.dof) break;
+      const JointEnc& J = R.j[d];
+      fk_joint(J, J.kind, J.axis_code, J.flags & 7, (J.flags >> 3) & 1, q[d], m, p);
+    }
+    fk_tip_offset(R, R.tip_flags, m, p, t);
+  }
 #pragma unroll
   for (int r = 0; r < 3; ++r)
     tip[r] = E.base_p[r] + E.base_R[r * 3 + 0] * t[0] + E.base_R[r * 3 + 1] * t[1] + E.base_R[r * 3 + 2] * t[2];
@@ -207,6 +216,7 @@ struct ToolWarp {
   }
 
   // dynamics (dynamics.cpp:127-185) + FK + staging of the tool's obs columns
+  template <class CH>
   __device__ __forceinline__ static void step(ToolState& S, const MtParams& P, const ToolEnc& E, int t, const float* s_act_row,
                               float* s_act_out, float* o, int& sat, int& bad, float (&tip)[3], float (&axis)[3]) {
     float (&q)[kMaxToolDof] = S.q;
@@ -214,7 +224,10 @@ struct ToolWarp {
     float (&qt)[kMaxToolDof] = S.qt;
     uint64_t& act_s = S.act_s;
     const RobotTable& R = E.robot;
-    const int dof = R.dof, jaw = R.jaw, off = E.off, A = P.A;
+    // compile-time DoF count / jaw for the fixed chains
+    const int dof = CH::kExact ? CH::kDof : R.dof;
+    const int jaw = CH::kExact ? CH::jaw(R) : R.jaw;
+    const int off = E.off, A = P.A;
     const int mode = P.control_mode;
     float kpqt[kMaxToolDof], vt[kMaxToolDof], tc[kMaxToolDof];
     uint64_t ds = GEN ? act_s * E.col_mult + E.col_add : 0;
@@ -276,7 +289,7 @@ struct ToolWarp {
       o[A + off + d] = qd[d];
       o[2 * A + 3 * T + off + d] = qt[d];
     }
-    tool_fk(E, q, tip, axis);  // refresh_tips (envs.cpp:456-463)
+    tool_fk<CH>(E, q, tip, axis);  // refresh_tips (envs.cpp:456-463)
 #pragma unroll
     for (int k = 0; k < 3; ++k) o[2 * A + 3 * t + k] = tip[k];
   }
@@ -352,7 +365,22 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
     int sat = 0, bad = 0;
     {
       float tip[3], axis[3];
-      TW::step(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
+      // one code path per chain structure (not per tool: both PSM warps of a
+      // trimanual team share the PSM path)
+      switch (E.chain) {
+        case kChainPsm:
+          TW::template step<PsmChain>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
+          break;
+        case kChainEcm:
+          TW::template step<EcmChain>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
+          break;
+        case kChainStar:
+          TW::template step<StarChain>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
+          break;
+        default:
+          TW::template step<GenericChain<kMaxToolDof>>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat,
+                                                       bad, tip, axis);
+      }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         ts.tip[b][warp][k][lane] = tip[k];

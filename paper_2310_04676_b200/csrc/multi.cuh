@@ -26,6 +26,8 @@ struct ToolEnc {
   int32_t off;        // first action / DoF column of the tool
   double center[3];   // workspace centre: base.transform_point(FK(mid)) (envs.cpp:159-161)
   uint64_t col_mult, col_add;  // bench stream: advance by `off` draws (row start -> the tool's first column)
+  int32_t chain;               // ChainId (launch.hpp): compile-time structure of the tool's FK, or generic
+  int32_t pad[3];
 };
 
 struct MtParams {
