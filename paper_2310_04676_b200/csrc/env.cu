@@ -937,9 +937,8 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   // kernel selection: compile-time chain structure when the descriptor's
   // structure matches a builtin one and the dynamics are the reference
   // defaults' shape (position control, 4 substeps); generic chain otherwise
-  // ActiveTracking runs on the generic chains (runtime task; no specialised instantiation)
-  env->chain = cfg.task == SG_TASK_ACTIVE_TRACKING ? (P.robot.dof <= 8 ? sg::kChainGeneric8 : sg::kChainGeneric16)
-                                                    : select_chain(P.robot, dc.control_mode, dc.substeps);
+  // (every single-robot task, ActiveTracking included, has specialised instantiations)
+  env->chain = select_chain(P.robot, dc.control_mode, dc.substeps);
   env->team_warps = team_warps_for(env->chain);
   CK(cudaDeviceSynchronize());
   return env;

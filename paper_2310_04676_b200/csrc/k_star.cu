@@ -5,6 +5,7 @@ namespace sg {
 
 cudaError_t launch_star(const StepParams& P, const LaunchArgs& a) {
   if (a.task == kTaskPath) return launch_fixed<StarChain, kTaskPath, kModePosition, 4>(P, a);
+  if (a.task == kTaskTrack) return launch_fixed<StarChain, kTaskTrack, kModePosition, 4>(P, a);
   return launch_fixed<StarChain, kTaskTarget, kModePosition, 4>(P, a);
 }
 
