@@ -166,3 +166,30 @@ def test_image_matching_sharded_rows(sg, oracle):
     assert torch.equal(full._result().observations[56:], part._result().observations)
     assert torch.equal(full.images()["target"][56:], part.images()["target"])
     assert torch.equal(full.state()["rng_state"][56:], part.state()["rng_state"])
+
+
+@pytest.mark.parametrize("w,h,fov", [(48, 40, 0.9), (64, 64, 1.2)])
+def test_image_matching_render_configs(sg, oracle, w, h, fov):
+    """Non-default RenderConfig (render.hpp:31-38): 48 x 40 runs the
+    lane-per-column path (128 % w != 0), 64 x 64 the 4-pixels-per-lane path;
+    images within the pixel tolerance of the oracle over a reset burst."""
+    _cuda()
+    m = oracle.resolve_robot("ecm")
+    n = 24
+    rc = dict(render_w=w, render_h=h, render_fov=fov, render_near=0.01, render_far=1.5)
+    ref = oracle.Env(oracle.env_config(n_envs=n, seed=4, task=oracle.IMAGE_MATCHING, episode_len=30, **rc), m)
+    env = sg.VecTaskEnv(robots=("ecm",), n_envs=n, seed=4, task="image_matching", episode_len=30,
+                        render_width=w, render_height=h, render_fov=fov, render_near=0.01, render_far=1.5)
+    A = env.action_dim
+    assert env.obs_dim == ref.obs_dim == 3 * A + 3 + 2 * w * h
+    o_ref = ref.reset()
+    _check_obs(env.reset().cpu().numpy(), o_ref, A, w * h, "reset")
+    ar = oracle.make_stream(4, 0xAC7104)
+    for s in range(35):
+        a32 = oracle.fill_uniform_actions(ar, n, A).astype(np.float32)
+        res = env.step(torch.from_numpy(a32).cuda())
+        ref.step(a32.astype(np.float64))
+        r = ref.result()
+        np.testing.assert_array_equal(res.timed_out.cpu().numpy(), r["timed_out"])
+        _check_obs(res.observations.cpu().numpy(), ref.obs()[0], A, w * h, f"obs @{s}")
+        assert np.abs(res.rewards.cpu().numpy() - r["rewards"]).max() < 5e-3

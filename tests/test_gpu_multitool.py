@@ -241,3 +241,36 @@ def test_multitool_sharded_rows_and_cpp_example(sg, oracle, tmp_path):
     run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
     assert "tools 3  action_dim 20  obs_dim 78" in run.stdout and run.stdout.count("mean reward") == 10
+
+
+@pytest.mark.parametrize("mode", ["velocity", "torque"])
+def test_multitool_control_modes(sg, oracle, mode):
+    """Velocity / torque control (dynamics.cpp:141-150) on every tool with
+    adversarial actions in [-2, 2]: saturation counts exact, limits hold,
+    joint state within 10x the step tolerance of the oracle over 120 steps."""
+    _cuda()
+    robots = ("psm", "psm", "ecm")
+    ms = [oracle.resolve_robot(r) for r in robots]
+    dyns = []
+    for m in ms:
+        d = oracle.default_dynamics(m)
+        d.control_mode = {"velocity": 1, "torque": 2}[mode]
+        dyns.append(d)
+    n = 48
+    ref = oracle.MultiToolEnv(oracle.env_config(n_envs=n, seed=12, task=oracle.MULTI_TOOL), ms, dyns=dyns)
+    env = sg.VecTaskEnv(robots=robots, n_envs=n, seed=12, task="multi_tool_reaching",
+                        dynamics=dict(control_mode=mode))
+    ref.reset(); env.reset()
+    rng = oracle.make_stream(3, 0)
+    f32 = lambda v: np.float64(np.float32(v))
+    lo = np.concatenate([[f32(m.dof_joint(d).limit_lo) for d in range(m.dof)] for m in ms])
+    hi = np.concatenate([[f32(m.dof_joint(d).limit_hi) for d in range(m.dof)] for m in ms])
+    for s in range(120):
+        a = (2.0 * oracle.fill_uniform_actions(rng, n, 20)).astype(np.float32)
+        hr = env.step_host(a)
+        ref.step(a.astype(np.float64))
+        assert hr["action_saturations"] == ref.result()["saturations"]
+        q = env.state()["q"].cpu().numpy().T.astype(np.float64)
+        assert (q >= lo).all() and (q <= hi).all()
+        assert np.abs(q - ref.state()["q"]).max() <= 1e-4, s
+        np.testing.assert_array_equal(hr["timed_out"], ref.result()["timed_out"])
