@@ -27,6 +27,8 @@
  *   sg_env_bench_*           bench_sim's action stream + step loop  src/bench.cpp:31-35,97-135
  *   sg_robot_*               parse_robot / forward_kinematics_batch  src/robot_model.cpp:191-283,404-443
  *   sg_policy_*              Policy ctor / forward (tensor cores)   src/policy.cpp:42-161
+ *   sg_elu_*, sg_ppo_gather  ppo_update minibatch gather + ELU fwd/bwd  src/ppo.cpp:157-224, src/policy.cpp:33,163-218
+ *   sg_ppo_loss              ppo_loss_and_grad (loss, metrics, analytic gradients)  src/ppo.cpp:76-155
  *   sg_last_error            exception message (what()) of the reference's
  *                            ConfigError / ParseError / SimError  include/scalpel/errors.hpp:23-48
  *
@@ -302,6 +304,32 @@ int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d
                  float* d_grad_sq, int32_t* d_step, double lr, double beta1, double beta2, double eps,
                  double max_grad_norm, int64_t log_std_offset, int32_t log_std_n, double log_std_min,
                  double log_std_max, void* stream);
+/* PPO update helpers around the library GEMMs (Trainer::update / ppo_update,
+ * ppo.cpp:157-224; Policy::backward, policy.cpp:163-218). dtype 0 = fp32,
+ * 1 = bf16; count a multiple of 4 (fp32) / 8 (bf16) elements, 16-byte aligned.
+ * ELU forward h = z > 0 ? z : expm1(z) (may run in place); backward from the
+ * output: dz = dh * (h > 0 ? 1 : h + 1). Graph-capturable. */
+int sg_elu_forward(const void* d_z, void* d_h, int64_t count, int32_t dtype, void* stream);
+int sg_elu_backward(const void* d_h, const void* d_dh, void* d_dz, int64_t count, int32_t dtype, void* stream);
+/* Minibatch gather (ppo.cpp:173-190): rows d_idx[0..m) of the rollout buffer:
+ * obs (obs_w fp32 per row, obs_w % 4 == 0) into d_obs_out (fp32, or bf16 when
+ * obs_bf16), actions (A fp32), old log-probs, advantages, returns. */
+int sg_ppo_gather(const int64_t* d_idx, int64_t m, const float* d_obs, int32_t obs_w, void* d_obs_out,
+                  int32_t obs_bf16, const float* d_act, int32_t A, float* d_act_out, const float* d_logp,
+                  float* d_logp_out, const float* d_adv, float* d_adv_out, const float* d_ret, float* d_ret_out,
+                  void* stream);
+/* The data part of ppo_loss_and_grad (ppo.cpp:90-154) in one pass over a
+ * minibatch of B samples: d_mean / d_value are the padded last-layer outputs
+ * (row strides mstride >= A, vstride >= 1; dtype 0 fp32, 1 bf16), log-std
+ * clamped to [ls_min, ls_max]; writes the analytic gradients d_dmean /
+ * d_dvalue (same layout and dtype, padded columns zero) and d_dlog_std (A,
+ * zero outside the box), d_out = {loss, policy_loss, value_loss, entropy, kl,
+ * clip_fraction}; d_acc: 4 + A floats of scratch. A <= 16. */
+int sg_ppo_loss(const void* d_mean, int32_t mstride, const void* d_value, int32_t vstride, int32_t dtype,
+                const float* d_log_std_raw, const float* d_act, const float* d_old_logp, const float* d_adv,
+                const float* d_ret, int64_t B, int32_t A, double clip_eps, double value_coef, double entropy_coef,
+                double ls_min, double ls_max, void* d_dmean, void* d_dvalue, float* d_dlog_std, float* d_acc,
+                float* d_out, void* stream);
 /* Policy checkpoints in the reference's versioned binary format
  * (save_checkpoint / load_checkpoint, src/policy.cpp:220-295): "SCLPCKP1",
  * u32 version 1, obs_dim, action_dim, n_hidden, hidden[], length-prefixed

@@ -96,11 +96,8 @@ class TrainConfig:  # ppo.hpp:25-45
 
 
 class _Linear(torch.autograd.Function):
-    """y = x W^T + b with every gradient a GEMM. The weight gradient
-    dy^T x reduces over the whole minibatch (K = 131072) into a small output;
-    it is computed split-K as a batched GEMM over 4096-row chunks plus a sum,
-    so it fills the GPU instead of a handful of CTAs. The bias gradient is
-    ones^T dy (a GEMV) instead of a column reduction."""
+    """y = x W^T + b with every gradient a GEMM (_linear_grads); the bias
+    gradient is ones^T dy (a GEMV) instead of a column reduction."""
 
     _ones: dict = {}
 
@@ -117,30 +114,55 @@ class _Linear(torch.autograd.Function):
     @staticmethod
     def backward(ctx, gy):
         x, W = ctx.saved_tensors
-        gx = gy @ W if ctx.needs_input_grad[0] else None
-        B = gy.shape[0]
-        chunk = 4096
-        if B % chunk == 0 and B >= 4 * chunk:
-            S = B // chunk
-            gW = torch.bmm(gy.view(S, chunk, -1).transpose(1, 2), x.view(S, chunk, -1)).sum(0)
-        else:
-            gW = gy.t() @ x
-        key = (B, gy.dtype, gy.device)
-        ones = _Linear._ones.get(key)
-        if ones is None:
-            ones = _Linear._ones[key] = torch.ones(1, B, dtype=gy.dtype, device=gy.device)
-        gb = (ones @ gy).view(-1)
-        return gx, gW.to(ctx.w_dtype), gb.to(ctx.w_dtype), None, None
+        return _linear_grads(ctx, gy, x, W)
 
 
-def _linear(x, W, b, Wm=None, bm=None):
+def _linear_grads(ctx, gy, x, W):
+    """dX = dY W; dW = dY^T X and db = 1^T dY reduce over the whole minibatch
+    (K = 131072) straight into fp32 (out_dtype: one GEMM, fp32 accumulation
+    and output; tools/gw_probe.py: 24-31 us per layer vs 42-45 us for the
+    earlier bf16 split-K batched GEMM + sum, at 1/100 of its rounding error)."""
+    gx = gy @ W if ctx.needs_input_grad[0] else None
+    B = gy.shape[0]
+    out_dt = torch.float32 if gy.dtype in (torch.bfloat16, torch.float16) else None
+    gW = torch.mm(gy.t(), x, out_dtype=out_dt) if out_dt else gy.t() @ x
+    key = (B, gy.dtype, gy.device)
+    ones = _Linear._ones.get(key)
+    if ones is None:
+        ones = _Linear._ones[key] = torch.ones(1, B, dtype=gy.dtype, device=gy.device)
+    gb = (torch.mm(ones, gy, out_dtype=out_dt) if out_dt else ones @ gy).view(-1)
+    return gx, gW.to(ctx.w_dtype), gb.to(ctx.w_dtype), None, None
+
+
+class _LinearELU(torch.autograd.Function):
+    """h = ELU(x W^T + b) (policy.cpp:120-128): the GEMM in the library, the
+    activation in place on the device ELU kernel (train.cu). Only h is kept:
+    the derivative exp(z) = h + 1 on the negative side comes from the output."""
+
+    @staticmethod
+    def forward(ctx, x, W, b, Wc=None, bc=None):
+        Wc = W if Wc is None else Wc
+        bc = b if bc is None else bc
+        ctx.w_dtype = W.dtype
+        h = sg.elu_forward(torch.addmm(bc, x, Wc.t()), out=None)
+        ctx.save_for_backward(x, Wc, h)
+        return h
+
+    @staticmethod
+    def backward(ctx, gh):
+        x, W, h = ctx.saved_tensors
+        return _linear_grads(ctx, sg.elu_backward(h, gh.contiguous()), x, W)
+
+
+def _linear(x, W, b, Wm=None, bm=None, elu: bool = False):
+    fn = _LinearELU if elu else _Linear
     if torch.is_autocast_enabled():
         dt = torch.get_autocast_dtype("cuda")
         with torch.autocast("cuda", enabled=False):
             if Wm is not None and Wm.dtype == dt:
-                return _Linear.apply(x.to(dt), W, b, Wm, bm)
-            return _Linear.apply(x.to(dt), W.to(dt), b.to(dt))
-    return _Linear.apply(x, W, b)
+                return fn.apply(x.to(dt), W, b, Wm, bm)
+            return fn.apply(x.to(dt), W.to(dt), b.to(dt))
+    return fn.apply(x, W, b)
 
 
 def param_layout(obs_dim: int, act_dim: int):
@@ -199,17 +221,22 @@ def mlp_forward(params: torch.Tensor, obs: torch.Tensor, obs_dim: int, act_dim: 
     return mean, value, ls_off
 
 
-def mlp_layers(layers, obs):
-    """layers[k] = (W, b) or (W, b, W_bf16_mirror, b_bf16_mirror)."""
+def mlp_layers(layers, obs, device_elu: bool = False, full: bool = False):
+    """layers[k] = (W, b) or (W, b, W_bf16_mirror, b_bf16_mirror).
+    device_elu: hidden activations on the train.cu ELU kernels (CUDA tensors).
+    full: return the whole (padded) critic output instead of its column 0."""
     outs = []
     for trunk in (0, 1):
         h = obs
         for l in range(4):
-            h = _linear(h, *layers[4 * trunk + l])
-            if l < 3:
-                h = F.elu(h)
+            if device_elu and l < 3:
+                h = _linear(h, *layers[4 * trunk + l], elu=True)
+            else:
+                h = _linear(h, *layers[4 * trunk + l])
+                if l < 3:
+                    h = F.elu(h)
         outs.append(h)
-    return outs[0], outs[1][:, 0]
+    return (outs[0], outs[1]) if full else (outs[0], outs[1][:, 0])
 
 
 def loss_head(mean, value, log_std_raw, actions, old_logp, adv, ret, cfg: TrainConfig):
@@ -233,6 +260,35 @@ def loss_head(mean, value, log_std_raw, actions, old_logp, adv, ret, cfg: TrainC
                                (old_logp - logp).mean().detach(),
                                ((ratio - 1.0).abs() > cfg.clip_eps).float().mean()])
     return loss, metrics
+
+
+class _PPOLossDevice(torch.autograd.Function):
+    """The data part of ppo_loss_and_grad (ppo.cpp:90-154) on one fused device
+    kernel (train.cu sg_ppo_loss): it forms the loss, the metrics and, like the
+    reference, the analytic gradients in the same pass; backward only scales
+    them by the incoming gradient. mean_full / value_full are the padded
+    last-layer outputs (columns >= A, resp. >= 1, get zero gradient)."""
+
+    @staticmethod
+    def forward(ctx, mean_full, value_full, log_std_raw, act, old_logp, adv, ret, A, clip_eps, value_coef,
+                entropy_coef):
+        dmean = torch.empty_like(mean_full)
+        dvalue = torch.empty_like(value_full)
+        dls = torch.empty_like(log_std_raw)
+        acc = torch.empty(4 + A, device=mean_full.device)
+        out = torch.empty(6, device=mean_full.device)
+        sg.ppo_loss(mean_full, value_full, log_std_raw, act, old_logp, adv, ret, A, clip_eps, value_coef,
+                    entropy_coef, LOG_STD_MIN, LOG_STD_MAX, dmean, dvalue, dls, acc, out)
+        ctx.save_for_backward(dmean, dvalue, dls)
+        metrics = out[1:6]
+        ctx.mark_non_differentiable(metrics)
+        return out[0], metrics
+
+    @staticmethod
+    def backward(ctx, g_loss, g_metrics):
+        dmean, dvalue, dls = ctx.saved_tensors
+        g = g_loss.to(dmean.dtype)
+        return dmean * g, dvalue * g, dls * g_loss, None, None, None, None, None, None, None, None
 
 
 def ppo_loss(params, obs, actions, old_logp, adv, ret, cfg: TrainConfig, obs_dim, act_dim):
@@ -315,6 +371,9 @@ class Trainer:
         self.buf = dict(obs=z(T, N, _up8(O)), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
                         terminated=z(T, N, dt=torch.uint8), timed_out=z(T, N, dt=torch.uint8), boot=z(T, N),
                         task_error=z(T, N), adv=z(T, N), ret=z(T, N), last_values=z(N))
+        mb = (T * N + cfg.minibatch_count - 1) // cfg.minibatch_count
+        obs_dt = torch.bfloat16 if cfg.update_precision == "bf16" else torch.float32
+        self.mb_buf = dict(obs=z(mb, _up8(O), dt=obs_dt), act=z(mb, A), logp=z(mb), adv=z(mb), ret=z(mb))
         self.mean = z(N, A)
         self.ep_acc = z(N)
         self.stats = z(4, dt=torch.float64)
@@ -388,16 +447,21 @@ class Trainer:
         obs = b["obs"].view(cap, self.O_pad)
         act = b["actions"].view(cap, self.A)
         logp, adv, ret = b["logp"].view(cap), b["adv"].view(cap), b["ret"].view(cap)
+        g = self.mb_buf
         for e in range(cfg.epochs):
             for start in range(0, cap, mb):
                 idx = perms[e, start: start + mb]
+                m_rows = idx.numel()
+                # one launch gathers the minibatch rows (obs straight to the GEMM dtype)
+                sg.ppo_gather(idx, obs, act, logp, adv, ret, g["obs"][:m_rows], g["act"][:m_rows],
+                              g["logp"][:m_rows], g["adv"][:m_rows], g["ret"][:m_rows])
                 # (self.grad is zero here: initially, and after every fused Adam step)
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
-                    mean, value = mlp_layers(self.layers, obs.index_select(0, idx))
-                    loss, m = loss_head(mean[:, :self.A].float(), value.float(), self.log_std,
-                                        act.index_select(0, idx),
-                                        logp.index_select(0, idx), adv.index_select(0, idx),
-                                        ret.index_select(0, idx), cfg)
+                    mean_f, value_f = mlp_layers(self.layers, g["obs"][:m_rows], device_elu=True, full=True)
+                loss, m = _PPOLossDevice.apply(mean_f.contiguous(), value_f.contiguous(), self.log_std,
+                                               g["act"][:m_rows], g["logp"][:m_rows], g["adv"][:m_rows],
+                                               g["ret"][:m_rows], self.A, cfg.clip_eps, cfg.value_coef,
+                                               cfg.entropy_coef)
                 loss.backward()
                 allreduce_mean_(self.grad, self.dist)
                 self._adam_step()

@@ -140,6 +140,15 @@ _SIGS = {
                                      C.c_char_p, C.c_void_p, C.c_int64]),
     "sg_checkpoint_load": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p,
                                      C.c_int32, C.c_char_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
+    "sg_elu_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
+    "sg_elu_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
+    "sg_ppo_gather": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p]),
+    "sg_ppo_loss": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_double,
+                              C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p]),
     "sg_compute_gae": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -505,6 +514,58 @@ class Policy:
         _pcheck(lib().sg_policy_forward(self._h, obs.data_ptr(), n, obs.stride(0), mean.data_ptr(),
                                         value.data_ptr(), stream))
         return mean, value
+
+
+# -- PPO update kernels (train.cu) ---------------------------------------------
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.bfloat16:
+        return 1
+    if t.dtype == torch.float32:
+        return 0
+    raise SimError(f"unsupported dtype {t.dtype}")
+
+
+def elu_forward(z, out=None):
+    """ELU (policy.cpp:33) on the device kernel; out may alias z."""
+    import torch
+    out = torch.empty_like(z) if out is None else out
+    stream = torch.cuda.current_stream(z.device).cuda_stream
+    _pcheck(lib().sg_elu_forward(z.data_ptr(), out.data_ptr(), z.numel(), _dtype_code(z), stream))
+    return out
+
+
+def elu_backward(h, dh, out=None):
+    """d ELU from the output h: dz = dh * (h > 0 ? 1 : h + 1)."""
+    import torch
+    out = torch.empty_like(h) if out is None else out
+    stream = torch.cuda.current_stream(h.device).cuda_stream
+    _pcheck(lib().sg_elu_backward(h.data_ptr(), dh.data_ptr(), out.data_ptr(), h.numel(), _dtype_code(h), stream))
+    return out
+
+
+def ppo_gather(idx, obs, act, logp, adv, ret, obs_out, act_out, logp_out, adv_out, ret_out):
+    """Minibatch gather (ppo.cpp:173-190) of the rollout buffer in one launch."""
+    import torch
+    stream = torch.cuda.current_stream(obs.device).cuda_stream
+    _pcheck(lib().sg_ppo_gather(idx.data_ptr(), idx.numel(), obs.data_ptr(), obs.shape[1], obs_out.data_ptr(),
+                                1 if obs_out.dtype == torch.bfloat16 else 0, act.data_ptr(), act.shape[1],
+                                act_out.data_ptr(), logp.data_ptr(), logp_out.data_ptr(), adv.data_ptr(),
+                                adv_out.data_ptr(), ret.data_ptr(), ret_out.data_ptr(), stream))
+
+
+def ppo_loss(mean_full, value_full, log_std_raw, act, old_logp, adv, ret, A, clip_eps, value_coef, entropy_coef,
+             ls_min, ls_max, dmean, dvalue, dls, acc, out):
+    """ppo_loss_and_grad's data part (ppo.cpp:90-154) on the fused kernel:
+    out = {loss, policy_loss, value_loss, entropy, kl, clip_fraction};
+    dmean / dvalue / dls the analytic gradients (train.cu sg_ppo_loss)."""
+    import torch
+    stream = torch.cuda.current_stream(mean_full.device).cuda_stream
+    _pcheck(lib().sg_ppo_loss(mean_full.data_ptr(), mean_full.shape[1], value_full.data_ptr(), value_full.shape[1],
+                              _dtype_code(mean_full), log_std_raw.data_ptr(), act.data_ptr(), old_logp.data_ptr(),
+                              adv.data_ptr(), ret.data_ptr(), mean_full.shape[0], A, clip_eps, value_coef,
+                              entropy_coef, ls_min, ls_max, dmean.data_ptr(), dvalue.data_ptr(), dls.data_ptr(),
+                              acc.data_ptr(), out.data_ptr(), stream))
 
 
 # -- checkpoints (save_checkpoint / load_checkpoint, policy.cpp:220-295) -------

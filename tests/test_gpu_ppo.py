@@ -162,3 +162,91 @@ def test_trainer_checkpoint_round_trip(sg, tmp_path):
     pol2.forward(obs, m2, v2)
     torch.cuda.synchronize()
     assert torch.equal(m1, m2) and torch.equal(v1, v2)
+
+
+def test_update_kernels_elu_and_gather(sg):
+    """train.cu: device ELU forward / backward vs torch (fp32: within 2 ulp of
+    expm1; bf16: one rounding of the fp32 result), and the fused minibatch
+    gather vs index_select; the PPO loss gradients with the device ELU path
+    equal the torch-ELU path."""
+    from paper_2310_04676_b200 import ppo
+    g = torch.Generator(device="cuda").manual_seed(0)
+    z = torch.randn(4096, 64, device="cuda", generator=g) * 3
+    h = sg.elu_forward(z)
+    torch.testing.assert_close(h, torch.nn.functional.elu(z), rtol=3e-7, atol=1e-7)
+    dh = torch.randn_like(z)
+    zr = z.clone().requires_grad_(True)
+    torch.nn.functional.elu(zr).backward(dh)
+    torch.testing.assert_close(sg.elu_backward(h, dh), zr.grad, rtol=1e-6, atol=1e-6)
+    zb = z.bfloat16()
+    hb = sg.elu_forward(zb)
+    torch.testing.assert_close(hb.float(), torch.nn.functional.elu(zb.float()).bfloat16().float(), rtol=8e-3,
+                               atol=1e-6)
+    assert sg.elu_forward(zb, out=zb) is zb  # in place
+    # gather
+    cap, O, A, m = 5000, 32, 7, 1200
+    obs, act = torch.randn(cap, O, device="cuda"), torch.randn(cap, A, device="cuda")
+    logp, adv, ret = (torch.randn(cap, device="cuda") for _ in range(3))
+    idx = torch.randperm(cap, device="cuda")[:m]
+    for dt in (torch.float32, torch.bfloat16):
+        out = [torch.empty(m, O, device="cuda", dtype=dt), torch.empty(m, A, device="cuda")] + \
+              [torch.empty(m, device="cuda") for _ in range(3)]
+        sg.ppo_gather(idx, obs, act, logp, adv, ret, *out)
+        assert torch.equal(out[0], obs[idx].to(dt)) and torch.equal(out[1], act[idx])
+        for o, src in zip(out[2:], (logp, adv, ret)):
+            assert torch.equal(o, src[idx])
+    # loss gradients: device-ELU layers == torch-ELU layers (fp32)
+    torch.manual_seed(1)
+    layout, ls_off, total, _ = ppo.padded_layout(27, 7)
+    params = torch.randn(total, device="cuda") * 0.1
+    x = torch.randn(512, 32, device="cuda")
+    grads = []
+    for dev_elu in (False, True):
+        p = params.clone().requires_grad_(True)
+        layers = [(p[w0: w0 + o * i].view(o, i), p[b0: b0 + ob]) for (w0, o, i), (b0, ob) in layout]
+        mean, value = ppo.mlp_layers(layers, x, device_elu=dev_elu)
+        (mean.square().sum() + value.sum()).backward()
+        grads.append(p.grad.clone())
+    torch.testing.assert_close(grads[1], grads[0], rtol=1e-4, atol=1e-5)  # h + 1 vs exp(z), GEMM order
+
+
+def test_fused_ppo_loss_matches_reference_formulas(sg):
+    """sg_ppo_loss (ppo.cpp:90-154 in one kernel) == the autograd loss head
+    (tests/test_ppo_cpu.py pins that one to the reference's analytic
+    gradients): loss, metrics, dmean, dvalue, dlog_std, with clipped ratios,
+    both surrogate branches and a log-std outside the box."""
+    from paper_2310_04676_b200 import ppo
+    g = torch.Generator(device="cuda").manual_seed(5)
+    B, A, P = 3000, 7, 8
+    mean_full = torch.randn(B, P, device="cuda", generator=g) * 0.3
+    value_full = torch.randn(B, P, device="cuda", generator=g)
+    log_std = torch.tensor([-1.0, -0.5, 0.2, -6.0, 2.5, -1.2, 0.0], device="cuda")  # two outside [-5, 2]
+    lsc = log_std.clamp(ppo.LOG_STD_MIN, ppo.LOG_STD_MAX)
+    # actions drawn from the policy (as in a rollout): moderate log-probs
+    act = mean_full[:, :A] + torch.exp(lsc) * torch.randn(B, A, device="cuda", generator=g)
+    logp = (-0.5 * ((act - mean_full[:, :A]) * torch.exp(-lsc)) ** 2 - lsc - ppo.HALF_LOG_2PI).sum(1)
+    old_logp = logp + 0.3 * torch.randn(B, device="cuda", generator=g)  # ratios around 1 +- 30 %
+    adv = torch.randn(B, device="cuda", generator=g)
+    ret = torch.randn(B, device="cuda", generator=g)
+    cfg = ppo.TrainConfig(entropy_coef=0.01)
+    m_ref = mean_full[:, :A].clone().requires_grad_(True)
+    v_ref = value_full[:, 0].clone().requires_grad_(True)
+    ls_ref = log_std.clone().requires_grad_(True)
+    loss_ref, met_ref = ppo.loss_head(m_ref, v_ref, ls_ref, act, old_logp, adv, ret, cfg)
+    loss_ref.backward()
+    mf = mean_full.clone().requires_grad_(True)
+    vf = value_full.clone().requires_grad_(True)
+    ls = log_std.clone().requires_grad_(True)
+    loss, met = ppo._PPOLossDevice.apply(mf, vf, ls, act, old_logp, adv, ret, A, cfg.clip_eps, cfg.value_coef,
+                                         cfg.entropy_coef)
+    loss.backward()
+    assert 0.05 < float(met_ref[4]) < 0.95  # both surrogate branches present
+    torch.testing.assert_close(loss, loss_ref, rtol=1e-4, atol=1e-5)
+    # metrics: kl is a mean of near-cancelling terms, clip_fraction may flip a
+    # sample whose ratio sits on the clip boundary (fp32 exp)
+    torch.testing.assert_close(met, met_ref, rtol=1e-3, atol=1e-3)
+    torch.testing.assert_close(mf.grad[:, :A], m_ref.grad, rtol=1e-4, atol=1e-8)
+    assert (mf.grad[:, A:] == 0).all() and (vf.grad[:, 1:] == 0).all()
+    torch.testing.assert_close(vf.grad[:, 0], v_ref.grad, rtol=1e-5, atol=1e-9)
+    torch.testing.assert_close(ls.grad, ls_ref.grad, rtol=1e-4, atol=1e-6)
+    assert ls.grad[3] == 0 and ls.grad[4] == 0
