@@ -24,12 +24,23 @@ env = sg.VecTaskEnv(robots=('psm',), n_envs=16384); obs = env.reset()
 pol = sg.Policy(27, 7); pol.load_params(torch.from_numpy(pol.init_params(0)).cuda())
 for _ in range(6): pol.forward(obs)
 torch.cuda.synchronize()" > /dev/null 2>&1
+# the section-8f task kernels: multi-tool team kernel, ImageMatching renderer,
+# and the PathFollowing reset-record kernel (STAR)
+timeout 600 $NCU --set full --import-source on -k regex:mt_step_kernel -s 4 -c 1 -o $OUT/mt_step_multitool \
+  python bench.py --config multitool --steps 2000 --fuse 250 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 $NCU --set full --import-source on -k regex:im_step_kernel -s 4 -c 1 -o $OUT/im_step_image \
+  python bench.py --config image --steps 500 --fuse 250 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 $NCU --set full --import-source on -k regex:path_record_kernel -s 2 -c 1 -o $OUT/path_record_star \
+  python bench.py --config star --steps 1000 --fuse 250 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 $NCU --metrics gpu__time_duration.sum --csv --log-file $OUT/launches_ppo.csv \
   python bench.py --config ppo --steps 64 --warmup 3 --no-cpu-baseline > $OUT/launches_ppo.log 2>&1
-for f in env_step_psm env_step_ecm env_step_star policy_fwd; do
+for f in env_step_psm env_step_ecm env_step_star policy_fwd mt_step_multitool im_step_image path_record_star; do
   [ -f $OUT/$f.ncu-rep ] || continue
   ncu -i $OUT/$f.ncu-rep --page details --csv > $OUT/${f}_details.csv 2>/dev/null
   ncu -i $OUT/$f.ncu-rep --page raw --csv > $OUT/${f}_raw.csv 2>/dev/null
-  ncu -i $OUT/$f.ncu-rep --page source --print-source sass --csv > $OUT/${f}_sass.csv 2>/dev/null
+  # SASS page only for the headline kernel (the pages are ~7 MB each and
+  # gpurun copies back at most 64 MiB)
+  [ $f = env_step_psm ] && ncu -i $OUT/$f.ncu-rep --page source --print-source sass --csv > $OUT/${f}_sass.csv 2>/dev/null
 done
+rm -f $OUT/*.ncu-rep
 ls -la $OUT

@@ -108,7 +108,8 @@ def main(src, rnd):
     dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
     summary = {}
-    for f in ("env_step_psm", "env_step_ecm", "env_step_star", "policy_fwd"):
+    for f in ("env_step_psm", "env_step_ecm", "env_step_star", "policy_fwd", "mt_step_multitool", "im_step_image",
+              "path_record_star"):
         d, r = os.path.join(src, f + "_details.csv"), os.path.join(src, f + "_raw.csv")
         if not os.path.exists(d):
             continue
@@ -128,8 +129,8 @@ def main(src, rnd):
             except StopIteration:
                 pass
         summary[f] = ent
-        if f.startswith("env_step_") and "dram_bytes_per_launch" in ent:
-            cfg = f[len("env_step_"):]
+        if f.split("_")[0] in ("env", "mt", "im") and "dram_bytes_per_launch" in ent:
+            cfg = f.split("_")[-1]
             units = {"B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             b = 0.0
             for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
