@@ -338,6 +338,7 @@ template <int DMAX>
 struct GenericChain {
   static constexpr int kDof = DMAX;
   static constexpr bool kExact = false;
+  static constexpr int kTipFlags = -1;  // runtime (RobotTable::tip_flags)
   __device__ static int dof(const RobotTable& R) { return R.dof; }
   __device__ static int jaw(const RobotTable& R) { return R.jaw; }
   __device__ static void fk(const RobotTable& R, const float (&q)[DMAX], float (&tip)[3]) {
@@ -949,6 +950,50 @@ __device__ __forceinline__ void fk_range(const RobotTable& R, const float* q, Xf
   }
 }
 
+// Right-to-left POINT form of fk_walk for a FixedChain joint:
+// v <- o_j + Motion_j(q_j) v (T_j = Trans(o_j) Motion_j; the builtin
+// signatures carry no origin rotation). A revolute joint rotates two
+// coordinates (4 ops), a prismatic one shifts one; no rotation matrix is
+// composed, and the sin/cos of every joint are independent of v.
+template <class CH, int D>
+__device__ __forceinline__ void point_joint(const RobotTable& R, float qv, float s, float c, float (&v)[3]) {
+  constexpr int sig = CH::kSig[D];
+  constexpr int kind = sig & 3, axis = (sig >> 2) & 7, of = (sig >> 5) & 7;
+  static_assert(((sig >> 8) & 1) == 0, "the point form needs identity origin rotations");
+  if constexpr (kind == kRevolute) {
+    const float sn = axis >= 3 ? -s : s;
+    if constexpr (axis % 3 == 2) {  // z
+      const float x = v[0], y = v[1];
+      v[0] = fmaf(c, x, -sn * y);
+      v[1] = fmaf(sn, x, c * y);
+    } else if constexpr (axis % 3 == 0) {  // x
+      const float y = v[1], z = v[2];
+      v[1] = fmaf(c, y, -sn * z);
+      v[2] = fmaf(sn, y, c * z);
+    } else {  // y
+      const float x = v[0], z = v[2];
+      v[0] = fmaf(c, x, sn * z);
+      v[2] = fmaf(-sn, x, c * z);
+    }
+  } else {
+    v[axis % 3] += axis >= 3 ? -qv : qv;
+  }
+  const JointEnc& J = R.j[D];
+  if constexpr ((of & 1) != 0) v[0] += J.o[0];
+  if constexpr ((of & 2) != 0) v[1] += J.o[1];
+  if constexpr ((of & 4) != 0) v[2] += J.o[2];
+}
+
+// v <- T_B ... T_{B+N-1} v (right to left), sin/cos precomputed.
+template <class CH, int B, int N>
+__device__ __forceinline__ void point_range(const RobotTable& R, const float* q, const float* sn, const float* cs,
+                                            float (&v)[3]) {
+  if constexpr (N > 0) {
+    point_joint<CH, B + N - 1>(R, q[N - 1], sn[N - 1], cs[N - 1], v);
+    point_range<CH, B, N - 1>(R, q, sn, cs, v);
+  }
+}
+
 template <class CH>
 __device__ __forceinline__ int tip_flags_of(const RobotTable& R) {
   if constexpr (CH::kExact) return CH::kTipFlags;
@@ -1246,13 +1291,34 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   // matrix-vector products: the last warp publishes v = p + R * tip (3 floats;
   // its final rotation is dead code when the tip offset is zero), middle warps
   // publish (R, p), the scorer applies them to its own transform.
+  // With a non-zero tool-tip offset (ECM, STAR) the last warp of a
+  // FixedChain team (S = G - 1) uses the right-to-left point form: it maps
+  // the tip point through its joints (no rotation matrix composed) and
+  // publishes it; the scorer keeps the left-to-right transform of its own
+  // joints, built before the barrier, and applies it after. With a zero tip
+  // offset (PSM) the left-to-right form already drops the last rotation and
+  // measured faster (tools/ab.sh: ECM 33.9 -> 35.4 G env-steps/s, STAR
+  // unchanged, PSM 23.2 -> 22.2 with the point form).
+  constexpr bool kPoint = CH::kExact && CH::kTipFlags != 0 && G >= 2 && S == G - 1 && Blk::N > 0;
   Xform x;
   const auto publish = [&](int b, float* s_obs) {
+    if constexpr (kPoint) {
+      float psn[NB], pcs[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) __sincosf(q[j], &psn[j], &pcs[j]);
+      float v[3] = {(CH::kTipFlags & 1) ? R.tip[0] : 0.f, (CH::kTipFlags & 2) ? R.tip[1] : 0.f,
+                    (CH::kTipFlags & 4) ? R.tip[2] : 0.f};
+      point_range<CH, B0, Blk::N>(R, q, psn, pcs, v);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ts.xf[b][S][9 + k][lane] = v[k];
+    } else {
 #pragma unroll
     for (int k = 0; k < 9; ++k) x.m[k] = (k % 4 == 0) ? 1.f : 0.f;
     x.p[0] = x.p[1] = x.p[2] = 0.f;
     fk_range<CH, B0>(R, q, x, std::make_integer_sequence<int, Blk::N>{});
-    if (S > 0 && S == G - 1) {
+    }
+    if (kPoint) {
+    } else if (S > 0 && S == G - 1) {
       float v[3];
       fk_tip_offset(R, tip_flags_of<CH>(R), x.m, x.p, v);
 #pragma unroll
