@@ -40,3 +40,19 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_step_bytes_task_configs():
+    """Per-tool state and the ImageMatching target read in the roofline bytes."""
+    mt = bench.step_bytes(20, 78, fused=250, reset_frac=1 / 300, tools=3)
+    assert mt["per_launch"] == 3 * 20 * 4 * 2 + 3 * 3 * 4 * 3 + 32
+    im = bench.step_bytes(7, 2072, fused=250, reset_frac=1 / 300, step_read=4 * 1024)
+    assert im["per_step"] == 28 + 2072 * 4 + 10 + 4096
+
+
+def test_task_reference_arms_run_on_cpu():
+    """The CPU baselines of the section-8f configs (oracle ports of the tasks)."""
+    for name in ("multitool", "image"):
+        cfg = dict(bench.CONFIGS[name], n_envs=64)
+        rate, lanes, sample = bench.cpu_reference(cfg, steps=3, budget_s=0.5)
+        assert rate > 0 and lanes >= 1 and "64 envs" in sample
