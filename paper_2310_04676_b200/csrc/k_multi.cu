@@ -264,6 +264,41 @@ struct ToolWarp {
     }
     if (GEN) act_s = act_s * P.jump_mult + P.jump_add;
     const float dt = P.dt_sub;
+    if (CH::kExact && mode == kModePosition) {
+      // position control on a specialised chain: the PD law with dt / inertia
+      // folded into the gains, read from shared memory once per step (not per
+      // substep): u = clamp(gk qt - gk q - gd qd, +-ge), vv = clamp(gc qd + u,
+      // +-vl) (fp32 rounding differs from the reference's operation order by a
+      // few ulp, as in the single-tool specialised kernels)
+      float gk[kMaxToolDof], gd[kMaxToolDof], gc[kMaxToolDof], ge[kMaxToolDof], vl[kMaxToolDof],
+          lo[kMaxToolDof], hi[kMaxToolDof];
+#pragma unroll
+      for (int d = 0; d < kMaxToolDof; ++d) {
+        gk[d] = gd[d] = gc[d] = ge[d] = vl[d] = lo[d] = hi[d] = 0.f;
+        if (d >= dof) continue;
+        const float dti = R.dt_over_inertia[d];
+        gk[d] = R.kp[d] * dti;
+        gd[d] = R.kd[d] * dti;
+        gc[d] = 1.f - R.damping[d] * dti;
+        ge[d] = R.eff[d] * dti;
+        vl[d] = R.vel[d];
+        lo[d] = R.lo[d];
+        hi[d] = R.hi[d];
+        kpqt[d] = gk[d] * qt[d];
+      }
+      for (int s = 0; s < P.substeps; ++s) {
+#pragma unroll
+        for (int d = 0; d < kMaxToolDof; ++d) {
+          if (d >= dof) continue;
+          const float u = fminf(fmaxf(fmaf(-gd[d], qd[d], fmaf(-gk[d], q[d], kpqt[d])), -ge[d]), ge[d]);
+          const float vv = fminf(fmaxf(fmaf(qd[d], gc[d], u), -vl[d]), vl[d]);
+          const float qq = fmaf(vv, dt, q[d]);
+          const float qc = fminf(fmaxf(qq, lo[d]), hi[d]);  // limit projection
+          qd[d] = qc != qq ? 0.f : vv;
+          q[d] = qc;
+        }
+      }
+    } else
     for (int s = 0; s < P.substeps; ++s) {
 #pragma unroll
       for (int d = 0; d < kMaxToolDof; ++d) {
