@@ -464,6 +464,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, lanes, sample = cpu_reference(cfg, 10_000, budget_s=args.cpu_budget)
         cpu = dict(value=rate, unit="env-steps/s", cores=lanes, kind="port", sample=sample)
+        # HostInfo-style (bench.hpp:41-45): hardware threads, and the same
+        # protocol on one pool lane (all lanes and 1 lane)
+        rate1, _, sample1 = cpu_reference(cfg, 10_000, budget_s=min(5.0, args.cpu_budget), threads=1)
+        cpu.update(hardware_threads=os.cpu_count(), value_1_lane=rate1, sample_1_lane=sample1)
 
     if rank == 0:
         line = dict(
