@@ -47,31 +47,53 @@ union Bf8 {
   __nv_bfloat162 h[4];
 };
 
+// bf16 kernels: kVec independent 16-byte vectors per thread per iteration
+// (loads issued before any use: more bytes in flight per SM)
+constexpr int kVec = 4;
+
 __global__ void elu_fwd_bf16(const uint4* __restrict__ z, uint4* __restrict__ h, int64_t n8) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
-    Bf8 v;
-    v.u = z[k];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < n8; k0 += stride * kVec) {
+    Bf8 v[kVec];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(v.h[j]);
-      v.h[j] = __floats2bfloat162_rn(elu_f(f.x, true), elu_f(f.y, true));
+    for (int u = 0; u < kVec; ++u)
+      if (k0 + u * stride < n8) v[u].u = z[k0 + u * stride];
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      if (k0 + u * stride >= n8) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(v[u].h[j]);
+        v[u].h[j] = __floats2bfloat162_rn(elu_f(f.x, true), elu_f(f.y, true));
+      }
+      h[k0 + u * stride] = v[u].u;
     }
-    h[k] = v.u;
   }
 }
 
 __global__ void elu_bwd_bf16(const uint4* __restrict__ h, const uint4* __restrict__ dh, uint4* __restrict__ dz,
                              int64_t n8) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
-    Bf8 a, g, o;
-    a.u = h[k];
-    g.u = dh[k];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < n8; k0 += stride * kVec) {
+    Bf8 a[kVec], g[kVec];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 fa = __bfloat1622float2(a.h[j]), fg = __bfloat1622float2(g.h[j]);
-      o.h[j] = __floats2bfloat162_rn(fa.x > 0.f ? fg.x : fg.x * (fa.x + 1.f), fa.y > 0.f ? fg.y : fg.y * (fa.y + 1.f));
+    for (int u = 0; u < kVec; ++u)
+      if (k0 + u * stride < n8) {
+        a[u].u = h[k0 + u * stride];
+        g[u].u = dh[k0 + u * stride];
+      }
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      if (k0 + u * stride >= n8) continue;
+      Bf8 o;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 fa = __bfloat1622float2(a[u].h[j]), fg = __bfloat1622float2(g[u].h[j]);
+        o.h[j] = __floats2bfloat162_rn(fa.x > 0.f ? fg.x : fg.x * (fa.x + 1.f),
+                                       fa.y > 0.f ? fg.y : fg.y * (fa.y + 1.f));
+      }
+      dz[k0 + u * stride] = o.u;
     }
-    dz[k] = o.u;
   }
 }
 
@@ -123,7 +145,7 @@ int sg_elu_forward(const void* z, void* h, int64_t count, int32_t dtype, void* s
   const cudaStream_t st = (cudaStream_t)stream;
   if (dtype == 1) {
     if (count % 8) return SG_ERR_CONFIG;
-    elu_fwd_bf16<<<grid_for(count / 8, 256), 256, 0, st>>>((const uint4*)z, (uint4*)h, count / 8);
+    elu_fwd_bf16<<<grid_for((count / 8 + kVec - 1) / kVec, 256), 256, 0, st>>>((const uint4*)z, (uint4*)h, count / 8);
   } else {
     if (count % 4) return SG_ERR_CONFIG;
     elu_fwd_f32<<<grid_for(count / 4, 256), 256, 0, st>>>((const float4*)z, (float4*)h, count / 4);
@@ -135,8 +157,8 @@ int sg_elu_backward(const void* h, const void* dh, void* dz, int64_t count, int3
   const cudaStream_t st = (cudaStream_t)stream;
   if (dtype == 1) {
     if (count % 8) return SG_ERR_CONFIG;
-    elu_bwd_bf16<<<grid_for(count / 8, 256), 256, 0, st>>>((const uint4*)h, (const uint4*)dh, (uint4*)dz,
-                                                            count / 8);
+    elu_bwd_bf16<<<grid_for((count / 8 + kVec - 1) / kVec, 256), 256, 0, st>>>((const uint4*)h, (const uint4*)dh,
+                                                                              (uint4*)dz, count / 8);
   } else {
     if (count % 4) return SG_ERR_CONFIG;
     elu_bwd_f32<<<grid_for(count / 4, 256), 256, 0, st>>>((const float4*)h, (const float4*)dh, (float4*)dz,
