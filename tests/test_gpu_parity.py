@@ -453,3 +453,21 @@ rpy = 0 0 0
     rob = sg.Robot.parse(text)
     pos = rob.fk(torch.from_numpy(qs.astype(np.float32)).cuda()).cpu().numpy()
     assert np.abs(pos - ref).max() < 2e-6
+
+
+def test_cpp_dropin_runs_on_the_device(sg, tmp_path):
+    """examples/bench_sim_cpp.cpp (scalpel_b200::VecTaskEnv, include/sg/env.hpp)
+    runs the reference's bench_sim loop on the device from C++."""
+    _cuda()
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(sg.lib_path())
+    exe = str(tmp_path / "bench_sim_cpp")
+    r = subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "examples", "bench_sim_cpp.cpp"), f"-L{libdir}", "-lsg_env",
+                        f"-Wl,-rpath,{libdir}", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    run = subprocess.run([exe, "1024", "50"], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stdout + run.stderr
+    assert "1024 envs x 50 steps" in run.stdout
