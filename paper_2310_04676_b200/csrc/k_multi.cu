@@ -2,13 +2,15 @@
 // team of T warps per 32 envs, warp t = tool t (lane = env): the tool's joint
 // state (DoF-major SoA in HBM, one 128-byte line per DoF per warp) stays in
 // registers for the whole fused launch, is integrated with the reference's
-// per-DoF PD law (dynamics.cpp:127-185, the same fp32 operation order as the
-// single-tool generic kernel), and the tool FK (robot_model.cpp:371-395) is
-// mapped through the tool's base pose. Warp 0 scores; observation rows are
-// staged in shared memory and stored as one contiguous float4 run per team.
+// per-DoF PD law (dynamics.cpp:127-185; position control on a specialised
+// chain with dt / inertia folded into the gains like the single-tool
+// kernels), and the tool FK (robot_model.cpp:371-395, on the tool's
+// compile-time chain structure when it has one) is mapped through the tool's
+// base pose. Warp 0 scores; observation rows are staged in shared memory and
+// stored as one contiguous float4 run per team. The reset kernel stages one
+// warp's 32 rows per warp (odd row stride Os: conflict-free).
 #include "multi.cuh"
 #include "launch.hpp"
-
 
 namespace sg {
 namespace {
