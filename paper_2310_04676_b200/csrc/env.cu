@@ -602,6 +602,9 @@ std::unique_ptr<sg_env> make_multi_env(const sg_env_config& cfg, const sg_dynami
   }
   for (int k = 0; k < 3; ++k) env->center[k] = env->centers[0][k];
   M.A = A;
+  M.scorer = 0;
+  for (int t = 1; t < T; ++t)  // the least-loaded tool warp also scores
+    if (models[t].dof_count <= models[M.scorer].dof_count) M.scorer = t;
   M.O = 3 * A + 6 * T;  // envs.cpp:166-192
   M.Os = M.O | 1;
   M.episode_len = cfg.episode_len;

@@ -393,7 +393,8 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
     sc = active ? P.step_count[i] : 0;
     hc = active ? P.hold_count[i] : 0;
   };
-  if (warp == 0) load_task();
+  const int scorer = P.scorer;  // the tool warp with the fewest DoFs scores (shortest own step)
+  if (warp == scorer) load_task();
 
   for (int step = 0; step < k_steps; ++step) {
     const int b = step & 1;
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
     }
     __syncthreads();  // B1: every tool published
 
-    if (warp == 0) {  // ---- scoring (envs.cpp:540-593)
+    if (warp == scorer) {  // ---- scoring (envs.cpp:540-593)
       float tw[T][3];
 #pragma unroll
       for (int u = 0; u < T; ++u)
@@ -529,7 +530,8 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
         const int r = __ffs(m) - 1;
         for (int c = threadIdx.x; c < O; c += 32 * T) P.tobs[(row0 + r) * O + c] = s_rows[r * O + c];
       }
-      if (warp == 0) {
+      __syncthreads();  // every terminal row copied before the scorer re-stages the reset rows
+      if (warp == scorer) {
         if ((ended >> lane) & 1) {
           const int e = mt_reset_env<T>(P, i);
           if (e) atomicOr(P.err, e);
@@ -545,7 +547,7 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
       if ((ended >> lane) & 1) TW::load(st, P, E, i, active);
     }
   }
-  if (warp == 0 && active) {
+  if (warp == scorer && active) {
     P.step_count[i] = sc;
     P.hold_count[i] = hc;
   }

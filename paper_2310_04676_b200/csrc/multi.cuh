@@ -33,6 +33,7 @@ struct ToolEnc {
 struct MtParams {
   ToolEnc tool[kMaxTools];
   int32_t T, A, O, Os;  // tools, action dim, obs dim, padded shared-memory row stride (odd)
+  int32_t scorer, pad_s;  // team warp that scores (the tool with the fewest DoFs)
   int32_t episode_len, success_hold, substeps, control_mode;
   int64_t n;
   float rho, success_radius, dt_sub;
