@@ -471,3 +471,14 @@ def test_cpp_dropin_runs_on_the_device(sg, tmp_path):
     run = subprocess.run([exe, "1024", "50"], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
     assert "1024 envs x 50 steps" in run.stdout
+
+
+@pytest.mark.parametrize("robot", ["ecm", "star"])
+def test_active_tracking_specialised_chains(sg, oracle, robot):
+    """ActiveTracking on the ECM / STAR specialised-chain kernels (point-form
+    FK in the last team warp): streams and flags bit-exact, goals within
+    2e-5 m over a reset burst."""
+    sigma = 0.15 if robot == "star" else 0.05
+    env, ref, worst = _run_pair(sg, oracle, robot, oracle.ACTIVE_TRACKING, 64, 310, seed=7, sigma=sigma,
+                                tol=dict(goals=2e-5))
+    assert (ref.counters()["episode_count"] == 1).all()
