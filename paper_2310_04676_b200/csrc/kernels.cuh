@@ -1567,8 +1567,13 @@ __device__ __forceinline__ void team_dispatch(const StepParams& P, int k_steps, 
   ((w == S ? team_run<CH, G, S, TASK, MODE, SUB, GEN>(P, k_steps, s_obs, s_act, ts) : void()), ...);
 }
 
-template <class CH, int G, int TASK, int MODE, int SUB, bool GEN>
-__global__ void __launch_bounds__(32 * G) env_step_kernel(const __grid_constant__ StepParams P, int k_steps) {
+// MINB: CTAs per SM the register budget targets. 1 (no cap: ~156 registers,
+// 6 two-warp teams per SM) unless the launch has more teams than the GPU holds
+// at once; then 8 (128 registers): ECM at 65,536 envs is 2,048 teams, three
+// partial waves at 6 per SM and two at 8 (tools/ab.sh: +6.5 %; the cap costs
+// 8-9 % when every team is resident anyway, PSM / STAR at 16,384 envs).
+template <class CH, int G, int TASK, int MODE, int SUB, bool GEN, int MINB = 1>
+__global__ void __launch_bounds__(32 * G, MINB) env_step_kernel(const __grid_constant__ StepParams P, int k_steps) {
   extern __shared__ __align__(16) float smem[];
   const int A = CH::dof(P.robot);
   const int O = 3 * A + 6;
@@ -1654,6 +1659,32 @@ inline cudaError_t launch_team(const StepParams& P, int k_steps, bool gen, cudaS
       e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, false>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
+  }
+  if constexpr (CH::kExact && G == 2) {
+    // more teams than resident slots at the uncapped register count: the
+    // 8-CTAs-per-SM build (fewer, fuller waves)
+    static int slots = -1;
+    if (slots < 0) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, env_step_kernel<CH, G, TASK, MODE, SUB, true>, 32 * G,
+                                                    sm);
+      slots = sms * per_sm;
+    }
+    if ((int64_t)grid > slots) {
+      if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, true, 8>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, false, 8>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+      }
+      if (gen) env_step_kernel<CH, G, TASK, MODE, SUB, true, 8><<<grid, 32 * G, sm, st>>>(P, k_steps);
+      else env_step_kernel<CH, G, TASK, MODE, SUB, false, 8><<<grid, 32 * G, sm, st>>>(P, k_steps);
+      return cudaGetLastError();
+    }
   }
   if (gen) env_step_kernel<CH, G, TASK, MODE, SUB, true><<<grid, 32 * G, sm, st>>>(P, k_steps);
   else env_step_kernel<CH, G, TASK, MODE, SUB, false><<<grid, 32 * G, sm, st>>>(P, k_steps);
