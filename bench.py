@@ -270,7 +270,10 @@ def bench_ppo(args, cfg, rank, world, local, dist):
             roofline=dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak,
                           traffic=None, peak_kind=pk, kernel="policy_fwd_kernel (tcgen05)",
                           flops_per_env=POLICY_FLOPS_PER_ENV, avg_launch_us=fwd_s * 1e6),
-            cpu_baseline=None, e2e=None, gpu_launches=iters * (tcfg.n_steps * 3 + 2),
+            cpu_baseline=None, e2e=None,
+            # ours per iteration: rollout (policy fwd, sample, env step, bootstrap per step + last fwd), GAE,
+            # per minibatch gather + 6 ELU fwd + 6 ELU bwd + loss (2) + Adam (2), policy repack
+            gpu_launches=iters * (4 * tcfg.n_steps + 1 + 1 + tcfg.epochs * tcfg.minibatch_count * 17 + 1),
             clocks=clk.summary(),
         )
         print(json.dumps(line), flush=True)
