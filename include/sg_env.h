@@ -39,7 +39,7 @@
  * exhaustion). The message is thread-local, read with sg_last_error().
  * Device-detected errors (non-finite action/reward, goal-sampling exhaustion)
  * are latched in a device error word and reported by the next synchronising
- * call (sg_env_step_host, sg_env_synchronize, sg_env_read_*).
+ * call (sg_env_step_host, sg_env_synchronize).
  */
 #ifndef SG_ENV_H
 #define SG_ENV_H
