@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
   const bool active = i < n;
   const int rows = (int)min((int64_t)32, n - row0);
   float* s_obs = smem;              // [2][32][O]
-  float* s_act = smem + 2 * 32 * O;  // [32][A]
+  float* s_act = smem + 2 * 32 * O;  // [2][32][A]: GEN draws by step parity (caller actions: [32][A])
   const bool full = rows == 32;
 
   // one register state per thread; the warp's tool index selects the code
@@ -400,6 +400,9 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
     const int b = step & 1;
     float* s_rows = s_obs + b * 32 * O;
     float* o = s_rows + lane * O;
+    // a warp that finished storing step k-1's action rows may draw step k+1
+    // while another still reads: the GEN draws alternate between two buffers
+    float* sa = GEN ? s_act + b * 32 * A : s_act;
     int sat = 0, bad = 0;
     {
       float tip[3], axis[3];
@@ -407,16 +410,16 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
       // trimanual team share the PSM path)
       switch (E.chain) {
         case kChainPsm:
-          TW::template step<PsmChain>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
+          TW::template step<PsmChain>(st, P, E, warp, sa + lane * A, sa + lane * A, o, sat, bad, tip, axis);
           break;
         case kChainEcm:
-          TW::template step<EcmChain>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
+          TW::template step<EcmChain>(st, P, E, warp, sa + lane * A, sa + lane * A, o, sat, bad, tip, axis);
           break;
         case kChainStar:
-          TW::template step<StarChain>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat, bad, tip, axis);
+          TW::template step<StarChain>(st, P, E, warp, sa + lane * A, sa + lane * A, o, sat, bad, tip, axis);
           break;
         default:
-          TW::template step<GenericChain<kMaxToolDof>>(st, P, E, warp, s_act + lane * A, s_act + lane * A, o, sat,
+          TW::template step<GenericChain<kMaxToolDof>>(st, P, E, warp, sa + lane * A, sa + lane * A, o, sat,
                                                        bad, tip, axis);
       }
 #pragma unroll
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(32 * T) mt_step_kernel(const __grid_constant__
     }
     if (GEN) {
       float* g_act = P.act_buf + row0 * A;
-      for (int k = threadIdx.x; k < rows * A; k += 32 * T) g_act[k] = s_act[k];
+      for (int k = threadIdx.x; k < rows * A; k += 32 * T) g_act[k] = sa[k];
     }
     const unsigned ended = ts.ended[b];
     if (ended) {  // ---- terminal copy, reset_row, re-observe (envs.cpp:604-615)
@@ -593,7 +596,7 @@ cudaError_t launch_t(const MtParams& P, int k_steps, bool gen, bool reset, cudaS
     mt_reset_kernel<T><<<grid, 32 * kMtWarps, sm, st>>>(P);
   } else {
     const unsigned tgrid = (unsigned)((P.n + 31) / 32);
-    const size_t tsm = (size_t)(2 * 32 * P.O + 32 * P.A) * sizeof(float);
+    const size_t tsm = (size_t)(2 * 32 * P.O + 2 * 32 * P.A) * sizeof(float);
     const void* fn = gen ? (const void*)mt_step_kernel<T, true> : (const void*)mt_step_kernel<T, false>;
     if (tsm > 40 * 1024 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm)) !=
                                cudaSuccess)
