@@ -45,6 +45,9 @@ CONFIGS = {
     "image": dict(robot="psm", task="image_matching", n_envs=16384, goal_sigma=0.05,
                   workload="PSM ImageMatching (32x32 camera render per env-step), 16384 envs/GPU, random actions "
                            "(SURVEY 8f rank 4; not a BASELINE config)"),
+    "policy": dict(robot="psm", task="target_reaching", n_envs=16384, goal_sigma=0.05,
+                   workload="random-init-policy rollout on PSM reach, 16384 envs/GPU: tcgen05 policy forward + "
+                            "Gaussian sampling + env step per step, no update (north_star; ppo.cpp:258-313)"),
     "ppo": dict(robot="psm", task="target_reaching", n_envs=16384, goal_sigma=0.05,
                 workload="full PPO rollout+update on PSM reach, 16384 envs/GPU, n_steps 32, 5 epochs x 4 "
                          "minibatches, 256/128/64 ELU MLP (BASELINE configs[4])"),
@@ -196,6 +199,220 @@ def cpu_reference_multi(O, cfg: dict, steps: int, budget_s: float, threads: int 
     return n * done / dt, lanes, sample
 
 
+def _np_policy(O: int, A: int, seed: int = 0):
+    """Random-init fp64 MLP weights for the CPU rollout baseline with the
+    reference's init law (policy.cpp:87-102: N(0, 2/fan_in), last layer x0.01,
+    zero biases; drawn with numpy here -- the values do not change the cost)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    dims = [O, 256, 128, 64]
+    trunks = []
+    for out_last in (A, 1):
+        layers = []
+        for l in range(4):
+            i, o = dims[l], (dims[l + 1] if l < 3 else out_last)
+            W = rng.normal(0.0, (2.0 / i) ** 0.5, size=(o, i)) * (0.01 if l == 3 else 1.0)
+            layers.append((W, np.zeros(o)))
+        trunks.append(layers)
+    return trunks
+
+
+def _np_forward(trunks, x):
+    """Policy::forward / trunk_forward (policy.cpp:110-161): x W^T + b, ELU
+    (expm1, policy.cpp:33) on the hidden layers, fp64. Runs on torch's CPU
+    kernels (multithreaded BLAS GEMM + vectorised ELU over all host threads)
+    as the stand-in for the reference's Eigen GEMMs on its thread pool."""
+    import torch
+    h0 = torch.from_numpy(x)
+    outs = []
+    for layers in trunks:
+        h = h0
+        for l, (W, b) in enumerate(layers):
+            h = torch.addmm(torch.from_numpy(b), h, torch.from_numpy(W).t())
+            if l < 3:
+                h = torch.nn.functional.elu(h)
+        outs.append(h.numpy())
+    return outs[0], outs[1][:, 0]
+
+
+def cpu_policy_reference(cfg: dict, steps: int, budget_s: float, threads: int = 0):
+    """The reference's rollout step on the host cores (ppo.cpp:258-313 without
+    the update): Policy::forward in fp64, one serial trainer stream for the
+    Gaussian noise (make_stream(seed, 0x7261696e)), log-probs, env step on the
+    oracle's pool, bootstrap forward of the timed-out rows. Returns
+    (env-steps/s, lanes, sample description)."""
+    import numpy as np
+    from oracle import oracle as O
+    O.build()
+    m = O.resolve_robot(cfg["robot"])
+    n = cfg["n_envs"]
+    lanes = threads or os.cpu_count() or 1
+    import torch
+    torch.set_num_threads(lanes)
+    e = O.Env(O.env_config(n_envs=n, seed=0, goal_sigma=cfg["goal_sigma"]), m, threads=lanes)
+    obs = e.reset()
+    A, Od = m.dof, obs.shape[1]
+    trunks = _np_policy(Od, A)
+    log_std = np.full(A, -1.0)
+    sigma = np.exp(log_std)
+    rs = O.make_stream(0, 0x7261696E)
+    half_log_2pi = 0.9189385332046727
+
+    def one_step(obs):
+        mean, value = _np_forward(trunks, obs)
+        z = O.fill_normals(rs, n, A)
+        act = mean + sigma * z
+        logp = (-0.5 * z * z - log_std - half_log_2pi).sum(1)
+        e.step(act)
+        r = e.result()
+        boot = r["timed_out"].astype(bool) & ~r["terminated"].astype(bool)
+        if boot.any():
+            _np_forward(trunks, e.obs()[1][boot])
+        return e.obs()[0], logp, value
+
+    obs = one_step(obs)[0]  # warm-up step (timing starts after the first step)
+    done, t0 = 0, time.perf_counter()
+    while done < steps and time.perf_counter() - t0 < budget_s:
+        obs = one_step(obs)[0]
+        done += 1
+    dt = time.perf_counter() - t0
+    sample = (f"{n} envs x {done} rollout steps after a warm-up step (fp64 Policy::forward on torch CPU kernels, "
+              f"serial trainer-stream noise, oracle env step on {lanes} pool lanes, bootstrap forward)")
+    return n * done / dt, lanes, sample
+
+
+def bench_policy(args, cfg, rank, world, local, dist):
+    """north_star's random-init-policy workload: rollout-only env-steps/s with
+    the tcgen05 policy in the loop (ppo.cpp:258-313: policy forward -> Gaussian
+    sample on the trainer stream -> env step -> rollout buffer + timeout
+    bootstrap), no PPO update. Whole 32-step rollouts (one CUDA-graph replay
+    each) are timed with CUDA events, L2 flushed before each, gated like the
+    env bench; max over ranks."""
+    import torch
+    from paper_2310_04676_b200 import ppo, sg
+    n = cfg["n_envs"]
+    dev = f"cuda:{local}"
+    plan = shard_plan(rank, world, n)
+    env = sg.VecTaskEnv(robots=(cfg["robot"],), device=local, n_envs=n, seed=0, task=cfg["task"],
+                        goal_sigma=cfg["goal_sigma"], row_offset=plan["row_offset"])
+    pol = sg.Policy(env.obs_dim, env.action_dim, device=local)
+    tcfg = ppo.TrainConfig(seed=0)
+    tr = ppo.Trainer(env, pol, tcfg, dist=dist)
+    T = tcfg.n_steps
+    rollouts = max(1, -(-args.steps // T))
+    for _ in range(max(2, -(-args.warmup // T))):  # the 2nd rollout captures the graph the timed ones replay
+        tr.rollout()
+    torch.cuda.synchronize()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    class _Roll:
+        def bench_step(self, k):
+            tr.rollout()
+
+    runs = max(1, args.runs)
+    with Clocks(local) as clk:
+        res = timed_runs(_Roll(), [T] * rollouts, flush, runs, not args.no_gate, dist, dev)
+    tr.env.synchronize()
+    t_runs = [r["t_ms"] for r in res]
+    t_ms = statistics.mean(t_runs)
+    steps = rollouts * T
+    value = world * n * steps / (t_ms * 1e-3)
+    vals = [world * n * steps / (t * 1e-3) for t in t_runs]
+
+    # dominant tensor-core kernel: policy_fwd on the env's observation rows,
+    # CUDA events on the launching stream
+    obs = env._result().observations
+    mean = torch.empty(n, env.action_dim, device=dev)
+    val = torch.empty(n, device=dev)
+    for _ in range(5):
+        pol.forward(obs, mean, val)
+    reps = 200
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        pol.forward(obs, mean, val)
+    e1.record()
+    torch.cuda.synchronize()
+    fwd_s = e0.elapsed_time(e1) * 1e-3 / reps
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        pk = "measured burst"
+    except Exception:
+        peak, pk = 1590.0, "fallback"
+    achieved = n * POLICY_FLOPS_PER_ENV / fwd_s / 1e12
+
+    # e2e: the same rollout through the public per-call API (3 C-ABI calls per
+    # step: policy forward, sample, env step) with the step's result read back
+    # to pinned host memory every step (observations, rewards, flags: what the
+    # reference's host trainer loop consumes), synchronised per step
+    e2e = None
+    E = min(args.e2e_steps or steps, 2000)
+    if E > 0:
+        h_obs = torch.empty((n, env.obs_dim), dtype=torch.float32).pin_memory()
+        h_rew = torch.empty(n, dtype=torch.float32).pin_memory()
+        h_flags = torch.empty((2, n), dtype=torch.uint8).pin_memory()
+        acts = torch.empty(n, env.action_dim, device=dev)
+        logp = torch.empty(n, device=dev)
+        L = sg.lib()
+        st = torch.cuda.current_stream().cuda_stream
+        d_pos = torch.zeros(1, dtype=torch.int64, device=dev)
+        ls = tr.log_std_c
+        o = env._result().observations
+
+        def host_step(o):
+            pol.forward(o, mean, val)
+            sg._pcheck(L.sg_policy_sample(mean.data_ptr(), n, env.action_dim, ls.data_ptr(), tr.stream_state,
+                                          tr.stream_inc, d_pos.data_ptr(), 0, acts.data_ptr(), logp.data_ptr(), st))
+            r = env.step(acts)
+            h_obs.copy_(r.observations, non_blocking=True)
+            h_rew.copy_(r.rewards, non_blocking=True)
+            h_flags[0].copy_(r.terminated, non_blocking=True)
+            h_flags[1].copy_(r.timed_out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return r.observations
+
+        o = host_step(o)
+        if dist:
+            dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(E):
+            o = host_step(o)
+        a1.record()
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(a0.elapsed_time(a1), dist, dev)
+        e2e = dict(value=world * n * E / (e_ms * 1e-3), unit="env-steps/s", h2d_bytes_per_step=0,
+                   d2h_bytes_per_step=n * (env.obs_dim * 4 + 4 + 2), steps=E,
+                   path="sg_policy_forward + sg_policy_sample + sg_env_step per step, observations / rewards / "
+                        "flags copied to pinned host buffers and synchronised every step (no host inputs: the "
+                        "actions are the policy's)")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, lanes, sample = cpu_policy_reference(cfg, 10_000, budget_s=args.cpu_budget)
+        cpu = dict(value=rate, unit="env-steps/s", cores=lanes, kind="port", sample=sample)
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit="env-steps/s (random-init policy rollout)", n_gpus=world, steps=steps,
+            warmup=args.warmup, ms_per_step=t_ms / steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+            dtype="bf16 policy fwd / fp32 env", data="synthetic",
+            config=dict(workload=cfg["workload"], n_envs_per_gpu=n, global_envs=world * n, rollouts=rollouts,
+                        rollout_steps=T, parallelism=f"env-shard x{world}",
+                        l2="256 MiB flush before every timed rollout"),
+            runs=dict(n=runs, value_mean=statistics.mean(vals), value_std=statistics.pstdev(vals),
+                      gate_held=[r["gate_held"] for r in res]),
+            roofline=dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak,
+                          traffic=None, peak_kind=pk, kernel="policy_fwd_kernel (tcgen05)",
+                          flops_per_env=POLICY_FLOPS_PER_ENV, avg_launch_us=fwd_s * 1e6),
+            cpu_baseline=cpu, e2e=e2e,
+            # per rollout step: policy fwd, sample, env step, bootstrap; + the last-value fwd per rollout
+            gpu_launches=runs * rollouts * (4 * T + 1),
+            clocks=clk.summary(),
+        )
+        print(json.dumps(line), flush=True)
+
+
 def bench_ppo(args, cfg, rank, world, local, dist):
     """Config 5: env-steps/s with learning (bench_learning, bench.cpp:137-174):
     whole trainer iterations (rollout of n_steps x N env steps with the tcgen05
@@ -279,17 +496,123 @@ def bench_ppo(args, cfg, rank, world, local, dist):
         print(json.dumps(line), flush=True)
 
 
+def contract_bytes(A: int, O: int, tools: int = 1, step_read: int = 0) -> int:
+    """SURVEY.md 8(d) algorithmic bytes per env-step (the fp32 SoA per-call step
+    contract): read actions 4A + q, qdot 8A + goal 12 per tool + counters 16;
+    write q, qdot, q_target 12A + observation row 4O + reward, task_error 8 +
+    two flags 2. PSM 314 B, ECM 278 B, STAR 350 B. `step_read`: per-step task
+    inputs beyond that (the ImageMatching target image)."""
+    return 24 * A + 4 * O + 12 * tools + 26 + step_read
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks on this node the
+    way the driver does (torch.distributed.run, 127.0.0.1 rendezvous, NCCL
+    comm-init logging on) and return their exit code."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def init_dist(world: int, local: int, backend: str | None = None):
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    if backend is None:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        dist.init_process_group("gloo")
+    return dist
+
+
+def dry_run(args, cfg, rank, world, local) -> None:
+    """The N-rank plumbing without a GPU (CPU tests): process group, shard
+    plan, gathered plans and the max-over-ranks reduction of a per-rank time."""
+    dist = init_dist(world, local, backend="gloo")
+    plan = shard_plan(rank, world, cfg["n_envs"])
+    plans = [plan]
+    if dist:
+        plans = [None] * world
+        dist.all_gather_object(plans, plan)
+    t = max_over_ranks(1.0 + rank, dist, "cpu")
+    if rank == 0:
+        print(json.dumps(dict(dry_run=True, n_gpus=world, plans=plans, max_time=t, backend="gloo" if dist else None)),
+              flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def gate_cycles(n_launches: int) -> int:
+    """Length of the device-side gate: long enough for the host to enqueue every
+    flush / event / launch of one timed run behind it (~150 us each, generous)."""
+    return int((2000 + 150 * n_launches) * 1e-6 * 2.0e9)
+
+
+def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, extra=None):
+    """`runs` independent timed runs of the same launch sequence. Each run is
+    bracketed by barrier + synchronize; every launch is preceded by an L2
+    flush (256 MiB write) and timed by CUDA events on the env's stream (the
+    current stream). With `gate`, a spin kernel (torch.cuda._sleep) heads the
+    run so the host has enqueued the whole sequence before the GPU reaches the
+    first event: the events then see only device time, never host-enqueue
+    latency (with one launch per run there is nothing else to hide it).
+    Returns per run: summed launch ms (max over ranks), per-launch ms, and
+    whether the gate was still closed when enqueueing finished."""
+    import torch
+    out = []
+    for _ in range(runs):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        g = None
+        if gate:
+            torch.cuda._sleep(gate_cycles(len(launches)))
+            g = torch.cuda.Event()
+            g.record()
+        for (e0, e1), kf in zip(ev, launches):
+            flush.zero_()
+            e0.record()
+            env.bench_step(kf)
+            e1.record()
+        held = (not g.query()) if g is not None else None
+        torch.cuda.synchronize()
+        ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+        t = max_over_ranks(sum(ms), dist, device)
+        if dist:
+            dist.barrier()
+        out.append(dict(t_ms=t, launch_ms=ms, gate_held=held))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=None, help="timed env steps (default 64000; ppo: 320)")
+    ap.add_argument("--steps", type=int, default=None, help="timed env steps per run (default 64000; ppo: 320)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="psm", choices=sorted(CONFIGS))
     ap.add_argument("--fuse", type=int, default=250, help="steps per fused launch")
-    ap.add_argument("--e2e-steps", type=int, default=400)
+    ap.add_argument("--runs", type=int, default=5, help="independent timed runs of --steps steps (mean +- std)")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="enqueue the timed launches without the device-side gate (round-1 protocol; "
+                         "host-enqueue latency lands inside the events)")
+    ap.add_argument("--e2e-steps", type=int, default=None, help="host-API steps (default: --steps, <= 4000)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (CPU, gloo)")
     ap.add_argument("--envs", type=int, default=None,
                     help="override envs per GPU (scaling studies; the headline uses the BASELINE config)")
     ap.add_argument("--update-precision", default="bf16", choices=["fp32", "tf32", "bf16"])
@@ -301,40 +624,70 @@ def main():
     if args.steps is None:
         args.steps = 320 if args.config == "ppo" else 64000
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
+    if args.dry_run:
+        dry_run(args, cfg, rank, world, local)
+        return
 
     if args.impl == "reference":
         if rank != 0:
             return
         total = max(args.steps, 3)
-        rate, lanes, sample = cpu_reference(cfg, total, budget_s=120.0)
+        if args.config == "policy":
+            rate, lanes, sample = cpu_policy_reference(cfg, total, budget_s=120.0)
+        else:
+            rate, lanes, sample = cpu_reference(cfg, total, budget_s=120.0)
         line = dict(metric=METRIC, value=rate, unit="env-steps/s", n_gpus=args.gpus, steps=args.steps,
                     warmup=args.warmup, ms_per_step=1e3 * cfg["n_envs"] / rate, higher_is_better=True,
                     scaling="weak", vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
-                    config=dict(workload=cfg["workload"], n_envs=cfg["n_envs"]),
+                    config=dict(workload=cfg["workload"], n_envs_per_gpu=cfg["n_envs"]),
                     cpu_baseline=dict(value=rate, unit="env-steps/s", cores=lanes, kind="port", sample=sample),
                     e2e=dict(value=rate, unit="env-steps/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
         print(json.dumps(line), flush=True)
         return
 
-    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = init_dist(world, local, backend="nccl")
+    try:
+        if args.config == "ppo":
+            bench_ppo(args, cfg, rank, world, local, dist)
+        elif args.config == "policy":
+            bench_policy(args, cfg, rank, world, local, dist)
+        else:
+            bench_env(args, cfg, rank, world, local, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+def load_profile_counters(config: str, fused: int) -> dict:
+    """ncu numbers of the dominant kernel at THIS run's fused-step count
+    (profiles/r2/traffic_<config>_k<F>.json, written by tools/profile_r2.sh
+    from one `ncu --set full` capture): DRAM and L2 bytes per launch and the
+    issue-slot utilisation."""
+    p = os.path.join(ROOT, "profiles", "r2", f"traffic_{config}_k{fused}.json")
+    if not os.path.exists(p):
+        return {}
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def bench_env(args, cfg, rank, world, local, dist):
     import torch
     from paper_2310_04676_b200 import sg
 
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    if args.config == "ppo":
-        bench_ppo(args, cfg, rank, world, local, dist)
-        if dist:
-            dist.destroy_process_group()
-        return
-
     n = cfg["n_envs"]
+    dev = f"cuda:{local}"
     plan = shard_plan(rank, world, n)
     robots = cfg.get("robots", (cfg.get("robot"),))
     env = sg.VecTaskEnv(robots=robots, device=local, n_envs=n, seed=0, task=cfg["task"],
@@ -343,96 +696,49 @@ def main():
     env.reset()
     env.bench_begin(0, first_step=0, global_n_envs=plan["global_n_envs"])
     F = max(1, min(args.fuse, args.steps))
-    # warm-up: W untimed steps (first is the bench_sim warm-up step), plus one
+    # warm-up: W untimed steps (the first is bench_sim's warm-up step), plus one
     # untimed fused launch so the timed launches see a warm instruction cache
+    torch.cuda.nvtx.range_push("warmup")
     for _ in range(max(args.warmup, 1)):
         env.bench_step(1)
     env.bench_step(F)
+    torch.cuda.nvtx.range_pop()
     steps_done = max(args.warmup, 1) + F
     torch.cuda.synchronize()
 
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     launches = []
     k = args.steps
     while k > 0:
         launches.append(min(F, k))
         k -= launches[-1]
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
+    runs = max(1, args.runs)
     with Clocks(local) as clk:
-        for (e0, e1), kf in zip(ev, launches):
-            flush.zero_()
-            e0.record()
-            env.bench_step(kf)
-            e1.record()
-        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("timed")
+        res = timed_runs(env, launches, flush, runs, not args.no_gate, dist, dev)
+        torch.cuda.nvtx.range_pop()
     env.synchronize()
-    steps_done += args.steps
-    launch_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
-    t_ms = sum(launch_ms)
-    t_ms = max_over_ranks(t_ms, dist, f"cuda:{local}")
-    if dist:
-        dist.barrier()
+    steps_done += runs * args.steps
+    t_runs = [r["t_ms"] for r in res]
+    t_ms = statistics.mean(t_runs)
     value = world * n * args.steps / (t_ms * 1e-3)
+    vals = [world * n * args.steps / (t * 1e-3) for t in t_runs]
 
-    # ---- roofline of the dominant kernel (env_step_kernel, fused bench variant)
-    resets = (steps_done // 300) - ((steps_done - args.steps) // 300)
-    # ImageMatching reads the env's target image every step (reward + observation copy)
+    # ---- roofline of the dominant kernel (SURVEY 8(d) per-call contract bytes)
     wh = (O - 3 * A - 3) // 2 if cfg["task"] == "image_matching" else 0
-    b = step_bytes(A, O, F, resets / max(args.steps, 1), tools=len(robots), step_read=4 * wh)
-    full = [ms for ms, kf in zip(launch_ms, launches) if kf == F]
-    avg_launch_s = (sum(full) / len(full)) * 1e-3 if full else t_ms * 1e-3 / len(launches)
+    cb = contract_bytes(A, O, tools=len(robots), step_read=4 * wh)
+    full = [ms for r in res for ms, kf in zip(r["launch_ms"], launches) if kf == F]
+    avg_launch_s = (sum(full) / len(full)) * 1e-3
     peak, peak_kind = peaks()
-    achieved = n * b["per_env_launch"] / avg_launch_s / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    achieved = n * F * cb / avg_launch_s / 1e9
+    # the same launch with state read / written once per launch (fused amortised bytes)
+    resets = (steps_done // 300) - ((steps_done - runs * args.steps) // 300)
+    b = step_bytes(A, O, F, resets / max(runs * args.steps, 1), tools=len(robots), step_read=4 * wh)
+    prof = load_profile_counters(args.config, F)
 
     # ---- e2e through the host C-ABI call (pinned host buffers) --------------
-    e2e = None
-    if args.e2e_steps > 0:
-        E = args.e2e_steps
-        h_act = torch.empty((E, n, A), dtype=torch.float32).pin_memory()
-        for s in range(E):  # pre-generate the bench stream (device generator), outside timing
-            env.bench_step(1)
-            h_act[s].copy_(env.bench_actions())
-        outs = {k2: torch.empty(shape, dtype=dt).pin_memory() for k2, shape, dt in (
-            ("observations", (n, O), torch.float32), ("terminal_observations", (n, O), torch.float32),
-            ("rewards", (n,), torch.float32), ("task_error", (n,), torch.float32),
-            ("terminated", (n,), torch.uint8), ("timed_out", (n,), torch.uint8))}
-        hr = sg.HostResult()
-        for k2, t in outs.items():
-            setattr(hr, k2, t.data_ptr())
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # the timed region spans a synchronized reset burst (every 300 steps),
-        # so the conditional terminal-observation copy is exercised
-        for s in range(E):
-            env.step_host_ptr(h_act[s].data_ptr(), hr)
-            if s == 0:
-                ended0 = env.host_counters()[0]
-                e0.record()
-        e1.record()
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1)
-        E -= 1
-        burst_steps = -(-(env.host_counters()[0] - ended0) // n)
-        e2e_ms = max_over_ranks(e2e_ms, dist, f"cuda:{local}")
-        tobs_b = outs["terminal_observations"].numel() * 4
-        d2h = sum(t.numel() * t.element_size() for k2, t in outs.items() if k2 != "terminal_observations") + 16
-        d2h += tobs_b * burst_steps / max(E, 1)
-        e2e = dict(value=world * n * E / (e2e_ms * 1e-3), unit="env-steps/s", h2d_bytes_per_step=n * A * 4,
-                   d2h_bytes_per_step=d2h, steps=E, reset_burst_steps=burst_steps,
-                   path="sg_env_step_host (C-ABI), 1 launch/step; terminal observations copied on steps "
-                        "where rows ended")
+    E = min(args.e2e_steps or args.steps, 4000)
+    e2e = bench_e2e(env, E, n, A, O, dist, dev, world, torch, sg) if E > 0 else None
 
     # ---- per-step API in a CUDA graph (1 launch per step, no fusion) --------
     single = None
@@ -468,30 +774,86 @@ def main():
         rate, lanes, sample = cpu_reference(cfg, 10_000, budget_s=args.cpu_budget)
         cpu = dict(value=rate, unit="env-steps/s", cores=lanes, kind="port", sample=sample)
         # HostInfo-style (bench.hpp:41-45): hardware threads, and the same
-        # protocol on one pool lane (all lanes and 1 lane)
+        # protocol on one pool lane and at config 1's 64 envs
         rate1, _, sample1 = cpu_reference(cfg, 10_000, budget_s=min(5.0, args.cpu_budget), threads=1)
         cpu.update(hardware_threads=os.cpu_count(), value_1_lane=rate1, sample_1_lane=sample1)
+        rate64, l64, sample64 = cpu_reference(dict(cfg, n_envs=64), 100_000, budget_s=min(3.0, args.cpu_budget))
+        cpu.update(value_64_envs=rate64, sample_64_envs=sample64)
 
+    kname = (f"mt_step_kernel<T={len(robots)}, GEN>" if len(robots) > 1 else
+             f"im_step_kernel<{cfg['robot'].upper()} chain, GEN>" if wh else
+             f"env_step_kernel<{cfg['robot'].upper()} chain, 2 team warps, GEN>")
     if rank == 0:
+        roof = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+                    traffic=prof.get("dram_bytes_per_launch"), peak_kind=peak_kind,
+                    kernel=f"{kname} ({F} fused steps/launch)", bytes_per_env_step=cb,
+                    bytes_per_env_step_source="SURVEY.md 8(d) per-call step contract (24A + 4O + 12 + 26)",
+                    bytes_per_launch=n * F * cb, avg_launch_us=avg_launch_s * 1e6,
+                    fused_amortised=dict(bytes_per_env_step=b["per_env_step"],
+                                         frac=n * b["per_env_launch"] / avg_launch_s / 1e9 / peak,
+                                         note="state read/written once per fused launch"),
+                    l2_bytes_per_launch=prof.get("lts_bytes_per_launch"),
+                    issue_active_pct=prof.get("issue_active_pct"),
+                    profile=prof.get("source"))
         line = dict(
             metric=METRIC, value=value, unit="env-steps/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
             ms_per_step=t_ms / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
             dtype="fp32", data="synthetic",
             config=dict(workload=cfg["workload"], n_envs_per_gpu=n, global_envs=world * n,
                         fused_steps_per_launch=F, parallelism=f"env-shard x{world}",
-                        l2="256 MiB flush between timed launches; per-launch state read cold from HBM"),
-            roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                          traffic=traffic, peak_kind=peak_kind, kernel=(f"mt_step_kernel<T={len(robots)}, GEN> ({F} fused steps/launch)" if len(robots) > 1 else
-                                  f"im_step_kernel<{cfg['robot'].upper()} chain, GEN> ({F} fused steps/launch)" if wh else
-                                  f"env_step_kernel<{cfg['robot'].upper()} chain, 2 team warps, GEN> ({F} fused steps/launch)"),
-                          bytes_per_env_step=b["per_env_step"], bytes_per_launch=n * b["per_env_launch"],
-                          avg_launch_us=avg_launch_s * 1e6),
-            cpu_baseline=cpu, e2e=e2e, single_step_launches=single,
-            gpu_launches=len(launches), clocks=clk.summary(),
+                        l2="256 MiB flush before every timed launch; per-launch state read cold from HBM",
+                        timing=("device-gated: a spin kernel heads each run so every launch is enqueued "
+                                "before the GPU reaches it" if not args.no_gate else "host-enqueued (no gate)")),
+            runs=dict(n=runs, value_mean=statistics.mean(vals), value_std=statistics.pstdev(vals),
+                      ms_per_step_mean=t_ms / args.steps,
+                      ms_per_step_std=statistics.pstdev([t / args.steps for t in t_runs]),
+                      gate_held=[r["gate_held"] for r in res]),
+            roofline=roof, cpu_baseline=cpu, e2e=e2e, single_step_launches=single,
+            gpu_launches=runs * len(launches) * (2 if cfg["task"] == "path_following" and F > 1 else 1),
+            clocks=clk.summary(),
         )
         print(json.dumps(line), flush=True)
+
+
+def bench_e2e(env, E, n, A, O, dist, dev, world, torch, sg):
+    """`E` steps through the host C-ABI call sg_env_step_host: per step the
+    action rows come from pinned host memory and the full StepResult goes back
+    to pinned host buffers (terminal rows on steps where envs ended). Actions
+    are the bench stream, pre-generated into a ring of up to 300 steps."""
+    ring = min(E + 1, 300)
+    h_act = torch.empty((ring, n, A), dtype=torch.float32).pin_memory()
+    for s in range(ring):  # pre-generate the bench stream (device generator), outside timing
+        env.bench_step(1)
+        h_act[s].copy_(env.bench_actions())
+    outs = {k2: torch.empty(shape, dtype=dt).pin_memory() for k2, shape, dt in (
+        ("observations", (n, O), torch.float32), ("terminal_observations", (n, O), torch.float32),
+        ("rewards", (n,), torch.float32), ("task_error", (n,), torch.float32),
+        ("terminated", (n,), torch.uint8), ("timed_out", (n,), torch.uint8))}
+    hr = sg.HostResult()
+    for k2, t in outs.items():
+        setattr(hr, k2, t.data_ptr())
+    torch.cuda.synchronize()
     if dist:
-        dist.destroy_process_group()
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("e2e")
+    env.step_host_ptr(h_act[0].data_ptr(), hr)  # untimed first host step
+    ended0 = env.host_counters()[0]
+    e0.record()
+    for s in range(E):
+        env.step_host_ptr(h_act[(s + 1) % ring].data_ptr(), hr)
+    e1.record()
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), dist, dev)
+    burst_steps = -(-(env.host_counters()[0] - ended0) // n)
+    tobs_b = outs["terminal_observations"].numel() * 4
+    d2h = sum(t.numel() * t.element_size() for k2, t in outs.items() if k2 != "terminal_observations") + 16
+    d2h += tobs_b * burst_steps / max(E, 1)
+    return dict(value=world * n * E / (e2e_ms * 1e-3), unit="env-steps/s", h2d_bytes_per_step=n * A * 4,
+                d2h_bytes_per_step=d2h, steps=E, reset_burst_steps=burst_steps,
+                path="sg_env_step_host (C-ABI), 1 launch + 1 synchronisation per step; terminal observations "
+                     "copied on steps where rows ended")
 
 
 if __name__ == "__main__":

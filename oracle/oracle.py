@@ -132,6 +132,7 @@ def _load(precision: str) -> C.CDLL:
         "sgo_pcg32_normal": (C.c_double, [_P(Pcg32)]),
         "sgo_make_stream": (None, [C.c_uint64, C.c_uint64, _P(Pcg32)]),
         "sgo_fill_uniform_actions": (None, [_P(Pcg32), _d, C.c_int64]),
+        "sgo_fill_normals": (None, [_P(Pcg32), _d, C.c_int64]),
         "sgo_parse_robot": (C.c_int, [C.c_char_p, C.c_char_p, _P(Robot), C.c_char_p, C.c_int]),
         "sgo_jaw_dof": (C.c_int, [_P(Robot)]),
         "sgo_fk": (None, [_P(Robot), _d, _d, _d]),
@@ -224,6 +225,13 @@ def uniform(r: Pcg32, lo: float, hi: float) -> float:
 
 def normal(r: Pcg32) -> float:
     return lib().sgo_pcg32_normal(C.byref(r))
+
+
+def fill_normals(r: Pcg32, n: int, a: int) -> np.ndarray:
+    """n x a standard normals from one serial stream, row-major (ppo.cpp:264-270)."""
+    out = np.empty((n, a), dtype=np.float64)
+    lib().sgo_fill_normals(C.byref(r), _ptr(out), out.size)
+    return out
 
 
 def fill_uniform_actions(r: Pcg32, n: int, a: int) -> np.ndarray:

@@ -91,6 +91,11 @@ void sgo_fill_uniform_actions(sgo_pcg32* r, double* a, int64_t count) { /* bench
   for (int64_t k = 0; k < count; ++k) a[k] = sgo_pcg32_uniform(r, -1.0, 1.0);
 }
 
+/* the trainer's per-step noise: one serial stream, row-major (ppo.cpp:264-270) */
+void sgo_fill_normals(sgo_pcg32* r, double* z, int64_t count) {
+  for (int64_t k = 0; k < count; ++k) z[k] = sgo_pcg32_normal(r);
+}
+
 /* ======================================================================
  * Quaternion / vector helpers with Eigen semantics (geometry.hpp:25-49)
  * ====================================================================== */

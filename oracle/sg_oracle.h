@@ -36,6 +36,7 @@ double sgo_pcg32_normal(sgo_pcg32* r);
 void sgo_make_stream(uint64_t seed, uint64_t stream_id, sgo_pcg32* out);
 /* bench.cpp:31-35 — row-major fill from one stream. */
 void sgo_fill_uniform_actions(sgo_pcg32* r, double* actions, int64_t count);
+void sgo_fill_normals(sgo_pcg32* r, double* z, int64_t count);
 
 /* ---- robot_model.hpp:29-61 -------------------------------------------- */
 #define SGO_MAX_JOINTS 32
