@@ -163,21 +163,44 @@ static char* trim(char* s) { /* robot_model.cpp:39-44 */
   return s;
 }
 
-/* robot_model.cpp:46-59: exactly `expect` numbers and nothing else. */
+/* robot_model.cpp:46-59: exactly `expect` numbers and nothing else, with the
+ * number grammar of formatted stream extraction (`in >> double`, libstdc++
+ * num_get in the "C" locale): [sign] digits [. digits] [(e|E) [sign] digits],
+ * greedy; no inf / nan / hex. A token that runs to the end of the value ends
+ * the read with eof set (a malformed tail such as a lone "-" or "1e" is then
+ * dropped, not an error); a malformed token before the end is an error. */
 static int parse_numbers(const char* v, int expect, double* out) {
   const char* p = v;
   int n = 0;
   for (;;) {
     while (isspace((unsigned char)*p)) ++p;
-    if (!*p) break;
-    char* end;
-    double x = strtod(p, &end);
-    if (end == p) return 0;
-    if (n < expect) out[n] = x;
+    if (!*p) return n == expect;
+    const char* s = p;
+    int mant = 0, has_e = 0, expd = 0;
+    if (*p == '+' || *p == '-') ++p;
+    while (isdigit((unsigned char)*p)) ++p, ++mant;
+    if (*p == '.') {
+      ++p;
+      while (isdigit((unsigned char)*p)) ++p, ++mant;
+    }
+    if (mant && (*p == 'e' || *p == 'E')) {
+      has_e = 1;
+      ++p;
+      if (*p == '+' || *p == '-') ++p;
+      while (isdigit((unsigned char)*p)) ++p, ++expd;
+    }
+    const int valid = mant > 0 && (!has_e || expd > 0);
+    const int at_end = *p == 0;
+    if (!valid) return at_end ? n == expect : 0;
+    char buf[128];
+    size_t len = (size_t)(p - s);
+    if (len >= sizeof(buf)) return 0;
+    memcpy(buf, s, len);
+    buf[len] = 0;
+    if (n < expect) out[n] = strtod(buf, NULL);
     ++n;
-    p = end;
+    if (at_end) return n == expect;
   }
-  return n == expect;
 }
 
 #define MAX_FIELDS 24

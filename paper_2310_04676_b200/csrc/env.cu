@@ -203,6 +203,17 @@ int team_warps_for(int chain) {
   return v >= 4 ? 4 : (v < 1 ? 1 : v);
 }
 
+// Team layout of the specialised two-warp kernels (kernels.cuh TeamLayout):
+// automatic unless SG_TEAM_LAYOUT=legacy|packed (tests exercise both layouts
+// at every size; A/B measurements).
+int team_layout_from_env() {
+  const char* s = std::getenv("SG_TEAM_LAYOUT");
+  if (!s) return sg::kLayoutAuto;
+  if (std::string(s) == "legacy") return sg::kLayoutLegacy;
+  if (std::string(s) == "packed") return sg::kLayoutPacked;
+  return sg::kLayoutAuto;
+}
+
 template <typename F>
 int guard(F&& f) {
   try {
@@ -294,9 +305,10 @@ struct sg_env {
 
   int chain = sg::kChainGeneric8;
   int team_warps = 1;
+  int team_layout = sg::kLayoutAuto;
 
   void launch(int k_steps, bool gen, bool reset) {
-    sg::LaunchArgs a{k_steps, gen, reset, P.task.task, team_warps, stream};
+    sg::LaunchArgs a{k_steps, gen, reset, P.task.task, team_warps, stream, team_layout};
     cudaError_t e = cudaSuccess;
     switch (chain) {
       case sg::kChainPsm: e = sg::launch_psm(P, a); break;
@@ -943,6 +955,7 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   // (every single-robot task, ActiveTracking included, has specialised instantiations)
   env->chain = select_chain(P.robot, dc.control_mode, dc.substeps);
   env->team_warps = team_warps_for(env->chain);
+  env->team_layout = team_layout_from_env();
   CK(cudaDeviceSynchronize());
   return env;
 }

@@ -1013,11 +1013,13 @@ struct TeamSmem {
 // all shared loads of the thread are issued before its global stores. g must
 // be 16-byte aligned (an env's row block always is).
 template <class CH, int FULL, int NT>
-__device__ __forceinline__ void team_store(float* __restrict__ g, const float* __restrict__ s, int count, bool full,
+__device__ __forceinline__ void team_store(float* __restrict__ g, const float* __restrict__ s, int count, bool vec,
                                            int t) {
-  if (CH::kExact && full) {
-    constexpr int n4 = FULL / 4;
-    constexpr int iters = (n4 + NT - 1) / NT;
+  // vec: count % 4 == 0 (a team's rows start at a multiple of 4 envs, so g is
+  // 16-byte aligned); the unroll bound is the full 32-env team
+  if (CH::kExact && vec) {
+    constexpr int iters = (FULL / 4 + NT - 1) / NT;
+    const int n4 = count >> 2;
     float4* g4 = reinterpret_cast<float4*>(g);
     const float4* s4 = reinterpret_cast<const float4*>(s);
     float4 v[iters];
@@ -1027,11 +1029,54 @@ __device__ __forceinline__ void team_store(float* __restrict__ g, const float* _
 #pragma unroll
     for (int it = 0; it < iters; ++it)
       if (t + it * NT < n4) g4[t + it * NT] = v[it];
-    if constexpr (FULL % 4 != 0)
-      for (int k = n4 * 4 + t; k < FULL; k += NT) g[k] = s[k];
   } else {
     for (int k = t; k < count; k += NT) g[k] = s[k];
   }
+}
+
+// Shared memory of one team (TeamSmem + double-buffered observation rows and
+// action rows), a multiple of 16 bytes.
+template <int G>
+__host__ __device__ constexpr size_t team_smem_bytes_g(int A) {
+  return (sizeof(TeamSmem<G>) + 15) / 16 * 16 + (size_t)(2 * kTeamEnvs * (3 * A + 6) + 2 * (kTeamEnvs * A + 4)) * 4;
+}
+template <int G>
+inline size_t team_smem_bytes(int A) {
+  return team_smem_bytes_g<G>(A);
+}
+
+// Rows of one team and its synchronisation. TPC == 1: the CTA is the team
+// (32 envs per CTA, CTA barriers). TPC > 1 ("packed"): TPC teams per CTA with
+// one CTA per SM; the env quads (4 envs) are split evenly over all
+// gridDim.x * TPC teams (<= 32 envs each), so every SM carries the same
+// number of envs, and the team's warps meet at a named barrier (id 1 + team).
+struct Team {
+  int64_t row0;
+  int rows;     // <= 0: empty team
+  int id;       // team index within the CTA
+  int tthread;  // thread index within the team (role * 32 + lane)
+};
+
+template <int G, int TPC>
+__device__ __forceinline__ bool team_sync_or(const Team& tm, bool v) {
+  if constexpr (TPC == 1) {
+    return __syncthreads_or(v);
+  } else {
+    uint32_t r;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n barrier.cta.red.or.pred q, %2, %3, p;\n"
+        " selp.u32 %0, 1, 0, q;\n}"
+        : "=r"(r)
+        : "r"((uint32_t)v), "r"(1 + tm.id), "r"(32 * G)
+        : "memory");
+    return r != 0;
+  }
+}
+
+template <int G, int TPC>
+__device__ __forceinline__ void team_sync(const Team& tm) {
+  if constexpr (TPC == 1) __syncthreads();
+  else asm volatile("barrier.cta.sync %0, %1;" ::"r"(1 + tm.id), "r"(32 * G) : "memory");
 }
 
 // One team warp. Warp 0 is the SCORER, warps 1..G-1 are PRODUCERS. Per step k
@@ -1046,9 +1091,9 @@ __device__ __forceinline__ void team_store(float* __restrict__ g, const float* _
 // state: B(k+1) returns that fact (barrier OR), and producers redo step k+1
 // for those rows from the reset state with the same actions (one extra
 // barrier, one step in 300 under random actions).
-template <class CH, int G, int S, int TASK, int MODE, int SUB, bool GEN>
+template <class CH, int G, int S, int TASK, int MODE, int SUB, bool GEN, int TPC>
 __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float* s_obs_base, float* s_act_base,
-                                         TeamSmem<G>& ts) {
+                                         TeamSmem<G>& ts, const Team& tm) {
   using Blk = Block<CH, G, S>;
   constexpr int NB = Blk::N > 0 ? Blk::N : 1;
   constexpr int B0 = Blk::B;
@@ -1061,10 +1106,10 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   const int substeps = SUB > 0 ? SUB : T.substeps;
   const int64_t n = T.n;
   const int lane = threadIdx.x & 31;
-  const int64_t row0 = (int64_t)blockIdx.x * kTeamEnvs;
+  const int64_t row0 = tm.row0;
   const int64_t i = row0 + lane;
-  const bool active = i < n;
-  const int rows = (int)min((int64_t)kTeamEnvs, n - row0);
+  const int rows = tm.rows;
+  const bool active = lane < rows;
   // runtime DoF count of this block (generic chains)
   const auto has = [&](int j) { return Blk::N > 0 && (CH::kExact || B0 + j < A); };
 
@@ -1171,13 +1216,13 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     const int cnt = rows * A;
     if (P.actions_aligned) {
       const int n4 = cnt >> 2;
-      for (int k = threadIdx.x; k < n4; k += 32 * G)
+      for (int k = tm.tthread; k < n4; k += 32 * G)
         reinterpret_cast<float4*>(s_act_base)[k] = reinterpret_cast<const float4*>(src)[k];
-      for (int k = (n4 << 2) + threadIdx.x; k < cnt; k += 32 * G) s_act_base[k] = src[k];
+      for (int k = (n4 << 2) + tm.tthread; k < cnt; k += 32 * G) s_act_base[k] = src[k];
     } else {
-      for (int k = threadIdx.x; k < cnt; k += 32 * G) s_act_base[k] = src[k];
+      for (int k = tm.tthread; k < cnt; k += 32 * G) s_act_base[k] = src[k];
     }
-    __syncthreads();
+    team_sync<G, TPC>(tm);
   }
 
   // ---- dynamics (dynamics.cpp:133-185) on this block; count: saturation /
@@ -1347,11 +1392,11 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     const float* so = s_obs_base + pb * (kTeamEnvs * O);
     if constexpr (GEN && G == 1)
       team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act_base + pb * (kTeamEnvs * A + 4),
-                                               rows * A, rows == kTeamEnvs, lane);
-    team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.obs + row0 * O, so, rows * O, rows == kTeamEnvs, lane);
+                                               rows * A, (rows & 3) == 0, lane);
+    team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.obs + row0 * O, so, rows * O, (rows & 3) == 0, lane);
     if constexpr (!GEN) {
       if (P.p.h_obs)
-        team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.h_obs + row0 * O, so, rows * O, rows == kTeamEnvs,
+        team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.h_obs + row0 * O, so, rows * O, (rows & 3) == 0,
                                                            lane);
     }
   };
@@ -1368,7 +1413,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       const int e = reset_env<CH, TASK>(P, i);  // reset_row (envs.cpp:304-360) through HBM
       if (e) atomicOr(P.p.err, e);
     }
-    __syncthreads();
+    team_sync<G, TPC>(tm);
     if constexpr (S == 0) {
       float* so = s_obs_base + pb * (kTeamEnvs * O);
       if (active && ts.ended[pb][lane]) {  // the post-reset observation row
@@ -1406,7 +1451,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     }
     // B(step); its OR says rows of step-1 ended: reset them as a team, then the
     // scorer produces this step and producers redo it for the reset rows
-    if (__syncthreads_or(S == 0 && pend)) {
+    if (team_sync_or<G, TPC>(tm, S == 0 && pend)) {
       reset_phase(b ^ 1);
       if constexpr (S == 0) {
         draw(s_act);
@@ -1421,14 +1466,14 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
           publish(b, s_obs);
         }
       }
-      __syncthreads();
+      team_sync<G, TPC>(tm);
     }
 
     if constexpr (S > 0) {
       // producers store the step's generated action rows, then move on
       if (GEN)
         team_store<CH, kTeamEnvs * CH::kDof, (G - 1) * 32>(P.p.act_buf + row0 * A, s_act, rows * A,
-                                                          rows == kTeamEnvs, threadIdx.x - 32);
+                                                          (rows & 3) == 0, tm.tthread - 32);
     } else {
       // ---- scorer: tip, reward, flags (envs.cpp:456-463, 478-593) -----------
       float v[3];
@@ -1530,7 +1575,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   // rows that ended at the last step: team reset, then the scorer stores the
   // rows; the producers' registers of those rows are stale (the reset state
   // is already in HBM)
-  const bool fix = __syncthreads_or(S == 0 && pend);
+  const bool fix = team_sync_or<G, TPC>(tm, S == 0 && pend);
   if (fix) reset_phase((k_steps - 1) & 1);
   const bool stale = S > 0 && fix && ts.ended[(k_steps - 1) & 1][lane];
   if (active) {
@@ -1560,11 +1605,11 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   }
 }
 
-template <class CH, int G, int TASK, int MODE, int SUB, bool GEN, int... S>
+template <class CH, int G, int TASK, int MODE, int SUB, bool GEN, int TPC, int... S>
 __device__ __forceinline__ void team_dispatch(const StepParams& P, int k_steps, float* s_obs, float* s_act,
-                                              TeamSmem<G>& ts, std::integer_sequence<int, S...>) {
-  const int w = threadIdx.x >> 5;
-  ((w == S ? team_run<CH, G, S, TASK, MODE, SUB, GEN>(P, k_steps, s_obs, s_act, ts) : void()), ...);
+                                              TeamSmem<G>& ts, const Team& tm, int role,
+                                              std::integer_sequence<int, S...>) {
+  ((role == S ? team_run<CH, G, S, TASK, MODE, SUB, GEN, TPC>(P, k_steps, s_obs, s_act, ts, tm) : void()), ...);
 }
 
 // MINB: CTAs per SM the register budget targets. 1 (no cap: ~156 registers,
@@ -1572,16 +1617,42 @@ __device__ __forceinline__ void team_dispatch(const StepParams& P, int k_steps, 
 // at once; then 8 (128 registers): ECM at 65,536 envs is 2,048 teams, three
 // partial waves at 6 per SM and two at 8 (tools/ab.sh: +6.5 %; the cap costs
 // 8-9 % when every team is resident anyway, PSM / STAR at 16,384 envs).
-template <class CH, int G, int TASK, int MODE, int SUB, bool GEN, int MINB = 1>
-__global__ void __launch_bounds__(32 * G, MINB) env_step_kernel(const __grid_constant__ StepParams P, int k_steps) {
+//
+// TPC: teams per CTA (1, or 4 for the packed one-CTA-per-SM layout). Warp w
+// has role w / TPC (0 = scorer) in team (w % TPC + role) % TPC, so every SM
+// sub-partition (warp slot % 4) hosts one warp of each role: the scorer and
+// producer instruction streams differ in length, and with one two-warp team
+// per CTA all producers of an SM shared two sub-partitions.
+template <class CH, int G, int TASK, int MODE, int SUB, bool GEN, int MINB = 1, int TPC = 1>
+__global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __grid_constant__ StepParams P,
+                                                                      int k_steps) {
   extern __shared__ __align__(16) float smem[];
   const int A = CH::dof(P.robot);
   const int O = 3 * A + 6;
-  TeamSmem<G>& ts = *reinterpret_cast<TeamSmem<G>*>(smem);
-  float* s_obs = smem + (sizeof(TeamSmem<G>) + 15) / 16 * 4;  // 2 x 32 x O
+  const int64_t n = P.task.n;
+  const int w = threadIdx.x >> 5;
+  const int role = w / TPC;
+  Team tm;
+  tm.id = (w % TPC + role) % TPC;
+  tm.tthread = role * 32 + (threadIdx.x & 31);
+  if constexpr (TPC == 1) {
+    tm.row0 = (int64_t)blockIdx.x * kTeamEnvs;
+    tm.rows = (int)min((int64_t)kTeamEnvs, n - tm.row0);
+  } else {
+    const int64_t quads = (n + 3) / 4, teams = (int64_t)gridDim.x * TPC;
+    const int64_t g = (int64_t)blockIdx.x * TPC + tm.id;
+    const int64_t q0 = g * quads / teams, q1 = (g + 1) * quads / teams;
+    tm.row0 = 4 * q0;
+    tm.rows = (int)(min(4 * q1, n) - tm.row0);
+  }
+  float* base = smem + tm.id * (team_smem_bytes_g<G>(A) / sizeof(float));
+  TeamSmem<G>& ts = *reinterpret_cast<TeamSmem<G>*>(base);
+  float* s_obs = base + (sizeof(TeamSmem<G>) + 15) / 16 * 4;  // 2 x 32 x O
   float* s_act = s_obs + 2 * kTeamEnvs * O;                    // 2 x (32 x A + 4)
   if (P.p.ended_clear && blockIdx.x == 0 && threadIdx.x == 0) *P.p.ended_clear = 0;
-  team_dispatch<CH, G, TASK, MODE, SUB, GEN>(P, k_steps, s_obs, s_act, ts, std::make_integer_sequence<int, G>{});
+  if (tm.rows > 0)
+    team_dispatch<CH, G, TASK, MODE, SUB, GEN, TPC>(P, k_steps, s_obs, s_act, ts, tm, role,
+                                                    std::make_integer_sequence<int, G>{});
   if (P.p.h_status) {  // host step: the last CTA to finish publishes the counters
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1597,11 +1668,6 @@ __global__ void __launch_bounds__(32 * G, MINB) env_step_kernel(const __grid_con
   }
 }
 
-template <int G>
-inline size_t team_smem_bytes(int A) {
-  const int O = 3 * A + 6;
-  return (sizeof(TeamSmem<G>) + 15) / 16 * 16 + (size_t)(2 * kTeamEnvs * O + 2 * (kTeamEnvs * A + 4)) * sizeof(float);
-}
 
 // reset() (envs.cpp:425-435): every row through reset_row, episode_count := 0,
 // observe, clear flags and rewards.
@@ -1648,8 +1714,43 @@ __global__ void __launch_bounds__(128) env_reset_kernel(const __grid_constant__ 
 // kernels (parallel compilation) and exposes a launcher.
 constexpr int kResetBlock = 64;
 
+// Team layout of a launch: kLayoutAuto picks the packed one-CTA-per-SM layout
+// (TPC = 4) for the specialised two-warp teams when the envs fill between one
+// and four 32-env teams per SM, and one 32-env team per CTA otherwise.
+enum TeamLayout : int { kLayoutAuto = 0, kLayoutLegacy = 1, kLayoutPacked = 2 };
+constexpr int kPackedTeams = 4;
+
+inline int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
 template <class CH, int TASK, int MODE, int SUB, int G>
-inline cudaError_t launch_team(const StepParams& P, int k_steps, bool gen, cudaStream_t st) {
+inline cudaError_t launch_team(const StepParams& P, int k_steps, bool gen, cudaStream_t st, int layout = kLayoutAuto) {
+  if constexpr (CH::kExact && G == 2) {
+    const int64_t sms = sm_count();
+    const int64_t n = P.task.n;
+    const bool fits = n <= sms * kTeamEnvs * kPackedTeams;
+    if (fits && (layout == kLayoutPacked || (layout == kLayoutAuto && n >= sms * kTeamEnvs))) {
+      constexpr int TPC = kPackedTeams;
+      const size_t sm = TPC * team_smem_bytes<G>(P.robot.dof);
+      cudaError_t e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, true, 1, TPC>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, false, 1, TPC>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      const unsigned grid = (unsigned)sms;
+      if (gen) env_step_kernel<CH, G, TASK, MODE, SUB, true, 1, TPC><<<grid, 32 * G * TPC, sm, st>>>(P, k_steps);
+      else env_step_kernel<CH, G, TASK, MODE, SUB, false, 1, TPC><<<grid, 32 * G * TPC, sm, st>>>(P, k_steps);
+      return cudaGetLastError();
+    }
+  }
   const unsigned grid = (unsigned)((P.task.n + kTeamEnvs - 1) / kTeamEnvs);
   const size_t sm = team_smem_bytes<G>(P.robot.dof);
   if (sm > 48 * 1024) {

@@ -20,6 +20,7 @@ struct LaunchArgs {
   int task;
   int team_warps;
   cudaStream_t stream;
+  int layout = kLayoutAuto;  // TeamLayout (kernels.cuh)
 };
 
 cudaError_t launch_generic8(const StepParams& P, const LaunchArgs& a);
@@ -33,7 +34,7 @@ inline cudaError_t launch_fixed(const StepParams& P, const LaunchArgs& a) {
   if (a.reset) return launch_reset<CH, TASK>(P, a.stream);
   switch (a.team_warps) {
     case 1: return launch_team<CH, TASK, MODE, SUB, 1>(P, a.k_steps, a.gen, a.stream);
-    case 2: return launch_team<CH, TASK, MODE, SUB, 2>(P, a.k_steps, a.gen, a.stream);
+    case 2: return launch_team<CH, TASK, MODE, SUB, 2>(P, a.k_steps, a.gen, a.stream, a.layout);
     case 3: return launch_team<CH, TASK, MODE, SUB, 3>(P, a.k_steps, a.gen, a.stream);
     default: return launch_team<CH, TASK, MODE, SUB, 4>(P, a.k_steps, a.gen, a.stream);
   }
