@@ -218,6 +218,15 @@ int sg_env_images(const sg_env* env, float** d_target, float** d_scenes, float**
                   int32_t* height);
 
 int sg_env_reset(sg_env* env, sg_step_views* out);
+/* VecTaskEnv::reset() returning host observations (envs.cpp:425-435,
+ * `const MatrixXdR& reset()`): reset on the device, copy the n_envs x obs_dim
+ * fp32 observation rows into h_observations (pinned or pageable), synchronise
+ * and report errors. */
+int sg_env_reset_host(sg_env* env, float* h_observations);
+/* Page-locked host memory for the host-step buffers (zero-copy path of
+ * sg_env_step_host); any FFI caller can use it instead of its own allocator. */
+int sg_host_alloc(size_t bytes, void** out);
+int sg_host_free(void* p);
 /* d_actions: device, row-major n_envs x action_dim fp32 (stride = action_dim). */
 int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out);
 /* Host actions (pinned or pageable): H2D copy, step, D2H copy of the fields
@@ -226,8 +235,9 @@ int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out);
  * rows only); otherwise the host buffer is left untouched. */
 int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out);
 int sg_env_task_error(const sg_env* env, float** d_task_error);
-/* Running totals observed by the last sg_env_step_host (host side, no sync):
- * rows that ended (terminated or timed out) and saturated action entries. */
+/* Running totals over the sg_env_step_host calls so far (host side, no sync):
+ * rows that ended (terminated or timed out) and saturated action entries in
+ * those host steps; device-side steps (sg_env_step, bench) are not counted. */
 int sg_env_host_counters(const sg_env* env, uint64_t* ended_rows_total, uint64_t* saturations_total);
 int sg_env_state(const sg_env* env, sg_state_views* out);
 /* Waits for the env stream and converts the device error word. */
@@ -299,7 +309,11 @@ int sg_compute_gae(const float* d_rewards, const float* d_values, const uint8_t*
  * step counter *d_step incremented on device), box projection of the log-std
  * segment [log_std_offset, +log_std_n) to [log_std_min, log_std_max], d_grad
  * zeroed, and (if non-NULL) a bf16 copy of the new parameters written to
- * d_bf16_mirror. d_grad_sq: one float of scratch. Graph-capturable. */
+ * d_bf16_mirror. d_grad_sq: two floats, [0] scratch (the squared norm),
+ * [1] a sticky flag set to 1 when the gradient norm is not finite; the
+ * parameters and moments are then left unchanged (the reference throws
+ * "ppo_update: non-finite loss", ppo.cpp:193-199; the caller clears [1] and
+ * raises after its next synchronisation). Graph-capturable. */
 int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d_bf16_mirror, int64_t n,
                  float* d_grad_sq, int32_t* d_step, double lr, double beta1, double beta2, double eps,
                  double max_grad_norm, int64_t log_std_offset, int32_t log_std_n, double log_std_min,

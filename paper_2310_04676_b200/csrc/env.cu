@@ -264,7 +264,6 @@ struct sg_env {
   std::vector<sg::RobotModel> tools;
   std::vector<std::array<double, 7>> bases;    // per tool: xyz, quaternion wxyz
   std::vector<std::array<double, 3>> centers;  // per tool workspace centre
-  unsigned long long mt_ended_seen = 0;        // device ended-row total at the last host step
   // ImageMatching (image.cuh)
   bool image = false;
   sg::ImParams I{};
@@ -920,11 +919,14 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   p.task_error = dalloc<float>(n);
   p.terminated = dalloc<uint8_t>(n);
   p.timed_out = dalloc<uint8_t>(n);
-  // device counters in one 64-byte block; the host step reads them through
-  // a mapped pinned status the kernel's last CTA fills (no copy, no memset)
+  // device counters in one 64-byte block: {saturation total, ended rows of
+  // host-step slot A, error word, ended rows of slot B, CTA ticket, ended rows
+  // of device steps, saturations of host-step slot A, of slot B}. The host
+  // step reads its slot through a mapped pinned status the kernel's last CTA
+  // fills (no copy, no memset); device steps never touch the host slots.
   env->counters = dalloc<unsigned long long>(8);
   p.sat_total = env->counters;
-  p.ended_total = env->counters + 1;
+  p.ended_total = env->counters + 5;
   p.err = reinterpret_cast<int32_t*>(env->counters + 2);
   CK(cudaHostAlloc(&env->h_counters, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&env->d_status), env->h_counters, 0));
@@ -1091,6 +1093,34 @@ int sg_env_reset(sg_env* env, sg_step_views* out) {
   });
 }
 
+int sg_env_reset_host(sg_env* env, float* h_observations) {
+  return guard([&] {
+    if (!h_observations) throw sg::SimError("env.reset: null observation buffer");
+    CK(cudaSetDevice(env->device));
+    if (env->own_kernel()) env->launch_mt(0, false, true);
+    else env->launch_reset();
+    sg_step_views v;
+    env->views(&v);
+    CK(cudaMemcpyAsync(h_observations, v.observations, env->n * env->O * sizeof(float), cudaMemcpyDeviceToHost,
+                       env->stream));
+    env->check();
+  });
+}
+
+int sg_host_alloc(size_t bytes, void** out) {
+  return guard([&] {
+    if (!out) throw sg::ConfigError("sg_host_alloc: null output pointer");
+    *out = nullptr;
+    CK(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped));
+  });
+}
+
+int sg_host_free(void* p) {
+  return guard([&] {
+    if (p) CK(cudaFreeHost(p));
+  });
+}
+
 int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
   return guard([&] {
     if (!d_actions) throw sg::SimError("env.step: action shape mismatch");
@@ -1132,6 +1162,9 @@ static void task_step_host(sg_env* env, const float* h_actions, sg_host_result* 
   CK(cudaMemcpyAsync(env->d_actions_in, h_actions, n * env->A * sizeof(float), cudaMemcpyHostToDevice, s));
   env->M.actions = env->d_actions_in;
   env->I.actions = env->d_actions_in;
+  // counters before the launch ({sat, ended} into h_counters[2..3]) and after
+  // it: this step's deltas, whatever device steps ran since the last host step
+  CK(cudaMemcpyAsync(env->h_counters + 2, env->counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   env->launch_mt(1, false, false);
   sg_step_views v;
   env->views(&v);
@@ -1144,18 +1177,19 @@ static void task_step_host(sg_env* env, const float* h_actions, sg_host_result* 
     if (out->terminated) CK(cudaMemcpyAsync(out->terminated, v.terminated, n, cudaMemcpyDeviceToHost, s));
     if (out->timed_out) CK(cudaMemcpyAsync(out->timed_out, v.timed_out, n, cudaMemcpyDeviceToHost, s));
   }
-  CK(cudaMemcpyAsync(env->h_counters, env->counters, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(env->h_counters, env->counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  const unsigned long long sat = env->h_counters[0], ended_total = env->h_counters[1];
-  env->raise(static_cast<int32_t>(env->h_counters[2] & 0xffffffffu));
-  const unsigned long long ended = ended_total - env->mt_ended_seen;
-  env->mt_ended_seen = ended_total;
+  const unsigned long long sat = env->h_counters[0] - env->h_counters[2];
+  const unsigned long long ended = env->h_counters[1] - env->h_counters[3];
+  int32_t err = 0;
+  CK(cudaMemcpy(&err, env->counters + 2, sizeof(err), cudaMemcpyDeviceToHost));
+  env->raise(err);
   if (out && out->terminal_observations && ended != 0)
     CK(cudaMemcpy(out->terminal_observations, v.terminal_observations, n * O * sizeof(float),
                   cudaMemcpyDeviceToHost));
   env->last_ended += ended;
-  if (out) out->action_saturations = static_cast<int64_t>(sat - env->last_sat);
-  env->last_sat = sat;
+  env->last_sat += sat;
+  if (out) out->action_saturations = static_cast<int64_t>(sat);
 }
 
 int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
@@ -1191,6 +1225,8 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
     env->host_slot ^= 1;
     p.ended_total = env->counters + (slot ? 3 : 1);
     p.ended_clear = env->counters + (slot ? 1 : 3);
+    p.sat_step = env->counters + (slot ? 7 : 6);
+    p.sat_clear = env->counters + (slot ? 6 : 7);
     p.ticket = reinterpret_cast<unsigned int*>(env->counters + 4);
     p.h_status = env->d_status;
     if (zc) {
@@ -1221,9 +1257,10 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
       }
     }
     p.h_status = nullptr;
-    p.ended_clear = nullptr;
+    p.ended_clear = p.sat_step = p.sat_clear = nullptr;
+    p.ended_total = env->counters + 5;
     CK(cudaStreamSynchronize(s));
-    const unsigned long long sat = env->h_counters[0], ended = env->h_counters[1];
+    const unsigned long long sat = env->h_counters[0], ended = env->h_counters[1];  // this step's
     env->raise(static_cast<int32_t>(env->h_counters[2] & 0xffffffffu));
     // terminal_observations are only meaningful on ended rows (envs.hpp:87);
     // staged path: copied only on steps where some row ended (1 step in 300
@@ -1231,10 +1268,8 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
     if (!zc && out && out->terminal_observations && ended != 0)
       CK(cudaMemcpy(out->terminal_observations, p.tobs, n * O * sizeof(float), cudaMemcpyDeviceToHost));
     env->last_ended += ended;
-    if (out) {
-      out->action_saturations = static_cast<int64_t>(sat - env->last_sat);
-      env->last_sat = sat;
-    }
+    env->last_sat += sat;
+    if (out) out->action_saturations = static_cast<int64_t>(sat);
   });
 }
 

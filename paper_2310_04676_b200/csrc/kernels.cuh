@@ -140,6 +140,8 @@ struct EnvPtrs {
   // host reads them after its one synchronisation without a copy.
   unsigned long long* h_status;
   unsigned long long* ended_clear;  // zeroed at launch start: the next host step's ended slot
+  unsigned long long* sat_step;     // host step: saturations of THIS step (nullable)
+  unsigned long long* sat_clear;    // zeroed at launch start: the next host step's saturation slot
   unsigned int* ticket;             // CTA completion counter (last CTA publishes, then re-arms it)
   float* h_rewards;
   float* h_task_error;
@@ -907,8 +909,13 @@ __device__ __forceinline__ void apply_xform(const float* m, const float* p, floa
 #ifndef SG_SCORER_SHARE
 #define SG_SCORER_SHARE 1  // the scorer takes this many DoFs fewer than D / G (at least 1)
 #endif
+#ifndef SG_SCORER_DOFS
+#define SG_SCORER_DOFS -1  // >= 0: the scorer's DoF count (A/B); -1: the SG_SCORER_SHARE rule
+#endif
 __host__ __device__ constexpr int scorer_dofs(int D, int G) {
-  return G == 1 ? D : (D / G - SG_SCORER_SHARE > 1 ? D / G - SG_SCORER_SHARE : 1);
+  return G == 1 ? D
+                : (SG_SCORER_DOFS >= 0 ? (SG_SCORER_DOFS < D ? SG_SCORER_DOFS : D - 1)
+                                       : (D / G - SG_SCORER_SHARE > 1 ? D / G - SG_SCORER_SHARE : 1));
 }
 __host__ __device__ constexpr int dof_block_begin(int D, int G, int S) {
   return S == 0 ? 0
@@ -1266,6 +1273,31 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       }
     }
     const float dt = T.dt_sub;
+#ifdef SG_SAT_DYN
+    if constexpr (kPd) {
+      // Saturating form: the torque and velocity clamps become FFMA.SAT into
+      // [0, 1] on pre-scaled gains (a clamp to [-e, e] is e * (2 sat(x / 2e + 1/2) - 1)),
+      // which shortens the per-substep dependency chain from 12 to 9 ops.
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const float i2e = 0.5f / ge[j], i2v = 0.5f / gvl[j];
+        const float ak = -gk[j] * i2e, ad = -gd[j] * i2e, k0 = fmaf(kpqt[j], i2e, 0.5f);
+        const float bv = gc[j] * i2v, cs = ge[j] / gvl[j], c0 = 0.5f - ge[j] * i2v;
+        const float v2 = 2.f * gvl[j], v2dt = v2 * dt, vdt = gvl[j] * dt;
+#pragma unroll
+        for (int st = 0; st < SUB; ++st) {
+          const float qm = q[j] - vdt;
+          const float su = __saturatef(fmaf(ad, qd[j], fmaf(ak, q[j], k0)));
+          const float sv = __saturatef(fmaf(qd[j], bv, fmaf(su, cs, c0)));
+          const float vv = fmaf(sv, v2, -gvl[j]);
+          const float qq = fmaf(sv, v2dt, qm);
+          const float qc = fminf(fmaxf(qq, glo[j]), ghi[j]);
+          qd[j] = qc != qq ? 0.f : vv;
+          q[j] = qc;
+        }
+      }
+    } else
+#endif
     if constexpr (kPd) {
       const auto clampf = [](float x, float l, float h) { return fminf(fmaxf(x, l), h); };
       const auto finish = [&](int j, float vv, float qq) {  // limit projection (velocity already limited)
@@ -1326,7 +1358,10 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     if (!GEN && count) {
       if (!active) sat = bad = 0;
       const unsigned wsat = __reduce_add_sync(0xffffffffu, (unsigned)sat);
-      if (wsat && lane == 0) atomicAdd(P.p.sat_total, (unsigned long long)wsat);
+      if (wsat && lane == 0) {
+        atomicAdd(P.p.sat_total, (unsigned long long)wsat);
+        if (P.p.sat_step) atomicAdd(P.p.sat_step, (unsigned long long)wsat);
+      }
       if (__any_sync(0xffffffffu, bad) && bad) atomicOr(P.p.err, kErrNonFiniteAction);
     }
   };
@@ -1439,6 +1474,19 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   };
 
   bool pend = false;  // scorer: rows ended at the previous step (reset pending)
+#ifdef SG_PHASE_PROBE
+  long long t_prod = 0, t_bar = 0, t_post = 0, t_mark = clock64();
+#define SG_MARK(acc)                    \
+  do {                                  \
+    const long long now_ = clock64();   \
+    acc += now_ - t_mark;               \
+    t_mark = now_;                      \
+  } while (0)
+#else
+#define SG_MARK(acc) \
+  do {               \
+  } while (0)
+#endif
   for (int step = 0; step < k_steps; ++step) {
     const int b = step & 1;
     float* s_obs = s_obs_base + b * (kTeamEnvs * O);
@@ -1449,9 +1497,12 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       prefetch();
       publish(b, s_obs);
     }
+    SG_MARK(t_prod);
     // B(step); its OR says rows of step-1 ended: reset them as a team, then the
     // scorer produces this step and producers redo it for the reset rows
-    if (team_sync_or<G, TPC>(tm, S == 0 && pend)) {
+    const bool any_end = team_sync_or<G, TPC>(tm, S == 0 && pend);
+    SG_MARK(t_bar);
+    if (any_end) {
       reset_phase(b ^ 1);
       if constexpr (S == 0) {
         draw(s_act);
@@ -1571,7 +1622,14 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         store_rows(b);
       }
     }
+    SG_MARK(t_post);
   }
+#ifdef SG_PHASE_PROBE
+  if (blockIdx.x < 3 && lane == 0)
+    printf("probe cta %d warp %d: produce %lld barrier %lld post %lld cycles over %d steps\n", (int)blockIdx.x, S,
+           t_prod, t_bar, t_post, k_steps);
+#endif
+#undef SG_MARK
   // rows that ended at the last step: team reset, then the scorer stores the
   // rows; the producers' registers of those rows are stale (the reset state
   // is already in HBM)
@@ -1649,7 +1707,10 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
   TeamSmem<G>& ts = *reinterpret_cast<TeamSmem<G>*>(base);
   float* s_obs = base + (sizeof(TeamSmem<G>) + 15) / 16 * 4;  // 2 x 32 x O
   float* s_act = s_obs + 2 * kTeamEnvs * O;                    // 2 x (32 x A + 4)
-  if (P.p.ended_clear && blockIdx.x == 0 && threadIdx.x == 0) *P.p.ended_clear = 0;
+  if (P.p.ended_clear && blockIdx.x == 0 && threadIdx.x == 0) {
+    *P.p.ended_clear = 0;
+    if (P.p.sat_clear) *P.p.sat_clear = 0;
+  }
   if (tm.rows > 0)
     team_dispatch<CH, G, TASK, MODE, SUB, GEN, TPC>(P, k_steps, s_obs, s_act, ts, tm, role,
                                                     std::make_integer_sequence<int, G>{});
@@ -1659,7 +1720,7 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
       __threadfence();
       if (atomicAdd(P.p.ticket, 1u) == gridDim.x - 1) {
         __threadfence();
-        P.p.h_status[0] = *reinterpret_cast<volatile unsigned long long*>(P.p.sat_total);
+        P.p.h_status[0] = *reinterpret_cast<volatile unsigned long long*>(P.p.sat_step ? P.p.sat_step : P.p.sat_total);
         P.p.h_status[1] = *reinterpret_cast<volatile unsigned long long*>(P.p.ended_total);
         P.p.h_status[2] = static_cast<unsigned long long>(static_cast<uint32_t>(*reinterpret_cast<volatile int32_t*>(P.p.err)));
         *P.p.ticket = 0;
@@ -1714,9 +1775,12 @@ __global__ void __launch_bounds__(128) env_reset_kernel(const __grid_constant__ 
 // kernels (parallel compilation) and exposes a launcher.
 constexpr int kResetBlock = 64;
 
-// Team layout of a launch: kLayoutAuto picks the packed one-CTA-per-SM layout
-// (TPC = 4) for the specialised two-warp teams when the envs fill between one
-// and four 32-env teams per SM, and one 32-env team per CTA otherwise.
+// Team layout of a launch: one 32-env team per CTA (kLayoutAuto / Legacy), or
+// the packed one-CTA-per-SM layout (TPC = 4 teams per CTA, env quads spread
+// evenly, roles spread over the SM sub-partitions) when SG_TEAM_LAYOUT=packed.
+// Packed balances issue across sub-partitions exactly but measured slower
+// (PSM 16K: 192 vs 172 us per 250-step launch): the kernel is bound by the
+// per-team step latency, not by issue.
 enum TeamLayout : int { kLayoutAuto = 0, kLayoutLegacy = 1, kLayoutPacked = 2 };
 constexpr int kPackedTeams = 4;
 
@@ -1736,7 +1800,7 @@ inline cudaError_t launch_team(const StepParams& P, int k_steps, bool gen, cudaS
     const int64_t sms = sm_count();
     const int64_t n = P.task.n;
     const bool fits = n <= sms * kTeamEnvs * kPackedTeams;
-    if (fits && (layout == kLayoutPacked || (layout == kLayoutAuto && n >= sms * kTeamEnvs))) {
+    if (fits && layout == kLayoutPacked) {
       constexpr int TPC = kPackedTeams;
       const size_t sm = TPC * team_smem_bytes<G>(P.robot.dof);
       cudaError_t e = cudaFuncSetAttribute(env_step_kernel<CH, G, TASK, MODE, SUB, true, 1, TPC>,

@@ -602,7 +602,12 @@ __global__ void adam_kernel(float* __restrict__ p, float* __restrict__ g, float*
                             const int32_t* __restrict__ step, const __grid_constant__ AdamArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const float norm = sqrtf(*grad_sq);
+  const float norm = sqrtf(grad_sq[0]);
+  if (!isfinite(norm)) {  // ppo.cpp:193-199 throws here: leave the parameters, flag it (sticky)
+    if (i == 0) const_cast<float*>(grad_sq)[1] = 1.f;
+    g[i] = 0.f;
+    return;
+  }
   const float scale = (a.max_norm > 0.f && norm > a.max_norm) ? a.max_norm / norm : 1.f;
   const int t = *step;
   const float bc1 = 1.f - powf(a.beta1, (float)t), bc2 = 1.f - powf(a.beta2, (float)t);

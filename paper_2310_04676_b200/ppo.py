@@ -30,6 +30,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import math
+
 import torch
 import torch.nn.functional as F
 
@@ -39,27 +41,7 @@ HALF_LOG_2PI = 0.9189385332046727  # ppo.cpp:28
 LOG_STD_MIN, LOG_STD_MAX = -5.0, 2.0  # policy.hpp:28-29
 TRAIN_STREAM = 0x7261696E  # ppo.cpp:233
 
-M64 = (1 << 64) - 1
-
-
-def make_stream(seed: int, stream_id: int) -> tuple[int, int]:
-    """rng.hpp:69-83 (host side; returns PCG32 (state, inc))."""
-    x = (seed ^ ((0x2545F4914F6CDD1D * (stream_id + 1)) & M64)) & M64
-
-    def splitmix(x):
-        x = (x + 0x9E3779B97F4A7C15) & M64
-        z = x
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
-        return x, z ^ (z >> 31)
-
-    x, a = splitmix(x)
-    x, b = splitmix(x)
-    inc = ((b << 1) | 1) & M64
-    s = inc  # 0 * mult + inc
-    s = (s + a) & M64
-    s = (s * 6364136223846793005 + inc) & M64
-    return s, inc
+make_stream = sg.make_stream  # rng.hpp:69-83 (host side; PCG32 (state, inc))
 
 
 @dataclass
@@ -298,9 +280,11 @@ def ppo_loss(params, obs, actions, old_logp, adv, ret, cfg: TrainConfig, obs_dim
                      cfg)
 
 
-def allreduce_mean_(t: torch.Tensor, dist) -> torch.Tensor:
-    """Gradient all-reduce (sum, then / world) before clipping (ppo.cpp:201)."""
-    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+def allreduce_mean_(t: torch.Tensor, dist, force: bool = False) -> torch.Tensor:
+    """Gradient all-reduce (sum, then / world) before clipping (ppo.cpp:201).
+    force: issue the collective even at world size 1 (tests of the captured
+    NCCL path on a single GPU)."""
+    if dist is not None and dist.is_initialized() and (dist.get_world_size() > 1 or force):
         dist.all_reduce(t)
         t /= dist.get_world_size()
     return t
@@ -354,13 +338,16 @@ class Trainer:
                 self.layers.append((W, b))
         self.log_std = self.params[self.ls_off: self.ls_off + A].detach().requires_grad_(True)
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]
-        single = dist is None or not dist.is_initialized() or dist.get_world_size() == 1
-        self.use_graph = cfg.cuda_graph and single
+        # The whole update is one CUDA-graph replay at any world size: the NCCL
+        # gradient all-reduce of every minibatch is captured with the GEMMs
+        # (the communicator is created by the warm-up updates before capture).
+        self.use_graph = cfg.cuda_graph
+        self.force_collectives = False
         # Adam state (ppo.cpp:50-64) for the fused optimizer step
         self.adam_m = torch.zeros_like(self.params)
         self.adam_v = torch.zeros_like(self.params)
         self.adam_t = torch.zeros(1, device=dev, dtype=torch.int32)
-        self.grad_sq = torch.zeros(1, device=dev)
+        self.grad_sq = torch.zeros(2, device=dev)  # [squared norm scratch, sticky non-finite flag]
         if self.mirror is not None:
             self.mirror.copy_(self.params)
         policy.load_params(self.ref_params())
@@ -381,6 +368,15 @@ class Trainer:
         self.ep_acc = z(N)
         self.stats = z(4, dt=torch.float64)
         self.stream_state, self.stream_inc = make_stream(cfg.seed, TRAIN_STREAM)
+        # The reference draws every rollout step's noise from ONE stream over
+        # all global rows (ppo.cpp:264-270) and shuffles the global buffer
+        # (:175-178). A shard of global rows [row_off, row_off + N) of
+        # world * N takes its rows' slice of each step's draws, and the stream
+        # advances by the global draw counts.
+        multi = dist is not None and dist.is_initialized()
+        self.world = dist.get_world_size() if multi else 1
+        self.global_n = self.world * N
+        self.row_off = int(env.cfg.row_offset)
         self.draw_pos = 0  # u32 draws consumed from the trainer stream
         self.d_pos = torch.zeros(1, dtype=torch.int64, device=dev)
         self.obs = None
@@ -412,7 +408,7 @@ class Trainer:
             self._rollout_body()
             if self.use_graph:  # record (not run) the graph the next rollouts replay
                 self._capture_rollout()
-        self.draw_pos += 2 * T * N * A
+        self.draw_pos += 2 * T * self.global_n * A
         self.env_steps += N * T
 
     def _capture_rollout(self) -> None:
@@ -439,7 +435,8 @@ class Trainer:
             obs = self.obs
             pol.forward(obs, self.mean, b["values"][t])
             sg._pcheck(L.sg_policy_sample(self.mean.data_ptr(), N, A, log_std.data_ptr(), self.stream_state,
-                                          self.stream_inc, self.d_pos.data_ptr(), 2 * t * N * A,
+                                          self.stream_inc, self.d_pos.data_ptr(),
+                                          2 * A * (t * self.global_n + self.row_off),
                                           b["actions"][t].data_ptr(), b["logp"][t].data_ptr(), st))
             b["obs"][t][:, :self.O].copy_(obs)
             res = env.step(b["actions"][t])
@@ -497,7 +494,7 @@ class Trainer:
                                                g["ret"][:m_rows], self.A, cfg.clip_eps, cfg.value_coef,
                                                cfg.entropy_coef)
                 loss.backward()
-                allreduce_mean_(self.grad, self.dist)
+                allreduce_mean_(self.grad, self.dist, force=self.force_collectives)
                 self._adam_step()
                 metrics += m
 
@@ -559,8 +556,8 @@ class Trainer:
                 self._update_body(self.perms, metrics)
         finally:
             torch.backends.cuda.matmul.allow_tf32 = prev_tf32
-        # the reference's Fisher-Yates consumed cap-1 draws per epoch from the stream
-        self.draw_pos += cfg.epochs * (cap - 1)
+        # the reference's Fisher-Yates consumed (global buffer size - 1) draws per epoch
+        self.draw_pos += cfg.epochs * (self.T * self.global_n - 1)
         self.policy.load_params(self.ref_params())
         return metrics / (cfg.epochs * cfg.minibatch_count)
 
@@ -590,8 +587,16 @@ class Trainer:
         self.gae()
         m = self.update()
         self.iteration += 1
+        # one synchronisation per iteration: device-detected env errors
+        # (non-finite action / reward, goal-sampling exhaustion) raise here,
+        # and a non-finite minibatch loss or gradient (ppo.cpp:193-199)
+        self.env.synchronize()
         s = self.stats.tolist()
         pm = m.tolist()
+        nonfinite = self.grad_sq[1].item() != 0.0 or not all(math.isfinite(x) for x in pm)
+        if nonfinite:
+            self.grad_sq[1] = 0.0
+            raise sg.SimError(f"ppo_update: non-finite loss (iteration {self.iteration}, metrics {pm})")
         return dict(iteration=self.iteration, env_steps=self.env_steps, episodes_completed=int(s[3]),
                     mean_episode_reward=s[1] / s[3] if s[3] else float("nan"),
                     mean_final_error=s[2] / s[3] if s[3] else float("nan"),

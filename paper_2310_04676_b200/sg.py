@@ -107,6 +107,9 @@ _SIGS = {
                                 _P(C.c_int32)]),
     "sg_env_tools": (C.c_int, [C.c_void_p, _P(C.c_int32), _P(C.c_double), _P(C.c_double), _P(C.c_int32)]),
     "sg_env_reset": (C.c_int, [C.c_void_p, _P(StepViews)]),
+    "sg_env_reset_host": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sg_host_alloc": (C.c_int, [C.c_size_t, _P(C.c_void_p)]),
+    "sg_host_free": (C.c_int, [C.c_void_p]),
     "sg_env_step": (C.c_int, [C.c_void_p, C.c_void_p, _P(StepViews)]),
     "sg_env_step_host": (C.c_int, [C.c_void_p, C.c_void_p, _P(HostResult)]),
     "sg_env_task_error": (C.c_int, [C.c_void_p, _P(C.c_void_p)]),
@@ -465,6 +468,31 @@ class VecTaskEnv:
 
 # ----------------------------------------------------------------------------- policy
 
+TRAIN_STREAM = 0x7261696E  # ppo.cpp:233
+_M64 = (1 << 64) - 1
+
+
+def make_stream(seed: int, stream_id: int) -> tuple[int, int]:
+    """rng.hpp:69-83 on the host: splitmix64 of seed ^ (0x2545f4914f6cdd1d *
+    (id + 1)) -> pcg32_srandom(initstate, initseq); returns PCG32 (state, inc)."""
+    x = (seed ^ ((0x2545F4914F6CDD1D * (stream_id + 1)) & _M64)) & _M64
+
+    def splitmix(x):
+        x = (x + 0x9E3779B97F4A7C15) & _M64
+        z = x
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        return x, z ^ (z >> 31)
+
+    x, a = splitmix(x)
+    x, b = splitmix(x)
+    inc = ((b << 1) | 1) & _M64
+    s = inc  # 0 * mult + inc
+    s = (s + a) & _M64
+    s = (s * 6364136223846793005 + inc) & _M64
+    return s, inc
+
+
 def _pcheck(rc: int) -> None:
     if rc == SG_OK:
         return
@@ -514,6 +542,25 @@ class Policy:
         _pcheck(lib().sg_policy_forward(self._h, obs.data_ptr(), n, obs.stride(0), mean.data_ptr(),
                                         value.data_ptr(), stream))
         return mean, value
+
+    def sample(self, mean, seed: int = 0, log_std=None, draw_pos: int = 0, step_offset: int = 0):
+        """Trainer rollout sampling (ppo.cpp:262-277): a = mean + exp(log_std) z,
+        z from make_stream(seed, 0x7261696e) at draw draw_pos + step_offset +
+        2 A e for env e; log_std defaults to the init value -1. Returns
+        (actions, log_probs)."""
+        import torch
+        n, A = mean.shape
+        dev = mean.device
+        if log_std is None:
+            log_std = torch.full((A,), -1.0, device=dev)
+        s0, inc = make_stream(seed, TRAIN_STREAM)
+        pos = torch.tensor([draw_pos], dtype=torch.int64, device=dev)
+        acts = torch.empty((n, A), device=dev)
+        logp = torch.empty((n,), device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _pcheck(lib().sg_policy_sample(mean.data_ptr(), n, A, log_std.data_ptr(), s0, inc, pos.data_ptr(), step_offset,
+                                       acts.data_ptr(), logp.data_ptr(), stream))
+        return acts, logp
 
 
 # -- PPO update kernels (train.cu) ---------------------------------------------

@@ -56,3 +56,51 @@ def test_task_reference_arms_run_on_cpu():
         cfg = dict(bench.CONFIGS[name], n_envs=64)
         rate, lanes, sample = bench.cpu_reference(cfg, steps=3, budget_s=0.5)
         assert rate > 0 and lanes >= 1 and "64 envs" in sample
+
+
+def _json_lines(text):
+    out = []
+    for ln in text.splitlines():
+        ln = ln.strip()
+        if ln.startswith("{"):
+            out.append(json.loads(ln))
+    return out
+
+
+def test_gpus_flag_spawns_ranks_dry_run():
+    """`bench.py --gpus 2` outside torchrun launches two ranks itself
+    (torch.distributed.run on 127.0.0.1) -- the driver's N>1 entry -- and the
+    ranks agree on the shard plan and the max-over-ranks timing (gloo here)."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = _json_lines(out.stdout)
+    assert len(lines) == 1, out.stdout
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["backend"] == "gloo"
+    rows = []
+    for p in line["plans"]:
+        rows.extend(range(p["row_offset"], p["row_offset"] + p["n_envs"]))
+        assert p["global_n_envs"] == 2 * 16384
+    assert rows == list(range(2 * 16384))
+    assert line["max_time"] == 2.0
+
+
+def test_gpus_flag_reference_arm_prints_one_line():
+    """The reference arm under N ranks: rank 0 alone runs and prints."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--steps", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = _json_lines(out.stdout)
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+
+
+def test_contract_bytes_match_survey():
+    """314 / 278 / 350 B per env-step (PSM / ECM / STAR)."""
+    assert bench.contract_bytes(7, 27) == 314
+    assert bench.contract_bytes(6, 24) == 278
+    assert bench.contract_bytes(8, 30) == 350

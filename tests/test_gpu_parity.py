@@ -26,15 +26,21 @@ def _soa(t):  # device SoA (dof x n) -> host (n x dof)
     return t.detach().cpu().numpy().T.astype(np.float64)
 
 
-def _run_pair(sg, oracle, robot, task, n, steps, seed=0, sigma=0.05, check_every=1, actions_fn=None, tol=None):
-    """Step the device env and the fp64 oracle with the same actions; compare."""
+def _run_pair(sg, oracle, robot, task, n, steps, seed=0, sigma=0.05, check_every=1, actions_fn=None, tol=None,
+              mode="position", per_step=None):
+    """Step the device env and the fp64 oracle with the same actions; compare.
+    mode: control mode (dynamics.cpp:133-185); per_step(s, env, ref, res, a32):
+    extra checks after every step."""
     _cuda()
     TOL = dict(globals()["TOL"], **(tol or {}))
     m = oracle.resolve_robot(robot)
     ocfg = oracle.env_config(n_envs=n, seed=seed, task=task, goal_sigma=sigma)
-    ref = oracle.Env(ocfg, m)
+    dyn = oracle.default_dynamics(m)
+    dyn.control_mode = {"position": 0, "velocity": 1, "torque": 2}[mode]
+    ref = oracle.Env(ocfg, m, dyn)
     ref.reset()
-    env = sg.VecTaskEnv(robots=(robot,), n_envs=n, seed=seed, task=task, goal_sigma=sigma)
+    env = sg.VecTaskEnv(robots=(robot,), n_envs=n, seed=seed, task=task, goal_sigma=sigma,
+                        dynamics=dict(control_mode=mode))
     obs = env.reset()
     torch.cuda.synchronize()
     A, O = env.action_dim, env.obs_dim
@@ -47,6 +53,8 @@ def _run_pair(sg, oracle, robot, task, n, steps, seed=0, sigma=0.05, check_every
         a32 = a.astype(np.float32)
         res = env.step(torch.from_numpy(a32).cuda())
         ref.step(a32.astype(np.float64))
+        if per_step is not None:
+            per_step(s, env, ref, res, a32)
         if s % check_every and s != steps - 1:
             continue
         torch.cuda.synchronize()
@@ -254,6 +262,53 @@ def test_sharded_rows_match_single_device(sg, oracle):
     assert torch.equal(full.state()["rng_state"][128:], part.state()["rng_state"])
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_star_path_following_shards_match_single_device(sg, oracle, world):
+    """BASELINE config 4 sharding: STAR PathFollowing ranks with row_offset
+    (global rows [r*N, (r+1)*N), dynamics.cpp:238 streams seeded by global row)
+    are bit-identical to the same rows of one device stepping world*N envs,
+    through fused bench launches (reset-record kernel, two synchronized reset
+    bursts: envs.cpp:241-267 paths + spline waypoint tables) and through
+    caller-action steps (each rank applies its slice of the global rows)."""
+    _cuda()
+    N = 96
+    kw = dict(robots=("star",), seed=11, task="path_following", goal_sigma=0.15)
+    full = sg.VecTaskEnv(n_envs=world * N, **kw)
+    parts = [sg.VecTaskEnv(n_envs=N, row_offset=r * N, **kw) for r in range(world)]
+    full.reset()
+    for p in parts:
+        p.reset()
+    full.bench_begin(11)
+    for p in parts:
+        p.bench_begin(11, global_n_envs=world * N)
+    for k in (1, 349, 300):
+        full.bench_step(k)
+        for p in parts:
+            p.bench_step(k)
+    rng = np.random.default_rng(2)
+    for _ in range(3):  # caller actions: every rank steps its rows of the global batch
+        act = torch.from_numpy(rng.uniform(-1.1, 1.1, size=(world * N, 8)).astype(np.float32)).cuda()
+        full.step(act)
+        for r, p in enumerate(parts):
+            p.step(act[r * N:(r + 1) * N].contiguous())
+    torch.cuda.synchronize()
+    sf, rf = full.state(), full._result()
+    for r, p in enumerate(parts):
+        rows = slice(r * N, (r + 1) * N)
+        sp, rp = p.state(), p._result()
+        for k in ("step_count", "hold_count", "episode_count", "rng_state", "waypoint_idx", "waypoint_len"):
+            assert torch.equal(sf[k][rows], sp[k]), (r, k)
+        for k in ("q", "qdot", "q_target", "goals", "tips"):
+            assert torch.equal(sf[k][:, rows], sp[k]), (r, k)
+        wl = sp["waypoint_len"].cpu().numpy()
+        wf, wp = sf["waypoints"][rows].cpu().numpy(), sp["waypoints"].cpu().numpy()
+        for e in range(N):
+            np.testing.assert_array_equal(wf[e, : wl[e]], wp[e, : wl[e]])
+        for k in ("observations", "rewards", "task_error", "terminated", "timed_out"):
+            assert torch.equal(getattr(rf, k)[rows], getattr(rp, k)), (r, k)
+    assert int(sf["episode_count"].min()) >= 2  # two synchronized reset bursts (steps 300 and 600)
+
+
 def test_host_step_matches_device_step(sg, oracle):
     """sg_env_step_host == sg_env_step; terminal observations reach the host on
     every step where rows ended (episode_len 3 -> ends every third step)."""
@@ -331,6 +386,34 @@ def test_host_step_zero_copy_matches_staged_and_device(sg, oracle, robot, n):
     assert envs[0].host_counters()[0] == 2 * n
 
 
+@pytest.mark.parametrize("robots,task", [(("psm",), "target_reaching"), (("psm", "psm", "ecm"), "multi_tool_reaching")])
+def test_host_step_counts_only_its_own_rows(sg, oracle, robots, task):
+    """A host step after device steps reports the rows that ended and the
+    saturated entries of THAT step only (StepResult.action_saturations is per
+    step, envs.hpp:82-89): ended rows / saturations of earlier sg_env_step calls
+    must not leak into it, and a host step without result buffers still
+    advances the totals."""
+    _cuda()
+    n = 96
+    env = sg.VecTaskEnv(robots=robots, n_envs=n, seed=5, episode_len=3, task=task)
+    env.reset()
+    A = env.action_dim
+    sat_act = np.full((n, A), 1.5, dtype=np.float32)  # every entry saturates
+    for _ in range(3):  # device steps: every row times out at the third
+        env.step(torch.from_numpy(sat_act).cuda())
+    torch.cuda.synchronize()
+    act = np.zeros((n, A), dtype=np.float32)
+    act[:5, 0] = 2.0  # 5 saturated entries
+    r = env.step_host(act)
+    assert r["action_saturations"] == 5
+    assert not (r["terminated"] | r["timed_out"]).any()
+    assert env.host_counters() == (0, 5)
+    sg._check(sg.lib().sg_env_step_host(env._h, torch.from_numpy(act).pin_memory().data_ptr(), None))  # no result
+    r = env.step_host(act)  # third step of the episode: every row times out
+    assert r["action_saturations"] == 5 and r["timed_out"].all()
+    assert env.host_counters() == (n, 15)
+
+
 def test_nonfinite_action_is_sim_error(sg, oracle):
     _cuda()
     env = sg.VecTaskEnv(robots=("psm",), n_envs=8)
@@ -345,37 +428,37 @@ def test_nonfinite_action_is_sim_error(sg, oracle):
 
 @pytest.mark.parametrize("mode", ["position", "velocity", "torque"])
 def test_control_modes_limits_and_parity(sg, oracle, mode):
-    """Adversarial actions in [-2, 2] (test_dynamics.cpp:134-163): limits and
-    velocity bounds hold; state matches the oracle in every control mode."""
-    _cuda()
+    """Adversarial actions in [-2, 2] (test_dynamics.cpp:134-163) in every
+    control mode (these run on the generic-chain kernel): every field --
+    q, qdot, q_target, tips, goals, observations, terminal observations,
+    rewards, task_error -- at the standard per-step tolerances, flags /
+    counters / streams bit-exact, saturation counts exact per step, and the
+    joint and velocity limits hold on every step."""
     m = oracle.resolve_robot("psm")
-    n = 64
-    dyn = oracle.default_dynamics(m)
-    dyn.control_mode = {"position": 0, "velocity": 1, "torque": 2}[mode]
-    ref = oracle.Env(oracle.env_config(n_envs=n, seed=99), m, dyn)
-    ref.reset()
-    env = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=99, dynamics=dict(control_mode=mode))
-    env.reset()
-    rng = oracle.make_stream(42, 0)
     # the device stores limits in fp32: the bounds hold against the fp32-rounded limits
     f32 = lambda v: np.float64(np.float32(v))
     lo = np.array([f32(m.dof_joint(d).limit_lo) for d in range(m.dof)])
     hi = np.array([f32(m.dof_joint(d).limit_hi) for d in range(m.dof)])
     vl = np.array([f32(m.dof_joint(d).velocity_limit) for d in range(m.dof)])
-    sat_total = 0
-    for s in range(250):
-        a = (2.0 * oracle.fill_uniform_actions(rng, n, m.dof)).astype(np.float32)
-        hr = env.step_host(a)
-        ref.step(a.astype(np.float64))
-        sat_total += hr["action_saturations"]
-        assert hr["action_saturations"] == ref.result()["saturations"]
+    rng = oracle.make_stream(42, 0)
+    n = 64
+    seen = dict(sat=0)
+
+    def actions(s):
+        return 2.0 * oracle.fill_uniform_actions(rng, n, m.dof)
+
+    def check(s, env, ref, res, a32):
         st = env.state()
         q, qd = _soa(st["q"]), _soa(st["qdot"])
         assert (q >= lo).all() and (q <= hi).all()
         assert (np.abs(qd) <= vl).all()
-        sr = ref.state()
-        assert np.abs(q - sr["q"]).max() <= TOL["q"] * 10
-    assert sat_total > 0
+        assert int(((a32 < -1) | (a32 > 1)).sum()) == ref.result()["saturations"]
+        seen["sat"] += ref.result()["saturations"]
+        assert int(res.saturations_total.item()) == seen["sat"]  # device running total, exact
+
+    _run_pair(sg, oracle, "psm", oracle.TARGET_REACHING, n, 250, seed=99, actions_fn=actions, mode=mode,
+              per_step=check)
+    assert seen["sat"] > 0
 
 
 def test_fk_batch_matches_matrix_oracle(sg, oracle):

@@ -99,7 +99,7 @@ def test_fused_adam_step_matches_reference_formulas(sg):
     M, V = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
     mirror = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
     t = torch.zeros(1, dtype=torch.int32, device="cuda")
-    gsq = torch.zeros(1, device="cuda")
+    gsq = torch.zeros(2, device="cuda")
     lr, b1, b2, eps, max_norm = 1e-2, 0.9, 0.999, 1e-8, 1.0
     for step, gscale in enumerate((0.001, 1.0, 0.003, 5.0), start=1):
         g = rng.normal(size=n) * gscale
@@ -123,6 +123,20 @@ def test_fused_adam_step_matches_reference_formulas(sg):
         p = P.cpu().numpy().astype(np.float64)  # continue from the device's fp32 state
         m = M.cpu().numpy().astype(np.float64)
         v = V.cpu().numpy().astype(np.float64)
+    assert gsq[1].item() == 0.0
+    # a non-finite gradient (ppo.cpp:193-199 throws): parameters and moments
+    # untouched, gradient cleared, sticky flag raised
+    before = [x.clone() for x in (P, M, V)]
+    G.copy_(torch.tensor(rng.normal(size=n), dtype=torch.float32))
+    G[17] = float("nan")
+    sg._pcheck(sg.lib().sg_adam_step(P.data_ptr(), G.data_ptr(), M.data_ptr(), V.data_ptr(), mirror.data_ptr(),
+                                     n, gsq.data_ptr(), t.data_ptr(), lr, b1, b2, eps, max_norm, ls_off, ls_n,
+                                     -5.0, 2.0, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert gsq[1].item() == 1.0
+    for a, b in zip((P, M, V), before):
+        assert torch.equal(a, b)
+    assert not G.any()
 
 
 def test_ppo_trainer_bf16_update_runs(sg):
@@ -250,3 +264,69 @@ def test_fused_ppo_loss_matches_reference_formulas(sg):
     torch.testing.assert_close(vf.grad[:, 0], v_ref.grad, rtol=1e-5, atol=1e-9)
     torch.testing.assert_close(ls.grad, ls_ref.grad, rtol=1e-4, atol=1e-6)
     assert ls.grad[3] == 0 and ls.grad[4] == 0
+
+
+def test_update_graph_with_captured_nccl_allreduce(sg):
+    """The multi-GPU update path on one GPU: a world-1 NCCL group with the
+    gradient all-reduce forced on is captured inside the update's CUDA graph
+    (ppo.cpp:201-204 all-reduce before clipping); all-reduce-mean over one
+    rank is the identity, so the parameters equal a trainer without any
+    collective bit for bit."""
+    import socket
+    import torch.distributed as dist
+    from paper_2310_04676_b200 import ppo
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        res = []
+        for use_dist in (False, True):
+            env = sg.VecTaskEnv(robots=("psm",), n_envs=2048, seed=2, episode_len=40)
+            tr = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim),
+                             ppo.TrainConfig(seed=1, n_steps=32, update_precision="fp32"),
+                             dist=dist if use_dist else None)
+            tr.force_collectives = use_dist
+            for _ in range(3):
+                tr.iterate()
+            assert tr.graph is not None  # the update ran as a graph replay
+            res.append(tr.params.clone())
+        assert torch.equal(res[0], res[1])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_trainer_raises_on_nonfinite_training(sg):
+    """A diverged policy (non-finite parameters) is a SimError at the next
+    iteration's synchronisation -- non-finite actions reach the env
+    (dynamics.cpp:198-200) and the loss / gradient check (ppo.cpp:193-199) --
+    instead of training on silently."""
+    from paper_2310_04676_b200 import ppo
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=1024, seed=0)
+    tr = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim), ppo.TrainConfig(seed=0))
+    tr.iterate()
+    with torch.no_grad():
+        tr.params[5] = float("nan")
+    tr.policy.load_params(tr.ref_params())
+    with pytest.raises(sg.SimError):
+        tr.iterate()
+
+
+def test_shard_sampling_takes_its_rows_of_the_global_stream(sg):
+    """ppo.cpp:264-270 draws each rollout step's noise from ONE stream over all
+    global rows. A shard owning global rows [r*N, (r+1)*N) of world*N
+    (Trainer: step_offset = 2A (t*world*N + row_offset)) gets exactly those
+    rows' draws -- shards never share noise."""
+    torch.manual_seed(0)
+    world, N, A, t = 4, 300, 7, 3
+    mean = torch.randn(world * N, A, device="cuda")
+    pol = sg.Policy(27, A)
+    full, lp_full = pol.sample(mean, seed=5, step_offset=2 * A * t * world * N)
+    for r in range(world):
+        part, lp = pol.sample(mean[r * N:(r + 1) * N].contiguous(), seed=5,
+                              step_offset=2 * A * (t * world * N + r * N))
+        assert torch.equal(part, full[r * N:(r + 1) * N])
+        assert torch.equal(lp, lp_full[r * N:(r + 1) * N])
+    assert not torch.equal(full[:N], full[N:2 * N])
