@@ -562,7 +562,7 @@ def gate_cycles(n_launches: int) -> int:
     return int((10000 + 200 * n_launches) * 1e-6 * 2.0e9)
 
 
-def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, retries: int = 3):
+def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, retries: int = 3, do_flush: bool = True):
     """`runs` independent timed runs of the same launch sequence. Each run is
     bracketed by barrier + synchronize; every launch is preceded by an L2
     flush (256 MiB write) and timed by CUDA events on the env's stream (the
@@ -597,7 +597,8 @@ def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, retrie
                 g = torch.cuda.Event()
                 g.record()
             for (e0, e1), kf in zip(ev, launches):
-                flush.zero_()
+                if do_flush:
+                    flush.zero_()
                 e0.record()
                 env.bench_step(kf)
                 e1.record()
@@ -631,6 +632,7 @@ def main():
                     help="enqueue the timed launches without the device-side gate (round-1 protocol; "
                          "host-enqueue latency lands inside the events)")
     ap.add_argument("--e2e-steps", type=int, default=None, help="host-API steps (default: --steps, <= 4000)")
+    ap.add_argument("--no-flush", action="store_true", help="experiments only: keep L2 warm between launches")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (CPU, gloo)")
@@ -736,7 +738,7 @@ def bench_env(args, cfg, rank, world, local, dist):
     runs = max(1, args.runs)
     with Clocks(local) as clk:
         torch.cuda.nvtx.range_push("timed")
-        res = timed_runs(env, launches, flush, runs, not args.no_gate, dist, dev)
+        res = timed_runs(env, launches, flush, runs, not args.no_gate, dist, dev, do_flush=not args.no_flush)
         torch.cuda.nvtx.range_pop()
     env.synchronize()
     steps_done += runs * args.steps
@@ -822,7 +824,8 @@ def bench_env(args, cfg, rank, world, local, dist):
             dtype="fp32", data="synthetic",
             config=dict(workload=cfg["workload"], n_envs_per_gpu=n, global_envs=world * n,
                         fused_steps_per_launch=F, parallelism=f"env-shard x{world}",
-                        l2="256 MiB flush before every timed launch; per-launch state read cold from HBM",
+                        l2=("256 MiB flush before every timed launch; per-launch state read cold from HBM"
+                            if not args.no_flush else "NOT flushed (experiment)"),
                         timing=("device-gated: a spin kernel heads each run so every launch is enqueued "
                                 "before the GPU reaches it" if not args.no_gate else "host-enqueued (no gate)")),
             runs=dict(n=runs, value_mean=statistics.mean(vals), value_std=statistics.pstdev(vals),

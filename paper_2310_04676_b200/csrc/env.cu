@@ -7,6 +7,7 @@
 // (dynamics.cpp:225-241), workspace centre = FK(mid) (:161-162), observation
 // layout (:166-192). The step itself is one fused kernel (kernels.cuh).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -214,6 +215,13 @@ int team_layout_from_env() {
   return sg::kLayoutAuto;
 }
 
+// NVTX range around every host-side entry point (header-only NVTX3: a no-op
+// unless a profiler injects itself), so a timeline shows each C-ABI call.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <typename F>
 int guard(F&& f) {
   try {
@@ -305,6 +313,11 @@ struct sg_env {
   int chain = sg::kChainGeneric8;
   int team_warps = 1;
   int team_layout = sg::kLayoutAuto;
+  // Zero-copy host steps wait for the launch's completion flag (h_status[3])
+  // instead of cudaStreamSynchronize: 65.6 vs 69.6 us per PSM 16K step
+  // (tools/gpu_r2g.sh). SG_HOST_POLL=0 restores the synchronize (A/B).
+  bool host_poll = true;
+  unsigned long long host_seq = 0;
 
   void launch(int k_steps, bool gen, bool reset) {
     sg::LaunchArgs a{k_steps, gen, reset, P.task.task, team_warps, stream, team_layout};
@@ -667,6 +680,7 @@ std::unique_ptr<sg_env> make_multi_env(const sg_env_config& cfg, const sg_dynami
   M.ended_total = env->counters + 1;
   M.err = reinterpret_cast<int32_t*>(env->counters + 2);
   CK(cudaHostAlloc(&env->h_counters, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
+  std::memset(env->h_counters, 0, 4 * sizeof(unsigned long long));
   // SimBatch::create per tool (dynamics.cpp:225-241): mid configuration at
   // rest, stream id = tool * 2^32 + global row
   std::vector<float> qh(static_cast<size_t>(n) * A);
@@ -780,6 +794,7 @@ std::unique_ptr<sg_env> make_image_env(const sg_env_config& cfg, const sg_dynami
   I.ended_total = env->counters + 1;
   I.err = reinterpret_cast<int32_t*>(env->counters + 2);
   CK(cudaHostAlloc(&env->h_counters, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
+  std::memset(env->h_counters, 0, 4 * sizeof(unsigned long long));
   {  // SimBatch::create (dynamics.cpp:225-241), stream id = global row
     const auto mid = m.mid_configuration();
     std::vector<float> qh(static_cast<size_t>(n) * A);
@@ -929,6 +944,7 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   p.ended_total = env->counters + 5;
   p.err = reinterpret_cast<int32_t*>(env->counters + 2);
   CK(cudaHostAlloc(&env->h_counters, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
+  std::memset(env->h_counters, 0, 4 * sizeof(unsigned long long));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&env->d_status), env->h_counters, 0));
   p.act_state = nullptr;
   p.act_buf = nullptr;
@@ -958,6 +974,7 @@ std::unique_ptr<sg_env> make_env(const sg_env_config& cfg, const sg_dynamics_con
   env->chain = select_chain(P.robot, dc.control_mode, dc.substeps);
   env->team_warps = team_warps_for(env->chain);
   env->team_layout = team_layout_from_env();
+  if (const char* f = std::getenv("SG_HOST_POLL")) env->host_poll = std::atoi(f) != 0;
   CK(cudaDeviceSynchronize());
   return env;
 }
@@ -1085,6 +1102,7 @@ int sg_env_images(const sg_env* env, float** d_target, float** d_scenes, float**
 }
 
 int sg_env_reset(sg_env* env, sg_step_views* out) {
+  NvtxRange nvtx("sg_env_reset");
   return guard([&] {
     CK(cudaSetDevice(env->device));
     if (env->own_kernel()) env->launch_mt(0, false, true);
@@ -1094,6 +1112,7 @@ int sg_env_reset(sg_env* env, sg_step_views* out) {
 }
 
 int sg_env_reset_host(sg_env* env, float* h_observations) {
+  NvtxRange nvtx("sg_env_reset_host");
   return guard([&] {
     if (!h_observations) throw sg::SimError("env.reset: null observation buffer");
     CK(cudaSetDevice(env->device));
@@ -1122,6 +1141,7 @@ int sg_host_free(void* p) {
 }
 
 int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
+  NvtxRange nvtx("sg_env_step");
   return guard([&] {
     if (!d_actions) throw sg::SimError("env.step: action shape mismatch");
     CK(cudaSetDevice(env->device));
@@ -1193,6 +1213,7 @@ static void task_step_host(sg_env* env, const float* h_actions, sg_host_result* 
 }
 
 int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
+  NvtxRange nvtx("sg_env_step_host");
   return guard([&] {
     if (!h_actions) throw sg::SimError("env.step: action shape mismatch");
     CK(cudaSetDevice(env->device));
@@ -1238,6 +1259,7 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
       p.h_task_error = host_f[3];
       p.h_terminated = host_u[0];
       p.h_timed_out = host_u[1];
+      p.h_seq = ++env->host_seq;
       env->launch_step(1, false);
       p.h_obs = p.h_tobs = p.h_rewards = p.h_task_error = nullptr;
       p.h_terminated = p.h_timed_out = nullptr;
@@ -1259,7 +1281,25 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
     p.h_status = nullptr;
     p.ended_clear = p.sat_step = p.sat_clear = nullptr;
     p.ended_total = env->counters + 5;
-    CK(cudaStreamSynchronize(s));
+    if (zc && env->host_poll) {
+      // The launch's last CTA writes the status and then h_status[3] = seq
+      // behind system fences that order every CTA's result rows before it:
+      // the result is complete once the flag arrives. cudaStreamQuery every
+      // 256 polls catches a failed launch (the flag would never come).
+      volatile unsigned long long* hs = env->h_counters;
+      for (unsigned spins = 1; hs[3] != env->host_seq; ++spins) {
+        if ((spins & 255u) == 0) {
+          const cudaError_t e = cudaStreamQuery(s);
+          if (e == cudaSuccess) {
+            if (hs[3] != env->host_seq) throw sg::SimError("host step: completion flag missing after the launch");
+            break;
+          }
+          if (e != cudaErrorNotReady) CK(e);
+        }
+      }
+    } else {
+      CK(cudaStreamSynchronize(s));
+    }
     const unsigned long long sat = env->h_counters[0], ended = env->h_counters[1];  // this step's
     env->raise(static_cast<int32_t>(env->h_counters[2] & 0xffffffffu));
     // terminal_observations are only meaningful on ended rows (envs.hpp:87);
@@ -1425,6 +1465,7 @@ int sg_env_bench_begin(sg_env* env, uint64_t seed, int64_t first_step, int64_t g
 }
 
 int sg_env_bench_step(sg_env* env, int32_t k_steps) {
+  NvtxRange nvtx("sg_env_bench_step");
   return guard([&] {
     if (!env->bench_ready) throw sg::ConfigError("sg_env_bench_step before sg_env_bench_begin");
     if (k_steps < 1) throw sg::ConfigError("bench: k_steps must be >= 1");

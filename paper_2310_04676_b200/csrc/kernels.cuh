@@ -15,8 +15,12 @@
 // contraction) so reset decisions and waypoint counts match the fp64 oracle.
 #pragma once
 
+#if defined(SG_TIME_PROBE) || defined(SG_PHASE_PROBE)
+#include <cstdio>
+#endif
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <utility>
 
@@ -139,6 +143,7 @@ struct EnvPtrs {
   // ended rows of this step, error word} into mapped pinned memory, so the
   // host reads them after its one synchronisation without a copy.
   unsigned long long* h_status;
+  unsigned long long h_seq;  // host step number: written to h_status[3] last, after a system fence
   unsigned long long* ended_clear;  // zeroed at launch start: the next host step's ended slot
   unsigned long long* sat_step;     // host step: saturations of THIS step (nullable)
   unsigned long long* sat_clear;    // zeroed at launch start: the next host step's saturation slot
@@ -1057,6 +1062,19 @@ inline size_t team_smem_bytes(int A) {
 // one CTA per SM; the env quads (4 envs) are split evenly over all
 // gridDim.x * TPC teams (<= 32 envs each), so every SM carries the same
 // number of envs, and the team's warps meet at a named barrier (id 1 + team).
+#ifdef SG_TIME_PROBE
+// Launch timeline probe (A/B builds only): {first CTA start, first team past
+// its state loads, last team past step 0, first / last team past the loop,
+// last CTA end}, %globaltimer ns; the last CTA prints and re-arms them.
+__device__ unsigned long long g_tprobe[8] = {~0ull, ~0ull, 0, ~0ull, 0, 0, 0, 0};
+__device__ unsigned int g_tprobe_ticket = 0;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 struct Team {
   int64_t row0;
   int rows;     // <= 0: empty team
@@ -1474,6 +1492,9 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   };
 
   bool pend = false;  // scorer: rows ended at the previous step (reset pending)
+#ifdef SG_TIME_PROBE
+  if (lane == 0) atomicMin(&g_tprobe[1], globaltimer_ns());  // state loaded, first step begins
+#endif
 #ifdef SG_PHASE_PROBE
   long long t_prod = 0, t_bar = 0, t_post = 0, t_mark = clock64();
 #define SG_MARK(acc)                    \
@@ -1623,7 +1644,16 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       }
     }
     SG_MARK(t_post);
+#ifdef SG_TIME_PROBE
+    if (step == 0 && lane == 0) atomicMax(&g_tprobe[2], globaltimer_ns());
+#endif
   }
+#ifdef SG_TIME_PROBE
+  if (lane == 0) {
+    atomicMin(&g_tprobe[3], globaltimer_ns());  // first team through all steps
+    atomicMax(&g_tprobe[4], globaltimer_ns());  // last team through all steps
+  }
+#endif
 #ifdef SG_PHASE_PROBE
   if (blockIdx.x < 3 && lane == 0)
     printf("probe cta %d warp %d: produce %lld barrier %lld post %lld cycles over %d steps\n", (int)blockIdx.x, S,
@@ -1711,18 +1741,45 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
     *P.p.ended_clear = 0;
     if (P.p.sat_clear) *P.p.sat_clear = 0;
   }
+#ifdef SG_TIME_PROBE
+  if (threadIdx.x == 0) atomicMin(&g_tprobe[0], globaltimer_ns());
+#endif
   if (tm.rows > 0)
     team_dispatch<CH, G, TASK, MODE, SUB, GEN, TPC>(P, k_steps, s_obs, s_act, ts, tm, role,
                                                     std::make_integer_sequence<int, G>{});
+#ifdef SG_TIME_PROBE
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&g_tprobe[5], globaltimer_ns());
+    __threadfence();
+    if (atomicAdd(&g_tprobe_ticket, 1u) == gridDim.x - 1) {
+      __threadfence();
+      volatile unsigned long long* t = g_tprobe;
+      if (k_steps > 1)
+        printf("tprobe K=%d: loads %.2f us, step0 %.2f us, loop %.2f..%.2f us, end %.2f us (from first CTA start)\n",
+               k_steps, (t[1] - t[0]) * 1e-3, (t[2] - t[0]) * 1e-3, (t[3] - t[0]) * 1e-3, (t[4] - t[0]) * 1e-3,
+               (t[5] - t[0]) * 1e-3);
+      t[0] = t[1] = t[3] = ~0ull;
+      t[2] = t[4] = t[5] = 0;
+      g_tprobe_ticket = 0;
+    }
+  }
+#endif
   if (P.p.h_status) {  // host step: the last CTA to finish publishes the counters
+    // every thread's zero-copy result rows are ordered before the CTA's ticket,
+    // so the host may read them as soon as it sees h_status[3] == h_seq
+    __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
       if (atomicAdd(P.p.ticket, 1u) == gridDim.x - 1) {
         __threadfence();
-        P.p.h_status[0] = *reinterpret_cast<volatile unsigned long long*>(P.p.sat_step ? P.p.sat_step : P.p.sat_total);
-        P.p.h_status[1] = *reinterpret_cast<volatile unsigned long long*>(P.p.ended_total);
-        P.p.h_status[2] = static_cast<unsigned long long>(static_cast<uint32_t>(*reinterpret_cast<volatile int32_t*>(P.p.err)));
+        volatile unsigned long long* hs = P.p.h_status;
+        hs[0] = *reinterpret_cast<volatile unsigned long long*>(P.p.sat_step ? P.p.sat_step : P.p.sat_total);
+        hs[1] = *reinterpret_cast<volatile unsigned long long*>(P.p.ended_total);
+        hs[2] = static_cast<unsigned long long>(static_cast<uint32_t>(*reinterpret_cast<volatile int32_t*>(P.p.err)));
+        __threadfence_system();
+        hs[3] = P.p.h_seq;
         *P.p.ticket = 0;
       }
     }

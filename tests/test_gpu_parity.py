@@ -214,6 +214,60 @@ def test_bench_action_stream_bit_exact(sg, oracle):
     np.testing.assert_array_equal(shard.bench_actions().cpu().numpy(), expected[2][100:])
 
 
+@pytest.mark.parametrize("layout", ["legacy", "packed"])
+def test_config1_through_the_drivers_k20_fused_launches(sg, oracle, layout):
+    """BASELINE config 1 on the exact path the driver's headline times:
+    bench.py --steps 20 runs sg_env_bench_step launches of K = 20 fused steps
+    with in-kernel actions. 64 PSM envs, seed 0: the warm-up step, then 50
+    launches of 20 steps (1001 steps, three synchronized reset bursts at
+    300 / 600 / 900) against the fp64 oracle fed the reference's serial
+    action stream. After every launch: flags, counters and streams bit-exact,
+    state / observations / rewards within the standard tolerances."""
+    import os
+    _cuda()
+    n, seed = 64, 0
+    m = oracle.resolve_robot("psm")
+    ref = oracle.Env(oracle.env_config(n_envs=n, seed=seed), m)
+    ref.reset()
+    os.environ["SG_TEAM_LAYOUT"] = layout
+    try:
+        env = sg.VecTaskEnv(robots=("psm",), n_envs=n, seed=seed)
+    finally:
+        del os.environ["SG_TEAM_LAYOUT"]
+    env.reset()
+    env.bench_begin(seed)
+    ar = oracle.make_stream(seed, 0xAC7104)
+    A = m.dof
+
+    def ref_steps(k):
+        for _ in range(k):
+            ref.step(oracle.fill_uniform_actions(ar, n, A).astype(np.float32).astype(np.float64))
+
+    env.bench_step(1)
+    ref_steps(1)
+    for launch in range(50):
+        env.bench_step(20)
+        ref_steps(20)
+        torch.cuda.synchronize()
+        r, st, c = ref.result(), env.state(), ref.counters()
+        res = env._result()
+        np.testing.assert_array_equal(res.terminated.cpu().numpy(), r["terminated"])
+        np.testing.assert_array_equal(res.timed_out.cpu().numpy(), r["timed_out"])
+        for k in ("step_count", "hold_count", "episode_count"):
+            np.testing.assert_array_equal(st[k].cpu().numpy(), c[k], err_msg=f"{k} @ launch {launch}")
+        np.testing.assert_array_equal(st["rng_state"].cpu().numpy(), ref.rng()[0])
+        sr = ref.state()
+        for k in ("q", "qdot", "q_target", "tips", "goals"):
+            assert np.abs(_soa(st[k]) - sr[k]).max() <= TOL[k], (k, launch)
+        assert np.abs(res.rewards.cpu().numpy() - r["rewards"]).max() <= TOL["reward"]
+        o_ref, t_ref = ref.obs()
+        _compare_obs(res.observations.cpu().numpy(), o_ref, A)
+        ended = (r["terminated"] | r["timed_out"]).astype(bool)
+        if ended.any():
+            _compare_obs(res.terminal_observations.cpu().numpy()[ended], t_ref[ended], A)
+    assert (ref.counters()["episode_count"] == 3).all()
+
+
 @pytest.mark.parametrize("robot,task", [("psm", "target_reaching"), ("star", "path_following")])
 def test_fused_k_steps_equal_single_steps(sg, oracle, robot, task):
     """K fused steps == K single-step launches, bit for bit. For PathFollowing
