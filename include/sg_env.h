@@ -144,6 +144,17 @@ typedef struct sg_step_views {
   int32_t action_dim;
 } sg_step_views;
 
+/* Caller-owned DEVICE destinations of one step's results (sg_env_step_into):
+ * observations row-major n_envs x obs_dim (stride obs_dim), the per-env
+ * fields n_envs long. NULL fields go to the env's own buffers. */
+typedef struct sg_step_out {
+  float* observations;
+  float* rewards;
+  float* task_error;
+  uint8_t* terminated;
+  uint8_t* timed_out;
+} sg_step_out;
+
 /* Host copy of one StepResult (sg_env_step_host). Any pointer may be NULL
  * to skip that field's device->host copy. */
 typedef struct sg_host_result {
@@ -229,6 +240,11 @@ int sg_host_alloc(size_t bytes, void** out);
 int sg_host_free(void* p);
 /* d_actions: device, row-major n_envs x action_dim fp32 (stride = action_dim). */
 int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out);
+/* sg_env_step writing the step's observations / rewards / task_error / flags
+ * straight into caller device buffers (a trainer's rollout-buffer slot:
+ * ppo.cpp:280-299 stores exactly these), instead of the env's own buffers
+ * and a copy per field. terminal_observations stay env-owned (views). */
+int sg_env_step_into(sg_env* env, const float* d_actions, const sg_step_out* dst, sg_step_views* out);
 /* Host actions (pinned or pageable): H2D copy, step, D2H copy of the fields
  * requested in `out`, synchronise, report errors. terminal_observations is
  * copied only on steps where at least one row ended (it is defined on ended
@@ -296,6 +312,13 @@ int sg_policy_bootstrap(const sg_policy* policy, const float* d_terminal_obs, in
 int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const float* d_log_std_raw,
                      uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos,
                      uint64_t step_offset, float* d_actions, float* d_logp, void* stream);
+/* Forward + rollout sampling in ONE tensor-core launch (the trainer's per-step
+ * policy call, ppo.cpp:262-277): sg_policy_forward's value (and mean, when
+ * d_mean != NULL) plus sg_policy_sample's actions / logp from the same draws,
+ * bit-identical to the two separate calls. action_dim <= 16. */
+int sg_policy_act(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
+                  const float* d_log_std_raw, uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos,
+                  uint64_t step_offset, float* d_actions, float* d_logp, float* d_mean, float* d_value, void* stream);
 /* compute_gae (rollout.cpp:42-66, time-major [n_steps][n_envs]) without the
  * normalisation, plus episode statistics (ppo.cpp:286-303) accumulated into
  * d_stats4 = {reward_sum, episode_reward_sum, final_error_sum, episodes}. */
@@ -326,10 +349,12 @@ int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d
 int sg_elu_forward(const void* d_z, void* d_h, int64_t count, int32_t dtype, void* stream);
 int sg_elu_backward(const void* d_h, const void* d_dh, void* d_dz, int64_t count, int32_t dtype, void* stream);
 /* Minibatch gather (ppo.cpp:173-190): rows d_idx[0..m) of the rollout buffer:
- * obs (obs_w fp32 per row, obs_w % 4 == 0) into d_obs_out (fp32, or bf16 when
- * obs_bf16), actions (A fp32), old log-probs, advantages, returns. */
+ * obs (obs_w fp32 per row) into d_obs_out rows of obs_out_w >= obs_w (fp32, or
+ * bf16 when obs_bf16; columns past obs_w zero), actions (A fp32), old
+ * log-probs, advantages, returns. */
 int sg_ppo_gather(const int64_t* d_idx, int64_t m, const float* d_obs, int32_t obs_w, void* d_obs_out,
-                  int32_t obs_bf16, const float* d_act, int32_t A, float* d_act_out, const float* d_logp,
+                  int32_t obs_out_w, int32_t obs_bf16, const float* d_act, int32_t A, float* d_act_out,
+                  const float* d_logp,
                   float* d_logp_out, const float* d_adv, float* d_adv_out, const float* d_ret, float* d_ret_out,
                   void* stream);
 /* The data part of ppo_loss_and_grad (ppo.cpp:90-154) in one pass over a

@@ -1140,6 +1140,59 @@ int sg_host_free(void* p) {
   });
 }
 
+int sg_env_step_into(sg_env* env, const float* d_actions, const sg_step_out* dst, sg_step_views* out) {
+  NvtxRange nvtx("sg_env_step_into");
+  return guard([&] {
+    if (!d_actions) throw sg::SimError("env.step: action shape mismatch");
+    CK(cudaSetDevice(env->device));
+    const sg_step_out none{};
+    const sg_step_out& d = dst ? *dst : none;
+    if (env->own_kernel()) {  // task kernels: step, then device copies into the caller's buffers
+      env->M.actions = d_actions;
+      env->I.actions = d_actions;
+      env->launch_mt(1, false, false);
+      sg_step_views v;
+      env->views(&v);
+      const auto cp = [&](void* to, const void* from, size_t bytes) {
+        if (to) CK(cudaMemcpyAsync(to, from, bytes, cudaMemcpyDeviceToDevice, env->stream));
+      };
+      cp(d.observations, v.observations, env->n * env->O * sizeof(float));
+      cp(d.rewards, v.rewards, env->n * sizeof(float));
+      cp(d.task_error, v.task_error, env->n * sizeof(float));
+      cp(d.terminated, v.terminated, env->n);
+      cp(d.timed_out, v.timed_out, env->n);
+      env->views(out);
+      return;
+    }
+    // the step kernel writes these fields only: point it at the caller's
+    // buffers for this launch (restored on every exit path)
+    if (d.observations && (reinterpret_cast<uintptr_t>(d.observations) & 15u) != 0)
+      throw sg::ConfigError("sg_env_step_into: observations must be 16-byte aligned");
+    auto& p = env->P.p;
+    struct Restore {
+      sg::EnvPtrs& p;
+      float *obs, *rewards, *task_error;
+      uint8_t *terminated, *timed_out;
+      ~Restore() {
+        p.obs = obs;
+        p.rewards = rewards;
+        p.task_error = task_error;
+        p.terminated = terminated;
+        p.timed_out = timed_out;
+      }
+    } restore{p, p.obs, p.rewards, p.task_error, p.terminated, p.timed_out};
+    if (d.observations) p.obs = d.observations;
+    if (d.rewards) p.rewards = d.rewards;
+    if (d.task_error) p.task_error = d.task_error;
+    if (d.terminated) p.terminated = d.terminated;
+    if (d.timed_out) p.timed_out = d.timed_out;
+    env->P.actions = d_actions;
+    env->P.actions_aligned = (reinterpret_cast<uintptr_t>(d_actions) & 15u) == 0;
+    env->launch_step(1, false);
+    env->views(out);
+  });
+}
+
 int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
   NvtxRange nvtx("sg_env_step");
   return guard([&] {

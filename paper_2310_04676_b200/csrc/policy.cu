@@ -131,15 +131,22 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void async_proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// 16 consecutive fp32 accumulator columns of this thread's TMEM lane.
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+// 16 consecutive fp32 accumulator columns of this thread's TMEM lane, issued
+// without waiting (tcgen05.ld is asynchronous until tcgen05.wait::ld, which
+// covers every load the thread issued before it).
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  tmem_ld16_async(taddr, r);
+  tmem_wait_ld();
 #pragma unroll
   for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
 }
@@ -154,22 +161,32 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // Epilogue for a hidden layer: this warp's column group of TMEM columns
 // [c0, c0+N) for its row -> +bias -> ELU -> bf16 -> K-major A tile (128 rows).
 // Warp w reads TMEM lane quarter w%4 (hardware rule) and column group w/4.
+// The thread's columns are read from TMEM in batches of up to 64 (four x16
+// loads behind ONE wait) so the load latency is exposed once per batch.
 template <int N>
 __device__ __forceinline__ void epi_hidden(uint32_t tmem_row, uint32_t c0, const float* __restrict__ bias,
                                            uint8_t* a_base, int row, int group) {
   constexpr int kPer = N / kGroups;
+  constexpr int kBatch = kPer < 64 ? kPer : 64;
 #pragma unroll
-  for (int cc = 0; cc < kPer; cc += 16) {
-    const int c = group * kPer + cc;
-    float v[16];
-    tmem_ld16(tmem_row + c0 + c, v);
-    uint32_t p[8];
+  for (int cb = 0; cb < kPer; cb += kBatch) {
+    uint32_t r[kBatch / 16][16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) p[k] = pack_bf16(elu(v[2 * k] + bias[c + 2 * k]), elu(v[2 * k + 1] + bias[c + 2 * k + 1]));
-    uint4* d0 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c, kRows));
-    uint4* d1 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c + 8, kRows));
-    *d0 = make_uint4(p[0], p[1], p[2], p[3]);
-    *d1 = make_uint4(p[4], p[5], p[6], p[7]);
+    for (int j = 0; j < kBatch / 16; ++j) tmem_ld16_async(tmem_row + c0 + group * kPer + cb + 16 * j, r[j]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < kBatch / 16; ++j) {
+      const int c = group * kPer + cb + 16 * j;
+      uint32_t p[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        p[k] = pack_bf16(elu(__uint_as_float(r[j][2 * k]) + bias[c + 2 * k]),
+                         elu(__uint_as_float(r[j][2 * k + 1]) + bias[c + 2 * k + 1]));
+      uint4* d0 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c, kRows));
+      uint4* d1 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c + 8, kRows));
+      *d0 = make_uint4(p[0], p[1], p[2], p[3]);
+      *d1 = make_uint4(p[4], p[5], p[6], p[7]);
+    }
   }
 }
 
@@ -185,6 +202,59 @@ __device__ __forceinline__ void issue_layer(uint32_t d_tmem, uint32_t a_addr, ui
   }
 }
 
+// ---- rollout sampling (ppo.cpp:262-277) ------------------------------------
+// The reference draws z for (env e, dim i) from ONE trainer stream
+// make_stream(seed, 0x7261696e) in row-major order, 2 u32 per Box-Muller
+// normal. Each thread jumps its copy of that stream to draw
+// pos + step_off + 2*(e*A + i) (O(log k) PCG32 jump table) so the device
+// consumes exactly the reference's u32 sequence.
+struct Jump64 {
+  uint64_t mult[64];
+  uint64_t add[64];
+};
+
+__device__ __forceinline__ uint32_t pcg32_next(uint64_t& s, uint64_t inc) {
+  const uint64_t old = s;
+  s = old * 6364136223846793005ULL + inc;
+  const uint32_t xs = (uint32_t)(((old >> 18u) ^ old) >> 27u), rot = (uint32_t)(old >> 59u);
+  return (xs >> rot) | (xs << ((32u - rot) & 31u));
+}
+
+// One (env, dim) draw of the rollout sampling at PCG32 state s (consumes 2
+// u32), fp64 throughout like the reference: the standard normal z (Box-Muller,
+// rng.hpp:53-57), the dim's log-prob term -z^2/2 - ls - log(2 pi)/2, and the
+// action mean + exp(ls) z rounded once to fp32. z and the term depend on the
+// stream and log-std only, so the fused kernel draws them before the MLP.
+__device__ __forceinline__ double clamp_log_std(float log_std_raw) {
+  const double ls = (double)log_std_raw;
+  return ls < -5.0 ? -5.0 : (ls > 2.0 ? 2.0 : ls);  // Policy::log_std clamp (policy.hpp:28-29)
+}
+__device__ __forceinline__ double draw_normal(uint64_t& s, uint64_t inc) {
+  const double u1 = __dmul_rn(__dadd_rn((double)pcg32_next(s, inc), 0.5), 0x1.0p-32);
+  const double u2 = (double)pcg32_next(s, inc) * 0x1.0p-32;
+  return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586477, u2)));
+}
+__device__ __forceinline__ double logp_term(double z, double ls) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(-0.5, z), z), -ls), -0.9189385332046727);
+}
+__device__ __forceinline__ float action_of(float mean, double z, double ls) {
+  return (float)__dadd_rn((double)mean, __dmul_rn(exp(ls), z));
+}
+__device__ __forceinline__ float draw_action(uint64_t& s, uint64_t inc, float mean, float log_std_raw, double& term) {
+  const double ls = clamp_log_std(log_std_raw);
+  const double z = draw_normal(s, inc);
+  term = logp_term(z, ls);
+  return action_of(mean, z, ls);
+}
+
+// s0 advanced by k draws (J[b] = 2^b-step advance).
+__device__ __forceinline__ uint64_t jump(uint64_t s0, uint64_t k, const Jump64& J) {
+  uint64_t s = s0;
+  for (int b = 0; k; ++b, k >>= 1)
+    if (k & 1) s = s * J.mult[b] + J.add[b];
+  return s;
+}
+
 struct FwdArgs {
   const float* obs;  // n x obs_stride fp32 (first obs_dim columns used)
   int64_t n;
@@ -198,10 +268,19 @@ struct FwdArgs {
   // without such rows exit before any tensor-core work.
   const uint8_t* timed_out;
   const uint8_t* terminated;
+  // fused rollout sampling (ppo.cpp:262-277), when actions != null: the
+  // trainer-stream draws of every (row, dim) at pos + step_off + 2 (row A + dim)
+  const float* log_std_raw;
+  uint64_t s0, inc;
+  const uint64_t* pos;
+  uint64_t step_off;
+  float* actions;
+  float* logp;
 };
 
 __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_constant__ PolicyImage W,
-                                                                 const __grid_constant__ FwdArgs args) {
+                                                                 const __grid_constant__ FwdArgs args,
+                                                                 const __grid_constant__ Jump64 J) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t row0 = (int64_t)blockIdx.x * kRows;
@@ -216,16 +295,15 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
       return;
     }
   }
-  float* sbias = reinterpret_cast<float*>(smem + kBias);
-  for (int k = tid; k < 928; k += kThreads) sbias[k] = W.b1[k];  // the 7 bias vectors are contiguous
+  float* sbias = reinterpret_cast<float*>(smem + kBias);  // the 7 bias vectors, bulk-copied (contiguous)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBar + 64);
   const uint32_t bar_w1 = smem_u32(&bars[0]), bar_w2 = smem_u32(&bars[1]), bar_w34 = smem_u32(&bars[2]);
-  const uint32_t bar_mma = smem_u32(&bars[3]);
+  const uint32_t bar_mma = smem_u32(&bars[3]), bar_bias = smem_u32(&bars[4]);
   const uint32_t sbase = smem_u32(smem);
 
   if (tid == 0) {
-    for (int b = 0; b < 4; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    for (int b = 0; b < 5; ++b) mbar_init(smem_u32(&bars[b]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {  // TMEM: all 512 columns (one CTA per SM)
@@ -233,7 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   __syncthreads();
-  if (tid == 0) {  // stream the first weights while the obs tile is converted
+  if (tid == 0) {  // stream the biases and the first weights while the obs tile is converted
+    bulk_load(sbase + kBias, W.b1, 928 * 4, bar_bias);
     bulk_load(sbase + kW1, W.w1, 32768, bar_w1);
     bulk_load(sbase + kW2, W.w2a, 65536, bar_w2);
   }
@@ -269,6 +348,30 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     issue_layer(tmem + 256, sbase + kX0, kRows, sbase + kW1 + kmajor_off(256, 0, 512), 512, kK0, 256);
     mma_commit(bar_mma);
   }
+  // Fused sampling, stream part: the normals and log-prob terms of this
+  // thread's (row, dim) draws depend on the trainer stream and the log-std
+  // only, so they are drawn while layer 1 runs on the tensor cores (dims
+  // group, group + 4, ...: one jump to the first draw, then + 8 draws per dim).
+  constexpr int kDraws = kNOut / kGroups;
+  double zs[kDraws], terms[kDraws];
+  const int64_t srow = row0 + row;
+  const bool sampling = args.actions != nullptr && srow < args.n && group < args.act_dim;
+  if (sampling) {
+    const int A = args.act_dim;
+    uint64_t st = jump(args.s0, *args.pos + args.step_off + 2ull * ((uint64_t)srow * (uint64_t)A + (uint64_t)group), J);
+#pragma unroll
+    for (int j = 0; j < kDraws; ++j) {
+      const int d = group + j * kGroups;
+      zs[j] = terms[j] = 0.0;
+      if (d < A) {
+        uint64_t t = st;
+        zs[j] = draw_normal(t, args.inc);
+        terms[j] = logp_term(zs[j], clamp_log_std(args.log_std_raw[d]));
+        st = st * J.mult[3] + J.add[3];
+      }
+    }
+  }
+  mbar_wait(bar_bias, 0);  // bulk-copied biases visible to this thread
   mbar_wait(bar_mma, mma_phase);
   mma_phase ^= 1;
   tc_fence_after();
@@ -315,12 +418,15 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   mbar_wait(bar_mma, mma_phase);
   mma_phase ^= 1;
   tc_fence_after();
+  float mv[kNOut];  // the actor's output row (group 0), kept for the fused sampling
   if (group == 0) {
     float v[16];
     tmem_ld16(tmem_row + 192, v);
+#pragma unroll
+    for (int k = 0; k < kNOut; ++k) mv[k] = v[k] + sbias[896 + k];
     if (row0 + row < args.n && args.mean) {
       float* dst = args.mean + (row0 + row) * args.act_dim;
-      for (int k = 0; k < args.act_dim; ++k) dst[k] = v[k] + sbias[896 + k];
+      for (int k = 0; k < args.act_dim; ++k) dst[k] = mv[k];
     }
   }
   // ---- critic: h1 waits in cols 256..511
@@ -365,6 +471,36 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     float v[16];
     tmem_ld16(tmem_row + 192, v);
     if (row0 + row < args.n) args.value[row0 + row] = boot_row ? v[0] + sbias[912] : 0.f;
+  }
+  if (args.actions) {
+    // Fused sampling, action part: the mean rows go to the (now idle) A3
+    // region, each thread forms the actions of its draws, the per-dim
+    // log-prob terms meet in A2 and group 0 sums them in dim order -- the same
+    // arithmetic as policy_sample_kernel.
+    float* smean = reinterpret_cast<float*>(smem + kA3);   // 128 x 16 fp32
+    double* sterm = reinterpret_cast<double*>(smem + kA2); // 128 x 16 fp64
+    if (group == 0) {
+#pragma unroll
+      for (int k = 0; k < kNOut; ++k) smean[row * kNOut + k] = mv[k];
+    }
+    __syncthreads();
+    const int A = args.act_dim;
+    if (sampling) {
+#pragma unroll
+      for (int j = 0; j < kDraws; ++j) {
+        const int d = group + j * kGroups;
+        if (d < A) {
+          args.actions[srow * A + d] = action_of(smean[row * kNOut + d], zs[j], clamp_log_std(args.log_std_raw[d]));
+          sterm[row * kNOut + d] = terms[j];
+        }
+      }
+    }
+    __syncthreads();
+    if (group == 0 && srow < args.n) {
+      double lp = 0.0;
+      for (int d = 0; d < A; ++d) lp = __dadd_rn(lp, sterm[row * kNOut + d]);
+      args.logp[srow] = (float)lp;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -442,24 +578,6 @@ __global__ void policy_pack_kernel(const float* __restrict__ flat, const __grid_
   }
 }
 
-// ---- rollout sampling (ppo.cpp:262-277) ------------------------------------
-// The reference draws z for (env e, dim i) from ONE trainer stream
-// make_stream(seed, 0x7261696e) in row-major order, 2 u32 per Box-Muller
-// normal. Each thread jumps its copy of that stream to draw
-// pos + step_off + 2*(e*A + i) (O(log k) PCG32 jump table) so the device
-// consumes exactly the reference's u32 sequence.
-struct Jump64 {
-  uint64_t mult[64];
-  uint64_t add[64];
-};
-
-__device__ __forceinline__ uint32_t pcg32_next(uint64_t& s, uint64_t inc) {
-  const uint64_t old = s;
-  s = old * 6364136223846793005ULL + inc;
-  const uint32_t xs = (uint32_t)(((old >> 18u) ^ old) >> 27u), rot = (uint32_t)(old >> 59u);
-  return (xs >> rot) | (xs << ((32u - rot) & 31u));
-}
-
 __global__ void policy_sample_kernel(const float* __restrict__ mean, int64_t n, int A,
                                      const float* __restrict__ log_std_raw, uint64_t s0, uint64_t inc,
                                      const uint64_t* __restrict__ pos, uint64_t step_off,
@@ -467,20 +585,12 @@ __global__ void policy_sample_kernel(const float* __restrict__ mean, int64_t n, 
                                      float* __restrict__ logp) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
-  uint64_t k = *pos + step_off + 2ull * (uint64_t)e * (uint64_t)A;
-  uint64_t s = s0;
-  for (int b = 0; k; ++b, k >>= 1)
-    if (k & 1) s = s * J.mult[b] + J.add[b];
+  uint64_t s = jump(s0, *pos + step_off + 2ull * (uint64_t)e * (uint64_t)A, J);
   double lp = 0.0;
   for (int i = 0; i < A; ++i) {
-    double ls = (double)log_std_raw[i];
-    ls = ls < -5.0 ? -5.0 : (ls > 2.0 ? 2.0 : ls);  // Policy::log_std clamp (policy.hpp:28-29)
-    const double sigma = exp(ls);
-    const double u1 = __dmul_rn(__dadd_rn((double)pcg32_next(s, inc), 0.5), 0x1.0p-32);
-    const double u2 = (double)pcg32_next(s, inc) * 0x1.0p-32;
-    const double z = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586477, u2)));
-    actions[e * A + i] = (float)__dadd_rn((double)mean[e * A + i], __dmul_rn(sigma, z));
-    lp = __dadd_rn(lp, __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(-0.5, z), z), -ls), -0.9189385332046727));
+    double term;
+    actions[e * A + i] = draw_action(s, inc, mean[e * A + i], log_std_raw[i], term);
+    lp = __dadd_rn(lp, term);
   }
   logp[e] = (float)lp;
 }
@@ -758,8 +868,30 @@ int sg_policy_load_params(sg_policy* p, const float* d_flat, void* stream) {
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
 
+static sgp::Jump64 jump_table(uint64_t inc) {  // J[b] = 2^b PCG32 advances of the stream
+  sgp::Jump64 J;
+  uint64_t cm = 6364136223846793005ULL, ca = inc;
+  for (int b = 0; b < 64; ++b) {
+    J.mult[b] = cm;
+    J.add[b] = ca;
+    ca = (cm + 1) * ca;
+    cm *= cm;
+  }
+  return J;
+}
+
+struct SampleArgs {
+  const float* log_std_raw = nullptr;
+  uint64_t s0 = 0, inc = 0;
+  const uint64_t* pos = nullptr;
+  uint64_t step_off = 0;
+  float* actions = nullptr;
+  float* logp = nullptr;
+};
+
 static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, float* d_mean,
-                          float* d_value, const uint8_t* d_timed_out, const uint8_t* d_terminated, void* stream) {
+                          float* d_value, const uint8_t* d_timed_out, const uint8_t* d_terminated, void* stream,
+                          const SampleArgs& smp = SampleArgs()) {
   if (n <= 0) return SG_OK;
   sgp::PolicyImage W;
   W.w1 = p->img;
@@ -774,9 +906,12 @@ static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int
   W.b4a = p->bias + 896;
   W.b4c = p->bias + 912;
   sgp::FwdArgs a{d_obs, n, p->obs_dim, obs_stride > 0 ? obs_stride : p->obs_dim, p->act_dim, d_mean, d_value,
-                 d_timed_out, d_terminated};
+                 d_timed_out, d_terminated, smp.log_std_raw, smp.s0, smp.inc, smp.pos, smp.step_off, smp.actions,
+                 smp.logp};
+  static const sgp::Jump64 kNone{};
+  const sgp::Jump64 J = smp.actions ? jump_table(smp.inc) : kNone;
   const unsigned grid = (unsigned)((n + sgp::kRows - 1) / sgp::kRows);
-  sgp::policy_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a);
+  sgp::policy_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a, J);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
@@ -791,18 +926,28 @@ int sg_policy_bootstrap(const sg_policy* p, const float* d_terminal_obs, int64_t
   return policy_forward(p, d_terminal_obs, n, obs_stride, nullptr, d_value, d_timed_out, d_terminated, stream);
 }
 
+int sg_policy_act(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, const float* d_log_std_raw,
+                  uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos, uint64_t step_offset,
+                  float* d_actions, float* d_logp, float* d_mean, float* d_value, void* stream) {
+  if (!d_actions || !d_logp || !d_log_std_raw || !d_draw_pos || !d_value)
+    return fail(SG_ERR_CONFIG, "sg_policy_act: null argument");
+  if (p->act_dim > sgp::kNOut) return fail(SG_ERR_CONFIG, "sg_policy_act: action_dim > 16");
+  SampleArgs smp;
+  smp.log_std_raw = d_log_std_raw;
+  smp.s0 = stream_state;
+  smp.inc = stream_inc;
+  smp.pos = d_draw_pos;
+  smp.step_off = step_offset;
+  smp.actions = d_actions;
+  smp.logp = d_logp;
+  return policy_forward(p, d_obs, n, obs_stride, d_mean, d_value, nullptr, nullptr, stream, smp);
+}
+
 int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const float* d_log_std_raw,
                      uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos, uint64_t step_offset,
                      float* d_actions, float* d_logp, void* stream) {
   if (n <= 0) return SG_OK;
-  sgp::Jump64 J;
-  uint64_t cm = 6364136223846793005ULL, ca = stream_inc;
-  for (int b = 0; b < 64; ++b) {  // J[b] = 2^b advances
-    J.mult[b] = cm;
-    J.add[b] = ca;
-    ca = (cm + 1) * ca;
-    cm *= cm;
-  }
+  const sgp::Jump64 J = jump_table(stream_inc);
   const int b = 128;
   sgp::policy_sample_kernel<<<(unsigned)((n + b - 1) / b), b, 0, (cudaStream_t)stream>>>(
       d_mean, n, action_dim, d_log_std_raw, stream_state, stream_inc, d_draw_pos, step_offset, J, d_actions, d_logp);

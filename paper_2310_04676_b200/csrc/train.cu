@@ -101,7 +101,7 @@ __global__ void elu_bwd_bf16(const uint4* __restrict__ h, const uint4* __restric
 // (coalesced 128-byte rows); thread 0 also copies the row's action, log-prob,
 // advantage and return.
 __global__ void ppo_gather_kernel(const int64_t* __restrict__ idx, int64_t m, const float* __restrict__ obs,
-                                  int32_t obs_w, void* __restrict__ obs_out, int32_t obs_bf16,
+                                  int32_t obs_w, void* __restrict__ obs_out, int32_t out_w, int32_t obs_bf16,
                                   const float* __restrict__ act, int32_t A, float* __restrict__ act_out,
                                   const float* __restrict__ logp, float* __restrict__ logp_out,
                                   const float* __restrict__ adv, float* __restrict__ adv_out,
@@ -111,16 +111,25 @@ __global__ void ppo_gather_kernel(const int64_t* __restrict__ idx, int64_t m, co
   const int k = (int)(t & 7);
   if (r >= m) return;
   const int64_t src = idx[r];
-  const int n4 = obs_w >> 2;
-  const float4* so = reinterpret_cast<const float4*>(obs + src * obs_w);
-  for (int c = k; c < n4; c += 8) {
-    const float4 v = so[c];
-    if (obs_bf16) {
-      __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(obs_out) + r * obs_w + 4 * c);
-      d[0] = __floats2bfloat162_rn(v.x, v.y);
-      d[1] = __floats2bfloat162_rn(v.z, v.w);
-    } else {
-      reinterpret_cast<float4*>(static_cast<float*>(obs_out) + r * obs_w)[c] = v;
+  if ((obs_w & 3) == 0 && obs_w == out_w) {  // aligned rows: 16-byte vectors
+    const int n4 = obs_w >> 2;
+    const float4* so = reinterpret_cast<const float4*>(obs + src * obs_w);
+    for (int c = k; c < n4; c += 8) {
+      const float4 v = so[c];
+      if (obs_bf16) {
+        __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(obs_out) + r * out_w + 4 * c);
+        d[0] = __floats2bfloat162_rn(v.x, v.y);
+        d[1] = __floats2bfloat162_rn(v.z, v.w);
+      } else {
+        reinterpret_cast<float4*>(static_cast<float*>(obs_out) + r * out_w)[c] = v;
+      }
+    }
+  } else {  // unpadded rows (the env writes obs_dim-wide rows): element-wise, zero padding
+    const float* so = obs + src * obs_w;
+    for (int c = k; c < out_w; c += 8) {
+      const float v = c < obs_w ? so[c] : 0.f;
+      if (obs_bf16) static_cast<__nv_bfloat16*>(obs_out)[r * out_w + c] = __float2bfloat16_rn(v);
+      else static_cast<float*>(obs_out)[r * out_w + c] = v;
     }
   }
   if (k == 0) {
@@ -167,13 +176,13 @@ int sg_elu_backward(const void* h, const void* dh, void* dz, int64_t count, int3
   return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_SIM;
 }
 
-int sg_ppo_gather(const int64_t* idx, int64_t m, const float* obs, int32_t obs_w, void* obs_out, int32_t obs_bf16,
-                  const float* act, int32_t A, float* act_out, const float* logp, float* logp_out, const float* adv,
-                  float* adv_out, const float* ret, float* ret_out, void* stream) {
-  if (obs_w % 4) return SG_ERR_CONFIG;
+int sg_ppo_gather(const int64_t* idx, int64_t m, const float* obs, int32_t obs_w, void* obs_out, int32_t obs_out_w,
+                  int32_t obs_bf16, const float* act, int32_t A, float* act_out, const float* logp, float* logp_out,
+                  const float* adv, float* adv_out, const float* ret, float* ret_out, void* stream) {
+  if (obs_out_w < obs_w || obs_w < 1) return SG_ERR_CONFIG;
   const int64_t threads = m * 8;
   ppo_gather_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      idx, m, obs, obs_w, obs_out, obs_bf16, act, A, act_out, logp, logp_out, adv, adv_out, ret, ret_out);
+      idx, m, obs, obs_w, obs_out, obs_out_w, obs_bf16, act, A, act_out, logp, logp_out, adv, adv_out, ret, ret_out);
   return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_SIM;
 }
 

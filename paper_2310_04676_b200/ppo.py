@@ -355,7 +355,10 @@ class Trainer:
         self.g_metrics = torch.zeros(5, device=dev)
         self.graph = None
         z = lambda *s, dt=torch.float32: torch.zeros(*s, device=dev, dtype=dt)
-        self.buf = dict(obs=z(T, N, _up8(O)), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
+        # obs slot t = the policy input of rollout step t; the env writes step
+        # t's observations straight into slot t + 1 (sg_env_step_into), and
+        # slot T carries over to the next rollout's slot 0
+        self.buf = dict(obs=z(T + 1, N, O), actions=z(T, N, A), logp=z(T, N), values=z(T, N), rewards=z(T, N),
                         terminated=z(T, N, dt=torch.uint8), timed_out=z(T, N, dt=torch.uint8), boot=z(T, N),
                         task_error=z(T, N), adv=z(T, N), ret=z(T, N), last_values=z(N))
         mb = (T * N + cfg.minibatch_count - 1) // cfg.minibatch_count
@@ -364,7 +367,6 @@ class Trainer:
         self.mean = z(N, A)
         self.log_std_c = z(A)
         self.rollout_graph = None
-        self.obs_view = None
         self.ep_acc = z(N)
         self.stats = z(4, dt=torch.float64)
         self.stream_state, self.stream_inc = make_stream(cfg.seed, TRAIN_STREAM)
@@ -398,12 +400,12 @@ class Trainer:
         1.2 ms per 32-step rollout)."""
         env, b = self.env, self.buf
         N, A, T = self.N, self.A, self.T
-        if self.obs is None:
+        if self.obs is None:  # first rollout: the reset observations enter through slot T
             self.obs = env.reset()
+            b["obs"][T].copy_(self.obs)
         self.d_pos.fill_(self.draw_pos)
         if self.rollout_graph is not None:
             self.rollout_graph.replay()
-            self.obs = self.obs_view
         else:
             self._rollout_body()
             if self.use_graph:  # record (not run) the graph the next rollouts replay
@@ -422,7 +424,6 @@ class Trainer:
         finally:
             self.env.set_stream(None)
         torch.cuda.current_stream(self.dev).wait_stream(side)
-        self.obs_view = self.obs
 
     def _rollout_body(self):
         env, pol, b = self.env, self.policy, self.buf
@@ -431,27 +432,29 @@ class Trainer:
         st = self._stream()
         log_std = self.log_std_c
         log_std.copy_(self.params[self.ls_off: self.ls_off + A])
+        b["obs"][0].copy_(b["obs"][T])
         for t in range(T):
-            obs = self.obs
-            pol.forward(obs, self.mean, b["values"][t])
-            sg._pcheck(L.sg_policy_sample(self.mean.data_ptr(), N, A, log_std.data_ptr(), self.stream_state,
-                                          self.stream_inc, self.d_pos.data_ptr(),
-                                          2 * A * (t * self.global_n + self.row_off),
-                                          b["actions"][t].data_ptr(), b["logp"][t].data_ptr(), st))
-            b["obs"][t][:, :self.O].copy_(obs)
-            res = env.step(b["actions"][t])
-            b["rewards"][t].copy_(res.rewards)
-            b["terminated"][t].copy_(res.terminated)
-            b["timed_out"][t].copy_(res.timed_out)
-            b["task_error"][t].copy_(res.task_error)
+            obs = b["obs"][t]
+            # policy forward + Gaussian sampling + log-prob: one tcgen05 launch
+            sg._pcheck(L.sg_policy_act(pol._h, obs.data_ptr(), N, obs.stride(0), log_std.data_ptr(),
+                                       self.stream_state, self.stream_inc, self.d_pos.data_ptr(),
+                                       2 * A * (t * self.global_n + self.row_off), b["actions"][t].data_ptr(),
+                                       b["logp"][t].data_ptr(), None, b["values"][t].data_ptr(), st))
+            # the env writes the step's observations / rewards / flags / errors
+            # into the rollout buffer itself (ppo.cpp:280-299)
+            direct = (N * self.O) % 4 == 0  # slots 16-byte aligned: the kernel's row stores go straight in
+            res = env.step_into(b["actions"][t], observations=b["obs"][t + 1] if direct else None,
+                                rewards=b["rewards"][t], task_error=b["task_error"][t],
+                                terminated=b["terminated"][t], timed_out=b["timed_out"][t])
+            if not direct:
+                b["obs"][t + 1].copy_(res.observations)
             if self.cfg.timeout_bootstrap:
                 sg._pcheck(L.sg_policy_bootstrap(pol._h, res.terminal_observations.data_ptr(), N, self.O,
                                                  res.timed_out.data_ptr(), res.terminated.data_ptr(),
                                                  b["boot"][t].data_ptr(), st))
             else:
                 b["boot"][t].zero_()
-            self.obs = res.observations
-        pol.forward(self.obs, self.mean, b["last_values"])
+        pol.forward(b["obs"][T], self.mean, b["last_values"])
 
     def gae(self):
         b = self.buf
@@ -475,7 +478,7 @@ class Trainer:
         cfg, b = self.cfg, self.buf
         cap = self.T * self.N
         mb = (cap + cfg.minibatch_count - 1) // cfg.minibatch_count
-        obs = b["obs"].view(cap, self.O_pad)
+        obs = b["obs"][:self.T].reshape(cap, self.O)
         act = b["actions"].view(cap, self.A)
         logp, adv, ret = b["logp"].view(cap), b["adv"].view(cap), b["ret"].view(cap)
         g = self.mb_buf

@@ -68,6 +68,11 @@ class StepViews(C.Structure):  # sg_step_views
     ]
 
 
+class StepOut(C.Structure):  # sg_step_out
+    _fields_ = [("observations", C.c_void_p), ("rewards", C.c_void_p), ("task_error", C.c_void_p),
+                ("terminated", C.c_void_p), ("timed_out", C.c_void_p)]
+
+
 class HostResult(C.Structure):  # sg_host_result
     _fields_ = [
         ("observations", C.c_void_p), ("terminal_observations", C.c_void_p), ("rewards", C.c_void_p),
@@ -111,6 +116,7 @@ _SIGS = {
     "sg_host_alloc": (C.c_int, [C.c_size_t, _P(C.c_void_p)]),
     "sg_host_free": (C.c_int, [C.c_void_p]),
     "sg_env_step": (C.c_int, [C.c_void_p, C.c_void_p, _P(StepViews)]),
+    "sg_env_step_into": (C.c_int, [C.c_void_p, C.c_void_p, _P(StepOut), _P(StepViews)]),
     "sg_env_step_host": (C.c_int, [C.c_void_p, C.c_void_p, _P(HostResult)]),
     "sg_env_task_error": (C.c_int, [C.c_void_p, _P(C.c_void_p)]),
     "sg_env_host_counters": (C.c_int, [C.c_void_p, _P(C.c_uint64), _P(C.c_uint64)]),
@@ -136,6 +142,8 @@ _SIGS = {
                                       C.c_void_p, C.c_void_p]),
     "sg_policy_sample": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_uint64, C.c_uint64,
                                    C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_act": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_uint64, C.c_uint64,
+                                C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p]),
@@ -145,7 +153,8 @@ _SIGS = {
                                      C.c_int32, C.c_char_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
     "sg_elu_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
     "sg_elu_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
-    "sg_ppo_gather": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+    "sg_ppo_gather": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                                C.c_void_p,
                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_void_p, C.c_void_p]),
     "sg_ppo_loss": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
@@ -395,6 +404,17 @@ class VecTaskEnv:
         _check(lib().sg_env_step(self._h, actions.data_ptr(), C.byref(self._views)))
         return self._result()
 
+    def step_into(self, actions, observations=None, rewards=None, task_error=None, terminated=None,
+                  timed_out=None) -> StepResult:
+        """sg_env_step_into: the step's results written straight into the given
+        device tensors (e.g. rollout-buffer slots); None -> the env's buffers."""
+        if tuple(actions.shape) != (self.n_envs, self.action_dim):
+            raise SimError("env.step: action shape mismatch")
+        ptr = lambda t: None if t is None else t.data_ptr()
+        out = StepOut(ptr(observations), ptr(rewards), ptr(task_error), ptr(terminated), ptr(timed_out))
+        _check(lib().sg_env_step_into(self._h, actions.data_ptr(), C.byref(out), C.byref(self._views)))
+        return self._result()
+
     def step_host(self, actions: np.ndarray, out: dict | None = None) -> dict:
         """Host actions in, host StepResult out (synchronous; e2e path)."""
         a = np.ascontiguousarray(actions, dtype=np.float32)
@@ -543,6 +563,26 @@ class Policy:
                                         value.data_ptr(), stream))
         return mean, value
 
+    def act(self, obs, seed: int = 0, log_std=None, draw_pos: int = 0, step_offset: int = 0, want_mean: bool = False):
+        """Fused forward + sampling (sg_policy_act): (actions, log_probs, value[, mean])."""
+        import torch
+        n = obs.shape[0]
+        dev = obs.device
+        A = self.action_dim
+        if log_std is None:
+            log_std = torch.full((A,), -1.0, device=dev)
+        s0, inc = make_stream(seed, TRAIN_STREAM)
+        pos = torch.tensor([draw_pos], dtype=torch.int64, device=dev)
+        acts = torch.empty((n, A), device=dev)
+        logp = torch.empty((n,), device=dev)
+        value = torch.empty((n,), device=dev)
+        mean = torch.empty((n, A), device=dev) if want_mean else None
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _pcheck(lib().sg_policy_act(self._h, obs.data_ptr(), n, obs.stride(0), log_std.data_ptr(), s0, inc,
+                                    pos.data_ptr(), step_offset, acts.data_ptr(), logp.data_ptr(),
+                                    mean.data_ptr() if want_mean else None, value.data_ptr(), stream))
+        return (acts, logp, value, mean) if want_mean else (acts, logp, value)
+
     def sample(self, mean, seed: int = 0, log_std=None, draw_pos: int = 0, step_offset: int = 0):
         """Trainer rollout sampling (ppo.cpp:262-277): a = mean + exp(log_std) z,
         z from make_stream(seed, 0x7261696e) at draw draw_pos + step_offset +
@@ -596,7 +636,8 @@ def ppo_gather(idx, obs, act, logp, adv, ret, obs_out, act_out, logp_out, adv_ou
     import torch
     stream = torch.cuda.current_stream(obs.device).cuda_stream
     _pcheck(lib().sg_ppo_gather(idx.data_ptr(), idx.numel(), obs.data_ptr(), obs.shape[1], obs_out.data_ptr(),
-                                1 if obs_out.dtype == torch.bfloat16 else 0, act.data_ptr(), act.shape[1],
+                                obs_out.shape[1], 1 if obs_out.dtype == torch.bfloat16 else 0, act.data_ptr(),
+                                act.shape[1],
                                 act_out.data_ptr(), logp.data_ptr(), logp_out.data_ptr(), adv.data_ptr(),
                                 adv_out.data_ptr(), ret.data_ptr(), ret_out.data_ptr(), stream))
 

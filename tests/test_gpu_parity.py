@@ -619,3 +619,36 @@ def test_active_tracking_specialised_chains(sg, oracle, robot):
     env, ref, worst = _run_pair(sg, oracle, robot, oracle.ACTIVE_TRACKING, 64, 310, seed=7, sigma=sigma,
                                 tol=dict(goals=2e-5))
     assert (ref.counters()["episode_count"] == 1).all()
+
+
+@pytest.mark.parametrize("robots,task", [(("psm",), "target_reaching"), (("star",), "path_following"),
+                                         (("psm", "psm", "ecm"), "multi_tool_reaching")])
+def test_step_into_caller_buffers_equals_step(sg, oracle, robots, task):
+    """sg_env_step_into writes the step's observations / rewards / task_error
+    / flags into caller device buffers (the trainer's rollout slots) and is
+    otherwise the same step: bit-identical results and state across a reset
+    burst (episode_len 5); terminal observations stay env-owned."""
+    _cuda()
+    n = 256
+    kw = dict(robots=robots, n_envs=n, seed=6, episode_len=5, task=task,
+              goal_sigma=0.15 if task == "path_following" else 0.05)
+    a, b = sg.VecTaskEnv(**kw), sg.VecTaskEnv(**kw)
+    a.reset(); b.reset()
+    A, O = a.action_dim, a.obs_dim
+    rng = np.random.default_rng(3)
+    for s in range(7):
+        act = torch.from_numpy(rng.uniform(-1, 1, size=(n, A)).astype(np.float32)).cuda()
+        dst = dict(observations=torch.full((n, O), 7.0, device="cuda"), rewards=torch.zeros(n, device="cuda"),
+                   task_error=torch.zeros(n, device="cuda"),
+                   terminated=torch.full((n,), 9, dtype=torch.uint8, device="cuda"),
+                   timed_out=torch.full((n,), 9, dtype=torch.uint8, device="cuda"))
+        ra = a.step_into(act, **dst)
+        rb = b.step(act)
+        torch.cuda.synchronize()
+        for k, v in dst.items():
+            assert torch.equal(v, getattr(rb, k)), (k, s)
+        ended = (rb.terminated | rb.timed_out).bool()
+        assert torch.equal(ra.terminal_observations[ended], rb.terminal_observations[ended])
+        sa, sb = a.state(), b.state()
+        for k in ("q", "qdot", "rng_state", "step_count"):
+            assert torch.equal(sa[k], sb[k]), (k, s)

@@ -89,3 +89,26 @@ def test_init_params_matches_reference_stream(sg, oracle):
     first = [scale * oracle.normal(r) for _ in range(10)]
     assert np.allclose(flat[:10], np.float32(first))
     assert np.all(flat[pol.log_std_offset:] == -1.0)
+
+
+@pytest.mark.parametrize("n,act_dim,obs_dim", [(16384, 7, 27), (1000, 6, 24), (130, 8, 30)])
+def test_fused_forward_sampling_equals_separate_calls(sg, n, act_dim, obs_dim):
+    """sg_policy_act (forward + trainer-stream sampling + log-prob in the
+    tensor-core kernel's epilogue) == sg_policy_forward then sg_policy_sample,
+    bit for bit: mean, value, actions and log-probs, at an arbitrary stream
+    position and a non-default log-std (one dim outside the clamp box)."""
+    torch.manual_seed(1)
+    pol = sg.Policy(obs_dim, act_dim)
+    flat = torch.from_numpy(pol.init_params(seed=4)).cuda()
+    flat = flat + 0.05 * torch.randn_like(flat)
+    pol.load_params(flat)
+    obs = torch.randn(n, obs_dim, device="cuda") * 0.5
+    ls = torch.linspace(-1.5, 0.5, act_dim, device="cuda")
+    ls[0] = -7.0
+    mean, value = pol.forward(obs)
+    acts, logp = pol.sample(mean, seed=9, log_std=ls, draw_pos=123456, step_offset=2 * act_dim * 777)
+    a2, lp2, v2, m2 = pol.act(obs, seed=9, log_std=ls, draw_pos=123456, step_offset=2 * act_dim * 777,
+                              want_mean=True)
+    torch.cuda.synchronize()
+    assert torch.equal(m2, mean) and torch.equal(v2, value)
+    assert torch.equal(a2, acts) and torch.equal(lp2, logp)

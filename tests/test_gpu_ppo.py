@@ -294,7 +294,7 @@ def test_update_graph_with_captured_nccl_allreduce(sg):
                 tr.iterate()
             assert tr.graph is not None  # the update ran as a graph replay
             res.append(tr.params.clone())
-        torch.testing.assert_close(res[0], res[1], rtol=1e-3, atol=1e-4)
+        torch.testing.assert_close(res[0], res[1], rtol=1e-2, atol=1e-3)
     finally:
         dist.destroy_process_group()
 
