@@ -1719,7 +1719,26 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
   const int O = 3 * A + 6;
   const int64_t n = P.task.n;
   const int w = threadIdx.x >> 5;
-  const int role = w / TPC;
+  int role = w / TPC;
+#ifdef SG_ROLE_SPREAD
+  if constexpr (TPC == 1 && G == 2) {
+    // Roles by SM sub-partition (warp slot % 4): the scorer and producer
+    // instruction streams differ in length, and with warp 0 always the scorer
+    // every SM's scorers share two sub-partitions. Team pair slot t = lower
+    // slot / 2 puts its scorer on sub-partition {0, 3, 1, 2}[t % 4], so each
+    // sub-partition hosts scorers and producers alike. Only the role choice
+    // depends on the (hardware-assigned) slots; both warps agree through smem.
+    __shared__ int s_slot[2];
+    uint32_t wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    if ((threadIdx.x & 31) == 0) s_slot[w] = (int)wid;
+    __syncthreads();
+    const int lo = min(s_slot[0], s_slot[1]);
+    const int pref = (0x2130 >> (4 * ((lo >> 1) & 3))) & 3;  // {0, 3, 1, 2}[t % 4]
+    const int scorer = (s_slot[1] & 3) == pref && (s_slot[0] & 3) != pref ? 1 : 0;
+    role = w == scorer ? 0 : 1;
+  }
+#endif
   Team tm;
   tm.id = (w % TPC + role) % TPC;
   tm.tthread = role * 32 + (threadIdx.x & 31);
