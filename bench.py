@@ -281,6 +281,30 @@ def cpu_policy_reference(cfg: dict, steps: int, budget_s: float, threads: int = 
     return n * done / dt, lanes, sample
 
 
+def policy_fwd_seconds(pol, obs, mean, val, dev, reps=200):
+    """Average duration of one policy_fwd launch: CUDA events around one
+    replay of a CUDA graph of `reps` back-to-back launches on the launching
+    stream (the graph removes the per-call host launch path; a Python loop of
+    launches measures ~2 us more per launch)."""
+    import torch
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            pol.forward(obs, mean, val)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                pol.forward(obs, mean, val)
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        g.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
 def bench_policy(args, cfg, rank, world, local, dist):
     """north_star's random-init-policy workload: rollout-only env-steps/s with
     the tcgen05 policy in the loop (ppo.cpp:258-313: policy forward -> Gaussian
@@ -324,17 +348,7 @@ def bench_policy(args, cfg, rank, world, local, dist):
     obs = env._result().observations
     mean = torch.empty(n, env.action_dim, device=dev)
     val = torch.empty(n, device=dev)
-    for _ in range(5):
-        pol.forward(obs, mean, val)
-    reps = 200
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        pol.forward(obs, mean, val)
-    e1.record()
-    torch.cuda.synchronize()
-    fwd_s = e0.elapsed_time(e1) * 1e-3 / reps
+    fwd_s = policy_fwd_seconds(pol, obs, mean, val, dev)
     try:
         peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
         pk = "measured burst"
@@ -457,17 +471,7 @@ def bench_ppo(args, cfg, rank, world, local, dist):
     obs = env._result().observations
     mean = torch.empty(n, env.action_dim, device=f"cuda:{local}")
     val = torch.empty(n, device=f"cuda:{local}")
-    for _ in range(5):
-        pol.forward(obs, mean, val)
-    reps = 200
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        pol.forward(obs, mean, val)
-    e1.record()
-    torch.cuda.synchronize()
-    fwd_s = e0.elapsed_time(e1) * 1e-3 / reps
+    fwd_s = policy_fwd_seconds(pol, obs, mean, val, f"cuda:{local}")
     peak = None
     try:
         peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])

@@ -6,17 +6,25 @@
 // flat fp64 parameter vector laid out actor (W_l [out x in] row-major, b_l)
 // for l = 0..3, then critic, then log_std (policy.cpp:42-63).
 //
-// Device design (one CTA = one 128-row tile, 4 warps, 1 CTA per SM):
+// Device design (one CTA = one 128-row tile, 16 warps, 1 CTA per SM):
 //  * weights are packed once per parameter update into bf16 images in the
-//    UMMA K-major no-swizzle canonical layout and streamed into shared memory
-//    with 1-D bulk copies (cp.async.bulk -> UBLKCP, mbarrier complete_tx);
+//    UMMA K-major no-swizzle canonical layout; every CTA bulk-copies all of
+//    them into shared memory at launch (cp.async.bulk -> UBLKCP, mbarrier
+//    complete_tx; 200 KB, L2-resident across CTAs);
 //  * every layer is tcgen05.mma.cta_group::1.kind::f16 (BF16 x BF16 -> FP32)
 //    issued by one thread, M = 128, accumulators in TMEM (512 columns);
-//  * the epilogue warps read their TMEM lane quarter (tcgen05.ld 32x32b),
-//    add bias, apply ELU, round to bf16 and write the next layer's A operand
-//    straight into shared memory; the last layer writes fp32 mean / value.
-//  * L1 of actor and critic is ONE N=512 product (shared input); the critic's
-//    hidden layer waits in TMEM columns 256..511 while the actor finishes.
+//  * activations never leave tensor memory: the epilogue reads its TMEM lane
+//    (tcgen05.ld 32x32b), adds the bias, applies ELU, packs bf16 pairs and
+//    writes them back with tcgen05.st as the next layer's A operand
+//    (tcgen05.mma with A in TMEM); only the last layer's fp32 mean / value
+//    leave the SM;
+//  * L1 of actor and critic is issued together; then the actor (warps 0-7)
+//    and the critic (warps 8-15) run as two pipelines with their own MMA
+//    issuer, commit barrier and named barrier, the critic one epilogue
+//    behind, so one trunk's MUFU-bound ELU overlaps the other's MMAs;
+//  * fused rollout sampling: the fp64 Box-Muller draws run while layer 2 is
+//    on the tensor cores; the actions / log-probs are formed from the mean
+//    row in the kernel's tail.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -35,21 +43,20 @@ constexpr int kRows = 128;  // UMMA M
 constexpr int kK0 = 32;     // padded obs width
 constexpr int kH1 = 256, kH2 = 128, kH3 = 64, kNOut = 16;  // kNOut: padded output width
 
-// Shared-memory plan (bytes). R0 holds the obs tile + W1 during layer 1 and
-// W3/W4 afterwards; R1 = A2 (h1), R2 = W2 (actor, then critic), R3 = A3,
-// R4 = A4.
-constexpr uint32_t kX0 = 0;                                // 128 x 32 bf16
-constexpr uint32_t kW1 = 8192;                             // 512 x 32 bf16
-constexpr uint32_t kW3a = 0, kW3c = 16384;                 // 64 x 128 bf16 each
-constexpr uint32_t kW4a = 32768, kW4c = 34816;             // 16 x 64 bf16 each
-constexpr uint32_t kA2 = 40960;                            // 128 x 256 bf16
-constexpr uint32_t kW2 = kA2 + 65536;                      // 128 x 256 bf16
-constexpr uint32_t kA3 = kW2 + 65536;                      // 128 x 128 bf16
-constexpr uint32_t kA4 = kA3 + 32768;                      // 128 x 64 bf16
-constexpr uint32_t kBar = kA4 + 16384;                     // mbarriers + TMEM slot
-constexpr uint32_t kBias = kBar + 128;                     // 928 fp32 biases
-constexpr uint32_t kSmem = kBias + 928 * 4;
-constexpr int kThreads = 512;  // 16 warps: 4 TMEM lane quarters x 4 column groups
+// Shared-memory plan (bytes): every weight image stays resident (bulk-copied
+// once per launch, L2-resident across CTAs); activations never touch shared
+// memory -- they live in TMEM as the next layer's A operand. The X / W1 region
+// is free once layer 1 has run and holds the fused sampling's scratch.
+constexpr uint32_t kX0 = 0;                  // 128 x 32 bf16 obs tile
+constexpr uint32_t kW1 = 8192;               // 512 x 32 bf16 (actor rows | critic rows)
+constexpr uint32_t kW2a = 40960;             // 128 x 256 bf16
+constexpr uint32_t kW2c = kW2a + 65536;      // 128 x 256 bf16
+constexpr uint32_t kW34 = kW2c + 65536;      // W3a | W3c (64 x 128) | W4a | W4c (16 x 64)
+constexpr uint32_t kW3a = kW34, kW3c = kW34 + 16384, kW4a = kW34 + 32768, kW4c = kW34 + 34816;
+constexpr uint32_t kBar = kW34 + 36864;      // mbarriers + TMEM slot
+constexpr uint32_t kBias = kBar + 128;       // 928 fp32 biases
+constexpr uint32_t kSmem = kBias + 928 * 4;  // 212,736 B
+constexpr int kThreads = 512;  // 16 warps: 2 trunks x 2 column halves x 4 TMEM lane quarters
 constexpr int kGroups = kThreads / kRows;
 
 // Packed parameter image (global): same byte layout as the smem regions.
@@ -158,39 +165,67 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// Epilogue for a hidden layer: this warp's column group of TMEM columns
-// [c0, c0+N) for its row -> +bias -> ELU -> bf16 -> K-major A tile (128 rows).
-// Warp w reads TMEM lane quarter w%4 (hardware rule) and column group w/4.
-// The thread's columns are read from TMEM in batches of up to 64 (four x16
-// loads behind ONE wait) so the load latency is exposed once per batch.
-template <int N>
-__device__ __forceinline__ void epi_hidden(uint32_t tmem_row, uint32_t c0, const float* __restrict__ bias,
-                                           uint8_t* a_base, int row, int group) {
-  constexpr int kPer = N / kGroups;
-  constexpr int kBatch = kPer < 64 ? kPer : 64;
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ELU(acc + bias) (policy.cpp:33) of two adjacent columns -> one bf16x2 word:
+// max(x, 2^min(x log2 e, 0) - 1) == (x > 0 ? x : e^x - 1) (e^x - 1 >= x), the
+// column pair in packed fp32 ops (FADD2 / FMUL2), one MUFU.EX2 per value.
+__device__ __forceinline__ uint32_t elu_pair(uint32_t a0, uint32_t a1, float2 b) {
+  const float2 x = __fadd2_rn(make_float2(__uint_as_float(a0), __uint_as_float(a1)), b);
+  const float2 t = __fmul2_rn(x, make_float2(1.4426950408889634f, 1.4426950408889634f));
+  const float2 e =
+      __fadd2_rn(make_float2(ex2_approx(fminf(t.x, 0.f)), ex2_approx(fminf(t.y, 0.f))), make_float2(-1.f, -1.f));
+  return pack_bf16(fmaxf(x.x, e.x), fmaxf(x.y, e.y));
+}
+
+// Hidden-layer epilogue in tensor memory: this thread's NC accumulator
+// columns [src, src + NC) of its TMEM lane -> ELU(acc + bias) -> bf16 pairs
+// written to columns [dst, dst + NC/2) of the same lane, where the next
+// layer's MMA reads them as its A operand (row = lane, two K elements per
+// 32-bit column). Batches of 32 columns (REV: last batch first), the next
+// batch's TMEM loads in flight while the current one is converted; a batch
+// only overwrites columns that this thread has already read (packing in
+// place: dst == src forward, or dst == src + NC/2 in reverse) or a disjoint
+// range.
+template <int NC, bool REV = false>
+__device__ __forceinline__ void epi_tmem(uint32_t trow, uint32_t src, uint32_t dst, const float* __restrict__ bias) {
+  constexpr int NB = NC / 32;
+  const auto bat = [](int j) { return REV ? NB - 1 - j : j; };
+  uint32_t r[2][2][16];
+  tmem_ld16_async(trow + src + 32 * bat(0), r[0][0]);
+  tmem_ld16_async(trow + src + 32 * bat(0) + 16, r[0][1]);
 #pragma unroll
-  for (int cb = 0; cb < kPer; cb += kBatch) {
-    uint32_t r[kBatch / 16][16];
-#pragma unroll
-    for (int j = 0; j < kBatch / 16; ++j) tmem_ld16_async(tmem_row + c0 + group * kPer + cb + 16 * j, r[j]);
+  for (int j = 0; j < NB; ++j) {
     tmem_wait_ld();
-#pragma unroll
-    for (int j = 0; j < kBatch / 16; ++j) {
-      const int c = group * kPer + cb + 16 * j;
-      uint32_t p[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        p[k] = pack_bf16(elu(__uint_as_float(r[j][2 * k]) + bias[c + 2 * k]),
-                         elu(__uint_as_float(r[j][2 * k + 1]) + bias[c + 2 * k + 1]));
-      uint4* d0 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c, kRows));
-      uint4* d1 = reinterpret_cast<uint4*>(a_base + kmajor_off(row, c + 8, kRows));
-      *d0 = make_uint4(p[0], p[1], p[2], p[3]);
-      *d1 = make_uint4(p[4], p[5], p[6], p[7]);
+    if (j + 1 < NB) {
+      tmem_ld16_async(trow + src + 32 * bat(j + 1), r[(j + 1) & 1][0]);
+      tmem_ld16_async(trow + src + 32 * bat(j + 1) + 16, r[(j + 1) & 1][1]);
     }
+    const int c = 32 * bat(j);
+    uint32_t p[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      p[k] = elu_pair(r[j & 1][k >> 3][2 * (k & 7)], r[j & 1][k >> 3][2 * (k & 7) + 1],
+                      *reinterpret_cast<const float2*>(bias + c + 2 * k));
+    tmem_st16(trow + dst + c / 2, p);
   }
 }
 
-// Issue one layer: D[128 x N] (+)= A[128 x K] * B[N x K]^T, K in steps of 16.
+// Issue one layer with A in shared memory: D[128 x N] (+)= A[128 x K] * B[N x K]^T, K in steps of 16.
 __device__ __forceinline__ void issue_layer(uint32_t d_tmem, uint32_t a_addr, uint32_t a_rows, uint32_t b_addr,
                                             uint32_t b_rows, int K, int N) {
   const uint32_t idesc = make_idesc(kRows, N);
@@ -199,6 +234,29 @@ __device__ __forceinline__ void issue_layer(uint32_t d_tmem, uint32_t a_addr, ui
     const uint64_t a = make_desc(a_addr + 2u * s * lbo_a, lbo_a, 128u);
     const uint64_t b = make_desc(b_addr + 2u * s * lbo_b, lbo_b, 128u);
     mma_bf16(d_tmem, a, b, idesc, s > 0 ? 1u : 0u);
+  }
+}
+
+// tcgen05.mma with the A operand in tensor memory (.kind::f16, BF16 x BF16 -> FP32).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// Issue one layer with A in TMEM: K-step s (16 elements = 8 packed columns)
+// reads A at column a0 + 8 s for s < split, a1 + 8 (s - split) after (the
+// epilogue's two column halves); B = N rows of a K-major image with row
+// stride lbo (bytes between K chunks).
+__device__ __forceinline__ void issue_layer_ts(uint32_t d_tmem, uint32_t a0, uint32_t a1, int split, uint32_t b_addr,
+                                               uint32_t lbo, int K, int N) {
+  const uint32_t idesc = make_idesc(kRows, N);
+  for (int s = 0; s < K / 16; ++s) {
+    const uint32_t a = s < split ? a0 + 8u * s : a1 + 8u * (s - split);
+    mma_bf16_ts(d_tmem, a, make_desc(b_addr + 2u * s * lbo, lbo, 128u), idesc, s > 0 ? 1u : 0u);
   }
 }
 
@@ -255,6 +313,30 @@ __device__ __forceinline__ uint64_t jump(uint64_t s0, uint64_t k, const Jump64& 
   return s;
 }
 
+// PCG32 state s0 advanced by k draws, computed by a whole warp: lane l takes
+// the jumps of bits l and l + 32 of k, and the (commuting) affine maps are
+// combined by a 5-round butterfly. Every lane returns the result.
+__device__ __forceinline__ uint64_t jump_warp(uint64_t s0, uint64_t k, const Jump64& J) {
+  const int lane = threadIdx.x & 31;
+  uint64_t m = 1, a = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int b = lane + 32 * h;
+    if ((k >> b) & 1) {
+      const uint64_t M = J.mult[b], Ad = J.add[b];
+      a = a * M + Ad;
+      m *= M;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const uint64_t m2 = __shfl_xor_sync(0xffffffffu, m, off), a2 = __shfl_xor_sync(0xffffffffu, a, off);
+    a = a * m2 + a2;
+    m *= m2;
+  }
+  return s0 * m + a;
+}
+
 struct FwdArgs {
   const float* obs;  // n x obs_stride fp32 (first obs_dim columns used)
   int64_t n;
@@ -278,6 +360,32 @@ struct FwdArgs {
   float* logp;
 };
 
+#ifdef SG_POLICY_PROBE
+// Phase probe (A/B builds only): clock64 at each phase of CTA 0, printed by
+// lane 0 of warps 0 / 4 / 8 / 12 (actor halves, critic halves).
+#define PPROBE(k) (probe_t[k] = clock64())
+#else
+#define PPROBE(k) ((void)0)
+#endif
+
+// One CTA = one 128-row tile. Layer 1 of both trunks is issued together;
+// then the actor (warps 0-7) and the critic (warps 8-15) run as two
+// independent pipelines, each with its own MMA issuer (lane 0 of its first
+// warp), commit mbarrier and named barrier, so one trunk's epilogue (TMEM ->
+// ELU -> TMEM, MUFU / FMA pipes) overlaps the other trunk's MMAs. Warp w of
+// a trunk reads TMEM lane quarter w % 4 and column half (w / 4) % 2.
+//
+// TMEM columns of trunk t (T = 256 t), fp32 accumulators / packed bf16 A:
+//   L1 acc        [T, T+256)                     (N = 256)
+//   A2 (h1)       [T, T+64) | [T+192, T+256)     (half 0 packs forward in place, half 1 backwards
+//                                                 into the top of its range)
+//   L2 acc        [T+64, T+192)                  (N = 128)
+//   A3 (h2)       [T, T+64)
+//   L3 acc        [T+64, T+128)                  (N = 64)
+//   A4 (h3)       [T+128, T+160)
+//   L4 acc        [T, T+16)                      (N = 16)
+// The critic's first epilogue starts when the actor's is done: from then on
+// one trunk's epilogue (MUFU-bound ELU) runs while the other trunk's MMAs do.
 __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_constant__ PolicyImage W,
                                                                  const __grid_constant__ FwdArgs args,
                                                                  const __grid_constant__ Jump64 J) {
@@ -285,7 +393,12 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t row0 = (int64_t)blockIdx.x * kRows;
   const int row = tid & (kRows - 1);  // TMEM lane == tile row (lane quarter = warp % 4)
-  const int group = tid / kRows;      // column group (warp / 4)
+  const int group = tid / kRows;      // warp / 4: trunk * 2 + column half
+  const int trunk = warp >> 3, half = (warp >> 2) & 1;
+#ifdef SG_POLICY_PROBE
+  long long probe_t[12] = {};
+#endif
+  PPROBE(0);
   bool boot_row = true;
   if (args.timed_out) {
     const int64_t r = row0 + row;
@@ -298,12 +411,13 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   float* sbias = reinterpret_cast<float*>(smem + kBias);  // the 7 bias vectors, bulk-copied (contiguous)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBar + 64);
-  const uint32_t bar_w1 = smem_u32(&bars[0]), bar_w2 = smem_u32(&bars[1]), bar_w34 = smem_u32(&bars[2]);
-  const uint32_t bar_mma = smem_u32(&bars[3]), bar_bias = smem_u32(&bars[4]);
+  const uint32_t bar_bias = smem_u32(&bars[0]), bar_w1 = smem_u32(&bars[1]);
+  const uint32_t bar_w2 = smem_u32(&bars[2 + trunk]), bar_w34 = smem_u32(&bars[4]);
+  const uint32_t bar_mma = smem_u32(&bars[5 + trunk]);
   const uint32_t sbase = smem_u32(smem);
 
   if (tid == 0) {
-    for (int b = 0; b < 5; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    for (int b = 0; b < 7; ++b) mbar_init(smem_u32(&bars[b]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {  // TMEM: all 512 columns (one CTA per SM)
@@ -311,10 +425,16 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   __syncthreads();
-  if (tid == 0) {  // stream the biases and the first weights while the obs tile is converted
-    bulk_load(sbase + kBias, W.b1, 928 * 4, bar_bias);
-    bulk_load(sbase + kW1, W.w1, 32768, bar_w1);
-    bulk_load(sbase + kW2, W.w2a, 65536, bar_w2);
+  if (tid == 0) {  // every weight image, in the order the layers need them, while the obs tile is converted
+    bulk_load(sbase + kBias, W.b1, 928 * 4, smem_u32(&bars[0]));
+    bulk_load(sbase + kW1, W.w1, 32768, smem_u32(&bars[1]));
+    bulk_load(sbase + kW2a, W.w2a, 65536, smem_u32(&bars[2]));
+    bulk_load(sbase + kW2c, W.w2c, 65536, smem_u32(&bars[3]));
+    bulk_load(sbase + kW34, W.w34, 36864, smem_u32(&bars[4]));
+  }
+  if (warp == 1 && args.actions) {  // the trainer-stream state of this tile's first draw (row0, dim 0)
+    const uint64_t s = jump_warp(args.s0, *args.pos + args.step_off + 2ull * (uint64_t)row0 * (uint64_t)args.act_dim, J);
+    if ((tid & 31) == 0) *reinterpret_cast<uint64_t*>(smem + kBar + 72) = s;
   }
   // obs tile -> bf16 K-major [128 x 32] (zero padded rows / columns); thread
   // (row, group) converts the 8 columns of K chunk `group`
@@ -337,28 +457,69 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  uint32_t mma_phase = 0;
+  PPROBE(1);
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t T = 256u * trunk;
+  const bool issuer = (tid & 255) == 0;
 
-  // ---- layer 1: [128 x 32] x [512 x 32]^T -> TMEM cols 0..511 (actor | critic)
+  // ---- layer 1 of both trunks: [128 x 32] x [256 x 32]^T -> cols 0..255 | 256..511
   if (tid == 0) {
     mbar_wait(bar_w1, 0);
     tc_fence_after();
     issue_layer(tmem + 0, sbase + kX0, kRows, sbase + kW1, 512, kK0, 256);
     issue_layer(tmem + 256, sbase + kX0, kRows, sbase + kW1 + kmajor_off(256, 0, 512), 512, kK0, 256);
-    mma_commit(bar_mma);
+    mma_commit(smem_u32(&bars[5]));
+    mma_commit(smem_u32(&bars[6]));
   }
-  // Fused sampling, stream part: the normals and log-prob terms of this
-  // thread's (row, dim) draws depend on the trainer stream and the log-std
-  // only, so they are drawn while layer 1 runs on the tensor cores (dims
-  // group, group + 4, ...: one jump to the first draw, then + 8 draws per dim).
   constexpr int kDraws = kNOut / kGroups;
   double zs[kDraws], terms[kDraws];
   const int64_t srow = row0 + row;
   const bool sampling = args.actions != nullptr && srow < args.n && group < args.act_dim;
+  mbar_wait(bar_bias, 0);  // bulk-copied biases visible to this thread
+  const float* b1 = sbias + 256 * trunk;
+  const float* b2 = sbias + 512 + 128 * trunk;
+  const float* b3 = sbias + 768 + 64 * trunk;
+  const float* b4 = sbias + 896 + 16 * trunk;
+  const auto trunk_sync = [&]() {  // named barrier of this trunk's 8 warps
+    asm volatile("bar.sync %0, 256;" ::"r"(1 + trunk) : "memory");
+  };
+  const auto handoff = [&]() {  // this thread's TMEM stores -> the trunk's next MMA
+    tmem_wait_st();
+    tc_fence_before();
+    trunk_sync();
+  };
+
+  // h1 = ELU(L1 + b1) -> A2
+  mbar_wait(bar_mma, 0);
+  tc_fence_after();
+  PPROBE(2);
+#ifndef SG_POLICY_NO_STAGGER
+  if (trunk == 1) asm volatile("bar.sync 3, 512;" ::: "memory");
+#endif
+  if (half == 0)
+    epi_tmem<128>(trow, T, T, b1);
+  else
+    epi_tmem<128, true>(trow, T + 128, T + 192, b1 + 128);
+  handoff();
+#ifndef SG_POLICY_NO_STAGGER
+  if (trunk == 0) asm volatile("bar.arrive 3, 512;" ::: "memory");
+#endif
+  PPROBE(3);
+  if (issuer) {  // layer 2: N = 128, K = 256 (A2 halves at T and T + 192)
+    tc_fence_after();
+    mbar_wait(bar_w2, 0);
+    issue_layer_ts(tmem + T + 64, tmem + T, tmem + T + 192, 8, sbase + (trunk ? kW2c : kW2a), kH2 * 16, kH1, kH2);
+    mma_commit(bar_mma);
+  }
+  // Fused sampling, stream part: the normals and log-prob terms of this
+  // thread's (row, dim) draws depend on the trainer stream and the log-std
+  // only, so they are drawn while layer 2 -- the longest MMA -- runs (dims
+  // group, group + 4, ...: a <= 13-bit jump from the tile's first draw, then
+  // + 8 draws per dim; fp64 Box-Muller like the reference).
   if (sampling) {
     const int A = args.act_dim;
-    uint64_t st = jump(args.s0, *args.pos + args.step_off + 2ull * ((uint64_t)srow * (uint64_t)A + (uint64_t)group), J);
+    uint64_t st = jump(*reinterpret_cast<const uint64_t*>(smem + kBar + 72),
+                       2ull * ((uint64_t)row * (uint64_t)A + (uint64_t)group), J);
 #pragma unroll
     for (int j = 0; j < kDraws; ++j) {
       const int d = group + j * kGroups;
@@ -371,114 +532,56 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
       }
     }
   }
-  mbar_wait(bar_bias, 0);  // bulk-copied biases visible to this thread
-  mbar_wait(bar_mma, mma_phase);
-  mma_phase ^= 1;
+  // h2 = ELU(L2 + b2) -> A3
+  PPROBE(4);
+  mbar_wait(bar_mma, 1);
   tc_fence_after();
-  // R0 is free: stream W3/W4 (both trunks) while the actor's h1 is processed
-  if (tid == 0) bulk_load(sbase + kW3a, W.w34, 36864, bar_w34);
-  epi_hidden<kH1>(tmem_row, 0, sbias, smem + kA2, row, group);
-
-  // ---- actor: layer 2 (A2 x W2a -> cols 0..127), 3 (-> 128..191), 4 (-> 192..207)
-  async_proxy_fence();
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc_fence_after();
-    mbar_wait(bar_w2, 0);
-    issue_layer(tmem + 0, sbase + kA2, kRows, sbase + kW2, kH2, kH1, kH2);
-    mma_commit(bar_mma);
-  }
-  mbar_wait(bar_mma, mma_phase);
-  mma_phase ^= 1;
-  tc_fence_after();
-  if (tid == 0) bulk_load(sbase + kW2, W.w2c, 65536, bar_w2);  // W2a consumed: stream W2c
-  epi_hidden<kH2>(tmem_row, 0, sbias + 512, smem + kA3, row, group);
-  async_proxy_fence();
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
+  PPROBE(5);
+  epi_tmem<64>(trow, T + 64 + 64 * half, T + 32 * half, b2 + 64 * half);
+  handoff();
+  PPROBE(6);
+  if (issuer) {  // layer 3: N = 64, K = 128
     tc_fence_after();
     mbar_wait(bar_w34, 0);
-    issue_layer(tmem + 128, sbase + kA3, kRows, sbase + kW3a, kH3, kH2, kH3);
+    issue_layer_ts(tmem + T + 64, tmem + T, tmem + T, 8, sbase + (trunk ? kW3c : kW3a), kH3 * 16, kH2, kH3);
     mma_commit(bar_mma);
   }
-  mbar_wait(bar_mma, mma_phase);
-  mma_phase ^= 1;
+  // h3 = ELU(L3 + b3) -> A4
+  mbar_wait(bar_mma, 0);
   tc_fence_after();
-  epi_hidden<kH3>(tmem_row, 128, sbias + 768, smem + kA4, row, group);
-  async_proxy_fence();
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
+  PPROBE(7);
+  epi_tmem<32>(trow, T + 64 + 32 * half, T + 128 + 16 * half, b3 + 32 * half);
+  handoff();
+  if (issuer) {  // layer 4: N = 16, K = 64
     tc_fence_after();
-    issue_layer(tmem + 192, sbase + kA4, kRows, sbase + kW4a, kNOut, kH3, kNOut);
+    issue_layer_ts(tmem + T, tmem + T + 128, tmem + T + 128, 4, sbase + (trunk ? kW4c : kW4a), kNOut * 16, kH3, kNOut);
     mma_commit(bar_mma);
   }
-  mbar_wait(bar_mma, mma_phase);
-  mma_phase ^= 1;
+  mbar_wait(bar_mma, 1);
   tc_fence_after();
-  float mv[kNOut];  // the actor's output row (group 0), kept for the fused sampling
-  if (group == 0) {
+  PPROBE(8);
+  float mv[kNOut];  // the actor's output row (trunk 0, half 0), kept for the fused sampling
+  if (half == 0) {
     float v[16];
-    tmem_ld16(tmem_row + 192, v);
+    tmem_ld16(trow + T, v);
+    if (trunk == 0) {
 #pragma unroll
-    for (int k = 0; k < kNOut; ++k) mv[k] = v[k] + sbias[896 + k];
-    if (row0 + row < args.n && args.mean) {
-      float* dst = args.mean + (row0 + row) * args.act_dim;
-      for (int k = 0; k < args.act_dim; ++k) dst[k] = mv[k];
+      for (int k = 0; k < kNOut; ++k) mv[k] = v[k] + b4[k];
+      if (row0 + row < args.n && args.mean) {
+        float* dst = args.mean + (row0 + row) * args.act_dim;
+        for (int k = 0; k < args.act_dim; ++k) dst[k] = mv[k];
+      }
+    } else if (row0 + row < args.n) {
+      args.value[row0 + row] = boot_row ? v[0] + b4[0] : 0.f;
     }
   }
-  // ---- critic: h1 waits in cols 256..511
-  epi_hidden<kH1>(tmem_row, 256, sbias + 256, smem + kA2, row, group);
-  async_proxy_fence();
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc_fence_after();
-    mbar_wait(bar_w2, 1);
-    issue_layer(tmem + 0, sbase + kA2, kRows, sbase + kW2, kH2, kH1, kH2);
-    mma_commit(bar_mma);
-  }
-  mbar_wait(bar_mma, mma_phase);
-  mma_phase ^= 1;
-  tc_fence_after();
-  epi_hidden<kH2>(tmem_row, 0, sbias + 640, smem + kA3, row, group);
-  async_proxy_fence();
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc_fence_after();
-    issue_layer(tmem + 128, sbase + kA3, kRows, sbase + kW3c, kH3, kH2, kH3);
-    mma_commit(bar_mma);
-  }
-  mbar_wait(bar_mma, mma_phase);
-  mma_phase ^= 1;
-  tc_fence_after();
-  epi_hidden<kH3>(tmem_row, 128, sbias + 832, smem + kA4, row, group);
-  async_proxy_fence();
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc_fence_after();
-    issue_layer(tmem + 192, sbase + kA4, kRows, sbase + kW4c, kNOut, kH3, kNOut);
-    mma_commit(bar_mma);
-  }
-  mbar_wait(bar_mma, mma_phase);
-  mma_phase ^= 1;
-  tc_fence_after();
-  if (group == 0) {
-    float v[16];
-    tmem_ld16(tmem_row + 192, v);
-    if (row0 + row < args.n) args.value[row0 + row] = boot_row ? v[0] + sbias[912] : 0.f;
-  }
   if (args.actions) {
-    // Fused sampling, action part: the mean rows go to the (now idle) A3
-    // region, each thread forms the actions of its draws, the per-dim
-    // log-prob terms meet in A2 and group 0 sums them in dim order -- the same
-    // arithmetic as policy_sample_kernel.
-    float* smean = reinterpret_cast<float*>(smem + kA3);   // 128 x 16 fp32
-    double* sterm = reinterpret_cast<double*>(smem + kA2); // 128 x 16 fp64
+    // Fused sampling, action part: the mean rows go to the (idle since layer 1)
+    // X / W1 region, each thread forms the actions of its draws, the per-dim
+    // log-prob terms meet there too and group 0 sums them in dim order -- the
+    // same arithmetic as policy_sample_kernel.
+    float* smean = reinterpret_cast<float*>(smem + kX0);           // 128 x 16 fp32
+    double* sterm = reinterpret_cast<double*>(smem + kX0 + 8192);  // 128 x 16 fp64
     if (group == 0) {
 #pragma unroll
       for (int k = 0; k < kNOut; ++k) smean[row * kNOut + k] = mv[k];
@@ -502,8 +605,17 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
       args.logp[srow] = (float)lp;
     }
   }
+  PPROBE(9);
   tc_fence_before();
   __syncthreads();
+  PPROBE(10);
+#ifdef SG_POLICY_PROBE
+  if (blockIdx.x == 0 && (tid & 127) == 0)
+    printf("pprobe warp %2d: obs %lld L1 %lld epi1 %lld draws %lld L2 %lld epi2 %lld L3 %lld epi3+L4 %lld out %lld end %lld\n",
+           warp, probe_t[1] - probe_t[0], probe_t[2] - probe_t[1], probe_t[3] - probe_t[2], probe_t[4] - probe_t[3],
+           probe_t[5] - probe_t[4], probe_t[6] - probe_t[5], probe_t[7] - probe_t[6], probe_t[8] - probe_t[7],
+           probe_t[9] - probe_t[8], probe_t[10] - probe_t[0]);
+#endif
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
