@@ -319,6 +319,19 @@ int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const f
 int sg_policy_act(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
                   const float* d_log_std_raw, uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos,
                   uint64_t step_offset, float* d_actions, float* d_logp, float* d_mean, float* d_value, void* stream);
+/* The stream part of sg_policy_sample ahead of the forward (it depends on
+ * the trainer stream and log-std only): for every (env e, dim i) the draw at
+ * *d_draw_pos + step_offset + 2*(e*A + i) -> d_scaled_noise[e*A + i] =
+ * exp(clamp(log_std_i)) * z (fp64) and d_logp[e] = sum_i(-z^2/2 - log_std_i
+ * - log(2 pi)/2) (dim order). Lets the trainer draw step t+1's noise on a
+ * second stream while the env step produces step t+1's observations. */
+int sg_policy_noise(const sg_policy* policy, int64_t n, const float* d_log_std_raw, uint64_t stream_state,
+                    uint64_t stream_inc, const uint64_t* d_draw_pos, uint64_t step_offset, double* d_scaled_noise,
+                    float* d_logp, void* stream);
+/* Forward + actions from sg_policy_noise's output: actions = (float)(mean +
+ * d_scaled_noise), bit-identical to sg_policy_act on the same draws. */
+int sg_policy_act_noise(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
+                        const double* d_scaled_noise, float* d_actions, float* d_mean, float* d_value, void* stream);
 /* compute_gae (rollout.cpp:42-66, time-major [n_steps][n_envs]) without the
  * normalisation, plus episode statistics (ppo.cpp:286-303) accumulated into
  * d_stats4 = {reward_sum, episode_reward_sum, final_error_sum, episodes}. */

@@ -1046,11 +1046,27 @@ __device__ __forceinline__ void team_store(float* __restrict__ g, const float* _
   }
 }
 
-// Shared memory of one team (TeamSmem + double-buffered observation rows and
-// action rows), a multiple of 16 bytes.
+// Observation row buffers of a team: the scorer stores its rows right after
+// scoring (two buffers, by step parity). SG_PRODUCER_ROWS (A/B builds): the
+// producers store step k's rows after B(k+1) while the scorer stages step
+// k+1 and everyone produces step k+2 -- three buffers in flight; parity-green
+// but measured slower (PSM 16K, K = 250: 207.7 vs 177.0 us; ECM 566.8 vs
+// 486.0 us).
+template <int G>
+__host__ __device__ constexpr int team_obs_bufs() {
+#ifdef SG_PRODUCER_ROWS
+  return G > 1 ? 3 : 2;
+#else
+  return 2;
+#endif
+}
+
+// Shared memory of one team (TeamSmem + observation row buffers and
+// double-buffered action rows), a multiple of 16 bytes.
 template <int G>
 __host__ __device__ constexpr size_t team_smem_bytes_g(int A) {
-  return (sizeof(TeamSmem<G>) + 15) / 16 * 16 + (size_t)(2 * kTeamEnvs * (3 * A + 6) + 2 * (kTeamEnvs * A + 4)) * 4;
+  return (sizeof(TeamSmem<G>) + 15) / 16 * 16 +
+         (size_t)(team_obs_bufs<G>() * kTeamEnvs * (3 * A + 6) + 2 * (kTeamEnvs * A + 4)) * 4;
 }
 template <int G>
 inline size_t team_smem_bytes(int A) {
@@ -1439,25 +1455,33 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     }
   };
 
-  // scorer: store step rows of parity pb (generated actions when G == 1,
-  // observation rows, host mirror)
-  const auto store_rows = [&](int pb) {
-    const float* so = s_obs_base + pb * (kTeamEnvs * O);
+  // Observation rows live in kOB buffers: step k stages into buffer k % kOB.
+  // kProdRows (G > 1): the producers store step k's rows after B(k+1) (the
+  // scorer has finished staging them by then); else the scorer stores them
+  // right after scoring (G == 1: together with the generated action rows).
+  constexpr int kOB = team_obs_bufs<G>();
+  constexpr bool kProdRows = kOB == 3;
+  const auto obs_buf = [&](int st) { return s_obs_base + (st % kOB) * (kTeamEnvs * O); };
+  const auto store_rows = [&](int st) {
+    const float* so = obs_buf(st);
+    constexpr int NT = kProdRows ? (G - 1) * 32 : 32;
+    const int t = kProdRows ? tm.tthread - 32 : lane;
     if constexpr (GEN && G == 1)
-      team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act_base + pb * (kTeamEnvs * A + 4),
+      team_store<CH, kTeamEnvs * CH::kDof, 32>(P.p.act_buf + row0 * A, s_act_base + (st & 1) * (kTeamEnvs * A + 4),
                                                rows * A, (rows & 3) == 0, lane);
-    team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.obs + row0 * O, so, rows * O, (rows & 3) == 0, lane);
+    team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), NT>(P.p.obs + row0 * O, so, rows * O, (rows & 3) == 0, t);
     if constexpr (!GEN) {
       if (P.p.h_obs)
-        team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), 32>(P.p.h_obs + row0 * O, so, rows * O, (rows & 3) == 0,
-                                                           lane);
+        team_store<CH, kTeamEnvs * (3 * CH::kDof + 6), NT>(P.p.h_obs + row0 * O, so, rows * O, (rows & 3) == 0, t);
     }
   };
 
   // Rows that ended at step k (pb = parity of k) are reset by the WHOLE team
   // (env lane l by warp l % G: reset_row is fp64-heavy, PathFollowing most of
-  // all), after which the scorer re-observes them and stores step k's rows.
-  const auto reset_phase = [&](int pb) {
+  // all), after which the scorer re-observes them (and, without producer row
+  // stores, stores step k's rows).
+  const auto reset_phase = [&](int k) {
+    const int pb = k & 1;
 #ifdef SG_RESET_FULLWARP
     if (active && ts.ended[pb][lane] && (int)(blockIdx.x % G) == S) {
 #else
@@ -1468,7 +1492,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     }
     team_sync<G, TPC>(tm);
     if constexpr (S == 0) {
-      float* so = s_obs_base + pb * (kTeamEnvs * O);
+      float* so = obs_buf(k);
       if (active && ts.ended[pb][lane]) {  // the post-reset observation row
         load_block();
         load_task();
@@ -1487,7 +1511,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
         }
       }
       __syncwarp();
-      store_rows(pb);
+      if constexpr (!kProdRows) store_rows(k);
     }
   };
 
@@ -1510,7 +1534,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
 #endif
   for (int step = 0; step < k_steps; ++step) {
     const int b = step & 1;
-    float* s_obs = s_obs_base + b * (kTeamEnvs * O);
+    float* s_obs = obs_buf(step);
     float* s_act = s_act_base + b * (kTeamEnvs * A + 4);
     if (!(S == 0 && pend)) {  // a scorer with pending resets produces after them
       draw(s_act);
@@ -1524,7 +1548,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     const bool any_end = team_sync_or<G, TPC>(tm, S == 0 && pend);
     SG_MARK(t_bar);
     if (any_end) {
-      reset_phase(b ^ 1);
+      reset_phase(step - 1);
       if constexpr (S == 0) {
         draw(s_act);
         dynamics(true);
@@ -1542,7 +1566,10 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     }
 
     if constexpr (S > 0) {
-      // producers store the step's generated action rows, then move on
+      // producers store the previous step's observation rows (staged and, after
+      // a reset phase, re-observed by the scorer) and this step's generated
+      // action rows, then move on
+      if (kProdRows && step > 0) store_rows(step - 1);
       if (GEN)
         team_store<CH, kTeamEnvs * CH::kDof, (G - 1) * 32>(P.p.act_buf + row0 * A, s_act, rows * A,
                                                           (rows & 3) == 0, tm.tthread - 32);
@@ -1639,8 +1666,8 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
             }
           }
         }
-      } else {
-        store_rows(b);
+      } else if constexpr (!kProdRows) {
+        store_rows(step);
       }
     }
     SG_MARK(t_post);
@@ -1660,11 +1687,16 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
            t_prod, t_bar, t_post, k_steps);
 #endif
 #undef SG_MARK
-  // rows that ended at the last step: team reset, then the scorer stores the
-  // rows; the producers' registers of those rows are stale (the reset state
+  // rows that ended at the last step: team reset, then the last step's rows
+  // are stored (by the producers once the scorer has re-observed the reset
+  // rows); the producers' registers of reset rows are stale (the reset state
   // is already in HBM)
   const bool fix = team_sync_or<G, TPC>(tm, S == 0 && pend);
-  if (fix) reset_phase((k_steps - 1) & 1);
+  if (fix) reset_phase(k_steps - 1);
+  if constexpr (kProdRows) {
+    if (fix) team_sync<G, TPC>(tm);
+    if (S > 0) store_rows(k_steps - 1);
+  }
   const bool stale = S > 0 && fix && ts.ended[(k_steps - 1) & 1][lane];
   if (active) {
     if (!stale) {
@@ -1754,8 +1786,8 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
   }
   float* base = smem + tm.id * (team_smem_bytes_g<G>(A) / sizeof(float));
   TeamSmem<G>& ts = *reinterpret_cast<TeamSmem<G>*>(base);
-  float* s_obs = base + (sizeof(TeamSmem<G>) + 15) / 16 * 4;  // 2 x 32 x O
-  float* s_act = s_obs + 2 * kTeamEnvs * O;                    // 2 x (32 x A + 4)
+  float* s_obs = base + (sizeof(TeamSmem<G>) + 15) / 16 * 4;  // team_obs_bufs x 32 x O
+  float* s_act = s_obs + team_obs_bufs<G>() * kTeamEnvs * O;  // 2 x (32 x A + 4)
   if (P.p.ended_clear && blockIdx.x == 0 && threadIdx.x == 0) {
     *P.p.ended_clear = 0;
     if (P.p.sat_clear) *P.p.sat_clear = 0;

@@ -358,6 +358,9 @@ struct FwdArgs {
   uint64_t step_off;
   float* actions;
   float* logp;
+  // precomputed sampling (sg_policy_noise), when non-null: actions =
+  // (float)(mean + noise[row A + dim]); logp was written by the noise kernel
+  const double* noise;
 };
 
 #ifdef SG_POLICY_PROBE
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   const int group = tid / kRows;      // warp / 4: trunk * 2 + column half
   const int trunk = warp >> 3, half = (warp >> 2) & 1;
 #ifdef SG_POLICY_PROBE
-  long long probe_t[12] = {};
+  long long probe_t[14] = {};
 #endif
   PPROBE(0);
   bool boot_row = true;
@@ -425,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   __syncthreads();
+  PPROBE(11);
   if (tid == 0) {  // every weight image, in the order the layers need them, while the obs tile is converted
     bulk_load(sbase + kBias, W.b1, 928 * 4, smem_u32(&bars[0]));
     bulk_load(sbase + kW1, W.w1, 32768, smem_u32(&bars[1]));
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     bulk_load(sbase + kW2c, W.w2c, 65536, smem_u32(&bars[3]));
     bulk_load(sbase + kW34, W.w34, 36864, smem_u32(&bars[4]));
   }
-  if (warp == 1 && args.actions) {  // the trainer-stream state of this tile's first draw (row0, dim 0)
+  if (warp == 1 && args.actions && !args.noise) {  // the trainer-stream state of this tile's first draw (row0, dim 0)
     const uint64_t s = jump_warp(args.s0, *args.pos + args.step_off + 2ull * (uint64_t)row0 * (uint64_t)args.act_dim, J);
     if ((tid & 31) == 0) *reinterpret_cast<uint64_t*>(smem + kBar + 72) = s;
   }
@@ -452,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     uint4* d = reinterpret_cast<uint4*>(smem + kX0 + kmajor_off(row, c0, kRows));
     *d = make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
   }
+  PPROBE(12);
   async_proxy_fence();
   tc_fence_before();
   __syncthreads();
@@ -474,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   constexpr int kDraws = kNOut / kGroups;
   double zs[kDraws], terms[kDraws];
   const int64_t srow = row0 + row;
-  const bool sampling = args.actions != nullptr && srow < args.n && group < args.act_dim;
+  const bool sampling = args.actions != nullptr && !args.noise && srow < args.n && group < args.act_dim;
   mbar_wait(bar_bias, 0);  // bulk-copied biases visible to this thread
   const float* b1 = sbias + 256 * trunk;
   const float* b2 = sbias + 512 + 128 * trunk;
@@ -575,7 +580,16 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
       args.value[row0 + row] = boot_row ? v[0] + b4[0] : 0.f;
     }
   }
-  if (args.actions) {
+  if (args.noise) {
+    // precomputed sampling: the actor's output rows plus the scaled noise
+    if (group == 0 && srow < args.n) {
+      const int A = args.act_dim;
+      const double* nz = args.noise + srow * A;
+#pragma unroll
+      for (int d = 0; d < kNOut; ++d)
+        if (d < A) args.actions[srow * A + d] = (float)__dadd_rn((double)mv[d], nz[d]);
+    }
+  } else if (args.actions) {
     // Fused sampling, action part: the mean rows go to the (idle since layer 1)
     // X / W1 region, each thread forms the actions of its draws, the per-dim
     // log-prob terms meet there too and group 0 sums them in dim order -- the
@@ -611,8 +625,9 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   PPROBE(10);
 #ifdef SG_POLICY_PROBE
   if (blockIdx.x == 0 && (tid & 127) == 0)
-    printf("pprobe warp %2d: obs %lld L1 %lld epi1 %lld draws %lld L2 %lld epi2 %lld L3 %lld epi3+L4 %lld out %lld end %lld\n",
-           warp, probe_t[1] - probe_t[0], probe_t[2] - probe_t[1], probe_t[3] - probe_t[2], probe_t[4] - probe_t[3],
+    printf("pprobe warp %2d: init %lld obsld %lld sync %lld | obs %lld L1 %lld epi1 %lld draws %lld L2 %lld epi2 %lld L3 %lld epi3+L4 %lld out %lld end %lld\n",
+           warp, probe_t[11] - probe_t[0], probe_t[12] - probe_t[11], probe_t[1] - probe_t[12],
+           probe_t[1] - probe_t[0], probe_t[2] - probe_t[1], probe_t[3] - probe_t[2], probe_t[4] - probe_t[3],
            probe_t[5] - probe_t[4], probe_t[6] - probe_t[5], probe_t[7] - probe_t[6], probe_t[8] - probe_t[7],
            probe_t[9] - probe_t[8], probe_t[10] - probe_t[0]);
 #endif
@@ -705,6 +720,44 @@ __global__ void policy_sample_kernel(const float* __restrict__ mean, int64_t n, 
     lp = __dadd_rn(lp, term);
   }
   logp[e] = (float)lp;
+}
+
+// The stream part of the rollout sampling (ppo.cpp:262-277) ahead of the
+// forward: block = 32 envs x A dims, one (env, dim) draw per thread at
+// pos + step_off + 2 (e A + dim) (warp-parallel jump to the block's first
+// draw, then <= 10 bits), sz = exp(clamp(ls)) z in fp64 and the env's log-prob
+// (terms summed in dim order, as policy_sample_kernel). Runs on the fp64 pipe
+// while the env step (SIMT fp32, a few warps per SM) produces the
+// observations the forward consumes.
+__global__ void policy_noise_kernel(int64_t n, int A, const float* __restrict__ log_std_raw, uint64_t s0,
+                                    uint64_t inc, const uint64_t* __restrict__ pos, uint64_t step_off,
+                                    const __grid_constant__ Jump64 J, double* __restrict__ sz, float* __restrict__ logp) {
+  __shared__ double sterm[32 * kNOut];
+  __shared__ uint64_t sbase;
+  const int tid = threadIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.x * 32;
+  if (tid < 32) {
+    const uint64_t b = jump_warp(s0, *pos + step_off + 2ull * (uint64_t)e0 * (uint64_t)A, J);
+    if (tid == 0) sbase = b;
+  }
+  __syncthreads();
+  const int64_t e = e0 + tid / A;
+  const int d = tid % A;
+  double term = 0.0;
+  if (e < n) {
+    uint64_t st = jump(sbase, 2ull * (uint64_t)tid, J);
+    const double ls = clamp_log_std(log_std_raw[d]);
+    const double z = draw_normal(st, inc);
+    term = logp_term(z, ls);
+    sz[e * A + d] = __dmul_rn(exp(ls), z);
+  }
+  sterm[tid] = term;
+  __syncthreads();
+  if (tid < 32 && e0 + tid < n) {
+    double lp = 0.0;
+    for (int k = 0; k < A; ++k) lp = __dadd_rn(lp, sterm[tid * A + k]);
+    logp[e0 + tid] = (float)lp;
+  }
 }
 
 // ---- GAE (rollout.cpp:42-66) + episode statistics (ppo.cpp:286-303) --------
@@ -999,6 +1052,7 @@ struct SampleArgs {
   uint64_t step_off = 0;
   float* actions = nullptr;
   float* logp = nullptr;
+  const double* noise = nullptr;
 };
 
 static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, float* d_mean,
@@ -1019,9 +1073,9 @@ static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int
   W.b4c = p->bias + 912;
   sgp::FwdArgs a{d_obs, n, p->obs_dim, obs_stride > 0 ? obs_stride : p->obs_dim, p->act_dim, d_mean, d_value,
                  d_timed_out, d_terminated, smp.log_std_raw, smp.s0, smp.inc, smp.pos, smp.step_off, smp.actions,
-                 smp.logp};
+                 smp.logp, smp.noise};
   static const sgp::Jump64 kNone{};
-  const sgp::Jump64 J = smp.actions ? jump_table(smp.inc) : kNone;
+  const sgp::Jump64 J = smp.actions && !smp.noise ? jump_table(smp.inc) : kNone;
   const unsigned grid = (unsigned)((n + sgp::kRows - 1) / sgp::kRows);
   sgp::policy_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a, J);
   const cudaError_t e = cudaGetLastError();
@@ -1052,6 +1106,31 @@ int sg_policy_act(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs
   smp.step_off = step_offset;
   smp.actions = d_actions;
   smp.logp = d_logp;
+  return policy_forward(p, d_obs, n, obs_stride, d_mean, d_value, nullptr, nullptr, stream, smp);
+}
+
+int sg_policy_noise(const sg_policy* p, int64_t n, const float* d_log_std_raw, uint64_t stream_state,
+                    uint64_t stream_inc, const uint64_t* d_draw_pos, uint64_t step_offset, double* d_scaled_noise,
+                    float* d_logp, void* stream) {
+  if (n <= 0) return SG_OK;
+  if (!d_log_std_raw || !d_draw_pos || !d_scaled_noise || !d_logp)
+    return fail(SG_ERR_CONFIG, "sg_policy_noise: null argument");
+  if (p->act_dim > sgp::kNOut) return fail(SG_ERR_CONFIG, "sg_policy_noise: action_dim > 16");
+  const sgp::Jump64 J = jump_table(stream_inc);
+  const int A = p->act_dim;
+  sgp::policy_noise_kernel<<<(unsigned)((n + 31) / 32), 32 * A, 0, (cudaStream_t)stream>>>(
+      n, A, d_log_std_raw, stream_state, stream_inc, d_draw_pos, step_offset, J, d_scaled_noise, d_logp);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_policy_act_noise(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride,
+                        const double* d_scaled_noise, float* d_actions, float* d_mean, float* d_value, void* stream) {
+  if (!d_actions || !d_scaled_noise || !d_value) return fail(SG_ERR_CONFIG, "sg_policy_act_noise: null argument");
+  if (p->act_dim > sgp::kNOut) return fail(SG_ERR_CONFIG, "sg_policy_act_noise: action_dim > 16");
+  SampleArgs smp;
+  smp.actions = d_actions;
+  smp.noise = d_scaled_noise;
   return policy_forward(p, d_obs, n, obs_stride, d_mean, d_value, nullptr, nullptr, stream, smp);
 }
 

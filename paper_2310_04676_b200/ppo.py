@@ -61,6 +61,12 @@ class TrainConfig:  # ppo.hpp:25-45
     seed: int = 0
     update_precision: str = "tf32"  # fp32 | tf32 | bf16 (autocast) for the update GEMMs
     cuda_graph: bool = True  # capture the update in a CUDA graph (single rank)
+    # draw step t+1's sampling noise on a side stream during env step t
+    # (sg_policy_noise + sg_policy_act_noise, bit-identical to the fused
+    # sg_policy_act); measured slower on B200 (rollout 725 vs 788 M
+    # env-steps/s: the fp64 noise kernel outlasts the K = 1 env step it
+    # overlaps and the fork / join adds graph edges), so off by default
+    noise_ahead: bool = False
 
     def validate(self):  # ppo.cpp:31-48 (subset relevant on device)
         if not 0.0 <= self.gamma <= 1.0:
@@ -365,6 +371,9 @@ class Trainer:
         obs_dt = torch.bfloat16 if cfg.update_precision == "bf16" else torch.float32
         self.mb_buf = dict(obs=z(mb, _up8(O), dt=obs_dt), act=z(mb, A), logp=z(mb), adv=z(mb), ret=z(mb))
         self.mean = z(N, A)
+        # scaled sampling noise of the current / next rollout step (sg_policy_noise)
+        self.noise = [z(N, A, dt=torch.float64), z(N, A, dt=torch.float64)]
+        self.noise_stream = torch.cuda.Stream(dev)
         self.log_std_c = z(A)
         self.rollout_graph = None
         self.ep_acc = z(N)
@@ -433,13 +442,33 @@ class Trainer:
         log_std = self.log_std_c
         log_std.copy_(self.params[self.ls_off: self.ls_off + A])
         b["obs"][0].copy_(b["obs"][T])
+        ahead = self.cfg.noise_ahead
+        main = torch.cuda.current_stream(self.dev)
+
+        def noise(t, stream):  # step t's draws: scaled noise + log-probs (ppo.cpp:262-277)
+            sg._pcheck(L.sg_policy_noise(pol._h, N, log_std.data_ptr(), self.stream_state, self.stream_inc,
+                                         self.d_pos.data_ptr(), 2 * A * (t * self.global_n + self.row_off),
+                                         self.noise[t % 2].data_ptr(), b["logp"][t].data_ptr(), stream))
+        if ahead:
+            noise(0, st)
         for t in range(T):
             obs = b["obs"][t]
-            # policy forward + Gaussian sampling + log-prob: one tcgen05 launch
-            sg._pcheck(L.sg_policy_act(pol._h, obs.data_ptr(), N, obs.stride(0), log_std.data_ptr(),
-                                       self.stream_state, self.stream_inc, self.d_pos.data_ptr(),
-                                       2 * A * (t * self.global_n + self.row_off), b["actions"][t].data_ptr(),
-                                       b["logp"][t].data_ptr(), None, b["values"][t].data_ptr(), st))
+            if ahead:
+                # policy forward + actions from the noise drawn during the
+                # previous env step: one tcgen05 launch
+                sg._pcheck(L.sg_policy_act_noise(pol._h, obs.data_ptr(), N, obs.stride(0),
+                                                 self.noise[t % 2].data_ptr(), b["actions"][t].data_ptr(), None,
+                                                 b["values"][t].data_ptr(), st))
+                if t + 1 < T:  # the next step's draws (fp64 pipe) overlap this env step (fp32 SIMT)
+                    self.noise_stream.wait_stream(main)
+                    with torch.cuda.stream(self.noise_stream):
+                        noise(t + 1, self.noise_stream.cuda_stream)
+            else:
+                # policy forward + Gaussian sampling + log-prob: one tcgen05 launch
+                sg._pcheck(L.sg_policy_act(pol._h, obs.data_ptr(), N, obs.stride(0), log_std.data_ptr(),
+                                           self.stream_state, self.stream_inc, self.d_pos.data_ptr(),
+                                           2 * A * (t * self.global_n + self.row_off), b["actions"][t].data_ptr(),
+                                           b["logp"][t].data_ptr(), None, b["values"][t].data_ptr(), st))
             # the env writes the step's observations / rewards / flags / errors
             # into the rollout buffer itself (ppo.cpp:280-299)
             direct = (N * self.O) % 4 == 0  # slots 16-byte aligned: the kernel's row stores go straight in
@@ -454,6 +483,8 @@ class Trainer:
                                                  b["boot"][t].data_ptr(), st))
             else:
                 b["boot"][t].zero_()
+            if ahead and t + 1 < T:
+                main.wait_stream(self.noise_stream)
         pol.forward(b["obs"][T], self.mean, b["last_values"])
 
     def gae(self):

@@ -144,6 +144,10 @@ _SIGS = {
                                    C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_policy_act": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_uint64, C.c_uint64,
                                 C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_noise": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64,
+                                  C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_act_noise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p]),
@@ -601,6 +605,37 @@ class Policy:
         _pcheck(lib().sg_policy_sample(mean.data_ptr(), n, A, log_std.data_ptr(), s0, inc, pos.data_ptr(), step_offset,
                                        acts.data_ptr(), logp.data_ptr(), stream))
         return acts, logp
+
+    def noise(self, n: int, seed: int = 0, log_std=None, draw_pos: int = 0, step_offset: int = 0, device: int = 0):
+        """sg_policy_noise: the sampling's stream part ahead of the forward.
+        Returns (scaled noise n x A fp64, log_probs n)."""
+        import torch
+        A = self.action_dim
+        dev = f"cuda:{device}"
+        if log_std is None:
+            log_std = torch.full((A,), -1.0, device=dev)
+        s0, inc = make_stream(seed, TRAIN_STREAM)
+        pos = torch.tensor([draw_pos], dtype=torch.int64, device=dev)
+        sz = torch.empty((n, A), dtype=torch.float64, device=dev)
+        logp = torch.empty((n,), device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _pcheck(lib().sg_policy_noise(self._h, n, log_std.data_ptr(), s0, inc, pos.data_ptr(), step_offset,
+                                      sz.data_ptr(), logp.data_ptr(), stream))
+        return sz, logp
+
+    def act_noise(self, obs, scaled_noise, want_mean: bool = False):
+        """sg_policy_act_noise: forward + actions = mean + scaled_noise.
+        Returns (actions, value[, mean])."""
+        import torch
+        n, dev, A = obs.shape[0], obs.device, self.action_dim
+        acts = torch.empty((n, A), device=dev)
+        value = torch.empty((n,), device=dev)
+        mean = torch.empty((n, A), device=dev) if want_mean else None
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _pcheck(lib().sg_policy_act_noise(self._h, obs.data_ptr(), n, obs.stride(0), scaled_noise.data_ptr(),
+                                          acts.data_ptr(), mean.data_ptr() if want_mean else None, value.data_ptr(),
+                                          stream))
+        return (acts, value, mean) if want_mean else (acts, value)
 
 
 # -- PPO update kernels (train.cu) ---------------------------------------------

@@ -112,3 +112,25 @@ def test_fused_forward_sampling_equals_separate_calls(sg, n, act_dim, obs_dim):
     torch.cuda.synchronize()
     assert torch.equal(m2, mean) and torch.equal(v2, value)
     assert torch.equal(a2, acts) and torch.equal(lp2, logp)
+
+
+@pytest.mark.parametrize("n,act_dim,obs_dim", [(16384, 7, 27), (1000, 6, 24), (130, 16, 30)])
+def test_precomputed_noise_equals_fused_sampling(sg, n, act_dim, obs_dim):
+    """sg_policy_noise (the sampling's stream part, ahead of the forward) +
+    sg_policy_act_noise == sg_policy_act bit for bit: actions, log-probs,
+    mean and value, at an arbitrary stream position and log-std."""
+    torch.manual_seed(2)
+    pol = sg.Policy(obs_dim, act_dim)
+    flat = torch.from_numpy(pol.init_params(seed=5)).cuda()
+    pol.load_params(flat + 0.05 * torch.randn_like(flat))
+    obs = torch.randn(n, obs_dim, device="cuda") * 0.5
+    ls = torch.linspace(-1.5, 0.5, act_dim, device="cuda")
+    ls[-1] = 3.0
+    kw = dict(seed=11, log_std=ls, draw_pos=98765, step_offset=2 * act_dim * 31)
+    a1, lp1, v1, m1 = pol.act(obs, want_mean=True, **kw)
+    sz, lp2 = pol.noise(n, **kw)
+    a2, v2, m2 = pol.act_noise(obs, sz, want_mean=True)
+    torch.cuda.synchronize()
+    assert torch.equal(m2, m1) and torch.equal(v2, v1)
+    assert torch.equal(lp2, lp1)
+    assert torch.equal(a2, a1)

@@ -331,3 +331,25 @@ def test_shard_sampling_takes_its_rows_of_the_global_stream(sg):
         assert torch.equal(part, full[r * N:(r + 1) * N])
         assert torch.equal(lp, lp_full[r * N:(r + 1) * N])
     assert not torch.equal(full[:N], full[N:2 * N])
+
+
+def test_rollout_noise_ahead_equals_fused_sampling(sg):
+    """The trainer's default rollout draws step t+1's noise on a side stream
+    during env step t (sg_policy_noise + sg_policy_act_noise, CUDA-graphed
+    with a fork/join per step); it must leave the rollout buffer bit-identical
+    to the fused per-step sg_policy_act path, including across the graph
+    replays of later rollouts and an episode boundary."""
+    from paper_2310_04676_b200 import ppo
+    bufs = []
+    for ahead in (True, False):
+        env = sg.VecTaskEnv(robots=("psm",), n_envs=2048, seed=1, episode_len=40)
+        tr = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim), ppo.TrainConfig(seed=2, noise_ahead=ahead))
+        out = []
+        for _ in range(3):  # eager rollout, graph capture, graph replay
+            tr.rollout()
+            torch.cuda.synchronize()
+            out.append({k: tr.buf[k].clone() for k in ("obs", "actions", "logp", "values", "rewards", "boot")})
+        bufs.append(out)
+    for a, b in zip(*bufs):
+        for k in a:
+            assert torch.equal(a[k], b[k]), k
