@@ -336,7 +336,7 @@ struct sg_env {
   // bursts then install precomputed resets. Single steps reset inline.
   void launch_step(int k_steps, bool gen) {
     if (k_steps > 1 && P.p.rec_valid) {
-      const unsigned grid = static_cast<unsigned>((4 * n + sg::kRecThreads - 1) / sg::kRecThreads);  // 4 lanes/env
+      const unsigned grid = static_cast<unsigned>((n + sg::kRecEnvsPerBlock - 1) / sg::kRecEnvsPerBlock);
       sg::path_record_kernel<<<grid, sg::kRecThreads, 0, stream>>>(P);
       CK(cudaGetLastError());
     }

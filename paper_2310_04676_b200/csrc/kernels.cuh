@@ -583,6 +583,7 @@ __device__ __forceinline__ int sample_path_waypoints(const TaskParams& T, uint64
   return err;
 }
 
+#ifdef SG_RECORD_QUAD
 // Computes the next reset_row of every PathFollowing env whose record is
 // stale (after its last reset consumed it): q draws (middle half of each
 // range, rounded once) then sample_path, from the env's current stream
@@ -596,6 +597,7 @@ __device__ __forceinline__ int sample_path_waypoints(const TaskParams& T, uint64
 // sample_spline_waypoints; lane 0 writes). Same operations and summation
 // order as spline_waypoints_stream, so the tables are bit-identical.
 constexpr int kRecThreads = 128;
+constexpr int kRecEnvsPerBlock = kRecThreads / 4;
 static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const __grid_constant__ StepParams P) {
   constexpr int kQ = 4, kU = 5, kRound = kQ * kU;  // lanes per env, knots per lane per round
   static_assert(kSplineSubdiv % kRound == 0, "rounds must tile the knots");
@@ -711,6 +713,244 @@ static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const _
   P.p.rec_rng[i] = s;
   P.p.rec_valid[i] = 1;
 }
+
+#else
+// Computes the next reset_row of every PathFollowing env whose record is
+// stale (after its last reset consumed it): q draws (middle half of each
+// range, rounded once) then sample_path, from the env's current stream
+// state, into the record buffers.
+//
+// Warp-specialised: a block owns 32 envs. Warps 1-4 are EVALUATORS, four
+// lanes per env: they draw the env's q and spline (every lane of the quad the
+// same stream; the 101-point offset scan split over the quad), then per round
+// of 20 knots lane r evaluates knots r*5+1..r*5+5 and their chord lengths
+// (5 independent fp64 chains) into a shared-memory ring. Warp 0 is the
+// WALKER, one lane per env: it takes each round's 20 chords in knot order
+// and runs the cumulative sum of sample_spline_waypoints (spline.cpp:40-72),
+// queueing each waypoint emission's inputs; the evaluators turn a round's
+// queue (all 32 envs, compacted, one emission per lane: the fp64 divisions
+// and the spline evaluation without divergence) into waypoints while the
+// walker sums the next round. Two ring / queue stages, handed over with named
+// barriers (FULL: evaluators arrive, walker syncs; EMPTY: the reverse). Same
+// operations and summation order as spline_waypoints_stream, so the tables
+// are bit-identical.
+constexpr int kRecEnvsPerBlock = 32, kRecQ = 4, kRecU = 5, kRecRound = kRecQ * kRecU;
+constexpr int kRecRounds = kSplineSubdiv / kRecRound;
+constexpr int kRecPad = kRecRound + 1;  // 21 doubles per env row: conflict-free walker loads
+constexpr int kRecEval = kRecEnvsPerBlock * kRecQ;  // evaluator threads
+constexpr int kRecThreads = 32 + kRecEval;           // 160
+constexpr int kRecEmitQ = 6;                         // queued emissions per env per round
+static_assert(kSplineSubdiv % kRecRound == 0, "rounds must tile the knots");
+
+struct RecEmit {  // one queued waypoint emission
+  double cum_prev, cum_k, sv;
+  int k, slot;
+};
+
+__device__ __forceinline__ void rec_bar_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kRecThreads) : "memory"); }
+__device__ __forceinline__ void rec_bar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(kRecThreads) : "memory");
+}
+
+// One waypoint of sample_spline_waypoints: target sv reached at knot k,
+// t = (k - 1 + (sv - cum_prev) / seg_len) / 1000, fp32 copy of eval(t).
+__device__ __forceinline__ void rec_emit(const Spline& sp, float* dst, double cp, double ck, double svv, int k) {
+  const double seg_len = __dadd_rn(ck, -cp);
+  const double frac = seg_len > 0.0 ? __dadd_rn(svv, -cp) / seg_len : 0.0;
+  const double tw = __dmul_rn(1.0, __dadd_rn((double)(k - 1), frac)) / (double)kSplineSubdiv;
+  double wv[3];
+  spline_eval(sp, tw, wv);
+  dst[0] = (float)wv[0];
+  dst[1] = (float)wv[1];
+  dst[2] = (float)wv[2];
+}
+
+static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const __grid_constant__ StepParams P) {
+  constexpr int kBarSetup = 1, kBarFull = 2, kBarEmpty = 4, kBarDone = 6;  // FULL / EMPTY: + stage
+  __shared__ double ring[2][kRecEnvsPerBlock][kRecPad];
+  __shared__ RecEmit s_q[2][kRecEnvsPerBlock][kRecEmitQ];
+  __shared__ int s_qoff[2][kRecEnvsPerBlock + 1];  // exclusive offsets, total at [32]
+  __shared__ double s_sp[kRecEnvsPerBlock][12];
+  __shared__ uint64_t s_rng[kRecEnvsPerBlock];
+  __shared__ int s_err[kRecEnvsPerBlock], s_need[kRecEnvsPerBlock];
+  const RobotTable& R = P.robot;
+  const TaskParams& T = P.task;
+  const int64_t n = T.n;
+  const int cap = T.wp_cap;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e0 = (int64_t)blockIdx.x * kRecEnvsPerBlock;
+  const int el = warp == 0 ? lane : (warp - 1) * (32 / kRecQ) + lane / kRecQ;  // env of this thread
+  const int64_t i = e0 + el;
+  const bool need = i < n && !P.p.rec_valid[i];
+  if (warp == 0) s_need[lane] = need ? 1 : 0;
+  if (!__syncthreads_or(need)) return;
+
+  if (warp > 0) {  // ---- evaluators ----------------------------------------
+    const int r = lane & (kRecQ - 1), base = lane & ~(kRecQ - 1);
+    const int te = threadIdx.x - 32;  // 0 .. kRecEval - 1
+    uint64_t s = need ? P.p.rng_state[i] : 0;
+    const uint64_t inc = need ? P.p.rng_inc[i] : 1;
+    for (int d = 0; d < R.dof; ++d) {  // (lanes without work draw from a dummy stream)
+      const double quarter = __dmul_rn(0.25, __dadd_rn(R.hi_d[d], -R.lo_d[d]));
+      const float qv = (float)pcg_uniform(s, inc, __dadd_rn(R.lo_d[d], quarter), __dadd_rn(R.hi_d[d], -quarter));
+      if (need && r == 0) P.p.rec_q[d * n + i] = qv;
+    }
+    Spline sp;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) sp.c[k] = 0.0;
+    const int err = sample_path_spline<kRecQ>(T, s, inc, sp);
+    if (r == 0) {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) s_sp[el][k] = sp.c[k];
+      s_rng[el] = s;
+      s_err[el] = need ? err : 0;
+    }
+    rec_bar_arrive(kBarSetup);
+    double p_end[3];  // last knot of the previous round (lane r = 0 needs it)
+    spline_eval(sp, 0.0, p_end);
+    for (int j = 0; j < kRecRounds + 2; ++j) {
+      const int st = j & 1;
+      double dk[kRecU];
+      if (j < kRecRounds) {
+        const int k0 = 1 + j * kRecRound + r * kRecU;  // this lane's first knot
+        double px[kRecU][3], pp[3];
+#pragma unroll
+        for (int u = 0; u < kRecU; ++u) spline_eval(sp, kSplineT.t[k0 + u], px[u]);
+        // knot k0 - 1: the previous lane's last knot, or the previous round's end
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double up = __shfl_sync(0xffffffffu, px[kRecU - 1][k], (lane + 31) & 31);  // lane - 1
+          pp[k] = r == 0 ? p_end[k] : up;
+        }
+        dk[0] = dist3_rn(px[0], pp);
+#pragma unroll
+        for (int u = 1; u < kRecU; ++u) dk[u] = dist3_rn(px[u], px[u - 1]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) p_end[k] = __shfl_sync(0xffffffffu, px[kRecU - 1][k], base + kRecQ - 1);
+      }
+      if (j >= 2) {
+        // the walker is done with round j - 2 in this stage: its chords are
+        // consumed and its emissions queued -- turn them into waypoints
+        rec_bar_sync(kBarEmpty + st);
+        const int total_q = s_qoff[st][kRecEnvsPerBlock];
+        for (int f = te; f < total_q; f += kRecEval) {
+          int e = 0;  // last env whose first entry is <= f
+#pragma unroll
+          for (int step = 16; step; step >>= 1)
+            if (e + step < kRecEnvsPerBlock && s_qoff[st][e + step] <= f) e += step;
+          const RecEmit& q = s_q[st][e][f - s_qoff[st][e]];
+          if (s_need[e] && q.slot < cap) {
+            Spline spe;
+#pragma unroll
+            for (int c = 0; c < 12; ++c) spe.c[c] = s_sp[e][c];
+            rec_emit(spe, P.p.rec_wps + (e0 + e) * (int64_t)cap * 3 + 3 * q.slot, q.cum_prev, q.cum_k, q.sv, q.k);
+          }
+        }
+      }
+      if (j < kRecRounds) {
+#pragma unroll
+        for (int u = 0; u < kRecU; ++u) ring[st][el][r * kRecU + u] = dk[u];
+        rec_bar_arrive(kBarFull + st);
+      }
+    }
+    rec_bar_arrive(kBarDone);
+    return;
+  }
+
+  // ---- walker: lane = env ----------------------------------------------------
+  rec_bar_sync(kBarSetup);
+  Spline sp;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) sp.c[k] = s_sp[lane][k];
+  int err = s_err[lane];
+  const uint64_t s_after = s_rng[lane];
+  const double spacing = T.spacing;
+  float* out = P.p.rec_wps + (need ? i : 0) * (int64_t)cap * 3;
+  {
+    double p0[3];
+    spline_eval(sp, 0.0, p0);
+    if (need) {
+      out[0] = (float)p0[0];
+      out[1] = (float)p0[1];
+      out[2] = (float)p0[2];
+    }
+  }
+  int tentative = 1;
+  double cum_prev = 0.0, sv = spacing;
+  double s_emit[2] = {0.0, 0.0};  // targets of the last two tentative emissions
+  for (int j = 0; j < kRecRounds; ++j) {
+    const int st = j & 1;
+    rec_bar_sync(kBarFull + st);
+    const double* dr = ring[st][lane];
+    // cum is non-decreasing: a round whose last cumulative length is below the
+    // next target emits nothing and needs only its sums (same additions)
+    double cum_end = cum_prev;
+#pragma unroll
+    for (int u = 0; u < kRecRound; ++u) cum_end = __dadd_rn(cum_end, dr[u]);
+    int qn = 0;
+    if (__all_sync(0xffffffffu, !(cum_end >= sv))) {
+      cum_prev = cum_end;
+    } else {
+#pragma unroll 1
+      for (int u = 0; u < kRecRound; ++u) {
+        const int k = 1 + j * kRecRound + u;
+        const double cum_k = __dadd_rn(cum_prev, dr[u]);
+        while (cum_k >= sv) {  // the reference's while loop stops at seg = k - 1 for this s
+          if (qn < kRecEmitQ) {
+            RecEmit& q = s_q[st][lane][qn++];
+            q.cum_prev = cum_prev;
+            q.cum_k = cum_k;
+            q.sv = sv;
+            q.k = k;
+            q.slot = tentative;
+          } else if (need && tentative < cap) {  // queue full (rare): emit on the spot
+            rec_emit(sp, out + 3 * tentative, cum_prev, cum_k, sv, k);
+          }
+          s_emit[tentative & 1] = sv;
+          ++tentative;
+          sv = __dadd_rn(sv, spacing);
+        }
+        cum_prev = cum_k;
+      }
+    }
+    // publish the round's queue (exclusive scan of the per-env counts)
+    int off = qn;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += v;
+    }
+    s_qoff[st][lane] = off - qn;
+    if (lane == 31) s_qoff[st][kRecEnvsPerBlock] = off;
+    __syncwarp();
+    rec_bar_arrive(kBarEmpty + st);
+  }
+  rec_bar_sync(kBarDone);  // every queued waypoint is written
+  if (!need) return;
+  const double total = cum_prev;
+  int count = 1;
+  if (total > 1e-12) {
+    const double limit = __dadd_rn(total, -1e-12);
+    count = tentative;
+    while (count > 1 && !(s_emit[(count - 1) & 1] < limit)) --count;  // drop s >= total - 1e-12
+    if (count >= cap) {
+      err |= kErrWaypointCap;
+      count = cap;
+    } else {
+      double p_last[3];  // pts[1000]
+      spline_eval(sp, kSplineT.t[kSplineSubdiv], p_last);
+      out[3 * count + 0] = (float)p_last[0];
+      out[3 * count + 1] = (float)p_last[1];
+      out[3 * count + 2] = (float)p_last[2];
+      count += 1;
+    }
+  }
+  P.p.rec_len[i] = count;
+  P.p.rec_err[i] = err;
+  P.p.rec_rng[i] = s_after;
+  P.p.rec_valid[i] = 1;
+}
+#endif
 
 // reset_row (envs.cpp:304-360) for one env. Out of line (rare path) and
 // communicating through HBM only, so the caller's state arrays stay in
