@@ -765,7 +765,11 @@ __device__ __forceinline__ void rec_emit(const Spline& sp, float* dst, double cp
   dst[2] = (float)wv[2];
 }
 
-static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const __grid_constant__ StepParams P) {
+// 4 blocks per SM: the 512 blocks of 16,384 envs run in one wave on 148 SMs
+#ifndef SG_REC_MINB
+#define SG_REC_MINB 4
+#endif
+static __global__ void __launch_bounds__(kRecThreads, SG_REC_MINB) path_record_kernel(const __grid_constant__ StepParams P) {
   constexpr int kBarSetup = 1, kBarFull = 2, kBarEmpty = 4, kBarDone = 6;  // FULL / EMPTY: + stage
   __shared__ double ring[2][kRecEnvsPerBlock][kRecPad];
   __shared__ RecEmit s_q[2][kRecEnvsPerBlock][kRecEmitQ];
@@ -882,19 +886,24 @@ static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const _
     const int st = j & 1;
     rec_bar_sync(kBarFull + st);
     const double* dr = ring[st][lane];
-    // cum is non-decreasing: a round whose last cumulative length is below the
-    // next target emits nothing and needs only its sums (same additions)
-    double cum_end = cum_prev;
+    // the round's cumulative lengths (one dependent fp64 add per knot, in the
+    // reference's order); cum is non-decreasing, so a round whose last value
+    // is below the next target emits nothing
+    double cum[kRecRound];
+    {
+      double c = cum_prev;
 #pragma unroll
-    for (int u = 0; u < kRecRound; ++u) cum_end = __dadd_rn(cum_end, dr[u]);
+      for (int u = 0; u < kRecRound; ++u) {
+        c = __dadd_rn(c, dr[u]);
+        cum[u] = c;
+      }
+    }
     int qn = 0;
-    if (__all_sync(0xffffffffu, !(cum_end >= sv))) {
-      cum_prev = cum_end;
-    } else {
-#pragma unroll 1
+    if (__any_sync(0xffffffffu, cum[kRecRound - 1] >= sv)) {
+#pragma unroll
       for (int u = 0; u < kRecRound; ++u) {
         const int k = 1 + j * kRecRound + u;
-        const double cum_k = __dadd_rn(cum_prev, dr[u]);
+        const double cum_k = cum[u];
         while (cum_k >= sv) {  // the reference's while loop stops at seg = k - 1 for this s
           if (qn < kRecEmitQ) {
             RecEmit& q = s_q[st][lane][qn++];
@@ -913,6 +922,7 @@ static __global__ void __launch_bounds__(kRecThreads) path_record_kernel(const _
         cum_prev = cum_k;
       }
     }
+    cum_prev = cum[kRecRound - 1];
     // publish the round's queue (exclusive scan of the per-env counts)
     int off = qn;
 #pragma unroll
