@@ -31,6 +31,7 @@ import ctypes as C
 from dataclasses import dataclass
 
 import math
+import os
 
 import torch
 import torch.nn.functional as F
@@ -96,6 +97,7 @@ class _Linear(torch.autograd.Function):
         Wc = W if Wc is None else Wc
         bc = b if bc is None else bc
         ctx.w_dtype = W.dtype
+        ctx.direct = _direct_grads(W, b)
         ctx.save_for_backward(x, Wc)
         return torch.addmm(bc, x, Wc.t())
 
@@ -103,6 +105,19 @@ class _Linear(torch.autograd.Function):
     def backward(ctx, gy):
         x, W = ctx.saved_tensors
         return _linear_grads(ctx, gy, x, W)
+
+
+_DIRECT_GRADS = os.environ.get("SG_NO_DIRECT_GRAD") != "1"  # A/B switch
+
+
+def _direct_grads(W, b):
+    """(W.grad, b.grad) when the trainer owns them (zeroed before every
+    minibatch, each layer used once per forward): the backward GEMMs then
+    write the gradients straight into the flat gradient buffer instead of
+    returning them for autograd to accumulate (one add kernel per tensor)."""
+    if _DIRECT_GRADS and getattr(W, "_sg_direct_grad", False) and W.grad is not None and b.grad is not None:
+        return W.grad, b.grad
+    return None
 
 
 def _linear_grads(ctx, gy, x, W):
@@ -113,11 +128,20 @@ def _linear_grads(ctx, gy, x, W):
     gx = gy @ W if ctx.needs_input_grad[0] else None
     B = gy.shape[0]
     out_dt = torch.float32 if gy.dtype in (torch.bfloat16, torch.float16) else None
-    gW = torch.mm(gy.t(), x, out_dtype=out_dt) if out_dt else gy.t() @ x
     key = (B, gy.dtype, gy.device)
     ones = _Linear._ones.get(key)
     if ones is None:
         ones = _Linear._ones[key] = torch.ones(1, B, dtype=gy.dtype, device=gy.device)
+    if ctx.direct is not None and (out_dt is not None or gy.dtype == ctx.w_dtype):
+        gW_buf, gb_buf = ctx.direct
+        if out_dt:
+            torch.mm(gy.t(), x, out_dtype=out_dt, out=gW_buf)
+            torch.mm(ones, gy, out_dtype=out_dt, out=gb_buf.view(1, -1))
+        else:
+            torch.mm(gy.t(), x, out=gW_buf)
+            torch.mm(ones, gy, out=gb_buf.view(1, -1))
+        return gx, None, None, None, None
+    gW = torch.mm(gy.t(), x, out_dtype=out_dt) if out_dt else gy.t() @ x
     gb = (torch.mm(ones, gy, out_dtype=out_dt) if out_dt else ones @ gy).view(-1)
     return gx, gW.to(ctx.w_dtype), gb.to(ctx.w_dtype), None, None
 
@@ -132,6 +156,7 @@ class _LinearELU(torch.autograd.Function):
         Wc = W if Wc is None else Wc
         bc = b if bc is None else bc
         ctx.w_dtype = W.dtype
+        ctx.direct = _direct_grads(W, b)
         h = sg.elu_forward(torch.addmm(bc, x, Wc.t()), out=None)
         ctx.save_for_backward(x, Wc, h)
         return h
@@ -259,7 +284,8 @@ class _PPOLossDevice(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, mean_full, value_full, log_std_raw, act, old_logp, adv, ret, A, clip_eps, value_coef,
-                entropy_coef):
+                entropy_coef, unit_grad=False):
+        ctx.unit_grad = unit_grad
         dmean = torch.empty_like(mean_full)
         dvalue = torch.empty_like(value_full)
         dls = torch.empty_like(log_std_raw)
@@ -274,9 +300,14 @@ class _PPOLossDevice(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g_loss, g_metrics):
+        # the trainer backpropagates the loss itself (loss.backward(): g_loss
+        # == 1), so the analytic gradients pass through unscaled (no extra
+        # elementwise launches); other callers get them scaled
         dmean, dvalue, dls = ctx.saved_tensors
+        if ctx.unit_grad:
+            return dmean, dvalue, dls, None, None, None, None, None, None, None, None, None
         g = g_loss.to(dmean.dtype)
-        return dmean * g, dvalue * g, dls * g_loss, None, None, None, None, None, None, None, None
+        return dmean * g, dvalue * g, dls * g_loss, None, None, None, None, None, None, None, None, None
 
 
 def ppo_loss(params, obs, actions, old_logp, adv, ret, cfg: TrainConfig, obs_dim, act_dim):
@@ -338,6 +369,7 @@ class Trainer:
             b = self.params[b0: b0 + ob].detach().requires_grad_(True)
             W.grad = self.grad[w0: w0 + o * i].view(o, i)
             b.grad = self.grad[b0: b0 + ob]
+            W._sg_direct_grad = True  # the backward GEMMs write these views directly
             if self.mirror is not None:
                 self.layers.append((W, b, self.mirror[w0: w0 + o * i].view(o, i), self.mirror[b0: b0 + ob]))
             else:
@@ -526,8 +558,8 @@ class Trainer:
                 loss, m = _PPOLossDevice.apply(mean_f.contiguous(), value_f.contiguous(), self.log_std,
                                                g["act"][:m_rows], g["logp"][:m_rows], g["adv"][:m_rows],
                                                g["ret"][:m_rows], self.A, cfg.clip_eps, cfg.value_coef,
-                                               cfg.entropy_coef)
-                loss.backward()
+                                               cfg.entropy_coef, True)
+                loss.backward()  # d loss = 1: the loss head's gradients pass through unscaled
                 allreduce_mean_(self.grad, self.dist, force=self.force_collectives)
                 self._adam_step()
                 metrics += m

@@ -10,6 +10,11 @@ struct Big {
   unsigned char b[2776];
 };
 
+__global__ void spin_kernel(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {
+  }
+}
 __global__ void small_kernel(int* out) {
   if (threadIdx.x == 0 && out) out[blockIdx.x] = 1;
 }
@@ -27,25 +32,37 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  // Gated: a 5 ms spin kernel heads each batch, so every flush / event /
+  // launch of the batch is enqueued before the GPU reaches it (the bench's
+  // protocol); the event pairs then time the GPU side only.
+  const int reps = 20;
+  cudaEvent_t ev[2 * reps];
+  for (int k = 0; k < 2 * reps; ++k) cudaEventCreate(&ev[k]);
   for (int variant = 0; variant < 4; ++variant) {
     const bool use_big = variant & 1, do_flush = variant & 2;
     float total = 0.f;
-    const int reps = 50;
-    for (int r = 0; r < reps + 5; ++r) {
-      if (do_flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
-      cudaEventRecord(e0);
-      if (use_big)
-        big_kernel<<<512, 64>>>(big, out);
-      else
-        small_kernel<<<512, 64>>>(out);
-      cudaEventRecord(e1);
-      cudaEventSynchronize(e1);
-      float ms;
-      cudaEventElapsedTime(&ms, e0, e1);
-      if (r >= 5) total += ms;
+    for (int batch = 0; batch < 3; ++batch) {
+      spin_kernel<<<1, 1>>>(10000000);
+      for (int r = 0; r < reps; ++r) {
+        if (do_flush) cudaMemsetAsync(flush, r & 0xff, flush_bytes);
+        cudaEventRecord(ev[2 * r]);
+        if (use_big)
+          big_kernel<<<512, 64>>>(big, out);
+        else
+          small_kernel<<<512, 64>>>(out);
+        cudaEventRecord(ev[2 * r + 1]);
+      }
+      cudaDeviceSynchronize();
+      if (batch == 0) continue;
+      for (int r = 0; r < reps; ++r) {
+        float ms;
+        cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]);
+        total += ms;
+      }
     }
-    printf("launch probe: %s params, %s: %.2f us per launch (event to event)\n", use_big ? "2776-byte" : "8-byte",
-           do_flush ? "after a 256 MiB L2 flush" : "no flush", 1e3f * total / reps);
+    printf("launch probe (gated): %s params, %s: %.2f us per launch (event to event)\n",
+           use_big ? "2776-byte" : "8-byte", do_flush ? "after a 256 MiB L2 flush" : "no flush",
+           1e3f * total / (2 * reps));
   }
   return 0;
 }
