@@ -332,6 +332,22 @@ int sg_policy_noise(const sg_policy* policy, int64_t n, const float* d_log_std_r
  * d_scaled_noise), bit-identical to sg_policy_act on the same draws. */
 int sg_policy_act_noise(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
                         const double* d_scaled_noise, float* d_actions, float* d_mean, float* d_value, void* stream);
+/* The PPO update's minibatch forward (ppo.cpp:157-224 -> Policy::forward) on
+ * the tensor cores, for the backward pass: bf16 observation rows d_obs_bf16
+ * (n x obs_stride, obs_stride >= 32 and a multiple of 8, columns >= obs_dim
+ * zero) -> every hidden activation, bf16 row-major per trunk (actor, critic):
+ * d_h1 [2][n][256], d_h2 [2][n][128], d_h3 [2][n][64], and the last layer's
+ * padded outputs d_out [2][n][8] (actor mean; critic value in column 0).
+ * Uses the parameters of the last sg_policy_load_params. */
+int sg_policy_train_forward(const sg_policy* policy, const void* d_obs_bf16, int64_t n, int32_t obs_stride, void* d_h1,
+                            void* d_h2, void* d_h3, void* d_out, void* stream);
+/* Flat-parameter layout sg_policy_load_params packs from: per (trunk, layer)
+ * (actor layers 0..3 then critic) the offsets of W [out x in] row-major and
+ * of b, the row stride in_dim[layer] and the row count out_dim[trunk*4 + l]
+ * (a trainer's padded copy, e.g. obs width 27 -> 32, outputs 7 -> 8; padded
+ * entries must be zero). Default: the reference layout (policy.cpp:42-63). */
+int sg_policy_set_param_layout(sg_policy* policy, const int64_t* w_off, const int64_t* b_off, const int32_t* in_dim,
+                               const int32_t* out_dim);
 /* compute_gae (rollout.cpp:42-66, time-major [n_steps][n_envs]) without the
  * normalisation, plus episode statistics (ppo.cpp:286-303) accumulated into
  * d_stats4 = {reward_sum, episode_reward_sum, final_error_sum, episodes}. */

@@ -201,8 +201,9 @@ __device__ __forceinline__ uint32_t elu_pair(uint32_t a0, uint32_t a1, float2 b)
 // only overwrites columns that this thread has already read (packing in
 // place: dst == src forward, or dst == src + NC/2 in reverse) or a disjoint
 // range.
-template <int NC, bool REV = false>
-__device__ __forceinline__ void epi_tmem(uint32_t trow, uint32_t src, uint32_t dst, const float* __restrict__ bias) {
+template <int NC, bool REV = false, bool STORE = false>
+__device__ __forceinline__ void epi_tmem(uint32_t trow, uint32_t src, uint32_t dst, const float* __restrict__ bias,
+                                         __nv_bfloat16* __restrict__ g = nullptr) {
   constexpr int NB = NC / 32;
   const auto bat = [](int j) { return REV ? NB - 1 - j : j; };
   uint32_t r[2][2][16];
@@ -222,6 +223,15 @@ __device__ __forceinline__ void epi_tmem(uint32_t trow, uint32_t src, uint32_t d
       p[k] = elu_pair(r[j & 1][k >> 3][2 * (k & 7)], r[j & 1][k >> 3][2 * (k & 7) + 1],
                       *reinterpret_cast<const float2*>(bias + c + 2 * k));
     tmem_st16(trow + dst + c / 2, p);
+    if constexpr (STORE) {  // the activations the backward pass needs: bf16 row segment of this thread
+      if (g) {
+        uint4* gv = reinterpret_cast<uint4*>(g + c);
+        gv[0] = make_uint4(p[0], p[1], p[2], p[3]);
+        gv[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        gv[2] = make_uint4(p[8], p[9], p[10], p[11]);
+        gv[3] = make_uint4(p[12], p[13], p[14], p[15]);
+      }
+    }
   }
 }
 
@@ -635,6 +645,168 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+}
+
+// ---- training forward: the PPO update's minibatch forward ---------------------
+// The update (ppo.cpp:157-224) runs Policy::forward on 131,072-row minibatches
+// and backpropagates through it. This kernel is the rollout forward made
+// persistent (one CTA per SM loops over 128-row tiles; weights, barriers and
+// TMEM set up once) with bf16 observation rows in, and every hidden
+// activation the backward pass needs stored as it is packed for the next
+// layer: h1 / h2 / h3 of both trunks (bf16, row-major [trunk][n][width]) and
+// the padded last-layer outputs (bf16 [trunk][n][8]: actor mean, critic
+// value in column 0). Same arithmetic as the library path it replaces (bf16
+// operands, fp32 accumulation, bias + ELU in fp32, one rounding to bf16).
+struct TrainFwdArgs {
+  const __nv_bfloat16* obs;  // n x obs_stride bf16 (the first 32 columns, zero padded)
+  int64_t n;
+  int32_t obs_stride;
+  __nv_bfloat16* h1;   // [2][n][256]
+  __nv_bfloat16* h2;   // [2][n][128]
+  __nv_bfloat16* h3;   // [2][n][64]
+  __nv_bfloat16* out;  // [2][n][8]
+};
+
+__global__ void __launch_bounds__(kThreads, 1) policy_train_fwd_kernel(const __grid_constant__ PolicyImage W,
+                                                                       const __grid_constant__ TrainFwdArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int row = tid & (kRows - 1);
+  const int group = tid / kRows;
+  const int trunk = warp >> 3, half = (warp >> 2) & 1;
+  float* sbias = reinterpret_cast<float*>(smem + kBias);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBar + 64);
+  const uint32_t bar_bias = smem_u32(&bars[0]), bar_w1 = smem_u32(&bars[1]);
+  const uint32_t bar_w2 = smem_u32(&bars[2 + trunk]), bar_w34 = smem_u32(&bars[4]);
+  const uint32_t bar_mma = smem_u32(&bars[5 + trunk]);
+  const uint32_t sbase = smem_u32(smem);
+  if (tid == 0) {
+    for (int b = 0; b < 7; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    bulk_load(sbase + kBias, W.b1, 928 * 4, smem_u32(&bars[0]));
+    bulk_load(sbase + kW1, W.w1, 32768, smem_u32(&bars[1]));
+    bulk_load(sbase + kW2a, W.w2a, 65536, smem_u32(&bars[2]));
+    bulk_load(sbase + kW2c, W.w2c, 65536, smem_u32(&bars[3]));
+    bulk_load(sbase + kW34, W.w34, 36864, smem_u32(&bars[4]));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t T = 256u * trunk;
+  const bool issuer = (tid & 255) == 0;
+  const float* b1 = sbias + 256 * trunk;
+  const float* b2 = sbias + 512 + 128 * trunk;
+  const float* b3 = sbias + 768 + 64 * trunk;
+  const float* b4 = sbias + 896 + 16 * trunk;
+  const int64_t n = args.n;
+  const auto trunk_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + trunk) : "memory"); };
+  const auto handoff = [&]() {
+    tmem_wait_st();
+    tc_fence_before();
+    trunk_sync();
+  };
+  const int64_t tiles = (n + kRows - 1) / kRows;
+  // obs tile: thread (row, group) copies K chunk `group` (8 bf16 = 16 B); the
+  // next tile's chunk is loaded into registers while this tile computes
+  const auto load_obs = [&](int64_t tile) {
+    const int64_t rr = tile * kRows + row;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (tile < tiles && rr < n) v = *reinterpret_cast<const uint4*>(args.obs + rr * args.obs_stride + 8 * group);
+    return v;
+  };
+  uint4 obs_next = load_obs(blockIdx.x);
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t row0 = tile * kRows, r = row0 + row;
+    const bool valid = r < n;
+    *reinterpret_cast<uint4*>(smem + kX0 + kmajor_off(row, 8 * group, kRows)) = obs_next;
+    obs_next = load_obs(tile + gridDim.x);
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      mbar_wait(bar_w1, 0);
+      tc_fence_after();
+      issue_layer(tmem + 0, sbase + kX0, kRows, sbase + kW1, 512, kK0, 256);
+      issue_layer(tmem + 256, sbase + kX0, kRows, sbase + kW1 + kmajor_off(256, 0, 512), 512, kK0, 256);
+      mma_commit(smem_u32(&bars[5]));
+      mma_commit(smem_u32(&bars[6]));
+    }
+    mbar_wait(bar_bias, 0);
+    const int64_t tr = trunk * n + r;  // activation row of this thread
+    // h1 -> A2 (+ global)
+    mbar_wait(bar_mma, 0);
+    tc_fence_after();
+#ifndef SG_TRAIN_NO_STAGGER
+    if (trunk == 1) asm volatile("bar.sync 3, 512;" ::: "memory");
+#endif
+    if (half == 0)
+      epi_tmem<128, false, true>(trow, T, T, b1, valid ? args.h1 + tr * 256 : nullptr);
+    else
+      epi_tmem<128, true, true>(trow, T + 128, T + 192, b1 + 128, valid ? args.h1 + tr * 256 + 128 : nullptr);
+    handoff();
+#ifndef SG_TRAIN_NO_STAGGER
+    if (trunk == 0) asm volatile("bar.arrive 3, 512;" ::: "memory");
+#endif
+    if (issuer) {
+      tc_fence_after();
+      mbar_wait(bar_w2, 0);
+      issue_layer_ts(tmem + T + 64, tmem + T, tmem + T + 192, 8, sbase + (trunk ? kW2c : kW2a), kH2 * 16, kH1, kH2);
+      mma_commit(bar_mma);
+    }
+    // h2 -> A3 (+ global)
+    mbar_wait(bar_mma, 1);
+    tc_fence_after();
+    epi_tmem<64, false, true>(trow, T + 64 + 64 * half, T + 32 * half, b2 + 64 * half,
+                              valid ? args.h2 + tr * 128 + 64 * half : nullptr);
+    handoff();
+    if (issuer) {
+      tc_fence_after();
+      mbar_wait(bar_w34, 0);
+      issue_layer_ts(tmem + T + 64, tmem + T, tmem + T, 8, sbase + (trunk ? kW3c : kW3a), kH3 * 16, kH2, kH3);
+      mma_commit(bar_mma);
+    }
+    // h3 -> A4 (+ global)
+    mbar_wait(bar_mma, 0);
+    tc_fence_after();
+    epi_tmem<32, false, true>(trow, T + 64 + 32 * half, T + 128 + 16 * half, b3 + 32 * half,
+                              valid ? args.h3 + tr * 64 + 32 * half : nullptr);
+    handoff();
+    if (issuer) {
+      tc_fence_after();
+      issue_layer_ts(tmem + T, tmem + T + 128, tmem + T + 128, 4, sbase + (trunk ? kW4c : kW4a), kNOut * 16, kH3,
+                     kNOut);
+      mma_commit(bar_mma);
+    }
+    mbar_wait(bar_mma, 1);
+    tc_fence_after();
+    if (half == 0) {  // padded last-layer outputs (8 columns)
+      float v[16];
+      tmem_ld16(trow + T, v);
+      if (valid) {
+        uint4 o;
+        o.x = pack_bf16(v[0] + b4[0], v[1] + b4[1]);
+        o.y = pack_bf16(v[2] + b4[2], v[3] + b4[3]);
+        o.z = pack_bf16(v[4] + b4[4], v[5] + b4[5]);
+        o.w = pack_bf16(v[6] + b4[6], v[7] + b4[7]);
+        *reinterpret_cast<uint4*>(args.out + tr * 8) = o;
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // every TMEM read of this tile is done before the next tile's layer 1
+    tc_fence_after();
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // ---- packing: flat fp32 params (reference layout) -> bf16 UMMA images -----
@@ -1132,6 +1304,57 @@ int sg_policy_act_noise(const sg_policy* p, const float* d_obs, int64_t n, int32
   smp.actions = d_actions;
   smp.noise = d_scaled_noise;
   return policy_forward(p, d_obs, n, obs_stride, d_mean, d_value, nullptr, nullptr, stream, smp);
+}
+
+int sg_policy_train_forward(const sg_policy* p, const void* d_obs_bf16, int64_t n, int32_t obs_stride, void* d_h1,
+                            void* d_h2, void* d_h3, void* d_out, void* stream) {
+  if (n <= 0) return SG_OK;
+  if (!d_obs_bf16 || !d_h1 || !d_h2 || !d_h3 || !d_out)
+    return fail(SG_ERR_CONFIG, "sg_policy_train_forward: null argument");
+  if (obs_stride < sgp::kK0 || obs_stride % 8 != 0)
+    return fail(SG_ERR_CONFIG, "sg_policy_train_forward: obs_stride must be >= 32 and a multiple of 8");
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(sgp::policy_train_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sgp::kSmem) !=
+        cudaSuccess)
+      return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+    attr = true;
+  }
+  sgp::PolicyImage W;
+  W.w1 = p->img;
+  W.w2a = p->img + 32768;
+  W.w2c = p->img + 32768 + 65536;
+  W.w34 = p->img + 32768 + 131072;
+  W.b1 = p->bias;
+  W.b2a = p->bias + 512;
+  W.b2c = p->bias + 640;
+  W.b3a = p->bias + 768;
+  W.b3c = p->bias + 832;
+  W.b4a = p->bias + 896;
+  W.b4c = p->bias + 912;
+  const sgp::TrainFwdArgs a{static_cast<const __nv_bfloat16*>(d_obs_bf16), n, obs_stride,
+                            static_cast<__nv_bfloat16*>(d_h1), static_cast<__nv_bfloat16*>(d_h2),
+                            static_cast<__nv_bfloat16*>(d_h3), static_cast<__nv_bfloat16*>(d_out)};
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (n + sgp::kRows - 1) / sgp::kRows;
+  const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+  sgp::policy_train_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_policy_set_param_layout(sg_policy* p, const int64_t* w_off, const int64_t* b_off, const int32_t* in_dim,
+                               const int32_t* out_dim) {
+  for (int t = 0; t < 2; ++t)
+    for (int l = 0; l < 4; ++l) {
+      p->table.w_off[t][l] = w_off[4 * t + l];
+      p->table.b_off[t][l] = b_off[4 * t + l];
+      p->table.out_dim[t][l] = out_dim[4 * t + l];
+    }
+  for (int l = 0; l < 4; ++l) p->table.in_dim[l] = in_dim[l];
+  return SG_OK;
 }
 
 int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const float* d_log_std_raw,

@@ -68,6 +68,9 @@ class TrainConfig:  # ppo.hpp:25-45
     # env-steps/s: the fp64 noise kernel outlasts the K = 1 env step it
     # overlaps and the fork / join adds graph edges), so off by default
     noise_ahead: bool = False
+    # bf16 update: the minibatch forward on the tensor cores
+    # (sg_policy_train_forward) instead of library GEMMs + ELU passes
+    fused_forward: bool = True
 
     def validate(self):  # ppo.cpp:31-48 (subset relevant on device)
         if not 0.0 <= self.gamma <= 1.0:
@@ -176,6 +179,51 @@ def _linear(x, W, b, Wm=None, bm=None, elu: bool = False):
                 return fn.apply(x.to(dt), W, b, Wm, bm)
             return fn.apply(x.to(dt), W.to(dt), b.to(dt))
     return fn.apply(x, W, b)
+
+
+class _FusedMLP(torch.autograd.Function):
+    """The update's minibatch Policy::forward (bf16) as ONE tensor-core launch
+    (sg_policy_train_forward: both trunks, every hidden activation stored as
+    it is packed for the next layer) instead of 8 library GEMMs + 6 ELU passes;
+    the backward pass is the library one (_linear_grads per layer, direct
+    gradient writes, the train.cu ELU derivative from the stored outputs).
+    `leaf` is any trainer parameter, passed only so autograd calls backward."""
+
+    @staticmethod
+    def forward(ctx, trainer, obs, leaf):
+        m = obs.shape[0]
+        h1, h2, h3, out = trainer.fused_buffers(m)
+        trainer.train_policy.load_params(trainer.params)  # this minibatch's weights (Adam ran since)
+        trainer.train_policy.train_forward(obs, h1, h2, h3, out)
+        ctx.trainer, ctx.obs, ctx.acts = trainer, obs, (h1, h2, h3)
+        return out[0], out[1]
+
+    @staticmethod
+    def backward(ctx, g_mean, g_value):
+        tr, obs = ctx.trainer, ctx.obs
+        h1, h2, h3 = ctx.acts
+        for t, gy in ((0, g_mean), (1, g_value)):
+            ins = (obs, h1[t], h2[t], h3[t])
+            g = gy.contiguous().to(torch.bfloat16)
+            for l in (3, 2, 1, 0):
+                W, b, Wm, _ = tr.layers[4 * t + l]
+                lctx = _LayerCtx(needs_gx=l > 0, direct=_direct_grads(W, b), w_dtype=W.dtype)
+                gx, gW, gb, _, _ = _linear_grads(lctx, g, ins[l], Wm)
+                if lctx.direct is None:  # (only without the trainer-owned gradient views)
+                    W.grad.add_(gW)
+                    b.grad.add_(gb)
+                if l > 0:
+                    g = sg.elu_backward(ins[l], gx.contiguous())
+        return None, None, None
+
+
+class _LayerCtx:
+    """The attributes _linear_grads reads from an autograd ctx."""
+
+    def __init__(self, needs_gx: bool, direct, w_dtype):
+        self.needs_input_grad = (needs_gx,)
+        self.direct = direct
+        self.w_dtype = w_dtype
 
 
 def param_layout(obs_dim: int, act_dim: int):
@@ -375,6 +423,12 @@ class Trainer:
             else:
                 self.layers.append((W, b))
         self.log_std = self.params[self.ls_off: self.ls_off + A].detach().requires_grad_(True)
+        # the fused minibatch forward packs its weights from the padded copy
+        self.train_policy = None
+        self._fused_buf = None
+        if cfg.fused_forward and cfg.update_precision == "bf16" and os.environ.get("SG_NO_FUSED_FWD") != "1":
+            self.train_policy = sg.Policy(O, A, device=policy.device)
+            self.train_policy.set_param_layout(layout, [_up8(O), 256, 128, 64])
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]
         # The whole update is one CUDA-graph replay at any world size: the NCCL
         # gradient all-reduce of every minibatch is captured with the GEMMs
@@ -427,6 +481,20 @@ class Trainer:
         self.iteration = 0
         self.gen = torch.Generator(device=dev)
         self.gen.manual_seed(cfg.seed * 1000003 + (dist.get_rank() if dist is not None and dist.is_initialized() else 0))
+
+    def fused_buffers(self, m: int):
+        """bf16 activation buffers of the fused minibatch forward, [2][m][width]
+        views of one allocation sized for the largest minibatch (fixed
+        addresses: the update is graph-captured)."""
+        if self._fused_buf is None:
+            mb = (self.T * self.N + self.cfg.minibatch_count - 1) // self.cfg.minibatch_count
+            self._fused_buf = torch.empty(2 * mb * (256 + 128 + 64 + 8), dtype=torch.bfloat16, device=self.dev)
+        buf, out = self._fused_buf, []
+        off = 0
+        for w in (256, 128, 64, 8):
+            out.append(buf[off: off + 2 * m * w].view(2, m, w))
+            off += 2 * m * w
+        return out
 
     # -- rollout -----------------------------------------------------------
     def _stream(self):
@@ -553,8 +621,11 @@ class Trainer:
                 sg.ppo_gather(idx, obs, act, logp, adv, ret, g["obs"][:m_rows], g["act"][:m_rows],
                               g["logp"][:m_rows], g["adv"][:m_rows], g["ret"][:m_rows])
                 # (self.grad is zero here: initially, and after every fused Adam step)
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
-                    mean_f, value_f = mlp_layers(self.layers, g["obs"][:m_rows], device_elu=True, full=True)
+                if self.train_policy is not None:  # one tensor-core launch (bf16 obs rows in)
+                    mean_f, value_f = _FusedMLP.apply(self, g["obs"][:m_rows], self.layers[0][0])
+                else:
+                    with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.update_precision == "bf16"):
+                        mean_f, value_f = mlp_layers(self.layers, g["obs"][:m_rows], device_elu=True, full=True)
                 loss, m = _PPOLossDevice.apply(mean_f.contiguous(), value_f.contiguous(), self.log_std,
                                                g["act"][:m_rows], g["logp"][:m_rows], g["adv"][:m_rows],
                                                g["ret"][:m_rows], self.A, cfg.clip_eps, cfg.value_coef,

@@ -148,6 +148,9 @@ _SIGS = {
                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_policy_act_noise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_train_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_set_param_layout": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p]),
@@ -551,7 +554,9 @@ class Policy:
     def load_params(self, flat) -> None:
         """flat: cuda fp32 tensor (param_count) in the reference layout."""
         import torch
-        assert flat.is_cuda and flat.dtype == torch.float32 and flat.numel() == self.param_count
+        need = getattr(self, "_layout_numel", None)
+        assert flat.is_cuda and flat.dtype == torch.float32
+        assert flat.numel() == self.param_count if need is None else flat.numel() >= need
         stream = torch.cuda.current_stream(flat.device).cuda_stream
         _pcheck(lib().sg_policy_load_params(self._h, flat.contiguous().data_ptr(), stream))
 
@@ -605,6 +610,23 @@ class Policy:
         _pcheck(lib().sg_policy_sample(mean.data_ptr(), n, A, log_std.data_ptr(), s0, inc, pos.data_ptr(), step_offset,
                                        acts.data_ptr(), logp.data_ptr(), stream))
         return acts, logp
+
+    def set_param_layout(self, layout, in_dims) -> None:
+        """sg_policy_set_param_layout: pack from a trainer's (padded) flat
+        layout. layout[k] = ((w_off, out, in), (b_off, out)) for k = trunk*4 + l."""
+        w = (C.c_int64 * 8)(*[L[0][0] for L in layout])
+        b = (C.c_int64 * 8)(*[L[1][0] for L in layout])
+        o = (C.c_int32 * 8)(*[L[0][1] for L in layout])
+        i = (C.c_int32 * 4)(*in_dims)
+        _pcheck(lib().sg_policy_set_param_layout(self._h, w, b, i, o))
+        self._layout_numel = max(L[1][0] + L[1][1] for L in layout)
+
+    def train_forward(self, obs_bf16, h1, h2, h3, out) -> None:
+        """sg_policy_train_forward into caller buffers (bf16 CUDA tensors)."""
+        import torch
+        stream = torch.cuda.current_stream(obs_bf16.device).cuda_stream
+        _pcheck(lib().sg_policy_train_forward(self._h, obs_bf16.data_ptr(), obs_bf16.shape[0], obs_bf16.stride(0),
+                                              h1.data_ptr(), h2.data_ptr(), h3.data_ptr(), out.data_ptr(), stream))
 
     def noise(self, n: int, seed: int = 0, log_std=None, draw_pos: int = 0, step_offset: int = 0, device: int = 0):
         """sg_policy_noise: the sampling's stream part ahead of the forward.

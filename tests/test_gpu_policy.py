@@ -134,3 +134,89 @@ def test_precomputed_noise_equals_fused_sampling(sg, n, act_dim, obs_dim):
     assert torch.equal(m2, m1) and torch.equal(v2, v1)
     assert torch.equal(lp2, lp1)
     assert torch.equal(a2, a1)
+
+
+@pytest.mark.parametrize("n", [131072, 1000, 129])
+def test_train_forward_matches_bf16_reference(sg, n):
+    """sg_policy_train_forward (the PPO update's minibatch forward: persistent
+    tensor-core kernel, bf16 obs rows in, every hidden activation stored) ==
+    the bf16-emulating fp32 reference, for the activations h1..h3 of both
+    trunks and the padded outputs, with the trainer's padded layout (obs width
+    27 -> 32, last layers 7 -> 8 and 1 -> 8 rows)."""
+    from paper_2310_04676_b200 import ppo
+    torch.manual_seed(3)
+    O, A = 27, 7
+    layout, ls_pad, total, ref_to_pad = ppo.padded_layout(O, A)
+    pol = sg.Policy(O, A)
+    ref = torch.from_numpy(pol.init_params(seed=6)).cuda()
+    ref = ref + 0.05 * torch.randn_like(ref)
+    flat = torch.zeros(total, device="cuda")
+    flat[torch.from_numpy(ref_to_pad).cuda()] = ref
+    tp = sg.Policy(O, A)
+    tp.set_param_layout(layout, [32, 256, 128, 64])
+    tp.load_params(flat)
+    obs = torch.zeros(n, 32, device="cuda", dtype=torch.bfloat16)
+    obs[:, :O] = (torch.randn(n, O, device="cuda") * 0.5).to(torch.bfloat16)
+    h1 = torch.empty(2, n, 256, device="cuda", dtype=torch.bfloat16)
+    h2 = torch.empty(2, n, 128, device="cuda", dtype=torch.bfloat16)
+    h3 = torch.empty(2, n, 64, device="cuda", dtype=torch.bfloat16)
+    out = torch.empty(2, n, 8, device="cuda", dtype=torch.bfloat16)
+    tp.train_forward(obs, h1, h2, h3, out)
+    torch.cuda.synchronize()
+    r = lambda t: t.to(torch.bfloat16).float()  # noqa: E731
+    for t in (0, 1):
+        h = obs.float()
+        for l, got in enumerate((h1[t], h2[t], h3[t], out[t])):
+            (w0, o, i), (b0, ob) = layout[4 * t + l]
+            W = flat[w0: w0 + o * i].view(o, i)
+            b = flat[b0: b0 + ob]
+            z = h @ r(W).T + b
+            h = r(torch.where(z > 0, z, torch.expm1(z))) if l < 3 else r(z)
+            err = (got.float() - h).abs().max().item()
+            scale = h.abs().max().item() + 1e-6
+            # one bf16 rounding of an fp32 value that differs by accumulation order
+            assert err <= 1.6e-2 * scale, (t, l, err, scale)
+            h = got.float()  # continue from the kernel's own activations
+    # padded output columns are exact zeros (zero weights and biases)
+    assert torch.all(out[0][:, A:] == 0) and torch.all(out[1][:, 1:] == 0)
+
+
+def test_fused_update_forward_matches_library_gradients(sg):
+    """One PPO minibatch gradient with the fused tensor-core forward ==
+    the library forward (bf16 GEMMs + ELU kernels) within bf16 tolerance, and
+    a whole bf16 iteration learns (finite metrics)."""
+    from paper_2310_04676_b200 import ppo
+    grads = []
+    for fused in (True, False):
+        env = sg.VecTaskEnv(robots=("psm",), n_envs=2048, seed=1, episode_len=50)
+        tr = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim),
+                         ppo.TrainConfig(seed=4, update_precision="bf16", fused_forward=fused, cuda_graph=False))
+        assert (tr.train_policy is not None) == fused
+        tr.rollout()
+        tr.gae()
+        cap = tr.T * tr.N
+        idx = torch.randperm(cap, device="cuda", generator=torch.Generator(device="cuda").manual_seed(0))[: cap // 4]
+        b, g = tr.buf, tr.mb_buf
+        m = idx.numel()
+        sg.ppo_gather(idx, b["obs"][:tr.T].reshape(cap, tr.O), b["actions"].view(cap, tr.A), b["logp"].view(cap),
+                      b["adv"].view(cap), b["ret"].view(cap), g["obs"][:m], g["act"][:m], g["logp"][:m],
+                      g["adv"][:m], g["ret"][:m])
+        tr.grad.zero_()
+        if fused:
+            mean_f, value_f = ppo._FusedMLP.apply(tr, g["obs"][:m], tr.layers[0][0])
+        else:
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                mean_f, value_f = ppo.mlp_layers(tr.layers, g["obs"][:m], device_elu=True, full=True)
+        loss, _ = ppo._PPOLossDevice.apply(mean_f.contiguous(), value_f.contiguous(), tr.log_std, g["act"][:m],
+                                           g["logp"][:m], g["adv"][:m], g["ret"][:m], tr.A, tr.cfg.clip_eps,
+                                           tr.cfg.value_coef, tr.cfg.entropy_coef, True)
+        loss.backward()
+        torch.cuda.synchronize()
+        grads.append(tr.grad.clone())
+    a, b2 = grads
+    rel = ((a - b2).norm() / b2.norm()).item()
+    assert rel < 3e-2, rel
+    env = sg.VecTaskEnv(robots=("psm",), n_envs=2048, seed=1, episode_len=50)
+    tr = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim), ppo.TrainConfig(seed=4, update_precision="bf16"))
+    h = tr.iterate()
+    assert all(np.isfinite(h[k]) for k in ("policy_loss", "value_loss", "kl"))
