@@ -850,14 +850,17 @@ def bench_e2e(env, E, n, A, O, dist, dev, world, torch, sg):
     to pinned host buffers (terminal rows on steps where envs ended). Actions
     are the bench stream, pre-generated into a ring of up to 300 steps."""
     ring = min(E + 1, 300)
-    h_act = torch.empty((ring, n, A), dtype=torch.float32).pin_memory()
+    # host buffers from the library's pinned allocator (sg_host_alloc)
+    keep = [sg.HostBuffer((ring, n, A), torch.float32)]
+    h_act = keep[0].tensor
     for s in range(ring):  # pre-generate the bench stream (device generator), outside timing
         env.bench_step(1)
         h_act[s].copy_(env.bench_actions())
-    outs = {k2: torch.empty(shape, dtype=dt).pin_memory() for k2, shape, dt in (
-        ("observations", (n, O), torch.float32), ("terminal_observations", (n, O), torch.float32),
-        ("rewards", (n,), torch.float32), ("task_error", (n,), torch.float32),
-        ("terminated", (n,), torch.uint8), ("timed_out", (n,), torch.uint8))}
+    spec = (("observations", (n, O), torch.float32), ("terminal_observations", (n, O), torch.float32),
+            ("rewards", (n,), torch.float32), ("task_error", (n,), torch.float32),
+            ("terminated", (n,), torch.uint8), ("timed_out", (n,), torch.uint8))
+    keep += [sg.HostBuffer(shape, dt) for _, shape, dt in spec]
+    outs = {k2: buf.tensor for (k2, _, _), buf in zip(spec, keep[1:])}
     hr = sg.HostResult()
     for k2, t in outs.items():
         setattr(hr, k2, t.data_ptr())

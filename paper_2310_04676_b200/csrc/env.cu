@@ -12,6 +12,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <array>
 #include <algorithm>
 #include <cstring>
@@ -263,6 +265,11 @@ struct sg_env {
   // device {sat_total, ended slot A, err, ended slot B, ticket, pad...}
   unsigned long long* counters = nullptr;
   unsigned long long* h_counters = nullptr;  // pinned, mapped: {sat_total, ended, err} of the last host step
+  // zero-copy host step: teams reading their action rows over PCIe at once
+  // (SG_HOST_READ_WINDOW, 0 = all at once). 128 of 512 teams (PSM 16K): later
+  // teams' reads overlap earlier teams' result writes, 63.5 -> 62.0 us per
+  // step (tools/gpu_r3a.sh: 64 / 256 / 384 no better)
+  int read_window = std::getenv("SG_HOST_READ_WINDOW") ? std::atoi(std::getenv("SG_HOST_READ_WINDOW")) : 128;
   unsigned long long* d_status = nullptr;    // device alias of h_counters
   int host_slot = 0;                          // ended slot of the next host step
   bool bench_ready = false;
@@ -1126,17 +1133,38 @@ int sg_env_reset_host(sg_env* env, float* h_observations) {
   });
 }
 
+// Pinned, mapped host allocations made by sg_host_alloc: host base -> {bytes,
+// device alias base}. A host step resolves its buffers here without a CUDA
+// call per pointer (cudaPointerGetAttributes only for foreign buffers).
+namespace {
+struct HostAlloc {
+  size_t bytes;
+  uintptr_t dev;
+};
+std::mutex g_host_mu;
+std::map<uintptr_t, HostAlloc> g_host_allocs;
+}  // namespace
+
 int sg_host_alloc(size_t bytes, void** out) {
   return guard([&] {
     if (!out) throw sg::ConfigError("sg_host_alloc: null output pointer");
     *out = nullptr;
     CK(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped));
+    void* dev = nullptr;
+    CK(cudaHostGetDevicePointer(&dev, *out, 0));
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    g_host_allocs[reinterpret_cast<uintptr_t>(*out)] = HostAlloc{bytes ? bytes : 1, reinterpret_cast<uintptr_t>(dev)};
   });
 }
 
 int sg_host_free(void* p) {
   return guard([&] {
-    if (p) CK(cudaFreeHost(p));
+    if (!p) return;
+    {
+      std::lock_guard<std::mutex> lk(g_host_mu);
+      g_host_allocs.erase(reinterpret_cast<uintptr_t>(p));
+    }
+    CK(cudaFreeHost(p));
   });
 }
 
@@ -1217,6 +1245,15 @@ int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
 // equals the host address), or nullptr for pageable memory.
 static void* mapped_alias(const void* h) {
   if (!h) return nullptr;
+  {
+    const uintptr_t u = reinterpret_cast<uintptr_t>(h);
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = g_host_allocs.upper_bound(u);
+    if (it != g_host_allocs.begin()) {
+      --it;
+      if (u - it->first < it->second.bytes) return reinterpret_cast<void*>(it->second.dev + (u - it->first));
+    }
+  }
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -1313,7 +1350,15 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
       p.h_terminated = host_u[0];
       p.h_timed_out = host_u[1];
       p.h_seq = ++env->host_seq;
+      // rolling PCIe read window (kernels.cuh StepParams::read_gate): only
+      // (a team waits only on teams dispatched before it: CTAs start in index order)
+      const int64_t teams = (n + 31) / 32;
+      if (env->read_window > 0 && teams <= (int64_t)sg::sm_count() * 8) {
+        p.read_gate = reinterpret_cast<unsigned int*>(env->counters + 4) + 1;
+        p.read_window = env->read_window;
+      }
       env->launch_step(1, false);
+      p.read_gate = nullptr;
       p.h_obs = p.h_tobs = p.h_rewards = p.h_task_error = nullptr;
       p.h_terminated = p.h_timed_out = nullptr;
     } else {

@@ -148,6 +148,12 @@ struct EnvPtrs {
   unsigned long long* sat_step;     // host step: saturations of THIS step (nullable)
   unsigned long long* sat_clear;    // zeroed at launch start: the next host step's saturation slot
   unsigned int* ticket;             // CTA completion counter (last CTA publishes, then re-arms it)
+  // Host step read window (nullable): teams that finished staging their
+  // action rows; team b stages once read_gate >= b - read_window + 1, so at
+  // most ~read_window teams read over PCIe at once and later teams' reads
+  // overlap earlier teams' result writes (the last CTA re-arms it)
+  unsigned int* read_gate;
+  int read_window;
   float* h_rewards;
   float* h_task_error;
   uint8_t* h_terminated;
@@ -1503,6 +1509,14 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     // aligned) loads into shared memory, then each warp picks its DoFs (one
     // pass over PCIe when the actions are in mapped host memory). A launch
     // with caller actions applies the same rows at every step.
+    const bool gate = TPC == 1 && P.p.read_gate != nullptr;
+    if (gate && (int)blockIdx.x >= P.p.read_window) {
+      if (tm.tthread == 0) {
+        const unsigned need = blockIdx.x - P.p.read_window + 1;
+        while (*reinterpret_cast<volatile unsigned*>(P.p.read_gate) < need) __nanosleep(64);
+      }
+      team_sync<G, TPC>(tm);
+    }
     const float* src = P.actions + row0 * A;
     const int cnt = rows * A;
     if (P.actions_aligned) {
@@ -1514,6 +1528,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
       for (int k = tm.tthread; k < cnt; k += 32 * G) s_act_base[k] = src[k];
     }
     team_sync<G, TPC>(tm);
+    if (gate && tm.tthread == 0) atomicAdd(P.p.read_gate, 1u);
   }
 
   // ---- dynamics (dynamics.cpp:133-185) on this block; count: saturation /
@@ -2082,6 +2097,7 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
         __threadfence_system();
         hs[3] = P.p.h_seq;
         *P.p.ticket = 0;
+        if (P.p.read_gate) *P.p.read_gate = 0;
       }
     }
   }

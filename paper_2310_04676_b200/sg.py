@@ -527,6 +527,29 @@ def _pcheck(rc: int) -> None:
     raise (ConfigError if rc == SG_ERR_CONFIG else SimError)(msg)
 
 
+class HostBuffer:
+    """Pinned, device-mapped host memory from sg_host_alloc (the library's
+    allocator for host-step buffers: sg_env_step_host resolves them without a
+    CUDA pointer query). .tensor is a CPU torch view; freed with the object."""
+
+    def __init__(self, shape, dtype):
+        import torch
+        self.shape = tuple(shape)
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        nbytes = max(1, int(np.prod(self.shape)) * itemsize)
+        p = C.c_void_p()
+        _check(lib().sg_host_alloc(nbytes, C.byref(p)))
+        self.ptr = p.value
+        raw = (C.c_uint8 * nbytes).from_address(self.ptr)
+        self.tensor = torch.frombuffer(raw, dtype=torch.uint8).view(dtype).view(self.shape)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _LIB is not None:
+            self.tensor = None
+            _LIB.sg_host_free(self.ptr)
+            self.ptr = None
+
+
 class Policy:
     """Actor-critic MLP (policy.hpp:63-72) with the tcgen05 forward kernel.
     Parameters live in one flat fp32 vector in the reference's layout."""
