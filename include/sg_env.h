@@ -319,6 +319,17 @@ int sg_policy_sample(const float* d_mean, int64_t n, int32_t action_dim, const f
 int sg_policy_act(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
                   const float* d_log_std_raw, uint64_t stream_state, uint64_t stream_inc, const uint64_t* d_draw_pos,
                   uint64_t step_offset, float* d_actions, float* d_logp, float* d_mean, float* d_value, void* stream);
+/* sg_policy_act for rollout step t that also computes step t-1's timeout
+ * bootstrap values (sg_policy_bootstrap's result: V(d_boot_obs row) where
+ * d_timed_out && !d_terminated, else 0, into d_boot_value) in the same
+ * launch: tiles with such rows run the critic trunk again on the terminal
+ * rows, the others only write zeros. Bit-identical to the two calls. */
+int sg_policy_act_bootstrap(const sg_policy* policy, const float* d_obs, int64_t n, int32_t obs_stride,
+                            const float* d_log_std_raw, uint64_t stream_state, uint64_t stream_inc,
+                            const uint64_t* d_draw_pos, uint64_t step_offset, float* d_actions, float* d_logp,
+                            float* d_mean, float* d_value, const float* d_boot_obs, int32_t boot_stride,
+                            const uint8_t* d_timed_out, const uint8_t* d_terminated, float* d_boot_value,
+                            void* stream);
 /* The stream part of sg_policy_sample ahead of the forward (it depends on
  * the trainer stream and log-std only): for every (env e, dim i) the draw at
  * *d_draw_pos + step_offset + 2*(e*A + i) -> d_scaled_noise[e*A + i] =

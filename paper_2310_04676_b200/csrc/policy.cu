@@ -371,6 +371,15 @@ struct FwdArgs {
   // precomputed sampling (sg_policy_noise), when non-null: actions =
   // (float)(mean + noise[row A + dim]); logp was written by the noise kernel
   const double* noise;
+  // folded bootstrap of the PREVIOUS rollout step (ppo.cpp:304-313), when
+  // boot_obs != null: boot_value[r] = V(boot_obs row r) for rows with
+  // boot_timed_out && !boot_terminated, 0 elsewhere (what sg_policy_bootstrap
+  // computes, without its own launch; tiles with no such row only write zeros)
+  const float* boot_obs;
+  int32_t boot_stride;
+  const uint8_t* boot_timed_out;
+  const uint8_t* boot_terminated;
+  float* boot_value;
 };
 
 #ifdef SG_POLICY_PROBE
@@ -627,6 +636,85 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
       double lp = 0.0;
       for (int d = 0; d < A; ++d) lp = __dadd_rn(lp, sterm[row * kNOut + d]);
       args.logp[srow] = (float)lp;
+    }
+  }
+  if (args.boot_obs) {
+    // ---- folded bootstrap: the critic trunk again, on the previous step's
+    // terminal rows (only in tiles that have a timed-out, non-terminated row)
+    const int64_t r = row0 + row;
+    const bool need = r < args.n && args.boot_timed_out[r] && !args.boot_terminated[r];
+    tc_fence_before();
+    if (!__syncthreads_or(group == 0 && need)) {
+      if (group == 0 && r < args.n) args.boot_value[r] = 0.f;
+    } else {
+      // W1's smem was the sampling scratch: bulk-copy it again (phase 1 of its barrier)
+      if (tid == 0) {
+        async_proxy_fence();
+        bulk_load(sbase + kW1, W.w1, 32768, bar_w1);
+      }
+      {
+        float x[8];
+        const int c0 = group * 8;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = 0.f;
+        if (r < args.n) {
+          const float* src = args.boot_obs + r * args.boot_stride;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (c0 + k < args.obs_dim) x[k] = __ldg(src + c0 + k);
+        }
+        uint4* d = reinterpret_cast<uint4*>(smem + kX0 + kmajor_off(row, c0, kRows));
+        *d = make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
+      }
+      async_proxy_fence();
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      if (trunk == 1) {
+        if (issuer) {
+          mbar_wait(bar_w1, 1);
+          tc_fence_after();
+          issue_layer(tmem + 256, sbase + kX0, kRows, sbase + kW1 + kmajor_off(256, 0, 512), 512, kK0, 256);
+          mma_commit(bar_mma);
+        }
+        mbar_wait(bar_mma, 0);
+        tc_fence_after();
+        if (half == 0)
+          epi_tmem<128>(trow, T, T, b1);
+        else
+          epi_tmem<128, true>(trow, T + 128, T + 192, b1 + 128);
+        handoff();
+        if (issuer) {
+          tc_fence_after();
+          issue_layer_ts(tmem + T + 64, tmem + T, tmem + T + 192, 8, sbase + kW2c, kH2 * 16, kH1, kH2);
+          mma_commit(bar_mma);
+        }
+        mbar_wait(bar_mma, 1);
+        tc_fence_after();
+        epi_tmem<64>(trow, T + 64 + 64 * half, T + 32 * half, b2 + 64 * half);
+        handoff();
+        if (issuer) {
+          tc_fence_after();
+          issue_layer_ts(tmem + T + 64, tmem + T, tmem + T, 8, sbase + kW3c, kH3 * 16, kH2, kH3);
+          mma_commit(bar_mma);
+        }
+        mbar_wait(bar_mma, 0);
+        tc_fence_after();
+        epi_tmem<32>(trow, T + 64 + 32 * half, T + 128 + 16 * half, b3 + 32 * half);
+        handoff();
+        if (issuer) {
+          tc_fence_after();
+          issue_layer_ts(tmem + T, tmem + T + 128, tmem + T + 128, 4, sbase + kW4c, kNOut * 16, kH3, kNOut);
+          mma_commit(bar_mma);
+        }
+        mbar_wait(bar_mma, 1);
+        tc_fence_after();
+        if (half == 0) {
+          float v[16];
+          tmem_ld16(trow + T, v);
+          if (r < args.n) args.boot_value[r] = need ? v[0] + b4[0] : 0.f;
+        }
+      }
     }
   }
   PPROBE(9);
@@ -1225,6 +1313,12 @@ struct SampleArgs {
   float* actions = nullptr;
   float* logp = nullptr;
   const double* noise = nullptr;
+  // folded bootstrap of the previous step
+  const float* boot_obs = nullptr;
+  int32_t boot_stride = 0;
+  const uint8_t* boot_timed_out = nullptr;
+  const uint8_t* boot_terminated = nullptr;
+  float* boot_value = nullptr;
 };
 
 static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride, float* d_mean,
@@ -1245,7 +1339,8 @@ static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int
   W.b4c = p->bias + 912;
   sgp::FwdArgs a{d_obs, n, p->obs_dim, obs_stride > 0 ? obs_stride : p->obs_dim, p->act_dim, d_mean, d_value,
                  d_timed_out, d_terminated, smp.log_std_raw, smp.s0, smp.inc, smp.pos, smp.step_off, smp.actions,
-                 smp.logp, smp.noise};
+                 smp.logp, smp.noise, smp.boot_obs, smp.boot_stride, smp.boot_timed_out, smp.boot_terminated,
+                 smp.boot_value};
   static const sgp::Jump64 kNone{};
   const sgp::Jump64 J = smp.actions && !smp.noise ? jump_table(smp.inc) : kNone;
   const unsigned grid = (unsigned)((n + sgp::kRows - 1) / sgp::kRows);
@@ -1278,6 +1373,33 @@ int sg_policy_act(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs
   smp.step_off = step_offset;
   smp.actions = d_actions;
   smp.logp = d_logp;
+  return policy_forward(p, d_obs, n, obs_stride, d_mean, d_value, nullptr, nullptr, stream, smp);
+}
+
+int sg_policy_act_bootstrap(const sg_policy* p, const float* d_obs, int64_t n, int32_t obs_stride,
+                            const float* d_log_std_raw, uint64_t stream_state, uint64_t stream_inc,
+                            const uint64_t* d_draw_pos, uint64_t step_offset, float* d_actions, float* d_logp,
+                            float* d_mean, float* d_value, const float* d_boot_obs, int32_t boot_stride,
+                            const uint8_t* d_timed_out, const uint8_t* d_terminated, float* d_boot_value,
+                            void* stream) {
+  if (!d_actions || !d_logp || !d_log_std_raw || !d_draw_pos || !d_value)
+    return fail(SG_ERR_CONFIG, "sg_policy_act_bootstrap: null argument");
+  if (!d_boot_obs || !d_timed_out || !d_terminated || !d_boot_value)
+    return fail(SG_ERR_CONFIG, "sg_policy_act_bootstrap: null bootstrap argument");
+  if (p->act_dim > sgp::kNOut) return fail(SG_ERR_CONFIG, "sg_policy_act_bootstrap: action_dim > 16");
+  SampleArgs smp;
+  smp.log_std_raw = d_log_std_raw;
+  smp.s0 = stream_state;
+  smp.inc = stream_inc;
+  smp.pos = d_draw_pos;
+  smp.step_off = step_offset;
+  smp.actions = d_actions;
+  smp.logp = d_logp;
+  smp.boot_obs = d_boot_obs;
+  smp.boot_stride = boot_stride > 0 ? boot_stride : p->obs_dim;
+  smp.boot_timed_out = d_timed_out;
+  smp.boot_terminated = d_terminated;
+  smp.boot_value = d_boot_value;
   return policy_forward(p, d_obs, n, obs_stride, d_mean, d_value, nullptr, nullptr, stream, smp);
 }
 

@@ -71,6 +71,9 @@ class TrainConfig:  # ppo.hpp:25-45
     # bf16 update: the minibatch forward on the tensor cores
     # (sg_policy_train_forward) instead of library GEMMs + ELU passes
     fused_forward: bool = True
+    # the timeout bootstrap of step t-1 inside step t's policy launch
+    # (sg_policy_act_bootstrap) instead of its own launch per step
+    fold_bootstrap: bool = True
 
     def validate(self):  # ppo.cpp:31-48 (subset relevant on device)
         if not 0.0 <= self.gamma <= 1.0:
@@ -543,6 +546,8 @@ class Trainer:
         log_std.copy_(self.params[self.ls_off: self.ls_off + A])
         b["obs"][0].copy_(b["obs"][T])
         ahead = self.cfg.noise_ahead
+        fold = self.cfg.fold_bootstrap and self.cfg.timeout_bootstrap and not ahead
+        tobs = None
         main = torch.cuda.current_stream(self.dev)
 
         def noise(t, stream):  # step t's draws: scaled noise + log-probs (ppo.cpp:262-277)
@@ -563,6 +568,16 @@ class Trainer:
                     self.noise_stream.wait_stream(main)
                     with torch.cuda.stream(self.noise_stream):
                         noise(t + 1, self.noise_stream.cuda_stream)
+            elif fold and t > 0:
+                # policy forward + sampling + log-prob, and step t-1's timeout
+                # bootstrap (its terminal rows are still in the env's buffer):
+                # one tcgen05 launch
+                sg._pcheck(L.sg_policy_act_bootstrap(
+                    pol._h, obs.data_ptr(), N, obs.stride(0), log_std.data_ptr(), self.stream_state, self.stream_inc,
+                    self.d_pos.data_ptr(), 2 * A * (t * self.global_n + self.row_off), b["actions"][t].data_ptr(),
+                    b["logp"][t].data_ptr(), None, b["values"][t].data_ptr(), tobs.data_ptr(), self.O,
+                    b["timed_out"][t - 1].data_ptr(), b["terminated"][t - 1].data_ptr(), b["boot"][t - 1].data_ptr(),
+                    st))
             else:
                 # policy forward + Gaussian sampling + log-prob: one tcgen05 launch
                 sg._pcheck(L.sg_policy_act(pol._h, obs.data_ptr(), N, obs.stride(0), log_std.data_ptr(),
@@ -577,12 +592,12 @@ class Trainer:
                                 terminated=b["terminated"][t], timed_out=b["timed_out"][t])
             if not direct:
                 b["obs"][t + 1].copy_(res.observations)
-            if self.cfg.timeout_bootstrap:
-                sg._pcheck(L.sg_policy_bootstrap(pol._h, res.terminal_observations.data_ptr(), N, self.O,
-                                                 res.timed_out.data_ptr(), res.terminated.data_ptr(),
-                                                 b["boot"][t].data_ptr(), st))
-            else:
+            tobs = res.terminal_observations
+            if not self.cfg.timeout_bootstrap:
                 b["boot"][t].zero_()
+            elif not fold or t == T - 1:
+                sg._pcheck(L.sg_policy_bootstrap(pol._h, tobs.data_ptr(), N, self.O, res.timed_out.data_ptr(),
+                                                 res.terminated.data_ptr(), b["boot"][t].data_ptr(), st))
             if ahead and t + 1 < T:
                 main.wait_stream(self.noise_stream)
         pol.forward(b["obs"][T], self.mean, b["last_values"])

@@ -353,3 +353,26 @@ def test_rollout_noise_ahead_equals_fused_sampling(sg):
     for a, b in zip(*bufs):
         for k in a:
             assert torch.equal(a[k], b[k]), k
+
+
+def test_rollout_folded_bootstrap_equals_separate_launch(sg):
+    """The default rollout computes step t-1's timeout bootstrap inside step
+    t's policy launch (sg_policy_act_bootstrap); the rollout buffer --
+    bootstrap values included, across timeouts and graph replays -- is
+    bit-identical to a separate sg_policy_bootstrap launch per step."""
+    from paper_2310_04676_b200 import ppo
+    bufs = []
+    for fold in (True, False):
+        env = sg.VecTaskEnv(robots=("psm",), n_envs=2048, seed=3, episode_len=37)
+        tr = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim), ppo.TrainConfig(seed=5, fold_bootstrap=fold))
+        out = []
+        for _ in range(3):  # eager rollout, graph capture, graph replay
+            tr.rollout()
+            torch.cuda.synchronize()
+            out.append({k: tr.buf[k].clone() for k in ("obs", "actions", "logp", "values", "boot", "timed_out")})
+        bufs.append(out)
+    n_boot = sum(int((o["boot"] != 0).sum()) for o in bufs[0])
+    assert n_boot > 0  # timeouts inside the rollouts exercised the folded path
+    for a, b in zip(*bufs):
+        for k in a:
+            assert torch.equal(a[k], b[k]), k
