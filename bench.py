@@ -335,7 +335,7 @@ def bench_policy(args, cfg, rank, world, local, dist):
 
     runs = max(1, args.runs)
     with Clocks(local) as clk:
-        res = timed_runs(_Roll(), [T] * rollouts, flush, runs, not args.no_gate, dist, dev)
+        res = timed_runs(_Roll(), [T] * rollouts, flush, runs, not args.no_gate, dist, dev, gate_us=1000.0)
     tr.env.synchronize()
     t_runs = [r["t_ms"] for r in res]
     t_ms = statistics.mean(t_runs)
@@ -558,15 +558,16 @@ def dry_run(args, cfg, rank, world, local) -> None:
         dist.destroy_process_group()
 
 
-def gate_cycles(n_launches: int) -> int:
+def gate_cycles(n_launches: int, us_per_launch: float = 200.0) -> int:
     """Length of the device-side gate: long enough for the host to enqueue every
     flush / event / launch of one timed run behind it (generous: 200 us per
-    launch on top of 10 ms), and long enough for the SM clocks to be up when
-    the first timed launch starts."""
-    return int((10000 + 200 * n_launches) * 1e-6 * 2.0e9)
+    launch on top of 10 ms; a whole rollout graph replay gets more), and long
+    enough for the SM clocks to be up when the first timed launch starts."""
+    return int((10000 + us_per_launch * n_launches) * 1e-6 * 2.0e9)
 
 
-def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, retries: int = 3, do_flush: bool = True):
+def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, retries: int = 3, do_flush: bool = True,
+               gate_us: float = 200.0):
     """`runs` independent timed runs of the same launch sequence. Each run is
     bracketed by barrier + synchronize; every launch is preceded by an L2
     flush (256 MiB write) and timed by CUDA events on the env's stream (the
@@ -597,7 +598,7 @@ def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, retrie
             torch.cuda.synchronize()
             g = None
             if gate:
-                torch.cuda._sleep(gate_cycles(len(launches)))
+                torch.cuda._sleep(gate_cycles(len(launches), gate_us))
                 g = torch.cuda.Event()
                 g.record()
             for (e0, e1), kf in zip(ev, launches):
@@ -626,7 +627,7 @@ def timed_runs(env, launches, flush, runs: int, gate: bool, dist, device, retrie
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=None, help="timed env steps per run (default 64000; ppo: 320)")
+    ap.add_argument("--steps", type=int, default=None, help="timed env steps per run (default 25000; policy: 6400; ppo: 320)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="psm", choices=sorted(CONFIGS))
@@ -649,7 +650,11 @@ def main():
         cfg["n_envs"] = args.envs
         cfg["workload"] += f" [override: {args.envs} envs/GPU]"
     if args.steps is None:
-        args.steps = 320 if args.config == "ppo" else 64000
+        # default run lengths keep every launch of a run behind the device gate
+        # (the command queue holds ~1000 entries: 100 fused launches or 200
+        # rollouts with their flushes and events; longer runs stall the host
+        # mid-run and let host latency into the timed intervals)
+        args.steps = {"ppo": 320, "policy": 6400}.get(args.config, 25000)
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         sys.exit(spawn_ranks(args))
