@@ -2043,11 +2043,21 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
     tm.row0 = (int64_t)blockIdx.x * kTeamEnvs;
     tm.rows = (int)min((int64_t)kTeamEnvs, n - tm.row0);
   } else {
+#ifdef SG_PACKED32
+    // full 32-env teams, 3 or 4 per CTA (SM): the legacy layout's rows with
+    // the packed layout's role placement
+    const int64_t teams = (n + kTeamEnvs - 1) / kTeamEnvs;
+    const int64_t t0 = (int64_t)blockIdx.x * teams / gridDim.x, t1 = ((int64_t)blockIdx.x + 1) * teams / gridDim.x;
+    const int64_t g = t0 + tm.id;
+    tm.row0 = g * kTeamEnvs;
+    tm.rows = g < t1 ? (int)min((int64_t)kTeamEnvs, n - tm.row0) : 0;
+#else
     const int64_t quads = (n + 3) / 4, teams = (int64_t)gridDim.x * TPC;
     const int64_t g = (int64_t)blockIdx.x * TPC + tm.id;
     const int64_t q0 = g * quads / teams, q1 = (g + 1) * quads / teams;
     tm.row0 = 4 * q0;
     tm.rows = (int)(min(4 * q1, n) - tm.row0);
+#endif
   }
   float* base = smem + tm.id * (team_smem_bytes_g<G>(A) / sizeof(float));
   TeamSmem<G>& ts = *reinterpret_cast<TeamSmem<G>*>(base);
