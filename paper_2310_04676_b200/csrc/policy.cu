@@ -192,6 +192,36 @@ __device__ __forceinline__ uint32_t elu_pair(uint32_t a0, uint32_t a1, float2 b)
   return pack_bf16(fmaxf(x.x, e.x), fmaxf(x.y, e.y));
 }
 
+// The same on the FMA pipe: 2^t for t in [-127, 0] as 2^round(t) * p(t - round(t)),
+// round by the 1.5 * 2^23 magic add, p a degree-5 fit of 2^f on [-0.5, 0.5]
+// (max rel. error 1.9e-7 in fp32 Horner, like MUFU.EX2's ~2 ulp), the
+// exponent added in the integer domain. Meant to move every kPolyEvery-th
+// column pair off the MUFU pipe; measured slower (forward in a CUDA graph:
+// all MUFU 10.11 us, every 8th pair 10.23, 4th 10.66, 3rd 10.87): the
+// epilogues are issue / latency bound, not MUFU bound. Off by default.
+#ifndef SG_ELU_POLY_EVERY
+#define SG_ELU_POLY_EVERY 0
+#endif
+constexpr int kPolyEvery = SG_ELU_POLY_EVERY;  // 0: all MUFU
+__device__ __forceinline__ uint32_t elu_pair_poly(uint32_t a0, uint32_t a1, float2 b) {
+  const float2 x = __fadd2_rn(make_float2(__uint_as_float(a0), __uint_as_float(a1)), b);
+  const float2 tl = __fmul2_rn(x, make_float2(1.4426950408889634f, 1.4426950408889634f));
+  const float2 t = make_float2(fmaxf(fminf(tl.x, 0.f), -127.f), fmaxf(fminf(tl.y, 0.f), -127.f));
+  const float2 y = __fadd2_rn(t, make_float2(12582912.f, 12582912.f));
+  const float2 fi = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(t, make_float2(-fi.x, -fi.y));
+  float2 p = __ffma2_rn(f, make_float2(0.0013264729641377926f, 0.0013264729641377926f),
+                        make_float2(0.009671512991189957f, 0.009671512991189957f));
+  p = __ffma2_rn(p, f, make_float2(0.05550733581185341f, 0.05550733581185341f));
+  p = __ffma2_rn(p, f, make_float2(0.24022242426872253f, 0.24022242426872253f));
+  p = __ffma2_rn(p, f, make_float2(0.6931470036506653f, 0.6931470036506653f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  const float ex = __int_as_float(__float_as_int(p.x) + ((__float_as_int(y.x) - 0x4B400000) << 23));
+  const float ey = __int_as_float(__float_as_int(p.y) + ((__float_as_int(y.y) - 0x4B400000) << 23));
+  const float2 e = __fadd2_rn(make_float2(ex, ey), make_float2(-1.f, -1.f));
+  return pack_bf16(fmaxf(x.x, e.x), fmaxf(x.y, e.y));
+}
+
 // Hidden-layer epilogue in tensor memory: this thread's NC accumulator
 // columns [src, src + NC) of its TMEM lane -> ELU(acc + bias) -> bf16 pairs
 // written to columns [dst, dst + NC/2) of the same lane, where the next
@@ -220,8 +250,11 @@ __device__ __forceinline__ void epi_tmem(uint32_t trow, uint32_t src, uint32_t d
     uint32_t p[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k)
-      p[k] = elu_pair(r[j & 1][k >> 3][2 * (k & 7)], r[j & 1][k >> 3][2 * (k & 7) + 1],
-                      *reinterpret_cast<const float2*>(bias + c + 2 * k));
+      p[k] = (kPolyEvery > 0 && k % kPolyEvery == kPolyEvery - 1)
+                 ? elu_pair_poly(r[j & 1][k >> 3][2 * (k & 7)], r[j & 1][k >> 3][2 * (k & 7) + 1],
+                                 *reinterpret_cast<const float2*>(bias + c + 2 * k))
+                 : elu_pair(r[j & 1][k >> 3][2 * (k & 7)], r[j & 1][k >> 3][2 * (k & 7) + 1],
+                            *reinterpret_cast<const float2*>(bias + c + 2 * k));
     tmem_st16(trow + dst + c / 2, p);
     if constexpr (STORE) {  // the activations the backward pass needs: bf16 row segment of this thread
       if (g) {
