@@ -352,6 +352,23 @@ int sg_policy_act_noise(const sg_policy* policy, const float* d_obs, int64_t n, 
  * Uses the parameters of the last sg_policy_load_params. */
 int sg_policy_train_forward(const sg_policy* policy, const void* d_obs_bf16, int64_t n, int32_t obs_stride, void* d_h1,
                             void* d_h2, void* d_h3, void* d_out, void* stream);
+/* W^T images for sg_policy_dgrad_elu, packed from a flat fp32 parameter
+ * vector: image i (i = trunk*3 + layer - 1, hidden layers 1..3) holds
+ * W_i^T (in_dim[i] rows x out_dim[i] rounded up to 16 columns, bf16, the
+ * UMMA K-major layout) at the byte offset of the images before it
+ * (in_dim * round16(out_dim) * 2 bytes each); w_off[i] = offset of W_i
+ * [out x in] row-major in d_flat. */
+int sg_policy_pack_wt(const float* d_flat, const int64_t* w_off, const int32_t* out_dim, const int32_t* in_dim,
+                      uint8_t* d_images, void* stream);
+/* Backward through one hidden layer of the update's minibatch
+ * (Policy::backward, policy.cpp:163-218): d_dz = (d_dy W) * ELU'(d_h), where
+ * ELU'(h) = h > 0 ? 1 : h + 1 from the stored output h; d_dy bf16 [m x k]
+ * (row stride dy_stride), d_wt_image one sg_policy_pack_wt image, d_h /
+ * d_dz bf16 [m x n_in]. One tensor-core launch (fp32 accumulation, one
+ * rounding), instead of a GEMM writing d_dy W plus an elementwise pass.
+ * Shapes of the 256/128/64 trunk: (n_in, k) = (256, 128), (128, 64), (64, <= 16). */
+int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
+                        const void* d_h, void* d_dz, int64_t m, void* stream);
 /* Flat-parameter layout sg_policy_load_params packs from: per (trunk, layer)
  * (actor layers 0..3 then critic) the offsets of W [out x in] row-major and
  * of b, the row stride in_dim[layer] and the row count out_dim[trunk*4 + l]

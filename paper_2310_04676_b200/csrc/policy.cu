@@ -930,6 +930,152 @@ __global__ void __launch_bounds__(kThreads, 1) policy_train_fwd_kernel(const __g
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---- fused data gradient + ELU derivative (the update's backward) ---------
+// Policy::backward (policy.cpp:163-218) through one hidden layer of the PPO
+// update's minibatch: dZ = (dY W) * ELU'(h), ELU'(h) = h > 0 ? 1 : h + 1 (from
+// the stored output h), as one persistent tensor-core kernel instead of a
+// library GEMM that writes dY W in bf16 plus an elementwise pass that reads it
+// back: D[128 x N] = dY_tile [128 x KP] x (W^T)[N x KP]^T in TMEM (fp32),
+// multiplied by ELU'(h) in the epilogue and rounded once to bf16.
+// W^T is packed per minibatch into a K-major image (policy_pack_wt_kernel).
+struct DgradArgs {
+  const __nv_bfloat16* dy;  // [m x k], row stride dy_stride
+  int32_t dy_stride;
+  int32_t k;
+  const uint8_t* wt;        // W^T image [N x KP] bf16, K-major canonical
+  const __nv_bfloat16* h;   // [m x N]
+  __nv_bfloat16* dz;        // [m x N]
+  int64_t m;
+};
+
+#ifndef SG_DGRAD_CTAS
+#define SG_DGRAD_CTAS 2
+#endif
+constexpr int kDgradCtas = SG_DGRAD_CTAS;  // CTAs per SM (one's epilogue overlaps the other's loads / MMA)
+
+template <int N, int KP>
+__global__ void __launch_bounds__(256, kDgradCtas) policy_dgrad_elu_kernel(const __grid_constant__ DgradArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr uint32_t kBBytes = N * KP * 2, kABytes = kRows * KP * 2;
+  constexpr uint32_t kA = kBBytes, kBarOff = kA + kABytes;
+  constexpr int kChunks = kRows * KP / 8 / 256;  // 16-byte A chunks per thread per tile
+  constexpr uint32_t kCols = N < 32 ? 32 : N;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kBarOff + 16);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_b = smem_u32(&bars[0]), bar_mma = smem_u32(&bars[1]);
+  if (tid == 0) {
+    mbar_init(bar_b, 1);
+    mbar_init(bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  if (tid == 0) bulk_load(sbase, a.wt, kBBytes, bar_b);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const int half = warp >> 2;
+  const int64_t tiles = (a.m + kRows - 1) / kRows;
+  const auto load_a = [&](int64_t tile, uint4 (&v)[kChunks]) {
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const int c = tid + 256 * j, row = c % kRows, kc = c / kRows;
+      const int64_t r = tile * kRows + row;
+      v[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (tile < tiles && r < a.m && kc * 8 < a.k)
+        v[j] = *reinterpret_cast<const uint4*>(a.dy + r * a.dy_stride + kc * 8);
+    }
+  };
+  uint4 nxt[kChunks];
+  load_a(blockIdx.x, nxt);
+  uint32_t phase = 0;
+  bool first = true;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const int c = tid + 256 * j, row = c % kRows, kc = c / kRows;
+      *reinterpret_cast<uint4*>(smem + kA + kmajor_off(row, kc * 8, kRows)) = nxt[j];
+    }
+    load_a(tile + gridDim.x, nxt);  // the next tile's rows are in flight during this tile
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      if (first) mbar_wait(bar_b, 0);
+      tc_fence_after();
+      issue_layer(tmem, sbase + kA, kRows, sbase, N, KP, N);
+      mma_commit(bar_mma);
+    }
+    first = false;
+    mbar_wait(bar_mma, phase);
+    phase ^= 1;
+    tc_fence_after();
+    const int64_t r = tile * kRows + (warp & 3) * 32 + lane;
+#pragma unroll
+    for (int cb = 0; cb < N / 2; cb += 16) {
+      const int c = half * (N / 2) + cb;
+      uint32_t d[16];
+      tmem_ld16_async(trow + c, d);
+      uint4 hv[2] = {};
+      if (r < a.m) {
+        const uint4* hp = reinterpret_cast<const uint4*>(a.h + r * N + c);
+        hv[0] = hp[0];
+        hv[1] = hp[1];
+      }
+      tmem_wait_ld();
+      if (r < a.m) {
+        uint4 o[2];
+        uint32_t* ow = reinterpret_cast<uint32_t*>(o);
+        const uint32_t* hw = reinterpret_cast<const uint32_t*>(hv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[q]));
+          const float gx = hf.x > 0.f ? 1.f : hf.x + 1.f, gy = hf.y > 0.f ? 1.f : hf.y + 1.f;
+          ow[q] = pack_bf16(__uint_as_float(d[2 * q]) * gx, __uint_as_float(d[2 * q + 1]) * gy);
+        }
+        uint4* zp = reinterpret_cast<uint4*>(a.dz + r * N + c);
+        zp[0] = o[0];
+        zp[1] = o[1];
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // A smem and the TMEM accumulator are reused by the next tile
+    tc_fence_after();
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+}
+
+struct WtTable {
+  int64_t w_off[6];   // flat offset of W [K x N] row-major (trunk * 3 + layer 1..3)
+  int32_t k[6], n[6], kp[6];
+  int64_t img_off[6];  // byte offset of the image
+  int64_t total;       // elements over all images
+};
+
+// W^T images for policy_dgrad_elu_kernel: element (n, k) = W[k][n] (0 for
+// k >= K), bf16, K-major canonical over KP columns.
+__global__ void policy_pack_wt_kernel(const float* __restrict__ flat, const __grid_constant__ WtTable t,
+                                      uint8_t* __restrict__ out) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= t.total) return;
+  int i = 0;
+  while (e >= (int64_t)t.n[i] * t.kp[i]) {
+    e -= (int64_t)t.n[i] * t.kp[i];
+    ++i;
+  }
+  const int nn = (int)(e / t.kp[i]), kk = (int)(e % t.kp[i]);
+  const float v = kk < t.k[i] ? flat[t.w_off[i] + (int64_t)kk * t.n[i] + nn] : 0.f;
+  *reinterpret_cast<__nv_bfloat16*>(out + t.img_off[i] + kmajor_off(nn, kk, t.n[i])) = __float2bfloat16_rn(v);
+}
+
 // ---- packing: flat fp32 params (reference layout) -> bf16 UMMA images -----
 struct PackTable {
   int64_t w_off[2][4];  // flat offsets of W_l [out x in] per trunk
@@ -1192,6 +1338,26 @@ __global__ void adam_kernel(float* __restrict__ p, float* __restrict__ g, float*
 }
 
 }  // namespace sgp
+
+template <int N, int KP>
+static int launch_dgrad(const sgp::DgradArgs& a, cudaStream_t st) {
+  constexpr size_t smem = (size_t)N * KP * 2 + (size_t)sgp::kRows * KP * 2 + 64;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(sgp::policy_dgrad_elu_kernel<N, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (a.m + sgp::kRows - 1) / sgp::kRows;
+  const int64_t slots = (int64_t)sms * sgp::kDgradCtas;
+  sgp::policy_dgrad_elu_kernel<N, KP><<<(unsigned)(tiles < slots ? tiles : slots), 256, smem, st>>>(a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
 
 extern "C" {
 
@@ -1498,6 +1664,41 @@ int sg_policy_train_forward(const sg_policy* p, const void* d_obs_bf16, int64_t 
   sgp::policy_train_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_policy_pack_wt(const float* d_flat, const int64_t* w_off, const int32_t* out_dim, const int32_t* in_dim,
+                      uint8_t* d_images, void* stream) {
+  sgp::WtTable t{};
+  int64_t off = 0, total = 0;
+  for (int i = 0; i < 6; ++i) {
+    t.w_off[i] = w_off[i];
+    t.k[i] = out_dim[i];
+    t.n[i] = in_dim[i];
+    t.kp[i] = (out_dim[i] + 15) / 16 * 16;
+    t.img_off[i] = off;
+    off += (int64_t)t.n[i] * t.kp[i] * 2;
+    total += (int64_t)t.n[i] * t.kp[i];
+  }
+  t.total = total;
+  const int b = 256;
+  sgp::policy_pack_wt_kernel<<<(unsigned)((total + b - 1) / b), b, 0, (cudaStream_t)stream>>>(d_flat, t, d_images);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
+                        const void* d_h, void* d_dz, int64_t m, void* stream) {
+  if (m <= 0) return SG_OK;
+  if (!d_dy || !d_wt_image || !d_h || !d_dz) return fail(SG_ERR_CONFIG, "sg_policy_dgrad_elu: null argument");
+  const sgp::DgradArgs a{static_cast<const __nv_bfloat16*>(d_dy), dy_stride, k,
+                         static_cast<const uint8_t*>(d_wt_image), static_cast<const __nv_bfloat16*>(d_h),
+                         static_cast<__nv_bfloat16*>(d_dz), m};
+  const cudaStream_t st = (cudaStream_t)stream;
+  const int kp = (k + 15) / 16 * 16;
+  if (n_in == 64 && kp == 16) return launch_dgrad<64, 16>(a, st);
+  if (n_in == 128 && kp == 64) return launch_dgrad<128, 64>(a, st);
+  if (n_in == 256 && kp == 128) return launch_dgrad<256, 128>(a, st);
+  return fail(SG_ERR_CONFIG, "sg_policy_dgrad_elu: layer shape not instantiated (256/128/64 trunk)");
 }
 
 int sg_policy_set_param_layout(sg_policy* p, const int64_t* w_off, const int64_t* b_off, const int32_t* in_dim,

@@ -197,6 +197,8 @@ class _FusedMLP(torch.autograd.Function):
         m = obs.shape[0]
         h1, h2, h3, out = trainer.fused_buffers(m)
         trainer.train_policy.load_params(trainer.params)  # this minibatch's weights (Adam ran since)
+        if trainer.wt_images is not None:
+            trainer.wt_images.pack(trainer.params)  # W^T for the fused backward
         trainer.train_policy.train_forward(obs, h1, h2, h3, out)
         ctx.trainer, ctx.obs, ctx.acts = trainer, obs, (h1, h2, h3)
         return out[0], out[1]
@@ -210,12 +212,15 @@ class _FusedMLP(torch.autograd.Function):
             g = gy.contiguous().to(torch.bfloat16)
             for l in (3, 2, 1, 0):
                 W, b, Wm, _ = tr.layers[4 * t + l]
-                lctx = _LayerCtx(needs_gx=l > 0, direct=_direct_grads(W, b), w_dtype=W.dtype)
+                fused = tr.wt_images is not None and l > 0
+                lctx = _LayerCtx(needs_gx=l > 0 and not fused, direct=_direct_grads(W, b), w_dtype=W.dtype)
                 gx, gW, gb, _, _ = _linear_grads(lctx, g, ins[l], Wm)
                 if lctx.direct is None:  # (only without the trainer-owned gradient views)
                     W.grad.add_(gW)
                     b.grad.add_(gb)
-                if l > 0:
+                if fused:  # (dY W) * ELU'(h) in one tensor-core launch
+                    g = sg.dgrad_elu(g, tr.wt_images.image(t, l), ins[l].shape[1], ins[l])
+                elif l > 0:
                     g = sg.elu_backward(ins[l], gx.contiguous())
         return None, None, None
 
@@ -428,10 +433,17 @@ class Trainer:
         self.log_std = self.params[self.ls_off: self.ls_off + A].detach().requires_grad_(True)
         # the fused minibatch forward packs its weights from the padded copy
         self.train_policy = None
+        self.wt_images = None
         self._fused_buf = None
         if cfg.fused_forward and cfg.update_precision == "bf16" and os.environ.get("SG_NO_FUSED_FWD") != "1":
             self.train_policy = sg.Policy(O, A, device=policy.device)
             self.train_policy.set_param_layout(layout, [_up8(O), 256, 128, 64])
+            # the fused backward (sg_policy_dgrad_elu) is parity-tested but
+            # measured slower than library GEMM + ELU pass (15.4 vs 14.5 ms per
+            # update: its per-row bf16 loads / stores of h and dz are poorly
+            # coalesced); opt in with SG_FUSED_BWD=1
+            if os.environ.get("SG_FUSED_BWD") == "1":
+                self.wt_images = sg.WtImages(layout, dev)
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]
         # The whole update is one CUDA-graph replay at any world size: the NCCL
         # gradient all-reduce of every minibatch is captured with the GEMMs

@@ -155,6 +155,9 @@ _SIGS = {
     "sg_policy_train_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_policy_set_param_layout": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_pack_wt": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sg_policy_dgrad_elu": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                      C.c_void_p, C.c_int64, C.c_void_p]),
     "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p]),
@@ -712,6 +715,49 @@ def elu_backward(h, dh, out=None):
     out = torch.empty_like(h) if out is None else out
     stream = torch.cuda.current_stream(h.device).cuda_stream
     _pcheck(lib().sg_elu_backward(h.data_ptr(), dh.data_ptr(), out.data_ptr(), h.numel(), _dtype_code(h), stream))
+    return out
+
+
+class WtImages:
+    """sg_policy_pack_wt images of the six hidden-layer weights (trunk x layer
+    1..3) of a flat parameter vector, for sg_policy_dgrad_elu."""
+
+    def __init__(self, layout, device):
+        import torch
+        self.dims, self.offs = [], []
+        w_off, out_d, in_d = [], [], []
+        off = 0
+        for t in (0, 1):
+            for l in (1, 2, 3):
+                (w0, o, i), _ = layout[4 * t + l]
+                w_off.append(w0)
+                out_d.append(o)
+                in_d.append(i)
+                self.dims.append((o, i))
+                self.offs.append(off)
+                off += i * ((o + 15) // 16 * 16) * 2
+        self.buf = torch.zeros(off, dtype=torch.uint8, device=device)
+        self._w = (C.c_int64 * 6)(*w_off)
+        self._o = (C.c_int32 * 6)(*out_d)
+        self._i = (C.c_int32 * 6)(*in_d)
+
+    def pack(self, flat) -> None:
+        import torch
+        stream = torch.cuda.current_stream(flat.device).cuda_stream
+        _pcheck(lib().sg_policy_pack_wt(flat.data_ptr(), self._w, self._o, self._i, self.buf.data_ptr(), stream))
+
+    def image(self, trunk: int, layer: int) -> int:
+        return self.buf.data_ptr() + self.offs[3 * trunk + layer - 1]
+
+
+def dgrad_elu(dy, wt_ptr: int, n_in: int, h, out=None):
+    """sg_policy_dgrad_elu: (dy W) * ELU'(h) for one hidden layer (bf16)."""
+    import torch
+    m, k = dy.shape
+    out = torch.empty((m, n_in), dtype=torch.bfloat16, device=dy.device) if out is None else out
+    stream = torch.cuda.current_stream(dy.device).cuda_stream
+    _pcheck(lib().sg_policy_dgrad_elu(dy.data_ptr(), dy.stride(0), k, wt_ptr, n_in, h.data_ptr(), out.data_ptr(), m,
+                                      stream))
     return out
 
 

@@ -220,3 +220,32 @@ def test_fused_update_forward_matches_library_gradients(sg):
     tr = ppo.Trainer(env, sg.Policy(env.obs_dim, env.action_dim), ppo.TrainConfig(seed=4, update_precision="bf16"))
     h = tr.iterate()
     assert all(np.isfinite(h[k]) for k in ("policy_loss", "value_loss", "kl"))
+
+
+@pytest.mark.parametrize("n_in,k,m", [(256, 128, 131072), (128, 64, 1000), (64, 8, 129)])
+def test_dgrad_elu_matches_reference(sg, n_in, k, m):
+    """sg_policy_dgrad_elu (backward through a hidden layer: (dY W) * ELU'(h),
+    ELU'(h) = h > 0 ? 1 : h + 1, one tensor-core launch) == the fp32 product of
+    the same bf16 operands, rounded once to bf16; W^T packed by
+    sg_policy_pack_wt from a padded flat layout."""
+    from paper_2310_04676_b200 import ppo
+    torch.manual_seed(7)
+    layout, ls_pad, total, _ = ppo.padded_layout(27, 7)
+    flat = torch.randn(total, device="cuda") * 0.1
+    imgs = sg.WtImages(layout, 0)
+    imgs.pack(flat)
+    l = {256: 1, 128: 2, 64: 3}[n_in]
+    for t in (0, 1):
+        (w0, o, i), _ = layout[4 * t + l]
+        assert (o, i) == (k, n_in)
+        W = flat[w0: w0 + o * i].view(o, i).to(torch.bfloat16).float()
+        dy = (torch.randn(m, k, device="cuda") * 0.5).to(torch.bfloat16)
+        h = torch.where(torch.rand(m, n_in, device="cuda") < 0.5, torch.rand(m, n_in, device="cuda"),
+                        -torch.rand(m, n_in, device="cuda")).to(torch.bfloat16)
+        dz = sg.dgrad_elu(dy, imgs.image(t, l), n_in, h)
+        torch.cuda.synchronize()
+        hf = h.float()
+        ref = (dy.float() @ W) * torch.where(hf > 0, torch.ones_like(hf), hf + 1)
+        err = (dz.float() - ref).abs()
+        tol = 8e-3 * ref.abs() + 1e-4 * ref.abs().max()
+        assert torch.all(err <= tol), (t, err.max().item())
