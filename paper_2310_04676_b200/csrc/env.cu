@@ -6,6 +6,7 @@
 // dynamics.cpp:69-86, DynamicsConfig::validate :44-67), SimBatch seeding
 // (dynamics.cpp:225-241), workspace centre = FK(mid) (:161-162), observation
 // layout (:166-192). The step itself is one fused kernel (kernels.cuh).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -36,6 +37,13 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw sg::SimError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 #define CK(x) cuda_check((x), #x)
+// driver-API calls (stream memory operations)
+#define CU(x)                                                                                    \
+  do {                                                                                           \
+    const CUresult r_ = (x);                                                                     \
+    if (r_ != CUDA_SUCCESS)                                                                      \
+      throw sg::SimError(std::string("CUDA driver error ") + std::to_string((int)r_) + " in " #x); \
+  } while (0)
 
 // ---- host PCG32 (rng.hpp:25-83) for stream seeding and jump tables --------
 struct HostPcg {
@@ -270,6 +278,16 @@ struct sg_env {
   // teams' reads overlap earlier teams' result writes, 63.5 -> 62.0 us per
   // step (tools/gpu_r3a.sh: 64 / 256 / 384 no better)
   int read_window = std::getenv("SG_HOST_READ_WINDOW") ? std::atoi(std::getenv("SG_HOST_READ_WINDOW")) : 128;
+  // zero-copy host step: observation rows by the copy engine in chunks of
+  // teams, each chunk's copy starting as soon as its teams are done
+  // (SG_HOST_CE_CHUNKS, 0 = the kernel writes them over PCIe itself).
+  // Parity-tested but slower (PSM 16K: 62.9 us per step zero-copy, 85 / 99 /
+  // 124 / 172 us with 2 / 4 / 8 / 16 chunks: every chunk's stream wait +
+  // copy costs more than the copy engine gains over the SMs' PCIe writes)
+  int ce_chunks = std::getenv("SG_HOST_CE_CHUNKS") ? std::atoi(std::getenv("SG_HOST_CE_CHUNKS")) : 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_done = nullptr;
+  unsigned int* d_chunks = nullptr;  // [64] counts | [64] flags
   unsigned long long* d_status = nullptr;    // device alias of h_counters
   int host_slot = 0;                          // ended slot of the next host step
   bool bench_ready = false;
@@ -287,6 +305,12 @@ struct sg_env {
   ~sg_env() {
     cudaSetDevice(device);
     cudaStreamSynchronize(stream);
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+      cudaEventDestroy(copy_done);
+      cudaFree(d_chunks);
+    }
     if (h_counters) cudaFreeHost(h_counters);
     const auto& p = P.p;
     void* bufs[] = {p.q,   p.qd,       p.qt,         p.goals,      p.tips,     p.step_count, p.hold_count,
@@ -1240,6 +1264,22 @@ int sg_env_step(sg_env* env, const float* d_actions, sg_step_views* out) {
   });
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry-point lookup (the
+// library does not link libcuda, so it still loads on a machine without a
+// driver for the CPU-side tests).
+using StreamWaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static StreamWaitValue32Fn stream_wait_value32() {
+  static StreamWaitValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      throw sg::SimError("host step: cuStreamWaitValue32 unavailable");
+    return reinterpret_cast<StreamWaitValue32Fn>(p);
+  }();
+  return fn;
+}
+
 // Device alias of a host pointer the GPU can address directly (pinned memory
 // from cudaMallocHost / cudaHostAlloc / cudaHostRegister; under UVA the alias
 // equals the host address), or nullptr for pageable memory.
@@ -1357,7 +1397,39 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
         p.read_gate = reinterpret_cast<unsigned int*>(env->counters + 4) + 1;
         p.read_window = env->read_window;
       }
+      // observation rows by the copy engine, chunk by chunk (the legacy
+      // one-team-per-CTA layout: chunk = block range)
+      const int64_t teams_total = (n + 31) / 32;
+      const int chunks = (int)std::min<int64_t>(std::min(env->ce_chunks, 64), teams_total);
+      const bool ce = chunks > 0 && host_f[0] != nullptr && env->team_layout != sg::kLayoutPacked &&
+                      !env->own_kernel();
+      int chunk_teams = 0;
+      if (ce) {
+        if (!env->copy_stream) {
+          CK(cudaStreamCreateWithFlags(&env->copy_stream, cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&env->copy_done, cudaEventDisableTiming));
+          CK(cudaMalloc(&env->d_chunks, 128 * sizeof(unsigned int)));
+          CK(cudaMemset(env->d_chunks, 0, 128 * sizeof(unsigned int)));
+        }
+        chunk_teams = (int)((teams_total + chunks - 1) / chunks);
+        p.chunk_count = env->d_chunks;
+        p.chunk_flag = env->d_chunks + 64;
+        p.chunk_teams = chunk_teams;
+        p.h_obs = nullptr;  // rows stay in HBM (P.p.obs) for the copy engine
+      }
       env->launch_step(1, false);
+      if (ce) {
+        const unsigned seq = static_cast<unsigned>(p.h_seq);
+        for (int c = 0; c * chunk_teams < teams_total; ++c) {
+          const int64_t r0 = (int64_t)c * chunk_teams * 32, r1 = std::min<int64_t>(n, r0 + (int64_t)chunk_teams * 32);
+          CU(stream_wait_value32()(env->copy_stream, reinterpret_cast<CUdeviceptr>(env->d_chunks + 64 + c), seq,
+                                   CU_STREAM_WAIT_VALUE_GEQ));
+          CK(cudaMemcpyAsync(out->observations + r0 * O, p.obs + r0 * O, (r1 - r0) * O * sizeof(float),
+                             cudaMemcpyDeviceToHost, env->copy_stream));
+        }
+        CK(cudaEventRecord(env->copy_done, env->copy_stream));
+        p.chunk_count = p.chunk_flag = nullptr;
+      }
       p.read_gate = nullptr;
       p.h_obs = p.h_tobs = p.h_rewards = p.h_task_error = nullptr;
       p.h_terminated = p.h_timed_out = nullptr;
@@ -1398,6 +1470,8 @@ int sg_env_step_host(sg_env* env, const float* h_actions, sg_host_result* out) {
     } else {
       CK(cudaStreamSynchronize(s));
     }
+    if (zc && env->copy_done && env->ce_chunks > 0 && out && out->observations)
+      CK(cudaEventSynchronize(env->copy_done));  // the copy engine's observation rows
     const unsigned long long sat = env->h_counters[0], ended = env->h_counters[1];  // this step's
     env->raise(static_cast<int32_t>(env->h_counters[2] & 0xffffffffu));
     // terminal_observations are only meaningful on ended rows (envs.hpp:87);

@@ -154,6 +154,13 @@ struct EnvPtrs {
   // overlap earlier teams' result writes (the last CTA re-arms it)
   unsigned int* read_gate;
   int read_window;
+  // Host step with the observation rows copied by the copy engine (nullable):
+  // team b counts into chunk_count[b / chunk_teams]; the chunk's last team
+  // publishes chunk_flag[chunk] = h_seq, on which the copy stream waits
+  // (cuStreamWaitValue32) before copying the chunk's rows to the host
+  unsigned int* chunk_count;
+  unsigned int* chunk_flag;
+  int chunk_teams;
   float* h_rewards;
   float* h_task_error;
   uint8_t* h_terminated;
@@ -2096,6 +2103,15 @@ __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __gr
     // so the host may read them as soon as it sees h_status[3] == h_seq
     __threadfence_system();
     __syncthreads();
+    if (threadIdx.x == 0 && P.p.chunk_flag) {  // this team's rows are in HBM: count it into its chunk
+      const unsigned c = blockIdx.x / P.p.chunk_teams;
+      const unsigned in_chunk = min((unsigned)P.p.chunk_teams, gridDim.x - c * P.p.chunk_teams);
+      if (atomicAdd(&P.p.chunk_count[c], 1u) == in_chunk - 1) {
+        P.p.chunk_count[c] = 0;
+        __threadfence_system();
+        atomicExch(&P.p.chunk_flag[c], (unsigned)P.p.h_seq);
+      }
+    }
     if (threadIdx.x == 0) {
       __threadfence();
       if (atomicAdd(P.p.ticket, 1u) == gridDim.x - 1) {
