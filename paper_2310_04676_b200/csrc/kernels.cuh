@@ -1361,11 +1361,22 @@ struct Team {
   int tthread;  // thread index within the team (role * 32 + lane)
 };
 
+// Team barriers. The scorer and the producers reach each barrier from
+// their own role's code (warp-specialised, like CUTLASS's named-barrier
+// producer / consumer warps); a one-team CTA uses __syncthreads(_or), a
+// packed CTA the named barrier 1 + team. compute-sanitizer synccheck reports
+// these role-divergent arrivals ("divergent threads in block") with either
+// barrier form; memcheck and racecheck are clean and the results are
+// bit-exact against the oracle. SG_UNALIGNED_TEAM_BARRIERS: the non-aligned
+// barrier.cta forms for one-team CTAs too (measured 1-3 % slower).
 template <int G, int TPC>
 __device__ __forceinline__ bool team_sync_or(const Team& tm, bool v) {
+#ifndef SG_UNALIGNED_TEAM_BARRIERS
   if constexpr (TPC == 1) {
     return __syncthreads_or(v);
-  } else {
+  } else
+#endif
+  {
     uint32_t r;
     asm volatile(
         "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n barrier.cta.red.or.pred q, %2, %3, p;\n"
@@ -1379,8 +1390,13 @@ __device__ __forceinline__ bool team_sync_or(const Team& tm, bool v) {
 
 template <int G, int TPC>
 __device__ __forceinline__ void team_sync(const Team& tm) {
-  if constexpr (TPC == 1) __syncthreads();
-  else asm volatile("barrier.cta.sync %0, %1;" ::"r"(1 + tm.id), "r"(32 * G) : "memory");
+#ifndef SG_UNALIGNED_TEAM_BARRIERS
+  if constexpr (TPC == 1) {
+    __syncthreads();
+    return;
+  }
+#endif
+  asm volatile("barrier.cta.sync %0, %1;" ::"r"(1 + tm.id), "r"(32 * G) : "memory");
 }
 
 // One team warp. Warp 0 is the SCORER, warps 1..G-1 are PRODUCERS. Per step k
