@@ -1281,6 +1281,7 @@ template <int G>
 struct TeamSmem {
   float xf[2][G][12][kTeamEnvs];  // partial transforms, lane-contiguous (conflict-free)
   int32_t ended[2][kTeamEnvs];    // rows that ended at the step of that parity
+  int32_t any_end[2];             // the scorer's "rows ended" flag for the barrier of that parity
 };
 
 // Coalesced team store of `count` staged floats with 16-byte vectors. For a
@@ -1386,6 +1387,26 @@ __device__ __forceinline__ bool team_sync_or(const Team& tm, bool v) {
         : "memory");
     return r != 0;
   }
+}
+
+template <int G, int TPC>
+__device__ __forceinline__ void team_sync(const Team& tm);
+
+// A team barrier that also hands every warp the scorer's warp-uniform flag
+// v (S == 0: "rows ended at the previous step"): the barrier OR-reduction.
+// SG_FLAG_TEAM_BARRIER (A/B): the scorer's lane 0 stores the flag into `slot`
+// (one per step parity) before a plain barrier and everyone reads it after
+// -- same result, 5 % slower at K = 250 (187.6 vs 177.5 us), and synccheck
+// reports the plain barrier's role-divergent arrivals just the same.
+template <int G, int TPC, int S>
+__device__ __forceinline__ bool team_sync_flag(const Team& tm, int32_t& slot, bool v) {
+#ifndef SG_FLAG_TEAM_BARRIER
+  return team_sync_or<G, TPC>(tm, S == 0 && v);
+#else
+  if (S == 0 && (threadIdx.x & 31) == 0) slot = v ? 1 : 0;
+  team_sync<G, TPC>(tm);
+  return *reinterpret_cast<volatile int32_t*>(&slot) != 0;
+#endif
 }
 
 template <int G, int TPC>
@@ -1833,7 +1854,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
     SG_MARK(t_prod);
     // B(step); its OR says rows of step-1 ended: reset them as a team, then the
     // scorer produces this step and producers redo it for the reset rows
-    const bool any_end = team_sync_or<G, TPC>(tm, S == 0 && pend);
+    const bool any_end = team_sync_flag<G, TPC, S>(tm, ts.any_end[b], pend);
     SG_MARK(t_bar);
     if (any_end) {
       reset_phase(step - 1);
@@ -1979,7 +2000,7 @@ __device__ __forceinline__ void team_run(const StepParams& P, int k_steps, float
   // are stored (by the producers once the scorer has re-observed the reset
   // rows); the producers' registers of reset rows are stale (the reset state
   // is already in HBM)
-  const bool fix = team_sync_or<G, TPC>(tm, S == 0 && pend);
+  const bool fix = team_sync_flag<G, TPC, S>(tm, ts.any_end[k_steps & 1], pend);
   if (fix) reset_phase(k_steps - 1);
   if constexpr (kProdRows) {
     if (fix) team_sync<G, TPC>(tm);
