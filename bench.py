@@ -375,9 +375,10 @@ def bench_policy(args, cfg, rank, world, local, dist):
         o = env._result().observations
 
         def host_step(o):
-            pol.forward(o, mean, val)
-            sg._pcheck(L.sg_policy_sample(mean.data_ptr(), n, env.action_dim, ls.data_ptr(), tr.stream_state,
-                                          tr.stream_inc, d_pos.data_ptr(), 0, acts.data_ptr(), logp.data_ptr(), st))
+            # one fused tensor-core launch: forward + Gaussian sampling + log-prob
+            sg._pcheck(L.sg_policy_act(pol._h, o.data_ptr(), n, o.stride(0), ls.data_ptr(), tr.stream_state,
+                                       tr.stream_inc, d_pos.data_ptr(), 0, acts.data_ptr(), logp.data_ptr(), None,
+                                       val.data_ptr(), st))
             r = env.step(acts)
             h_obs.copy_(r.observations, non_blocking=True)
             h_rew.copy_(r.rewards, non_blocking=True)
@@ -398,9 +399,9 @@ def bench_policy(args, cfg, rank, world, local, dist):
         e_ms = max_over_ranks(a0.elapsed_time(a1), dist, dev)
         e2e = dict(value=world * n * E / (e_ms * 1e-3), unit="env-steps/s", h2d_bytes_per_step=0,
                    d2h_bytes_per_step=n * (env.obs_dim * 4 + 4 + 2), steps=E,
-                   path="sg_policy_forward + sg_policy_sample + sg_env_step per step, observations / rewards / "
-                        "flags copied to pinned host buffers and synchronised every step (no host inputs: the "
-                        "actions are the policy's)")
+                   path="sg_policy_act (forward + sampling, one launch) + sg_env_step per step, observations / "
+                        "rewards / flags copied to pinned host buffers and synchronised every step (no host inputs: "
+                        "the actions are the policy's)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -420,8 +421,9 @@ def bench_policy(args, cfg, rank, world, local, dist):
                           traffic=None, peak_kind=pk, kernel="policy_fwd_kernel (tcgen05)",
                           flops_per_env=POLICY_FLOPS_PER_ENV, avg_launch_us=fwd_s * 1e6),
             cpu_baseline=cpu, e2e=e2e,
-            # per rollout step: policy fwd, sample, env step, bootstrap; + the last-value fwd per rollout
-            gpu_launches=runs * rollouts * (4 * T + 1),
+            # per rollout step: one policy launch (act; + the previous step's bootstrap from step 1 on)
+            # and one env step; per rollout: the last step's bootstrap and the last-value forward
+            gpu_launches=runs * rollouts * (2 * T + 2),
             clocks=clk.summary(),
         )
         print(json.dumps(line), flush=True)
