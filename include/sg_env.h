@@ -405,6 +405,13 @@ int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d
  * output: dz = dh * (h > 0 ? 1 : h + 1). Graph-capturable. */
 int sg_elu_forward(const void* d_z, void* d_h, int64_t count, int32_t dtype, void* stream);
 int sg_elu_backward(const void* d_h, const void* d_dh, void* d_dz, int64_t count, int32_t dtype, void* stream);
+/* ELU backward fused with the next-lower layer's bias gradient, bf16 row-major
+ * [m x n] (n a multiple of 8): d_dz = d_dh * ELU'(d_h) and d_colsum[c] +=
+ * sum over rows of d_dz[., c] (fp32 atomics: d_colsum is the bias gradient,
+ * zero before the minibatch). d_h == NULL: a plain column sum of d_dh (the
+ * last layer's bias gradient); d_dz == NULL: no dz output. */
+int sg_elu_backward_colsum(const void* d_h, const void* d_dh, void* d_dz, int64_t m, int32_t n, float* d_colsum,
+                           void* stream);
 /* Minibatch gather (ppo.cpp:173-190): rows d_idx[0..m) of the rollout buffer:
  * obs (obs_w fp32 per row) into d_obs_out rows of obs_out_w >= obs_w (fp32, or
  * bf16 when obs_bf16; columns past obs_w zero), actions (A fp32), old

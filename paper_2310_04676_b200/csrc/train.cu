@@ -97,6 +97,59 @@ __global__ void elu_bwd_bf16(const uint4* __restrict__ h, const uint4* __restric
   }
 }
 
+// ELU backward + the bias gradient of the layer below in one pass
+// (Policy::backward, policy.cpp:163-218): dz = dh * ELU'(h) over a row-major
+// bf16 [m x n] activation, and colsum[c] += sum over rows of dz[., c] (the
+// next-lower layer's db = 1^T dZ, which otherwise is an M = 1 split-K GEMM
+// plus its reduction). h == null: dz = dh (a plain column sum of dh, the
+// last layer's db); dz == null: no dz output. A thread owns 8 columns (one
+// 16-byte vector) of rows t / (n/8), t / (n/8) + 256 / (n/8), ... and keeps
+// fp32 column sums in registers; the block folds them in shared memory and
+// adds one fp32 atomic per column.
+__global__ void elu_bwd_colsum_bf16(const uint4* __restrict__ h, const uint4* __restrict__ dh, uint4* __restrict__ dz,
+                                    int64_t m, int n, float* __restrict__ colsum) {
+  extern __shared__ float sred[];  // [256 / tpr][n]
+  const int tpr = n / 8, rpb = blockDim.x / tpr;  // threads per row, rows per block pass
+  const int c8 = threadIdx.x % tpr, r0 = threadIdx.x / tpr;
+  float acc[8] = {};
+  if (r0 < rpb) {
+    for (int64_t r = (int64_t)blockIdx.x * rpb + r0; r < m; r += (int64_t)gridDim.x * rpb) {
+      const int64_t k = r * tpr + c8;
+      Bf8 g, o;
+      g.u = dh[k];
+      if (h) {
+        Bf8 a;
+        a.u = h[k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 fa = __bfloat1622float2(a.h[j]), fg = __bfloat1622float2(g.h[j]);
+          o.h[j] = __floats2bfloat162_rn(fa.x > 0.f ? fg.x : fg.x * (fa.x + 1.f),
+                                         fa.y > 0.f ? fg.y : fg.y * (fa.y + 1.f));
+        }
+      } else {
+        o.u = g.u;
+      }
+      if (dz) dz[k] = o.u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(o.h[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+    }
+  }
+  if (r0 < rpb) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sred[r0 * n + c8 * 8 + j] = acc[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    float t = 0.f;
+    for (int q = 0; q < rpb; ++q) t += sred[q * n + c];
+    atomicAdd(&colsum[c], t);
+  }
+}
+
 // 8 threads per minibatch row: thread k copies float4 k of the obs row
 // (coalesced 128-byte rows); thread 0 also copies the row's action, log-prob,
 // advantage and return.
@@ -159,6 +212,17 @@ int sg_elu_forward(const void* z, void* h, int64_t count, int32_t dtype, void* s
     if (count % 4) return SG_ERR_CONFIG;
     elu_fwd_f32<<<grid_for(count / 4, 256), 256, 0, st>>>((const float4*)z, (float4*)h, count / 4);
   }
+  return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_SIM;
+}
+
+int sg_elu_backward_colsum(const void* h, const void* dh, void* dz, int64_t m, int32_t n, float* colsum,
+                           void* stream) {
+  if (n % 8 || n < 8 || n > 2048 || !dh || !colsum) return SG_ERR_CONFIG;
+  const int tpr = n / 8, rpb = 256 / tpr > 0 ? 256 / tpr : 1;
+  const unsigned grid = grid_for((m + rpb - 1) / rpb, 1);
+  const size_t smem = (size_t)rpb * n * sizeof(float);
+  elu_bwd_colsum_bf16<<<grid < 592u ? grid : 592u, 256, smem, (cudaStream_t)stream>>>(
+      (const uint4*)h, (const uint4*)dh, (uint4*)dz, m, n, colsum);
   return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_SIM;
 }
 

@@ -140,12 +140,15 @@ def _linear_grads(ctx, gy, x, W):
         ones = _Linear._ones[key] = torch.ones(1, B, dtype=gy.dtype, device=gy.device)
     if ctx.direct is not None and (out_dt is not None or gy.dtype == ctx.w_dtype):
         gW_buf, gb_buf = ctx.direct
+        skip_gb = getattr(ctx, "gb_done", False)  # the bias gradient came from a column-sum pass
         if out_dt:
             torch.mm(gy.t(), x, out_dtype=out_dt, out=gW_buf)
-            torch.mm(ones, gy, out_dtype=out_dt, out=gb_buf.view(1, -1))
+            if not skip_gb:
+                torch.mm(ones, gy, out_dtype=out_dt, out=gb_buf.view(1, -1))
         else:
             torch.mm(gy.t(), x, out=gW_buf)
-            torch.mm(ones, gy, out=gb_buf.view(1, -1))
+            if not skip_gb:
+                torch.mm(ones, gy, out=gb_buf.view(1, -1))
         return gx, None, None, None, None
     gW = torch.mm(gy.t(), x, out_dtype=out_dt) if out_dt else gy.t() @ x
     gb = (torch.mm(ones, gy, out_dtype=out_dt) if out_dt else ones @ gy).view(-1)
@@ -207,19 +210,28 @@ class _FusedMLP(torch.autograd.Function):
     def backward(ctx, g_mean, g_value):
         tr, obs = ctx.trainer, ctx.obs
         h1, h2, h3 = ctx.acts
+        colsum = tr.colsum_bias
         for t, gy in ((0, g_mean), (1, g_value)):
             ins = (obs, h1[t], h2[t], h3[t])
             g = gy.contiguous().to(torch.bfloat16)
             for l in (3, 2, 1, 0):
                 W, b, Wm, _ = tr.layers[4 * t + l]
+                direct = _direct_grads(W, b)
+                cs = colsum and direct is not None
+                if cs and l == 3:  # the last layer's db: one column-sum pass over dY
+                    sg.elu_backward_colsum(None, g, b.grad, out=False)
                 fused = tr.wt_images is not None and l > 0
-                lctx = _LayerCtx(needs_gx=l > 0 and not fused, direct=_direct_grads(W, b), w_dtype=W.dtype)
+                lctx = _LayerCtx(needs_gx=l > 0 and not fused, direct=direct, w_dtype=W.dtype, gb_done=cs)
                 gx, gW, gb, _, _ = _linear_grads(lctx, g, ins[l], Wm)
                 if lctx.direct is None:  # (only without the trainer-owned gradient views)
                     W.grad.add_(gW)
                     b.grad.add_(gb)
                 if fused:  # (dY W) * ELU'(h) in one tensor-core launch
                     g = sg.dgrad_elu(g, tr.wt_images.image(t, l), ins[l].shape[1], ins[l])
+                    if cs:
+                        sg.elu_backward_colsum(None, g, tr.layers[4 * t + l - 1][1].grad, out=False)
+                elif l > 0 and cs:  # ELU' and the next-lower layer's db in one pass
+                    g = sg.elu_backward_colsum(ins[l], gx.contiguous(), tr.layers[4 * t + l - 1][1].grad)
                 elif l > 0:
                     g = sg.elu_backward(ins[l], gx.contiguous())
         return None, None, None
@@ -228,10 +240,11 @@ class _FusedMLP(torch.autograd.Function):
 class _LayerCtx:
     """The attributes _linear_grads reads from an autograd ctx."""
 
-    def __init__(self, needs_gx: bool, direct, w_dtype):
+    def __init__(self, needs_gx: bool, direct, w_dtype, gb_done: bool = False):
         self.needs_input_grad = (needs_gx,)
         self.direct = direct
         self.w_dtype = w_dtype
+        self.gb_done = gb_done
 
 
 def param_layout(obs_dim: int, act_dim: int):
@@ -434,6 +447,9 @@ class Trainer:
         # the fused minibatch forward packs its weights from the padded copy
         self.train_policy = None
         self.wt_images = None
+        # bias gradients from column-sum passes (fused into the ELU backward)
+        # instead of M = 1 split-K GEMMs; SG_NO_COLSUM_BIAS=1 for the GEMMs
+        self.colsum_bias = os.environ.get("SG_NO_COLSUM_BIAS") != "1"
         self._fused_buf = None
         if cfg.fused_forward and cfg.update_precision == "bf16" and os.environ.get("SG_NO_FUSED_FWD") != "1":
             self.train_policy = sg.Policy(O, A, device=policy.device)

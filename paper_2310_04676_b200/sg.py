@@ -158,6 +158,8 @@ _SIGS = {
     "sg_policy_pack_wt": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_policy_dgrad_elu": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                                       C.c_void_p, C.c_int64, C.c_void_p]),
+    "sg_elu_backward_colsum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                         C.c_void_p]),
     "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p]),
@@ -759,6 +761,18 @@ def dgrad_elu(dy, wt_ptr: int, n_in: int, h, out=None):
     _pcheck(lib().sg_policy_dgrad_elu(dy.data_ptr(), dy.stride(0), k, wt_ptr, n_in, h.data_ptr(), out.data_ptr(), m,
                                       stream))
     return out
+
+
+def elu_backward_colsum(h, dh, colsum, out=True):
+    """sg_elu_backward_colsum: dz = dh * ELU'(h) (h None: dz = dh) and
+    colsum += column sums of dz (fp32). Returns dz (or None with out=False)."""
+    import torch
+    m, n = dh.shape
+    dz = torch.empty_like(dh) if out else None
+    stream = torch.cuda.current_stream(dh.device).cuda_stream
+    _pcheck(lib().sg_elu_backward_colsum(h.data_ptr() if h is not None else None, dh.data_ptr(),
+                                         dz.data_ptr() if dz is not None else None, m, n, colsum.data_ptr(), stream))
+    return dz
 
 
 def ppo_gather(idx, obs, act, logp, adv, ret, obs_out, act_out, logp_out, adv_out, ret_out):

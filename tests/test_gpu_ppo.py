@@ -376,3 +376,25 @@ def test_rollout_folded_bootstrap_equals_separate_launch(sg):
     for a, b in zip(*bufs):
         for k in a:
             assert torch.equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("m,n", [(131072, 256), (1000, 128), (257, 64), (131072, 8)])
+def test_elu_backward_colsum_matches_reference(sg, m, n):
+    """sg_elu_backward_colsum: dz = dh * ELU'(h) (bit-identical to
+    sg_elu_backward) and the fp32 column sums of dz accumulated into the
+    bias gradient (what 1^T dZ gives, to fp32 summation-order noise); h = NULL
+    gives the plain column sums of dh."""
+    torch.manual_seed(3)
+    h = torch.where(torch.rand(m, n, device="cuda") < 0.5, torch.rand(m, n, device="cuda"),
+                    -torch.rand(m, n, device="cuda")).to(torch.bfloat16)
+    dh = (torch.randn(m, n, device="cuda") * 0.3).to(torch.bfloat16)
+    acc = torch.full((n,), 0.25, device="cuda")  # accumulates on top of what is there
+    dz = sg.elu_backward_colsum(h, dh, acc)
+    ref_dz = sg.elu_backward(h, dh)
+    acc2 = torch.zeros(n, device="cuda")
+    sg.elu_backward_colsum(None, dh, acc2, out=False)
+    torch.cuda.synchronize()
+    assert torch.equal(dz, ref_dz)
+    ref = ref_dz.double().sum(0) + 0.25
+    assert torch.allclose(acc.double(), ref, rtol=1e-4, atol=1e-3)
+    assert torch.allclose(acc2.double(), dh.double().sum(0), rtol=1e-4, atol=1e-3)
