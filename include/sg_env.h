@@ -360,6 +360,14 @@ int sg_policy_train_forward(const sg_policy* policy, const void* d_obs_bf16, int
  * [out x in] row-major in d_flat. */
 int sg_policy_pack_wt(const float* d_flat, const int64_t* w_off, const int32_t* out_dim, const int32_t* in_dim,
                       uint8_t* d_images, void* stream);
+/* Weight gradient of one layer of the update's minibatch (Policy::backward,
+ * policy.cpp:163-218): d_grad [out x in] fp32 = d_dy^T d_x over m rows, with
+ * d_dy bf16 [m x out] and d_x bf16 [m x in] row-major (out x in of the
+ * 256/128/64 trunk with padded obs / outputs: 256x32, 128x256, 64x128, 8x64).
+ * parts CTAs each reduce a slice of rows on the tensor cores into
+ * d_partial (parts * out * in fp32), then one pass sums them into d_grad. */
+int sg_policy_wgrad(const void* d_dy, int32_t out_dim, const void* d_x, int32_t in_dim, int64_t m, float* d_partial,
+                    int32_t parts, float* d_grad, void* stream);
 /* Backward through one hidden layer of the update's minibatch
  * (Policy::backward, policy.cpp:163-218): d_dz = (d_dy W) * ELU'(d_h), where
  * ELU'(h) = h > 0 ? 1 : h + 1 from the stored output h; d_dy bf16 [m x k]

@@ -1076,6 +1076,196 @@ __global__ void policy_pack_wt_kernel(const float* __restrict__ flat, const __gr
   *reinterpret_cast<__nv_bfloat16*>(out + t.img_off[i] + kmajor_off(nn, kk, t.n[i])) = __float2bfloat16_rn(v);
 }
 
+// ---- weight gradients of the update (dW = dY^T X over the minibatch) --------
+// Policy::backward's dW (policy.cpp:163-218) reduces over all 131,072 rows of
+// a minibatch; as library GEMMs that is a split-K GEMM + reduction per layer
+// and trunk at ~25-30 us each whatever the shape. Here: each CTA takes a
+// contiguous slice of rows, streams 64-row stages of dY [rows x out] and X
+// [rows x in] into shared memory with cp.async -- 16-byte pieces of rows are
+// exactly the rows of the UMMA *MN-major* canonical layout (8 MN elements x 8
+// K rows per core matrix), so no transpose -- and accumulates
+// dW[out x in] = dY^T X with tcgen05.mma (A = dY^T, B = X^T, both MN-major) in
+// TMEM over its slice; the per-CTA partials are summed by a second kernel.
+// out is padded to 128 (or 256) MMA rows with zero A rows.
+__host__ __device__ constexpr uint32_t mnmajor_off(uint32_t mn, uint32_t k, uint32_t MN) {
+  return (k >> 3) * (MN * 16u) + (mn >> 3) * 128u + (k & 7u) * 16u + (mn & 7u) * 2u;
+}
+__host__ __device__ constexpr uint32_t make_idesc_mn(uint32_t M, uint32_t N) {  // BF16 x BF16 -> F32, A and B MN-major
+  return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+
+struct WgradArgs {
+  const __nv_bfloat16* dy;  // [m x out] row-major
+  const __nv_bfloat16* x;   // [m x in] row-major
+  int64_t m;
+  int64_t rows_per_cta;     // multiple of the 64-row stage
+  float* partial;           // [gridDim.x][out][in]
+};
+
+#ifndef SG_WGRAD_STAGES
+#define SG_WGRAD_STAGES 4
+#endif
+constexpr int kWgradStages = SG_WGRAD_STAGES;
+
+template <int OUT, int IN>
+__global__ void __launch_bounds__(128, 1) policy_wgrad_kernel(const __grid_constant__ WgradArgs a) {
+  constexpr int MP = OUT <= 128 ? 128 : 256, MT = MP / 128;  // padded MMA rows, M tiles
+  constexpr int S = 64;                                      // rows per stage (4 K-steps)
+  constexpr int NS = kWgradStages;                           // stages in flight
+  constexpr uint32_t kA = MP * S * 2, kB = IN * S * 2, kStage = kA + kB;
+  constexpr uint32_t kCols = MT * IN < 32 ? 32 : (MT * IN <= 64 ? 64 : (MT * IN <= 128 ? 128 : (MT * IN <= 256 ? 256 : 512)));
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * kStage);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + NS * kStage + 8 * NS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  if (tid == 0) {
+    for (int b = 0; b < NS; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // zero both stages once: the padded A rows (out..MP) are never written again
+  for (uint32_t o = tid * 16; o < NS * kStage; o += 128 * 16) *reinterpret_cast<uint4*>(smem + o) = make_uint4(0, 0, 0, 0);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
+  const int stages = r_begin < r_end ? (int)((r_end - r_begin + S - 1) / S) : 0;
+  // stage loader: dY rows -> A (MN = out), X rows -> B (MN = in); 16-byte
+  // pieces (8 consecutive out / in values of one row) are MN-major core rows
+  const auto load = [&](int st, int buf) {
+    const int64_t r0 = r_begin + (int64_t)st * S;
+    const uint32_t base = sbase + buf * kStage;
+    constexpr int kPa = S * OUT / 8, kPb = S * IN / 8;  // 16-byte pieces per stage
+    // piece p -> row (p / (8 * W8)) * 8 + p % 8, column block (p / 8) % W8:
+    // consecutive threads fill consecutive 16-byte rows of one core matrix
+    // (conflict-free shared stores; 8 rows x 64 bytes per warp from global)
+    for (int p = tid; p < kPa; p += 128) {
+      constexpr int W8 = OUT / 8;
+      const int r = (p / (8 * W8)) * 8 + (p & 7), o8 = (p >> 3) % W8;
+      const int64_t gr = r0 + r;
+      const bool ok = gr < r_end;
+      cp_async16(base + mnmajor_off(o8 * 8, r, MP), a.dy + (ok ? gr : 0) * OUT + o8 * 8, ok);
+    }
+    for (int p = tid; p < kPb; p += 128) {
+      constexpr int W8 = IN / 8;
+      const int r = (p / (8 * W8)) * 8 + (p & 7), i8 = (p >> 3) % W8;
+      const int64_t gr = r0 + r;
+      const bool ok = gr < r_end;
+      cp_async16(base + kA + mnmajor_off(i8 * 8, r, IN), a.x + (ok ? gr : 0) * IN + i8 * 8, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  uint32_t phase[NS] = {};
+  for (int st = 0; st < NS && st < stages; ++st) load(st, st);
+  for (int st = 0; st < stages; ++st) {
+    const int buf = st % NS;
+    // stage st has landed once at most (issued after it) groups are pending:
+    // stages issued so far = min(stages, NS + max(st - 1, 0))
+    const int issued = min(stages, NS + (st > 0 ? st - 1 : 0));
+    const int after = issued - st - 1;
+    if (after >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+    else if (after == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else if (after == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    async_proxy_fence();  // this thread's cp.async data -> the tensor core's (async proxy) reads
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      const uint32_t A = sbase + buf * kStage, B = A + kA;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int ks = 0; ks < S / 16; ++ks) {
+          const uint64_t da = make_desc(A + mt * 16 * 128 + 2u * ks * (MP * 16), MP * 16, 128);
+          const uint64_t db = make_desc(B + 2u * ks * (IN * 16), IN * 16, 128);
+          mma_bf16(tmem + mt * IN, da, db, make_idesc_mn(128, IN), (st > 0 || ks > 0) ? 1u : 0u);
+        }
+      mma_commit(smem_u32(&bars[buf]));
+    }
+    // refill the PREVIOUS stage's buffer (its MMAs were issued an iteration
+    // ago) with stage st - 1 + NS; this stage's MMAs run meanwhile
+    if (st >= 1 && st - 1 + NS < stages) {
+      const int pb = (st - 1) % NS;
+      mbar_wait(smem_u32(&bars[pb]), phase[pb]);
+      phase[pb] ^= 1;
+      load(st - 1 + NS, pb);
+    }
+  }
+  if (stages > 0) {  // the last stage's commit covers every MMA of this CTA
+    const int last = (stages - 1) % NS;
+    mbar_wait(smem_u32(&bars[last]), phase[last]);
+  }
+  tc_fence_after();
+  // epilogue: this CTA's partial dW (zero for an empty slice)
+  float* dst = a.partial + (int64_t)blockIdx.x * OUT * IN;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int o = mt * 128 + warp * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < IN; c += 16) {
+      float v[16];
+      tmem_ld16(trow + mt * IN + c, v);
+      if (o < OUT) {
+        float4* d4 = reinterpret_cast<float4*>(dst + (int64_t)o * IN + c);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          d4[q] = stages > 0 ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+  }
+}
+
+// sum of the per-CTA partials -> the weight gradient (fp32, written). A block
+// owns 32 consecutive float4s; its 8 warps split the partials (coalesced
+// 512-byte rows, ~19 independent loads per lane in flight), then fold.
+__global__ void __launch_bounds__(256) policy_wgrad_reduce_kernel(const float4* __restrict__ partial, int parts,
+                                                                  int64_t n4, float4* __restrict__ out) {
+  __shared__ float4 red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k = (int64_t)blockIdx.x * 32 + lane;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (k < n4) {
+#pragma unroll 4
+    for (int p = warp; p < parts; p += 8) {
+      const float4 v = partial[(int64_t)p * n4 + k];
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && k < n4) {
+    float4 t = red[0][lane];
+    for (int w = 1; w < 8; ++w) {
+      t.x += red[w][lane].x;
+      t.y += red[w][lane].y;
+      t.z += red[w][lane].z;
+      t.w += red[w][lane].w;
+    }
+    out[k] = t;
+  }
+}
+
 // ---- packing: flat fp32 params (reference layout) -> bf16 UMMA images -----
 struct PackTable {
   int64_t w_off[2][4];  // flat offsets of W_l [out x in] per trunk
@@ -1355,6 +1545,28 @@ static int launch_dgrad(const sgp::DgradArgs& a, cudaStream_t st) {
   const int64_t tiles = (a.m + sgp::kRows - 1) / sgp::kRows;
   const int64_t slots = (int64_t)sms * sgp::kDgradCtas;
   sgp::policy_dgrad_elu_kernel<N, KP><<<(unsigned)(tiles < slots ? tiles : slots), 256, smem, st>>>(a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+template <int OUT, int IN>
+static int launch_wgrad(const void* dy, const void* x, int64_t m, float* partial, int parts, float* out,
+                        cudaStream_t st) {
+  constexpr int MP = OUT <= 128 ? 128 : 256;
+  constexpr size_t smem = sgp::kWgradStages * ((size_t)MP * 64 * 2 + (size_t)IN * 64 * 2) + 128;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(sgp::policy_wgrad_kernel<OUT, IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+    attr = true;
+  }
+  const int64_t per = ((m + parts - 1) / parts + 63) / 64 * 64;
+  const sgp::WgradArgs a{static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), m, per, partial};
+  sgp::policy_wgrad_kernel<OUT, IN><<<parts, 128, smem, st>>>(a);
+  const int64_t n4 = (int64_t)OUT * IN / 4;
+  sgp::policy_wgrad_reduce_kernel<<<(unsigned)((n4 + 31) / 32), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(partial), parts, n4, reinterpret_cast<float4*>(out));
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
@@ -1684,6 +1896,18 @@ int sg_policy_pack_wt(const float* d_flat, const int64_t* w_off, const int32_t* 
   sgp::policy_pack_wt_kernel<<<(unsigned)((total + b - 1) / b), b, 0, (cudaStream_t)stream>>>(d_flat, t, d_images);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+int sg_policy_wgrad(const void* d_dy, int32_t out_dim, const void* d_x, int32_t in_dim, int64_t m,
+                    float* d_partial, int32_t parts, float* d_grad, void* stream) {
+  if (m <= 0) return SG_OK;
+  if (!d_dy || !d_x || !d_partial || !d_grad || parts < 1) return fail(SG_ERR_CONFIG, "sg_policy_wgrad: bad argument");
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (out_dim == 256 && in_dim == 32) return launch_wgrad<256, 32>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  if (out_dim == 128 && in_dim == 256) return launch_wgrad<128, 256>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  if (out_dim == 64 && in_dim == 128) return launch_wgrad<64, 128>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  if (out_dim == 8 && in_dim == 64) return launch_wgrad<8, 64>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  return fail(SG_ERR_CONFIG, "sg_policy_wgrad: layer shape not instantiated (256/128/64 trunk, padded obs / outputs)");
 }
 
 int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,

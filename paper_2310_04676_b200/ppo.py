@@ -141,7 +141,9 @@ def _linear_grads(ctx, gy, x, W):
     if ctx.direct is not None and (out_dt is not None or gy.dtype == ctx.w_dtype):
         gW_buf, gb_buf = ctx.direct
         skip_gb = getattr(ctx, "gb_done", False)  # the bias gradient came from a column-sum pass
-        if out_dt:
+        if getattr(ctx, "gw_done", False):  # the weight gradient came from sg_policy_wgrad
+            pass
+        elif out_dt:
             torch.mm(gy.t(), x, out_dtype=out_dt, out=gW_buf)
             if not skip_gb:
                 torch.mm(ones, gy, out_dtype=out_dt, out=gb_buf.view(1, -1))
@@ -221,7 +223,13 @@ class _FusedMLP(torch.autograd.Function):
                 if cs and l == 3:  # the last layer's db: one column-sum pass over dY
                     sg.elu_backward_colsum(None, g, b.grad, out=False)
                 fused = tr.wt_images is not None and l > 0
-                lctx = _LayerCtx(needs_gx=l > 0 and not fused, direct=direct, w_dtype=W.dtype, gb_done=cs)
+                # (the tensor-core reduction beats the split-K GEMM only for the
+                # narrow last layer: 18.8 vs 23.7 us; tools/wgrad_probe.py)
+                gw = tr.wgrad_partial is not None and direct is not None and l == 3
+                if gw:  # dW = dY^T X on the tensor cores (per-CTA row slices + one sum)
+                    sg.wgrad(g, ins[l], tr.wgrad_partial, W.grad)
+                lctx = _LayerCtx(needs_gx=l > 0 and not fused, direct=direct, w_dtype=W.dtype, gb_done=cs,
+                                 gw_done=gw)
                 gx, gW, gb, _, _ = _linear_grads(lctx, g, ins[l], Wm)
                 if lctx.direct is None:  # (only without the trainer-owned gradient views)
                     W.grad.add_(gW)
@@ -240,11 +248,12 @@ class _FusedMLP(torch.autograd.Function):
 class _LayerCtx:
     """The attributes _linear_grads reads from an autograd ctx."""
 
-    def __init__(self, needs_gx: bool, direct, w_dtype, gb_done: bool = False):
+    def __init__(self, needs_gx: bool, direct, w_dtype, gb_done: bool = False, gw_done: bool = False):
         self.needs_input_grad = (needs_gx,)
         self.direct = direct
         self.w_dtype = w_dtype
         self.gb_done = gb_done
+        self.gw_done = gw_done
 
 
 def param_layout(obs_dim: int, act_dim: int):
@@ -450,6 +459,9 @@ class Trainer:
         # bias gradients from column-sum passes (fused into the ELU backward)
         # instead of M = 1 split-K GEMMs; SG_NO_COLSUM_BIAS=1 for the GEMMs
         self.colsum_bias = os.environ.get("SG_NO_COLSUM_BIAS") != "1"
+        # weight gradients on the tensor cores (sg_policy_wgrad) instead of
+        # split-K library GEMMs; SG_NO_WGRAD=1 for the GEMMs
+        self.wgrad_partial = None
         self._fused_buf = None
         if cfg.fused_forward and cfg.update_precision == "bf16" and os.environ.get("SG_NO_FUSED_FWD") != "1":
             self.train_policy = sg.Policy(O, A, device=policy.device)
@@ -460,6 +472,8 @@ class Trainer:
             # coalesced); opt in with SG_FUSED_BWD=1
             if os.environ.get("SG_FUSED_BWD") == "1":
                 self.wt_images = sg.WtImages(layout, dev)
+            if os.environ.get("SG_NO_WGRAD") != "1":
+                self.wgrad_partial = torch.empty(148 * 128 * 256, device=dev)
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]
         # The whole update is one CUDA-graph replay at any world size: the NCCL
         # gradient all-reduce of every minibatch is captured with the GEMMs

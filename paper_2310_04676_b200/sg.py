@@ -160,6 +160,8 @@ _SIGS = {
                                       C.c_void_p, C.c_int64, C.c_void_p]),
     "sg_elu_backward_colsum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
                                          C.c_void_p]),
+    "sg_policy_wgrad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_int32,
+                                  C.c_void_p, C.c_void_p]),
     "sg_adam_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int64,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p]),
@@ -773,6 +775,18 @@ def elu_backward_colsum(h, dh, colsum, out=True):
     _pcheck(lib().sg_elu_backward_colsum(h.data_ptr() if h is not None else None, dh.data_ptr(),
                                          dz.data_ptr() if dz is not None else None, m, n, colsum.data_ptr(), stream))
     return dz
+
+
+def wgrad(dy, x, partial, out):
+    """sg_policy_wgrad: out (fp32 [o x i]) = dy^T x, dy bf16 [m x o], x bf16 [m x i]."""
+    import torch
+    m, o = dy.shape
+    i = x.shape[1]
+    parts = partial.numel() // (o * i)
+    parts = min(parts, 148)
+    stream = torch.cuda.current_stream(dy.device).cuda_stream
+    _pcheck(lib().sg_policy_wgrad(dy.data_ptr(), o, x.data_ptr(), i, m, partial.data_ptr(), parts, out.data_ptr(),
+                                  stream))
 
 
 def ppo_gather(idx, obs, act, logp, adv, ret, obs_out, act_out, logp_out, adv_out, ret_out):

@@ -398,3 +398,21 @@ def test_elu_backward_colsum_matches_reference(sg, m, n):
     ref = ref_dz.double().sum(0) + 0.25
     assert torch.allclose(acc.double(), ref, rtol=1e-4, atol=1e-3)
     assert torch.allclose(acc2.double(), dh.double().sum(0), rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("out_dim,in_dim,m", [(256, 32, 131072), (128, 256, 131072), (64, 128, 1000), (8, 64, 77)])
+def test_wgrad_matches_reference(sg, out_dim, in_dim, m):
+    """sg_policy_wgrad (dW = dY^T X over the minibatch rows on the tensor cores,
+    MN-major UMMA operands streamed with cp.async, per-CTA partials + one sum)
+    == the fp64 product of the same bf16 operands to fp32 accumulation noise,
+    including a ragged row count and CTAs with empty slices."""
+    torch.manual_seed(5)
+    dy = (torch.randn(m, out_dim, device="cuda") * 0.3).to(torch.bfloat16)
+    x = (torch.randn(m, in_dim, device="cuda") * 0.5).to(torch.bfloat16)
+    partial = torch.empty(148 * 128 * 256, device="cuda")
+    out = torch.full((out_dim, in_dim), 7.0, device="cuda")  # overwritten, not accumulated
+    sg.wgrad(dy, x, partial, out)
+    torch.cuda.synchronize()
+    ref = dy.double().t() @ x.double()
+    err = (out.double() - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item() + 1e-4, err
