@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -1529,16 +1530,24 @@ __global__ void adam_kernel(float* __restrict__ p, float* __restrict__ g, float*
 
 }  // namespace sgp
 
+// cudaFuncSetAttribute is per device: remember which devices a kernel's
+// shared-memory opt-in was made for (one bit per device, up to 64).
+static bool smem_opt_in(const void* fn, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load() & bit) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  done.fetch_or(bit);
+  return true;
+}
+
 template <int N, int KP>
 static int launch_dgrad(const sgp::DgradArgs& a, cudaStream_t st) {
   constexpr size_t smem = (size_t)N * KP * 2 + (size_t)sgp::kRows * KP * 2 + 64;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(sgp::policy_dgrad_elu_kernel<N, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
-    attr = true;
-  }
+  static std::atomic<unsigned long long> done{0};
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_dgrad_elu_kernel<N, KP>), (int)smem, done))
+    return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1554,13 +1563,9 @@ static int launch_wgrad(const void* dy, const void* x, int64_t m, float* partial
                         cudaStream_t st) {
   constexpr int MP = OUT <= 128 ? 128 : 256;
   constexpr size_t smem = sgp::kWgradStages * ((size_t)MP * 64 * 2 + (size_t)IN * 64 * 2) + 128;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(sgp::policy_wgrad_kernel<OUT, IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
-    attr = true;
-  }
+  static std::atomic<unsigned long long> done{0};
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_wgrad_kernel<OUT, IN>), (int)smem, done))
+    return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
   const int64_t per = ((m + parts - 1) / parts + 63) / 64 * 64;
   const sgp::WgradArgs a{static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), m, per, partial};
   sgp::policy_wgrad_kernel<OUT, IN><<<parts, 128, smem, st>>>(a);
@@ -1846,13 +1851,9 @@ int sg_policy_train_forward(const sg_policy* p, const void* d_obs_bf16, int64_t 
     return fail(SG_ERR_CONFIG, "sg_policy_train_forward: null argument");
   if (obs_stride < sgp::kK0 || obs_stride % 8 != 0)
     return fail(SG_ERR_CONFIG, "sg_policy_train_forward: obs_stride must be >= 32 and a multiple of 8");
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(sgp::policy_train_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sgp::kSmem) !=
-        cudaSuccess)
-      return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
-    attr = true;
-  }
+  static std::atomic<unsigned long long> done{0};
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_train_fwd_kernel), (int)sgp::kSmem, done))
+    return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
   sgp::PolicyImage W;
   W.w1 = p->img;
   W.w2a = p->img + 32768;
