@@ -25,6 +25,7 @@
 //  * fused rollout sampling: the fp64 Box-Muller draws run while layer 2 is
 //    on the tensor cores; the actions / log-probs are formed from the mean
 //    row in the kernel's tail.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -32,6 +33,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1234,6 +1236,127 @@ __global__ void __launch_bounds__(128, 1) policy_wgrad_kernel(const __grid_const
   }
 }
 
+// The same reduction fed by TMA for the wide layers (OUT, IN multiples of 64):
+// one 2-D tensor-map box per 64-column block and 64-row stage, written by
+// the TMA unit with the 128-byte swizzle, which is the UMMA MN-major
+// SWIZZLE_128B canonical layout (64 MN elements per 128-byte row, 8-row
+// groups 1 KB apart: SBO = 1 KB; the next 64-column block = the next box,
+// LBO = 8 KB). One thread issues the TMA boxes and the MMAs (a 4-stage
+// full / empty mbarrier ring); all warps drain TMEM at the end.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100)
+  d |= (uint64_t)2 << 61;  // layout type: SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+
+template <int OUT, int IN>
+__global__ void __launch_bounds__(128, 1) policy_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mdy,
+                                                                  const __grid_constant__ CUtensorMap mx,
+                                                                  const __grid_constant__ WgradArgs a) {
+  constexpr int MP = OUT <= 128 ? 128 : 256, MT = MP / 128;
+  constexpr int S = 64, NS = 4;
+  constexpr uint32_t kBox = S * 128;  // one 64-column x 64-row box
+  constexpr uint32_t kA = (OUT / 64) * kBox, kB = (IN / 64) * kBox, kStage = kA + kB;
+  static_assert(OUT % 64 == 0 && IN % 64 == 0, "TMA path: 64-column blocks");
+  constexpr uint32_t kCols = MT * IN <= 64 ? 64 : (MT * IN <= 128 ? 128 : (MT * IN <= 256 ? 256 : 512));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // 1 KB alignment for the swizzle
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * kStage);  // full[NS] | empty[NS]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + NS * kStage + 16 * NS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  if (tid == 0) {
+    for (int b = 0; b < 2 * NS; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mdy)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mx)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int64_t r_begin = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
+  const int stages = r_begin < r_end ? (int)((r_end - r_begin + S - 1) / S) : 0;
+  if (tid == 0 && stages > 0) {
+    const auto issue = [&](int st, int buf) {  // rows beyond m are zero-filled by the TMA unit
+      const uint32_t base = sbase + buf * kStage, full = smem_u32(&bars[buf]);
+      const int row = (int)(r_begin + (int64_t)st * S);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"(kStage) : "memory");
+#pragma unroll
+      for (int b = 0; b < OUT / 64; ++b) tma_load_2d(base + b * kBox, &mdy, b * 64, row, full);
+#pragma unroll
+      for (int b = 0; b < IN / 64; ++b) tma_load_2d(base + kA + b * kBox, &mx, b * 64, row, full);
+    };
+    uint32_t fph[NS] = {}, eph[NS] = {};
+    for (int st = 0; st < NS && st < stages; ++st) issue(st, st);
+    for (int st = 0; st < stages; ++st) {
+      const int buf = st % NS;
+      mbar_wait(smem_u32(&bars[buf]), fph[buf]);
+      fph[buf] ^= 1;
+      tc_fence_after();
+      const uint32_t A = sbase + buf * kStage, B = A + kA;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int ks = 0; ks < S / 16; ++ks)
+          mma_bf16(tmem + mt * IN, make_desc_sw128(A + mt * 2 * kBox + ks * 2048, kBox, 1024),
+                   make_desc_sw128(B + ks * 2048, kBox, 1024), make_idesc_mn(128, IN), (st > 0 || ks > 0) ? 1u : 0u);
+      mma_commit(smem_u32(&bars[NS + buf]));
+      if (st >= 1 && st - 1 + NS < stages) {  // refill the previous stage's buffer
+        const int pb = (st - 1) % NS;
+        mbar_wait(smem_u32(&bars[NS + pb]), eph[pb]);
+        eph[pb] ^= 1;
+        issue(st - 1 + NS, pb);
+      }
+    }
+    const int last = (stages - 1) % NS;  // its commit covers every MMA
+    mbar_wait(smem_u32(&bars[NS + last]), eph[last]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  float* dst = a.partial + (int64_t)blockIdx.x * OUT * IN;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int o = mt * 128 + warp * 32 + lane;
+#pragma unroll 4
+    for (int c = 0; c < IN; c += 16) {
+      float v[16];
+      tmem_ld16(trow + mt * IN + c, v);
+      if (o < OUT) {
+        float4* d4 = reinterpret_cast<float4*>(dst + (int64_t)o * IN + c);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          d4[q] = stages > 0 ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+  }
+}
+
 // sum of the per-CTA partials -> the weight gradient (fp32, written). A block
 // owns 32 consecutive float4s; its 8 warps split the partials (coalesced
 // 512-byte rows, ~19 independent loads per lane in flight), then fold.
@@ -1554,6 +1677,53 @@ static int launch_dgrad(const sgp::DgradArgs& a, cudaStream_t st) {
   const int64_t tiles = (a.m + sgp::kRows - 1) / sgp::kRows;
   const int64_t slots = (int64_t)sms * sgp::kDgradCtas;
   sgp::policy_dgrad_elu_kernel<N, KP><<<(unsigned)(tiles < slots ? tiles : slots), 256, smem, st>>>(a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
+using TensorMapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TensorMapEncodeFn tensor_map_encode() {
+  static TensorMapEncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<TensorMapEncodeFn>(nullptr);
+    return reinterpret_cast<TensorMapEncodeFn>(p);
+  }();
+  return fn;
+}
+// 2-D bf16 row-major [rows x cols] map, 64 x 64 boxes, 128-byte swizzle
+static bool encode_rows(CUtensorMap* map, const void* base, int cols, int64_t rows) {
+  const TensorMapEncodeFn enc = tensor_map_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int OUT, int IN>
+static int launch_wgrad_tma(const void* dy, const void* x, int64_t m, float* partial, int parts, float* out,
+                            cudaStream_t st) {
+  constexpr size_t smem = 4 * (size_t)(OUT / 64 + IN / 64) * 64 * 128 + 1024 + 256;
+  static std::atomic<unsigned long long> done{0};
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_wgrad_tma_kernel<OUT, IN>), (int)smem, done))
+    return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+  CUtensorMap mdy, mx;
+  if (!encode_rows(&mdy, dy, OUT, m) || !encode_rows(&mx, x, IN, m))
+    return fail(SG_ERR_SIM, "sg_policy_wgrad: cuTensorMapEncodeTiled failed");
+  const int64_t per = ((m + parts - 1) / parts + 63) / 64 * 64;
+  const sgp::WgradArgs a{static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), m, per, partial};
+  sgp::policy_wgrad_tma_kernel<OUT, IN><<<parts, 128, smem, st>>>(mdy, mx, a);
+  const int64_t n4 = (int64_t)OUT * IN / 4;
+  sgp::policy_wgrad_reduce_kernel<<<(unsigned)((n4 + 31) / 32), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(partial), parts, n4, reinterpret_cast<float4*>(out));
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
@@ -1905,8 +2075,13 @@ int sg_policy_wgrad(const void* d_dy, int32_t out_dim, const void* d_x, int32_t 
   if (!d_dy || !d_x || !d_partial || !d_grad || parts < 1) return fail(SG_ERR_CONFIG, "sg_policy_wgrad: bad argument");
   const cudaStream_t st = (cudaStream_t)stream;
   if (out_dim == 256 && in_dim == 32) return launch_wgrad<256, 32>(d_dy, d_x, m, d_partial, parts, d_grad, st);
-  if (out_dim == 128 && in_dim == 256) return launch_wgrad<128, 256>(d_dy, d_x, m, d_partial, parts, d_grad, st);
-  if (out_dim == 64 && in_dim == 128) return launch_wgrad<64, 128>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  const bool tma = std::getenv("SG_WGRAD_CPASYNC") == nullptr;  // A/B: the cp.async ring
+  if (out_dim == 128 && in_dim == 256)
+    return tma ? launch_wgrad_tma<128, 256>(d_dy, d_x, m, d_partial, parts, d_grad, st)
+               : launch_wgrad<128, 256>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  if (out_dim == 64 && in_dim == 128)
+    return tma ? launch_wgrad_tma<64, 128>(d_dy, d_x, m, d_partial, parts, d_grad, st)
+               : launch_wgrad<64, 128>(d_dy, d_x, m, d_partial, parts, d_grad, st);
   if (out_dim == 8 && in_dim == 64) return launch_wgrad<8, 64>(d_dy, d_x, m, d_partial, parts, d_grad, st);
   return fail(SG_ERR_CONFIG, "sg_policy_wgrad: layer shape not instantiated (256/128/64 trunk, padded obs / outputs)");
 }
