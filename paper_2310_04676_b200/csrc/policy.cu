@@ -1243,13 +1243,14 @@ __global__ void __launch_bounds__(128, 1) policy_wgrad_kernel(const __grid_const
 // groups 1 KB apart: SBO = 1 KB; the next 64-column block = the next box,
 // LBO = 8 KB). One thread issues the TMA boxes and the MMAs (a 4-stage
 // full / empty mbarrier ring); all warps drain TMEM at the end.
-__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// swizzled UMMA smem descriptor; layout type 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
+__device__ __forceinline__ uint64_t make_desc_sw(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t type) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;  // version (sm_100)
-  d |= (uint64_t)2 << 61;  // layout type: SWIZZLE_128B
+  d |= (uint64_t)type << 61;
   return d;
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
@@ -1260,15 +1261,18 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-template <int OUT, int IN>
+template <int OUT, int IN, bool ATOMIC>
 __global__ void __launch_bounds__(128, 1) policy_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mdy,
                                                                   const __grid_constant__ CUtensorMap mx,
                                                                   const __grid_constant__ WgradArgs a) {
   constexpr int MP = OUT <= 128 ? 128 : 256, MT = MP / 128;
   constexpr int S = 64, NS = 4;
-  constexpr uint32_t kBox = S * 128;  // one 64-column x 64-row box
-  constexpr uint32_t kA = (OUT / 64) * kBox, kB = (IN / 64) * kBox, kStage = kA + kB;
-  static_assert(OUT % 64 == 0 && IN % 64 == 0, "TMA path: 64-column blocks");
+  constexpr uint32_t kBox = S * 128;  // one 64-column x 64-row box (128-byte swizzle)
+  constexpr int BW = IN >= 64 ? 64 : IN;  // B box width: 64 (SWIZZLE_128B) or 32 (SWIZZLE_64B)
+  constexpr uint32_t kBoxB = S * BW * 2, kRowB = BW * 2;
+  constexpr uint32_t kSwB = BW == 64 ? 2u : 4u;
+  constexpr uint32_t kA = (OUT / 64) * kBox, kB = (IN / BW) * kBoxB, kStage = kA + kB;
+  static_assert(OUT % 64 == 0 && (IN % 64 == 0 || IN == 32), "TMA path: 64-column blocks (or one 32-column B)");
   constexpr uint32_t kCols = MT * IN <= 64 ? 64 : (MT * IN <= 128 ? 128 : (MT * IN <= 256 ? 256 : 512));
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // 1 KB alignment for the swizzle
@@ -1301,7 +1305,7 @@ __global__ void __launch_bounds__(128, 1) policy_wgrad_tma_kernel(const __grid_c
 #pragma unroll
       for (int b = 0; b < OUT / 64; ++b) tma_load_2d(base + b * kBox, &mdy, b * 64, row, full);
 #pragma unroll
-      for (int b = 0; b < IN / 64; ++b) tma_load_2d(base + kA + b * kBox, &mx, b * 64, row, full);
+      for (int b = 0; b < IN / BW; ++b) tma_load_2d(base + kA + b * kBoxB, &mx, b * BW, row, full);
     };
     uint32_t fph[NS] = {}, eph[NS] = {};
     for (int st = 0; st < NS && st < stages; ++st) issue(st, st);
@@ -1315,8 +1319,9 @@ __global__ void __launch_bounds__(128, 1) policy_wgrad_tma_kernel(const __grid_c
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int ks = 0; ks < S / 16; ++ks)
-          mma_bf16(tmem + mt * IN, make_desc_sw128(A + mt * 2 * kBox + ks * 2048, kBox, 1024),
-                   make_desc_sw128(B + ks * 2048, kBox, 1024), make_idesc_mn(128, IN), (st > 0 || ks > 0) ? 1u : 0u);
+          mma_bf16(tmem + mt * IN, make_desc_sw(A + mt * 2 * kBox + ks * 2048, kBox, 1024, 2),
+                   make_desc_sw(B + ks * 16 * kRowB, kBoxB, 8 * kRowB, kSwB), make_idesc_mn(128, IN),
+                   (st > 0 || ks > 0) ? 1u : 0u);
       mma_commit(smem_u32(&bars[NS + buf]));
       if (st >= 1 && st - 1 + NS < stages) {  // refill the previous stage's buffer
         const int pb = (st - 1) % NS;
@@ -1331,7 +1336,9 @@ __global__ void __launch_bounds__(128, 1) policy_wgrad_tma_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  float* dst = a.partial + (int64_t)blockIdx.x * OUT * IN;
+  // ATOMIC: add this CTA's slice sum straight into the (zeroed) gradient
+  // with vector reductions; else write the partial for the reduction pass
+  float* dst = ATOMIC ? a.partial : a.partial + (int64_t)blockIdx.x * OUT * IN;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -1341,11 +1348,22 @@ __global__ void __launch_bounds__(128, 1) policy_wgrad_tma_kernel(const __grid_c
       float v[16];
       tmem_ld16(trow + mt * IN + c, v);
       if (o < OUT) {
-        float4* d4 = reinterpret_cast<float4*>(dst + (int64_t)o * IN + c);
+        float* row = dst + (int64_t)o * IN + c;
+        if constexpr (ATOMIC) {
+          if (stages > 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          d4[q] = stages > 0 ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < 4; ++q)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * q), "f"(v[4 * q]),
+                           "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                           : "memory");
+          }
+        } else {
+          float4* d4 = reinterpret_cast<float4*>(row);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            d4[q] = stages > 0 ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
     }
   }
@@ -1695,32 +1713,42 @@ static TensorMapEncodeFn tensor_map_encode() {
   }();
   return fn;
 }
-// 2-D bf16 row-major [rows x cols] map, 64 x 64 boxes, 128-byte swizzle
+// 2-D bf16 row-major [rows x cols] map, boxes of min(cols, 64) columns x 64
+// rows, 128-byte (64-column) or 64-byte (32-column) swizzle
 static bool encode_rows(CUtensorMap* map, const void* base, int cols, int64_t rows) {
   const TensorMapEncodeFn enc = tensor_map_encode();
   if (!enc) return false;
+  const int bw = cols >= 64 ? 64 : cols;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t box[2] = {(cuuint32_t)bw, 64};
   const cuuint32_t estr[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, bw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int OUT, int IN>
+template <int OUT, int IN, bool ATOMIC = false>
 static int launch_wgrad_tma(const void* dy, const void* x, int64_t m, float* partial, int parts, float* out,
                             cudaStream_t st) {
-  constexpr size_t smem = 4 * (size_t)(OUT / 64 + IN / 64) * 64 * 128 + 1024 + 256;
+  constexpr size_t smem = 4 * ((size_t)(OUT / 64) * 64 * 128 + (size_t)IN * 64 * 2) + 1024 + 256;
   static std::atomic<unsigned long long> done{0};
-  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_wgrad_tma_kernel<OUT, IN>), (int)smem, done))
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_wgrad_tma_kernel<OUT, IN, ATOMIC>), (int)smem, done))
     return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
   CUtensorMap mdy, mx;
   if (!encode_rows(&mdy, dy, OUT, m) || !encode_rows(&mx, x, IN, m))
     return fail(SG_ERR_SIM, "sg_policy_wgrad: cuTensorMapEncodeTiled failed");
   const int64_t per = ((m + parts - 1) / parts + 63) / 64 * 64;
+  if constexpr (ATOMIC) {  // vector reductions into the zeroed gradient
+    const sgp::WgradArgs a{static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), m, per, out};
+    if (cudaMemsetAsync(out, 0, (size_t)OUT * IN * sizeof(float), st) != cudaSuccess)
+      return fail(SG_ERR_SIM, "sg_policy_wgrad: memset failed");
+    sgp::policy_wgrad_tma_kernel<OUT, IN, true><<<parts, 128, smem, st>>>(mdy, mx, a);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+  }
   const sgp::WgradArgs a{static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), m, per, partial};
-  sgp::policy_wgrad_tma_kernel<OUT, IN><<<parts, 128, smem, st>>>(mdy, mx, a);
+  sgp::policy_wgrad_tma_kernel<OUT, IN, false><<<parts, 128, smem, st>>>(mdy, mx, a);
   const int64_t n4 = (int64_t)OUT * IN / 4;
   sgp::policy_wgrad_reduce_kernel<<<(unsigned)((n4 + 31) / 32), 256, 0, st>>>(
       reinterpret_cast<const float4*>(partial), parts, n4, reinterpret_cast<float4*>(out));
@@ -2074,14 +2102,23 @@ int sg_policy_wgrad(const void* d_dy, int32_t out_dim, const void* d_x, int32_t 
   if (m <= 0) return SG_OK;
   if (!d_dy || !d_x || !d_partial || !d_grad || parts < 1) return fail(SG_ERR_CONFIG, "sg_policy_wgrad: bad argument");
   const cudaStream_t st = (cudaStream_t)stream;
-  if (out_dim == 256 && in_dim == 32) return launch_wgrad<256, 32>(d_dy, d_x, m, d_partial, parts, d_grad, st);
   const bool tma = std::getenv("SG_WGRAD_CPASYNC") == nullptr;  // A/B: the cp.async ring
-  if (out_dim == 128 && in_dim == 256)
-    return tma ? launch_wgrad_tma<128, 256>(d_dy, d_x, m, d_partial, parts, d_grad, st)
-               : launch_wgrad<128, 256>(d_dy, d_x, m, d_partial, parts, d_grad, st);
-  if (out_dim == 64 && in_dim == 128)
-    return tma ? launch_wgrad_tma<64, 128>(d_dy, d_x, m, d_partial, parts, d_grad, st)
-               : launch_wgrad<64, 128>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  const bool red = std::getenv("SG_WGRAD_PARTIALS") == nullptr;   // A/B: partials + reduction pass
+  if (out_dim == 256 && in_dim == 32) {
+    if (!tma) return launch_wgrad<256, 32>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+    return red ? launch_wgrad_tma<256, 32, true>(d_dy, d_x, m, d_partial, parts, d_grad, st)
+               : launch_wgrad_tma<256, 32, false>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  }
+  if (out_dim == 128 && in_dim == 256) {
+    if (!tma) return launch_wgrad<128, 256>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+    return red ? launch_wgrad_tma<128, 256, true>(d_dy, d_x, m, d_partial, parts, d_grad, st)
+               : launch_wgrad_tma<128, 256, false>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  }
+  if (out_dim == 64 && in_dim == 128) {
+    if (!tma) return launch_wgrad<64, 128>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+    return red ? launch_wgrad_tma<64, 128, true>(d_dy, d_x, m, d_partial, parts, d_grad, st)
+               : launch_wgrad_tma<64, 128, false>(d_dy, d_x, m, d_partial, parts, d_grad, st);
+  }
   if (out_dim == 8 && in_dim == 64) return launch_wgrad<8, 64>(d_dy, d_x, m, d_partial, parts, d_grad, st);
   return fail(SG_ERR_CONFIG, "sg_policy_wgrad: layer shape not instantiated (256/128/64 trunk, padded obs / outputs)");
 }

@@ -223,10 +223,10 @@ class _FusedMLP(torch.autograd.Function):
                 if cs and l == 3:  # the last layer's db: one column-sum pass over dY
                     sg.elu_backward_colsum(None, g, b.grad, out=False)
                 fused = tr.wt_images is not None and l > 0
-                # (the tensor-core reduction beats the split-K GEMM for the two
-                # narrow layers: 64x128 18.7 vs 27.5 us (TMA-fed), 8x64 18.7 vs
-                # 23.7 us; the wide ones are at par or behind; tools/wgrad_probe.py)
-                gw = tr.wgrad_partial is not None and direct is not None and l >= 2
+                # (tensor-core reductions beat the split-K GEMMs on every layer:
+                # 256x32 23.7 vs 30.8 us, 128x256 26.7 vs 32.0, 64x128 19.4 vs
+                # 27.5 (TMA-fed), 8x64 18.7 vs 24.6; tools/wgrad_probe.py)
+                gw = tr.wgrad_partial is not None and direct is not None
                 if gw:  # dW = dY^T X on the tensor cores (per-CTA row slices + one sum)
                     sg.wgrad(g, ins[l], tr.wgrad_partial, W.grad)
                 lctx = _LayerCtx(needs_gx=l > 0 and not fused, direct=direct, w_dtype=W.dtype, gb_done=cs,
