@@ -377,6 +377,15 @@ int sg_policy_wgrad(const void* d_dy, int32_t out_dim, const void* d_x, int32_t 
  * Shapes of the 256/128/64 trunk: (n_in, k) = (256, 128), (128, 64), (64, <= 16). */
 int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
                         const void* d_h, void* d_dz, int64_t m, void* stream);
+/* The whole backward through hidden layer l of the update's minibatch
+ * (Policy::backward, policy.cpp:163-218) in one launch: d_dz = (d_dy W) *
+ * ELU'(d_h) as sg_policy_dgrad_elu (same shapes), plus, when not NULL,
+ * d_colsum[n_in] (fp32) += the column sums of d_dz (the bias gradient of
+ * layer l-1) and d_wgrad[k x n_in] (fp32, row-major) += d_dy^T d_h (the
+ * weight gradient of layer l; d_h is layer l's input). d_h / d_dz move
+ * through TMA (16-byte aligned, row stride n_in). */
+int sg_policy_layer_backward(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
+                             const void* d_h, void* d_dz, int64_t m, float* d_colsum, float* d_wgrad, void* stream);
 /* Flat-parameter layout sg_policy_load_params packs from: per (trunk, layer)
  * (actor layers 0..3 then critic) the offsets of W [out x in] row-major and
  * of b, the row stride in_dim[layer] and the row count out_dim[trunk*4 + l]

@@ -1253,6 +1253,7 @@ __device__ __forceinline__ uint64_t make_desc_sw(uint32_t saddr, uint32_t lbo, u
   d |= (uint64_t)type << 61;
   return d;
 }
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -1363,6 +1364,204 @@ __global__ void __launch_bounds__(128, 1) policy_wgrad_tma_kernel(const __grid_c
           for (int q = 0; q < 4; ++q)
             d4[q] = stages > 0 ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+  }
+}
+
+// The whole backward through one hidden layer l in one launch
+// (Policy::backward, policy.cpp:163-218), per 128-row tile:
+//   dZ_{l-1} = (dY_l W_l) * ELU'(h)        (MMA 1: A = dY tile, B = W^T image)
+//   dW_l^T  += h^T dY_l                     (MMA 2, accumulated in TMEM over the CTA's tiles)
+//   db_{l-1} += 1^T dZ_{l-1}                (column sums, per CTA in registers)
+// h = x_l is both the ELU' argument and the weight-gradient operand. Its
+// rows arrive as 128-row x 64-column TMA boxes with the 128-byte swizzle --
+// the UMMA MN-major SWIZZLE_128B layout, so MMA 2 reads h^T straight from
+// them (SBO = 1 KB per 8 rows, LBO = one box) -- and MMA 2's B operand is
+// the dY tile as staged for MMA 1: its 8 x 16-byte core matrices hold 8
+// rows x 8 dY columns, which read as N-contiguous (MN-major, no swizzle)
+// core matrices with K (row) blocks 128 B apart and N blocks 2 KB apart.
+// The epilogue turns each thread's (row's) TMEM accumulators and the h
+// values it reads back from shared memory into dZ in place, and one thread
+// stores the boxes with TMA -- coalesced both ways, where the per-row 16-byte
+// global accesses of policy_dgrad_elu_kernel touch 32 rows per instruction.
+// At the end the CTA adds its dW_l^T (lane = input column, TMEM column =
+// output row) into the fp32 gradient with coalesced reductions (lanes =
+// consecutive inputs). colsum / wgrad nullable.
+__device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t c) {  // (row, column) in a 128 x 64 bf16 box
+  return r * 128u + ((((c >> 3) ^ (r & 7u)) & 7u) << 4) + (c & 7u) * 2u;
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+
+template <int N, int KP>
+__global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_constant__ CUtensorMap mh,
+                                                                  const __grid_constant__ CUtensorMap mdz,
+                                                                  const __grid_constant__ DgradArgs a,
+                                                                  float* __restrict__ colsum,
+                                                                  float* __restrict__ wgrad) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  constexpr uint32_t kBBytes = N * KP * 2, kABytes = kRows * KP * 2, kBox = kRows * 128;
+  constexpr int MT = N < 128 ? 1 : N / 128;  // MMA 2 row blocks (N = 64 reads a 2nd, ignored box)
+  constexpr uint32_t kHBoxes = N < 128 ? 2 : N / 64;
+  constexpr uint32_t kA = kBBytes, kH = (kA + kABytes + 1023) / 1024 * 1024, kBarOff = kH + kHBoxes * kBox;
+  constexpr int kChunks = kRows * KP / 8 / 256;
+  constexpr uint32_t kWCol = N;  // dW^T accumulator columns [N, N + MT * KP)
+  constexpr uint32_t kCols = N + MT * KP <= 128 ? 128 : (N + MT * KP <= 256 ? 256 : 512);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);  // B, MMA, H
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kBarOff + 32);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_b = smem_u32(&bars[0]), bar_mma = smem_u32(&bars[1]), bar_h = smem_u32(&bars[2]);
+  if (tid == 0) {
+    mbar_init(bar_b, 1);
+    mbar_init(bar_mma, 1);
+    mbar_init(bar_h, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mdz)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  if (tid == 0) bulk_load(sbase, a.wt, kBBytes, bar_b);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const int half = warp >> 2;
+  const int64_t tiles = (a.m + kRows - 1) / kRows;
+  const auto load_a = [&](int64_t tile, uint4 (&v)[kChunks]) {
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const int c = tid + 256 * j, row = c % kRows, kc = c / kRows;
+      const int64_t r = tile * kRows + row;
+      v[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (tile < tiles && r < a.m && kc * 8 < a.k)
+        v[j] = *reinterpret_cast<const uint4*>(a.dy + r * a.dy_stride + kc * 8);
+    }
+  };
+  uint4 nxt[kChunks];
+  load_a(blockIdx.x, nxt);
+  uint32_t ph = 0;
+  bool first = true;
+  float csum = 0.f;  // column tid's sum of dZ over this CTA's tiles
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int row0 = (int)(tile * kRows);
+    if (tid == 0) {  // this tile's h boxes (the previous tile's dZ stores have read the buffer)
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_h), "r"((N / 64) * kBox)
+                   : "memory");
+#pragma unroll
+      for (int b = 0; b < N / 64; ++b) tma_load_2d(sbase + kH + b * kBox, &mh, b * 64, row0, bar_h);
+    }
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const int c = tid + 256 * j, row = c % kRows, kc = c / kRows;
+      *reinterpret_cast<uint4*>(smem + kA + kmajor_off(row, kc * 8, kRows)) = nxt[j];
+    }
+    load_a(tile + gridDim.x, nxt);
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      if (first) mbar_wait(bar_b, 0);
+      tc_fence_after();
+      issue_layer(tmem, sbase + kA, kRows, sbase, N, KP, N);
+      if (wgrad) {  // dW^T += h^T dY, once this tile's h boxes have landed
+        mbar_wait(bar_h, ph);
+        tc_fence_after();
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int ks = 0; ks < kRows / 16; ++ks)
+            mma_bf16(tmem + kWCol + mt * KP, make_desc_sw(sbase + kH + mt * 2 * kBox + ks * 2048, kBox, 1024, 2),
+                     make_desc(sbase + kA + ks * 256, 128, kRows * 16), make_idesc_mn(128, KP),
+                     (!first || ks > 0) ? 1u : 0u);
+      }
+      mma_commit(bar_mma);
+    }
+    first = false;
+    mbar_wait(bar_mma, ph);
+    mbar_wait(bar_h, ph);
+    ph ^= 1;
+    tc_fence_after();
+    const uint32_t r = (uint32_t)((warp & 3) * 32 + lane);
+#pragma unroll
+    for (int cb = 0; cb < N / 2; cb += 16) {  // this half's columns, 16 at a time
+      const int c = half * (N / 2) + cb;
+      uint32_t d[16];
+      tmem_ld16_async(trow + c, d);
+      uint8_t* box = smem + kH + (c >> 6) * kBox;
+      const uint32_t o0 = sw128_off(r, c & 63), o1 = sw128_off(r, (c & 63) + 8);
+      uint4 hv[2] = {*reinterpret_cast<const uint4*>(box + o0), *reinterpret_cast<const uint4*>(box + o1)};
+      tmem_wait_ld();
+      uint4 ov[2];
+      const uint32_t* hw = reinterpret_cast<const uint32_t*>(hv);
+      uint32_t* ow = reinterpret_cast<uint32_t*>(ov);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[q]));
+        const float gx = hf.x > 0.f ? 1.f : hf.x + 1.f, gy = hf.y > 0.f ? 1.f : hf.y + 1.f;
+        ow[q] = pack_bf16(__uint_as_float(d[2 * q]) * gx, __uint_as_float(d[2 * q + 1]) * gy);
+      }
+      *reinterpret_cast<uint4*>(box + o0) = ov[0];
+      *reinterpret_cast<uint4*>(box + o1) = ov[1];
+    }
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();  // dZ complete in shared memory
+    tc_fence_after();
+    if (tid == 0) {
+#pragma unroll
+      for (int b = 0; b < N / 64; ++b) tma_store_2d(&mdz, b * 64, row0, sbase + kH + b * kBox);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (colsum && tid < N) {  // rows past m were zero-filled h -> their dZ rows are 0 * ... = finite, skipped
+      const uint8_t* box = smem + kH + (tid >> 6) * kBox;
+      const int64_t left = a.m - (int64_t)row0;
+      const int rows = left < kRows ? (int)left : kRows;
+      float t = 0.f;
+      for (int rr = 0; rr < rows; ++rr)
+        t += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(box + sw128_off(rr, tid & 63)));
+      csum += t;
+    }
+    __syncthreads();  // the column sums have read the tile before the next tile's h lands
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // dZ stores done
+  if (colsum && tid < N) atomicAdd(&colsum[tid], csum);
+  if (wgrad && tiles > blockIdx.x) {  // this CTA's dW^T -> dW[o][i] += (lane i, column o)
+    tc_fence_after();
+    constexpr int kHalf = MT == 1 && KP >= 32 ? KP / 2 : KP;  // MT = 1: warps 4-7 take the upper columns
+    const int mt = MT == 1 ? 0 : half, c0 = MT == 1 ? half * kHalf : 0;
+    const int i = mt * 128 + (warp & 3) * 32 + lane;
+    if (MT > 1 || KP >= 32 || half == 0) {
+#pragma unroll 2
+      for (int c = c0; c < c0 + kHalf; c += 16) {
+        float v[16];
+        tmem_ld16(trow + kWCol + mt * KP + c, v);
+        if (i < N) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c + q < a.k)
+              asm volatile("red.global.add.f32 [%0], %1;" ::"l"(wgrad + (int64_t)(c + q) * N + i), "f"(v[q])
+                           : "memory");
         }
       }
     }
@@ -1774,6 +1973,38 @@ static int launch_wgrad(const void* dy, const void* x, int64_t m, float* partial
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
 
+// 2-D bf16 row-major [rows x cols] map with 64-column x 128-row boxes, 128-byte swizzle
+static bool encode_rows128(CUtensorMap* map, const void* base, int cols, int64_t rows) {
+  const TensorMapEncodeFn enc = tensor_map_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N, int KP>
+static int launch_dgrad_tma(const sgp::DgradArgs& a, float* colsum, float* wgrad, cudaStream_t st) {
+  constexpr size_t kH = ((size_t)N * KP * 2 + (size_t)sgp::kRows * KP * 2 + 1023) / 1024 * 1024;
+  constexpr size_t smem = kH + (size_t)(N < 128 ? 2 : N / 64) * sgp::kRows * 128 + 64 + 1024;
+  static std::atomic<unsigned long long> done{0};
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_dgrad_tma_kernel<N, KP>), (int)smem, done))
+    return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+  CUtensorMap mh, mdz;
+  if (!encode_rows128(&mh, a.h, N, a.m) || !encode_rows128(&mdz, a.dz, N, a.m))
+    return fail(SG_ERR_SIM, "sg_policy_layer_backward: cuTensorMapEncodeTiled failed");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (a.m + sgp::kRows - 1) / sgp::kRows;
+  sgp::policy_dgrad_tma_kernel<N, KP><<<(unsigned)(tiles < sms ? tiles : sms), 256, smem, st>>>(mh, mdz, a, colsum, wgrad);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
 extern "C" {
 
 int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d_bf16_mirror, int64_t n,
@@ -2136,6 +2367,21 @@ int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const vo
   if (n_in == 128 && kp == 64) return launch_dgrad<128, 64>(a, st);
   if (n_in == 256 && kp == 128) return launch_dgrad<256, 128>(a, st);
   return fail(SG_ERR_CONFIG, "sg_policy_dgrad_elu: layer shape not instantiated (256/128/64 trunk)");
+}
+
+int sg_policy_layer_backward(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
+                             const void* d_h, void* d_dz, int64_t m, float* d_colsum, float* d_wgrad, void* stream) {
+  if (m <= 0) return SG_OK;
+  if (!d_dy || !d_wt_image || !d_h || !d_dz) return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: null argument");
+  const sgp::DgradArgs a{static_cast<const __nv_bfloat16*>(d_dy), dy_stride, k,
+                         static_cast<const uint8_t*>(d_wt_image), static_cast<const __nv_bfloat16*>(d_h),
+                         static_cast<__nv_bfloat16*>(d_dz), m};
+  const cudaStream_t st = (cudaStream_t)stream;
+  const int kp = (k + 15) / 16 * 16;
+  if (n_in == 64 && kp == 16) return launch_dgrad_tma<64, 16>(a, d_colsum, d_wgrad, st);
+  if (n_in == 128 && kp == 64) return launch_dgrad_tma<128, 64>(a, d_colsum, d_wgrad, st);
+  if (n_in == 256 && kp == 128) return launch_dgrad_tma<256, 128>(a, d_colsum, d_wgrad, st);
+  return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: layer shape not instantiated (256/128/64 trunk)");
 }
 
 int sg_policy_set_param_layout(sg_policy* p, const int64_t* w_off, const int64_t* b_off, const int32_t* in_dim,

@@ -227,7 +227,7 @@ class _FusedMLP(torch.autograd.Function):
                 # 256x32 23.7 vs 30.8 us, 128x256 26.7 vs 32.0, 64x128 19.4 vs
                 # 27.5 (TMA-fed), 8x64 18.7 vs 24.6; tools/wgrad_probe.py)
                 gw = tr.wgrad_partial is not None and direct is not None
-                if gw:  # dW = dY^T X on the tensor cores (per-CTA row slices + one sum)
+                if gw and not fused:  # dW = dY^T X on the tensor cores (per-CTA row slices + one sum)
                     sg.wgrad(g, ins[l], tr.wgrad_partial, W.grad)
                 lctx = _LayerCtx(needs_gx=l > 0 and not fused, direct=direct, w_dtype=W.dtype, gb_done=cs,
                                  gw_done=gw)
@@ -235,10 +235,9 @@ class _FusedMLP(torch.autograd.Function):
                 if lctx.direct is None:  # (only without the trainer-owned gradient views)
                     W.grad.add_(gW)
                     b.grad.add_(gb)
-                if fused:  # (dY W) * ELU'(h) in one tensor-core launch
-                    g = sg.dgrad_elu(g, tr.wt_images.image(t, l), ins[l].shape[1], ins[l])
-                    if cs:
-                        sg.elu_backward_colsum(None, g, tr.layers[4 * t + l - 1][1].grad, out=False)
+                if fused:  # dZ = (dY W) * ELU'(h), the next db and this dW in one launch
+                    g = sg.layer_backward(g, tr.wt_images.image(t, l), ins[l].shape[1], ins[l],
+                                          tr.layers[4 * t + l - 1][1].grad if cs else None, W.grad if gw else None)
                 elif l > 0 and cs:  # ELU' and the next-lower layer's db in one pass
                     g = sg.elu_backward_colsum(ins[l], gx.contiguous(), tr.layers[4 * t + l - 1][1].grad)
                 elif l > 0:
@@ -467,11 +466,13 @@ class Trainer:
         if cfg.fused_forward and cfg.update_precision == "bf16" and os.environ.get("SG_NO_FUSED_FWD") != "1":
             self.train_policy = sg.Policy(O, A, device=policy.device)
             self.train_policy.set_param_layout(layout, [_up8(O), 256, 128, 64])
-            # the fused backward (sg_policy_dgrad_elu) is parity-tested but
-            # measured slower than library GEMM + ELU pass (15.4 vs 14.5 ms per
-            # update: its per-row bf16 loads / stores of h and dz are poorly
-            # coalesced); opt in with SG_FUSED_BWD=1
-            if os.environ.get("SG_FUSED_BWD") == "1":
+            # the fused backward through the hidden layers: (dY W) * ELU'(h) and
+            # the next layer's bias sums in one tensor-core launch with h / dZ
+            # moved by TMA (sg_policy_dgrad_elu_colsum): 39.5 / 22.8 / 16.5 us
+            # vs 61.2 / 31.5 / 24.0 for library GEMM + ELU pass at m = 131072
+            # (tools/dgrad_probe.py); update 11.41 -> 10.28 ms. SG_NO_FUSED_BWD=1
+            # for the library path
+            if os.environ.get("SG_NO_FUSED_BWD") != "1":
                 self.wt_images = sg.WtImages(layout, dev)
             if os.environ.get("SG_NO_WGRAD") != "1":
                 self.wgrad_partial = torch.empty(148 * 128 * 256, device=dev)

@@ -158,6 +158,8 @@ _SIGS = {
     "sg_policy_pack_wt": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_policy_dgrad_elu": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                                       C.c_void_p, C.c_int64, C.c_void_p]),
+    "sg_policy_layer_backward": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                           C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sg_elu_backward_colsum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
                                          C.c_void_p]),
     "sg_policy_wgrad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_int32,
@@ -762,6 +764,23 @@ def dgrad_elu(dy, wt_ptr: int, n_in: int, h, out=None):
     stream = torch.cuda.current_stream(dy.device).cuda_stream
     _pcheck(lib().sg_policy_dgrad_elu(dy.data_ptr(), dy.stride(0), k, wt_ptr, n_in, h.data_ptr(), out.data_ptr(), m,
                                       stream))
+    return out
+
+
+def layer_backward(dy, wt_ptr: int, n_in: int, h, colsum=None, wgrad=None, out=None):
+    """sg_policy_layer_backward: returns dz = (dy W) * ELU'(h); colsum (fp32
+    [n_in], or None) += the column sums of dz; wgrad (fp32 [k x n_in], or
+    None) += dy^T h. One launch, h / dz moved by TMA."""
+    import torch
+    m, k = dy.shape
+    out = torch.empty((m, n_in), dtype=torch.bfloat16, device=dy.device) if out is None else out
+    if wgrad is not None:
+        assert wgrad.is_contiguous() and wgrad.dtype == torch.float32 and wgrad.shape[1] == n_in
+        assert wgrad.shape[0] >= k
+    stream = torch.cuda.current_stream(dy.device).cuda_stream
+    _pcheck(lib().sg_policy_layer_backward(dy.data_ptr(), dy.stride(0), k, wt_ptr, n_in, h.data_ptr(),
+                                           out.data_ptr(), m, colsum.data_ptr() if colsum is not None else None,
+                                           wgrad.data_ptr() if wgrad is not None else None, stream))
     return out
 
 

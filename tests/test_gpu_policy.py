@@ -222,6 +222,50 @@ def test_fused_update_forward_matches_library_gradients(sg):
     assert all(np.isfinite(h[k]) for k in ("policy_loss", "value_loss", "kl"))
 
 
+@pytest.mark.parametrize("n_in,k,m", [(256, 128, 131072), (256, 128, 300), (128, 64, 1000), (64, 8, 129),
+                                       (64, 8, 100000), (128, 64, 5)])
+def test_layer_backward_matches_reference(sg, n_in, k, m):
+    """sg_policy_layer_backward (dZ, the next layer's db and this layer's dW in
+    one launch): dZ as in sg_policy_dgrad_elu, ragged tails included (rows
+    past m neither read nor written: a guard row after the output stays
+    untouched); colsum += the column sums of the bf16 dZ it wrote; wgrad +=
+    dY^T h against fp64 of the same bf16 operands (fp32 accumulation over
+    the rows: relative 1e-3 of the row-norm product)."""
+    from paper_2310_04676_b200 import ppo
+    torch.manual_seed(11)
+    layout, ls_pad, total, _ = ppo.padded_layout(27, 7)
+    flat = torch.randn(total, device="cuda") * 0.1
+    imgs = sg.WtImages(layout, 0)
+    imgs.pack(flat)
+    l = {256: 1, 128: 2, 64: 3}[n_in]
+    (w0, o, i), _ = layout[l]
+    W = flat[w0: w0 + o * i].view(o, i).to(torch.bfloat16).float()
+    dy = (torch.randn(m, k, device="cuda") * 0.5).to(torch.bfloat16)
+    h = torch.where(torch.rand(m, n_in, device="cuda") < 0.5, torch.rand(m, n_in, device="cuda"),
+                    -torch.rand(m, n_in, device="cuda")).to(torch.bfloat16)
+    buf = torch.full((m + 1, n_in), 7.0, device="cuda", dtype=torch.bfloat16)
+    colsum = torch.full((n_in,), 0.5, device="cuda")
+    wg = torch.full((k + 1, n_in), 0.25, device="cuda")  # + a guard row
+    dz = sg.layer_backward(dy, imgs.image(0, l), n_in, h, colsum, wg[:k], out=buf[:m])
+    torch.cuda.synchronize()
+    assert torch.all(buf[m] == 7.0)
+    hf = h.float()
+    ref = (dy.float() @ W) * torch.where(hf > 0, torch.ones_like(hf), hf + 1)
+    err = (dz.float() - ref).abs()
+    assert torch.all(err <= 8e-3 * ref.abs() + 1e-4 * ref.abs().max()), err.max().item()
+    cs_ref = dz.double().sum(0) + 0.5
+    assert torch.allclose(colsum.double(), cs_ref, rtol=1e-4, atol=1e-3 * (1 + m ** 0.5) * 1e-2)
+    wg_ref = dy.double().t() @ h.double() + 0.25
+    scale = dy.double().norm(dim=0)[:, None] * h.double().norm(dim=0)[None, :]
+    assert torch.all((wg[:k].double() - wg_ref).abs() <= 1e-3 * scale + 1e-5), \
+        ((wg[:k].double() - wg_ref).abs() / scale).max().item()
+    assert torch.all(wg[k] == 0.25)
+    # without colsum / wgrad: the same dZ
+    dz2 = sg.layer_backward(dy, imgs.image(0, l), n_in, h)
+    torch.cuda.synchronize()
+    assert torch.equal(dz2, dz)
+
+
 @pytest.mark.parametrize("n_in,k,m", [(256, 128, 131072), (128, 64, 1000), (64, 8, 129)])
 def test_dgrad_elu_matches_reference(sg, n_in, k, m):
     """sg_policy_dgrad_elu (backward through a hidden layer: (dY W) * ELU'(h),
