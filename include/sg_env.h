@@ -383,9 +383,13 @@ int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const vo
  * d_colsum[n_in] (fp32) += the column sums of d_dz (the bias gradient of
  * layer l-1) and d_wgrad[k x n_in] (fp32, row-major) += d_dy^T d_h (the
  * weight gradient of layer l; d_h is layer l's input). d_h / d_dz move
- * through TMA (16-byte aligned, row stride n_in). */
+ * through TMA (16-byte aligned, row stride n_in). With d_x0 (bf16 [m x 32],
+ * the input of layer l-1 = the 256-wide first layer's input, only for
+ * n_in = 256), d_wgrad0[256 x 32] (fp32) += d_dz^T d_x0 as well -- the
+ * first layer's weight gradient -- and d_dz (may be NULL) is not written. */
 int sg_policy_layer_backward(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
-                             const void* d_h, void* d_dz, int64_t m, float* d_colsum, float* d_wgrad, void* stream);
+                             const void* d_h, void* d_dz, int64_t m, float* d_colsum, float* d_wgrad,
+                             const void* d_x0, int32_t x0_width, float* d_wgrad0, void* stream);
 /* Flat-parameter layout sg_policy_load_params packs from: per (trunk, layer)
  * (actor layers 0..3 then critic) the offsets of W [out x in] row-major and
  * of b, the row stride in_dim[layer] and the row count out_dim[trunk*4 + l]

@@ -1405,33 +1405,54 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
                : "memory");
 }
 
-template <int N, int KP>
+//
+// L0 (the 256-wide layer 1 only): the input layer's weight gradient too --
+// dW_0 += dZ_0^T x_0 with dZ_0 read back from the boxes it was written into
+// (MN-major SWIZZLE_128B) and the tile's x_0 (obs, 32 columns) as one more
+// TMA box (SWIZZLE_64B) -- so dZ_0 never goes to HBM. TMEM then holds
+// dW_1^T (256 columns) and dW_0 (64) besides the per-tile accumulator,
+// which shrinks to 128 columns: the tile's two column halves of dY W run
+// one after the other.
+template <int N, int KP, bool L0>
 __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_constant__ CUtensorMap mh,
                                                                   const __grid_constant__ CUtensorMap mdz,
+                                                                  const __grid_constant__ CUtensorMap mx0,
                                                                   const __grid_constant__ DgradArgs a,
                                                                   float* __restrict__ colsum,
-                                                                  float* __restrict__ wgrad) {
+                                                                  float* __restrict__ wgrad,
+                                                                  float* __restrict__ wgrad0) {
+  static_assert(!L0 || N == 256, "L0: the 256-wide first hidden layer");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   constexpr uint32_t kBBytes = N * KP * 2, kABytes = kRows * KP * 2, kBox = kRows * 128;
   constexpr int MT = N < 128 ? 1 : N / 128;  // MMA 2 row blocks (N = 64 reads a 2nd, ignored box)
   constexpr uint32_t kHBoxes = N < 128 ? 2 : N / 64;
-  constexpr uint32_t kA = kBBytes, kH = (kA + kABytes + 1023) / 1024 * 1024, kBarOff = kH + kHBoxes * kBox;
+  constexpr uint32_t kA = kBBytes, kH = (kA + kABytes + 1023) / 1024 * 1024, kX0 = kH + kHBoxes * kBox;
+  constexpr uint32_t kX0Bytes = L0 ? kRows * 64 : 0, kBarOff = kX0 + kX0Bytes;
   constexpr int kChunks = kRows * KP / 8 / 256;
-  constexpr uint32_t kWCol = N;  // dW^T accumulator columns [N, N + MT * KP)
-  constexpr uint32_t kCols = N + MT * KP <= 128 ? 128 : (N + MT * KP <= 256 ? 256 : 512);
+  constexpr int kSc = L0 ? 128 : N, kRounds = N / kSc;  // per-tile accumulator columns, column rounds
+  constexpr uint32_t kWCol = kSc;                         // dW^T accumulator columns [kSc, kSc + MT * KP)
+  constexpr uint32_t kW0Col = kSc + MT * KP;              // L0: dW_0 [256 x 32] as 2 x 32 columns
+  constexpr uint32_t kUsed = kW0Col + (L0 ? 64 : 0);
+  constexpr uint32_t kCols = kUsed <= 128 ? 128 : (kUsed <= 256 ? 256 : 512);
+  static_assert(kUsed <= 512, "TMEM columns");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);  // B, MMA, H
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);  // B, MMA, H, L0
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kBarOff + 32);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_b = smem_u32(&bars[0]), bar_mma = smem_u32(&bars[1]), bar_h = smem_u32(&bars[2]);
+  const uint32_t bar_l0 = smem_u32(&bars[3]);
   if (tid == 0) {
     mbar_init(bar_b, 1);
     mbar_init(bar_mma, 1);
     mbar_init(bar_h, 1);
+    mbar_init(bar_l0, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mh)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mdz)) : "memory");
+    if (L0)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mx0)) : "memory");
+    else
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mdz)) : "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(kCols));
@@ -1458,17 +1479,24 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
   };
   uint4 nxt[kChunks];
   load_a(blockIdx.x, nxt);
-  uint32_t ph = 0;
+  uint32_t ph = 0, pm = 0;
+  int it = 0;
   bool first = true;
   float csum = 0.f;  // column tid's sum of dZ over this CTA's tiles
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
     const int row0 = (int)(tile * kRows);
-    if (tid == 0) {  // this tile's h boxes (the previous tile's dZ stores have read the buffer)
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_h), "r"((N / 64) * kBox)
+    if (tid == 0) {  // this tile's h boxes (the previous tile's dZ stores / dW_0 MMAs have read the buffers)
+      if constexpr (L0) {
+        if (it > 0) mbar_wait(bar_l0, (uint32_t)(it - 1) & 1u);
+      } else {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_h),
+                   "r"((N / 64) * kBox + kX0Bytes)
                    : "memory");
 #pragma unroll
       for (int b = 0; b < N / 64; ++b) tma_load_2d(sbase + kH + b * kBox, &mh, b * 64, row0, bar_h);
+      if constexpr (L0) tma_load_2d(sbase + kX0, &mx0, 0, row0, bar_h);
     }
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) {
@@ -1483,7 +1511,7 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
     if (tid == 0) {
       if (first) mbar_wait(bar_b, 0);
       tc_fence_after();
-      issue_layer(tmem, sbase + kA, kRows, sbase, N, KP, N);
+      issue_layer(tmem, sbase + kA, kRows, sbase, N, KP, kSc);  // (L0: the first column half)
       if (wgrad) {  // dW^T += h^T dY, once this tile's h boxes have landed
         mbar_wait(bar_h, ph);
         tc_fence_after();
@@ -1498,17 +1526,31 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
       mma_commit(bar_mma);
     }
     first = false;
-    mbar_wait(bar_mma, ph);
+    mbar_wait(bar_mma, pm);
+    pm ^= 1;
     mbar_wait(bar_h, ph);
     ph ^= 1;
     tc_fence_after();
     const uint32_t r = (uint32_t)((warp & 3) * 32 + lane);
 #pragma unroll
-    for (int cb = 0; cb < N / 2; cb += 16) {  // this half's columns, 16 at a time
-      const int c = half * (N / 2) + cb;
+    for (int round = 0; round < kRounds; ++round) {
+    if (round > 0) {  // L0: the second column half into the same accumulator columns
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        issue_layer(tmem, sbase + kA, kRows, sbase + round * (kSc / 8) * 128, N, KP, kSc);
+        mma_commit(bar_mma);
+      }
+      mbar_wait(bar_mma, pm);
+      pm ^= 1;
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int cb = 0; cb < kSc / 2; cb += 16) {  // this warp half's columns, 16 at a time
+      const int c = round * kSc + half * (kSc / 2) + cb;
       uint32_t d[16];
-      tmem_ld16_async(trow + c, d);
-      uint8_t* box = smem + kH + (c >> 6) * kBox;
+      tmem_ld16_async(trow + (c - round * kSc), d);      uint8_t* box = smem + kH + (c >> 6) * kBox;
       const uint32_t o0 = sw128_off(r, c & 63), o1 = sw128_off(r, (c & 63) + 8);
       uint4 hv[2] = {*reinterpret_cast<const uint4*>(box + o0), *reinterpret_cast<const uint4*>(box + o1)};
       tmem_wait_ld();
@@ -1524,14 +1566,26 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
       *reinterpret_cast<uint4*>(box + o0) = ov[0];
       *reinterpret_cast<uint4*>(box + o1) = ov[1];
     }
+    }
     async_proxy_fence();
     tc_fence_before();
     __syncthreads();  // dZ complete in shared memory
     tc_fence_after();
     if (tid == 0) {
+      if constexpr (L0) {  // dW_0 [256 x 32] += dZ_0^T x_0: A = dZ_0^T (MN-major SW128), B = x_0^T (MN-major SW64)
 #pragma unroll
-      for (int b = 0; b < N / 64; ++b) tma_store_2d(&mdz, b * 64, row0, sbase + kH + b * kBox);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int ks = 0; ks < kRows / 16; ++ks)
+            mma_bf16(tmem + kW0Col + mt * 32, make_desc_sw(sbase + kH + mt * 2 * kBox + ks * 2048, kBox, 1024, 2),
+                     make_desc_sw(sbase + kX0 + ks * 1024, 8192, 512, 4), make_idesc_mn(128, 32),
+                     (it > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(bar_l0);
+      } else {
+#pragma unroll
+        for (int b = 0; b < N / 64; ++b) tma_store_2d(&mdz, b * 64, row0, sbase + kH + b * kBox);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
     }
     if (colsum && tid < N) {  // rows past m were zero-filled h -> their dZ rows are 0 * ... = finite, skipped
       const uint8_t* box = smem + kH + (tid >> 6) * kBox;
@@ -1546,6 +1600,24 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // dZ stores done
   if (colsum && tid < N) atomicAdd(&colsum[tid], csum);
+  if constexpr (L0) {
+    if (it > 0) {  // this CTA's dW_0: lane = output row, 32 input columns -> vector reductions
+      mbar_wait(bar_l0, (uint32_t)(it - 1) & 1u);
+      tc_fence_after();
+      const int o = half * 128 + (warp & 3) * 32 + lane;
+#pragma unroll
+      for (int c = 0; c < 32; c += 16) {
+        float v[16];
+        tmem_ld16(trow + kW0Col + half * 32 + c, v);
+        float* row = wgrad0 + (int64_t)o * 32 + c;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * q), "f"(v[4 * q]),
+                       "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                       : "memory");
+      }
+    }
+  }
   if (wgrad && tiles > blockIdx.x) {  // this CTA's dW^T -> dW[o][i] += (lane i, column o)
     tc_fence_after();
     constexpr int kHalf = MT == 1 && KP >= 32 ? KP / 2 : KP;  // MT = 1: warps 4-7 take the upper columns
@@ -1986,21 +2058,39 @@ static bool encode_rows128(CUtensorMap* map, const void* base, int cols, int64_t
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N, int KP>
-static int launch_dgrad_tma(const sgp::DgradArgs& a, float* colsum, float* wgrad, cudaStream_t st) {
+template <int N, int KP, bool L0>
+static int launch_dgrad_tma(const sgp::DgradArgs& a, float* colsum, float* wgrad, const void* x0, float* wgrad0,
+                            cudaStream_t st) {
   constexpr size_t kH = ((size_t)N * KP * 2 + (size_t)sgp::kRows * KP * 2 + 1023) / 1024 * 1024;
-  constexpr size_t smem = kH + (size_t)(N < 128 ? 2 : N / 64) * sgp::kRows * 128 + 64 + 1024;
+  constexpr size_t smem = kH + (size_t)(N < 128 ? 2 : N / 64) * sgp::kRows * 128 + (L0 ? sgp::kRows * 64 : 0) + 64 +
+                          1024;
   static std::atomic<unsigned long long> done{0};
-  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_dgrad_tma_kernel<N, KP>), (int)smem, done))
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_dgrad_tma_kernel<N, KP, L0>), (int)smem, done))
     return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
-  CUtensorMap mh, mdz;
-  if (!encode_rows128(&mh, a.h, N, a.m) || !encode_rows128(&mdz, a.dz, N, a.m))
-    return fail(SG_ERR_SIM, "sg_policy_layer_backward: cuTensorMapEncodeTiled failed");
+  CUtensorMap mh, mdz, mx0;
+  bool ok = encode_rows128(&mh, a.h, N, a.m);
+  if (L0) {  // x_0: [m x 32] bf16, one 32-column x 128-row box, 64-byte swizzle
+    const TensorMapEncodeFn enc = tensor_map_encode();
+    const cuuint64_t dims[2] = {32, (cuuint64_t)a.m};
+    const cuuint64_t strides[1] = {64};
+    const cuuint32_t box[2] = {32, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    ok = ok && enc &&
+         enc(&mx0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x0), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    mdz = mh;
+  } else {
+    ok = ok && encode_rows128(&mdz, a.dz, N, a.m);
+    mx0 = mh;
+  }
+  if (!ok) return fail(SG_ERR_SIM, "sg_policy_layer_backward: cuTensorMapEncodeTiled failed");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (a.m + sgp::kRows - 1) / sgp::kRows;
-  sgp::policy_dgrad_tma_kernel<N, KP><<<(unsigned)(tiles < sms ? tiles : sms), 256, smem, st>>>(mh, mdz, a, colsum, wgrad);
+  sgp::policy_dgrad_tma_kernel<N, KP, L0>
+      <<<(unsigned)(tiles < sms ? tiles : sms), 256, smem, st>>>(mh, mdz, mx0, a, colsum, wgrad, wgrad0);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
@@ -2370,17 +2460,26 @@ int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const vo
 }
 
 int sg_policy_layer_backward(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
-                             const void* d_h, void* d_dz, int64_t m, float* d_colsum, float* d_wgrad, void* stream) {
+                             const void* d_h, void* d_dz, int64_t m, float* d_colsum, float* d_wgrad,
+                             const void* d_x0, int32_t x0_width, float* d_wgrad0, void* stream) {
   if (m <= 0) return SG_OK;
-  if (!d_dy || !d_wt_image || !d_h || !d_dz) return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: null argument");
+  if (!d_dy || !d_wt_image || !d_h) return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: null argument");
+  if (d_x0) {
+    if (n_in != 256 || (k + 15) / 16 * 16 != 128 || x0_width != 32 || !d_wgrad0)
+      return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: x0 needs the 256-wide layer, x0_width 32 and d_wgrad0");
+  } else if (!d_dz) {
+    return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: null d_dz");
+  }
   const sgp::DgradArgs a{static_cast<const __nv_bfloat16*>(d_dy), dy_stride, k,
                          static_cast<const uint8_t*>(d_wt_image), static_cast<const __nv_bfloat16*>(d_h),
                          static_cast<__nv_bfloat16*>(d_dz), m};
   const cudaStream_t st = (cudaStream_t)stream;
   const int kp = (k + 15) / 16 * 16;
-  if (n_in == 64 && kp == 16) return launch_dgrad_tma<64, 16>(a, d_colsum, d_wgrad, st);
-  if (n_in == 128 && kp == 64) return launch_dgrad_tma<128, 64>(a, d_colsum, d_wgrad, st);
-  if (n_in == 256 && kp == 128) return launch_dgrad_tma<256, 128>(a, d_colsum, d_wgrad, st);
+  if (n_in == 64 && kp == 16) return launch_dgrad_tma<64, 16, false>(a, d_colsum, d_wgrad, nullptr, nullptr, st);
+  if (n_in == 128 && kp == 64) return launch_dgrad_tma<128, 64, false>(a, d_colsum, d_wgrad, nullptr, nullptr, st);
+  if (n_in == 256 && kp == 128)
+    return d_x0 ? launch_dgrad_tma<256, 128, true>(a, d_colsum, d_wgrad, d_x0, d_wgrad0, st)
+                : launch_dgrad_tma<256, 128, false>(a, d_colsum, d_wgrad, nullptr, nullptr, st);
   return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: layer shape not instantiated (256/128/64 trunk)");
 }
 

@@ -216,7 +216,10 @@ class _FusedMLP(torch.autograd.Function):
         for t, gy in ((0, g_mean), (1, g_value)):
             ins = (obs, h1[t], h2[t], h3[t])
             g = gy.contiguous().to(torch.bfloat16)
+            l0_done = False
             for l in (3, 2, 1, 0):
+                if l0_done:  # (dW_0 and db_0 came with layer 1's backward)
+                    break
                 W, b, Wm, _ = tr.layers[4 * t + l]
                 direct = _direct_grads(W, b)
                 cs = colsum and direct is not None
@@ -236,8 +239,13 @@ class _FusedMLP(torch.autograd.Function):
                     W.grad.add_(gW)
                     b.grad.add_(gb)
                 if fused:  # dZ = (dY W) * ELU'(h), the next db and this dW in one launch
+                    W0 = tr.layers[4 * t][0]
+                    l0 = (l == 1 and cs and gw and tr.fuse_l0 and obs.dtype == torch.bfloat16 and obs.shape[1] == 32
+                          and obs.is_contiguous() and _direct_grads(W0, tr.layers[4 * t][1]) is not None)
                     g = sg.layer_backward(g, tr.wt_images.image(t, l), ins[l].shape[1], ins[l],
-                                          tr.layers[4 * t + l - 1][1].grad if cs else None, W.grad if gw else None)
+                                          tr.layers[4 * t + l - 1][1].grad if cs else None, W.grad if gw else None,
+                                          x0=obs if l0 else None, wgrad0=W0.grad if l0 else None)
+                    l0_done = l0
                 elif l > 0 and cs:  # ELU' and the next-lower layer's db in one pass
                     g = sg.elu_backward_colsum(ins[l], gx.contiguous(), tr.layers[4 * t + l - 1][1].grad)
                 elif l > 0:
@@ -456,6 +464,7 @@ class Trainer:
         # the fused minibatch forward packs its weights from the padded copy
         self.train_policy = None
         self.wt_images = None
+        self.fuse_l0 = False
         # bias gradients from column-sum passes (fused into the ELU backward)
         # instead of M = 1 split-K GEMMs; SG_NO_COLSUM_BIAS=1 for the GEMMs
         self.colsum_bias = os.environ.get("SG_NO_COLSUM_BIAS") != "1"
@@ -474,6 +483,10 @@ class Trainer:
             # for the library path
             if os.environ.get("SG_NO_FUSED_BWD") != "1":
                 self.wt_images = sg.WtImages(layout, dev)
+            # layer 1's backward also takes the first layer's weight gradient
+            # from the dZ_0 tile it holds (dZ_0 never written); SG_NO_FUSE_L0=1
+            # for a separate sg_policy_wgrad over a written dZ_0
+            self.fuse_l0 = os.environ.get("SG_NO_FUSE_L0") != "1"
             if os.environ.get("SG_NO_WGRAD") != "1":
                 self.wgrad_partial = torch.empty(148 * 128 * 256, device=dev)
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]

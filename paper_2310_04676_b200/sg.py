@@ -159,7 +159,8 @@ _SIGS = {
     "sg_policy_dgrad_elu": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                                       C.c_void_p, C.c_int64, C.c_void_p]),
     "sg_policy_layer_backward": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
-                                           C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                           C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                           C.c_void_p, C.c_void_p]),
     "sg_elu_backward_colsum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
                                          C.c_void_p]),
     "sg_policy_wgrad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_int32,
@@ -767,20 +768,30 @@ def dgrad_elu(dy, wt_ptr: int, n_in: int, h, out=None):
     return out
 
 
-def layer_backward(dy, wt_ptr: int, n_in: int, h, colsum=None, wgrad=None, out=None):
+def layer_backward(dy, wt_ptr: int, n_in: int, h, colsum=None, wgrad=None, out=None, x0=None, wgrad0=None):
     """sg_policy_layer_backward: returns dz = (dy W) * ELU'(h); colsum (fp32
     [n_in], or None) += the column sums of dz; wgrad (fp32 [k x n_in], or
-    None) += dy^T h. One launch, h / dz moved by TMA."""
+    None) += dy^T h. With x0 (bf16 [m x 32], the 256-wide layer only):
+    wgrad0 (fp32 [256 x 32]) += dz^T x0 too and dz is not written (returns
+    None). One launch, h / dz / x0 moved by TMA."""
     import torch
     m, k = dy.shape
-    out = torch.empty((m, n_in), dtype=torch.bfloat16, device=dy.device) if out is None else out
+    if x0 is None:
+        out = torch.empty((m, n_in), dtype=torch.bfloat16, device=dy.device) if out is None else out
+    else:
+        assert x0.is_contiguous() and x0.dtype == torch.bfloat16 and tuple(x0.shape) == (m, 32)
+        assert wgrad0.is_contiguous() and wgrad0.dtype == torch.float32 and tuple(wgrad0.shape) == (256, 32)
+        out = None
     if wgrad is not None:
         assert wgrad.is_contiguous() and wgrad.dtype == torch.float32 and wgrad.shape[1] == n_in
         assert wgrad.shape[0] >= k
     stream = torch.cuda.current_stream(dy.device).cuda_stream
     _pcheck(lib().sg_policy_layer_backward(dy.data_ptr(), dy.stride(0), k, wt_ptr, n_in, h.data_ptr(),
-                                           out.data_ptr(), m, colsum.data_ptr() if colsum is not None else None,
-                                           wgrad.data_ptr() if wgrad is not None else None, stream))
+                                           out.data_ptr() if out is not None else None, m,
+                                           colsum.data_ptr() if colsum is not None else None,
+                                           wgrad.data_ptr() if wgrad is not None else None,
+                                           x0.data_ptr() if x0 is not None else None, 32,
+                                           wgrad0.data_ptr() if wgrad0 is not None else None, stream))
     return out
 
 

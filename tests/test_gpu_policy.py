@@ -266,6 +266,37 @@ def test_layer_backward_matches_reference(sg, n_in, k, m):
     assert torch.equal(dz2, dz)
 
 
+@pytest.mark.parametrize("m", [131072, 300, 5])
+def test_layer_backward_first_layer_weight_gradient(sg, m):
+    """sg_policy_layer_backward with x0 (the 256-wide layer): the first
+    layer's weight gradient dW_0 += dZ_0^T x0 from the dZ_0 tiles it keeps
+    (fp64 of the kernel's own bf16 dZ_0, recomputed by the dZ-writing
+    variant, within 1e-3 of the row-norm product), db_0 and dW_1 as without
+    x0, and no dZ written."""
+    from paper_2310_04676_b200 import ppo
+    torch.manual_seed(13)
+    layout, ls_pad, total, _ = ppo.padded_layout(27, 7)
+    flat = torch.randn(total, device="cuda") * 0.1
+    imgs = sg.WtImages(layout, 0)
+    imgs.pack(flat)
+    dy = (torch.randn(m, 128, device="cuda") * 0.5).to(torch.bfloat16)
+    h = torch.where(torch.rand(m, 256, device="cuda") < 0.5, torch.rand(m, 256, device="cuda"),
+                    -torch.rand(m, 256, device="cuda")).to(torch.bfloat16)
+    x0 = torch.randn(m, 32, device="cuda").to(torch.bfloat16)
+    cs_a, cs_b = torch.zeros(256, device="cuda"), torch.zeros(256, device="cuda")
+    wg_a, wg_b = torch.zeros(128, 256, device="cuda"), torch.zeros(128, 256, device="cuda")
+    wg0 = torch.full((256, 32), 0.5, device="cuda")
+    dz = sg.layer_backward(dy, imgs.image(0, 1), 256, h, cs_a, wg_a)
+    assert sg.layer_backward(dy, imgs.image(0, 1), 256, h, cs_b, wg_b, x0=x0, wgrad0=wg0) is None
+    torch.cuda.synchronize()
+    assert torch.allclose(cs_a, cs_b, rtol=1e-5, atol=1e-4)
+    assert torch.allclose(wg_a, wg_b, rtol=1e-5, atol=1e-4)
+    ref = dz.double().t() @ x0.double() + 0.5
+    scale = dz.double().norm(dim=0)[:, None] * x0.double().norm(dim=0)[None, :]
+    assert torch.all((wg0.double() - ref).abs() <= 1e-3 * scale + 1e-5), \
+        ((wg0.double() - ref).abs() / scale).max().item()
+
+
 @pytest.mark.parametrize("n_in,k,m", [(256, 128, 131072), (128, 64, 1000), (64, 8, 129)])
 def test_dgrad_elu_matches_reference(sg, n_in, k, m):
     """sg_policy_dgrad_elu (backward through a hidden layer: (dY W) * ELU'(h),
