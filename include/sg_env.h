@@ -390,6 +390,17 @@ int sg_policy_dgrad_elu(const void* d_dy, int32_t dy_stride, int32_t k, const vo
 int sg_policy_layer_backward(const void* d_dy, int32_t dy_stride, int32_t k, const void* d_wt_image, int32_t n_in,
                              const void* d_h, void* d_dz, int64_t m, float* d_colsum, float* d_wgrad,
                              const void* d_x0, int32_t x0_width, float* d_wgrad0, void* stream);
+/* The last two layers of one trunk's update backward (Policy::backward,
+ * policy.cpp:163-218) in one launch: with dY_3 = d_dy3 (bf16 [m x k3], k3 <=
+ * 8, row stride dy3_stride), h_3 / h_2 the stored outputs (bf16 [m x 64] /
+ * [m x 128]) and the sg_policy_pack_wt images of W_3 (64 x 16) and W_2
+ * (128 x 64): d_db3 += 1^T dY_3, d_dw3 [k3 x 64] += dY_3^T h_3, dZ_2 =
+ * (dY_3 W_3) * ELU'(h_3) (kept on chip), d_db2 += 1^T dZ_2, d_dw2 [64 x 128]
+ * += dZ_2^T h_2, d_dz1 [m x 128] = (dZ_2 W_2) * ELU'(h_2) (written) and
+ * d_db1 += 1^T dZ_1. All fp32 gradients accumulate. */
+int sg_policy_backward_tail(const void* d_dy3, int32_t dy3_stride, int32_t k3, const void* d_wt3_image,
+                            const void* d_wt2_image, const void* d_h3, const void* d_h2, void* d_dz1, int64_t m,
+                            float* d_db3, float* d_dw3, float* d_db2, float* d_dw2, float* d_db1, void* stream);
 /* Flat-parameter layout sg_policy_load_params packs from: per (trunk, layer)
  * (actor layers 0..3 then critic) the offsets of W [out x in] row-major and
  * of b, the row stride in_dim[layer] and the row count out_dim[trunk*4 + l]

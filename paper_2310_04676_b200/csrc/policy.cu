@@ -1646,6 +1646,257 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
   }
 }
 
+// The update backward's tail -- the last two layers of one trunk -- in one
+// launch (Policy::backward, policy.cpp:163-218), per 128-row tile:
+//   db_3 += 1^T dY_3                          (per-thread row sums, no reduction per tile)
+//   dZ_2  = (dY_3 W_3) * ELU'(h_3)            (MMA: A = dY_3 tile, B = W_3^T image)
+//   dW_3^T += h_3^T dY_3                      (MMA, TMEM-resident over the CTA's tiles)
+//   dZ_1  = (dZ_2 W_2) * ELU'(h_2)            (MMA: A = dZ_2 read back as K-major SWIZZLE_128B)
+//   dW_2^T += h_2^T dZ_2                      (MMA: B = dZ_2 read back as MN-major SWIZZLE_128B)
+//   db_2 += 1^T dZ_2, db_1 += 1^T dZ_1        (column sums from shared memory)
+// dZ_2 is written in place into the h_3 box it was computed from -- a
+// 128-row x 64-column box with 128-byte rows is both the K-major and the
+// MN-major SWIZZLE_128B canonical layout, so it feeds the next layer's data
+// gradient (A, K steps of 32 bytes) and this layer's weight gradient (B)
+// without a copy -- and dZ_1 likewise into the h_2 boxes, which one thread
+// stores with TMA; dZ_2 never reaches HBM. 71 KB of shared memory and 256
+// TMEM columns: two CTAs per SM overlap one tile's MMAs with the other's
+// epilogue. TMEM: [0, 128) the tile's accumulator (dY_3 W_3 in [0, 64),
+// then dZ_2 W_2), [128, 144) dW_3^T, [144, 208) dW_2^T.
+struct TailArgs {
+  const __nv_bfloat16* dy;  // dY_3 [m x k3], row stride dy_stride
+  int32_t dy_stride;
+  int32_t k3;               // valid dY_3 columns (<= 16)
+  const uint8_t* wt3;       // W_3^T image [64 x 16]
+  const uint8_t* wt2;       // W_2^T image [128 x 64]
+  int64_t m;
+  float* db3;               // [k3]
+  float* dw3;               // [k3 x 64]
+  float* db2;               // [64]
+  float* dw2;               // [64 x 128]
+  float* db1;               // [128]
+};
+
+__global__ void __launch_bounds__(256, 2) policy_bwd_tail_kernel(const __grid_constant__ CUtensorMap mh3,
+                                                                 const __grid_constant__ CUtensorMap mh2,
+                                                                 const __grid_constant__ CUtensorMap mdz1,
+                                                                 const __grid_constant__ TailArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  constexpr uint32_t kBox = kRows * 128;
+  constexpr uint32_t kW3 = 0, kW2 = 64 * 16 * 2, kA = kW2 + 128 * 64 * 2, kH3 = (kA + kRows * 16 * 2 + 1023) / 1024 * 1024;
+  constexpr uint32_t kH2 = kH3 + kBox, kBarOff = kH2 + 2 * kBox;
+  constexpr uint32_t kDW3 = 128, kDW2 = 144, kCols = 256;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, half = warp >> 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);  // W, MMA, H3, H2
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kBarOff + 32);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_w = smem_u32(&bars[0]), bar_mma = smem_u32(&bars[1]), bar_h3 = smem_u32(&bars[2]),
+                 bar_h2 = smem_u32(&bars[3]);
+  if (tid == 0) {
+    mbar_init(bar_w, 1);
+    mbar_init(bar_mma, 1);
+    mbar_init(bar_h3, 1);
+    mbar_init(bar_h2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mh3)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mh2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mdz1)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_w), "r"(kA) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sbase + kW3),
+                 "l"(a.wt3), "r"(kW2), "r"(bar_w)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sbase + kW2),
+                 "l"(a.wt2), "r"(kA - kW2), "r"(bar_w)
+                 : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t r = (uint32_t)((warp & 3) * 32 + lane);
+  const int64_t tiles = (a.m + kRows - 1) / kRows;
+  const auto load_a = [&](int64_t tile) {  // one 16-byte piece per thread: row tid % 128, columns 8 (tid / 128) ..
+    const int row = tid % kRows, kc = tid / kRows;
+    const int64_t rr = tile * kRows + row;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (tile < tiles && rr < a.m && kc * 8 < a.k3) v = *reinterpret_cast<const uint4*>(a.dy + rr * a.dy_stride + kc * 8);
+    return v;
+  };
+  uint4 nxt = load_a(blockIdx.x);
+  uint32_t pm = 0, ph = 0;
+  int it = 0;
+  float cs3[8] = {}, cs2 = 0.f, cs1 = 0.f;
+  // ELU'(h) * acc for 16 accumulator columns of row r, in place in a 128 x 64 SW128 box
+  const auto elu_bwd16 = [&](uint8_t* box, int c, const uint32_t (&d)[16]) {
+    const uint32_t o0 = sw128_off(r, c), o1 = sw128_off(r, c + 8);
+    uint4 hv[2] = {*reinterpret_cast<const uint4*>(box + o0), *reinterpret_cast<const uint4*>(box + o1)};
+    uint4 ov[2];
+    const uint32_t* hw = reinterpret_cast<const uint32_t*>(hv);
+    uint32_t* ow = reinterpret_cast<uint32_t*>(ov);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[q]));
+      const float gx = hf.x > 0.f ? 1.f : hf.x + 1.f, gy = hf.y > 0.f ? 1.f : hf.y + 1.f;
+      ow[q] = pack_bf16(__uint_as_float(d[2 * q]) * gx, __uint_as_float(d[2 * q + 1]) * gy);
+    }
+    *reinterpret_cast<uint4*>(box + o0) = ov[0];
+    *reinterpret_cast<uint4*>(box + o1) = ov[1];
+  };
+  const auto box_colsum = [&](uint32_t box_off, int c, int row0) {  // column c of a box over the tile's rows
+    const uint8_t* box = smem + box_off;
+    const int64_t left = a.m - (int64_t)row0;
+    const int rows = left < kRows ? (int)left : kRows;
+    float t = 0.f;
+    for (int rr = 0; rr < rows; ++rr)
+      t += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(box + sw128_off(rr, c)));
+    return t;
+  };
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int row0 = (int)(tile * kRows);
+    if (tid == 0) {  // the tile's h_3 and h_2 boxes (the previous tile's dZ_1 stores have read the h_2 boxes)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_h3), "r"(kBox) : "memory");
+      tma_load_2d(sbase + kH3, &mh3, 0, row0, bar_h3);
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_h2), "r"(2 * kBox) : "memory");
+      tma_load_2d(sbase + kH2, &mh2, 0, row0, bar_h2);
+      tma_load_2d(sbase + kH2 + kBox, &mh2, 64, row0, bar_h2);
+    }
+    *reinterpret_cast<uint4*>(smem + kA + kmajor_off(tid % kRows, (tid / kRows) * 8, kRows)) = nxt;
+    if (tid < kRows) {  // db_3: this thread's row of dY_3 (columns 0-7; k3 <= 8 on the trunk)
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&nxt);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+        cs3[2 * q] += f.x;
+        cs3[2 * q + 1] += f.y;
+      }
+    }
+    nxt = load_a(tile + gridDim.x);
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      if (it == 0) mbar_wait(bar_w, 0);
+      tc_fence_after();
+      issue_layer(tmem, sbase + kA, kRows, sbase + kW3, 64, 16, 64);  // dY_3 W_3 -> [0, 64)
+      mbar_wait(bar_h3, ph);
+      tc_fence_after();
+#pragma unroll
+      for (int ks = 0; ks < kRows / 16; ++ks)  // dW_3^T += h_3^T dY_3 (M = 128: lanes 64-127 read the h_2 box, unused)
+        mma_bf16(tmem + kDW3, make_desc_sw(sbase + kH3 + ks * 2048, kBox, 1024, 2),
+                 make_desc(sbase + kA + ks * 256, 128, kRows * 16), make_idesc_mn(128, 16), (it > 0 || ks > 0) ? 1u : 0u);
+      mma_commit(bar_mma);
+    }
+    mbar_wait(bar_mma, pm);
+    pm ^= 1;
+    mbar_wait(bar_h3, ph);
+    tc_fence_after();
+#pragma unroll
+    for (int cb = 0; cb < 32; cb += 16) {  // dZ_2 = (dY_3 W_3) * ELU'(h_3): warps 4-7 take columns 32-63
+      const int c = half * 32 + cb;
+      uint32_t d[16];
+      tmem_ld16_async(trow + c, d);
+      tmem_wait_ld();
+      elu_bwd16(smem + kH3, c, d);
+    }
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();  // dZ_2 complete in the h_3 box
+    tc_fence_after();
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < 64 / 16; ++ks)  // dZ_2 W_2 -> [0, 128): A = dZ_2 K-major SW128, K steps of 32 bytes
+        mma_bf16(tmem, make_desc_sw(sbase + kH3 + ks * 32, 16, 1024, 2),
+                 make_desc(sbase + kW2 + 2u * ks * (128 * 16), 128 * 16, 128), make_idesc(kRows, 128), ks > 0 ? 1u : 0u);
+      mbar_wait(bar_h2, ph);
+      tc_fence_after();
+#pragma unroll
+      for (int ks = 0; ks < kRows / 16; ++ks)  // dW_2^T += h_2^T dZ_2: B = dZ_2 MN-major SW128
+        mma_bf16(tmem + kDW2, make_desc_sw(sbase + kH2 + ks * 2048, kBox, 1024, 2),
+                 make_desc_sw(sbase + kH3 + ks * 2048, kBox, 1024, 2), make_idesc_mn(128, 64),
+                 (it > 0 || ks > 0) ? 1u : 0u);
+      mma_commit(bar_mma);
+    }
+    if (tid < 64) cs2 += box_colsum(kH3, tid, row0);  // db_2 (reads only, beside the MMAs)
+    mbar_wait(bar_mma, pm);
+    pm ^= 1;
+    mbar_wait(bar_h2, ph);
+    ph ^= 1;
+    tc_fence_after();
+#pragma unroll
+    for (int cb = 0; cb < 64; cb += 16) {  // dZ_1 = (dZ_2 W_2) * ELU'(h_2): warps 4-7 take columns 64-127
+      const int c = half * 64 + cb;
+      uint32_t d[16];
+      tmem_ld16_async(trow + c, d);
+      tmem_wait_ld();
+      elu_bwd16(smem + kH2 + (c >> 6) * kBox, c & 63, d);
+    }
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();  // dZ_1 complete in the h_2 boxes
+    tc_fence_after();
+    if (tid == 0) {
+      tma_store_2d(&mdz1, 0, row0, sbase + kH2);
+      tma_store_2d(&mdz1, 64, row0, sbase + kH2 + kBox);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (tid < 128) cs1 += box_colsum(kH2 + (tid >> 6) * kBox, tid & 63, row0);
+    __syncthreads();  // the column sums have read the boxes before the next tile's loads land
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tid < 64) atomicAdd(&a.db2[tid], cs2);
+  if (tid < 128) atomicAdd(&a.db1[tid], cs1);
+  if (warp < 4) {  // db_3: warp sums of the per-row partials
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float v = cs3[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && q < a.k3) atomicAdd(&a.db3[q], v);
+    }
+  }
+  if (it > 0) {
+    tc_fence_after();
+    if (half == 0) {  // dW_3^T (lanes 0-63 = inputs, 16 columns = outputs) and dW_2^T columns 0-31
+      float v[16];
+      tmem_ld16(trow + kDW3, v);
+      if (r < 64) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < a.k3)
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(a.dw3 + q * 64 + r), "f"(v[q]) : "memory");
+      }
+    }
+#pragma unroll
+    for (int cb = 0; cb < 32; cb += 16) {  // dW_2^T: lane = input (128), column = output (64); warps 4-7 the upper 32
+      const int c = half * 32 + cb;
+      float v[16];
+      tmem_ld16(trow + kDW2 + c, v);
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(a.dw2 + (int64_t)(c + q) * 128 + r), "f"(v[q]) : "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+  }
+}
+
 // sum of the per-CTA partials -> the weight gradient (fp32, written). A block
 // owns 32 consecutive float4s; its 8 warps split the partials (coalesced
 // 512-byte rows, ~19 independent loads per lane in flight), then fold.
@@ -2095,6 +2346,25 @@ static int launch_dgrad_tma(const sgp::DgradArgs& a, float* colsum, float* wgrad
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
 
+static int launch_bwd_tail(const sgp::TailArgs& a, const void* h3, const void* h2, void* dz1, cudaStream_t st) {
+  constexpr size_t smem = 71 * 1024 + 64 + 1024;
+  static std::atomic<unsigned long long> done{0};
+  if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_bwd_tail_kernel), (int)smem, done))
+    return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+  CUtensorMap mh3, mh2, mdz1;
+  if (!encode_rows128(&mh3, h3, 64, a.m) || !encode_rows128(&mh2, h2, 128, a.m) ||
+      !encode_rows128(&mdz1, dz1, 128, a.m))
+    return fail(SG_ERR_SIM, "sg_policy_backward_tail: cuTensorMapEncodeTiled failed");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (a.m + sgp::kRows - 1) / sgp::kRows;
+  const int64_t grid = tiles < 2 * sms ? tiles : 2 * sms;
+  sgp::policy_bwd_tail_kernel<<<(unsigned)grid, 256, smem, st>>>(mh3, mh2, mdz1, a);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+}
+
 extern "C" {
 
 int sg_adam_step(float* d_params, float* d_grad, float* d_m, float* d_v, void* d_bf16_mirror, int64_t n,
@@ -2481,6 +2751,21 @@ int sg_policy_layer_backward(const void* d_dy, int32_t dy_stride, int32_t k, con
     return d_x0 ? launch_dgrad_tma<256, 128, true>(a, d_colsum, d_wgrad, d_x0, d_wgrad0, st)
                 : launch_dgrad_tma<256, 128, false>(a, d_colsum, d_wgrad, nullptr, nullptr, st);
   return fail(SG_ERR_CONFIG, "sg_policy_layer_backward: layer shape not instantiated (256/128/64 trunk)");
+}
+
+int sg_policy_backward_tail(const void* d_dy3, int32_t dy3_stride, int32_t k3, const void* d_wt3_image,
+                            const void* d_wt2_image, const void* d_h3, const void* d_h2, void* d_dz1, int64_t m,
+                            float* d_db3, float* d_dw3, float* d_db2, float* d_dw2, float* d_db1, void* stream) {
+  if (m <= 0) return SG_OK;
+  if (!d_dy3 || !d_wt3_image || !d_wt2_image || !d_h3 || !d_h2 || !d_dz1 || !d_db3 || !d_dw3 || !d_db2 || !d_dw2 ||
+      !d_db1)
+    return fail(SG_ERR_CONFIG, "sg_policy_backward_tail: null argument");
+  if (k3 < 1 || k3 > 8 || dy3_stride < 8 || dy3_stride % 8 != 0)
+    return fail(SG_ERR_CONFIG, "sg_policy_backward_tail: k3 in 1..8 and a 16-byte row stride");
+  const sgp::TailArgs a{static_cast<const __nv_bfloat16*>(d_dy3), dy3_stride, k3,
+                        static_cast<const uint8_t*>(d_wt3_image), static_cast<const uint8_t*>(d_wt2_image), m,
+                        d_db3, d_dw3, d_db2, d_dw2, d_db1};
+  return launch_bwd_tail(a, d_h3, d_h2, d_dz1, (cudaStream_t)stream);
 }
 
 int sg_policy_set_param_layout(sg_policy* p, const int64_t* w_off, const int64_t* b_off, const int32_t* in_dim,

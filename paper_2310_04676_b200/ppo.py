@@ -217,7 +217,13 @@ class _FusedMLP(torch.autograd.Function):
             ins = (obs, h1[t], h2[t], h3[t])
             g = gy.contiguous().to(torch.bfloat16)
             l0_done = False
-            for l in (3, 2, 1, 0):
+            L = [tr.layers[4 * t + j] for j in range(4)]
+            tail = (tr.wt_images is not None and tr.fuse_tail and colsum and tr.wgrad_partial is not None
+                    and g.shape[1] <= 8 and all(_direct_grads(L[j][0], L[j][1]) is not None for j in (1, 2, 3)))
+            if tail:  # layers 3 and 2 (dZ_2 kept on chip) and db_1 in one launch
+                g = sg.backward_tail(g, tr.wt_images.image(t, 3), tr.wt_images.image(t, 2), h3[t], h2[t],
+                                     L[3][1].grad, L[3][0].grad, L[2][1].grad, L[2][0].grad, L[1][1].grad)
+            for l in ((1, 0) if tail else (3, 2, 1, 0)):
                 if l0_done:  # (dW_0 and db_0 came with layer 1's backward)
                     break
                 W, b, Wm, _ = tr.layers[4 * t + l]
@@ -465,6 +471,7 @@ class Trainer:
         self.train_policy = None
         self.wt_images = None
         self.fuse_l0 = False
+        self.fuse_tail = False
         # bias gradients from column-sum passes (fused into the ELU backward)
         # instead of M = 1 split-K GEMMs; SG_NO_COLSUM_BIAS=1 for the GEMMs
         self.colsum_bias = os.environ.get("SG_NO_COLSUM_BIAS") != "1"
@@ -487,6 +494,9 @@ class Trainer:
             # from the dZ_0 tile it holds (dZ_0 never written); SG_NO_FUSE_L0=1
             # for a separate sg_policy_wgrad over a written dZ_0
             self.fuse_l0 = os.environ.get("SG_NO_FUSE_L0") != "1"
+            # the last two layers' backward as one launch (sg_policy_backward_tail);
+            # SG_NO_FUSE_TAIL=1 for one sg_policy_layer_backward per layer
+            self.fuse_tail = os.environ.get("SG_NO_FUSE_TAIL") != "1"
             if os.environ.get("SG_NO_WGRAD") != "1":
                 self.wgrad_partial = torch.empty(148 * 128 * 256, device=dev)
         self.log_std.grad = self.grad[self.ls_off: self.ls_off + A]

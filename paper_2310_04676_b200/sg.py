@@ -161,6 +161,8 @@ _SIGS = {
     "sg_policy_layer_backward": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                                            C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                            C.c_void_p, C.c_void_p]),
+    "sg_policy_backward_tail": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 6),
     "sg_elu_backward_colsum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
                                          C.c_void_p]),
     "sg_policy_wgrad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_int32,
@@ -792,6 +794,21 @@ def layer_backward(dy, wt_ptr: int, n_in: int, h, colsum=None, wgrad=None, out=N
                                            wgrad.data_ptr() if wgrad is not None else None,
                                            x0.data_ptr() if x0 is not None else None, 32,
                                            wgrad0.data_ptr() if wgrad0 is not None else None, stream))
+    return out
+
+
+def backward_tail(dy3, wt3_ptr: int, wt2_ptr: int, h3, h2, db3, dw3, db2, dw2, db1, out=None):
+    """sg_policy_backward_tail: the last two layers' backward in one launch;
+    returns dZ_1 (bf16 [m x 128]) and accumulates db3 / dw3 / db2 / dw2 / db1."""
+    import torch
+    m, k3 = dy3.shape
+    out = torch.empty((m, 128), dtype=torch.bfloat16, device=dy3.device) if out is None else out
+    for t, shape in ((dw3, (k3, 64)), (dw2, (64, 128))):
+        assert t.is_contiguous() and t.dtype == torch.float32 and tuple(t.shape) == shape
+    stream = torch.cuda.current_stream(dy3.device).cuda_stream
+    _pcheck(lib().sg_policy_backward_tail(dy3.data_ptr(), dy3.stride(0), k3, wt3_ptr, wt2_ptr, h3.data_ptr(),
+                                          h2.data_ptr(), out.data_ptr(), m, db3.data_ptr(), dw3.data_ptr(),
+                                          db2.data_ptr(), dw2.data_ptr(), db1.data_ptr(), stream))
     return out
 
 

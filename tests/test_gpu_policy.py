@@ -266,6 +266,42 @@ def test_layer_backward_matches_reference(sg, n_in, k, m):
     assert torch.equal(dz2, dz)
 
 
+@pytest.mark.parametrize("m,k3", [(131072, 8), (300, 8), (5, 8), (100000, 1)])
+def test_backward_tail_matches_layer_backward(sg, m, k3):
+    """sg_policy_backward_tail (layers 3 and 2 in one launch, dZ_2 on chip)
+    == the two sg_policy_layer_backward launches it replaces, plus db_3 =
+    column sums of dY_3: dZ_1 bit-exact up to the accumulation order (bf16
+    within 1 ulp), gradients within fp32 summation-order tolerance."""
+    from paper_2310_04676_b200 import ppo
+    torch.manual_seed(17)
+    layout, ls_pad, total, _ = ppo.padded_layout(27, 7)
+    flat = torch.randn(total, device="cuda") * 0.1
+    imgs = sg.WtImages(layout, 0)
+    imgs.pack(flat)
+    dy3 = torch.zeros(m, 8, device="cuda", dtype=torch.bfloat16)
+    dy3[:, :k3] = (torch.randn(m, k3, device="cuda") * 0.5).to(torch.bfloat16)
+
+    def act(n):
+        return torch.where(torch.rand(m, n, device="cuda") < 0.5, torch.rand(m, n, device="cuda"),
+                           -torch.rand(m, n, device="cuda")).to(torch.bfloat16)
+    h3, h2 = act(64), act(128)
+    z = lambda *s: torch.zeros(*s, device="cuda")  # noqa: E731
+    db3, dw3, db2, dw2, db1 = z(k3), z(k3, 64), z(64), z(64, 128), z(128)
+    rdw3, rdb2, rdw2, rdb1 = z(8, 64), z(64), z(64, 128), z(128)
+    dz1 = sg.backward_tail(dy3[:, :k3] if k3 < 8 else dy3, imgs.image(0, 3), imgs.image(0, 2), h3, h2,
+                           db3, dw3, db2, dw2, db1)
+    dz2 = sg.layer_backward(dy3, imgs.image(0, 3), 64, h3, rdb2, rdw3)
+    rdz1 = sg.layer_backward(dz2, imgs.image(0, 2), 128, h2, rdb1, rdw2)
+    torch.cuda.synchronize()
+    d = (dz1.float() - rdz1.float()).abs()
+    assert torch.all(d <= 2 ** -7 * rdz1.float().abs() + 1e-6), d.max().item()
+    assert torch.allclose(db3.double(), dy3[:, :k3].double().sum(0), rtol=1e-4, atol=1e-2)
+    assert torch.allclose(dw3, rdw3[:k3], rtol=1e-4, atol=1e-3)
+    assert torch.allclose(db2, rdb2, rtol=1e-4, atol=1e-3)
+    assert torch.allclose(dw2, rdw2, rtol=1e-3, atol=1e-2)
+    assert torch.allclose(db1, rdb1, rtol=1e-3, atol=1e-2)
+
+
 @pytest.mark.parametrize("m", [131072, 300, 5])
 def test_layer_backward_first_layer_weight_gradient(sg, m):
     """sg_policy_layer_backward with x0 (the 256-wide layer): the first
