@@ -1413,6 +1413,46 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
 // dW_1^T (256 columns) and dW_0 (64) besides the per-tile accumulator,
 // which shrinks to 128 columns: the tile's two column halves of dY W run
 // one after the other.
+// Column sums of an N-column bf16 tile held as 128-row x 64-column SW128
+// boxes: thread tid owns 8 consecutive columns (one 16-byte piece per row)
+// of every (256 / (N / 8))-th row, so a warp's load covers whole 128-byte box
+// rows (conflict-free) and each thread adds 8 columns per load; acc carries
+// the partial sums across tiles (one atomic per column per thread at the end).
+template <int N>
+__device__ __forceinline__ void boxes_colsum8(const uint8_t* boxes, int tid, float (&acc)[8]) {
+  constexpr int CG = N / 8, RG = 256 / CG, RPT = kRows / RG;
+  const int cg = tid % CG, rg = tid / CG, g = cg & 7;
+  const uint8_t* box = boxes + (cg >> 3) * (kRows * 128);
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int r = rg + RG * j;
+    const uint4 v = *reinterpret_cast<const uint4*>(box + r * 128 + ((g ^ (r & 7)) << 4));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      acc[2 * q] += __uint_as_float(w[q] << 16);
+      acc[2 * q + 1] += __uint_as_float(w[q] & 0xffff0000u);
+    }
+  }
+}
+// the CTA's column sums: the row groups' partials through shared memory
+// (red: 256 x 8 floats, free by now), then one atomic per column. Call with
+// every thread of the CTA.
+template <int N>
+__device__ __forceinline__ void colsum8_flush(float* colsum, float* red, int tid, const float (&acc)[8]) {
+  constexpr int CG = N / 8, RG = 256 / CG;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) red[(tid / CG) * N + (tid % CG) * 8 + q] = acc[q];
+  __syncthreads();
+  if (tid < N) {
+    float t = 0.f;
+#pragma unroll 8
+    for (int g = 0; g < RG; ++g) t += red[g * N + tid];
+    atomicAdd(&colsum[tid], t);
+  }
+  __syncthreads();
+}
+
 template <int N, int KP, bool L0>
 __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_constant__ CUtensorMap mh,
                                                                   const __grid_constant__ CUtensorMap mdz,
@@ -1482,7 +1522,7 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
   uint32_t ph = 0, pm = 0;
   int it = 0;
   bool first = true;
-  float csum = 0.f;  // column tid's sum of dZ over this CTA's tiles
+  float csum[8] = {};  // partial column sums of dZ over this CTA's tiles
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
     const int row0 = (int)(tile * kRows);
     if (tid == 0) {  // this tile's h boxes (the previous tile's dZ stores / dW_0 MMAs have read the buffers)
@@ -1587,19 +1627,10 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
-    if (colsum && tid < N) {  // rows past m were zero-filled h -> their dZ rows are 0 * ... = finite, skipped
-      const uint8_t* box = smem + kH + (tid >> 6) * kBox;
-      const int64_t left = a.m - (int64_t)row0;
-      const int rows = left < kRows ? (int)left : kRows;
-      float t = 0.f;
-      for (int rr = 0; rr < rows; ++rr)
-        t += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(box + sw128_off(rr, tid & 63)));
-      csum += t;
-    }
+    if (colsum) boxes_colsum8<N>(smem + kH, tid, csum);  // (rows past m: zero dY rows -> zero dZ rows)
     __syncthreads();  // the column sums have read the tile before the next tile's h lands
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // dZ stores done
-  if (colsum && tid < N) atomicAdd(&colsum[tid], csum);
   if constexpr (L0) {
     if (it > 0) {  // this CTA's dW_0: lane = output row, 32 input columns -> vector reductions
       mbar_wait(bar_l0, (uint32_t)(it - 1) & 1u);
@@ -1618,6 +1649,8 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
       }
     }
   }
+  __syncthreads();  // the dZ stores and the dW_0 MMAs have read the boxes: they hold the column-sum partials now
+  if (colsum && it > 0) colsum8_flush<N>(colsum, reinterpret_cast<float*>(smem + kH), tid, csum);
   if (wgrad && tiles > blockIdx.x) {  // this CTA's dW^T -> dW[o][i] += (lane i, column o)
     tc_fence_after();
     constexpr int kHalf = MT == 1 && KP >= 32 ? KP / 2 : KP;  // MT = 1: warps 4-7 take the upper columns
@@ -1736,7 +1769,7 @@ __global__ void __launch_bounds__(256, 2) policy_bwd_tail_kernel(const __grid_co
   uint4 nxt = load_a(blockIdx.x);
   uint32_t pm = 0, ph = 0;
   int it = 0;
-  float cs3[8] = {}, cs2 = 0.f, cs1 = 0.f;
+  float cs3[8] = {}, cs2[8] = {}, cs1[8] = {};
   // ELU'(h) * acc for 16 accumulator columns of row r, in place in a 128 x 64 SW128 box
   const auto elu_bwd16 = [&](uint8_t* box, int c, const uint32_t (&d)[16]) {
     const uint32_t o0 = sw128_off(r, c), o1 = sw128_off(r, c + 8);
@@ -1752,15 +1785,6 @@ __global__ void __launch_bounds__(256, 2) policy_bwd_tail_kernel(const __grid_co
     }
     *reinterpret_cast<uint4*>(box + o0) = ov[0];
     *reinterpret_cast<uint4*>(box + o1) = ov[1];
-  };
-  const auto box_colsum = [&](uint32_t box_off, int c, int row0) {  // column c of a box over the tile's rows
-    const uint8_t* box = smem + box_off;
-    const int64_t left = a.m - (int64_t)row0;
-    const int rows = left < kRows ? (int)left : kRows;
-    float t = 0.f;
-    for (int rr = 0; rr < rows; ++rr)
-      t += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(box + sw128_off(rr, c)));
-    return t;
   };
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
     const int row0 = (int)(tile * kRows);
@@ -1829,7 +1853,7 @@ __global__ void __launch_bounds__(256, 2) policy_bwd_tail_kernel(const __grid_co
                  (it > 0 || ks > 0) ? 1u : 0u);
       mma_commit(bar_mma);
     }
-    if (tid < 64) cs2 += box_colsum(kH3, tid, row0);  // db_2 (reads only, beside the MMAs)
+    boxes_colsum8<64>(smem + kH3, tid, cs2);  // db_2 (reads only, beside the MMAs)
     mbar_wait(bar_mma, pm);
     pm ^= 1;
     mbar_wait(bar_h2, ph);
@@ -1852,12 +1876,15 @@ __global__ void __launch_bounds__(256, 2) policy_bwd_tail_kernel(const __grid_co
       tma_store_2d(&mdz1, 64, row0, sbase + kH2 + kBox);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    if (tid < 128) cs1 += box_colsum(kH2 + (tid >> 6) * kBox, tid & 63, row0);
+    boxes_colsum8<128>(smem + kH2, tid, cs1);
     __syncthreads();  // the column sums have read the boxes before the next tile's loads land
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  if (tid < 64) atomicAdd(&a.db2[tid], cs2);
-  if (tid < 128) atomicAdd(&a.db1[tid], cs1);
+  __syncthreads();
+  if (it > 0) {  // (the h boxes are free: the last dZ_1 stores have read them)
+    colsum8_flush<64>(a.db2, reinterpret_cast<float*>(smem + kH2), tid, cs2);
+    colsum8_flush<128>(a.db1, reinterpret_cast<float*>(smem + kH2), tid, cs1);
+  }
   if (warp < 4) {  // db_3: warp sums of the per-row partials
 #pragma unroll
     for (int q = 0; q < 8; ++q) {

@@ -325,8 +325,8 @@ def test_layer_backward_first_layer_weight_gradient(sg, m):
     dz = sg.layer_backward(dy, imgs.image(0, 1), 256, h, cs_a, wg_a)
     assert sg.layer_backward(dy, imgs.image(0, 1), 256, h, cs_b, wg_b, x0=x0, wgrad0=wg0) is None
     torch.cuda.synchronize()
-    assert torch.allclose(cs_a, cs_b, rtol=1e-5, atol=1e-4)
-    assert torch.allclose(wg_a, wg_b, rtol=1e-5, atol=1e-4)
+    assert torch.allclose(cs_a, cs_b, rtol=1e-4, atol=1e-3)  # (two fp32 summation orders)
+    assert torch.allclose(wg_a, wg_b, rtol=1e-4, atol=1e-3)
     ref = dz.double().t() @ x0.double() + 0.5
     scale = dz.double().norm(dim=0)[:, None] * x0.double().norm(dim=0)[None, :]
     assert torch.all((wg0.double() - ref).abs() <= 1e-3 * scale + 1e-5), \
