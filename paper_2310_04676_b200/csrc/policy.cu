@@ -261,11 +261,22 @@ __device__ __forceinline__ void epi_tmem(uint32_t trow, uint32_t src, uint32_t d
     tmem_st16(trow + dst + c / 2, p);
     if constexpr (STORE) {  // the activations the backward pass needs: bf16 row segment of this thread
       if (g) {
+#ifndef SG_STORE_V4
+        // 32-byte stores (STG.E.ENL2.256): one full sector of the row per
+        // instruction, half the L1 wavefronts of 16-byte stores
+#pragma unroll
+        for (int q = 0; q < 16; q += 8)
+          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(g + c + 2 * q), "r"(p[q]),
+                       "r"(p[q + 1]), "r"(p[q + 2]), "r"(p[q + 3]), "r"(p[q + 4]), "r"(p[q + 5]), "r"(p[q + 6]),
+                       "r"(p[q + 7])
+                       : "memory");
+#else
         uint4* gv = reinterpret_cast<uint4*>(g + c);
         gv[0] = make_uint4(p[0], p[1], p[2], p[3]);
         gv[1] = make_uint4(p[4], p[5], p[6], p[7]);
         gv[2] = make_uint4(p[8], p[9], p[10], p[11]);
         gv[3] = make_uint4(p[12], p[13], p[14], p[15]);
+#endif
       }
     }
   }
