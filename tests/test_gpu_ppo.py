@@ -209,6 +209,18 @@ def test_update_kernels_elu_and_gather(sg):
         assert torch.equal(out[0], obs[idx].to(dt)) and torch.equal(out[1], act[idx])
         for o, src in zip(out[2:], (logp, adv, ret)):
             assert torch.equal(o, src[idx])
+    # unpadded rows (the env's obs_dim-wide rows) -> zero-padded bf16 / fp32 rows; A > 8
+    for ow, A2 in ((27, 9), (30, 3)):
+        obs2, act2 = torch.randn(cap, ow, device="cuda"), torch.randn(cap, A2, device="cuda")
+        for dt in (torch.float32, torch.bfloat16):
+            out = [torch.full((m, O), 5.0, device="cuda", dtype=dt), torch.empty(m, A2, device="cuda")] + \
+                  [torch.empty(m, device="cuda") for _ in range(3)]
+            sg.ppo_gather(idx, obs2, act2, logp, adv, ret, *out)
+            ref = torch.zeros(m, O, device="cuda")
+            ref[:, :ow] = obs2[idx]
+            assert torch.equal(out[0], ref.to(dt)) and torch.equal(out[1], act2[idx])
+            for o, src in zip(out[2:], (logp, adv, ret)):
+                assert torch.equal(o, src[idx])
     # loss gradients: device-ELU layers == torch-ELU layers (fp32)
     torch.manual_seed(1)
     layout, ls_off, total, _ = ppo.padded_layout(27, 7)
