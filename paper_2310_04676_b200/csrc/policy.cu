@@ -1690,6 +1690,237 @@ __global__ void __launch_bounds__(256, 1) policy_dgrad_tma_kernel(const __grid_c
   }
 }
 
+// The update backward's head -- layer 1 (256 wide) and the first layer's
+// weight gradient -- pipelined across tiles (policy_dgrad_tma_kernel<256,
+// 128, true> does the same work one tile at a time). Per tile, with the
+// tile's h_1 boxes split into the column halves A (0-127) and B (128-255):
+//   MMA  dY W (half A columns) + dW_1^T (rows of half A)   -> epilogue A (dZ_0 half A in place)
+//   MMA  dW_0 (half A) | dY W (half B) + dW_1^T (half B)  -> column sums A, epilogue B
+//   the NEXT tile's half-A boxes and x_0 (double-buffered) load now,
+//   MMA  dW_0 (half B)                                     -> column sums B
+//   and the next tile's half-B boxes load at its start, behind its first MMAs.
+// So every h_1 load is in flight while the previous half's MMAs / epilogue
+// run, where the one-tile kernel waits for all four boxes after the last
+// dW_0 MMA of the tile before.
+__global__ void __launch_bounds__(256, 1) policy_bwd_head_kernel(const __grid_constant__ CUtensorMap mh,
+                                                                 const __grid_constant__ CUtensorMap mx0,
+                                                                 const __grid_constant__ DgradArgs a,
+                                                                 float* __restrict__ colsum,
+                                                                 float* __restrict__ wgrad,
+                                                                 float* __restrict__ wgrad0) {
+  constexpr int N = 256, KP = 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  constexpr uint32_t kBBytes = N * KP * 2, kABytes = kRows * KP * 2, kBox = kRows * 128;
+  constexpr uint32_t kSlot = 2 * kBox;  // one column half of an h_1 tile (two boxes)
+  constexpr uint32_t kA = kBBytes, kH = kA + kABytes, kX0 = kH + 2 * kSlot, kX0Bytes = kRows * 64;
+  constexpr uint32_t kBarOff = kX0 + 2 * kX0Bytes;
+  constexpr int kChunks = kRows * KP / 8 / 256;
+  constexpr uint32_t kWCol = 128, kW0Col = 384;  // [0, 128) tile accumulator, dW_1^T, dW_0
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, half = warp >> 2;
+  // B, MMA, H0 (even tiles), H1, L0A, L0B, H0 (odd tiles)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kBarOff + 64);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_b = smem_u32(&bars[0]), bar_mma = smem_u32(&bars[1]), bar_ha = smem_u32(&bars[2]),
+                 bar_hb = smem_u32(&bars[3]), bar_l0a = smem_u32(&bars[4]), bar_l0b = smem_u32(&bars[5]);
+  if (tid == 0) {
+    for (int b = 0; b < 7; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mx0)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  const int64_t tiles = (a.m + kRows - 1) / kRows;
+  // column half h of every tile in slot h (measured: a ring of three slots that loads each half a
+  // half-tile earlier was slower, 52.1 vs 47.8 us)
+  const auto slot = [&](int i, int h) { return kH + (uint32_t)h * kSlot + 0u * (uint32_t)i; };
+  const auto load_half = [&](int64_t tile, int i, int h) {  // half 0 brings x_0 along (buffer i & 1)
+    const int row0 = (int)(tile * kRows);
+    const uint32_t bar = h ? bar_hb : smem_u32(&bars[(i & 1) ? 6 : 2]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kSlot + (h ? 0 : kX0Bytes))
+                 : "memory");
+    tma_load_2d(sbase + slot(i, h), &mh, 128 * h, row0, bar);
+    tma_load_2d(sbase + slot(i, h) + kBox, &mh, 128 * h + 64, row0, bar);
+    if (!h) tma_load_2d(sbase + kX0 + (i & 1) * kX0Bytes, &mx0, 0, row0, bar);
+  };
+  if (tid == 0) {
+    bulk_load(sbase, a.wt, kBBytes, bar_b);
+    if (blockIdx.x < tiles) load_half(blockIdx.x, 0, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t r = (uint32_t)((warp & 3) * 32 + lane);
+  const auto load_a = [&](int64_t tile, uint4 (&v)[kChunks]) {
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const int c = tid + 256 * j, row = c % kRows, kc = c / kRows;
+      const int64_t rr = tile * kRows + row;
+      v[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (tile < tiles && rr < a.m && kc * 8 < a.k)
+        v[j] = *reinterpret_cast<const uint4*>(a.dy + rr * a.dy_stride + kc * 8);
+    }
+  };
+  // dZ = acc * ELU'(h) for this warp half's 64 columns of a column half (in place in the boxes)
+  const auto epilogue = [&](uint32_t base) {  // base: the column half's ring slot
+#pragma unroll
+    for (int cb = 0; cb < 64; cb += 16) {
+      const int c = half * 64 + cb;  // column within the half
+      uint32_t d[16];
+      tmem_ld16_async(trow + c, d);
+      uint8_t* box = smem + base + (c >> 6) * kBox;
+      const uint32_t o0 = sw128_off(r, c & 63), o1 = sw128_off(r, (c & 63) + 8);
+      uint4 hv[2] = {*reinterpret_cast<const uint4*>(box + o0), *reinterpret_cast<const uint4*>(box + o1)};
+      tmem_wait_ld();
+      uint4 ov[2];
+      const uint32_t* hw = reinterpret_cast<const uint32_t*>(hv);
+      uint32_t* ow = reinterpret_cast<uint32_t*>(ov);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[q]));
+        const float gx = hf.x > 0.f ? 1.f : hf.x + 1.f, gy = hf.y > 0.f ? 1.f : hf.y + 1.f;
+        ow[q] = pack_bf16(__uint_as_float(d[2 * q]) * gx, __uint_as_float(d[2 * q + 1]) * gy);
+      }
+      *reinterpret_cast<uint4*>(box + o0) = ov[0];
+      *reinterpret_cast<uint4*>(box + o1) = ov[1];
+    }
+  };
+  const auto mma_w1t = [&](int mt, uint32_t base, bool acc0) {  // dW_1^T rows of column half mt += h^T dY
+#pragma unroll
+    for (int ks = 0; ks < kRows / 16; ++ks)
+      mma_bf16(tmem + kWCol + mt * KP, make_desc_sw(sbase + base + ks * 2048, kBox, 1024, 2),
+               make_desc(sbase + kA + ks * 256, 128, kRows * 16), make_idesc_mn(128, KP), (acc0 || ks > 0) ? 1u : 0u);
+  };
+  const auto mma_w0 = [&](int mt, uint32_t base, int buf, bool acc0) {  // dW_0 rows of column half mt += dZ_0^T x_0
+#pragma unroll
+    for (int ks = 0; ks < kRows / 16; ++ks)
+      mma_bf16(tmem + kW0Col + mt * 32, make_desc_sw(sbase + base + ks * 2048, kBox, 1024, 2),
+               make_desc_sw(sbase + kX0 + buf * kX0Bytes + ks * 1024, 8192, 512, 4), make_idesc_mn(128, 32),
+               (acc0 || ks > 0) ? 1u : 0u);
+  };
+  uint4 nxt[kChunks];
+  load_a(blockIdx.x, nxt);
+  uint32_t pm = 0;
+  int it = 0;
+  float csum[8] = {};  // partial column sums of dZ_0 (colsum_boxes layout over the 4 boxes)
+  float csa[8] = {}, csb[8] = {};
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const uint32_t ph = (uint32_t)it & 1u;
+    const int buf = it & 1;
+    const uint32_t bar_h0 = smem_u32(&bars[buf ? 6 : 2]), ph0 = (uint32_t)(it >> 1) & 1u;
+    const uint32_t s0 = slot(it, 0), s1 = slot(it, 1);
+    const bool more = tile + gridDim.x < tiles;
+    if (tid == 0) {  // this tile's half 1 (the previous tile's half-1 dW_0 MMAs have read the slot)
+      if (it > 0) mbar_wait(bar_l0b, ph ^ 1u);
+      load_half(tile, it, 1);
+    }
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const int c = tid + 256 * j, row = c % kRows, kc = c / kRows;
+      *reinterpret_cast<uint4*>(smem + kA + kmajor_off(row, kc * 8, kRows)) = nxt[j];
+    }
+    load_a(tile + gridDim.x, nxt);
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      if (it == 0) mbar_wait(bar_b, 0);
+      tc_fence_after();
+      issue_layer(tmem, sbase + kA, kRows, sbase, N, KP, 128);  // dY W, half 0 columns
+      mbar_wait(bar_h0, ph0);
+      tc_fence_after();
+      if (wgrad) mma_w1t(0, s0, it > 0);
+      mma_commit(bar_mma);
+    }
+    mbar_wait(bar_mma, pm);
+    pm ^= 1;
+    mbar_wait(bar_h0, ph0);
+    tc_fence_after();
+    epilogue(s0);
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();  // dZ_0 half 0 complete
+    tc_fence_after();
+    if (tid == 0) {
+      mma_w0(0, s0, buf, it > 0);
+      mma_commit(bar_l0a);
+      issue_layer(tmem, sbase + kA, kRows, sbase + 2048, N, KP, 128);  // dY W, half 1 columns
+      mbar_wait(bar_hb, ph);
+      tc_fence_after();
+      if (wgrad) mma_w1t(1, s1, it > 0);
+      mma_commit(bar_mma);
+    }
+    if (colsum) boxes_colsum8<128>(smem + s0, tid, csa);
+    mbar_wait(bar_mma, pm);
+    pm ^= 1;
+    mbar_wait(bar_hb, ph);
+    tc_fence_after();
+    epilogue(s1);
+    async_proxy_fence();
+    tc_fence_before();
+    __syncthreads();  // dZ_0 half 1 complete; the half-0 column sums have read their slot
+    tc_fence_after();
+    if (tid == 0) {
+      mbar_wait(bar_l0a, ph);  // the half-0 dW_0 MMAs have read their slot
+      if (more) load_half(tile + gridDim.x, it + 1, 0);  // the next tile's half 0 (+ x_0) into it
+      tc_fence_after();
+      mma_w0(1, s1, buf, it > 0);
+      mma_commit(bar_l0b);
+    }
+    if (colsum) boxes_colsum8<128>(smem + s1, tid, csb);
+    __syncthreads();  // the half-1 column sums have read their slot before it is reloaded
+  }
+  (void)csum;
+  if (it > 0) {  // this CTA's dW_0: lane = output row, 32 input columns -> vector reductions
+    mbar_wait(bar_l0b, (uint32_t)(it - 1) & 1u);
+    tc_fence_after();
+    const int o = half * 128 + (warp & 3) * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < 32; c += 16) {
+      float v[16];
+      tmem_ld16(trow + kW0Col + half * 32 + c, v);
+      float* row = wgrad0 + (int64_t)o * 32 + c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * q), "f"(v[4 * q]),
+                     "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                     : "memory");
+    }
+  }
+  __syncthreads();  // every MMA has read the boxes: they hold the column-sum partials now
+  if (colsum && it > 0) {
+    colsum8_flush<128>(colsum, reinterpret_cast<float*>(smem + kH), tid, csa);
+    colsum8_flush<128>(colsum + 128, reinterpret_cast<float*>(smem + kH), tid, csb);
+  }
+  if (wgrad && it > 0) {  // this CTA's dW_1^T -> dW_1[o][i] += (lane i, column o)
+    tc_fence_after();
+    const int i = half * 128 + (warp & 3) * 32 + lane;
+#pragma unroll 2
+    for (int c = 0; c < KP; c += 16) {
+      float v[16];
+      tmem_ld16(trow + kWCol + half * KP + c, v);
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (c + q < a.k)
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(wgrad + (int64_t)(c + q) * N + i), "f"(v[q]) : "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+
 // The update backward's tail -- the last two layers of one trunk -- in one
 // launch (Policy::backward, policy.cpp:163-218), per 128-row tile:
 //   db_3 += 1^T dY_3                          (per-thread row sums, no reduction per tile)
@@ -2378,6 +2609,20 @@ static int launch_dgrad_tma(const sgp::DgradArgs& a, float* colsum, float* wgrad
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (a.m + sgp::kRows - 1) / sgp::kRows;
+  if constexpr (L0) {
+    static const bool one_tile = getenv("SG_BWD_HEAD_ONETILE") != nullptr;  // A/B: the one-tile kernel
+    if (!one_tile) {
+      constexpr size_t hsmem = ((size_t)N * KP * 2 + (size_t)sgp::kRows * KP * 2) + 4 * (size_t)sgp::kRows * 128 +
+                               2 * (size_t)sgp::kRows * 64 + 128 + 1024;
+      static std::atomic<unsigned long long> hdone{0};
+      if (!smem_opt_in(reinterpret_cast<const void*>(sgp::policy_bwd_head_kernel), (int)hsmem, hdone))
+        return fail(SG_ERR_SIM, "policy: cannot reserve shared memory");
+      sgp::policy_bwd_head_kernel<<<(unsigned)(tiles < sms ? tiles : sms), 256, hsmem, st>>>(mh, mx0, a, colsum,
+                                                                                               wgrad, wgrad0);
+      const cudaError_t e = cudaGetLastError();
+      return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
+    }
+  }
   sgp::policy_dgrad_tma_kernel<N, KP, L0>
       <<<(unsigned)(tiles < sms ? tiles : sms), 256, smem, st>>>(mh, mdz, mx0, a, colsum, wgrad, wgrad0);
   const cudaError_t e = cudaGetLastError();

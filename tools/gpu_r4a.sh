@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 end-to-end check on one B200: GPU tests, smoke, driver command, reference arm, every config.
-O=gpurun_out/r4a; mkdir -p $O
+O=gpurun_out/r4b; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo pytest rc=$?
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke rc=$?
