@@ -549,6 +549,8 @@ class Trainer:
         self.obs = None
         self.env_steps = 0
         self.iteration = 0
+        self._perm_stream = (torch.cuda.Stream(dev) if os.environ.get("SG_NO_PERM_PREFETCH") != "1" else None)
+        self._perms_ready = None
         self.gen = torch.Generator(device=dev)
         self.gen.manual_seed(cfg.seed * 1000003 + (dist.get_rank() if dist is not None and dist.is_initialized() else 0))
 
@@ -765,10 +767,23 @@ class Trainer:
             if self.use_graph:
                 if self.graph is None:
                     self._capture_update()
-                self._new_perms()
+                cur = torch.cuda.current_stream(self.dev)
+                if self._perms_ready is not None:  # drawn after the previous update, beside the rollout
+                    cur.wait_event(self._perms_ready)
+                else:
+                    self._new_perms()
                 self.g_metrics.zero_()
                 self.graph.replay()
                 metrics = self.g_metrics.clone()
+                if self._perm_stream is not None:
+                    # the next update's permutations (same generator, same draw order) on a
+                    # side stream once this update has read its own: the sorts overlap the
+                    # next rollout's latency-bound launches instead of heading the update
+                    self._perm_stream.wait_stream(cur)
+                    with torch.cuda.stream(self._perm_stream):
+                        self._new_perms()
+                    self._perms_ready = torch.cuda.Event()
+                    self._perms_ready.record(self._perm_stream)
             else:
                 metrics = torch.zeros(5, device=self.dev)
                 self._new_perms()
