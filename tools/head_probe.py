@@ -19,6 +19,15 @@ z = lambda *s: torch.zeros(*s, device="cuda")  # noqa: E731
 for _ in range(3):
     sg.layer_backward(dy, imgs.image(0, 1), 256, h, cs, wg, x0=x0, wgrad0=wg0)
     sg.backward_tail(dy3, imgs.image(0, 3), imgs.image(0, 2), h3, h2, z(8), z(8, 64), z(64), z(64, 128), z(128))
+# the training forward on the same minibatch size (bf16 obs rows, padded layout)
+O, A = 27, 7
+tp = sg.Policy(O, A)
+tp.set_param_layout(layout, [32, 256, 128, 64])
+tp.load_params(flat)
+obs = torch.randn(m, 32, device="cuda").to(torch.bfloat16)
+acts = [torch.empty(2, m, w, device="cuda", dtype=torch.bfloat16) for w in (256, 128, 64, 8)]
+for _ in range(2):
+    tp.train_forward(obs, *acts)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
