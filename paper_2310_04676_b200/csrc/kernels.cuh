@@ -2056,6 +2056,10 @@ template <class CH, int G, int TASK, int MODE, int SUB, bool GEN, int MINB = 1, 
 __global__ void __launch_bounds__(32 * G * TPC, MINB) env_step_kernel(const __grid_constant__ StepParams P,
                                                                       int k_steps) {
   extern __shared__ __align__(16) float smem[];
+  // a kernel launched after this one with programmatic stream serialization
+  // (the policy forward of the next rollout step) may be scheduled as SMs
+  // free up; its griddepcontrol.wait still waits for this grid's completion
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int A = CH::dof(P.robot);
   const int O = 3 * A + 6;
   const int64_t n = P.task.n;

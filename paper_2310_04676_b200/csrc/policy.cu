@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
   PPROBE(0);
   bool boot_row = true;
   if (args.timed_out) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t r = row0 + row;
     boot_row = r < args.n && args.timed_out[r] && !args.terminated[r];
     if (!__syncthreads_or(group == 0 && boot_row)) {
@@ -502,6 +503,11 @@ __global__ void __launch_bounds__(kThreads, 1) policy_fwd_kernel(const __grid_co
     bulk_load(sbase + kW2c, W.w2c, 65536, smem_u32(&bars[3]));
     bulk_load(sbase + kW34, W.w34, 36864, smem_u32(&bars[4]));
   }
+  // Launched with programmatic stream serialization (sg_policy_act* after an
+  // env step): the set-up above (barriers, TMEM, the weight images -- written
+  // by the trainer long before the rollout's env step) overlaps the env
+  // step's last CTAs; everything below reads what the previous kernels wrote.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 1 && args.actions && !args.noise) {  // the trainer-stream state of this tile's first draw (row0, dim 0)
     const uint64_t s = jump_warp(args.s0, *args.pos + args.step_off + 2ull * (uint64_t)row0 * (uint64_t)args.act_dim, J);
     if ((tid & 31) == 0) *reinterpret_cast<uint64_t*>(smem + kBar + 72) = s;
@@ -2832,7 +2838,22 @@ static int policy_forward(const sg_policy* p, const float* d_obs, int64_t n, int
   static const sgp::Jump64 kNone{};
   const sgp::Jump64 J = smp.actions && !smp.noise ? jump_table(smp.inc) : kNone;
   const unsigned grid = (unsigned)((n + sgp::kRows - 1) / sgp::kRows);
-  sgp::policy_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a, J);
+  static const bool no_pdl = getenv("SG_NO_PDL") != nullptr;  // A/B: plain stream-ordered launch
+  if (no_pdl) {
+    sgp::policy_fwd_kernel<<<grid, sgp::kThreads, sgp::kSmem, (cudaStream_t)stream>>>(W, a, J);
+  } else {  // programmatic dependent launch: the prologue may start while the previous kernel drains
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(sgp::kThreads);
+    cfg.dynamicSmemBytes = sgp::kSmem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, sgp::policy_fwd_kernel, W, a, J);
+  }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : fail(SG_ERR_SIM, cudaGetErrorString(e));
 }
