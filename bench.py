@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -281,6 +282,126 @@ def cpu_policy_reference(cfg: dict, steps: int, budget_s: float, threads: int = 
     return n * done / dt, lanes, sample
 
 
+def cpu_ppo_reference(cfg: dict, budget_s: float, n_envs: int = 2048, threads: int = 0):
+    """Config 5 on the host cores (bench_learning, bench.cpp:137-174): whole
+    trainer iterations (ppo.cpp:243-341) of a bounded sample -- n_envs envs
+    instead of the GPU's 16,384; rollout and update costs are per sample, so
+    env-steps/s with learning does not depend on N -- in fp64: rollout of
+    n_steps (Policy::forward, trainer-stream noise, log-probs, oracle env step
+    on the pool, bootstrap forward of timed-out rows), GAE (rollout.cpp:42-76,
+    global advantage normalisation), epochs x minibatches of the PPO loss
+    (ppo.cpp:90-154; gradients by torch autograd on CPU instead of the
+    reference's hand-written backward), global-norm clip and Adam
+    (ppo.cpp:50-64, 157-224). The minibatch shuffle uses torch.randperm, not
+    the trainer stream (same cost class). Returns (env-steps/s, lanes, sample)."""
+    import numpy as np
+    import torch
+    import torch.nn.functional as F
+    from oracle import oracle as O
+    from paper_2310_04676_b200.ppo import HALF_LOG_2PI, LOG_STD_MAX, LOG_STD_MIN, TrainConfig
+    O.build()
+    lanes = threads or os.cpu_count() or 1
+    torch.set_num_threads(lanes)
+    tc = TrainConfig(seed=0)
+    m = O.resolve_robot(cfg["robot"])
+    n, T, A = n_envs, tc.n_steps, m.dof
+    e = O.Env(O.env_config(n_envs=n, seed=0, goal_sigma=cfg["goal_sigma"]), m, threads=lanes)
+    obs = e.reset()
+    Od = obs.shape[1]
+    params = [torch.from_numpy(x).clone().requires_grad_(True)
+              for trunk in _np_policy(Od, A) for W, b in trunk for x in (W, b)]
+    log_std = torch.full((A,), tc.init_log_std, dtype=torch.float64, requires_grad=True)
+    params.append(log_std)
+    adam_m = [torch.zeros_like(p) for p in params]
+    adam_v = [torch.zeros_like(p) for p in params]
+    rs = O.make_stream(0, 0x7261696E)
+
+    def forward(x):
+        outs = []
+        for t in range(2):
+            h = x
+            for l in range(4):
+                h = F.linear(h, params[8 * t + 2 * l], params[8 * t + 2 * l + 1])
+                if l < 3:
+                    h = F.elu(h)
+            outs.append(h)
+        return outs[0], outs[1][:, 0]
+
+    def iteration(obs, step_no):
+        buf = dict(obs=np.zeros((T, n, Od)), act=np.zeros((T, n, A)), logp=np.zeros((T, n)),
+                   val=np.zeros((T, n)), rew=np.zeros((T, n)), term=np.zeros((T, n), bool),
+                   tout=np.zeros((T, n), bool), boot=np.zeros((T, n)))
+        ls = log_std.detach().clamp(LOG_STD_MIN, LOG_STD_MAX).numpy()
+        with torch.no_grad():
+            for t in range(T):
+                mean, value = forward(torch.from_numpy(obs))
+                z = O.fill_normals(rs, n, A)
+                act = mean.numpy() + np.exp(ls) * z
+                buf["obs"][t], buf["act"][t], buf["val"][t] = obs, act, value.numpy()
+                buf["logp"][t] = (-0.5 * z * z - ls - HALF_LOG_2PI).sum(1)
+                e.step(act)
+                r = e.result()
+                buf["rew"][t], buf["term"][t], buf["tout"][t] = r["rewards"], r["terminated"], r["timed_out"]
+                bmask = buf["tout"][t] & ~buf["term"][t]
+                if bmask.any():
+                    buf["boot"][t][bmask] = forward(torch.from_numpy(e.obs()[1][bmask]))[1].numpy()
+                obs = e.obs()[0]
+            last = forward(torch.from_numpy(obs))[1].numpy()
+        adv, ret = np.zeros((T, n)), np.zeros((T, n))
+        running = np.zeros(n)
+        for t in range(T - 1, -1, -1):  # rollout.cpp:42-66, vectorised over envs
+            vn = last if t == T - 1 else buf["val"][t + 1]
+            ended = buf["term"][t] | buf["tout"][t]
+            nxt = np.where(buf["term"][t], 0.0, np.where(buf["tout"][t], buf["boot"][t], vn))
+            delta = buf["rew"][t] + tc.gamma * nxt - buf["val"][t]
+            running = np.where(ended, delta, delta + tc.gamma * tc.lam * running)
+            adv[t], ret[t] = running, running + buf["val"][t]
+        adv = (adv - adv.mean()) / (adv.std() + 1e-8)
+        flat = {k: torch.from_numpy(v.reshape(T * n, *v.shape[2:])) for k, v in
+                (("obs", buf["obs"]), ("act", buf["act"]), ("logp", buf["logp"]), ("adv", adv), ("ret", ret))}
+        mb = (T * n) // tc.minibatch_count
+        for _ in range(tc.epochs):
+            perm = torch.randperm(T * n)
+            for k in range(tc.minibatch_count):
+                idx = perm[k * mb:(k + 1) * mb]
+                mean, value = forward(flat["obs"][idx])
+                lsc = log_std.clamp(LOG_STD_MIN, LOG_STD_MAX)
+                logp = (-0.5 * ((flat["act"][idx] - mean) * torch.exp(-lsc)) ** 2 - lsc - HALF_LOG_2PI).sum(1)
+                ratio = torch.exp(logp - flat["logp"][idx])
+                a_ = flat["adv"][idx]
+                surr = torch.minimum(ratio * a_, ratio.clamp(1 - tc.clip_eps, 1 + tc.clip_eps) * a_)
+                loss = (-surr.mean() + tc.value_coef * 0.5 * ((value - flat["ret"][idx]) ** 2).mean()
+                        - tc.entropy_coef * (lsc + 0.5 + HALF_LOG_2PI).sum())
+                grads = torch.autograd.grad(loss, params)
+                gn = math.sqrt(sum(float((g * g).sum()) for g in grads))
+                if not math.isfinite(gn):
+                    raise RuntimeError("cpu_ppo_reference: non-finite gradient")
+                sc = min(1.0, tc.max_grad_norm / (gn + 1e-6))
+                step_no += 1
+                with torch.no_grad():
+                    for p, g, m1, v1 in zip(params, grads, adam_m, adam_v):
+                        g = g * sc
+                        m1.mul_(0.9).add_(g, alpha=0.1)
+                        v1.mul_(0.999).addcmul_(g, g, value=0.001)
+                        mh = m1 / (1 - 0.9 ** step_no)
+                        vh = v1 / (1 - 0.999 ** step_no)
+                        p.sub_(tc.learning_rate * mh / (vh.sqrt() + 1e-8))
+        return obs, step_no
+
+    obs, step_no = iteration(obs, 0)  # warm-up iteration
+    done, t0 = 0, time.perf_counter()
+    while True:
+        obs, step_no = iteration(obs, step_no)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    sample = (f"{n} envs x {done} PPO iterations ({T} rollout steps + {tc.epochs} x {tc.minibatch_count} minibatch "
+              f"updates) after a warm-up iteration: fp64 policy / loss / Adam on torch CPU kernels (autograd "
+              f"backward), oracle env step on {lanes} pool lanes")
+    return n * T * done / dt, lanes, sample
+
+
 def policy_fwd_seconds(pol, obs, mean, val, dev, reps=200):
     """Average duration of one policy_fwd launch: CUDA events around one
     replay of a CUDA graph of `reps` back-to-back launches on the launching
@@ -465,6 +586,29 @@ def bench_ppo(args, cfg, rank, world, local, dist):
         torch.cuda.synchronize()
     t_ms = sum(e[0].elapsed_time(e[3]) for e in ev)
     roll_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / iters
+    # e2e: the public call a training loop makes, Trainer.iterate(): rollout,
+    # GAE, update, then one synchronisation that reads the iteration's
+    # statistics and metrics back to the host (and checks the device error
+    # word and the non-finite flag); no host inputs (actions are the policy's)
+    e2e_iters = max(2, iters // 2)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(e2e_iters):
+        tr.iterate()
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(a0.elapsed_time(a1), dist, f"cuda:{local}")
+    e2e_val = world * n * tcfg.n_steps * e2e_iters / (e2e_ms * 1e-3)
+    # bytes iterate() reads back: stats (4 x f64), metrics (5 x f32), the
+    # non-finite flag and the log-std mean (f32 each)
+    d2h_iter = 4 * 8 + 5 * 4 + 4 + 4
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        rate, lanes, sample = cpu_ppo_reference(cfg, budget_s=args.cpu_budget)
+        cpu = dict(value=rate, unit="env-steps/s (with learning)", cores=lanes, kind="port", sample=sample)
     upd_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / iters
     t_ms = max_over_ranks(t_ms, dist, f"cuda:{local}")
     steps = iters * tcfg.n_steps
@@ -493,7 +637,11 @@ def bench_ppo(args, cfg, rank, world, local, dist):
             roofline=dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak,
                           traffic=None, peak_kind=pk, kernel="policy_fwd_kernel (tcgen05)",
                           flops_per_env=POLICY_FLOPS_PER_ENV, avg_launch_us=fwd_s * 1e6),
-            cpu_baseline=None, e2e=None,
+            cpu_baseline=cpu,
+            e2e=dict(value=e2e_val, unit="env-steps/s (with learning)", h2d_bytes_per_step=0,
+                     d2h_bytes_per_step=d2h_iter / tcfg.n_steps, iterations=e2e_iters,
+                     path="Trainer.iterate() per iteration (rollout + GAE + update + one synchronisation "
+                          f"reading {d2h_iter} B of statistics / metrics); a step = one rollout step of N envs"),
             # ours per iteration: rollout (policy fwd, sample, env step, bootstrap per step + last fwd), GAE,
             # per minibatch gather + 6 ELU fwd + 6 ELU bwd + loss (2) + Adam (2), policy repack
             gpu_launches=iters * (4 * tcfg.n_steps + 1 + 1 + tcfg.epochs * tcfg.minibatch_count * 17 + 1),
@@ -676,6 +824,8 @@ def main():
         total = max(args.steps, 3)
         if args.config == "policy":
             rate, lanes, sample = cpu_policy_reference(cfg, total, budget_s=120.0)
+        elif args.config == "ppo":
+            rate, lanes, sample = cpu_ppo_reference(cfg, budget_s=60.0)
         else:
             rate, lanes, sample = cpu_reference(cfg, total, budget_s=120.0)
         line = dict(metric=METRIC, value=rate, unit="env-steps/s", n_gpus=args.gpus, steps=args.steps,

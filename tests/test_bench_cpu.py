@@ -104,3 +104,10 @@ def test_contract_bytes_match_survey():
     assert bench.contract_bytes(7, 27) == 314
     assert bench.contract_bytes(6, 24) == 278
     assert bench.contract_bytes(8, 30) == 350
+
+
+def test_ppo_cpu_baseline_runs_on_cpu():
+    """Config 5's CPU baseline (bounded sample of whole fp64 PPO iterations)
+    runs on the host cores and reports env-steps/s with learning."""
+    rate, lanes, sample = bench.cpu_ppo_reference(dict(bench.CONFIGS["ppo"]), budget_s=0.1, n_envs=32)
+    assert rate > 0 and lanes >= 1 and "PPO iterations" in sample
