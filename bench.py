@@ -606,7 +606,7 @@ def bench_ppo(args, cfg, rank, world, local, dist):
     # non-finite flag and the log-std mean (f32 each)
     d2h_iter = 4 * 8 + 5 * 4 + 4 + 4
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, lanes, sample = cpu_ppo_reference(cfg, budget_s=args.cpu_budget)
         cpu = dict(value=rate, unit="env-steps/s (with learning)", cores=lanes, kind="port", sample=sample)
     upd_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / iters
