@@ -128,6 +128,15 @@ def test_active_tracking_drifting_goals(sg, oracle):
     assert worst["goals"] > 0.0
 
 
+@pytest.mark.parametrize("robot,task,sigma", [("psm", 0, 0.05), ("ecm", 0, 0.05), ("star", 3, 0.15)])
+@pytest.mark.parametrize("n", [1, 31, 33])
+def test_tiny_and_ragged_env_counts(sg, oracle, robot, task, sigma, n):
+    """One env, one short team, and one full team + a 1-env team (the ragged
+    last team computes on padding lanes and masks only its stores): every
+    chain, across the step-300 reset burst, against the fp64 oracle."""
+    _run_pair(sg, oracle, robot, task, n, 305, seed=9, sigma=sigma, check_every=4)
+
+
 def test_ecm_reach(sg, oracle):
     _run_pair(sg, oracle, "ecm", oracle.TARGET_REACHING, 96, 650, seed=3)
 
